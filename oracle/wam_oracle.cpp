@@ -1,0 +1,1116 @@
+// wam_oracle.cpp — CPU ORACLE for the wavelet-domain AM iteration of arXiv 1508.04458.
+//
+// TEST INFRASTRUCTURE ONLY.  Loaded exclusively by tests/, __graft_entry__.smoke()
+// and bench.py's cpu_baseline / --impl reference legs, as the checker.  The
+// product library (libwamgpu.so) never links, loads or calls anything here.
+//
+// What it restates (all citations relative to /root/reference/):
+//   * geometry defaults/validation ............ proj/include/wamrec/geometry.hpp:51-112
+//   * make_ray (parallel, flat fan) ........... proj/include/wamrec/projector.hpp:22-49
+//     + equiangular arc detector ............. pin P1
+//   * clip_axis / trace_ray (Siddon) .......... projector.hpp:52-119
+//   * build_system_matrix (row = v*D + k) ..... projector.hpp:123-148
+//   * CSC mirror by counting sort ............. system_matrix.hpp:61-75
+//   * parallel_for ............................ parallel.hpp:11-41
+//   * forward/back projection, Beer, I-div .... SPEC.md:63-98, 106-113
+//   * phantom rasterisation, Poisson data ..... SPEC.md:144-161, 167-173
+//   * orthonormal 2D Haar (Mallat layout) ..... SPEC.md:212-229, 265-266
+//   * footprints / phi = H*Omega*e_z .......... SPEC.md:230-247
+//   * active tree + expand_tree ............... SPEC.md:197-203, 248-256, 267-268
+//   * AM baseline ............................. SPEC.md:292-318, 330
+//   * root solver (errata E1, E2) ............. SPEC.md:362-370, 400, 403
+//   * wam_iterate / run ....................... SPEC.md:338-389, 399-404
+//
+// Parity pinning: the system matrix (ray table + Siddon) is pinned bit-for-bit
+// against the reference headers compiled verbatim (oracle/_ref, built by
+// oracle/Makefile from /root/reference).  The iteration itself has no
+// executable reference: it is pinned by the SPEC's scalar known-answer tests
+// (with errata E1/E2 applied) and its property tests (adjoint, Parseval,
+// monotone I-divergence, reduction equivalence, root-vs-bisection, Z0
+// validity, expansion-oracle set equality); see tests/test_oracle_*.py.
+//
+// Two storage modes (pin P7):
+//   mirror = 0  reference-faithful f64 storage everywhere.  b+/b- come from a
+//               direct per-(ray, coefficient) signed split over exact phi.
+//   mirror = 1  fp32 storage of h, mu, beta, q, d, I0 with fp64 accumulation,
+//               computing b+/b- the way the GPU does (b+ = [Omega^T H^T q](z) - b-,
+//               b- gathered from explicit negative phi columns), so the active
+//               tree can be compared bit-for-bit with the GPU.
+//
+// Build: -std=c++20 -O3 -ffp-contract=off (FMA contraction changes 16% of h
+// bitwise).
+#include "wam_oracle.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <numbers>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace orc {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+static Error config_error(const std::string& w) { return Error(ORC_ERR_CONFIG, w); }
+static Error contract_error(const std::string& w) { return Error(ORC_ERR_CONTRACT, w); }
+static Error numeric_error(const std::string& w) { return Error(ORC_ERR_NUMERIC, w); }
+
+static thread_local std::string g_err;
+
+// ---- parallel.hpp:11-41 restated: static contiguous chunks, disjoint writes only.
+static int resolve_threads(int requested) {
+    if (requested > 0) return requested;
+    unsigned hw = std::thread::hardware_concurrency();
+    return hw == 0 ? 1 : static_cast<int>(hw);
+}
+template <typename Fn>
+static void parallel_for(std::size_t n, int threads, Fn&& fn) {
+    threads = resolve_threads(threads);
+    if (n == 0) return;
+    if (threads <= 1 || n < 2) { fn(std::size_t{0}, n, 0); return; }
+    std::size_t nb = std::min<std::size_t>(static_cast<std::size_t>(threads), n);
+    std::size_t chunk = (n + nb - 1) / nb;
+    std::vector<std::thread> pool;
+    for (std::size_t b = 0; b < nb; ++b) {
+        std::size_t lo = b * chunk, hi = std::min(n, lo + chunk);
+        if (lo >= hi) break;
+        pool.emplace_back([&fn, lo, hi, b] { fn(lo, hi, (int)b); });
+    }
+    for (auto& t : pool) t.join();
+}
+
+// ---- geometry.hpp:21-112 restated (plus pin P1 arc detector).
+struct Geom {
+    int nx = 0, ny = 0, nz = 1;
+    double voxel = 1.0;
+    int detectors = 0;
+    double spacing = 1.0;
+    std::vector<double> angles;
+    int beam = 0;
+    double sod = 0.0, sdd = 0.0, dgamma = 0.0;
+    int views() const { return (int)angles.size(); }
+    double width() const { return nx * voxel; }   // geometry.hpp:44
+    double height() const { return ny * voxel; }  // geometry.hpp:45
+};
+
+static std::vector<double> uniform_angles(int views, double arc) {  // geometry.hpp:70-74
+    std::vector<double> a((std::size_t)views);
+    for (int v = 0; v < views; ++v) a[v] = arc * v / views;
+    return a;
+}
+
+static Geom make_geom(const orc_geometry* c) {
+    if (!c) throw contract_error("geometry: null");
+    Geom g;
+    g.nx = c->nx; g.ny = c->ny; g.nz = c->nz; g.voxel = c->voxel_size;
+    g.detectors = c->detectors; g.spacing = c->detector_spacing; g.beam = c->beam;
+    g.sod = c->source_to_center; g.sdd = c->source_to_detector; g.dgamma = c->fan_angle_step;
+    if (c->views < 1) throw config_error("geometry: at least one view required");
+    if (c->view_angles) g.angles.assign(c->view_angles, c->view_angles + c->views);
+    else g.angles = uniform_angles(c->views, g.beam == 0 ? std::numbers::pi : 2.0 * std::numbers::pi);
+    // validate(): geometry.hpp:51-67
+    if (g.nx < 4 || g.ny < 4) throw config_error("geometry: nx and ny must be >= 4");
+    if (g.nz < 1) throw config_error("geometry: nz must be >= 1");
+    if (!(g.voxel > 0.0)) throw config_error("geometry: voxel_size must be positive");
+    if (g.detectors < 1) throw config_error("geometry: at least one detector required");
+    if (g.beam != 2 && !(g.spacing > 0.0)) throw config_error("geometry: detector_spacing must be positive");
+    for (double a : g.angles)
+        if (!std::isfinite(a)) throw config_error("geometry: non-finite view angle");
+    if (g.beam < 0 || g.beam > 2) throw config_error("geometry: unknown beam type");
+    if (g.beam != 0) {
+        if (!(g.sod > 0.0)) throw config_error("geometry: source_to_center must be positive");
+        if (!(g.sdd > g.sod)) throw config_error("geometry: source_to_detector must exceed source_to_center");
+    }
+    if (g.beam == 2 && !(g.dgamma > 0.0)) throw config_error("geometry: fan_angle_step must be positive");
+    return g;
+}
+
+struct Ray { double ox, oy, dx, dy, tmin, tmax; };
+
+// projector.hpp:22-49 (beam 0/1) with the identical operation order; beam 2 is
+// the pinned equiangular array: same source, direction rotated by gamma_k from
+// the central ray, t in [0, SDD].
+static Ray make_ray(const Geom& g, int view, int det) {
+    const double theta = g.angles[view];
+    const double c = std::cos(theta), s = std::sin(theta);
+    Ray r{};
+    if (g.beam == 0) {
+        const double u = (det - 0.5 * (g.detectors - 1)) * g.spacing;
+        r.ox = -s * u; r.oy = c * u; r.dx = c; r.dy = s;
+        r.tmin = -std::numeric_limits<double>::max();
+        r.tmax = std::numeric_limits<double>::max();
+    } else if (g.beam == 1) {
+        const double u = (det - 0.5 * (g.detectors - 1)) * g.spacing;
+        const double sx = g.sod * c, sy = g.sod * s;
+        const double px = sx - g.sdd * c - s * u;
+        const double py = sy - g.sdd * s + c * u;
+        const double len = std::hypot(px - sx, py - sy);
+        r.ox = sx; r.oy = sy; r.dx = (px - sx) / len; r.dy = (py - sy) / len;
+        r.tmin = 0.0; r.tmax = len;
+    } else {
+        const double gam = (det - 0.5 * (g.detectors - 1)) * g.dgamma;
+        const double cg = std::cos(gam), sg = std::sin(gam);
+        r.ox = g.sod * c; r.oy = g.sod * s;
+        r.dx = -c * cg - s * sg;
+        r.dy = -s * cg + c * sg;
+        r.tmin = 0.0; r.tmax = g.sdd;
+    }
+    return r;
+}
+
+// projector.hpp:52-60
+static bool clip_axis(double o, double d, double lo, double hi, double& tmin, double& tmax) {
+    if (d == 0.0) return o >= lo && o <= hi;
+    double t0 = (lo - o) / d, t1 = (hi - o) / d;
+    if (t0 > t1) std::swap(t0, t1);
+    if (t0 > tmin) tmin = t0;
+    if (t1 < tmax) tmax = t1;
+    return tmin < tmax;
+}
+
+// projector.hpp:64-119, same operation order (exactness needs -ffp-contract=off).
+template <typename Emit>
+static void trace(const Geom& g, const Ray& ray, Emit&& emit) {
+    const double h = g.voxel;
+    const double xmin = -0.5 * g.width();
+    const double ymin = -0.5 * g.height();
+    double tmin = ray.tmin, tmax = ray.tmax;
+    if (!clip_axis(ray.ox, ray.dx, xmin, xmin + g.width(), tmin, tmax)) return;
+    if (!clip_axis(ray.oy, ray.dy, ymin, ymin + g.height(), tmin, tmax)) return;
+    if (!(tmax > tmin)) return;
+    auto cell = [](double pos, double origin, double edge, int n) {
+        int i = static_cast<int>(std::floor((pos - origin) / edge));
+        return std::clamp(i, 0, n - 1);
+    };
+    const double ex = ray.ox + tmin * ray.dx;
+    const double ey = ray.oy + tmin * ray.dy;
+    int ix = cell(ex, xmin, h, g.nx), iy = cell(ey, ymin, h, g.ny);
+    const int step_x = ray.dx > 0.0 ? 1 : -1, step_y = ray.dy > 0.0 ? 1 : -1;
+    const double big = std::numeric_limits<double>::max();
+    const double dt_x = ray.dx != 0.0 ? h / std::abs(ray.dx) : big;
+    const double dt_y = ray.dy != 0.0 ? h / std::abs(ray.dy) : big;
+    double next_x = big, next_y = big;
+    if (ray.dx != 0.0) { double e = xmin + (ray.dx > 0.0 ? ix + 1 : ix) * h; next_x = (e - ray.ox) / ray.dx; }
+    if (ray.dy != 0.0) { double e = ymin + (ray.dy > 0.0 ? iy + 1 : iy) * h; next_y = (e - ray.oy) / ray.dy; }
+    double t = tmin;
+    while (t < tmax) {
+        double t_stop = std::min({next_x, next_y, tmax});
+        double len = t_stop - t;
+        if (len > 0.0) emit(ix, iy, len);
+        if (t_stop >= tmax) break;
+        if (next_x <= t_stop) { ix += step_x; next_x += dt_x; if (ix < 0 || ix >= g.nx) break; }
+        if (next_y <= t_stop) { iy += step_y; next_y += dt_y; if (iy < 0 || iy >= g.ny) break; }
+        t = t_stop;
+    }
+}
+
+// ---- splitmix64 counter RNG (counter-based, per-ray streams)
+static inline uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static inline double uniform(uint64_t seed, uint64_t stream, uint64_t k) {
+    uint64_t x = mix64(mix64(seed) ^ mix64(stream * 0x100000001B3ull + k));
+    return ((double)(x >> 11) + 0.5) * 0x1.0p-53;  // open interval (0,1)
+}
+// Poisson sampling: inversion for mean < 12, PTRS transformed rejection
+// (Hoermann 1993) otherwise.
+static double poisson(uint64_t seed, uint64_t stream, double m) {
+    if (!(m >= 0.0) || !std::isfinite(m)) throw numeric_error("simulate: invalid Poisson mean");
+    if (m == 0.0) return 0.0;
+    if (m < 12.0) {
+        double u = uniform(seed, stream, 0);
+        double p = std::exp(-m), F = p;
+        double k = 0.0;
+        while (u > F && k < 1000.0) { k += 1.0; p *= m / k; F += p; }
+        return k;
+    }
+    const double slam = std::sqrt(m), loglam = std::log(m);
+    const double b = 0.931 + 2.53 * slam;
+    const double a = -0.059 + 0.02483 * b;
+    const double invalpha = 1.1239 + 1.1328 / (b - 3.4);
+    const double vr = 0.9277 - 3.6224 / (b - 2.0);
+    for (uint64_t j = 0;; ++j) {
+        double U = uniform(seed, stream, 2 * j + 1) - 0.5;
+        double V = uniform(seed, stream, 2 * j + 2);
+        double us = 0.5 - std::fabs(U);
+        double k = std::floor((2.0 * a / us + b) * U + m + 0.43);
+        if (us >= 0.07 && V <= vr) return k;
+        if (k < 0.0 || (us < 0.013 && V > us)) continue;
+        if (std::log(V) + std::log(invalpha) - std::log(a / (us * us) + b) <=
+            -m + k * loglam - std::lgamma(k + 1.0))
+            return k;
+    }
+}
+
+}  // namespace orc
+
+using namespace orc;
+
+struct orc_problem {
+    Geom g;
+    bool mirror = false;
+    int threads = 0;
+    uint64_t Ms = 0, Ns = 0;
+    int nz = 1;
+    std::vector<Ray> rays;
+    std::vector<uint64_t> rp;
+    std::vector<uint32_t> ci;
+    std::vector<double> hexact, hv;  // hv = stored h (fp32-rounded in mirror mode)
+    std::vector<uint64_t> cp;
+    std::vector<uint32_t> ri;
+    std::vector<double> cv;
+    std::vector<double> d, I0;  // stored data
+    // AM state
+    bool am_ready = false;
+    std::vector<double> am_mu, am_q, am_b;
+    double am_Z0 = 0.0;
+    int am_iter = 0;
+    // WAM state
+    bool wam_ready = false;
+    int L = 0;
+    std::vector<std::vector<uint8_t>> act;  // act[l], l = 1..L
+    std::vector<double> beta, q, bdata, bp_last, bm_last;
+    double Z0 = 0.0;
+    int64_t cum = 0, degen = 0;
+    int wam_iter = 0;
+    // mirror mode: explicit negative-phi columns for active details, per slice-0 Mallat z
+    std::vector<uint64_t> nphi_ptr;
+    std::vector<uint32_t> nphi_row;
+    std::vector<double> nphi_val;
+    std::chrono::steady_clock::time_point t0;
+
+    double st(double x) const { return mirror ? (double)(float)x : x; }
+};
+
+namespace orc {
+
+static void build_matrix(orc_problem* p) {
+    const Geom& g = p->g;
+    const int V = g.views(), D = g.detectors;
+    p->Ms = (uint64_t)V * D;
+    p->Ns = (uint64_t)g.nx * g.ny;
+    p->nz = g.nz;
+    p->rays.resize(p->Ms);
+    for (int v = 0; v < V; ++v)
+        for (int k = 0; k < D; ++k) p->rays[(uint64_t)v * D + k] = make_ray(g, v, k);
+    // threaded trace, per-chunk buffers concatenated in row order (== serial build)
+    int nt = resolve_threads(p->threads);
+    std::vector<std::vector<uint32_t>> cols(nt);
+    std::vector<std::vector<double>> vals(nt);
+    std::vector<uint64_t> cnt(p->Ms);
+    std::vector<std::size_t> chunk_lo(nt, 0), chunk_hi(nt, 0);
+    parallel_for(p->Ms, nt, [&](std::size_t lo, std::size_t hi, int b) {
+        chunk_lo[b] = lo; chunk_hi[b] = hi;
+        for (std::size_t y = lo; y < hi; ++y) {
+            uint64_t before = vals[b].size();
+            trace(g, p->rays[y], [&](int ix, int iy, double len) {
+                cols[b].push_back((uint32_t)iy * (uint32_t)g.nx + (uint32_t)ix);  // projector.hpp:141
+                vals[b].push_back(len);
+            });
+            cnt[y] = vals[b].size() - before;
+        }
+    });
+    p->rp.assign(p->Ms + 1, 0);
+    for (uint64_t y = 0; y < p->Ms; ++y) p->rp[y + 1] = p->rp[y] + cnt[y];
+    uint64_t nnz = p->rp[p->Ms];
+    p->ci.resize(nnz); p->hexact.resize(nnz);
+    uint64_t off = 0;
+    for (int b = 0; b < nt; ++b) {
+        std::copy(cols[b].begin(), cols[b].end(), p->ci.begin() + off);
+        std::copy(vals[b].begin(), vals[b].end(), p->hexact.begin() + off);
+        off += cols[b].size();
+    }
+    p->hv.resize(nnz);
+    for (uint64_t k = 0; k < nnz; ++k) p->hv[k] = p->st(p->hexact[k]);
+    // system_matrix.hpp:61-75 counting-sort transpose (rows ascending per column)
+    p->cp.assign(p->Ns + 1, 0);
+    for (uint32_t c : p->ci) p->cp[c + 1]++;
+    for (uint64_t c = 0; c < p->Ns; ++c) p->cp[c + 1] += p->cp[c];
+    p->ri.resize(nnz); p->cv.resize(nnz);
+    std::vector<uint64_t> next(p->cp.begin(), p->cp.end() - 1);
+    for (uint64_t y = 0; y < p->Ms; ++y)
+        for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) {
+            uint64_t dst = next[p->ci[k]]++;
+            p->ri[dst] = (uint32_t)y;
+            p->cv[dst] = p->hv[k];
+        }
+}
+
+// forward_project: l(s*M+y) = sum_k h_k mu(s*N+col_k), CSR order.
+static void forward(const orc_problem* p, const double* mu, double* out) {
+    parallel_for(p->Ms, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+        for (int s = 0; s < p->nz; ++s) {
+            const double* m = mu + (uint64_t)s * p->Ns;
+            for (std::size_t y = lo; y < hi; ++y) {
+                double acc = 0.0;
+                for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) acc += p->hv[k] * m[p->ci[k]];
+                out[(uint64_t)s * p->Ms + y] = acc;
+            }
+        }
+    });
+}
+
+// back_project: voxel-driven gather over the CSC mirror.
+static void back(const orc_problem* p, const double* w, double* out) {
+    parallel_for(p->Ns, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+        for (int s = 0; s < p->nz; ++s) {
+            const double* ws = w + (uint64_t)s * p->Ms;
+            for (std::size_t x = lo; x < hi; ++x) {
+                double acc = 0.0;
+                for (uint64_t k = p->cp[x]; k < p->cp[x + 1]; ++k) acc += p->cv[k] * ws[p->ri[k]];
+                out[(uint64_t)s * p->Ns + x] = acc;
+            }
+        }
+    });
+}
+
+// I-divergence term, SPEC.md:90-98 (0*ln0 = 0).
+static inline double idiv_term(double d, double q) {
+    return (d > 0.0 ? d * std::log(d / q) : 0.0) - d + q;
+}
+
+// ---- Haar.  One level on the leading h x w block of a slice
+// (row stride nx).  Fixed operation order shared with the GPU kernels:
+//   s1=a+b, s2=c+d, d1=a-b, d2=c-d; A=(s1+s2)/2 H=(s1-s2)/2 V=(d1+d2)/2 D=(d1-d2)/2
+// A -> (i,j), H -> (i+h/2, j), V -> (i, j+w/2), D -> (i+h/2, j+w/2).
+static void haar_fwd_level(double* x, int nx, int h, int w, std::vector<double>& tmp) {
+    tmp.assign((std::size_t)h * w, 0.0);
+    const int h2 = h / 2, w2 = w / 2;
+    for (int i = 0; i < h2; ++i)
+        for (int j = 0; j < w2; ++j) {
+            double a = x[(2 * i) * nx + 2 * j], b = x[(2 * i) * nx + 2 * j + 1];
+            double c = x[(2 * i + 1) * nx + 2 * j], d = x[(2 * i + 1) * nx + 2 * j + 1];
+            double s1 = a + b, s2 = c + d, d1 = a - b, d2 = c - d;
+            tmp[(std::size_t)i * w + j] = (s1 + s2) * 0.5;
+            tmp[(std::size_t)(i + h2) * w + j] = (s1 - s2) * 0.5;
+            tmp[(std::size_t)i * w + j + w2] = (d1 + d2) * 0.5;
+            tmp[(std::size_t)(i + h2) * w + j + w2] = (d1 - d2) * 0.5;
+        }
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < w; ++j) x[i * nx + j] = tmp[(std::size_t)i * w + j];
+}
+// Inverse: p=A+H m=A-H r=V+D t=V-D; a=(p+r)/2 b=(p-r)/2 c=(m+t)/2 d=(m-t)/2.
+static void haar_inv_level(double* x, int nx, int h, int w, std::vector<double>& tmp) {
+    tmp.assign((std::size_t)h * w, 0.0);
+    const int h2 = h / 2, w2 = w / 2;
+    for (int i = 0; i < h2; ++i)
+        for (int j = 0; j < w2; ++j) {
+            double A = x[i * nx + j], H = x[(i + h2) * nx + j];
+            double Vv = x[i * nx + j + w2], Dd = x[(i + h2) * nx + j + w2];
+            double pp = A + H, mm = A - H, r = Vv + Dd, t = Vv - Dd;
+            tmp[(std::size_t)(2 * i) * w + 2 * j] = (pp + r) * 0.5;
+            tmp[(std::size_t)(2 * i) * w + 2 * j + 1] = (pp - r) * 0.5;
+            tmp[(std::size_t)(2 * i + 1) * w + 2 * j] = (mm + t) * 0.5;
+            tmp[(std::size_t)(2 * i + 1) * w + 2 * j + 1] = (mm - t) * 0.5;
+        }
+    for (int i = 0; i < h; ++i)
+        for (int j = 0; j < w; ++j) x[i * nx + j] = tmp[(std::size_t)i * w + j];
+}
+static void check_haar_dims(int nx, int ny, int L) {
+    if (L < 0 || L > 20) throw config_error("haar: invalid depth");
+    if ((nx % (1 << L)) != 0 || (ny % (1 << L)) != 0)
+        throw config_error("haar: slice dimensions not divisible by 2^L");  // SPEC.md:214, E4
+}
+static void dwt2(int nx, int ny, int ns, int L, const double* in, double* out) {
+    check_haar_dims(nx, ny, L);
+    std::vector<double> tmp;
+    const std::size_t N = (std::size_t)nx * ny;
+    std::copy(in, in + N * ns, out);
+    for (int s = 0; s < ns; ++s)
+        for (int l = 1; l <= L; ++l) haar_fwd_level(out + s * N, nx, ny >> (l - 1), nx >> (l - 1), tmp);
+}
+static void idwt2(int nx, int ny, int ns, int L, const double* in, double* out) {
+    check_haar_dims(nx, ny, L);
+    std::vector<double> tmp;
+    const std::size_t N = (std::size_t)nx * ny;
+    std::copy(in, in + N * ns, out);
+    for (int s = 0; s < ns; ++s)
+        for (int l = L; l >= 1; --l) haar_inv_level(out + s * N, nx, ny >> (l - 1), nx >> (l - 1), tmp);
+}
+
+// Mallat indices of the level-l block (bi, bj): approx only at l == L.
+struct BlockIdx { uint32_t A, H, V, D; };
+static inline BlockIdx mallat(int nx, int ny, int l, int bi, int bj) {
+    const int hl = ny >> l, wl = nx >> l;
+    BlockIdx r;
+    r.A = (uint32_t)(bi * nx + bj);
+    r.H = (uint32_t)((hl + bi) * nx + bj);
+    r.V = (uint32_t)(bi * nx + wl + bj);
+    r.D = (uint32_t)((hl + bi) * nx + wl + bj);
+    return r;
+}
+
+// Per-ray walk producing phi(y|z) = sum_{x in block} h(y|x) w(x|z) for every
+// block the ray crosses, at every level (SPEC.md:239-247 phi_column; the sum is
+// the CSR-order SpMV of the footprint image).  A ray's cells
+// inside a block are contiguous in Siddon order (cells are monotone in ix and
+// iy), so a block is complete when the ray leaves it.  Detail sign pattern at
+// level l: H + on the top half, V + on the left half, D + on TL/BR quadrants;
+// weights 2^-l (approx 2^-L).  cb(level, bi, bj, phiA, phiH, phiV, phiD); phiA
+// is meaningful only for level == L.
+template <typename CB>
+static void phi_walk(const orc_problem* p, int L, uint64_t y, CB&& cb) {
+    const int nx = p->g.nx;
+    int curk[24];
+    double sA = 0.0, sH[24], sV[24], sD[24];
+    int cbi[24], cbj[24];
+    for (int l = 0; l <= L; ++l) { curk[l] = -1; sH[l] = sV[l] = sD[l] = 0.0; }
+    auto flush = [&](int l) {
+        if (curk[l] < 0) return;
+        if (l == 0) {  // L == 0: the approx "block" is a single voxel
+            cb(0, cbi[0], cbj[0], sA, 0.0, 0.0, 0.0);
+            sA = 0.0;
+            return;
+        }
+        double sc = std::ldexp(1.0, -l);
+        double pA = (l == L) ? sA * sc : 0.0;
+        cb(l, cbi[l], cbj[l], pA, sH[l] * sc, sV[l] * sc, sD[l] * sc);
+        sH[l] = sV[l] = sD[l] = 0.0;
+        if (l == L) sA = 0.0;
+    };
+    for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) {
+        const int ix = (int)(p->ci[k] % (uint32_t)nx), iy = (int)(p->ci[k] / (uint32_t)nx);
+        const double h = p->hv[k];
+        if (L == 0) {
+            int key = iy * nx + ix;
+            if (key != curk[0]) { flush(0); curk[0] = key; cbi[0] = iy; cbj[0] = ix; }
+            sA += h;
+            continue;
+        }
+        for (int l = 1; l <= L; ++l) {
+            const int bi = iy >> l, bj = ix >> l;
+            const int key = bi * (nx >> l) + bj;
+            if (key != curk[l]) { flush(l); curk[l] = key; cbi[l] = bi; cbj[l] = bj; }
+            const bool top = ((iy >> (l - 1)) & 1) == 0, left = ((ix >> (l - 1)) & 1) == 0;
+            sH[l] += top ? h : -h;
+            sV[l] += left ? h : -h;
+            sD[l] += (top == left) ? h : -h;
+            if (l == L) sA += h;
+        }
+    }
+    for (int l = (L == 0 ? 0 : 1); l <= L; ++l) flush(l);
+}
+
+static inline bool is_active(const orc_problem* p, int l, int bi, int bj) {
+    return p->act[l][(std::size_t)bi * (p->g.nx >> l) + bj] != 0;
+}
+
+// Z(y) = sum_{z in Zs} |phi(y|z)|, Eq. (1.61).  Order: per level running sums in
+// ray order; Z = totA + tot_L + ... + tot_1 (mirrored by the GPU kernel).
+static double z_row(const orc_problem* p, uint64_t y) {
+    const int L = p->L;
+    double totA = 0.0, tot[24];
+    for (int l = 0; l <= L; ++l) tot[l] = 0.0;
+    phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {
+        if (l == L) totA += std::fabs(pA);
+        if (l >= 1 && is_active(p, l, bi, bj)) tot[l] += std::fabs(pH) + std::fabs(pV) + std::fabs(pD);
+    });
+    double z = totA;
+    for (int l = L; l >= 1; --l) z += tot[l];
+    return z;
+}
+
+static void compute_z0(orc_problem* p) {
+    std::vector<double> zr(p->Ms);
+    parallel_for(p->Ms, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+        for (std::size_t y = lo; y < hi; ++y) zr[y] = z_row(p, y);
+    });
+    double m = 0.0;
+    for (double v : zr) m = std::max(m, v);
+    if (!(m > 0.0)) throw numeric_error("Z0: no ray intersects the active set");
+    p->Z0 = m;
+}
+
+// Explicit negative-phi columns (mirror mode, == the GPU's Phi^- CSC): for every
+// active detail coefficient of slice 0, rays ascending, value (float)phi < 0.
+static void build_nphi(orc_problem* p) {
+    const int L = p->L, nx = p->g.nx;
+    const uint64_t N = p->Ns;
+    std::vector<std::vector<std::pair<uint32_t, double>>> cols(N);
+    for (uint64_t y = 0; y < p->Ms; ++y) {
+        phi_walk(p, L, y, [&](int l, int bi, int bj, double, double pH, double pV, double pD) {
+            if (l < 1 || !is_active(p, l, bi, bj)) return;
+            BlockIdx z = mallat(nx, p->g.ny, l, bi, bj);
+            double v[3] = {(double)(float)pH, (double)(float)pV, (double)(float)pD};
+            uint32_t zz[3] = {z.H, z.V, z.D};
+            for (int t = 0; t < 3; ++t)
+                if (v[t] < 0.0) cols[zz[t]].push_back({(uint32_t)y, v[t]});
+        });
+    }
+    p->nphi_ptr.assign(N + 1, 0);
+    for (uint64_t z = 0; z < N; ++z) p->nphi_ptr[z + 1] = p->nphi_ptr[z] + cols[z].size();
+    p->nphi_row.resize(p->nphi_ptr[N]);
+    p->nphi_val.resize(p->nphi_ptr[N]);
+    for (uint64_t z = 0; z < N; ++z)
+        for (std::size_t i = 0; i < cols[z].size(); ++i) {
+            p->nphi_row[p->nphi_ptr[z] + i] = cols[z][i].first;
+            p->nphi_val[p->nphi_ptr[z] + i] = cols[z][i].second;
+        }
+}
+
+// Direct signed split (reference mode): b+(z), b-(z) for every active z of all
+// slices from the same q; per-thread
+// accumulators combined in chunk order.
+static void direct_split(const orc_problem* p, const std::vector<double>& w, std::vector<double>& bp,
+                         std::vector<double>& bm, bool all_coeffs) {
+    const int L = p->L, nx = p->g.nx, ny = p->g.ny, nz = p->nz;
+    const uint64_t N = p->Ns, M = p->Ms, NT = N * nz;
+    int nt = resolve_threads(p->threads);
+    std::vector<std::vector<double>> tp(nt), tm(nt);
+    parallel_for(M, nt, [&](std::size_t lo, std::size_t hi, int b) {
+        tp[b].assign(NT, 0.0); tm[b].assign(NT, 0.0);
+        auto& P = tp[b]; auto& Mn = tm[b];
+        for (std::size_t y = lo; y < hi; ++y) {
+            phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {
+                for (int s = 0; s < nz; ++s) {
+                    const double qy = w[(uint64_t)s * M + y];
+                    const uint64_t off = (uint64_t)s * N;
+                    if (l == 0) {  // L == 0: voxel-level approx
+                        P[off + (uint64_t)bi * nx + bj] += qy * pA;
+                        continue;
+                    }
+                    BlockIdx z = mallat(nx, ny, l, bi, bj);
+                    if (l == L) {
+                        double t = qy * pA;
+                        if (pA > 0.0) P[off + z.A] += t; else if (pA < 0.0) Mn[off + z.A] += t;
+                    }
+                    if (all_coeffs || is_active(p, l, bi, bj)) {
+                        double ph[3] = {pH, pV, pD};
+                        uint32_t zz[3] = {z.H, z.V, z.D};
+                        for (int t = 0; t < 3; ++t) {
+                            double v = qy * ph[t];
+                            if (ph[t] > 0.0) P[off + zz[t]] += v;
+                            else if (ph[t] < 0.0) Mn[off + zz[t]] += v;
+                        }
+                    }
+                }
+            });
+        }
+    });
+    bp.assign(NT, 0.0); bm.assign(NT, 0.0);
+    for (int b = 0; b < nt; ++b) {
+        if (tp[b].empty()) continue;
+        for (uint64_t z = 0; z < NT; ++z) { bp[z] += tp[b][z]; bm[z] += tm[b][z]; }
+    }
+}
+
+// solve_coefficient_update, SPEC.md:362-370, 400, 403 with errata E1/E2:
+// b+ u^2 - b u + b- = 0, u = exp(-Z0 (beta~ - beta^)), beta~ = beta^ - ln(u)/Z0.
+// returns 0 updated, 1 skipped (b+ = b- = 0), 2 degenerate (no positive root).
+static int solve_update(double b, double bp, double bm, double Z0, double beta, double* out) {
+    *out = beta;
+    if (std::fabs(bm) < 1e-300) bm = 0.0;
+    if (bp == 0.0 && bm == 0.0) return 1;
+    double u;
+    if (bp > 0.0) {
+        if (bm == 0.0) {
+            if (!(b > 0.0)) return 2;
+            u = b / bp;                                   // E2: u = b / b+
+        } else {
+            double sq = std::sqrt(b * b - 4.0 * bp * bm);
+            u = (b >= 0.0) ? (b + sq) / (2.0 * bp) : (2.0 * bm) / (b - sq);  // stable form
+        }
+    } else {
+        if (!(b < 0.0)) return 2;
+        u = bm / b;
+    }
+    if (!(u > 0.0) || !std::isfinite(u)) return 2;
+    double nb = beta - std::log(u) / Z0;
+    if (!std::isfinite(nb)) throw numeric_error("wam: non-finite coefficient update");
+    *out = nb;
+    return 0;
+}
+
+static int64_t active_count(const orc_problem* p) {
+    const int L = p->L, nx = p->g.nx, ny = p->g.ny;
+    int64_t c = (int64_t)(nx >> L) * (ny >> L);
+    for (int l = 1; l <= L; ++l)
+        for (uint8_t a : p->act[l]) c += 3 * (int64_t)(a != 0);
+    return c * p->nz;
+}
+
+// q = st(I0 exp(-H mu)) and objective I(d || q) from the unrounded q.
+static double refresh_q(orc_problem* p, const std::vector<double>& mu, std::vector<double>& qout) {
+    const uint64_t MT = p->Ms * p->nz;
+    std::vector<double> l(MT), term(MT);
+    forward(p, mu.data(), l.data());
+    qout.resize(MT);
+    parallel_for(MT, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+        for (std::size_t y = lo; y < hi; ++y) {
+            if (!std::isfinite(l[y])) throw numeric_error("non-finite line integral at ray " + std::to_string(y));
+            double qq = p->I0[y] * std::exp(-l[y]);
+            term[y] = idiv_term(p->d[y], qq);
+            qout[y] = p->st(qq);
+        }
+    });
+    double obj = 0.0;
+    for (uint64_t y = 0; y < MT; ++y) obj += term[y];
+    return obj;
+}
+
+static void set_data(orc_problem* p, const double* d, const double* I0) {
+    const uint64_t MT = p->Ms * p->nz;
+    p->d.resize(MT); p->I0.resize(MT);
+    for (uint64_t y = 0; y < MT; ++y) {
+        if (!(d[y] >= 0.0)) throw contract_error("data: d must be >= 0");
+        if (!(I0[y] > 0.0)) throw contract_error("data: I0 must be > 0");
+        p->d[y] = p->st(d[y]);
+        p->I0[y] = p->st(I0[y]);
+    }
+}
+
+static std::vector<double> image_of_beta(const orc_problem* p, bool round_storage) {
+    std::vector<double> mu(p->beta.size());
+    idwt2(p->g.nx, p->g.ny, p->nz, p->L, p->beta.data(), mu.data());
+    if (round_storage)
+        for (auto& v : mu) v = p->st(v);
+    return mu;
+}
+
+}  // namespace orc
+
+#define ORC_TRY(...)                                       \
+    try { __VA_ARGS__; return ORC_OK; }                     \
+    catch (const orc::Error& e) { g_err = e.what(); return e.code; } \
+    catch (const std::exception& e) { g_err = e.what(); return ORC_ERR_CONTRACT; }
+
+extern "C" {
+
+const char* orc_last_error(void) { return g_err.c_str(); }
+
+int orc_create(const orc_geometry* gc, int mirror, int threads, orc_problem** out) {
+    ORC_TRY({
+        if (!out) throw contract_error("null out");
+        auto* p = new orc_problem();
+        try {
+            p->g = make_geom(gc);
+            p->mirror = mirror != 0;
+            p->threads = threads;
+            build_matrix(p);
+        } catch (...) { delete p; throw; }
+        *out = p;
+    })
+}
+
+void orc_destroy(orc_problem* p) { delete p; }
+
+int orc_dims(const orc_problem* p, uint64_t* M, uint64_t* N, uint64_t* nnz, int* nz) {
+    ORC_TRY({
+        if (M) *M = p->Ms;
+        if (N) *N = p->Ns;
+        if (nnz) *nnz = p->rp.back();
+        if (nz) *nz = p->nz;
+    })
+}
+
+int orc_get_csr(const orc_problem* p, uint64_t* rp, uint32_t* ci, double* val) {
+    ORC_TRY({
+        if (rp) std::copy(p->rp.begin(), p->rp.end(), rp);
+        if (ci) std::copy(p->ci.begin(), p->ci.end(), ci);
+        if (val) std::copy(p->hexact.begin(), p->hexact.end(), val);
+    })
+}
+
+int orc_get_csc(const orc_problem* p, uint64_t* cp, uint32_t* ri, double* val) {
+    ORC_TRY({
+        if (cp) std::copy(p->cp.begin(), p->cp.end(), cp);
+        if (ri) std::copy(p->ri.begin(), p->ri.end(), ri);
+        if (val) std::copy(p->cv.begin(), p->cv.end(), val);
+    })
+}
+
+int orc_get_rays(const orc_problem* p, double* r6) {
+    ORC_TRY({
+        for (uint64_t y = 0; y < p->Ms; ++y) {
+            const Ray& r = p->rays[y];
+            double* o = r6 + 6 * y;
+            o[0] = r.ox; o[1] = r.oy; o[2] = r.dx; o[3] = r.dy; o[4] = r.tmin; o[5] = r.tmax;
+        }
+    })
+}
+
+int orc_forward_project(const orc_problem* p, const double* mu, double* out) {
+    ORC_TRY({ forward(p, mu, out); })
+}
+int orc_back_project(const orc_problem* p, const double* w, double* out) {
+    ORC_TRY({ back(p, w, out); })
+}
+
+int orc_predicted_means(uint64_t n, const double* I0, const double* l, double* q) {
+    ORC_TRY({
+        for (uint64_t y = 0; y < n; ++y) {
+            if (!std::isfinite(l[y])) throw numeric_error("predicted_means: non-finite line integral at ray " + std::to_string(y));
+            q[y] = I0[y] * std::exp(-l[y]);
+        }
+    })
+}
+
+int orc_i_divergence(uint64_t n, const double* d, const double* q, double* out) {
+    ORC_TRY({
+        double s = 0.0;
+        for (uint64_t y = 0; y < n; ++y) {
+            if (!(q[y] > 0.0)) throw numeric_error("i_divergence: q <= 0 at ray " + std::to_string(y));
+            s += idiv_term(d[y], q[y]);
+        }
+        *out = s;
+    })
+}
+
+int orc_rasterize(const orc_geometry* gc, const orc_primitive* pr, int np, double bg, double* mu) {
+    ORC_TRY({
+        Geom g = make_geom(gc);
+        const double h = g.voxel;
+        const double x0 = -0.5 * g.width(), y0 = -0.5 * g.height(), z0 = -0.5 * (g.nz * h);
+        for (int iz = 0; iz < g.nz; ++iz)
+            for (int iy = 0; iy < g.ny; ++iy)
+                for (int ix = 0; ix < g.nx; ++ix) {
+                    const double x = x0 + (ix + 0.5) * h, y = y0 + (iy + 0.5) * h, z = z0 + (iz + 0.5) * h;
+                    double v = bg;
+                    for (int i = 0; i < np; ++i) {  // painter's order
+                        const orc_primitive& q = pr[i];
+                        const double c = std::cos(q.angle), s = std::sin(q.angle);
+                        const double dx = x - q.cx, dy = y - q.cy;
+                        const double u = c * dx + s * dy, w = -s * dx + c * dy;
+                        const double t = z - q.cz;
+                        bool in;
+                        if (q.kind == 0) {
+                            double r = (u / q.ax) * (u / q.ax) + (w / q.ay) * (w / q.ay);
+                            if (g.nz > 1) r += (t / q.az) * (t / q.az);
+                            in = r <= 1.0;
+                        } else {
+                            in = std::fabs(u) <= q.ax && std::fabs(w) <= q.ay;
+                            if (g.nz > 1) in = in && std::fabs(t) <= q.az;
+                        }
+                        if (in) v = q.value;
+                    }
+                    mu[((std::size_t)iz * g.ny + iy) * g.nx + ix] = v;
+                }
+    })
+}
+
+int orc_simulate(const orc_problem* p, const double* mu, const double* I0, uint64_t seed, int noisy,
+                 double* dout) {
+    ORC_TRY({
+        const uint64_t M = p->Ms, N = p->Ns;
+        parallel_for(M, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+            for (int s = 0; s < p->nz; ++s)
+                for (std::size_t y = lo; y < hi; ++y) {
+                    double acc = 0.0;  // exact f64 h, CSR order
+                    for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k)
+                        acc += p->hexact[k] * mu[(uint64_t)s * N + p->ci[k]];
+                    const uint64_t id = (uint64_t)s * M + y;
+                    double m = I0[id] * std::exp(-acc);
+                    dout[id] = noisy ? poisson(seed, id, m) : m;
+                }
+        });
+    })
+}
+
+double orc_uniform(uint64_t seed, uint64_t stream, uint64_t k) { return uniform(seed, stream, k); }
+double orc_poisson(uint64_t seed, uint64_t stream, double mean) {
+    try { return poisson(seed, stream, mean); } catch (...) { return -1.0; }
+}
+
+int orc_dwt2(int nx, int ny, int ns, int L, const double* in, double* out) {
+    ORC_TRY({ dwt2(nx, ny, ns, L, in, out); })
+}
+int orc_idwt2(int nx, int ny, int ns, int L, const double* in, double* out) {
+    ORC_TRY({ idwt2(nx, ny, ns, L, in, out); })
+}
+
+int orc_solve_update(double b, double bp, double bm, double Z0, double beta, double* out) {
+    try { return solve_update(b, bp, bm, Z0, beta, out); }
+    catch (const orc::Error& e) { g_err = e.what(); return -e.code; }
+}
+
+// ---------------- am-baseline, SPEC.md:292-318 ----------------
+int orc_am_init(orc_problem* p, const double* d, const double* I0, const double* init_mu) {
+    ORC_TRY({
+        set_data(p, d, I0);
+        const uint64_t NT = p->Ns * p->nz;
+        p->am_mu.assign(NT, 0.0);
+        if (init_mu)
+            for (uint64_t x = 0; x < NT; ++x) p->am_mu[x] = p->st(init_mu[x]);
+        p->am_b.resize(NT);
+        back(p, p->d.data(), p->am_b.data());           // b(x) = sum_y d h
+        double z0 = 0.0;                                  // Z0 = max_y sum_x h
+        for (uint64_t y = 0; y < p->Ms; ++y) {
+            double s = 0.0;
+            for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) s += p->hv[k];
+            z0 = std::max(z0, s);
+        }
+        if (!(z0 > 0.0)) throw numeric_error("am: Z0 must be positive");
+        p->am_Z0 = z0;
+        refresh_q(p, p->am_mu, p->am_q);
+        p->am_iter = 0;
+        p->am_ready = true;
+        p->t0 = std::chrono::steady_clock::now();
+    })
+}
+
+int orc_am_iterate(orc_problem* p, int n, orc_record* recs) {
+    ORC_TRY({
+        if (!p->am_ready) throw contract_error("am: not initialised");
+        const uint64_t NT = p->Ns * p->nz;
+        std::vector<double> bh(NT);
+        for (int it = 0; it < n; ++it) {
+            back(p, p->am_q.data(), bh.data());          // b^(x) = sum_y q^ h
+            for (uint64_t x = 0; x < NT; ++x) {
+                const double b = p->am_b[x], c = bh[x];
+                if (!(b > 0.0) || !(c > 0.0)) continue;  // frozen voxel
+                double v = p->am_mu[x] + std::log(c / b) / p->am_Z0;
+                if (!std::isfinite(v)) throw numeric_error("am: non-finite update at voxel " + std::to_string(x));
+                p->am_mu[x] = p->st(std::max(0.0, v));
+            }
+            double obj = refresh_q(p, p->am_mu, p->am_q);
+            p->am_iter++;
+            if (recs) {
+                recs[it].iter = p->am_iter;
+                recs[it].objective = obj;
+                recs[it].elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - p->t0).count();
+                recs[it].active_set = (int64_t)NT;
+                recs[it].cum_updates = (int64_t)NT * p->am_iter;
+            }
+        }
+    })
+}
+
+int orc_am_get(const orc_problem* p, double* mu, double* q, double* Z0, double* b) {
+    ORC_TRY({
+        if (mu) std::copy(p->am_mu.begin(), p->am_mu.end(), mu);
+        if (q) std::copy(p->am_q.begin(), p->am_q.end(), q);
+        if (Z0) *Z0 = p->am_Z0;
+        if (b) std::copy(p->am_b.begin(), p->am_b.end(), b);
+    })
+}
+
+// ---------------- wavelet-am, SPEC.md:353-389 ----------------
+int orc_wam_init(orc_problem* p, const double* d, const double* I0, int L, const double* init_beta) {
+    ORC_TRY({
+        check_haar_dims(p->g.nx, p->g.ny, L);
+        set_data(p, d, I0);
+        p->L = L;
+        const uint64_t NT = p->Ns * p->nz;
+        p->act.assign(L + 1, {});
+        for (int l = 1; l <= L; ++l) p->act[l].assign((std::size_t)(p->g.nx >> l) * (p->g.ny >> l), 0);
+        p->beta.assign(NT, 0.0);
+        if (init_beta)
+            for (uint64_t z = 0; z < NT; ++z) p->beta[z] = p->st(init_beta[z]);
+        // b(z) = sum_y d(y) phi(y|z) for every z (data-only)
+        if (p->mirror) {
+            std::vector<double> g(NT);
+            back(p, p->d.data(), g.data());
+            p->bdata.resize(NT);
+            dwt2(p->g.nx, p->g.ny, p->nz, L, g.data(), p->bdata.data());
+            build_nphi(p);
+        } else {
+            std::vector<double> bp, bm;
+            direct_split(p, p->d, bp, bm, true);
+            p->bdata.resize(NT);
+            for (uint64_t z = 0; z < NT; ++z) p->bdata[z] = bp[z] + bm[z];
+        }
+        compute_z0(p);
+        std::vector<double> mu = image_of_beta(p, true);
+        refresh_q(p, mu, p->q);
+        p->cum = 0; p->degen = 0; p->wam_iter = 0;
+        p->bp_last.assign(NT, 0.0); p->bm_last.assign(NT, 0.0);
+        p->wam_ready = true;
+        p->t0 = std::chrono::steady_clock::now();
+    })
+}
+
+int orc_wam_iterate(orc_problem* p, int n, orc_record* recs) {
+    ORC_TRY({
+        if (!p->wam_ready) throw contract_error("wam: not initialised");
+        const int L = p->L, nx = p->g.nx, ny = p->g.ny;
+        const uint64_t N = p->Ns, NT = N * p->nz;
+        for (int it = 0; it < n; ++it) {
+            std::vector<double> bp, bm;
+            if (p->mirror) {
+                std::vector<double> g(NT), S(NT);
+                back(p, p->q.data(), g.data());
+                dwt2(nx, ny, p->nz, L, g.data(), S.data());
+                bm.assign(NT, 0.0);
+                for (int s = 0; s < p->nz; ++s)
+                    for (uint64_t z = 0; z < N; ++z) {
+                        double acc = 0.0;
+                        for (uint64_t k = p->nphi_ptr[z]; k < p->nphi_ptr[z + 1]; ++k)
+                            acc += p->q[(uint64_t)s * p->Ms + p->nphi_row[k]] * p->nphi_val[k];
+                        bm[(uint64_t)s * N + z] = acc;
+                    }
+                bp.resize(NT);
+                for (uint64_t z = 0; z < NT; ++z) bp[z] = S[z] - bm[z];
+            } else {
+                direct_split(p, p->q, bp, bm, false);
+            }
+            // simultaneous (Jacobi) update of every active z
+            int64_t upd = 0, deg = 0;
+            auto visit = [&](uint64_t z) {
+                double nb;
+                int r = solve_update(p->bdata[z], bp[z], bm[z], p->Z0, p->beta[z], &nb);
+                if (r == 0) { p->beta[z] = p->st(nb); ++upd; }
+                else if (r == 2) ++deg;
+            };
+            for (int s = 0; s < p->nz; ++s) {
+                const uint64_t off = (uint64_t)s * N;
+                for (int bi = 0; bi < (ny >> L); ++bi)
+                    for (int bj = 0; bj < (nx >> L); ++bj) visit(off + (uint64_t)bi * nx + bj);
+                for (int l = 1; l <= L; ++l)
+                    for (int bi = 0; bi < (ny >> l); ++bi)
+                        for (int bj = 0; bj < (nx >> l); ++bj) {
+                            if (!is_active(p, l, bi, bj)) continue;
+                            BlockIdx z = mallat(nx, ny, l, bi, bj);
+                            visit(off + z.H); visit(off + z.V); visit(off + z.D);
+                        }
+            }
+            p->bp_last = bp; p->bm_last = bm;
+            p->cum += upd; p->degen += deg;
+            std::vector<double> mu = image_of_beta(p, true);
+            double obj = refresh_q(p, mu, p->q);
+            p->wam_iter++;
+            if (recs) {
+                recs[it].iter = p->wam_iter;
+                recs[it].objective = obj;
+                recs[it].elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - p->t0).count();
+                recs[it].active_set = active_count(p);
+                recs[it].cum_updates = p->cum;
+            }
+        }
+    })
+}
+
+// expand_tree, SPEC.md:248-256, 267-268 (z-summed criterion, one level per event).
+int orc_wam_expand(orc_problem* p, double factor, int64_t* newly) {
+    ORC_TRY({
+        if (!p->wam_ready) throw contract_error("wam: not initialised");
+        const int L = p->L, nx = p->g.nx, ny = p->g.ny;
+        const uint64_t N = p->Ns;
+        std::vector<double> mu = image_of_beta(p, false);   // fp64 criterion image
+        std::vector<double> s(N, 0.0);
+        for (int sl = 0; sl < p->nz; ++sl)
+            for (uint64_t x = 0; x < N; ++x) s[x] += mu[(uint64_t)sl * N + x];
+        double mx = -std::numeric_limits<double>::infinity();
+        for (double v : s) mx = std::max(mx, v);
+        int64_t cnt = 0;
+        if (mx > 0.0 && L > 0) {
+            const double thr = factor * mx;
+            auto na = p->act;
+            for (int iy = 0; iy < ny; ++iy)
+                for (int ix = 0; ix < nx; ++ix) {
+                    if (!(s[(uint64_t)iy * nx + ix] > thr)) continue;
+                    for (int l = L; l >= 1; --l) {
+                        std::size_t bidx = (std::size_t)(iy >> l) * (nx >> l) + (ix >> l);
+                        if (!p->act[l][bidx]) {
+                            if (!na[l][bidx]) { na[l][bidx] = 1; ++cnt; }
+                            break;
+                        }
+                    }
+                }
+            p->act = na;
+            if (cnt > 0) {
+                compute_z0(p);
+                if (p->mirror) build_nphi(p);
+            }
+        }
+        if (newly) *newly = cnt;
+    })
+}
+
+int orc_wam_run(orc_problem* p, int iters, const int* sched, int nsched, double factor, orc_record* recs) {
+    ORC_TRY({
+        for (int it = 1; it <= iters; ++it) {
+            int r = orc_wam_iterate(p, 1, recs ? recs + (it - 1) : nullptr);
+            if (r != ORC_OK) return r;
+            for (int k = 0; k < nsched; ++k)
+                if (sched[k] == it) {
+                    r = orc_wam_expand(p, factor, nullptr);
+                    if (r != ORC_OK) return r;
+                    break;
+                }
+        }
+    })
+}
+
+int orc_wam_get(const orc_problem* p, double* beta, double* mu, double* q, double* Z0) {
+    ORC_TRY({
+        if (beta) std::copy(p->beta.begin(), p->beta.end(), beta);
+        if (mu) { auto m = image_of_beta(p, true); std::copy(m.begin(), m.end(), mu); }
+        if (q) std::copy(p->q.begin(), p->q.end(), q);
+        if (Z0) *Z0 = p->Z0;
+    })
+}
+
+int orc_wam_tree(const orc_problem* p, uint8_t* bits, uint64_t* nbytes) {
+    ORC_TRY({
+        uint64_t n = 0;
+        for (int l = 1; l <= p->L; ++l) {
+            if (bits) std::copy(p->act[l].begin(), p->act[l].end(), bits + n);
+            n += p->act[l].size();
+        }
+        if (nbytes) *nbytes = n;
+    })
+}
+
+int orc_wam_stats(const orc_problem* p, double* b, double* bp, double* bm) {
+    ORC_TRY({
+        if (b) std::copy(p->bdata.begin(), p->bdata.end(), b);
+        if (bp) std::copy(p->bp_last.begin(), p->bp_last.end(), bp);
+        if (bm) std::copy(p->bm_last.begin(), p->bm_last.end(), bm);
+    })
+}
+
+int orc_wam_counters(const orc_problem* p, int64_t* cum, int64_t* degen, int64_t* act) {
+    ORC_TRY({
+        if (cum) *cum = p->cum;
+        if (degen) *degen = p->degen;
+        if (act) *act = active_count(p);
+    })
+}
+
+int orc_wam_z0_rows(const orc_problem* p, double* zrow) {
+    ORC_TRY({
+        for (uint64_t y = 0; y < p->Ms; ++y) zrow[y] = z_row(p, y);
+    })
+}
+
+int orc_phi_column(const orc_problem* p, int L, uint32_t z, uint32_t* rows, double* vals, uint64_t cap,
+                   uint64_t* nnz) {
+    ORC_TRY({
+        const int nx = p->g.nx, ny = p->g.ny;
+        check_haar_dims(nx, ny, L);
+        uint64_t n = 0;
+        for (uint64_t y = 0; y < p->Ms; ++y) {
+            double val = 0.0;
+            bool hit = false;
+            phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {
+                if (L == 0) {
+                    if ((uint32_t)(bi * nx + bj) == z) { val = pA; hit = true; }
+                    return;
+                }
+                BlockIdx b = mallat(nx, ny, l, bi, bj);
+                if (l == L && b.A == z) { val = pA; hit = true; }
+                if (b.H == z) { val = pH; hit = true; }
+                if (b.V == z) { val = pV; hit = true; }
+                if (b.D == z) { val = pD; hit = true; }
+            });
+            if (hit && val != 0.0) {
+                if (n < cap) { rows[n] = (uint32_t)y; vals[n] = val; }
+                ++n;
+            }
+        }
+        *nnz = n;
+    })
+}
+
+}  // extern "C"
