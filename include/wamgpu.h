@@ -1,0 +1,164 @@
+/*
+ * wamgpu.h — C-ABI of the B200-native alternating-minimization (AM) iteration
+ * of arXiv 1508.04458 (wavelet-domain AM with an adaptive Haar tree, plus the
+ * image-domain AM baseline).
+ *
+ * Drop-in boundary.  The reference exposes C++20 free functions and value
+ * types in namespace wamrec (proj/include/wamrec/ and SPEC.md).  Each entry
+ * point below replaces one of them; the citation says which.  Conventions
+ * (SURVEY.md §8b):
+ *   - opaque handle, no exceptions across the ABI; every call returns a status
+ *     code mapping 1:1 onto the reference's error classes (errors.hpp:9-36);
+ *     wamgpu_last_error(ctx) gives the message (thread-local when ctx == NULL);
+ *   - caller-owned HOST arrays are copied in/out and never retained; device
+ *     memory is owned by the context;
+ *   - calls are synchronous at the ABI; one context is not re-entrant
+ *     (iterations are strictly sequential);
+ *   - image layout (z*ny + iy)*nx + ix (image.hpp:14), ray layout
+ *     z*M_slice + view*detectors + det (projector.hpp:123-125);
+ *   - coefficient layout: per-slice Mallat layout of the orthonormal Haar
+ *     transform (documented in DESIGN.md §3).
+ * Storage on the device is fp32 (h, mu, beta, q, d, I0) with fp64 accumulation
+ * of every reduction (north_star; pin P7).
+ */
+#ifndef WAMGPU_H
+#define WAMGPU_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (errors.hpp:9-36) */
+#define WAMGPU_OK 0
+#define WAMGPU_ERR_CONFIG 1   /* wamrec::ConfigError   errors.hpp:17-20 */
+#define WAMGPU_ERR_CONTRACT 2 /* wamrec::ContractError errors.hpp:22-25 */
+#define WAMGPU_ERR_NUMERIC 3  /* wamrec::NumericError  errors.hpp:27-30 */
+#define WAMGPU_ERR_IO 4       /* wamrec::IoError       errors.hpp:32-35 */
+#define WAMGPU_ERR_CUDA 5     /* CUDA / NCCL failure (no reference equivalent) */
+
+#define WAMGPU_BEAM_PARALLEL 0 /* make_parallel_geometry, geometry.hpp:77-92 */
+#define WAMGPU_BEAM_FAN_FLAT 1 /* make_fan_geometry,      geometry.hpp:95-112 */
+#define WAMGPU_BEAM_FAN_ARC 2  /* equiangular arc detector (pin P1) */
+
+typedef struct wamgpu_ctx wamgpu_ctx;
+
+/* wamrec::ScanGeometry (geometry.hpp:21-68) */
+typedef struct {
+    int nx, ny, nz;
+    double voxel_size;
+    int detectors;
+    double detector_spacing;  /* beams 0/1 */
+    int views;
+    const double* view_angles; /* NULL => uniform_angles(views, pi | 2pi), geometry.hpp:70-74 */
+    int beam;
+    double source_to_center, source_to_detector;
+    double fan_angle_step;     /* beam 2 */
+} wamgpu_geometry;
+
+/* PhantomSpec primitive */
+typedef struct {
+    int kind; /* 0 ellipse / ellipsoid, 1 rectangle / box */
+    double cx, cy, cz, ax, ay, az, angle, value;
+} wamgpu_primitive;
+
+/* ConvergenceRecord */
+typedef struct {
+    int iter;
+    double objective;
+    double elapsed_s;
+    int64_t active_set;
+    int64_t cum_updates;
+} wamgpu_record;
+
+/* Per-kernel device timings of the last run (CUDA events on the context stream). */
+typedef struct {
+    double total_ms;       /* whole run/iterate call, device clock */
+    double fwd_ms;         /* sum over launches of the fused forward kernel */
+    double back_ms;        /* sum over launches of the back-projection kernel */
+    double split_ms;       /* signed-split gather */
+    double update_ms;      /* Haar analysis + root solve + synthesis */
+    double expand_ms;      /* tree expansion (criterion, Z0, Phi^- rebuild) */
+    double comm_ms;        /* NCCL collectives */
+    int64_t fwd_launches, back_launches, split_launches, update_launches, expand_events;
+    int64_t kernel_launches; /* every kernel of this library launched in the call */
+    int64_t split_nnz;       /* Phi^- entries gathered per split launch (last) */
+} wamgpu_timing;
+
+int wamgpu_version(void);
+const char* wamgpu_last_error(const wamgpu_ctx* ctx);
+
+/* Context on one CUDA device.  Replaces the implicit process-wide state of the
+ * reference library (one context per GPU, one process per GPU). */
+int wamgpu_create(int device, wamgpu_ctx** out);
+int wamgpu_destroy(wamgpu_ctx* ctx);
+
+/* Multi-GPU view sharding (2D): NCCL communicator from a
+ * 128-byte ncclUniqueId shared by the caller.  Must precede the matrix. */
+int wamgpu_nccl_unique_id(void* id128);
+int wamgpu_set_comm(wamgpu_ctx* ctx, const void* id128, int rank, int nranks);
+
+/* System model.  set_geometry replaces build_system_matrix(g)
+ * (projector.hpp:126-148): the ray table is built on the host with the
+ * reference's make_ray arithmetic (projector.hpp:22-49) and the Siddon traversal
+ * (projector.hpp:52-119) runs on the device in fp64; CSR and CSC mirror
+ * (system_matrix.hpp:61-75) live in HBM as fp32 values + u32 indices.
+ * set_matrix_csr replaces SystemMatrix(rows, cols, row_ptr, col_idx, values)
+ * (system_matrix.hpp:24-35): caller's f64 CSR, converted to fp32. */
+int wamgpu_set_geometry(wamgpu_ctx* ctx, const wamgpu_geometry* g);
+int wamgpu_set_matrix_csr(wamgpu_ctx* ctx, uint64_t rows, uint64_t cols, uint64_t nnz,
+                          const uint64_t* row_ptr, const uint32_t* col_idx, const double* values);
+/* geometry of the image grid for set_matrix_csr users (nx*ny == cols) */
+int wamgpu_set_grid(wamgpu_ctx* ctx, int nx, int ny, int nz);
+int wamgpu_matrix_info(const wamgpu_ctx* ctx, uint64_t* rows, uint64_t* cols, uint64_t* nnz_local,
+                       uint64_t* row_begin, uint64_t* row_end);
+/* local rows of the device matrix (values as stored, fp32) */
+int wamgpu_get_matrix_csr(const wamgpu_ctx* ctx, uint64_t* row_ptr, uint32_t* col_idx, float* values);
+int wamgpu_get_matrix_csc(const wamgpu_ctx* ctx, uint64_t* col_ptr, uint32_t* row_idx, float* values);
+
+/* core-model: forward_project(H, mu) and back_project(H, w).
+ * mu: N_total doubles; l: local M rows x nz; w: local rows; out: N_total
+ * (all-reduced across ranks). */
+int wamgpu_forward_project(wamgpu_ctx* ctx, const double* mu, double* l);
+int wamgpu_back_project(wamgpu_ctx* ctx, const double* w, double* out);
+
+/* TransmissionData: d and I0 over ALL rays (z*M + y); each rank
+ * keeps its own view rows. */
+int wamgpu_set_data(wamgpu_ctx* ctx, const double* d, const double* I0);
+
+/* am-baseline: init (b = H^T d, Z0 = max row sum, q) and
+ * n iterations of mu <- max(0, mu + ln(b^/b)/Z0). */
+int wamgpu_am_init(wamgpu_ctx* ctx, const double* init_mu);
+int wamgpu_am_iterate(wamgpu_ctx* ctx, int n, wamgpu_record* recs);
+
+/* wavelet-am: init_state, wam_iterate, expand_tree, run. */
+int wamgpu_wam_init(wamgpu_ctx* ctx, int levels, const double* init_beta);
+int wamgpu_wam_iterate(wamgpu_ctx* ctx, int n, wamgpu_record* recs);
+int wamgpu_wam_expand(wamgpu_ctx* ctx, double factor, int64_t* newly_active_blocks);
+int wamgpu_wam_run(wamgpu_ctx* ctx, int iters, const int* schedule, int nsched, double factor,
+                   wamgpu_record* recs);
+
+/* state read-back */
+int wamgpu_get_image(const wamgpu_ctx* ctx, double* mu);   /* AM: mu; WAM: Omega*beta (fp32 storage) */
+int wamgpu_get_beta(const wamgpu_ctx* ctx, double* beta);
+int wamgpu_get_q(const wamgpu_ctx* ctx, double* q);        /* local rows */
+int wamgpu_get_tree(const wamgpu_ctx* ctx, uint8_t* bits, uint64_t* nbytes);
+int wamgpu_get_stats(const wamgpu_ctx* ctx, double* b, double* bplus, double* bminus);
+int wamgpu_get_scalars(const wamgpu_ctx* ctx, double* Z0, int64_t* cum_updates, int64_t* degenerate,
+                       int64_t* active_set);
+int wamgpu_get_z_rows(wamgpu_ctx* ctx, double* zrow);      /* per local in-plane ray sum |phi| */
+int wamgpu_get_timing(const wamgpu_ctx* ctx, wamgpu_timing* t);
+int wamgpu_set_kernel_timing(wamgpu_ctx* ctx, int on);
+
+/* phantom-sim, host-side, f64, seeded counter RNG. */
+int wamgpu_rasterize(const wamgpu_geometry* g, const wamgpu_primitive* prims, int nprims, double background,
+                     double* mu);
+int wamgpu_simulate(const wamgpu_geometry* g, const double* mu_true, const double* I0, uint64_t seed,
+                    int noisy, int threads, double* d);
+/* the host ray table used by set_geometry (6 doubles per in-plane ray) */
+int wamgpu_host_rays(const wamgpu_geometry* g, double* rays6);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

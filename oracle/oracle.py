@@ -123,10 +123,31 @@ class Problem:
         self.M, self.N, self.nnz, self.nz = M.value, N.value, nnz.value, nz.value
         self.L = None
 
+    @classmethod
+    def from_csr(cls, row_ptr, col, val, nx, ny, mirror=False, threads=1):
+        L = lib()
+        self = cls.__new__(cls)
+        rp = np.ascontiguousarray(row_ptr, np.uint64)
+        ci = np.ascontiguousarray(col, np.uint32)
+        v = np.ascontiguousarray(val, np.float64)
+        h = C.c_void_p()
+        _chk(L.orc_create_csr(C.c_uint64(rp.size - 1), int(nx), int(ny), P(rp, C.c_uint64), P(ci, C.c_uint32),
+                              P(v), int(mirror), int(threads), C.byref(h)))
+        self.h = h
+        self.geom = None
+        M, N, nnz, nz = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_int()
+        _chk(L.orc_dims(h, C.byref(M), C.byref(N), C.byref(nnz), C.byref(nz)))
+        self.M, self.N, self.nnz, self.nz = M.value, N.value, nnz.value, nz.value
+        self.L = None
+        return self
+
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
             _lib.orc_destroy(self.h)
             self.h = None
+
+    def am_set_clamp(self, clamp):
+        _chk(lib().orc_am_set_clamp(self.h, int(clamp)))
 
     # --- matrix
     def csr(self):

@@ -276,6 +276,7 @@ struct orc_problem {
     std::vector<double> am_mu, am_q, am_b;
     double am_Z0 = 0.0;
     int am_iter = 0;
+    bool am_clamp = true;
     // WAM state
     bool wam_ready = false;
     int L = 0;
@@ -703,6 +704,40 @@ int orc_create(const orc_geometry* gc, int mirror, int threads, orc_problem** ou
     })
 }
 
+int orc_create_csr(uint64_t M, int nx, int ny, const uint64_t* rp, const uint32_t* ci, const double* val,
+                   int mirror, int threads, orc_problem** out) {
+    ORC_TRY({
+        if (!out || !rp) throw contract_error("null argument");
+        if (nx < 1 || ny < 1) throw contract_error("grid must be positive");
+        auto* p = new orc_problem();
+        p->g.nx = nx; p->g.ny = ny; p->g.nz = 1; p->g.detectors = 1; p->g.angles.assign(1, 0.0);
+        p->mirror = mirror != 0; p->threads = threads;
+        p->Ms = M; p->Ns = (uint64_t)nx * ny; p->nz = 1;
+        const uint64_t nnz = rp[M];
+        p->rp.assign(rp, rp + M + 1);
+        p->ci.assign(ci, ci + nnz);
+        p->hexact.assign(val, val + nnz);
+        for (uint64_t k = 0; k < nnz; ++k)
+            if (p->ci[k] >= p->Ns) { delete p; throw contract_error("column index out of range"); }
+        p->hv.resize(nnz);
+        for (uint64_t k = 0; k < nnz; ++k) p->hv[k] = p->st(p->hexact[k]);
+        p->cp.assign(p->Ns + 1, 0);
+        for (uint32_t c : p->ci) p->cp[c + 1]++;
+        for (uint64_t c = 0; c < p->Ns; ++c) p->cp[c + 1] += p->cp[c];
+        p->ri.resize(nnz); p->cv.resize(nnz);
+        std::vector<uint64_t> next(p->cp.begin(), p->cp.end() - 1);
+        for (uint64_t y = 0; y < M; ++y)
+            for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) {
+                uint64_t dst = next[p->ci[k]]++;
+                p->ri[dst] = (uint32_t)y;
+                p->cv[dst] = p->hv[k];
+            }
+        *out = p;
+    })
+}
+
+int orc_am_set_clamp(orc_problem* p, int clamp) { ORC_TRY({ p->am_clamp = clamp != 0; }) }
+
 void orc_destroy(orc_problem* p) { delete p; }
 
 int orc_dims(const orc_problem* p, uint64_t* M, uint64_t* N, uint64_t* nnz, int* nz) {
@@ -871,7 +906,7 @@ int orc_am_iterate(orc_problem* p, int n, orc_record* recs) {
                 if (!(b > 0.0) || !(c > 0.0)) continue;  // frozen voxel
                 double v = p->am_mu[x] + std::log(c / b) / p->am_Z0;
                 if (!std::isfinite(v)) throw numeric_error("am: non-finite update at voxel " + std::to_string(x));
-                p->am_mu[x] = p->st(std::max(0.0, v));
+                p->am_mu[x] = p->st(p->am_clamp ? std::max(0.0, v) : v);
             }
             double obj = refresh_q(p, p->am_mu, p->am_q);
             p->am_iter++;

@@ -57,6 +57,9 @@ const char* orc_last_error(void);
 /* mirror = 0: reference-faithful f64 storage (image.hpp:54, system_matrix.hpp:80)
  * mirror = 1: fp32 storage + fp64 accumulation, mirroring the GPU (pin P7) */
 int orc_create(const orc_geometry* g, int mirror, int threads, orc_problem** out);
+/* explicit-H problem (SPEC.md:70, 79, 307 examples): CSR over an nx*ny grid */
+int orc_create_csr(uint64_t M, int nx, int ny, const uint64_t* row_ptr, const uint32_t* col,
+                   const double* val, int mirror, int threads, orc_problem** out);
 void orc_destroy(orc_problem* p);
 int orc_dims(const orc_problem* p, uint64_t* M_slice, uint64_t* N_slice, uint64_t* nnz, int* nz);
 /* CSR as built (f64 values, exactly what build_system_matrix returns) */
@@ -89,6 +92,8 @@ int orc_solve_update(double b, double bp, double bm, double Z0, double beta, dou
 /* am-baseline */
 int orc_am_init(orc_problem* p, const double* d, const double* I0, const double* init_mu);
 int orc_am_iterate(orc_problem* p, int n, orc_record* recs);
+/* clamp = 0 disables the max(0, .) of SPEC.md:317 (reduction-property test) */
+int orc_am_set_clamp(orc_problem* p, int clamp);
 int orc_am_get(const orc_problem* p, double* mu, double* q, double* Z0, double* bdata);
 
 /* wavelet-am */

@@ -1,0 +1,585 @@
+// kernels.cuh — sm_100a kernels of the AM / wavelet-AM iteration.
+//
+// Every kernel here is HBM- or latency-bound sparse/integer work; none is a
+// dense contraction, so there is no tensor-core path (north_star).  Layouts:
+//   H  CSR  rp[u64, M+1] + A[uint2{col, f32 bits}]       (projector.hpp:123-148)
+//   H  CSC  cp[u64, N+1] + C[uint2{row, f32 bits}]       (system_matrix.hpp:61-75)
+//   Phi^-   np[u64, N+1] + E[uint2{ray, f32 bits}]       (negative phi of active details)
+//   mu, beta, q, d, I0: fp32; g, b, b-: fp64; every reduction accumulates in fp64.
+// Reductions are deterministic (fixed lane-strided + xor-butterfly order, fixed
+// block order; no float atomics).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <float.h>
+
+namespace wamgpu {
+
+constexpr int LMAX = 6;                 // Haar depth supported on the device
+struct ActOff { unsigned long long off[LMAX + 2]; };
+
+struct RayDev { double ox, oy, dx, dy, tmin, tmax; };
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double hval(uint2 e) { return (double)__uint_as_float(e.y); }
+
+// Streaming (evict-first) 8-byte load of a matrix entry: the matrix is read
+// once per pass, keep L2 for the gathered vectors.
+__device__ __forceinline__ uint2 ld_stream(const uint2* p) { return __ldcs(p); }
+
+// ------------------------------------------------------------------ Siddon
+// projector.hpp:52-119 on the device, fp64, every operation an explicit
+// round-to-nearest intrinsic so no FMA contraction can change h.
+__device__ __forceinline__ bool clip_axis_dev(double o, double d, double lo, double hi, double& tmin,
+                                              double& tmax) {
+    if (d == 0.0) return o >= lo && o <= hi;
+    double t0 = __ddiv_rn(__dsub_rn(lo, o), d);
+    double t1 = __ddiv_rn(__dsub_rn(hi, o), d);
+    if (t0 > t1) { double t = t0; t0 = t1; t1 = t; }
+    if (t0 > tmin) tmin = t0;
+    if (t1 < tmax) tmax = t1;
+    return tmin < tmax;
+}
+
+template <class Emit>
+__device__ __forceinline__ void trace_dev(int nx, int ny, double h, const RayDev& r, Emit&& emit) {
+    const double W = __dmul_rn((double)nx, h), Hh = __dmul_rn((double)ny, h);
+    const double xmin = __dmul_rn(-0.5, W), ymin = __dmul_rn(-0.5, Hh);
+    double tmin = r.tmin, tmax = r.tmax;
+    if (!clip_axis_dev(r.ox, r.dx, xmin, __dadd_rn(xmin, W), tmin, tmax)) return;
+    if (!clip_axis_dev(r.oy, r.dy, ymin, __dadd_rn(ymin, Hh), tmin, tmax)) return;
+    if (!(tmax > tmin)) return;
+    const double ex = __dadd_rn(r.ox, __dmul_rn(tmin, r.dx));
+    const double ey = __dadd_rn(r.oy, __dmul_rn(tmin, r.dy));
+    int ix = (int)floor(__ddiv_rn(__dsub_rn(ex, xmin), h));
+    int iy = (int)floor(__ddiv_rn(__dsub_rn(ey, ymin), h));
+    ix = min(max(ix, 0), nx - 1);
+    iy = min(max(iy, 0), ny - 1);
+    const int sx = r.dx > 0.0 ? 1 : -1, sy = r.dy > 0.0 ? 1 : -1;
+    const double big = DBL_MAX;
+    const double dtx = r.dx != 0.0 ? __ddiv_rn(h, fabs(r.dx)) : big;
+    const double dty = r.dy != 0.0 ? __ddiv_rn(h, fabs(r.dy)) : big;
+    double nxt = big, nyt = big;
+    if (r.dx != 0.0) {
+        double e = __dadd_rn(xmin, __dmul_rn((double)(r.dx > 0.0 ? ix + 1 : ix), h));
+        nxt = __ddiv_rn(__dsub_rn(e, r.ox), r.dx);
+    }
+    if (r.dy != 0.0) {
+        double e = __dadd_rn(ymin, __dmul_rn((double)(r.dy > 0.0 ? iy + 1 : iy), h));
+        nyt = __ddiv_rn(__dsub_rn(e, r.oy), r.dy);
+    }
+    double t = tmin;
+    while (t < tmax) {
+        double ts = fmin(fmin(nxt, nyt), tmax);
+        double len = __dsub_rn(ts, t);
+        if (len > 0.0) emit(ix, iy, len);
+        if (ts >= tmax) break;
+        if (nxt <= ts) { ix += sx; nxt = __dadd_rn(nxt, dtx); if (ix < 0 || ix >= nx) break; }
+        if (nyt <= ts) { iy += sy; nyt = __dadd_rn(nyt, dty); if (iy < 0 || iy >= ny) break; }
+        t = ts;
+    }
+}
+
+__global__ void k_trace_count(const RayDev* __restrict__ rays, uint64_t M, int nx, int ny, double h,
+                              unsigned long long* __restrict__ cnt) {
+    uint64_t y = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (y > M) return;
+    if (y == M) { cnt[M] = 0; return; }
+    unsigned long long c = 0;
+    RayDev r = rays[y];
+    trace_dev(nx, ny, h, r, [&](int, int, double) { ++c; });
+    cnt[y] = c;
+}
+
+__global__ void k_trace_fill(const RayDev* __restrict__ rays, uint64_t M, int nx, int ny, double h,
+                             const unsigned long long* __restrict__ rp, uint2* __restrict__ A) {
+    uint64_t y = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= M) return;
+    uint64_t k = rp[y];
+    RayDev r = rays[y];
+    trace_dev(nx, ny, h, r, [&](int ix, int iy, double len) {
+        A[k++] = make_uint2((unsigned)iy * (unsigned)nx + (unsigned)ix, __float_as_uint((float)len));
+    });
+}
+
+// ------------------------------------------------------- CSC transpose helpers
+// warp per row: key = column, value = {row, f32 bits} (coalesced writes).
+__global__ void k_csr_to_pairs(uint64_t M, const unsigned long long* __restrict__ rp, const uint2* __restrict__ A,
+                               unsigned* __restrict__ keys, uint2* __restrict__ vals) {
+    const int lane = threadIdx.x & 31;
+    uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t y = w; y < M; y += W)
+        for (uint64_t k = rp[y] + lane; k < rp[y + 1]; k += 32) {
+            uint2 e = A[k];
+            keys[k] = e.x;
+            vals[k] = make_uint2((unsigned)y, e.y);
+        }
+}
+
+// ptr[c] = lower_bound(keys, c) for c in [0, n]
+__global__ void k_bounds(const unsigned* __restrict__ keys, uint64_t nkeys, uint64_t n,
+                         unsigned long long* __restrict__ ptr) {
+    uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > n) return;
+    uint64_t lo = 0, hi = nkeys;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    ptr[c] = lo;
+}
+
+__global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ out, uint64_t n) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (float)in[i];
+}
+
+// I-divergence term, SPEC.md:90-98 (0 ln 0 = 0).
+__device__ __forceinline__ double idiv_term(double d, double q) {
+    return (d > 0.0 ? d * log(d / q) : 0.0) - d + q;
+}
+
+// ------------------------------------------------------------ CSR forward
+// Warp per ray.  MODE 0: l = H mu written as fp64 (forward_project).
+// MODE 1: fused Beer's law + I-divergence: q = fp32(I0 exp(-l)), per-block fp64
+// partial of the objective (deterministic block order).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long long* __restrict__ rp,
+                                                 const uint2* __restrict__ A, const float* __restrict__ mu,
+                                                 const float* __restrict__ I0, const float* __restrict__ d,
+                                                 float* __restrict__ q, double* __restrict__ lout,
+                                                 double* __restrict__ partial, int* __restrict__ flag) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    double tacc = 0.0;
+    for (uint64_t y = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; y < M; y += W) {
+        const uint64_t lo = rp[y], hi = rp[y + 1];
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        uint64_t k = lo + lane;
+        for (; k + 96 < hi; k += 128) {
+            const uint2 e0 = ld_stream(A + k), e1 = ld_stream(A + k + 32);
+            const uint2 e2 = ld_stream(A + k + 64), e3 = ld_stream(A + k + 96);
+            a0 = fma(hval(e0), (double)__ldg(mu + e0.x), a0);
+            a1 = fma(hval(e1), (double)__ldg(mu + e1.x), a1);
+            a2 = fma(hval(e2), (double)__ldg(mu + e2.x), a2);
+            a3 = fma(hval(e3), (double)__ldg(mu + e3.x), a3);
+        }
+        for (; k < hi; k += 32) {
+            const uint2 e0 = ld_stream(A + k);
+            a0 = fma(hval(e0), (double)__ldg(mu + e0.x), a0);
+        }
+        const double l = warp_sum((a0 + a1) + (a2 + a3));
+        if (lane == 0) {
+            if (!isfinite(l)) atomicOr(flag, 1);
+            if (MODE == 0) {
+                lout[y] = l;
+            } else {
+                const double qq = (double)I0[y] * exp(-l);
+                q[y] = (float)qq;
+                tacc += idiv_term((double)d[y], qq);
+            }
+        }
+    }
+    if (MODE == 1) {
+        __shared__ double s[32];
+        if (lane == 0) s[wib] = tacc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+            partial[blockIdx.x] = t;
+        }
+    }
+}
+
+// ------------------------------------------------------------- CSC back
+// Warp per voxel: g(x) = sum_y h(y|x) w(y) in fp64 over the voxel's CSC column.
+// MODE 0: write g (fp64).  MODE 1: fused AM update:
+// mu <- max(0, mu + ln(g/b)/Z0) where b > 0 and g > 0, otherwise frozen.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_back(uint64_t N, const unsigned long long* __restrict__ cp,
+                                              const uint2* __restrict__ C, const float* __restrict__ w,
+                                              double* __restrict__ g, const double* __restrict__ bam,
+                                              float* __restrict__ mu, double Z0, int* __restrict__ flag) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t x = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; x < N; x += W) {
+        const uint64_t lo = cp[x], hi = cp[x + 1];
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        uint64_t k = lo + lane;
+        for (; k + 96 < hi; k += 128) {
+            const uint2 e0 = ld_stream(C + k), e1 = ld_stream(C + k + 32);
+            const uint2 e2 = ld_stream(C + k + 64), e3 = ld_stream(C + k + 96);
+            a0 = fma(hval(e0), (double)__ldg(w + e0.x), a0);
+            a1 = fma(hval(e1), (double)__ldg(w + e1.x), a1);
+            a2 = fma(hval(e2), (double)__ldg(w + e2.x), a2);
+            a3 = fma(hval(e3), (double)__ldg(w + e3.x), a3);
+        }
+        for (; k < hi; k += 32) {
+            const uint2 e0 = ld_stream(C + k);
+            a0 = fma(hval(e0), (double)__ldg(w + e0.x), a0);
+        }
+        const double c = warp_sum((a0 + a1) + (a2 + a3));
+        if (lane == 0) {
+            if (MODE == 0) {
+                g[x] = c;
+            } else {
+                const double b = bam[x];
+                if (b > 0.0 && c > 0.0) {
+                    const double v = (double)mu[x] + log(c / b) / Z0;
+                    if (!isfinite(v)) atomicOr(flag, 2);
+                    mu[x] = (float)((0.0 < v) ? v : 0.0);
+                }
+            }
+        }
+    }
+}
+
+// AM update from an (all-reduced) back projection g (multi-GPU path).
+__global__ void k_am_update(uint64_t N, const double* __restrict__ g, const double* __restrict__ bam,
+                            float* __restrict__ mu, double Z0, int* __restrict__ flag) {
+    uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= N) return;
+    const double b = bam[x], c = g[x];
+    if (b > 0.0 && c > 0.0) {
+        const double v = (double)mu[x] + log(c / b) / Z0;
+        if (!isfinite(v)) atomicOr(flag, 2);
+        mu[x] = (float)((0.0 < v) ? v : 0.0);
+    }
+}
+
+// ------------------------------------------------------- reductions / records
+// Single block: fixed-order sum of n partials -> out[0].
+__global__ void k_sum_partials(const double* __restrict__ part, int n, double* __restrict__ out) {
+    __shared__ double s[1024];
+    double a = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) a += part[i];
+    s[threadIdx.x] = a;
+    __syncthreads();
+    for (int st = blockDim.x >> 1; st > 0; st >>= 1) {
+        if ((int)threadIdx.x < st) s[threadIdx.x] += s[threadIdx.x + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = s[0];
+}
+
+__global__ void k_max_partials(const double* __restrict__ v, uint64_t n, double* __restrict__ part) {
+    double m = -DBL_MAX;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        m = fmax(m, v[i]);
+    m = warp_max(m);
+    __shared__ double s[32];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = -DBL_MAX;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, s[w]);
+        part[blockIdx.x] = r;
+    }
+}
+
+// records: obj[it] = *obj_scalar; cum[it] = counters[0]; (*it)++
+__global__ void k_record(const double* __restrict__ obj_scalar, const unsigned long long* __restrict__ counters,
+                         double* __restrict__ objs, unsigned long long* __restrict__ cums, int* __restrict__ it) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        int i = *it;
+        objs[i] = obj_scalar[0];
+        cums[i] = counters[0];
+        *it = i + 1;
+    }
+}
+
+// --------------------------------------------------------------- root solver
+// solve_coefficient_update, SPEC.md:362-370, 400, 403 (errata E1, E2):
+// b+ u^2 - b u + b- = 0, u = exp(-Z0 (beta~ - beta^)); returns 0 updated,
+// 1 skipped (b+ = b- = 0), 2 degenerate (no positive root, left unchanged).
+__device__ __forceinline__ int solve_update(double b, double bp, double bm, double Z0, double beta,
+                                            double* out) {
+    *out = beta;
+    if (fabs(bm) < 1e-300) bm = 0.0;
+    if (bp == 0.0 && bm == 0.0) return 1;
+    double u;
+    if (bp > 0.0) {
+        if (bm == 0.0) {
+            if (!(b > 0.0)) return 2;
+            u = b / bp;
+        } else {
+            const double sq = sqrt(b * b - 4.0 * bp * bm);
+            u = (b >= 0.0) ? (b + sq) / (2.0 * bp) : (2.0 * bm) / (b - sq);
+        }
+    } else {
+        if (!(b < 0.0)) return 2;
+        u = bm / b;
+    }
+    if (!(u > 0.0) || !isfinite(u)) return 2;
+    *out = beta - log(u) / Z0;
+    return 0;
+}
+
+// ------------------------------------------------------------ Haar tiles
+// One CTA per 2^L x 2^L tile: the tile holds the complete L-level Haar tree of
+// one approximation coefficient, so analysis, coefficient update and synthesis
+// are tile-local (fused K4 + K6 + K1).  The per-2x2 operation
+// order is the one fixed in DESIGN.md §3 (s1=a+b, s2=c+d, ... then *0.5).
+// mode 0: synthesis only (beta -> mu fp32, and mu64 if non-null)
+// mode 1: analysis of g, root solve of every active z, synthesis -> mu
+// mode 2: analysis only (g -> out Mallat fp64, used for b = Omega^T H^T d)
+__device__ __forceinline__ void tile_fwd(double* x, double* t, int TS, int L) {
+    for (int l = 1; l <= L; ++l) {
+        const int s = TS >> (l - 1), h2 = s >> 1;
+        for (int i = threadIdx.x; i < h2 * h2; i += blockDim.x) {
+            const int gi = i / h2, gj = i % h2;
+            const double a = x[(2 * gi) * TS + 2 * gj], b = x[(2 * gi) * TS + 2 * gj + 1];
+            const double c = x[(2 * gi + 1) * TS + 2 * gj], d = x[(2 * gi + 1) * TS + 2 * gj + 1];
+            const double s1 = a + b, s2 = c + d, d1 = a - b, d2 = c - d;
+            t[gi * TS + gj] = (s1 + s2) * 0.5;
+            t[(gi + h2) * TS + gj] = (s1 - s2) * 0.5;
+            t[gi * TS + gj + h2] = (d1 + d2) * 0.5;
+            t[(gi + h2) * TS + gj + h2] = (d1 - d2) * 0.5;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < s * s; i += blockDim.x) x[(i / s) * TS + i % s] = t[(i / s) * TS + i % s];
+        __syncthreads();
+    }
+}
+__device__ __forceinline__ void tile_inv(double* x, double* t, int TS, int L) {
+    for (int l = L; l >= 1; --l) {
+        const int s = TS >> (l - 1), h2 = s >> 1;
+        for (int i = threadIdx.x; i < h2 * h2; i += blockDim.x) {
+            const int gi = i / h2, gj = i % h2;
+            const double A = x[gi * TS + gj], H = x[(gi + h2) * TS + gj];
+            const double V = x[gi * TS + gj + h2], D = x[(gi + h2) * TS + gj + h2];
+            const double p = A + H, m = A - H, r = V + D, u = V - D;
+            t[(2 * gi) * TS + 2 * gj] = (p + r) * 0.5;
+            t[(2 * gi) * TS + 2 * gj + 1] = (p - r) * 0.5;
+            t[(2 * gi + 1) * TS + 2 * gj] = (m + u) * 0.5;
+            t[(2 * gi + 1) * TS + 2 * gj + 1] = (m - u) * 0.5;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < s * s; i += blockDim.x) x[(i / s) * TS + i % s] = t[(i / s) * TS + i % s];
+        __syncthreads();
+    }
+}
+
+// Global Mallat index + activity of local tile-tree position (r, c).
+struct CoefInfo { uint64_t z; int level; bool approx; bool active; };
+__device__ __forceinline__ CoefInfo coef_info(int r, int c, int ti, int tj, int L, int nx, int ny,
+                                              const uint8_t* __restrict__ act, const ActOff& off) {
+    CoefInfo ci;
+    const int m = max(r, c);
+    if (m == 0) {  // approximation coefficient (level L); L == 0: the voxel itself
+        ci.z = (uint64_t)ti * nx + tj; ci.level = L; ci.approx = true; ci.active = true;
+        return ci;
+    }
+    const int lg = 31 - __clz(m);      // m in [2^lg, 2^(lg+1))
+    const int l = L - lg, half = 1 << lg;
+    const int li = r & (half - 1), lj = c & (half - 1);
+    const int bi = ti * half + li, bj = tj * half + lj;
+    const int hl = ny >> l, wl = nx >> l;
+    const bool lo_r = r < half, lo_c = c < half;
+    if (!lo_r && lo_c) ci.z = (uint64_t)(hl + bi) * nx + bj;            // H
+    else if (lo_r && !lo_c) ci.z = (uint64_t)bi * nx + wl + bj;         // V
+    else ci.z = (uint64_t)(hl + bi) * nx + wl + bj;                     // D
+    ci.level = l; ci.approx = false;
+    ci.active = act[off.off[l] + (uint64_t)bi * wl + bj] != 0;
+    return ci;
+}
+
+__global__ void k_tile(int mode, int nx, int ny, int L, const double* __restrict__ g, const double* __restrict__ bm,
+                       const double* __restrict__ bdata, const uint8_t* __restrict__ act, ActOff off,
+                       float* __restrict__ beta, float* __restrict__ mu, double* __restrict__ mu64,
+                       double* __restrict__ out, double* __restrict__ bp_out, double* __restrict__ bm_out,
+                       double Z0, unsigned long long* __restrict__ counters, int* __restrict__ flag) {
+    extern __shared__ double sm[];
+    const int TS = 1 << L, T2 = TS * TS;
+    double* x = sm;
+    double* t = sm + T2;
+    const int ti = blockIdx.y, tj = blockIdx.x;
+    const uint64_t base = (uint64_t)ti * TS * nx + (uint64_t)tj * TS;
+    if (mode != 0) {
+        for (int i = threadIdx.x; i < T2; i += blockDim.x) x[i] = g[base + (uint64_t)(i / TS) * nx + i % TS];
+        __syncthreads();
+        tile_fwd(x, t, TS, L);
+    }
+    if (mode == 2) {
+        for (int i = threadIdx.x; i < T2; i += blockDim.x) {
+            CoefInfo ci = coef_info(i / TS, i % TS, ti, tj, L, nx, ny, act, off);
+            out[ci.z] = x[i];
+        }
+        return;
+    }
+    unsigned long long upd = 0, deg = 0;
+    for (int i = threadIdx.x; i < T2; i += blockDim.x) {
+        CoefInfo ci = coef_info(i / TS, i % TS, ti, tj, L, nx, ny, act, off);
+        float bo = beta[ci.z];
+        if (mode == 1 && ci.active) {
+            const double bmv = ci.approx ? 0.0 : bm[ci.z];
+            const double bpv = x[i] - bmv;
+            if (bp_out) { bp_out[ci.z] = bpv; bm_out[ci.z] = bmv; }
+            double nb;
+            const int r = solve_update(bdata[ci.z], bpv, bmv, Z0, (double)bo, &nb);
+            if (r == 0) {
+                if (!isfinite(nb)) atomicOr(flag, 4);
+                bo = (float)nb;
+                beta[ci.z] = bo;
+                ++upd;
+            } else if (r == 2) {
+                ++deg;
+            }
+        }
+        x[i] = (double)bo;
+    }
+    if (mode == 1) {
+        // warp-aggregated integer counters (exact, order-free)
+        for (int o = 16; o > 0; o >>= 1) {
+            upd += __shfl_xor_sync(0xffffffffu, upd, o);
+            deg += __shfl_xor_sync(0xffffffffu, deg, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (upd) atomicAdd(counters + 0, upd);
+            if (deg) atomicAdd(counters + 1, deg);
+        }
+    }
+    __syncthreads();
+    tile_inv(x, t, TS, L);
+    for (int i = threadIdx.x; i < T2; i += blockDim.x) {
+        const uint64_t p = base + (uint64_t)(i / TS) * nx + i % TS;
+        mu[p] = (float)x[i];
+        if (mu64) mu64[p] = x[i];
+    }
+}
+
+// ------------------------------------------------------------- expansion
+// expand_tree marking: pixel p with s(p) > thr activates the
+// detail triple of the coarsest level whose block at p is inactive in the OLD
+// tree (closure preserved).  Byte stores of 1 are idempotent.
+__global__ void k_mark(int nx, int ny, int L, const double* __restrict__ s, double thr,
+                       const uint8_t* __restrict__ act_old, uint8_t* __restrict__ act_new, ActOff off) {
+    uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= (uint64_t)nx * ny) return;
+    if (!(s[p] > thr)) return;
+    const int iy = (int)(p / nx), ix = (int)(p % nx);
+    for (int l = L; l >= 1; --l) {
+        const uint64_t idx = off.off[l] + (uint64_t)(iy >> l) * (nx >> l) + (ix >> l);
+        if (!act_old[idx]) { act_new[idx] = 1; return; }
+    }
+}
+
+// Per-ray walk over the CSR row producing phi(y|z) of every crossed block at
+// every level (cells of a ray inside a block are contiguous in Siddon order).
+// MODE 0: Z(y) = sum_{z active} |phi(y|z)|  (Eq. 1.61; order: totA + tot_L..tot_1)
+// MODE 1: count negative fp32 phi of active detail coefficients
+// MODE 2: emit them (key = Mallat z, value = {ray, f32 bits}) at pos[y]
+template <int MODE>
+__global__ void __launch_bounds__(128) k_walk(uint64_t M, const unsigned long long* __restrict__ rp,
+                                              const uint2* __restrict__ A, int nx, int ny, int L,
+                                              const uint8_t* __restrict__ act, ActOff off,
+                                              double* __restrict__ zrow, unsigned long long* __restrict__ cnt,
+                                              const unsigned long long* __restrict__ pos,
+                                              unsigned* __restrict__ keys, uint2* __restrict__ vals) {
+    const uint64_t y = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (y > M) return;
+    if (y == M) { if (MODE == 1) cnt[M] = 0; return; }
+    int cur[LMAX + 1], cbi[LMAX + 1], cbj[LMAX + 1];
+    double sH[LMAX + 1], sV[LMAX + 1], sD[LMAX + 1], tot[LMAX + 1];
+#pragma unroll
+    for (int l = 0; l <= LMAX; ++l) { cur[l] = -1; cbi[l] = cbj[l] = 0; sH[l] = sV[l] = sD[l] = tot[l] = 0.0; }
+    double sA = 0.0, totA = 0.0;
+    unsigned long long count = 0, wp = (MODE == 2) ? pos[y] : 0;
+
+    auto flush = [&](int l) {
+        const double sc = 1.0 / (double)(1 << l);
+        const double pH = sH[l] * sc, pV = sV[l] * sc, pD = sD[l] * sc;
+        if (l == L) { if (MODE == 0) totA += fabs(sA * sc); sA = 0.0; }
+        sH[l] = sV[l] = sD[l] = 0.0;
+        const int wl = nx >> l, hl = ny >> l;
+        if (!act[off.off[l] + (uint64_t)cbi[l] * wl + cbj[l]]) return;
+        if (MODE == 0) {
+            tot[l] += fabs(pH) + fabs(pV) + fabs(pD);
+        } else {
+            const float v[3] = {(float)pH, (float)pV, (float)pD};
+            const unsigned z[3] = {(unsigned)((hl + cbi[l]) * nx + cbj[l]), (unsigned)(cbi[l] * nx + wl + cbj[l]),
+                                   (unsigned)((hl + cbi[l]) * nx + wl + cbj[l])};
+#pragma unroll
+            for (int s = 0; s < 3; ++s)
+                if (v[s] < 0.0f) {
+                    if (MODE == 1) ++count;
+                    else { keys[wp] = z[s]; vals[wp] = make_uint2((unsigned)y, __float_as_uint(v[s])); ++wp; }
+                }
+        }
+    };
+
+    const uint64_t lo = rp[y], hi = rp[y + 1];
+    for (uint64_t k = lo; k < hi; ++k) {
+        const uint2 e = A[k];
+        const double h = hval(e);
+        if (L == 0) { if (MODE == 0) totA += fabs(h); continue; }
+        const int iy = (int)(e.x / (unsigned)nx), ix = (int)(e.x % (unsigned)nx);
+#pragma unroll
+        for (int l = 1; l <= LMAX; ++l) {
+            if (l > L) break;
+            const int bi = iy >> l, bj = ix >> l;
+            const int key = bi * (nx >> l) + bj;
+            if (key != cur[l]) {
+                if (cur[l] >= 0) flush(l);
+                cur[l] = key; cbi[l] = bi; cbj[l] = bj;
+            }
+            const bool top = ((iy >> (l - 1)) & 1) == 0, left = ((ix >> (l - 1)) & 1) == 0;
+            sH[l] += top ? h : -h;
+            sV[l] += left ? h : -h;
+            sD[l] += (top == left) ? h : -h;
+            if (l == L) sA += h;
+        }
+    }
+#pragma unroll
+    for (int l = 1; l <= LMAX; ++l)
+        if (l <= L && cur[l] >= 0) flush(l);
+    if (MODE == 0) {
+        double z = totA;
+#pragma unroll
+        for (int l = LMAX; l >= 1; --l)
+            if (l <= L) z += tot[l];
+        zrow[y] = z;
+    } else if (MODE == 1) {
+        cnt[y] = count;
+    }
+}
+
+// Signed split (K5): warp per active detail coefficient,
+// b-(z) = sum over its Phi^- column of q(y) phi(y|z) in fp64.
+__global__ void __launch_bounds__(256) k_split(uint64_t nlist, const unsigned* __restrict__ list,
+                                               const unsigned long long* __restrict__ ptr,
+                                               const uint2* __restrict__ E, const float* __restrict__ q,
+                                               double* __restrict__ bm) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlist; i += W) {
+        const unsigned z = list[i];
+        const uint64_t lo = ptr[z], hi = ptr[z + 1];
+        double a0 = 0.0, a1 = 0.0;
+        uint64_t k = lo + lane;
+        for (; k + 32 < hi; k += 64) {
+            const uint2 e0 = ld_stream(E + k), e1 = ld_stream(E + k + 32);
+            a0 = fma(hval(e0), (double)__ldg(q + e0.x), a0);
+            a1 = fma(hval(e1), (double)__ldg(q + e1.x), a1);
+        }
+        for (; k < hi; k += 32) {
+            const uint2 e0 = ld_stream(E + k);
+            a0 = fma(hval(e0), (double)__ldg(q + e0.x), a0);
+        }
+        const double s = warp_sum(a0 + a1);
+        if (lane == 0) bm[z] = s;
+    }
+}
+
+}  // namespace wamgpu

@@ -1,0 +1,1071 @@
+// wamgpu.cu — host orchestration and C-ABI of libwamgpu.so (include/wamgpu.h).
+//
+// One context per GPU.  Per wavelet-AM iteration (PAPER.md
+// Algorithm 1) the context launches, on its own stream:
+//   k_back<0>   g = H^T q                      (CSC gather, fp64)      K3
+//   k_split     b-(z) over Phi^- columns        (active details only)  K5
+//   [ncclAllReduce SUM fp64 over (g | b-)]      (view-sharded 2D only)
+//   k_tile<1>   S = Omega^T g; b+ = S - b-; root solve; mu = Omega beta  K4+K6+K1
+//   k_forward<1> l = H mu, q = I0 e^-l, I-div partials                  K2
+//   k_sum_partials + [allreduce] + k_record
+// At scheduled expansions: k_tile<0> (fp64 image) -> max -> k_mark ->
+// k_walk<0> (Z0) -> k_walk<1,2> + radix sort (Phi^- CSC rebuild)      K7, K8.
+// The AM baseline is k_back<1> (fused update) + k_forward<1>.
+#include <cub/cub.cuh>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/wamgpu.h"
+#include "host_model.hpp"
+#include "kernels.cuh"
+
+namespace wamgpu {
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+#define NK(x)                                                                                     \
+    do {                                                                                          \
+        ncclResult_t r_ = (x);                                                                    \
+        if (r_ != ncclSuccess) throw CudaError(std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void alloc(size_t n_) {
+        release();
+        if (n_) CK(cudaMalloc(&p, n_ * sizeof(T)));
+        n = n_;
+    }
+    void ensure(size_t n_) { if (n < n_) alloc(n_); }
+    void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+    void swap(DBuf& o) { std::swap(p, o.p); std::swap(n, o.n); }
+};
+
+enum Cat { T_FWD = 0, T_BACK, T_SPLIT, T_UPDATE, T_EXPAND, T_COMM, T_NCAT };
+
+}  // namespace wamgpu
+
+using wamgpu::DBuf;
+using wamgpu::ActOff;
+using wamgpu::Cat;
+using wamgpu::T_NCAT;
+using wamgpu::CudaError;
+
+struct wamgpu_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    int sms = 148;
+    std::string err;
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1;
+    // grid / matrix
+    int nx = 0, ny = 0, nz = 1;
+    bool have_grid = false, have_matrix = false;
+    uint64_t M = 0, N = 0, row0 = 0, row1 = 0, Ml = 0, nnz = 0;
+    DBuf<unsigned long long> rp, cp;
+    DBuf<uint2> A, C;
+    // data
+    DBuf<float> d, I0, q;
+    bool have_data = false;
+    // state
+    int algo = 0;  // 1 AM, 2 WAM
+    DBuf<float> mu, beta, fscratch;
+    DBuf<double> g, bdata, bam, mu64, bp_dbg, bm_dbg, zrow, dscratch;
+    int L = 0;
+    DBuf<uint8_t> act, act_new;
+    ActOff off{};
+    uint64_t act_bytes = 0;
+    std::vector<uint8_t> act_host;
+    DBuf<unsigned long long> np;
+    DBuf<uint2> E;
+    DBuf<unsigned> list;
+    uint64_t nlist = 0, nnz_phi = 0;
+    double Z0 = 0.0;
+    DBuf<double> scal, partial;
+    int nblk_row = 1, nblk_col = 1;
+    DBuf<unsigned long long> counters;
+    DBuf<int> flag, it;
+    DBuf<double> objs;
+    DBuf<unsigned long long> cums;
+    int iter = 0;
+    int64_t active = 0;
+    cudaEvent_t ev_t0 = nullptr, ev_a = nullptr, ev_b = nullptr;
+    std::vector<cudaEvent_t> ev_iter;
+    // timing
+    bool ktime = false;
+    wamgpu_timing tm{};
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev[T_NCAT];
+    size_t tev_used[T_NCAT] = {};
+    int64_t launches = 0;
+
+    void timer_begin(Cat c) {
+        if (!ktime) return;
+        auto& v = tev[c];
+        if (tev_used[c] == v.size()) {
+            cudaEvent_t a, b;
+            CK(cudaEventCreate(&a));
+            CK(cudaEventCreate(&b));
+            v.push_back({a, b});
+        }
+        CK(cudaEventRecord(v[tev_used[c]].first, st));
+    }
+    void timer_end(Cat c) {
+        if (!ktime) return;
+        CK(cudaEventRecord(tev[c][tev_used[c]].second, st));
+        tev_used[c]++;
+    }
+};
+
+namespace wamgpu {
+using Ctx = ::wamgpu_ctx;
+
+static thread_local std::string g_err;
+
+// ------------------------------------------------------------- utilities
+static inline unsigned blocks_for(uint64_t n, unsigned bs) { return (unsigned)((n + bs - 1) / bs); }
+
+static void launched(Ctx* c, int n = 1) { c->launches += n; }
+
+static void check_launch(Ctx* c) {
+    CK(cudaGetLastError());
+    launched(c);
+}
+
+static void exclusive_scan_u64(Ctx* c, unsigned long long* inout, uint64_t n) {
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, inout, inout, (int64_t)n, c->st));
+    DBuf<uint8_t> tmp;
+    tmp.alloc(tb + 1);
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, inout, inout, (int64_t)n, c->st));
+    launched(c);
+}
+
+static int bits_for(uint64_t n) {
+    int b = 1;
+    while ((1ull << b) <= n) ++b;
+    return b;
+}
+
+// stable sort of (key, value) pairs by key; output in keys_out / vals_out
+static void sort_pairs(Ctx* c, DBuf<unsigned>& kin, DBuf<uint2>& vin, DBuf<unsigned>& kout, DBuf<uint2>& vout,
+                       uint64_t n, uint64_t maxkey) {
+    kout.alloc(std::max<uint64_t>(n, 1));
+    vout.alloc(std::max<uint64_t>(n, 1));
+    if (n == 0) return;
+    const int bits = bits_for(maxkey);
+    auto vi = reinterpret_cast<unsigned long long*>(vin.p);
+    auto vo = reinterpret_cast<unsigned long long*>(vout.p);
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.p, kout.p, vi, vo, (int64_t)n, 0, bits, c->st));
+    DBuf<uint8_t> tmp;
+    tmp.alloc(tb + 1);
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, kin.p, kout.p, vi, vo, (int64_t)n, 0, bits, c->st));
+    launched(c, 4);
+}
+
+static void allreduce_sum(Ctx* c, double* buf, size_t n) {
+    if (c->nranks <= 1) return;
+    c->timer_begin(T_COMM);
+    NK(ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, c->comm, c->st));
+    c->timer_end(T_COMM);
+}
+static void allreduce_max(Ctx* c, double* buf, size_t n) {
+    if (c->nranks <= 1) return;
+    c->timer_begin(T_COMM);
+    NK(ncclAllReduce(buf, buf, n, ncclDouble, ncclMax, c->comm, c->st));
+    c->timer_end(T_COMM);
+}
+
+static void check_flag(Ctx* c, const char* where) {
+    int f = 0;
+    CK(cudaMemcpyAsync(&f, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (f) {
+        CK(cudaMemsetAsync(c->flag.p, 0, sizeof(int), c->st));
+        std::string what = std::string(where) + ": ";
+        if (f & 1) what += "non-finite line integral; ";
+        if (f & 2) what += "non-finite AM update; ";
+        if (f & 4) what += "non-finite coefficient update; ";
+        throw NumericError(what);
+    }
+}
+
+// ------------------------------------------------------------- system model
+static void finish_matrix(Ctx* c) {
+    // CSC mirror (system_matrix.hpp:61-75): stable radix sort of CSR entries by
+    // column keeps rows ascending within every column.
+    DBuf<unsigned> kin, kout;
+    DBuf<uint2> vin, vout;
+    kin.alloc(std::max<uint64_t>(c->nnz, 1));
+    vin.alloc(std::max<uint64_t>(c->nnz, 1));
+    if (c->nnz) {
+        k_csr_to_pairs<<<c->sms * 8, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, kin.p, vin.p);
+        check_launch(c);
+    }
+    sort_pairs(c, kin, vin, kout, vout, c->nnz, c->N);
+    kin.release();
+    vin.release();
+    c->cp.alloc(c->N + 1);
+    k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(kout.p, c->nnz, c->N, c->cp.p);
+    check_launch(c);
+    c->C.swap(vout);
+    c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->Ml + 7) / 8, (uint64_t)c->sms * 16));
+    c->nblk_col = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->N + 7) / 8, (uint64_t)c->sms * 16));
+    c->partial.alloc(std::max(c->nblk_row, 1024));
+    c->scal.alloc(8);
+    c->zrow.alloc(c->Ml + 1);
+    CK(cudaStreamSynchronize(c->st));
+    c->have_matrix = true;
+    c->algo = 0;
+}
+
+static void set_geometry(Ctx* c, const wamgpu_geometry& g) {
+    validate(g);
+    if (g.nz != 1) throw ConfigError("wamgpu: device path supports nz == 1 (2D slices) in this build");
+    std::vector<RayD> rays = ray_table(g);
+    const int V = g.views, D = g.detectors;
+    const int v0 = (int)((int64_t)V * c->rank / c->nranks), v1 = (int)((int64_t)V * (c->rank + 1) / c->nranks);
+    c->nx = g.nx; c->ny = g.ny; c->nz = g.nz; c->have_grid = true;
+    c->M = (uint64_t)V * D;
+    c->N = (uint64_t)g.nx * g.ny;
+    c->row0 = (uint64_t)v0 * D;
+    c->row1 = (uint64_t)v1 * D;
+    c->Ml = c->row1 - c->row0;
+    DBuf<RayDev> dr;
+    dr.alloc(std::max<uint64_t>(c->Ml, 1));
+    if (c->Ml)
+        CK(cudaMemcpyAsync(dr.p, rays.data() + c->row0, c->Ml * sizeof(RayDev), cudaMemcpyHostToDevice, c->st));
+    c->rp.alloc(c->Ml + 1);
+    k_trace_count<<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(dr.p, c->Ml, g.nx, g.ny, g.voxel_size, c->rp.p);
+    check_launch(c);
+    exclusive_scan_u64(c, c->rp.p, c->Ml + 1);
+    unsigned long long nnz = 0;
+    CK(cudaMemcpyAsync(&nnz, c->rp.p + c->Ml, sizeof(nnz), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->nnz = nnz;
+    c->A.alloc(std::max<uint64_t>(nnz, 1));
+    if (c->Ml) {
+        k_trace_fill<<<blocks_for(c->Ml, 128), 128, 0, c->st>>>(dr.p, c->Ml, g.nx, g.ny, g.voxel_size, c->rp.p, c->A.p);
+        check_launch(c);
+    }
+    finish_matrix(c);
+}
+
+static void set_matrix_csr(Ctx* c, uint64_t rows, uint64_t cols, uint64_t nnz, const uint64_t* rp,
+                           const uint32_t* ci, const double* val) {
+    if (!rp || (nnz && (!ci || !val))) throw ContractError("SystemMatrix: null array");
+    if (rp[0] != 0 || rp[rows] != nnz) throw ContractError("SystemMatrix: inconsistent CSR arrays");
+    for (uint64_t y = 0; y < rows; ++y)
+        if (rp[y + 1] < rp[y]) throw ContractError("SystemMatrix: row_ptr not monotone");
+    if (c->have_grid && (uint64_t)c->nx * c->ny != cols)
+        throw ContractError("SystemMatrix: cols != nx*ny of the grid");
+    c->M = rows;
+    c->N = cols;
+    c->row0 = rows * c->rank / c->nranks;
+    c->row1 = rows * (c->rank + 1) / c->nranks;
+    c->Ml = c->row1 - c->row0;
+    const uint64_t k0 = rp[c->row0], k1 = rp[c->row1];
+    c->nnz = k1 - k0;
+    std::vector<unsigned long long> lrp(c->Ml + 1);
+    for (uint64_t y = 0; y <= c->Ml; ++y) lrp[y] = rp[c->row0 + y] - k0;
+    std::vector<uint2> ent(std::max<uint64_t>(c->nnz, 1));
+    for (uint64_t k = 0; k < c->nnz; ++k) {
+        if (ci[k0 + k] >= cols) throw ContractError("SystemMatrix: column index out of range");
+        ent[k] = make_uint2(ci[k0 + k], 0);
+        float f = (float)val[k0 + k];
+        std::memcpy(&ent[k].y, &f, 4);
+    }
+    c->rp.alloc(c->Ml + 1);
+    c->A.alloc(std::max<uint64_t>(c->nnz, 1));
+    CK(cudaMemcpyAsync(c->rp.p, lrp.data(), (c->Ml + 1) * 8, cudaMemcpyHostToDevice, c->st));
+    if (c->nnz) CK(cudaMemcpyAsync(c->A.p, ent.data(), c->nnz * 8, cudaMemcpyHostToDevice, c->st));
+    if (!c->have_grid) { c->nx = (int)cols; c->ny = 1; c->nz = 1; }
+    finish_matrix(c);
+}
+
+// ------------------------------------------------------------- pipeline steps
+static void need_matrix(Ctx* c) { if (!c->have_matrix) throw ContractError("wamgpu: no system matrix set"); }
+static void need_data(Ctx* c) { if (!c->have_data) throw ContractError("wamgpu: no transmission data set"); }
+
+static void back_into(Ctx* c, const float* w, double* out) {
+    c->timer_begin(T_BACK);
+    k_back<0><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
+    check_launch(c);
+    c->timer_end(T_BACK);
+    c->tm.back_launches++;
+}
+
+// q = I0 exp(-H mu), objective -> scal[0] (all-reduced), record
+static void forward_fused(Ctx* c, bool record) {
+    c->timer_begin(T_FWD);
+    k_forward<1><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, c->q.p, nullptr,
+                                                c->partial.p, c->flag.p);
+    check_launch(c);
+    c->timer_end(T_FWD);
+    c->tm.fwd_launches++;
+    k_sum_partials<<<1, 1024, 0, c->st>>>(c->partial.p, c->nblk_row, c->scal.p);
+    check_launch(c);
+    allreduce_sum(c, c->scal.p, 1);
+    if (record) {
+        k_record<<<1, 32, 0, c->st>>>(c->scal.p, c->counters.p, c->objs.p, c->cums.p, c->it.p);
+        check_launch(c);
+    }
+}
+
+static double device_max(Ctx* c, const double* v, uint64_t n) {
+    const int nb = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + 255) / 256), 1024);
+    k_max_partials<<<nb, 256, 0, c->st>>>(v, n, c->partial.p);
+    check_launch(c);
+    k_max_partials<<<1, 256, 0, c->st>>>(c->partial.p, (uint64_t)nb, c->scal.p + 1);
+    check_launch(c);
+    allreduce_max(c, c->scal.p + 1, 1);
+    double m = 0.0;
+    CK(cudaMemcpyAsync(&m, c->scal.p + 1, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return m;
+}
+
+// Z0 = max_y sum_{z active} |phi(y|z)| (Eq. 1.61); AM: levels = 0 -> row sums.
+static double compute_z0(Ctx* c, int levels) {
+    if (c->Ml) {
+        k_walk<0><<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, levels,
+                                                                  c->act.p, c->off, c->zrow.p, nullptr, nullptr,
+                                                                  nullptr, nullptr);
+        check_launch(c);
+    }
+    double z0 = device_max(c, c->zrow.p, c->Ml);
+    if (!(z0 > 0.0)) throw NumericError("Z0: no ray intersects the active set");
+    return z0;
+}
+
+static void ensure_records(Ctx* c, int n) {
+    if ((int)c->objs.n < n) {
+        c->objs.alloc(n);
+        c->cums.alloc(n);
+    }
+    CK(cudaMemsetAsync(c->it.p, 0, sizeof(int), c->st));
+    while ((int)c->ev_iter.size() < n) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->ev_iter.push_back(e);
+    }
+}
+
+static void begin_call(Ctx* c) {
+    c->tm = wamgpu_timing{};
+    for (int k = 0; k < T_NCAT; ++k) c->tev_used[k] = 0;
+    c->launches = 0;
+    CK(cudaEventRecord(c->ev_a, c->st));
+}
+
+static void end_call(Ctx* c) {
+    CK(cudaEventRecord(c->ev_b, c->st));
+    CK(cudaEventSynchronize(c->ev_b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
+    c->tm.total_ms = ms;
+    double* dst[T_NCAT] = {&c->tm.fwd_ms, &c->tm.back_ms, &c->tm.split_ms, &c->tm.update_ms, &c->tm.expand_ms,
+                           &c->tm.comm_ms};
+    for (int k = 0; k < T_NCAT; ++k) {
+        double s = 0.0;
+        for (size_t i = 0; i < c->tev_used[k]; ++i) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, c->tev[k][i].first, c->tev[k][i].second));
+            s += t;
+        }
+        *dst[k] = s;
+    }
+    c->tm.kernel_launches = c->launches;
+    c->tm.split_nnz = (int64_t)c->nnz_phi;
+}
+
+static void fill_records(Ctx* c, int n, wamgpu_record* recs, int64_t active_at_start) {
+    if (!recs) return;
+    std::vector<double> o(n);
+    std::vector<unsigned long long> cu(n);
+    CK(cudaMemcpyAsync(o.data(), c->objs.p, n * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(cu.data(), c->cums.p, n * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (int i = 0; i < n; ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev_t0, c->ev_iter[i]));
+        recs[i].iter = c->iter - n + i + 1;
+        recs[i].objective = o[i];
+        recs[i].elapsed_s = ms * 1e-3;
+        recs[i].active_set = active_at_start;
+        recs[i].cum_updates = (int64_t)cu[i];
+    }
+}
+
+// ------------------------------------------------------------------ AM
+static void am_init(Ctx* c, const double* init_mu) {
+    need_matrix(c);
+    need_data(c);
+    c->mu.alloc(c->N);
+    c->g.alloc(2 * c->N);
+    c->bam.alloc(c->N);
+    if (init_mu) {
+        std::vector<float> m(c->N);
+        for (uint64_t x = 0; x < c->N; ++x) m[x] = (float)init_mu[x];
+        CK(cudaMemcpyAsync(c->mu.p, m.data(), c->N * 4, cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    } else {
+        CK(cudaMemsetAsync(c->mu.p, 0, c->N * 4, c->st));
+    }
+    back_into(c, c->d.p, c->bam.p);  // b(x) = sum_y d(y) h(y|x)
+    allreduce_sum(c, c->bam.p, c->N);
+    if (!c->act.p) { c->act.alloc(1); }
+    c->Z0 = compute_z0(c, 0);        // Z0 = max_y sum_x h(y|x)
+    forward_fused(c, false);
+    CK(cudaMemsetAsync(c->counters.p, 0, 16, c->st));
+    CK(cudaEventRecord(c->ev_t0, c->st));
+    check_flag(c, "am_init");
+    c->algo = 1;
+    c->iter = 0;
+    c->active = (int64_t)c->N;
+}
+
+static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
+    if (c->algo != 1) throw ContractError("am: not initialised");
+    ensure_records(c, n);
+    for (int i = 0; i < n; ++i) {
+        if (c->nranks == 1) {
+            c->timer_begin(T_BACK);
+            k_back<1><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, c->q.p, nullptr, c->bam.p, c->mu.p,
+                                                      c->Z0, c->flag.p);
+            check_launch(c);
+            c->timer_end(T_BACK);
+            c->tm.back_launches++;
+        } else {
+            back_into(c, c->q.p, c->g.p);
+            allreduce_sum(c, c->g.p, c->N);
+            k_am_update<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->g.p, c->bam.p, c->mu.p, c->Z0, c->flag.p);
+            check_launch(c);
+        }
+        CK(cudaMemsetAsync(c->counters.p, 0, 8, c->st));
+        forward_fused(c, true);
+        CK(cudaEventRecord(c->ev_iter[i], c->st));
+        c->iter++;
+    }
+    check_flag(c, "am_iterate");
+    if (recs) {
+        std::vector<double> o(n);
+        CK(cudaMemcpyAsync(o.data(), c->objs.p, n * 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        for (int i = 0; i < n; ++i) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, c->ev_t0, c->ev_iter[i]));
+            recs[i].iter = c->iter - n + i + 1;
+            recs[i].objective = o[i];
+            recs[i].elapsed_s = ms * 1e-3;
+            recs[i].active_set = (int64_t)c->N;
+            recs[i].cum_updates = (int64_t)c->N * recs[i].iter;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ WAM
+static void tile_launch(Ctx* c, int mode, double* mu64, double* out) {
+    const int TS = 1 << c->L;
+    dim3 grid(c->nx >> c->L, c->ny >> c->L);
+    const int bs = std::min(1024, std::max(32, TS * TS));
+    const size_t smem = 2ull * TS * TS * sizeof(double);
+    k_tile<<<grid, bs, smem, c->st>>>(mode, c->nx, c->ny, c->L, c->g.p, c->g.p + c->N, c->bdata.p, c->act.p, c->off,
+                                      c->beta.p, c->mu.p, mu64, out, c->bp_dbg.p, c->bm_dbg.p, c->Z0,
+                                      c->counters.p, c->flag.p);
+    check_launch(c);
+}
+
+static void rebuild_phi(Ctx* c) {
+    // active detail list from the host tree (ascending Mallat index)
+    std::vector<unsigned> lst;
+    for (int l = 1; l <= c->L; ++l) {
+        const int wl = c->nx >> l, hl = c->ny >> l;
+        const uint8_t* a = c->act_host.data() + c->off.off[l];
+        for (int bi = 0; bi < hl; ++bi)
+            for (int bj = 0; bj < wl; ++bj)
+                if (a[(uint64_t)bi * wl + bj]) {
+                    lst.push_back((unsigned)((hl + bi) * c->nx + bj));
+                    lst.push_back((unsigned)(bi * c->nx + wl + bj));
+                    lst.push_back((unsigned)((hl + bi) * c->nx + wl + bj));
+                }
+    }
+    std::sort(lst.begin(), lst.end());
+    c->nlist = lst.size();
+    c->list.alloc(std::max<size_t>(lst.size(), 1));
+    if (!lst.empty())
+        CK(cudaMemcpyAsync(c->list.p, lst.data(), lst.size() * 4, cudaMemcpyHostToDevice, c->st));
+    // Phi^- CSC over local rays: count -> scan -> emit -> stable sort by z
+    DBuf<unsigned long long> pos;
+    pos.alloc(c->Ml + 1);
+    k_walk<1><<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->L, c->act.p,
+                                                              c->off, nullptr, pos.p, nullptr, nullptr, nullptr);
+    check_launch(c);
+    exclusive_scan_u64(c, pos.p, c->Ml + 1);
+    unsigned long long tot = 0;
+    CK(cudaMemcpyAsync(&tot, pos.p + c->Ml, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    DBuf<unsigned> kin, kout;
+    DBuf<uint2> vin;
+    kin.alloc(std::max<uint64_t>(tot, 1));
+    vin.alloc(std::max<uint64_t>(tot, 1));
+    if (tot) {
+        k_walk<2><<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->L,
+                                                                  c->act.p, c->off, nullptr, nullptr, pos.p, kin.p,
+                                                                  vin.p);
+        check_launch(c);
+    }
+    DBuf<uint2> vout;
+    sort_pairs(c, kin, vin, kout, vout, tot, c->N);
+    c->np.alloc(c->N + 1);
+    k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(kout.p, tot, c->N, c->np.p);
+    check_launch(c);
+    c->E.swap(vout);
+    c->nnz_phi = tot;
+    CK(cudaStreamSynchronize(c->st));
+}
+
+static int64_t count_active(const Ctx* c) {
+    int64_t a = (int64_t)(c->nx >> c->L) * (c->ny >> c->L);
+    for (int l = 1; l <= c->L; ++l) {
+        const uint64_t n = (uint64_t)(c->nx >> l) * (c->ny >> l);
+        const uint8_t* p = c->act_host.data() + c->off.off[l];
+        for (uint64_t i = 0; i < n; ++i) a += 3 * (p[i] != 0);
+    }
+    return a * c->nz;
+}
+
+static void wam_init(Ctx* c, int L, const double* init_beta) {
+    need_matrix(c);
+    need_data(c);
+    if (!c->have_grid) throw ContractError("wam: image grid unknown (set_geometry or set_grid)");
+    if (L < 0 || L > LMAX) throw ConfigError("haar: depth must be in [0, " + std::to_string(LMAX) + "]");
+    if ((c->nx % (1 << L)) || (c->ny % (1 << L))) throw ConfigError("haar: slice dimensions not divisible by 2^L");
+    c->L = L;
+    const uint64_t N = c->N;
+    c->mu.alloc(N); c->beta.alloc(N); c->g.alloc(2 * N); c->bdata.alloc(N); c->mu64.alloc(N);
+    c->bp_dbg.alloc(N); c->bm_dbg.alloc(N);
+    CK(cudaMemsetAsync(c->g.p, 0, 2 * N * 8, c->st));
+    CK(cudaMemsetAsync(c->bp_dbg.p, 0, N * 8, c->st));
+    CK(cudaMemsetAsync(c->bm_dbg.p, 0, N * 8, c->st));
+    // tree bitmaps, level l at off[l]
+    uint64_t o = 0;
+    for (int l = 0; l <= LMAX + 1; ++l) c->off.off[l] = 0;
+    for (int l = 1; l <= L; ++l) { c->off.off[l] = o; o += (uint64_t)(c->nx >> l) * (c->ny >> l); }
+    c->act_bytes = o;
+    c->act.alloc(std::max<uint64_t>(o, 1));
+    c->act_new.alloc(std::max<uint64_t>(o, 1));
+    CK(cudaMemsetAsync(c->act.p, 0, std::max<uint64_t>(o, 1), c->st));
+    c->act_host.assign(o, 0);
+    if (init_beta) {
+        std::vector<float> b(N);
+        for (uint64_t z = 0; z < N; ++z) b[z] = (float)init_beta[z];
+        CK(cudaMemcpyAsync(c->beta.p, b.data(), N * 4, cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    } else {
+        CK(cudaMemsetAsync(c->beta.p, 0, N * 4, c->st));
+    }
+    // b(z) = [Omega^T H^T d](z) for every z
+    back_into(c, c->d.p, c->g.p);
+    allreduce_sum(c, c->g.p, N);
+    tile_launch(c, 2, nullptr, c->bdata.p);
+    CK(cudaMemsetAsync(c->g.p, 0, 2 * N * 8, c->st));
+    c->Z0 = compute_z0(c, L);
+    c->nlist = 0;
+    c->nnz_phi = 0;
+    rebuild_phi(c);
+    tile_launch(c, 0, nullptr, nullptr);  // mu = Omega beta
+    forward_fused(c, false);
+    CK(cudaMemsetAsync(c->counters.p, 0, 16, c->st));
+    CK(cudaEventRecord(c->ev_t0, c->st));
+    check_flag(c, "wam_init");
+    c->algo = 2;
+    c->iter = 0;
+    c->active = count_active(c);
+}
+
+static void wam_step(Ctx* c) {
+    back_into(c, c->q.p, c->g.p);
+    if (c->nlist) {
+        c->timer_begin(T_SPLIT);
+        const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist + 7) / 8, (uint64_t)c->sms * 16);
+        k_split<<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->np.p, c->E.p, c->q.p, c->g.p + c->N);
+        check_launch(c);
+        c->timer_end(T_SPLIT);
+        c->tm.split_launches++;
+    }
+    allreduce_sum(c, c->g.p, 2 * c->N);
+    c->timer_begin(T_UPDATE);
+    tile_launch(c, 1, nullptr, nullptr);
+    c->timer_end(T_UPDATE);
+    c->tm.update_launches++;
+    forward_fused(c, true);
+}
+
+static void wam_iterate(Ctx* c, int n, wamgpu_record* recs) {
+    if (c->algo != 2) throw ContractError("wam: not initialised");
+    ensure_records(c, n);
+    for (int i = 0; i < n; ++i) {
+        wam_step(c);
+        CK(cudaEventRecord(c->ev_iter[i], c->st));
+        c->iter++;
+    }
+    check_flag(c, "wam_iterate");
+    fill_records(c, n, recs, c->active);
+}
+
+static int64_t wam_expand(Ctx* c, double factor) {
+    if (c->algo != 2) throw ContractError("wam: not initialised");
+    c->timer_begin(T_EXPAND);
+    tile_launch(c, 0, c->mu64.p, nullptr);         // fp64 criterion image Omega beta
+    const double mx = device_max(c, c->mu64.p, c->N);  // nz == 1: the z-sum is the slice
+    int64_t newly = 0;
+    if (mx > 0.0 && c->L > 0) {
+        const double thr = factor * mx;
+        CK(cudaMemcpyAsync(c->act_new.p, c->act.p, c->act_bytes, cudaMemcpyDeviceToDevice, c->st));
+        k_mark<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->nx, c->ny, c->L, c->mu64.p, thr, c->act.p, c->act_new.p,
+                                                          c->off);
+        check_launch(c);
+        c->act.swap(c->act_new);
+        std::vector<uint8_t> h(c->act_bytes);
+        CK(cudaMemcpyAsync(h.data(), c->act.p, c->act_bytes, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        for (uint64_t i = 0; i < c->act_bytes; ++i) newly += (h[i] != 0) - (c->act_host[i] != 0);
+        c->act_host.swap(h);
+        if (newly > 0) {
+            c->Z0 = compute_z0(c, c->L);
+            rebuild_phi(c);
+            c->active = count_active(c);
+        }
+    }
+    c->timer_end(T_EXPAND);
+    c->tm.expand_events++;
+    return newly;
+}
+
+static void wam_run(Ctx* c, int iters, const int* sched, int nsched, double factor, wamgpu_record* recs) {
+    if (c->algo != 2) throw ContractError("wam: not initialised");
+    ensure_records(c, iters);
+    std::vector<int64_t> act_at(iters);
+    int done = 0;
+    for (int it = 1; it <= iters; ++it) {
+        act_at[it - 1] = c->active;
+        wam_step(c);
+        CK(cudaEventRecord(c->ev_iter[it - 1], c->st));
+        c->iter++;
+        ++done;
+        for (int k = 0; k < nsched; ++k)
+            if (sched[k] == it) { wam_expand(c, factor); break; }
+    }
+    check_flag(c, "wam_run");
+    if (recs) {
+        fill_records(c, iters, recs, 0);
+        for (int i = 0; i < iters; ++i) recs[i].active_set = act_at[i];
+    }
+}
+
+static Ctx* create(int device) {
+    auto c = std::make_unique<wamgpu_ctx>();
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) throw CudaError("wamgpu: requires an sm_100a (Blackwell) device");
+    c->sms = prop.multiProcessorCount;
+    CK(cudaEventCreate(&c->ev_t0));
+    CK(cudaEventCreate(&c->ev_a));
+    CK(cudaEventCreate(&c->ev_b));
+    c->flag.alloc(1);
+    c->it.alloc(1);
+    c->counters.alloc(2);
+    c->scal.alloc(8);
+    c->partial.alloc(1024);
+    CK(cudaMemsetAsync(c->flag.p, 0, 4, c->st));
+    CK(cudaMemsetAsync(c->counters.p, 0, 16, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return c.release();
+}
+
+static void destroy(Ctx* c) {
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->st);
+    for (auto& v : c->tev)
+        for (auto& p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    for (auto e : c->ev_iter) cudaEventDestroy(e);
+    if (c->ev_t0) cudaEventDestroy(c->ev_t0);
+    if (c->ev_a) cudaEventDestroy(c->ev_a);
+    if (c->ev_b) cudaEventDestroy(c->ev_b);
+    if (c->comm) ncclCommDestroy(c->comm);
+    c->A.release(); c->C.release(); c->E.release();
+    cudaStreamDestroy(c->st);
+    delete c;
+}
+
+}  // namespace wamgpu
+
+using namespace wamgpu;
+
+
+#define API_TRY(ctx, ...)                                                             \
+    try {                                                                             \
+        if (ctx) CK(cudaSetDevice((ctx)->device));                                    \
+        __VA_ARGS__;                                                                  \
+        return WAMGPU_OK;                                                             \
+    } catch (const wamgpu::Error& e) {                                                \
+        g_err = e.what();                                                             \
+        if (ctx) const_cast<wamgpu_ctx*>(ctx)->err = e.what();     \
+        return e.code;                                                                \
+    } catch (const std::exception& e) {                                               \
+        g_err = e.what();                                                             \
+        if (ctx) const_cast<wamgpu_ctx*>(ctx)->err = e.what();     \
+        return WAMGPU_ERR_CONTRACT;                                                   \
+    }
+
+#define NEED(p) do { if (!(p)) throw ContractError("null argument: " #p); } while (0)
+
+extern "C" {
+
+int wamgpu_version(void) { return 1; }
+
+const char* wamgpu_last_error(const wamgpu_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int wamgpu_create(int device, wamgpu_ctx** out) {
+    const wamgpu_ctx* none = nullptr;
+    API_TRY(none, {
+        NEED(out);
+        *out = create(device);
+    })
+}
+
+int wamgpu_destroy(wamgpu_ctx* ctx) {
+    if (!ctx) return WAMGPU_OK;
+    destroy(ctx);
+    return WAMGPU_OK;
+}
+
+int wamgpu_nccl_unique_id(void* id128) {
+    const wamgpu_ctx* none = nullptr;
+    API_TRY(none, {
+        NEED(id128);
+        ncclUniqueId id;
+        NK(ncclGetUniqueId(&id));
+        std::memcpy(id128, &id, sizeof(id));
+    })
+}
+
+int wamgpu_set_comm(wamgpu_ctx* ctx, const void* id128, int rank, int nranks) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw ContractError("set_comm: bad rank/nranks");
+        if (ctx->have_matrix) throw ContractError("set_comm must precede the system matrix");
+        if (ctx->comm) { ncclCommDestroy(ctx->comm); ctx->comm = nullptr; }
+        ctx->rank = rank;
+        ctx->nranks = nranks;
+        if (nranks > 1) {
+            NEED(id128);
+            ncclUniqueId id;
+            std::memcpy(&id, id128, sizeof(id));
+            NK(ncclCommInitRank(&ctx->comm, nranks, id, rank));
+        }
+    })
+}
+
+int wamgpu_set_geometry(wamgpu_ctx* ctx, const wamgpu_geometry* g) {
+    API_TRY(ctx, { NEED(ctx); NEED(g); set_geometry(ctx, *g); })
+}
+
+int wamgpu_set_grid(wamgpu_ctx* ctx, int nx, int ny, int nz) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (nx < 1 || ny < 1 || nz != 1) throw ConfigError("set_grid: invalid grid (nz must be 1)");
+        if (ctx->have_matrix && (uint64_t)nx * ny != ctx->N) throw ContractError("set_grid: nx*ny != matrix cols");
+        ctx->nx = nx; ctx->ny = ny; ctx->nz = nz; ctx->have_grid = true;
+    })
+}
+
+int wamgpu_set_matrix_csr(wamgpu_ctx* ctx, uint64_t rows, uint64_t cols, uint64_t nnz, const uint64_t* rp,
+                          const uint32_t* ci, const double* val) {
+    API_TRY(ctx, { NEED(ctx); set_matrix_csr(ctx, rows, cols, nnz, rp, ci, val); })
+}
+
+int wamgpu_matrix_info(const wamgpu_ctx* ctx, uint64_t* rows, uint64_t* cols, uint64_t* nnz, uint64_t* r0,
+                       uint64_t* r1) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (rows) *rows = ctx->M;
+        if (cols) *cols = ctx->N;
+        if (nnz) *nnz = ctx->nnz;
+        if (r0) *r0 = ctx->row0;
+        if (r1) *r1 = ctx->row1;
+    })
+}
+
+int wamgpu_get_matrix_csr(const wamgpu_ctx* ctx, uint64_t* rp, uint32_t* ci, float* val) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        Ctx* c = const_cast<wamgpu_ctx*>(ctx);
+        need_matrix(c);
+        std::vector<uint2> e(std::max<uint64_t>(c->nnz, 1));
+        if (rp) CK(cudaMemcpyAsync(rp, c->rp.p, (c->Ml + 1) * 8, cudaMemcpyDeviceToHost, c->st));
+        if (c->nnz) CK(cudaMemcpyAsync(e.data(), c->A.p, c->nnz * 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        for (uint64_t k = 0; k < c->nnz; ++k) {
+            if (ci) ci[k] = e[k].x;
+            if (val) std::memcpy(val + k, &e[k].y, 4);
+        }
+    })
+}
+
+int wamgpu_get_matrix_csc(const wamgpu_ctx* ctx, uint64_t* cp, uint32_t* ri, float* val) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        Ctx* c = const_cast<wamgpu_ctx*>(ctx);
+        need_matrix(c);
+        std::vector<uint2> e(std::max<uint64_t>(c->nnz, 1));
+        if (cp) CK(cudaMemcpyAsync(cp, c->cp.p, (c->N + 1) * 8, cudaMemcpyDeviceToHost, c->st));
+        if (c->nnz) CK(cudaMemcpyAsync(e.data(), c->C.p, c->nnz * 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        for (uint64_t k = 0; k < c->nnz; ++k) {
+            if (ri) ri[k] = e[k].x;
+            if (val) std::memcpy(val + k, &e[k].y, 4);
+        }
+    })
+}
+
+int wamgpu_forward_project(wamgpu_ctx* ctx, const double* mu, double* l) {
+    API_TRY(ctx, {
+        NEED(ctx); NEED(mu); NEED(l);
+        need_matrix(ctx);
+        Ctx* c = ctx;
+        c->fscratch.ensure(c->N);
+        c->dscratch.ensure(std::max<uint64_t>(c->Ml, 1));
+        std::vector<float> m(c->N);
+        for (uint64_t x = 0; x < c->N; ++x) m[x] = (float)mu[x];
+        CK(cudaMemcpyAsync(c->fscratch.p, m.data(), c->N * 4, cudaMemcpyHostToDevice, c->st));
+        k_forward<0><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->fscratch.p, nullptr, nullptr,
+                                                    nullptr, c->dscratch.p, nullptr, c->flag.p);
+        check_launch(c);
+        CK(cudaMemcpyAsync(l, c->dscratch.p, c->Ml * 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        check_flag(c, "forward_project");
+    })
+}
+
+int wamgpu_back_project(wamgpu_ctx* ctx, const double* w, double* out) {
+    API_TRY(ctx, {
+        NEED(ctx); NEED(w); NEED(out);
+        need_matrix(ctx);
+        Ctx* c = ctx;
+        c->fscratch.ensure(std::max<uint64_t>(c->Ml, 1));
+        c->dscratch.ensure(c->N);
+        std::vector<float> m(std::max<uint64_t>(c->Ml, 1));
+        for (uint64_t y = 0; y < c->Ml; ++y) m[y] = (float)w[y];
+        CK(cudaMemcpyAsync(c->fscratch.p, m.data(), c->Ml * 4, cudaMemcpyHostToDevice, c->st));
+        back_into(c, c->fscratch.p, c->dscratch.p);
+        allreduce_sum(c, c->dscratch.p, c->N);
+        CK(cudaMemcpyAsync(out, c->dscratch.p, c->N * 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    })
+}
+
+int wamgpu_set_data(wamgpu_ctx* ctx, const double* d, const double* I0) {
+    API_TRY(ctx, {
+        NEED(ctx); NEED(d); NEED(I0);
+        need_matrix(ctx);
+        Ctx* c = ctx;
+        std::vector<float> fd(std::max<uint64_t>(c->Ml, 1)), fi(std::max<uint64_t>(c->Ml, 1));
+        for (uint64_t y = 0; y < c->Ml; ++y) {
+            const double dv = d[c->row0 + y], iv = I0[c->row0 + y];
+            if (!(dv >= 0.0)) throw ContractError("TransmissionData: d must be >= 0");
+            if (!(iv > 0.0)) throw ContractError("TransmissionData: I0 must be > 0");
+            fd[y] = (float)dv;
+            fi[y] = (float)iv;
+        }
+        c->d.alloc(std::max<uint64_t>(c->Ml, 1));
+        c->I0.alloc(std::max<uint64_t>(c->Ml, 1));
+        c->q.alloc(std::max<uint64_t>(c->Ml, 1));
+        CK(cudaMemcpyAsync(c->d.p, fd.data(), c->Ml * 4, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(c->I0.p, fi.data(), c->Ml * 4, cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        c->have_data = true;
+        c->algo = 0;
+    })
+}
+
+int wamgpu_am_init(wamgpu_ctx* ctx, const double* init_mu) {
+    API_TRY(ctx, { NEED(ctx); begin_call(ctx); am_init(ctx, init_mu); end_call(ctx); })
+}
+
+int wamgpu_am_iterate(wamgpu_ctx* ctx, int n, wamgpu_record* recs) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (n < 0) throw ContractError("iterate: n < 0");
+        begin_call(ctx);
+        am_iterate(ctx, n, recs);
+        end_call(ctx);
+    })
+}
+
+int wamgpu_wam_init(wamgpu_ctx* ctx, int L, const double* init_beta) {
+    API_TRY(ctx, { NEED(ctx); begin_call(ctx); wam_init(ctx, L, init_beta); end_call(ctx); })
+}
+
+int wamgpu_wam_iterate(wamgpu_ctx* ctx, int n, wamgpu_record* recs) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (n < 0) throw ContractError("iterate: n < 0");
+        begin_call(ctx);
+        wam_iterate(ctx, n, recs);
+        end_call(ctx);
+    })
+}
+
+int wamgpu_wam_expand(wamgpu_ctx* ctx, double factor, int64_t* newly) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        begin_call(ctx);
+        int64_t n = wam_expand(ctx, factor);
+        end_call(ctx);
+        if (newly) *newly = n;
+    })
+}
+
+int wamgpu_wam_run(wamgpu_ctx* ctx, int iters, const int* sched, int nsched, double factor, wamgpu_record* recs) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (iters < 0 || nsched < 0 || (nsched && !sched)) throw ContractError("run: bad schedule");
+        for (int k = 1; k < nsched; ++k)
+            if (sched[k] < sched[k - 1]) throw ContractError("run: schedule must be sorted");
+        begin_call(ctx);
+        wam_run(ctx, iters, sched, nsched, factor, recs);
+        end_call(ctx);
+    })
+}
+
+int wamgpu_get_image(const wamgpu_ctx* ctx, double* mu) {
+    API_TRY(ctx, {
+        NEED(ctx); NEED(mu);
+        Ctx* c = const_cast<wamgpu_ctx*>(ctx);
+        if (!c->algo) throw ContractError("get_image: no solver state");
+        std::vector<float> m(c->N);
+        CK(cudaMemcpyAsync(m.data(), c->mu.p, c->N * 4, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        for (uint64_t x = 0; x < c->N; ++x) mu[x] = m[x];
+    })
+}
+
+int wamgpu_get_beta(const wamgpu_ctx* ctx, double* beta) {
+    API_TRY(ctx, {
+        NEED(ctx); NEED(beta);
+        Ctx* c = const_cast<wamgpu_ctx*>(ctx);
+        if (c->algo != 2) throw ContractError("get_beta: no wavelet-AM state");
+        std::vector<float> m(c->N);
+        CK(cudaMemcpyAsync(m.data(), c->beta.p, c->N * 4, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        for (uint64_t x = 0; x < c->N; ++x) beta[x] = m[x];
+    })
+}
+
+int wamgpu_get_q(const wamgpu_ctx* ctx, double* q) {
+    API_TRY(ctx, {
+        NEED(ctx); NEED(q);
+        Ctx* c = const_cast<wamgpu_ctx*>(ctx);
+        need_data(c);
+        std::vector<float> m(std::max<uint64_t>(c->Ml, 1));
+        CK(cudaMemcpyAsync(m.data(), c->q.p, c->Ml * 4, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        for (uint64_t y = 0; y < c->Ml; ++y) q[y] = m[y];
+    })
+}
+
+int wamgpu_get_tree(const wamgpu_ctx* ctx, uint8_t* bits, uint64_t* nbytes) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (bits) std::copy(ctx->act_host.begin(), ctx->act_host.end(), bits);
+        if (nbytes) *nbytes = ctx->act_host.size();
+    })
+}
+
+int wamgpu_get_stats(const wamgpu_ctx* ctx, double* b, double* bp, double* bm) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        Ctx* c = const_cast<wamgpu_ctx*>(ctx);
+        if (c->algo != 2) throw ContractError("get_stats: no wavelet-AM state");
+        if (b) CK(cudaMemcpyAsync(b, c->bdata.p, c->N * 8, cudaMemcpyDeviceToHost, c->st));
+        if (bp) CK(cudaMemcpyAsync(bp, c->bp_dbg.p, c->N * 8, cudaMemcpyDeviceToHost, c->st));
+        if (bm) CK(cudaMemcpyAsync(bm, c->bm_dbg.p, c->N * 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    })
+}
+
+int wamgpu_get_scalars(const wamgpu_ctx* ctx, double* Z0, int64_t* cum, int64_t* degen, int64_t* active) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        Ctx* c = const_cast<wamgpu_ctx*>(ctx);
+        unsigned long long cnt[2] = {0, 0};
+        CK(cudaMemcpyAsync(cnt, c->counters.p, 16, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        if (Z0) *Z0 = c->Z0;
+        if (cum) *cum = c->algo == 1 ? (int64_t)c->N * c->iter : (int64_t)cnt[0];
+        if (degen) *degen = (int64_t)cnt[1];
+        if (active) *active = c->active;
+    })
+}
+
+int wamgpu_get_z_rows(wamgpu_ctx* ctx, double* zrow) {
+    API_TRY(ctx, {
+        NEED(ctx); NEED(zrow);
+        Ctx* c = ctx;
+        need_matrix(c);
+        if (c->algo == 2) compute_z0(c, c->L); else compute_z0(c, 0);
+        CK(cudaMemcpyAsync(zrow, c->zrow.p, c->Ml * 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    })
+}
+
+int wamgpu_get_timing(const wamgpu_ctx* ctx, wamgpu_timing* t) {
+    API_TRY(ctx, { NEED(ctx); NEED(t); *t = ctx->tm; })
+}
+
+int wamgpu_set_kernel_timing(wamgpu_ctx* ctx, int on) {
+    API_TRY(ctx, { NEED(ctx); ctx->ktime = on != 0; })
+}
+
+int wamgpu_rasterize(const wamgpu_geometry* g, const wamgpu_primitive* prims, int n, double bg, double* mu) {
+    const wamgpu_ctx* none = nullptr;
+    API_TRY(none, { NEED(g); NEED(mu); if (n && !prims) throw ContractError("null prims"); rasterize(*g, prims, n, bg, mu); })
+}
+
+int wamgpu_simulate(const wamgpu_geometry* g, const double* mu, const double* I0, uint64_t seed, int noisy,
+                    int threads, double* d) {
+    const wamgpu_ctx* none = nullptr;
+    API_TRY(none, { NEED(g); NEED(mu); NEED(I0); NEED(d); simulate(*g, mu, I0, seed, noisy != 0, threads, d); })
+}
+
+int wamgpu_host_rays(const wamgpu_geometry* g, double* rays6) {
+    const wamgpu_ctx* none = nullptr;
+    API_TRY(none, {
+        NEED(g); NEED(rays6);
+        auto r = ray_table(*g);
+        std::memcpy(rays6, r.data(), r.size() * sizeof(RayD));
+    })
+}
+
+}  // extern "C"

@@ -1,0 +1,214 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs.
+
+Bars (north_star, pin P7):
+  * system matrix: bit-exact (structure and fp32-rounded values) vs the oracle,
+    which is itself bit-exact vs the reference headers (test_oracle_ref.py);
+  * Z0 and the active tree: bit-exact vs the fp32-mirror oracle at every
+    expansion;
+  * mu and the I-divergence trajectory: within 1e-4 relative L2 of the f64
+    (reference-precision) oracle; within 1e-6 of the fp32-mirror oracle.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from wam_testutil import problem_inputs, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL_F64 = 1e-4      # north_star tolerance vs the reference-precision oracle
+TOL_MIRROR = 1e-6   # vs the oracle run at the GPU's storage precision
+
+
+def _ctx(W, orc_problem, cfg):
+    from paper_1508_04458_b200 import configs
+    c = W.Context(0)
+    c.set_geometry(configs.geometry(cfg, W.Geometry))
+    return c
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "small_lug", "cfg1"])
+def test_device_matrix_bit_exact(wam, orc, name):
+    cfg, p, _, _, _ = problem_inputs(name, orc, wam)
+    c = _ctx(wam, p, cfg)
+    assert (c.M, c.N, c.nnz) == (p.M, p.N, p.nnz)
+    rp, ci, v = c.matrix_csr()
+    orp, oci, ov = p.csr()
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    assert np.array_equal(v, ov.astype(np.float32))
+    cp, ri, cv = c.matrix_csc()
+    ocp, ori, ocv = p.csc()
+    assert np.array_equal(cp, ocp) and np.array_equal(ri, ori)
+    assert np.array_equal(cv, ocv.astype(np.float32))
+
+
+@pytest.mark.parametrize("beam", [0, 1])
+def test_device_matrix_reference_beams(wam, orc, beam):
+    g = (wam.make_parallel_geometry(24, 16, 1, 0.7, 30, 40, 0.61) if beam == 0 else
+         wam.make_fan_geometry(64, 64, 1, 0.5, 60, 96, 0.71, 500.0, 1000.0))
+    og = orc.make_geometry(g.nx, g.ny, 1, g.voxel_size, g.views, g.detectors, spacing=g.detector_spacing,
+                           beam=beam, sod=g.source_to_center, sdd=g.source_to_detector)
+    p = orc.Problem(og)
+    c = wam.Context(0)
+    c.set_geometry(g)
+    rp, ci, v = c.matrix_csr()
+    orp, oci, ov = p.csr()
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci) and np.array_equal(v, ov.astype(np.float32))
+
+
+def test_spec_hand_examples_through_abi(wam):
+    c = wam.Context(0)
+    c.set_matrix_csr([0, 1, 3], [0, 0, 1], [1.0, 1.0, 1.0], cols=2)
+    assert np.allclose(c.forward_project([0.5, 0.2]), [0.5, 0.7], atol=1e-7)
+    assert np.array_equal(c.back_project([1.0, 2.0]), [3.0, 2.0])
+    assert np.array_equal(c.forward_project([0.0, 0.0]), [0.0, 0.0])
+    assert np.array_equal(c.back_project([0.0, 0.0]), [0.0, 0.0])
+
+
+def test_am_scalar_example_through_abi(wam):
+    c = wam.Context(0)
+    c.set_matrix_csr([0, 1], [0], [1.0], cols=1)
+    c.set_data([5.0], [10.0])
+    c.am_init()
+    rec = c.am_iterate(1)
+    assert abs(c.image()[0] - math.log(2.0)) < 1e-7
+    assert abs(rec[0]["objective"]) < 1e-5
+    assert c.scalars()["Z0"] == 1.0
+
+
+@pytest.mark.parametrize("name", ["small", "cfg1"])
+def test_forward_back_vs_mirror_oracle(wam, orc, name):
+    cfg, p, mu_true, I0, d = problem_inputs(name, orc, wam, mirror=True)
+    c = _ctx(wam, p, cfg)
+    mu32 = mu_true.astype(np.float32).astype(np.float64)
+    l_gpu = c.forward_project(mu_true)
+    l_orc = p.forward_project(mu32)
+    assert rel_l2(l_gpu, l_orc) < 1e-14
+    w = (I0 * np.exp(-l_orc)).astype(np.float32).astype(np.float64)
+    b_gpu = c.back_project(w)
+    b_orc = p.back_project(w)
+    assert rel_l2(b_gpu, b_orc) < 1e-14
+    # adjoint identity of the device operator (fp32 h, fp64 accumulation)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(p.N).astype(np.float32).astype(np.float64)
+    y = rng.standard_normal(p.M).astype(np.float32).astype(np.float64)
+    Hx, Hty = c.forward_project(x), c.back_project(y)
+    assert abs(Hx @ y - x @ Hty) <= 1e-12 * np.linalg.norm(Hx) * np.linalg.norm(y)
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "cfg1"])
+def test_am_parity(wam, orc, name):
+    cfg, p64, _, I0, d = problem_inputs(name, orc, wam)
+    p32 = orc.Problem(p64.geom, mirror=True)
+    J = cfg["J"]
+    c = _ctx(wam, p64, cfg)
+    c.set_data(d, I0)
+    c.am_init()
+    p64.am_init(d, I0)
+    p32.am_init(d, I0)
+    assert c.scalars()["Z0"] == p32.am_get()["Z0"]          # sequential row sums, same fp32 h
+    g = c.am_iterate(J)
+    r64 = p64.am_iterate(J)
+    r32 = p32.am_iterate(J)
+    og = np.array([r["objective"] for r in g])
+    assert rel_l2(og, [r[1] for r in r64]) < TOL_F64
+    assert rel_l2(og, [r[1] for r in r32]) < TOL_MIRROR
+    assert rel_l2(c.image(), p64.am_get()["mu"]) < TOL_F64
+    assert rel_l2(c.image(), p32.am_get()["mu"]) < TOL_MIRROR
+    for a, b in zip(og, og[1:]):
+        assert b <= a * (1 + 1e-6)
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "small_lug", "cfg1"])
+def test_wam_parity_tree_bit_exact(wam, orc, name):
+    cfg, p64, _, I0, d = problem_inputs(name, orc, wam)
+    p32 = orc.Problem(p64.geom, mirror=True)
+    L, J, sched = cfg["L"], cfg["J"], cfg["schedule"]
+    c = _ctx(wam, p64, cfg)
+    c.set_data(d, I0)
+    c.wam_init(L)
+    p64.wam_init(d, I0, L)
+    p32.wam_init(d, I0, L)
+    assert c.scalars()["Z0"] == p32.wam_get()["Z0"]
+    b_gpu, _, _ = c.stats()
+    b32, _, _ = p32.wam_stats()
+    assert rel_l2(b_gpu, b32) < 1e-12
+    obj_g, obj64, obj32 = [], [], []
+    done = 0
+    for ev in sched + [J]:
+        n = ev - done
+        obj_g += [r["objective"] for r in c.wam_iterate(n)]
+        obj64 += [r[1] for r in p64.wam_iterate(n)]
+        obj32 += [r[1] for r in p32.wam_iterate(n)]
+        done = ev
+        if ev == J:
+            break
+        n_g = c.wam_expand(0.1)
+        n_32 = p32.wam_expand(0.1)
+        p64.wam_expand(0.1)
+        assert n_g == n_32
+        t_g, t32, t64 = c.tree(), p32.wam_tree(), p64.wam_tree()
+        assert np.array_equal(t_g, t32), f"tree differs from mirror oracle after iteration {ev}"
+        assert np.array_equal(t_g, t64), f"tree differs from f64 oracle after iteration {ev}"
+        assert c.scalars()["Z0"] == p32.wam_get()["Z0"]
+        assert abs(c.scalars()["Z0"] - p64.wam_get()["Z0"]) <= 1e-6 * p64.wam_get()["Z0"]
+    assert rel_l2(obj_g, obj64) < TOL_F64
+    assert rel_l2(obj_g, obj32) < TOL_MIRROR
+    assert rel_l2(c.image(), p64.wam_get()["mu"]) < TOL_F64
+    assert rel_l2(c.image(), p32.wam_get()["mu"]) < TOL_MIRROR
+    assert rel_l2(c.beta(), p64.wam_get()["beta"]) < TOL_F64
+    s = c.scalars()
+    cnt = p32.wam_counters()
+    assert s["active_set"] == cnt["active_set"]
+    assert s["cum_updates"] == cnt["cum_updates"]
+    assert s["degenerate"] == cnt["degenerate"]
+    _, bp_g, bm_g = c.stats()
+    _, bp32, bm32 = p32.wam_stats()
+    assert rel_l2(bm_g, bm32) < TOL_MIRROR
+    assert rel_l2(bp_g, bp32) < TOL_MIRROR
+
+
+def test_wam_run_matches_stepwise(wam, orc):
+    cfg, p, _, I0, d = problem_inputs("small", orc, wam)
+    a = _ctx(wam, p, cfg)
+    a.set_data(d, I0)
+    a.wam_init(cfg["L"])
+    ra = a.wam_run(cfg["J"], cfg["schedule"], 0.1)
+    p.wam_init(d, I0, cfg["L"])
+    ro = p.wam_run(cfg["J"], cfg["schedule"], 0.1)
+    assert [r["active_set"] for r in ra] == [r[3] for r in ro]
+    assert rel_l2([r["objective"] for r in ra], [r[1] for r in ro]) < TOL_F64
+    el = [r["elapsed_s"] for r in ra]
+    assert all(b >= a_ for a_, b in zip(el, el[1:]))
+
+
+def test_z_rows_match_oracle(wam, orc):
+    cfg, p, _, I0, d = problem_inputs("small", orc, wam, mirror=True)
+    c = _ctx(wam, p, cfg)
+    c.set_data(d, I0)
+    c.wam_init(cfg["L"])
+    p.wam_init(d, I0, cfg["L"])
+    c.wam_iterate(4)
+    p.wam_iterate(4)
+    c.wam_expand(0.1)
+    p.wam_expand(0.1)
+    assert np.array_equal(c.z_rows(), p.wam_z0_rows())
+
+
+def test_error_mapping(wam):
+    c = wam.Context(0)
+    with pytest.raises(wam.ConfigError):
+        c.set_geometry(wam.make_fan_geometry(2, 2, 1, 1.0, 10, 10, 1.0, 500.0, 1000.0))
+    with pytest.raises(wam.ContractError):
+        c.set_data(np.ones(10), np.ones(10))
+    with pytest.raises(wam.ContractError):
+        c.am_iterate(1)
+    g = wam.make_arc_geometry(24, 24, 1, 1.0, 20, 32)
+    c.set_geometry(g)
+    c.set_data(np.ones(c.M), np.ones(c.M))
+    with pytest.raises(wam.ConfigError):
+        c.wam_init(4)                      # 24 not divisible by 16
+    with pytest.raises(wam.ContractError):
+        c.set_data(-np.ones(c.M), np.ones(c.M))
