@@ -149,6 +149,30 @@ __device__ __forceinline__ double idiv_term(double d, double q) {
     return (d > 0.0 ? d * log(d / q) : 0.0) - d + q;
 }
 
+// Warp-cooperative sparse dot product sum_k h_k x[idx_k] over entries [lo, hi):
+// rounds of UNROLL predicated 8-byte streaming loads per lane (all issued
+// before their gathers, so a row costs ~2 dependent memory latencies per
+// round), fp64 accumulation, fixed xor-butterfly reduction (deterministic).
+constexpr int UNROLL = 8;
+__device__ __forceinline__ double row_dot(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
+                                          uint64_t hi, int lane) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (uint64_t base = lo + lane; base < hi; base += 32 * UNROLL) {
+        uint2 e[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            const uint64_t k = base + 32 * u;
+            e[u] = (k < hi) ? ld_stream(A + k) : make_uint2(0u, 0u);
+        }
+        float v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(x + e[u].x);
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) acc[u & 3] = fma(hval(e[u]), (double)v[u], acc[u & 3]);
+    }
+    return warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+}
+
 // ------------------------------------------------------------ CSR forward
 // Warp per ray.  MODE 0: l = H mu written as fp64 (forward_project).
 // MODE 1: fused Beer's law + I-divergence: q = fp32(I0 exp(-l)), per-block fp64
@@ -162,23 +186,15 @@ __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     double tacc = 0.0;
-    for (uint64_t y = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; y < M; y += W) {
-        const uint64_t lo = rp[y], hi = rp[y + 1];
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        uint64_t k = lo + lane;
-        for (; k + 96 < hi; k += 128) {
-            const uint2 e0 = ld_stream(A + k), e1 = ld_stream(A + k + 32);
-            const uint2 e2 = ld_stream(A + k + 64), e3 = ld_stream(A + k + 96);
-            a0 = fma(hval(e0), (double)__ldg(mu + e0.x), a0);
-            a1 = fma(hval(e1), (double)__ldg(mu + e1.x), a1);
-            a2 = fma(hval(e2), (double)__ldg(mu + e2.x), a2);
-            a3 = fma(hval(e3), (double)__ldg(mu + e3.x), a3);
-        }
-        for (; k < hi; k += 32) {
-            const uint2 e0 = ld_stream(A + k);
-            a0 = fma(hval(e0), (double)__ldg(mu + e0.x), a0);
-        }
-        const double l = warp_sum((a0 + a1) + (a2 + a3));
+    uint64_t y = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+    uint64_t lo = 0, hi = 0;
+    if (y < M) { lo = rp[y]; hi = rp[y + 1]; }
+    for (; y < M; y += W) {
+        // prefetch the next row's extent while this row streams
+        const uint64_t yn = y + W;
+        uint64_t nlo = 0, nhi = 0;
+        if (yn < M) { nlo = __ldg(rp + yn); nhi = __ldg(rp + yn + 1); }
+        const double l = row_dot(A, mu, lo, hi, lane);
         if (lane == 0) {
             if (!isfinite(l)) atomicOr(flag, 1);
             if (MODE == 0) {
@@ -189,6 +205,7 @@ __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long
                 tacc += idiv_term((double)d[y], qq);
             }
         }
+        lo = nlo; hi = nhi;
     }
     if (MODE == 1) {
         __shared__ double s[32];
@@ -214,22 +231,7 @@ __global__ void __launch_bounds__(256) k_back(uint64_t N, const unsigned long lo
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t x = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; x < N; x += W) {
-        const uint64_t lo = cp[x], hi = cp[x + 1];
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        uint64_t k = lo + lane;
-        for (; k + 96 < hi; k += 128) {
-            const uint2 e0 = ld_stream(C + k), e1 = ld_stream(C + k + 32);
-            const uint2 e2 = ld_stream(C + k + 64), e3 = ld_stream(C + k + 96);
-            a0 = fma(hval(e0), (double)__ldg(w + e0.x), a0);
-            a1 = fma(hval(e1), (double)__ldg(w + e1.x), a1);
-            a2 = fma(hval(e2), (double)__ldg(w + e2.x), a2);
-            a3 = fma(hval(e3), (double)__ldg(w + e3.x), a3);
-        }
-        for (; k < hi; k += 32) {
-            const uint2 e0 = ld_stream(C + k);
-            a0 = fma(hval(e0), (double)__ldg(w + e0.x), a0);
-        }
-        const double c = warp_sum((a0 + a1) + (a2 + a3));
+        const double c = row_dot(C, w, cp[x], cp[x + 1], lane);
         if (lane == 0) {
             if (MODE == 0) {
                 g[x] = c;
@@ -422,10 +424,13 @@ __global__ void k_tile(int mode, int nx, int ny, int L, const double* __restrict
     for (int i = threadIdx.x; i < T2; i += blockDim.x) {
         CoefInfo ci = coef_info(i / TS, i % TS, ti, tj, L, nx, ny, act, off);
         float bo = beta[ci.z];
+        if (mode == 1) {
+            const double bmv0 = ci.approx ? 0.0 : bm[ci.z];
+            if (bp_out) { bp_out[ci.z] = x[i] - bmv0; bm_out[ci.z] = bmv0; }
+        }
         if (mode == 1 && ci.active) {
             const double bmv = ci.approx ? 0.0 : bm[ci.z];
             const double bpv = x[i] - bmv;
-            if (bp_out) { bp_out[ci.z] = bpv; bm_out[ci.z] = bmv; }
             double nb;
             const int r = solve_update(bdata[ci.z], bpv, bmv, Z0, (double)bo, &nb);
             if (r == 0) {
@@ -476,26 +481,51 @@ __global__ void k_mark(int nx, int ny, int L, const double* __restrict__ s, doub
 }
 
 // Per-ray walk over the CSR row producing phi(y|z) of every crossed block at
-// every level (cells of a ray inside a block are contiguous in Siddon order).
-// MODE 0: Z(y) = sum_{z active} |phi(y|z)|  (Eq. 1.61; order: totA + tot_L..tot_1)
-// MODE 1: count negative fp32 phi of active detail coefficients
-// MODE 2: emit them (key = Mallat z, value = {ray, f32 bits}) at pos[y]
+// every level (cells of a ray inside a block are contiguous in Siddon order,
+// so a block is complete when the ray leaves it).  One THREAD per ray keeps
+// the sequential, reference-order summation of every phi (bit-identical to the
+// oracle); the warp stages its 32 rays' rows through shared memory 32 entries
+// at a time with cp.async (coalesced 256-byte rows, zero-filled tails), so the
+// walk streams the CSR at HBM speed instead of 32 scattered 8-byte loads.
+// MODE 0: Z(y) = sum_{z active} |phi(y|z)| (Eq. 1.61; order totA + tot_L..tot_1)
+//         and cnt[y] = number of negative fp32 phi of active detail coefficients
+// MODE 2: emit those entries (key = Mallat z, value = {ray, f32 bits}) at pos[y]
+constexpr int WALK_WARPS = 4;
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(128) k_walk(uint64_t M, const unsigned long long* __restrict__ rp,
-                                              const uint2* __restrict__ A, int nx, int ny, int L,
-                                              const uint8_t* __restrict__ act, ActOff off,
-                                              double* __restrict__ zrow, unsigned long long* __restrict__ cnt,
-                                              const unsigned long long* __restrict__ pos,
-                                              unsigned* __restrict__ keys, uint2* __restrict__ vals) {
-    const uint64_t y = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (y > M) return;
-    if (y == M) { if (MODE == 1) cnt[M] = 0; return; }
+__global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsigned long long* __restrict__ rp,
+                                                          const uint2* __restrict__ A, int nx, int ny, int L,
+                                                          const uint8_t* __restrict__ act, ActOff off,
+                                                          double* __restrict__ zrow,
+                                                          unsigned long long* __restrict__ cnt,
+                                                          const unsigned long long* __restrict__ pos,
+                                                          unsigned* __restrict__ keys, uint2* __restrict__ vals) {
+    __shared__ uint2 buf[WALK_WARPS][32][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t y = ((uint64_t)blockIdx.x * WALK_WARPS + w) * 32 + lane;
+    if (MODE == 0 && y == M) cnt[M] = 0;
+    uint64_t lo = 0, hi = 0;
+    if (y < M) { lo = rp[y]; hi = rp[y + 1]; }
+    const unsigned long long len = hi - lo;
+    unsigned long long maxlen = len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    if (maxlen == 0 && y >= M) return;
+
     int cur[LMAX + 1], cbi[LMAX + 1], cbj[LMAX + 1];
     double sH[LMAX + 1], sV[LMAX + 1], sD[LMAX + 1], tot[LMAX + 1];
 #pragma unroll
     for (int l = 0; l <= LMAX; ++l) { cur[l] = -1; cbi[l] = cbj[l] = 0; sH[l] = sV[l] = sD[l] = tot[l] = 0.0; }
     double sA = 0.0, totA = 0.0;
-    unsigned long long count = 0, wp = (MODE == 2) ? pos[y] : 0;
+    unsigned long long count = 0, wp = (MODE == 2 && y < M) ? pos[y] : 0;
 
     auto flush = [&](int l) {
         const double sc = 1.0 / (double)(1 << l);
@@ -504,43 +534,53 @@ __global__ void __launch_bounds__(128) k_walk(uint64_t M, const unsigned long lo
         sH[l] = sV[l] = sD[l] = 0.0;
         const int wl = nx >> l, hl = ny >> l;
         if (!act[off.off[l] + (uint64_t)cbi[l] * wl + cbj[l]]) return;
-        if (MODE == 0) {
-            tot[l] += fabs(pH) + fabs(pV) + fabs(pD);
-        } else {
-            const float v[3] = {(float)pH, (float)pV, (float)pD};
-            const unsigned z[3] = {(unsigned)((hl + cbi[l]) * nx + cbj[l]), (unsigned)(cbi[l] * nx + wl + cbj[l]),
-                                   (unsigned)((hl + cbi[l]) * nx + wl + cbj[l])};
+        if (MODE == 0) tot[l] += fabs(pH) + fabs(pV) + fabs(pD);
+        const float v[3] = {(float)pH, (float)pV, (float)pD};
+        const unsigned z[3] = {(unsigned)((hl + cbi[l]) * nx + cbj[l]), (unsigned)(cbi[l] * nx + wl + cbj[l]),
+                               (unsigned)((hl + cbi[l]) * nx + wl + cbj[l])};
 #pragma unroll
-            for (int s = 0; s < 3; ++s)
-                if (v[s] < 0.0f) {
-                    if (MODE == 1) ++count;
-                    else { keys[wp] = z[s]; vals[wp] = make_uint2((unsigned)y, __float_as_uint(v[s])); ++wp; }
-                }
-        }
+        for (int s = 0; s < 3; ++s)
+            if (v[s] < 0.0f) {
+                if (MODE == 0) ++count;
+                else { keys[wp] = z[s]; vals[wp] = make_uint2((unsigned)y, __float_as_uint(v[s])); ++wp; }
+            }
     };
 
-    const uint64_t lo = rp[y], hi = rp[y + 1];
-    for (uint64_t k = lo; k < hi; ++k) {
-        const uint2 e = A[k];
-        const double h = hval(e);
-        if (L == 0) { if (MODE == 0) totA += fabs(h); continue; }
-        const int iy = (int)(e.x / (unsigned)nx), ix = (int)(e.x % (unsigned)nx);
-#pragma unroll
-        for (int l = 1; l <= LMAX; ++l) {
-            if (l > L) break;
-            const int bi = iy >> l, bj = ix >> l;
-            const int key = bi * (nx >> l) + bj;
-            if (key != cur[l]) {
-                if (cur[l] >= 0) flush(l);
-                cur[l] = key; cbi[l] = bi; cbj[l] = bj;
-            }
-            const bool top = ((iy >> (l - 1)) & 1) == 0, left = ((ix >> (l - 1)) & 1) == 0;
-            sH[l] += top ? h : -h;
-            sV[l] += left ? h : -h;
-            sD[l] += (top == left) ? h : -h;
-            if (l == L) sA += h;
+    for (unsigned long long base = 0; base < maxlen; base += 32) {
+        // stage entries [base, base+32) of each of the warp's 32 rays
+        for (int j = 0; j < 32; ++j) {
+            const unsigned long long lj = __shfl_sync(0xffffffffu, lo, j);
+            const unsigned long long nj = __shfl_sync(0xffffffffu, len, j);
+            const bool ok = base + lane < nj;
+            cp_async8(&buf[w][j][lane], A + (ok ? lj + base + lane : 0), ok);
         }
+        cp_async_wait_all();
+        __syncwarp();
+        const int n = (int)min(32ull, len > base ? len - base : 0ull);
+        for (int i = 0; i < n; ++i) {
+            const uint2 e = buf[w][lane][i];
+            const double h = hval(e);
+            if (L == 0) { if (MODE == 0) totA += fabs(h); continue; }
+            const int iy = (int)(e.x / (unsigned)nx), ix = (int)(e.x % (unsigned)nx);
+#pragma unroll
+            for (int l = 1; l <= LMAX; ++l) {
+                if (l > L) break;
+                const int bi = iy >> l, bj = ix >> l;
+                const int key = bi * (nx >> l) + bj;
+                if (key != cur[l]) {
+                    if (cur[l] >= 0) flush(l);
+                    cur[l] = key; cbi[l] = bi; cbj[l] = bj;
+                }
+                const bool top = ((iy >> (l - 1)) & 1) == 0, left = ((ix >> (l - 1)) & 1) == 0;
+                sH[l] += top ? h : -h;
+                sV[l] += left ? h : -h;
+                sD[l] += (top == left) ? h : -h;
+                if (l == L) sA += h;
+            }
+        }
+        __syncwarp();
     }
+    if (y >= M) return;
 #pragma unroll
     for (int l = 1; l <= LMAX; ++l)
         if (l <= L && cur[l] >= 0) flush(l);
@@ -550,7 +590,6 @@ __global__ void __launch_bounds__(128) k_walk(uint64_t M, const unsigned long lo
         for (int l = LMAX; l >= 1; --l)
             if (l <= L) z += tot[l];
         zrow[y] = z;
-    } else if (MODE == 1) {
         cnt[y] = count;
     }
 }

@@ -87,6 +87,10 @@ struct wamgpu_ctx {
     int algo = 0;  // 1 AM, 2 WAM
     DBuf<float> mu, beta, fscratch;
     DBuf<double> g, bdata, bam, mu64, bp_dbg, bm_dbg, zrow, dscratch;
+    DBuf<unsigned long long> wcnt;      // per-ray Phi^- counts from the Z0 walk (then scanned)
+    DBuf<uint8_t> cub_tmp;
+    DBuf<unsigned> kin_s, kout_s;
+    DBuf<uint2> vin_s;
     int L = 0;
     DBuf<uint8_t> act, act_new;
     ActOff off{};
@@ -150,9 +154,8 @@ static void check_launch(Ctx* c) {
 static void exclusive_scan_u64(Ctx* c, unsigned long long* inout, uint64_t n) {
     size_t tb = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, inout, inout, (int64_t)n, c->st));
-    DBuf<uint8_t> tmp;
-    tmp.alloc(tb + 1);
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, inout, inout, (int64_t)n, c->st));
+    c->cub_tmp.ensure(tb + 1);
+    CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tb, inout, inout, (int64_t)n, c->st));
     launched(c);
 }
 
@@ -165,7 +168,7 @@ static int bits_for(uint64_t n) {
 // stable sort of (key, value) pairs by key; output in keys_out / vals_out
 static void sort_pairs(Ctx* c, DBuf<unsigned>& kin, DBuf<uint2>& vin, DBuf<unsigned>& kout, DBuf<uint2>& vout,
                        uint64_t n, uint64_t maxkey) {
-    kout.alloc(std::max<uint64_t>(n, 1));
+    kout.ensure(std::max<uint64_t>(n, 1));
     vout.alloc(std::max<uint64_t>(n, 1));
     if (n == 0) return;
     const int bits = bits_for(maxkey);
@@ -173,9 +176,8 @@ static void sort_pairs(Ctx* c, DBuf<unsigned>& kin, DBuf<uint2>& vin, DBuf<unsig
     auto vo = reinterpret_cast<unsigned long long*>(vout.p);
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.p, kout.p, vi, vo, (int64_t)n, 0, bits, c->st));
-    DBuf<uint8_t> tmp;
-    tmp.alloc(tb + 1);
-    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, kin.p, kout.p, vi, vo, (int64_t)n, 0, bits, c->st));
+    c->cub_tmp.ensure(tb + 1);
+    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tb, kin.p, kout.p, vi, vo, (int64_t)n, 0, bits, c->st));
     launched(c, 4);
 }
 
@@ -214,6 +216,7 @@ static void finish_matrix(Ctx* c) {
     DBuf<uint2> vin, vout;
     kin.alloc(std::max<uint64_t>(c->nnz, 1));
     vin.alloc(std::max<uint64_t>(c->nnz, 1));
+    c->cub_tmp.release();
     if (c->nnz) {
         k_csr_to_pairs<<<c->sms * 8, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, kin.p, vin.p);
         check_launch(c);
@@ -225,6 +228,8 @@ static void finish_matrix(Ctx* c) {
     k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(kout.p, c->nnz, c->N, c->cp.p);
     check_launch(c);
     c->C.swap(vout);
+    kout.release();
+    c->cub_tmp.release();
     c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->Ml + 7) / 8, (uint64_t)c->sms * 16));
     c->nblk_col = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->N + 7) / 8, (uint64_t)c->sms * 16));
     c->partial.alloc(std::max(c->nblk_row, 1024));
@@ -344,9 +349,10 @@ static double device_max(Ctx* c, const double* v, uint64_t n) {
 // Z0 = max_y sum_{z active} |phi(y|z)| (Eq. 1.61); AM: levels = 0 -> row sums.
 static double compute_z0(Ctx* c, int levels) {
     if (c->Ml) {
-        k_walk<0><<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, levels,
-                                                                  c->act.p, c->off, c->zrow.p, nullptr, nullptr,
-                                                                  nullptr, nullptr);
+        c->wcnt.ensure(c->Ml + 1);
+        k_walk<0><<<blocks_for(c->Ml + 1, 32 * WALK_WARPS), 32 * WALK_WARPS, 0, c->st>>>(
+            c->Ml, c->rp.p, c->A.p, c->nx, c->ny, levels, c->act.p, c->off, c->zrow.p, c->wcnt.p, nullptr, nullptr,
+            nullptr);
         check_launch(c);
     }
     double z0 = device_max(c, c->zrow.p, c->Ml);
@@ -417,9 +423,9 @@ static void fill_records(Ctx* c, int n, wamgpu_record* recs, int64_t active_at_s
 static void am_init(Ctx* c, const double* init_mu) {
     need_matrix(c);
     need_data(c);
-    c->mu.alloc(c->N);
-    c->g.alloc(2 * c->N);
-    c->bam.alloc(c->N);
+    c->mu.ensure(c->N);
+    c->g.ensure(2 * c->N);
+    c->bam.ensure(c->N);
     if (init_mu) {
         std::vector<float> m(c->N);
         for (uint64_t x = 0; x < c->N; ++x) m[x] = (float)init_mu[x];
@@ -508,33 +514,27 @@ static void rebuild_phi(Ctx* c) {
     }
     std::sort(lst.begin(), lst.end());
     c->nlist = lst.size();
-    c->list.alloc(std::max<size_t>(lst.size(), 1));
+    c->list.ensure(std::max<size_t>(lst.size(), 1));
     if (!lst.empty())
         CK(cudaMemcpyAsync(c->list.p, lst.data(), lst.size() * 4, cudaMemcpyHostToDevice, c->st));
-    // Phi^- CSC over local rays: count -> scan -> emit -> stable sort by z
-    DBuf<unsigned long long> pos;
-    pos.alloc(c->Ml + 1);
-    k_walk<1><<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->L, c->act.p,
-                                                              c->off, nullptr, pos.p, nullptr, nullptr, nullptr);
-    check_launch(c);
-    exclusive_scan_u64(c, pos.p, c->Ml + 1);
+    // Phi^- CSC over local rays: counts (from the Z0 walk of this tree) -> scan
+    // -> emit -> stable radix sort by z (rays stay ascending within a column)
+    exclusive_scan_u64(c, c->wcnt.p, c->Ml + 1);
     unsigned long long tot = 0;
-    CK(cudaMemcpyAsync(&tot, pos.p + c->Ml, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&tot, c->wcnt.p + c->Ml, 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
-    DBuf<unsigned> kin, kout;
-    DBuf<uint2> vin;
-    kin.alloc(std::max<uint64_t>(tot, 1));
-    vin.alloc(std::max<uint64_t>(tot, 1));
+    c->kin_s.ensure(std::max<uint64_t>(tot, 1));
+    c->vin_s.ensure(std::max<uint64_t>(tot, 1));
     if (tot) {
-        k_walk<2><<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->L,
-                                                                  c->act.p, c->off, nullptr, nullptr, pos.p, kin.p,
-                                                                  vin.p);
+        k_walk<2><<<blocks_for(c->Ml + 1, 32 * WALK_WARPS), 32 * WALK_WARPS, 0, c->st>>>(
+            c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->L, c->act.p, c->off, nullptr, nullptr, c->wcnt.p, c->kin_s.p,
+            c->vin_s.p);
         check_launch(c);
     }
     DBuf<uint2> vout;
-    sort_pairs(c, kin, vin, kout, vout, tot, c->N);
-    c->np.alloc(c->N + 1);
-    k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(kout.p, tot, c->N, c->np.p);
+    sort_pairs(c, c->kin_s, c->vin_s, c->kout_s, vout, tot, c->N);
+    c->np.ensure(c->N + 1);
+    k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(c->kout_s.p, tot, c->N, c->np.p);
     check_launch(c);
     c->E.swap(vout);
     c->nnz_phi = tot;
@@ -559,8 +559,8 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     if ((c->nx % (1 << L)) || (c->ny % (1 << L))) throw ConfigError("haar: slice dimensions not divisible by 2^L");
     c->L = L;
     const uint64_t N = c->N;
-    c->mu.alloc(N); c->beta.alloc(N); c->g.alloc(2 * N); c->bdata.alloc(N); c->mu64.alloc(N);
-    c->bp_dbg.alloc(N); c->bm_dbg.alloc(N);
+    c->mu.ensure(N); c->beta.ensure(N); c->g.ensure(2 * N); c->bdata.ensure(N); c->mu64.ensure(N);
+    c->bp_dbg.ensure(N); c->bm_dbg.ensure(N);
     CK(cudaMemsetAsync(c->g.p, 0, 2 * N * 8, c->st));
     CK(cudaMemsetAsync(c->bp_dbg.p, 0, N * 8, c->st));
     CK(cudaMemsetAsync(c->bm_dbg.p, 0, N * 8, c->st));
@@ -569,8 +569,8 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     for (int l = 0; l <= LMAX + 1; ++l) c->off.off[l] = 0;
     for (int l = 1; l <= L; ++l) { c->off.off[l] = o; o += (uint64_t)(c->nx >> l) * (c->ny >> l); }
     c->act_bytes = o;
-    c->act.alloc(std::max<uint64_t>(o, 1));
-    c->act_new.alloc(std::max<uint64_t>(o, 1));
+    c->act.ensure(std::max<uint64_t>(o, 1));
+    c->act_new.ensure(std::max<uint64_t>(o, 1));
     CK(cudaMemsetAsync(c->act.p, 0, std::max<uint64_t>(o, 1), c->st));
     c->act_host.assign(o, 0);
     if (init_beta) {
