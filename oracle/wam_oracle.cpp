@@ -453,54 +453,57 @@ static inline BlockIdx mallat(int nx, int ny, int l, int bi, int bj) {
 }
 
 // Per-ray walk producing phi(y|z) = sum_{x in block} h(y|x) w(x|z) for every
-// block the ray crosses, at every level (SPEC.md:239-247 phi_column; the sum is
-// the CSR-order SpMV of the footprint image).  A ray's cells
-// inside a block are contiguous in Siddon order (cells are monotone in ix and
-// iy), so a block is complete when the ray leaves it.  Detail sign pattern at
-// level l: H + on the top half, V + on the left half, D + on TL/BR quadrants;
-// weights 2^-l (approx 2^-L).  cb(level, bi, bj, phiA, phiH, phiV, phiD); phiA
-// is meaningful only for level == L.
+// block the ray crosses, at every level (SPEC.md:239-247 phi_column,
+// PAPER.md:134).  A ray's cells inside a block are contiguous in Siddon order
+// (cells are monotone in ix and iy), so a block is complete when the ray leaves
+// it.  Summation order (fixed here and mirrored bit-for-bit by the GPU walk;
+// SPEC.md:109 allows any deterministic order): hierarchical quadrant sums.  A
+// level-l block keeps the plain sums TL, TR, BL, BR of its four level-(l-1)
+// quadrants (level 1: the four voxels' h, each visited once), and on exit
+//   st = TL+TR, sb = BL+BR, A = st+sb, H = st-sb, V = (TL+BL)-(TR+BR),
+//   D = (TL+BR)-(TR+BL);  phi = 2^-l * (A | H | V | D)   (A only at l == L),
+// then adds A into its parent's quadrant.  Sign patterns: H + on the top half,
+// V + on the left half, D + on TL/BR (Haar analysis of DESIGN.md §3).
+// cb(level, bi, bj, phiA, phiH, phiV, phiD) fires fine-to-coarse in ray order.
 template <typename CB>
 static void phi_walk(const orc_problem* p, int L, uint64_t y, CB&& cb) {
     const int nx = p->g.nx;
-    int curk[24];
-    double sA = 0.0, sH[24], sV[24], sD[24];
-    int cbi[24], cbj[24];
-    for (int l = 0; l <= L; ++l) { curk[l] = -1; sH[l] = sV[l] = sD[l] = 0.0; }
-    auto flush = [&](int l) {
-        if (curk[l] < 0) return;
-        if (l == 0) {  // L == 0: the approx "block" is a single voxel
-            cb(0, cbi[0], cbj[0], sA, 0.0, 0.0, 0.0);
-            sA = 0.0;
-            return;
+    if (L == 0) {  // Omega = I: every voxel is its own approximation block
+        for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) {
+            const int ix = (int)(p->ci[k] % (uint32_t)nx), iy = (int)(p->ci[k] / (uint32_t)nx);
+            cb(0, iy, ix, p->hv[k], 0.0, 0.0, 0.0);
         }
-        double sc = std::ldexp(1.0, -l);
-        double pA = (l == L) ? sA * sc : 0.0;
-        cb(l, cbi[l], cbj[l], pA, sH[l] * sc, sV[l] * sc, sD[l] * sc);
-        sH[l] = sV[l] = sD[l] = 0.0;
-        if (l == L) sA = 0.0;
+        return;
+    }
+    int cur[24], cbi[24], cbj[24];
+    double q[24][4];
+    for (int l = 0; l <= L; ++l) { cur[l] = -1; cbi[l] = cbj[l] = 0; q[l][0] = q[l][1] = q[l][2] = q[l][3] = 0.0; }
+    auto flush = [&](int l) {
+        const double TL = q[l][0], TR = q[l][1], BL = q[l][2], BR = q[l][3];
+        const double st = TL + TR, sb = BL + BR;
+        const double A = st + sb, H = st - sb, V = (TL + BL) - (TR + BR), D = (TL + BR) - (TR + BL);
+        const double sc = std::ldexp(1.0, -l);
+        cb(l, cbi[l], cbj[l], (l == L) ? A * sc : 0.0, H * sc, V * sc, D * sc);
+        if (l < L) q[l + 1][((cbi[l] & 1) << 1) | (cbj[l] & 1)] += A;
+        q[l][0] = q[l][1] = q[l][2] = q[l][3] = 0.0;
     };
     for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) {
         const int ix = (int)(p->ci[k] % (uint32_t)nx), iy = (int)(p->ci[k] / (uint32_t)nx);
-        const double h = p->hv[k];
-        if (L == 0) {
-            int key = iy * nx + ix;
-            if (key != curk[0]) { flush(0); curk[0] = key; cbi[0] = iy; cbj[0] = ix; }
-            sA += h;
-            continue;
-        }
+        int changed = 0;
         for (int l = 1; l <= L; ++l) {
-            const int bi = iy >> l, bj = ix >> l;
-            const int key = bi * (nx >> l) + bj;
-            if (key != curk[l]) { flush(l); curk[l] = key; cbi[l] = bi; cbj[l] = bj; }
-            const bool top = ((iy >> (l - 1)) & 1) == 0, left = ((ix >> (l - 1)) & 1) == 0;
-            sH[l] += top ? h : -h;
-            sV[l] += left ? h : -h;
-            sD[l] += (top == left) ? h : -h;
-            if (l == L) sA += h;
+            const int key = (iy >> l) * (nx >> l) + (ix >> l);
+            if (key == cur[l]) break;
+            if (cur[l] >= 0) flush(l);
+            changed = l;
         }
+        for (int l = 1; l <= changed; ++l) {
+            cbi[l] = iy >> l; cbj[l] = ix >> l;
+            cur[l] = cbi[l] * (nx >> l) + cbj[l];
+        }
+        q[1][((iy & 1) << 1) | (ix & 1)] += p->hv[k];
     }
-    for (int l = (L == 0 ? 0 : 1); l <= L; ++l) flush(l);
+    for (int l = 1; l <= L; ++l)
+        if (cur[l] >= 0) flush(l);
 }
 
 static inline bool is_active(const orc_problem* p, int l, int bi, int bj) {

@@ -149,34 +149,66 @@ __device__ __forceinline__ double idiv_term(double d, double q) {
     return (d > 0.0 ? d * log(d / q) : 0.0) - d + q;
 }
 
-// Warp-cooperative sparse dot product sum_k h_k x[idx_k] over entries [lo, hi):
-// rounds of UNROLL predicated 8-byte streaming loads per lane (all issued
-// before their gathers, so a row costs ~2 dependent memory latencies per
-// round), fp64 accumulation, fixed xor-butterfly reduction (deterministic).
+// Warp-cooperative segmented sparse dot products over a contiguous entry range
+// [lo, hi) holding G consecutive segments (rows or columns) split at b[0..G-2]:
+// out[g] = sum over segment g of h_k x[idx_k].  Software-pipelined: the
+// UNROLL predicated 8-byte streaming loads of round r+1 are issued before the
+// gathers of round r, so a warp keeps ~2*UNROLL*256 B in flight and pays about
+// one memory latency per 256*UNROLL/32 entries, across segment boundaries.
+// fp64 accumulation (products of two fp32 are exact in fp64); segment
+// selection is by predicated fma with h=0 (an exact no-op); fixed
+// xor-butterfly reduction (deterministic).
 constexpr int UNROLL = 8;
-__device__ __forceinline__ double row_dot(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
-                                          uint64_t hi, int lane) {
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (uint64_t base = lo + lane; base < hi; base += 32 * UNROLL) {
-        uint2 e[UNROLL];
+template <int G>
+__device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
+                                        const uint64_t (&b)[G > 1 ? G - 1 : 1], uint64_t hi, int lane,
+                                        double (&out)[G]) {
+    double acc[G][2];
+#pragma unroll
+    for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = 0.0;
+    uint2 ec[UNROLL];
+    uint64_t base = lo + lane;
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+        const uint64_t k = base + 32 * u;
+        ec[u] = (k < hi) ? ld_stream(A + k) : make_uint2(0u, 0u);
+    }
+    for (; base < hi; base += 32 * UNROLL) {
+        uint2 en[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
-            const uint64_t k = base + 32 * u;
-            e[u] = (k < hi) ? ld_stream(A + k) : make_uint2(0u, 0u);
+            const uint64_t k = base + 32 * (UNROLL + u);
+            en[u] = (k < hi) ? ld_stream(A + k) : make_uint2(0u, 0u);
         }
         float v[UNROLL];
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(x + e[u].x);
+        for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(x + ec[u].x);
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) acc[u & 3] = fma(hval(e[u]), (double)v[u], acc[u & 3]);
+        for (int u = 0; u < UNROLL; ++u) {
+            const double h = hval(ec[u]), xv = (double)v[u];
+            if (G == 1) {
+                acc[0][u & 1] = fma(h, xv, acc[0][u & 1]);
+            } else {
+                const uint64_t k = base + 32 * u;
+                int seg = 0;
+#pragma unroll
+                for (int g = 0; g < G - 1; ++g) seg += (k >= b[g]);
+#pragma unroll
+                for (int g = 0; g < G; ++g) acc[g][u & 1] = fma(seg == g ? h : 0.0, xv, acc[g][u & 1]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) ec[u] = en[u];
     }
-    return warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+#pragma unroll
+    for (int g = 0; g < G; ++g) out[g] = warp_sum(acc[g][0] + acc[g][1]);
 }
 
 // ------------------------------------------------------------ CSR forward
 // Warp per ray.  MODE 0: l = H mu written as fp64 (forward_project).
 // MODE 1: fused Beer's law + I-divergence: q = fp32(I0 exp(-l)), per-block fp64
 // partial of the objective (deterministic block order).
+constexpr int FG = 4;  // rows per warp task in the forward kernel
 template <int MODE>
 __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long long* __restrict__ rp,
                                                  const uint2* __restrict__ A, const float* __restrict__ mu,
@@ -185,31 +217,42 @@ __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long
                                                  double* __restrict__ partial, int* __restrict__ flag) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t ntask = (M + FG - 1) / FG;
     double tacc = 0.0;
-    uint64_t y = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
-    uint64_t lo = 0, hi = 0;
-    if (y < M) { lo = rp[y]; hi = rp[y + 1]; }
-    for (; y < M; y += W) {
-        // prefetch the next row's extent while this row streams
-        const uint64_t yn = y + W;
-        uint64_t nlo = 0, nhi = 0;
-        if (yn < M) { nlo = __ldg(rp + yn); nhi = __ldg(rp + yn + 1); }
-        const double l = row_dot(A, mu, lo, hi, lane);
-        if (lane == 0) {
-            if (!isfinite(l)) atomicOr(flag, 1);
+    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; t < ntask; t += W) {
+        const uint64_t y0 = t * FG;
+        const int nr = (int)((M - y0) < (uint64_t)FG ? (M - y0) : (uint64_t)FG);
+        // row extents: lane j < nr+1 loads rp[y0+j]
+        const unsigned long long myrp = (lane <= nr) ? __ldg(rp + y0 + lane) : 0ull;
+        const uint64_t lo = __shfl_sync(0xffffffffu, myrp, 0), hi = __shfl_sync(0xffffffffu, myrp, nr);
+        uint64_t bnd[FG - 1];
+#pragma unroll
+        for (int g = 0; g < FG - 1; ++g) bnd[g] = __shfl_sync(0xffffffffu, myrp, min(g + 1, nr));
+        double l[FG];
+        seg_dot<FG>(A, mu, lo, bnd, hi, lane, l);
+        // lane g finishes row y0+g: Beer's law, I-divergence term
+        double lg = l[0];
+#pragma unroll
+        for (int g = 1; g < FG; ++g) lg = (lane == g) ? l[g] : lg;
+        if (lane < nr) {
+            const uint64_t y = y0 + lane;
+            if (!isfinite(lg)) atomicOr(flag, 1);
             if (MODE == 0) {
-                lout[y] = l;
+                lout[y] = lg;
             } else {
-                const double qq = (double)I0[y] * exp(-l);
+                const double qq = (double)I0[y] * exp(-lg);
                 q[y] = (float)qq;
                 tacc += idiv_term((double)d[y], qq);
             }
         }
-        lo = nlo; hi = nhi;
     }
     if (MODE == 1) {
+        // deterministic block partial: lanes, then warps, in fixed order
         __shared__ double s[32];
-        if (lane == 0) s[wib] = tacc;
+        double v = tacc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s[wib] = v;
         __syncthreads();
         if (threadIdx.x == 0) {
             double t = 0.0;
@@ -231,7 +274,10 @@ __global__ void __launch_bounds__(256) k_back(uint64_t N, const unsigned long lo
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t x = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; x < N; x += W) {
-        const double c = row_dot(C, w, cp[x], cp[x + 1], lane);
+        const uint64_t nob[1] = {0};
+        double cc[1];
+        seg_dot<1>(C, w, cp[x], nob, cp[x + 1], lane, cc);
+        const double c = cc[0];
         if (lane == 0) {
             if (MODE == 0) {
                 g[x] = c;
@@ -482,11 +528,16 @@ __global__ void k_mark(int nx, int ny, int L, const double* __restrict__ s, doub
 
 // Per-ray walk over the CSR row producing phi(y|z) of every crossed block at
 // every level (cells of a ray inside a block are contiguous in Siddon order,
-// so a block is complete when the ray leaves it).  One THREAD per ray keeps
-// the sequential, reference-order summation of every phi (bit-identical to the
-// oracle); the warp stages its 32 rays' rows through shared memory 32 entries
-// at a time with cp.async (coalesced 256-byte rows, zero-filled tails), so the
-// walk streams the CSR at HBM speed instead of 32 scattered 8-byte loads.
+// so a block is complete when the ray leaves it).  Summation order: the
+// hierarchical quadrant sums fixed in DESIGN.md §4 (level-1 quadrants are
+// single voxels; a level-l block combines its four quadrant sums
+// st=TL+TR, sb=BL+BR, A=st+sb, H=st-sb, V=(TL+BL)-(TR+BR), D=(TL+BR)-(TR+BL)
+// and passes A to its parent), so each entry costs one fp64 add and a block
+// exit ~10 flops.  One THREAD per ray keeps that order exactly; the warp stages
+// its 32 rays' rows through shared memory 32 entries at a time with cp.async
+// (coalesced 256-byte row segments, zero-filled tails).  Activity of a block is
+// looked up only when its parent is active (tree closure), so sparse trees
+// cost almost no tree traffic.
 // MODE 0: Z(y) = sum_{z active} |phi(y|z)| (Eq. 1.61; order totA + tot_L..tot_1)
 //         and cnt[y] = number of negative fp32 phi of active detail coefficients
 // MODE 2: emit those entries (key = Mallat z, value = {ray, f32 bits}) at pos[y]
@@ -498,6 +549,12 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void add_quad(double (&q)[4], int quad, double v) {
+    q[0] += quad == 0 ? v : 0.0;
+    q[1] += quad == 1 ? v : 0.0;
+    q[2] += quad == 2 ? v : 0.0;
+    q[3] += quad == 3 ? v : 0.0;
 }
 
 template <int MODE>
@@ -519,31 +576,43 @@ __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsi
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
     if (maxlen == 0 && y >= M) return;
+    const bool pow2 = (nx & (nx - 1)) == 0;
+    const int lgx = 31 - __clz(nx);
 
     int cur[LMAX + 1], cbi[LMAX + 1], cbj[LMAX + 1];
-    double sH[LMAX + 1], sV[LMAX + 1], sD[LMAX + 1], tot[LMAX + 1];
+    bool actv[LMAX + 2];
+    double q[LMAX + 1][4], tot[LMAX + 1];
 #pragma unroll
-    for (int l = 0; l <= LMAX; ++l) { cur[l] = -1; cbi[l] = cbj[l] = 0; sH[l] = sV[l] = sD[l] = tot[l] = 0.0; }
-    double sA = 0.0, totA = 0.0;
+    for (int l = 0; l <= LMAX; ++l) {
+        cur[l] = -1; cbi[l] = cbj[l] = 0; actv[l] = false; tot[l] = 0.0;
+        q[l][0] = q[l][1] = q[l][2] = q[l][3] = 0.0;
+    }
+    actv[LMAX + 1] = true;
+    double totA = 0.0;
     unsigned long long count = 0, wp = (MODE == 2 && y < M) ? pos[y] : 0;
 
     auto flush = [&](int l) {
+        const double TL = q[l][0], TR = q[l][1], BL = q[l][2], BR = q[l][3];
+        const double st = TL + TR, sb = BL + BR;
+        const double Av = st + sb, H = st - sb, V = (TL + BL) - (TR + BR), D = (TL + BR) - (TR + BL);
         const double sc = 1.0 / (double)(1 << l);
-        const double pH = sH[l] * sc, pV = sV[l] * sc, pD = sD[l] * sc;
-        if (l == L) { if (MODE == 0) totA += fabs(sA * sc); sA = 0.0; }
-        sH[l] = sV[l] = sD[l] = 0.0;
-        const int wl = nx >> l, hl = ny >> l;
-        if (!act[off.off[l] + (uint64_t)cbi[l] * wl + cbj[l]]) return;
-        if (MODE == 0) tot[l] += fabs(pH) + fabs(pV) + fabs(pD);
-        const float v[3] = {(float)pH, (float)pV, (float)pD};
-        const unsigned z[3] = {(unsigned)((hl + cbi[l]) * nx + cbj[l]), (unsigned)(cbi[l] * nx + wl + cbj[l]),
-                               (unsigned)((hl + cbi[l]) * nx + wl + cbj[l])};
+        if (MODE == 0 && l == L) totA += fabs(Av * sc);
+        if (actv[l]) {
+            const double pH = H * sc, pV = V * sc, pD = D * sc;
+            if (MODE == 0) tot[l] += fabs(pH) + fabs(pV) + fabs(pD);
+            const int wl = nx >> l, hl = ny >> l;
+            const float v[3] = {(float)pH, (float)pV, (float)pD};
+            const unsigned z[3] = {(unsigned)((hl + cbi[l]) * nx + cbj[l]), (unsigned)(cbi[l] * nx + wl + cbj[l]),
+                                   (unsigned)((hl + cbi[l]) * nx + wl + cbj[l])};
 #pragma unroll
-        for (int s = 0; s < 3; ++s)
-            if (v[s] < 0.0f) {
-                if (MODE == 0) ++count;
-                else { keys[wp] = z[s]; vals[wp] = make_uint2((unsigned)y, __float_as_uint(v[s])); ++wp; }
-            }
+            for (int s = 0; s < 3; ++s)
+                if (v[s] < 0.0f) {
+                    if (MODE == 0) ++count;
+                    else { keys[wp] = z[s]; vals[wp] = make_uint2((unsigned)y, __float_as_uint(v[s])); ++wp; }
+                }
+        }
+        if (l < L) add_quad(q[l + 1], ((cbi[l] & 1) << 1) | (cbj[l] & 1), Av);
+        q[l][0] = q[l][1] = q[l][2] = q[l][3] = 0.0;
     };
 
     for (unsigned long long base = 0; base < maxlen; base += 32) {
@@ -561,22 +630,29 @@ __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsi
             const uint2 e = buf[w][lane][i];
             const double h = hval(e);
             if (L == 0) { if (MODE == 0) totA += fabs(h); continue; }
-            const int iy = (int)(e.x / (unsigned)nx), ix = (int)(e.x % (unsigned)nx);
+            int ix, iy;
+            if (pow2) { ix = (int)(e.x & (unsigned)(nx - 1)); iy = (int)(e.x >> lgx); }
+            else { iy = (int)(e.x / (unsigned)nx); ix = (int)(e.x % (unsigned)nx); }
+            int changed = 0;
 #pragma unroll
             for (int l = 1; l <= LMAX; ++l) {
                 if (l > L) break;
-                const int bi = iy >> l, bj = ix >> l;
-                const int key = bi * (nx >> l) + bj;
-                if (key != cur[l]) {
-                    if (cur[l] >= 0) flush(l);
-                    cur[l] = key; cbi[l] = bi; cbj[l] = bj;
-                }
-                const bool top = ((iy >> (l - 1)) & 1) == 0, left = ((ix >> (l - 1)) & 1) == 0;
-                sH[l] += top ? h : -h;
-                sV[l] += left ? h : -h;
-                sD[l] += (top == left) ? h : -h;
-                if (l == L) sA += h;
+                const int key = (iy >> l) * (nx >> l) + (ix >> l);
+                if (key == cur[l]) break;
+                if (cur[l] >= 0) flush(l);
+                changed = l;
             }
+            if (changed) {
+#pragma unroll
+                for (int l = LMAX; l >= 1; --l) {
+                    if (l > changed) continue;
+                    cbi[l] = iy >> l; cbj[l] = ix >> l;
+                    cur[l] = cbi[l] * (nx >> l) + cbj[l];
+                    const bool parent = (l == L) ? true : actv[l + 1];
+                    actv[l] = parent && act[off.off[l] + (uint64_t)cbi[l] * (nx >> l) + cbj[l]] != 0;
+                }
+            }
+            add_quad(q[1], (int)(((iy & 1) << 1) | (ix & 1)), h);
         }
         __syncwarp();
     }
@@ -604,19 +680,10 @@ __global__ void __launch_bounds__(256) k_split(uint64_t nlist, const unsigned* _
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlist; i += W) {
         const unsigned z = list[i];
-        const uint64_t lo = ptr[z], hi = ptr[z + 1];
-        double a0 = 0.0, a1 = 0.0;
-        uint64_t k = lo + lane;
-        for (; k + 32 < hi; k += 64) {
-            const uint2 e0 = ld_stream(E + k), e1 = ld_stream(E + k + 32);
-            a0 = fma(hval(e0), (double)__ldg(q + e0.x), a0);
-            a1 = fma(hval(e1), (double)__ldg(q + e1.x), a1);
-        }
-        for (; k < hi; k += 32) {
-            const uint2 e0 = ld_stream(E + k);
-            a0 = fma(hval(e0), (double)__ldg(q + e0.x), a0);
-        }
-        const double s = warp_sum(a0 + a1);
+        const uint64_t nob[1] = {0};
+        double ss[1];
+        seg_dot<1>(E, q, ptr[z], nob, ptr[z + 1], lane, ss);
+        const double s = ss[0];
         if (lane == 0) bm[z] = s;
     }
 }

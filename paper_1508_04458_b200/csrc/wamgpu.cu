@@ -230,7 +230,7 @@ static void finish_matrix(Ctx* c) {
     c->C.swap(vout);
     kout.release();
     c->cub_tmp.release();
-    c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->Ml + 7) / 8, (uint64_t)c->sms * 16));
+    c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>(((c->Ml + FG - 1) / FG + 7) / 8, (uint64_t)c->sms * 16));
     c->nblk_col = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->N + 7) / 8, (uint64_t)c->sms * 16));
     c->partial.alloc(std::max(c->nblk_row, 1024));
     c->scal.alloc(8);
