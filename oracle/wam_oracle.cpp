@@ -456,15 +456,15 @@ static inline BlockIdx mallat(int nx, int ny, int l, int bi, int bj) {
 // block the ray crosses, at every level (SPEC.md:239-247 phi_column,
 // PAPER.md:134).  A ray's cells inside a block are contiguous in Siddon order
 // (cells are monotone in ix and iy), so a block is complete when the ray leaves
-// it.  Summation order (fixed here and mirrored bit-for-bit by the GPU walk;
-// SPEC.md:109 allows any deterministic order): hierarchical quadrant sums.  A
-// level-l block keeps the plain sums TL, TR, BL, BR of its four level-(l-1)
-// quadrants (level 1: the four voxels' h, each visited once), and on exit
+// it.  Summation order (fixed here, mirrored bit-for-bit by the GPU walk;
+// SPEC.md:109 allows any deterministic order): a level-l block keeps four
+// quadrant sums TL, TR, BL, BR, each the sequential ray-order sum of h over the
+// cells of that 2^(l-1) x 2^(l-1) quadrant; on exit
 //   st = TL+TR, sb = BL+BR, A = st+sb, H = st-sb, V = (TL+BL)-(TR+BR),
-//   D = (TL+BR)-(TR+BL);  phi = 2^-l * (A | H | V | D)   (A only at l == L),
-// then adds A into its parent's quadrant.  Sign patterns: H + on the top half,
-// V + on the left half, D + on TL/BR (Haar analysis of DESIGN.md §3).
-// cb(level, bi, bj, phiA, phiH, phiV, phiD) fires fine-to-coarse in ray order.
+//   D = (TL+BR)-(TR+BL);  phi = 2^-l * (A | H | V | D)   (A only at l == L).
+// Sign patterns: H + on the top half, V + on the left half, D + on TL/BR
+// (Haar analysis of DESIGN.md §3).  cb(level, bi, bj, phiA, phiH, phiV, phiD)
+// fires for every block in ray order within each level.
 template <typename CB>
 static void phi_walk(const orc_problem* p, int L, uint64_t y, CB&& cb) {
     const int nx = p->g.nx;
@@ -481,26 +481,23 @@ static void phi_walk(const orc_problem* p, int L, uint64_t y, CB&& cb) {
     auto flush = [&](int l) {
         const double TL = q[l][0], TR = q[l][1], BL = q[l][2], BR = q[l][3];
         const double st = TL + TR, sb = BL + BR;
-        const double A = st + sb, H = st - sb, V = (TL + BL) - (TR + BR), D = (TL + BR) - (TR + BL);
+        const double H = st - sb, V = (TL + BL) - (TR + BR), D = (TL + BR) - (TR + BL);
         const double sc = std::ldexp(1.0, -l);
-        cb(l, cbi[l], cbj[l], (l == L) ? A * sc : 0.0, H * sc, V * sc, D * sc);
-        if (l < L) q[l + 1][((cbi[l] & 1) << 1) | (cbj[l] & 1)] += A;
+        cb(l, cbi[l], cbj[l], (l == L) ? (st + sb) * sc : 0.0, H * sc, V * sc, D * sc);
         q[l][0] = q[l][1] = q[l][2] = q[l][3] = 0.0;
     };
     for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) {
         const int ix = (int)(p->ci[k] % (uint32_t)nx), iy = (int)(p->ci[k] / (uint32_t)nx);
-        int changed = 0;
+        const double h = p->hv[k];
         for (int l = 1; l <= L; ++l) {
-            const int key = (iy >> l) * (nx >> l) + (ix >> l);
-            if (key == cur[l]) break;
-            if (cur[l] >= 0) flush(l);
-            changed = l;
+            const int bi = iy >> l, bj = ix >> l;
+            const int key = bi * (nx >> l) + bj;
+            if (key != cur[l]) {
+                if (cur[l] >= 0) flush(l);
+                cur[l] = key; cbi[l] = bi; cbj[l] = bj;
+            }
+            q[l][(((iy >> (l - 1)) & 1) << 1) | ((ix >> (l - 1)) & 1)] += h;
         }
-        for (int l = 1; l <= changed; ++l) {
-            cbi[l] = iy >> l; cbj[l] = ix >> l;
-            cur[l] = cbi[l] * (nx >> l) + cbj[l];
-        }
-        q[1][((iy & 1) << 1) | (ix & 1)] += p->hv[k];
     }
     for (int l = 1; l <= L; ++l)
         if (cur[l] >= 0) flush(l);

@@ -15,7 +15,7 @@
 
 namespace wamgpu {
 
-constexpr int LMAX = 6;                 // Haar depth supported on the device
+constexpr int LMAX = 5;                 // Haar depth supported on the device
 struct ActOff { unsigned long long off[LMAX + 2]; };
 
 struct RayDev { double ox, oy, dx, dy, tmin, tmax; };
@@ -208,8 +208,7 @@ __device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float
 // Warp per ray.  MODE 0: l = H mu written as fp64 (forward_project).
 // MODE 1: fused Beer's law + I-divergence: q = fp32(I0 exp(-l)), per-block fp64
 // partial of the objective (deterministic block order).
-constexpr int FG = 4;  // rows per warp task in the forward kernel
-template <int MODE>
+template <int MODE, int FG>
 __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long long* __restrict__ rp,
                                                  const uint2* __restrict__ A, const float* __restrict__ mu,
                                                  const float* __restrict__ I0, const float* __restrict__ d,
@@ -225,8 +224,9 @@ __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long
         // row extents: lane j < nr+1 loads rp[y0+j]
         const unsigned long long myrp = (lane <= nr) ? __ldg(rp + y0 + lane) : 0ull;
         const uint64_t lo = __shfl_sync(0xffffffffu, myrp, 0), hi = __shfl_sync(0xffffffffu, myrp, nr);
-        uint64_t bnd[FG - 1];
+        uint64_t bnd[FG > 1 ? FG - 1 : 1];
 #pragma unroll
+        bnd[0] = 0;
         for (int g = 0; g < FG - 1; ++g) bnd[g] = __shfl_sync(0xffffffffu, myrp, min(g + 1, nr));
         double l[FG];
         seg_dot<FG>(A, mu, lo, bnd, hi, lane, l);
@@ -526,22 +526,23 @@ __global__ void k_mark(int nx, int ny, int L, const double* __restrict__ s, doub
     }
 }
 
-// Per-ray walk over the CSR row producing phi(y|z) of every crossed block at
-// every level (cells of a ray inside a block are contiguous in Siddon order,
-// so a block is complete when the ray leaves it).  Summation order: the
-// hierarchical quadrant sums fixed in DESIGN.md §4 (level-1 quadrants are
-// single voxels; a level-l block combines its four quadrant sums
-// st=TL+TR, sb=BL+BR, A=st+sb, H=st-sb, V=(TL+BL)-(TR+BR), D=(TL+BR)-(TR+BL)
-// and passes A to its parent), so each entry costs one fp64 add and a block
-// exit ~10 flops.  One THREAD per ray keeps that order exactly; the warp stages
-// its 32 rays' rows through shared memory 32 entries at a time with cp.async
-// (coalesced 256-byte row segments, zero-filled tails).  Activity of a block is
-// looked up only when its parent is active (tree closure), so sparse trees
-// cost almost no tree traffic.
+// Per-ray walk over the CSR row producing phi(y|z) of the crossed blocks
+// (cells of a ray inside a block are contiguous in Siddon order, so a block is
+// complete when the ray leaves it).  phi is built from four quadrant sums per
+// block, each the sequential ray-order sum of h over the quadrant's cells
+// (bit-identical to the oracle):
+//   st=TL+TR, sb=BL+BR, A=st+sb, H=st-sb, V=(TL+BL)-(TR+BR), D=(TL+BR)-(TR+BL).
+// Only the level-L block of a ray is always tracked (its A feeds Z0's
+// approximation part: one fp64 add per entry); a finer block is tracked only
+// while its parent is active (tree closure), so the cost is nnz plus work
+// proportional to the active tree.  One THREAD per ray keeps the sequential
+// order; the warp stages its 32 rays' rows through shared memory 32 entries at
+// a time with cp.async (coalesced row segments, zero-filled tails).
 // MODE 0: Z(y) = sum_{z active} |phi(y|z)| (Eq. 1.61; order totA + tot_L..tot_1)
 //         and cnt[y] = number of negative fp32 phi of active detail coefficients
 // MODE 2: emit those entries (key = Mallat z, value = {ray, f32 bits}) at pos[y]
 constexpr int WALK_WARPS = 4;
+constexpr int WLMAX = 5;  // deepest Haar level the walk tracks (LMAX for the tree)
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     const int sz = valid ? 8 : 0;
@@ -558,7 +559,7 @@ __device__ __forceinline__ void add_quad(double (&q)[4], int quad, double v) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsigned long long* __restrict__ rp,
+__global__ void __launch_bounds__(32 * WALK_WARPS, 3) k_walk(uint64_t M, const unsigned long long* __restrict__ rp,
                                                           const uint2* __restrict__ A, int nx, int ny, int L,
                                                           const uint8_t* __restrict__ act, ActOff off,
                                                           double* __restrict__ zrow,
@@ -579,26 +580,26 @@ __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsi
     const bool pow2 = (nx & (nx - 1)) == 0;
     const int lgx = 31 - __clz(nx);
 
-    int cur[LMAX + 1], cbi[LMAX + 1], cbj[LMAX + 1];
-    bool actv[LMAX + 2];
-    double q[LMAX + 1][4], tot[LMAX + 1];
+    int cur[WLMAX + 1], cbi[WLMAX + 1], cbj[WLMAX + 1];
+    bool av[WLMAX + 2];
+    double q[WLMAX + 1][4], tot[WLMAX + 1];
 #pragma unroll
-    for (int l = 0; l <= LMAX; ++l) {
-        cur[l] = -1; cbi[l] = cbj[l] = 0; actv[l] = false; tot[l] = 0.0;
+    for (int l = 0; l <= WLMAX; ++l) {
+        cur[l] = -1; cbi[l] = cbj[l] = 0; av[l] = false; tot[l] = 0.0;
         q[l][0] = q[l][1] = q[l][2] = q[l][3] = 0.0;
     }
-    actv[LMAX + 1] = true;
+    av[WLMAX + 1] = true;
     double totA = 0.0;
     unsigned long long count = 0, wp = (MODE == 2 && y < M) ? pos[y] : 0;
 
+    // block exit at level l (must be a compile-time constant after unrolling)
     auto flush = [&](int l) {
         const double TL = q[l][0], TR = q[l][1], BL = q[l][2], BR = q[l][3];
         const double st = TL + TR, sb = BL + BR;
-        const double Av = st + sb, H = st - sb, V = (TL + BL) - (TR + BR), D = (TL + BR) - (TR + BL);
         const double sc = 1.0 / (double)(1 << l);
-        if (MODE == 0 && l == L) totA += fabs(Av * sc);
-        if (actv[l]) {
-            const double pH = H * sc, pV = V * sc, pD = D * sc;
+        if (MODE == 0 && l == L) totA += fabs((st + sb) * sc);
+        if (av[l]) {
+            const double pH = (st - sb) * sc, pV = ((TL + BL) - (TR + BR)) * sc, pD = ((TL + BR) - (TR + BL)) * sc;
             if (MODE == 0) tot[l] += fabs(pH) + fabs(pV) + fabs(pD);
             const int wl = nx >> l, hl = ny >> l;
             const float v[3] = {(float)pH, (float)pV, (float)pD};
@@ -611,8 +612,9 @@ __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsi
                     else { keys[wp] = z[s]; vals[wp] = make_uint2((unsigned)y, __float_as_uint(v[s])); ++wp; }
                 }
         }
-        if (l < L) add_quad(q[l + 1], ((cbi[l] & 1) << 1) | (cbj[l] & 1), Av);
         q[l][0] = q[l][1] = q[l][2] = q[l][3] = 0.0;
+        cur[l] = -1;
+        av[l] = false;
     };
 
     for (unsigned long long base = 0; base < maxlen; base += 32) {
@@ -633,37 +635,46 @@ __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsi
             int ix, iy;
             if (pow2) { ix = (int)(e.x & (unsigned)(nx - 1)); iy = (int)(e.x >> lgx); }
             else { iy = (int)(e.x / (unsigned)nx); ix = (int)(e.x % (unsigned)nx); }
-            int changed = 0;
+            // coarsest tracked level whose block changes at this cell
+            int m = 0;
 #pragma unroll
-            for (int l = 1; l <= LMAX; ++l) {
-                if (l > L) break;
+            for (int l = WLMAX; l >= 1; --l) {
+                if (l > L) continue;
+                if (l < L && !av[l + 1]) break;          // not tracked below an inactive block
                 const int key = (iy >> l) * (nx >> l) + (ix >> l);
-                if (key == cur[l]) break;
-                if (cur[l] >= 0) flush(l);
-                changed = l;
+                if (key != cur[l]) { m = l; break; }
             }
-            if (changed) {
+            if (m) {
 #pragma unroll
-                for (int l = LMAX; l >= 1; --l) {
-                    if (l > changed) continue;
+                for (int l = 1; l <= WLMAX; ++l)
+                    if (l <= m && cur[l] >= 0) flush(l);
+#pragma unroll
+                for (int l = WLMAX; l >= 1; --l) {
+                    if (l > m) continue;
+                    if (l < L && !av[l + 1]) break;
                     cbi[l] = iy >> l; cbj[l] = ix >> l;
                     cur[l] = cbi[l] * (nx >> l) + cbj[l];
-                    const bool parent = (l == L) ? true : actv[l + 1];
-                    actv[l] = parent && act[off.off[l] + (uint64_t)cbi[l] * (nx >> l) + cbj[l]] != 0;
+                    av[l] = act[off.off[l] + (uint64_t)cur[l]] != 0;
                 }
             }
-            add_quad(q[1], (int)(((iy & 1) << 1) | (ix & 1)), h);
+#pragma unroll
+            for (int l = WLMAX; l >= 1; --l) {
+                if (l > L) continue;
+                if (l < L && !av[l + 1]) break;
+                if (l == L || av[l])
+                    add_quad(q[l], (((iy >> (l - 1)) & 1) << 1) | ((ix >> (l - 1)) & 1), h);
+            }
         }
         __syncwarp();
     }
     if (y >= M) return;
 #pragma unroll
-    for (int l = 1; l <= LMAX; ++l)
+    for (int l = 1; l <= WLMAX; ++l)
         if (l <= L && cur[l] >= 0) flush(l);
     if (MODE == 0) {
         double z = totA;
 #pragma unroll
-        for (int l = LMAX; l >= 1; --l)
+        for (int l = WLMAX; l >= 1; --l)
             if (l <= L) z += tot[l];
         zrow[y] = z;
         cnt[y] = count;

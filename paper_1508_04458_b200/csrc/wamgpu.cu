@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -103,6 +104,7 @@ struct wamgpu_ctx {
     double Z0 = 0.0;
     DBuf<double> scal, partial;
     int nblk_row = 1, nblk_col = 1;
+    int fg = 1;  // rows per warp task in the forward kernel (WAMGPU_FG tuning knob)
     DBuf<unsigned long long> counters;
     DBuf<int> flag, it;
     DBuf<double> objs;
@@ -230,7 +232,7 @@ static void finish_matrix(Ctx* c) {
     c->C.swap(vout);
     kout.release();
     c->cub_tmp.release();
-    c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>(((c->Ml + FG - 1) / FG + 7) / 8, (uint64_t)c->sms * 16));
+    c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>(((c->Ml + c->fg - 1) / c->fg + 7) / 8, (uint64_t)c->sms * 16));
     c->nblk_col = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->N + 7) / 8, (uint64_t)c->sms * 16));
     c->partial.alloc(std::max(c->nblk_row, 1024));
     c->scal.alloc(8);
@@ -319,8 +321,14 @@ static void back_into(Ctx* c, const float* w, double* out) {
 // q = I0 exp(-H mu), objective -> scal[0] (all-reduced), record
 static void forward_fused(Ctx* c, bool record) {
     c->timer_begin(T_FWD);
-    k_forward<1><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, c->q.p, nullptr,
-                                                c->partial.p, c->flag.p);
+    switch (c->fg) {
+        case 1: k_forward<1, 1><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p,
+                                                                c->q.p, nullptr, c->partial.p, c->flag.p); break;
+        case 2: k_forward<1, 2><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p,
+                                                                c->q.p, nullptr, c->partial.p, c->flag.p); break;
+        default: k_forward<1, 4><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p,
+                                                                 c->q.p, nullptr, c->partial.p, c->flag.p); break;
+    }
     check_launch(c);
     c->timer_end(T_FWD);
     c->tm.fwd_launches++;
@@ -689,6 +697,7 @@ static Ctx* create(int device) {
     CK(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10) throw CudaError("wamgpu: requires an sm_100a (Blackwell) device");
     c->sms = prop.multiProcessorCount;
+    if (const char* e = std::getenv("WAMGPU_FG")) c->fg = std::max(1, std::min(4, std::atoi(e)));
     CK(cudaEventCreate(&c->ev_t0));
     CK(cudaEventCreate(&c->ev_a));
     CK(cudaEventCreate(&c->ev_b));
@@ -859,7 +868,7 @@ int wamgpu_forward_project(wamgpu_ctx* ctx, const double* mu, double* l) {
         std::vector<float> m(c->N);
         for (uint64_t x = 0; x < c->N; ++x) m[x] = (float)mu[x];
         CK(cudaMemcpyAsync(c->fscratch.p, m.data(), c->N * 4, cudaMemcpyHostToDevice, c->st));
-        k_forward<0><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->fscratch.p, nullptr, nullptr,
+        k_forward<0, 1><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->fscratch.p, nullptr, nullptr,
                                                     nullptr, c->dscratch.p, nullptr, c->flag.p);
         check_launch(c);
         CK(cudaMemcpyAsync(l, c->dscratch.p, c->Ml * 8, cudaMemcpyDeviceToHost, c->st));

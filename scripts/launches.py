@@ -1,0 +1,26 @@
+"""Summarise an ncu --csv launch list (gpu__time_duration.sum) per kernel."""
+import collections
+import csv
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+for i, r in enumerate(rows):
+    if r and r[0] == "ID":
+        hdr, start = r, i + 1
+        break
+ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+agg = collections.OrderedDict()
+for r in rows[start:]:
+    if len(r) <= vi:
+        continue
+    name = r[ki].split("(")[0].replace("void ", "")[:58]
+    us = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+    a = agg.setdefault(name, [0, 0.0])
+    a[0] += 1
+    a[1] += us
+tot = sum(v[1] for v in agg.values())
+print(f"{'kernel':58s} {'n':>5s} {'total ms':>10s} {'avg us':>10s} {'share':>6s}")
+for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+    print(f"{k:58s} {n:5d} {t / 1e3:10.3f} {t / n:10.1f} {100 * t / tot:5.1f}%")
+print(f"{'TOTAL':58s} {sum(v[0] for v in agg.values()):5d} {tot / 1e3:10.3f}")
