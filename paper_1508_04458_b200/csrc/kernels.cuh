@@ -149,66 +149,91 @@ __device__ __forceinline__ double idiv_term(double d, double q) {
     return (d > 0.0 ? d * log(d / q) : 0.0) - d + q;
 }
 
-// Warp-cooperative segmented sparse dot products over a contiguous entry range
-// [lo, hi) holding G consecutive segments (rows or columns) split at b[0..G-2]:
-// out[g] = sum over segment g of h_k x[idx_k].  Software-pipelined: the
-// UNROLL predicated 8-byte streaming loads of round r+1 are issued before the
-// gathers of round r, so a warp keeps ~2*UNROLL*256 B in flight and pays about
-// one memory latency per 256*UNROLL/32 entries, across segment boundaries.
-// fp64 accumulation (products of two fp32 are exact in fp64); segment
-// selection is by predicated fma with h=0 (an exact no-op); fixed
-// xor-butterfly reduction (deterministic).
-constexpr int UNROLL = 8;
-template <int G>
-__device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
-                                        const uint64_t (&b)[G > 1 ? G - 1 : 1], uint64_t hi, int lane,
-                                        double (&out)[G]) {
-    double acc[G][2];
-#pragma unroll
-    for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = 0.0;
+// Warp-cooperative sparse dot products of 32 consecutive rows (or columns)
+// [y0, y0+nr): row r = sum_{k in [ptr[y0+r], ptr[y0+r+1])} h_k x[idx_k].  The
+// warp streams the rows' contiguous entry range in rounds of 32*UNROLL entries
+// (predicated 8-byte streaming loads); the loads of round i+1 are issued
+// before the gathers of round i, so the pipeline never drains at row
+// boundaries and a warp keeps ~2*UNROLL*256 B in flight.  Row boundaries that
+// fall inside a round are closed with masked partial sums.  fp64 accumulation
+// (fp32 x fp32 products are exact in fp64), fixed lane-partial + xor-butterfly
+// order (deterministic).  Returns row (lane)'s value in lane `lane` (lane < nr).
+template <int UNROLL>
+__device__ __forceinline__ double stream_rows(const uint2* __restrict__ A, const float* __restrict__ x,
+                                              const unsigned long long* __restrict__ ptr, uint64_t y0, int nr,
+                                              int lane) {
+    const unsigned long long myp = (lane <= nr) ? __ldg(ptr + y0 + lane) : 0ull;
+    const uint64_t k0 = __shfl_sync(0xffffffffu, myp, 0), k1 = __shfl_sync(0xffffffffu, myp, nr);
+    int r = 0;
+    uint64_t rs = k0, nb = __shfl_sync(0xffffffffu, myp, 1 < nr ? 1 : nr);
+    double acc = 0.0, mine = 0.0;
+    // close leading empty rows
+    while (r < nr && nb <= rs) {
+        if (lane == r) mine = 0.0;
+        ++r;
+        nb = __shfl_sync(0xffffffffu, myp, r + 1 < nr ? r + 1 : nr);
+    }
     uint2 ec[UNROLL];
-    uint64_t base = lo + lane;
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-        const uint64_t k = base + 32 * u;
-        ec[u] = (k < hi) ? ld_stream(A + k) : make_uint2(0u, 0u);
+        const uint64_t k = k0 + lane + 32 * u;
+        ec[u] = (k < k1) ? ld_stream(A + k) : make_uint2(0u, 0u);
     }
-    for (; base < hi; base += 32 * UNROLL) {
+    for (uint64_t b0 = k0; b0 < k1; b0 += 32 * UNROLL) {
         uint2 en[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
-            const uint64_t k = base + 32 * (UNROLL + u);
-            en[u] = (k < hi) ? ld_stream(A + k) : make_uint2(0u, 0u);
+            const uint64_t k = b0 + 32 * UNROLL + lane + 32 * u;
+            en[u] = (k < k1) ? ld_stream(A + k) : make_uint2(0u, 0u);
         }
         float v[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(x + ec[u].x);
+        double p[UNROLL];
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-            const double h = hval(ec[u]), xv = (double)v[u];
-            if (G == 1) {
-                acc[0][u & 1] = fma(h, xv, acc[0][u & 1]);
-            } else {
-                const uint64_t k = base + 32 * u;
-                int seg = 0;
+        for (int u = 0; u < UNROLL; ++u) p[u] = hval(ec[u]) * (double)v[u];
+        const uint64_t re = b0 + 32 * UNROLL;
+        // rows that end inside this round
+        while (r < nr && nb <= re) {
+            double part = acc;
 #pragma unroll
-                for (int g = 0; g < G - 1; ++g) seg += (k >= b[g]);
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint64_t k = b0 + lane + 32 * u;
+                part += (k >= rs && k < nb) ? p[u] : 0.0;
+            }
+            const double tot = warp_sum(part);
+            if (lane == r) mine = tot;
+            acc = 0.0;
+            rs = nb;
+            ++r;
+            nb = __shfl_sync(0xffffffffu, myp, r + 1 < nr ? r + 1 : nr);
+        }
+        if (r < nr) {
 #pragma unroll
-                for (int g = 0; g < G; ++g) acc[g][u & 1] = fma(seg == g ? h : 0.0, xv, acc[g][u & 1]);
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint64_t k = b0 + lane + 32 * u;
+                acc += (k >= rs) ? p[u] : 0.0;
             }
         }
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) ec[u] = en[u];
     }
-#pragma unroll
-    for (int g = 0; g < G; ++g) out[g] = warp_sum(acc[g][0] + acc[g][1]);
+    // rows not closed inside the stream (trailing empty rows / last row)
+    while (r < nr) {
+        const double tot = warp_sum(acc);
+        if (lane == r) mine = tot;
+        acc = 0.0;
+        ++r;
+    }
+    return mine;
 }
 
 // ------------------------------------------------------------ CSR forward
-// Warp per ray.  MODE 0: l = H mu written as fp64 (forward_project).
-// MODE 1: fused Beer's law + I-divergence: q = fp32(I0 exp(-l)), per-block fp64
-// partial of the objective (deterministic block order).
-template <int MODE, int FG>
+// Warp task = 32 consecutive rays (contiguous CSR entries).  MODE 0: l = H mu
+// (forward_project, fp64 out).  MODE 1: fused Beer's law + I-divergence: the
+// 32 lanes finish their rays in parallel (q = fp32(I0 exp(-l)), coalesced),
+// and the per-block fp64 objective partial is summed in a fixed order.
+template <int MODE, int UNROLL>
 __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long long* __restrict__ rp,
                                                  const uint2* __restrict__ A, const float* __restrict__ mu,
                                                  const float* __restrict__ I0, const float* __restrict__ d,
@@ -216,38 +241,25 @@ __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long
                                                  double* __restrict__ partial, int* __restrict__ flag) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t ntask = (M + FG - 1) / FG;
+    const uint64_t ntask = (M + 31) / 32;
     double tacc = 0.0;
     for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; t < ntask; t += W) {
-        const uint64_t y0 = t * FG;
-        const int nr = (int)((M - y0) < (uint64_t)FG ? (M - y0) : (uint64_t)FG);
-        // row extents: lane j < nr+1 loads rp[y0+j]
-        const unsigned long long myrp = (lane <= nr) ? __ldg(rp + y0 + lane) : 0ull;
-        const uint64_t lo = __shfl_sync(0xffffffffu, myrp, 0), hi = __shfl_sync(0xffffffffu, myrp, nr);
-        uint64_t bnd[FG > 1 ? FG - 1 : 1];
-#pragma unroll
-        bnd[0] = 0;
-        for (int g = 0; g < FG - 1; ++g) bnd[g] = __shfl_sync(0xffffffffu, myrp, min(g + 1, nr));
-        double l[FG];
-        seg_dot<FG>(A, mu, lo, bnd, hi, lane, l);
-        // lane g finishes row y0+g: Beer's law, I-divergence term
-        double lg = l[0];
-#pragma unroll
-        for (int g = 1; g < FG; ++g) lg = (lane == g) ? l[g] : lg;
+        const uint64_t y0 = t * 32;
+        const int nr = (int)((M - y0) < 32 ? (M - y0) : 32);
+        const double l = stream_rows<UNROLL>(A, mu, rp, y0, nr, lane);
         if (lane < nr) {
             const uint64_t y = y0 + lane;
-            if (!isfinite(lg)) atomicOr(flag, 1);
+            if (!isfinite(l)) atomicOr(flag, 1);
             if (MODE == 0) {
-                lout[y] = lg;
+                lout[y] = l;
             } else {
-                const double qq = (double)I0[y] * exp(-lg);
+                const double qq = (double)I0[y] * exp(-l);
                 q[y] = (float)qq;
                 tacc += idiv_term((double)d[y], qq);
             }
         }
     }
     if (MODE == 1) {
-        // deterministic block partial: lanes, then warps, in fixed order
         __shared__ double s[32];
         double v = tacc;
 #pragma unroll
@@ -263,22 +275,24 @@ __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long
 }
 
 // ------------------------------------------------------------- CSC back
-// Warp per voxel: g(x) = sum_y h(y|x) w(y) in fp64 over the voxel's CSC column.
+// Warp task = 32 consecutive voxels: g(x) = sum_y h(y|x) w(y) in fp64 over each
+// voxel's CSC column (voxel-driven gather, no atomics).
 // MODE 0: write g (fp64).  MODE 1: fused AM update:
 // mu <- max(0, mu + ln(g/b)/Z0) where b > 0 and g > 0, otherwise frozen.
-template <int MODE>
+template <int MODE, int UNROLL>
 __global__ void __launch_bounds__(256) k_back(uint64_t N, const unsigned long long* __restrict__ cp,
                                               const uint2* __restrict__ C, const float* __restrict__ w,
                                               double* __restrict__ g, const double* __restrict__ bam,
                                               float* __restrict__ mu, double Z0, int* __restrict__ flag) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t x = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; x < N; x += W) {
-        const uint64_t nob[1] = {0};
-        double cc[1];
-        seg_dot<1>(C, w, cp[x], nob, cp[x + 1], lane, cc);
-        const double c = cc[0];
-        if (lane == 0) {
+    const uint64_t ntask = (N + 31) / 32;
+    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; t < ntask; t += W) {
+        const uint64_t x0 = t * 32;
+        const int nr = (int)((N - x0) < 32 ? (N - x0) : 32);
+        const double c = stream_rows<UNROLL>(C, w, cp, x0, nr, lane);
+        if (lane < nr) {
+            const uint64_t x = x0 + lane;
             if (MODE == 0) {
                 g[x] = c;
             } else {
@@ -532,17 +546,22 @@ __global__ void k_mark(int nx, int ny, int L, const double* __restrict__ s, doub
 // block, each the sequential ray-order sum of h over the quadrant's cells
 // (bit-identical to the oracle):
 //   st=TL+TR, sb=BL+BR, A=st+sb, H=st-sb, V=(TL+BL)-(TR+BR), D=(TL+BR)-(TR+BL).
-// Only the level-L block of a ray is always tracked (its A feeds Z0's
-// approximation part: one fp64 add per entry); a finer block is tracked only
-// while its parent is active (tree closure), so the cost is nnz plus work
-// proportional to the active tree.  One THREAD per ray keeps the sequential
-// order; the warp stages its 32 rays' rows through shared memory 32 entries at
-// a time with cp.async (coalesced row segments, zero-filled tails).
-// MODE 0: Z(y) = sum_{z active} |phi(y|z)| (Eq. 1.61; order totA + tot_L..tot_1)
-//         and cnt[y] = number of negative fp32 phi of active detail coefficients
-// MODE 2: emit those entries (key = Mallat z, value = {ray, f32 bits}) at pos[y]
+// L is a template parameter (no runtime level loops).  The tree-independent
+// approximation part of Z (sum over level-L blocks of |phi_A|) is computed once
+// at init (MODE 0) and cached per ray; at expansions (MODE 1, 2) only the
+// level-L block is tracked (one key compare per entry, level-L activity bytes
+// staged in shared memory) and finer blocks only under active parents (tree
+// closure): cost = nnz streaming + work proportional to the active tree.
+// One THREAD per ray keeps the sequential order; the warp stages its 32 rays'
+// rows through shared memory 32 entries at a time with cp.async (coalesced
+// row segments, zero-filled tails).
+// MODE 0 (init, empty tree): zA[y] = Z(y) = sum_{level-L blocks} |phi_A|
+//        (L == 0: sum_x h, the AM normaliser row sums)
+// MODE 1 (expand): Z(y) = zA[y] + tot_L + ... + tot_1 over active details;
+//        cnt[y] = number of negative fp32 phi of active detail coefficients
+// MODE 2 (fill): emit those entries (key = Mallat z, value = {ray, f32}) at pos[y]
 constexpr int WALK_WARPS = 4;
-constexpr int WLMAX = 5;  // deepest Haar level the walk tracks (LMAX for the tree)
+constexpr int WALK_TREE_SMEM = 4096;  // level-L activity bytes staged in smem
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     const int sz = valid ? 8 : 0;
@@ -558,18 +577,26 @@ __device__ __forceinline__ void add_quad(double (&q)[4], int quad, double v) {
     q[3] += quad == 3 ? v : 0.0;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(32 * WALK_WARPS, 3) k_walk(uint64_t M, const unsigned long long* __restrict__ rp,
-                                                          const uint2* __restrict__ A, int nx, int ny, int L,
+template <int MODE, int L>
+__global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsigned long long* __restrict__ rp,
+                                                          const uint2* __restrict__ A, int nx, int ny,
                                                           const uint8_t* __restrict__ act, ActOff off,
-                                                          double* __restrict__ zrow,
+                                                          double* __restrict__ zA, double* __restrict__ zrow,
                                                           unsigned long long* __restrict__ cnt,
                                                           const unsigned long long* __restrict__ pos,
                                                           unsigned* __restrict__ keys, uint2* __restrict__ vals) {
     __shared__ uint2 buf[WALK_WARPS][32][33];
+    __shared__ uint8_t treeL[WALK_TREE_SMEM];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint64_t y = ((uint64_t)blockIdx.x * WALK_WARPS + w) * 32 + lane;
-    if (MODE == 0 && y == M) cnt[M] = 0;
+    const int WLv = (L > 0) ? (nx >> L) : nx, HLv = (L > 0) ? (ny >> L) : ny;
+    const int nL = WLv * HLv;
+    const bool tree_smem = (MODE != 0) && L > 0 && nL <= WALK_TREE_SMEM;
+    if (tree_smem) {
+        for (int i = threadIdx.x; i < nL; i += blockDim.x) treeL[i] = act[off.off[L] + i];
+        __syncthreads();
+    }
+    if (MODE == 1 && y == M) cnt[M] = 0;
     uint64_t lo = 0, hi = 0;
     if (y < M) { lo = rp[y]; hi = rp[y + 1]; }
     const unsigned long long len = hi - lo;
@@ -580,27 +607,28 @@ __global__ void __launch_bounds__(32 * WALK_WARPS, 3) k_walk(uint64_t M, const u
     const bool pow2 = (nx & (nx - 1)) == 0;
     const int lgx = 31 - __clz(nx);
 
-    int cur[WLMAX + 1], cbi[WLMAX + 1], cbj[WLMAX + 1];
-    bool av[WLMAX + 2];
-    double q[WLMAX + 1][4], tot[WLMAX + 1];
+    constexpr int NL = L + 1;
+    int cur[NL], cbi[NL], cbj[NL];
+    bool av[NL + 1];
+    double q[NL][4], tot[NL];
 #pragma unroll
-    for (int l = 0; l <= WLMAX; ++l) {
+    for (int l = 0; l < NL; ++l) {
         cur[l] = -1; cbi[l] = cbj[l] = 0; av[l] = false; tot[l] = 0.0;
         q[l][0] = q[l][1] = q[l][2] = q[l][3] = 0.0;
     }
-    av[WLMAX + 1] = true;
+    av[NL] = true;
     double totA = 0.0;
     unsigned long long count = 0, wp = (MODE == 2 && y < M) ? pos[y] : 0;
 
-    // block exit at level l (must be a compile-time constant after unrolling)
+    // block exit at level l (compile-time after unrolling)
     auto flush = [&](int l) {
         const double TL = q[l][0], TR = q[l][1], BL = q[l][2], BR = q[l][3];
         const double st = TL + TR, sb = BL + BR;
         const double sc = 1.0 / (double)(1 << l);
         if (MODE == 0 && l == L) totA += fabs((st + sb) * sc);
-        if (av[l]) {
+        if (MODE != 0 && av[l]) {
             const double pH = (st - sb) * sc, pV = ((TL + BL) - (TR + BR)) * sc, pD = ((TL + BR) - (TR + BL)) * sc;
-            if (MODE == 0) tot[l] += fabs(pH) + fabs(pV) + fabs(pD);
+            if (MODE == 1) tot[l] += fabs(pH) + fabs(pV) + fabs(pD);
             const int wl = nx >> l, hl = ny >> l;
             const float v[3] = {(float)pH, (float)pV, (float)pD};
             const unsigned z[3] = {(unsigned)((hl + cbi[l]) * nx + cbj[l]), (unsigned)(cbi[l] * nx + wl + cbj[l]),
@@ -608,7 +636,7 @@ __global__ void __launch_bounds__(32 * WALK_WARPS, 3) k_walk(uint64_t M, const u
 #pragma unroll
             for (int s = 0; s < 3; ++s)
                 if (v[s] < 0.0f) {
-                    if (MODE == 0) ++count;
+                    if (MODE == 1) ++count;
                     else { keys[wp] = z[s]; vals[wp] = make_uint2((unsigned)y, __float_as_uint(v[s])); ++wp; }
                 }
         }
@@ -616,9 +644,12 @@ __global__ void __launch_bounds__(32 * WALK_WARPS, 3) k_walk(uint64_t M, const u
         cur[l] = -1;
         av[l] = false;
     };
+    auto is_act = [&](int l, int key) -> bool {
+        if (l == L && tree_smem) return treeL[key] != 0;
+        return act[off.off[l] + (uint64_t)key] != 0;
+    };
 
     for (unsigned long long base = 0; base < maxlen; base += 32) {
-        // stage entries [base, base+32) of each of the warp's 32 rays
         for (int j = 0; j < 32; ++j) {
             const unsigned long long lj = __shfl_sync(0xffffffffu, lo, j);
             const unsigned long long nj = __shfl_sync(0xffffffffu, len, j);
@@ -635,47 +666,56 @@ __global__ void __launch_bounds__(32 * WALK_WARPS, 3) k_walk(uint64_t M, const u
             int ix, iy;
             if (pow2) { ix = (int)(e.x & (unsigned)(nx - 1)); iy = (int)(e.x >> lgx); }
             else { iy = (int)(e.x / (unsigned)nx); ix = (int)(e.x % (unsigned)nx); }
+            if (MODE == 0) {
+                // approximation only: level-L quadrant sums of every crossed block
+                const int key = (iy >> L) * WLv + (ix >> L);
+                if (key != cur[L]) {
+                    if (cur[L] >= 0) flush(L);
+                    cur[L] = key;
+                }
+                add_quad(q[L], (((iy >> (L - 1)) & 1) << 1) | ((ix >> (L - 1)) & 1), h);
+                continue;
+            }
             // coarsest tracked level whose block changes at this cell
             int m = 0;
 #pragma unroll
-            for (int l = WLMAX; l >= 1; --l) {
-                if (l > L) continue;
-                if (l < L && !av[l + 1]) break;          // not tracked below an inactive block
+            for (int l = L; l >= 1; --l) {
+                if (l < L && !av[l + 1]) break;       // untracked below an inactive block
                 const int key = (iy >> l) * (nx >> l) + (ix >> l);
                 if (key != cur[l]) { m = l; break; }
             }
             if (m) {
 #pragma unroll
-                for (int l = 1; l <= WLMAX; ++l)
+                for (int l = 1; l <= L; ++l)
                     if (l <= m && cur[l] >= 0) flush(l);
 #pragma unroll
-                for (int l = WLMAX; l >= 1; --l) {
+                for (int l = L; l >= 1; --l) {
                     if (l > m) continue;
                     if (l < L && !av[l + 1]) break;
                     cbi[l] = iy >> l; cbj[l] = ix >> l;
                     cur[l] = cbi[l] * (nx >> l) + cbj[l];
-                    av[l] = act[off.off[l] + (uint64_t)cur[l]] != 0;
+                    av[l] = is_act(l, cur[l]);
                 }
             }
 #pragma unroll
-            for (int l = WLMAX; l >= 1; --l) {
-                if (l > L) continue;
-                if (l < L && !av[l + 1]) break;
-                if (l == L || av[l])
-                    add_quad(q[l], (((iy >> (l - 1)) & 1) << 1) | ((ix >> (l - 1)) & 1), h);
+            for (int l = L; l >= 1; --l) {
+                if (!av[l]) break;                     // details only inside active blocks
+                add_quad(q[l], (((iy >> (l - 1)) & 1) << 1) | ((ix >> (l - 1)) & 1), h);
             }
         }
         __syncwarp();
     }
     if (y >= M) return;
 #pragma unroll
-    for (int l = 1; l <= WLMAX; ++l)
-        if (l <= L && cur[l] >= 0) flush(l);
+    for (int l = 1; l <= L; ++l)
+        if (cur[l] >= 0) flush(l);
     if (MODE == 0) {
-        double z = totA;
+        zA[y] = totA;
+        zrow[y] = totA;
+    } else if (MODE == 1) {
+        double z = zA[y];
 #pragma unroll
-        for (int l = WLMAX; l >= 1; --l)
-            if (l <= L) z += tot[l];
+        for (int l = L; l >= 1; --l) z += tot[l];
         zrow[y] = z;
         cnt[y] = count;
     }
@@ -691,10 +731,19 @@ __global__ void __launch_bounds__(256) k_split(uint64_t nlist, const unsigned* _
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlist; i += W) {
         const unsigned z = list[i];
-        const uint64_t nob[1] = {0};
-        double ss[1];
-        seg_dot<1>(E, q, ptr[z], nob, ptr[z + 1], lane, ss);
-        const double s = ss[0];
+        const uint64_t lo = ptr[z], hi = ptr[z + 1];
+        double a0 = 0.0, a1 = 0.0;
+        uint64_t k = lo + lane;
+        for (; k + 32 < hi; k += 64) {
+            const uint2 e0 = ld_stream(E + k), e1 = ld_stream(E + k + 32);
+            a0 = fma(hval(e0), (double)__ldg(q + e0.x), a0);
+            a1 = fma(hval(e1), (double)__ldg(q + e1.x), a1);
+        }
+        for (; k < hi; k += 32) {
+            const uint2 e0 = ld_stream(E + k);
+            a0 = fma(hval(e0), (double)__ldg(q + e0.x), a0);
+        }
+        const double s = warp_sum(a0 + a1);
         if (lane == 0) bm[z] = s;
     }
 }

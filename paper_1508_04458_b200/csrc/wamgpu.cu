@@ -89,6 +89,7 @@ struct wamgpu_ctx {
     DBuf<float> mu, beta, fscratch;
     DBuf<double> g, bdata, bam, mu64, bp_dbg, bm_dbg, zrow, dscratch;
     DBuf<unsigned long long> wcnt;      // per-ray Phi^- counts from the Z0 walk (then scanned)
+    DBuf<double> zA;                    // per-ray approximation part of Z (tree-independent)
     DBuf<uint8_t> cub_tmp;
     DBuf<unsigned> kin_s, kout_s;
     DBuf<uint2> vin_s;
@@ -104,7 +105,7 @@ struct wamgpu_ctx {
     double Z0 = 0.0;
     DBuf<double> scal, partial;
     int nblk_row = 1, nblk_col = 1;
-    int fg = 1;  // rows per warp task in the forward kernel (WAMGPU_FG tuning knob)
+    int unroll = 8;  // SpMV pipeline depth (WAMGPU_UNROLL: 4 or 8)
     DBuf<unsigned long long> counters;
     DBuf<int> flag, it;
     DBuf<double> objs;
@@ -232,8 +233,8 @@ static void finish_matrix(Ctx* c) {
     c->C.swap(vout);
     kout.release();
     c->cub_tmp.release();
-    c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>(((c->Ml + c->fg - 1) / c->fg + 7) / 8, (uint64_t)c->sms * 16));
-    c->nblk_col = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->N + 7) / 8, (uint64_t)c->sms * 16));
+    c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>(((c->Ml + 31) / 32 + 7) / 8, (uint64_t)c->sms * 8));
+    c->nblk_col = (int)std::max<uint64_t>(1, std::min<uint64_t>(((c->N + 31) / 32 + 7) / 8, (uint64_t)c->sms * 8));
     c->partial.alloc(std::max(c->nblk_row, 1024));
     c->scal.alloc(8);
     c->zrow.alloc(c->Ml + 1);
@@ -312,7 +313,10 @@ static void need_data(Ctx* c) { if (!c->have_data) throw ContractError("wamgpu: 
 
 static void back_into(Ctx* c, const float* w, double* out) {
     c->timer_begin(T_BACK);
-    k_back<0><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
+    if (c->unroll == 4)
+        k_back<0, 4><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
+    else
+        k_back<0, 8><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
     check_launch(c);
     c->timer_end(T_BACK);
     c->tm.back_launches++;
@@ -321,14 +325,12 @@ static void back_into(Ctx* c, const float* w, double* out) {
 // q = I0 exp(-H mu), objective -> scal[0] (all-reduced), record
 static void forward_fused(Ctx* c, bool record) {
     c->timer_begin(T_FWD);
-    switch (c->fg) {
-        case 1: k_forward<1, 1><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p,
-                                                                c->q.p, nullptr, c->partial.p, c->flag.p); break;
-        case 2: k_forward<1, 2><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p,
-                                                                c->q.p, nullptr, c->partial.p, c->flag.p); break;
-        default: k_forward<1, 4><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p,
-                                                                 c->q.p, nullptr, c->partial.p, c->flag.p); break;
-    }
+    if (c->unroll == 4)
+        k_forward<1, 4><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, c->q.p,
+                                                       nullptr, c->partial.p, c->flag.p);
+    else
+        k_forward<1, 8><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, c->q.p,
+                                                       nullptr, c->partial.p, c->flag.p);
     check_launch(c);
     c->timer_end(T_FWD);
     c->tm.fwd_launches++;
@@ -354,14 +356,33 @@ static double device_max(Ctx* c, const double* v, uint64_t n) {
     return m;
 }
 
-// Z0 = max_y sum_{z active} |phi(y|z)| (Eq. 1.61); AM: levels = 0 -> row sums.
-static double compute_z0(Ctx* c, int levels) {
-    if (c->Ml) {
-        c->wcnt.ensure(c->Ml + 1);
-        k_walk<0><<<blocks_for(c->Ml + 1, 32 * WALK_WARPS), 32 * WALK_WARPS, 0, c->st>>>(
-            c->Ml, c->rp.p, c->A.p, c->nx, c->ny, levels, c->act.p, c->off, c->zrow.p, c->wcnt.p, nullptr, nullptr,
-            nullptr);
-        check_launch(c);
+template <int MODE>
+static void launch_walk(Ctx* c, int L, unsigned long long* cnt, const unsigned long long* pos, unsigned* keys,
+                        uint2* vals) {
+    const unsigned nb = blocks_for(c->Ml + 1, 32 * WALK_WARPS);
+#define WALK_CASE(LV)                                                                                        \
+    case LV:                                                                                                 \
+        k_walk<MODE, LV><<<nb, 32 * WALK_WARPS, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->act.p, \
+                                                             c->off, c->zA.p, c->zrow.p, cnt, pos, keys, vals); \
+        break;
+    switch (L) {
+        WALK_CASE(0) WALK_CASE(1) WALK_CASE(2) WALK_CASE(3) WALK_CASE(4) WALK_CASE(5)
+        default: throw ConfigError("haar: depth beyond the device walk");
+    }
+#undef WALK_CASE
+    check_launch(c);
+}
+
+// Z0 = max_y sum_{z active} |phi(y|z)| (Eq. 1.61).  init: the approximation part
+// (tree-independent, cached in zA); AM: levels = 0 -> row sums.
+static double compute_z0(Ctx* c, int levels, bool init) {
+    c->wcnt.ensure(c->Ml + 1);
+    c->zA.ensure(c->Ml + 1);
+    if (init) {
+        CK(cudaMemsetAsync(c->wcnt.p, 0, (c->Ml + 1) * 8, c->st));
+        if (c->Ml) launch_walk<0>(c, levels, nullptr, nullptr, nullptr, nullptr);
+    } else if (c->Ml) {
+        launch_walk<1>(c, levels, c->wcnt.p, nullptr, nullptr, nullptr);
     }
     double z0 = device_max(c, c->zrow.p, c->Ml);
     if (!(z0 > 0.0)) throw NumericError("Z0: no ray intersects the active set");
@@ -445,7 +466,7 @@ static void am_init(Ctx* c, const double* init_mu) {
     back_into(c, c->d.p, c->bam.p);  // b(x) = sum_y d(y) h(y|x)
     allreduce_sum(c, c->bam.p, c->N);
     if (!c->act.p) { c->act.alloc(1); }
-    c->Z0 = compute_z0(c, 0);        // Z0 = max_y sum_x h(y|x)
+    c->Z0 = compute_z0(c, 0, true);  // Z0 = max_y sum_x h(y|x)
     forward_fused(c, false);
     CK(cudaMemsetAsync(c->counters.p, 0, 16, c->st));
     CK(cudaEventRecord(c->ev_t0, c->st));
@@ -461,7 +482,7 @@ static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
     for (int i = 0; i < n; ++i) {
         if (c->nranks == 1) {
             c->timer_begin(T_BACK);
-            k_back<1><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, c->q.p, nullptr, c->bam.p, c->mu.p,
+            k_back<1, 8><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, c->q.p, nullptr, c->bam.p, c->mu.p,
                                                       c->Z0, c->flag.p);
             check_launch(c);
             c->timer_end(T_BACK);
@@ -534,10 +555,7 @@ static void rebuild_phi(Ctx* c) {
     c->kin_s.ensure(std::max<uint64_t>(tot, 1));
     c->vin_s.ensure(std::max<uint64_t>(tot, 1));
     if (tot) {
-        k_walk<2><<<blocks_for(c->Ml + 1, 32 * WALK_WARPS), 32 * WALK_WARPS, 0, c->st>>>(
-            c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->L, c->act.p, c->off, nullptr, nullptr, c->wcnt.p, c->kin_s.p,
-            c->vin_s.p);
-        check_launch(c);
+        launch_walk<2>(c, c->L, nullptr, c->wcnt.p, c->kin_s.p, c->vin_s.p);
     }
     DBuf<uint2> vout;
     sort_pairs(c, c->kin_s, c->vin_s, c->kout_s, vout, tot, c->N);
@@ -594,7 +612,7 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     allreduce_sum(c, c->g.p, N);
     tile_launch(c, 2, nullptr, c->bdata.p);
     CK(cudaMemsetAsync(c->g.p, 0, 2 * N * 8, c->st));
-    c->Z0 = compute_z0(c, L);
+    c->Z0 = compute_z0(c, L, true);
     c->nlist = 0;
     c->nnz_phi = 0;
     rebuild_phi(c);
@@ -657,7 +675,7 @@ static int64_t wam_expand(Ctx* c, double factor) {
         for (uint64_t i = 0; i < c->act_bytes; ++i) newly += (h[i] != 0) - (c->act_host[i] != 0);
         c->act_host.swap(h);
         if (newly > 0) {
-            c->Z0 = compute_z0(c, c->L);
+            c->Z0 = compute_z0(c, c->L, false);
             rebuild_phi(c);
             c->active = count_active(c);
         }
@@ -697,7 +715,7 @@ static Ctx* create(int device) {
     CK(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10) throw CudaError("wamgpu: requires an sm_100a (Blackwell) device");
     c->sms = prop.multiProcessorCount;
-    if (const char* e = std::getenv("WAMGPU_FG")) c->fg = std::max(1, std::min(4, std::atoi(e)));
+    if (const char* e = std::getenv("WAMGPU_UNROLL")) c->unroll = std::atoi(e) == 4 ? 4 : 8;
     CK(cudaEventCreate(&c->ev_t0));
     CK(cudaEventCreate(&c->ev_a));
     CK(cudaEventCreate(&c->ev_b));
@@ -868,7 +886,7 @@ int wamgpu_forward_project(wamgpu_ctx* ctx, const double* mu, double* l) {
         std::vector<float> m(c->N);
         for (uint64_t x = 0; x < c->N; ++x) m[x] = (float)mu[x];
         CK(cudaMemcpyAsync(c->fscratch.p, m.data(), c->N * 4, cudaMemcpyHostToDevice, c->st));
-        k_forward<0, 1><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->fscratch.p, nullptr, nullptr,
+        k_forward<0, 8><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->fscratch.p, nullptr, nullptr,
                                                     nullptr, c->dscratch.p, nullptr, c->flag.p);
         check_launch(c);
         CK(cudaMemcpyAsync(l, c->dscratch.p, c->Ml * 8, cudaMemcpyDeviceToHost, c->st));
@@ -1043,7 +1061,7 @@ int wamgpu_get_z_rows(wamgpu_ctx* ctx, double* zrow) {
         NEED(ctx); NEED(zrow);
         Ctx* c = ctx;
         need_matrix(c);
-        if (c->algo == 2) compute_z0(c, c->L); else compute_z0(c, 0);
+        if (c->algo == 2) compute_z0(c, c->L, false); else compute_z0(c, 0, true);
         CK(cudaMemcpyAsync(zrow, c->zrow.p, c->Ml * 8, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
     })
