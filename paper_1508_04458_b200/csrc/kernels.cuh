@@ -162,16 +162,22 @@ template <int UNROLL>
 __device__ __forceinline__ double stream_rows(const uint2* __restrict__ A, const float* __restrict__ x,
                                               const unsigned long long* __restrict__ ptr, uint64_t y0, int nr,
                                               int lane) {
-    const unsigned long long myp = (lane <= nr) ? __ldg(ptr + y0 + lane) : 0ull;
-    const uint64_t k0 = __shfl_sync(0xffffffffu, myp, 0), k1 = __shfl_sync(0xffffffffu, myp, nr);
+    // lane j holds ptr[y0+j] (j < nr); the end pointer ptr[y0+nr] is loaded
+    // uniformly (nr may be 32, beyond the lanes)
+    const unsigned long long myp = (lane < nr) ? __ldg(ptr + y0 + lane) : 0ull;
+    const uint64_t k0 = __shfl_sync(0xffffffffu, myp, 0), k1 = __ldg(ptr + y0 + nr);
+    auto row_end = [&](int rr) -> uint64_t {  // end of row rr (warp-uniform rr)
+        const uint64_t t = __shfl_sync(0xffffffffu, myp, rr + 1 < 32 ? rr + 1 : 31);
+        return (rr + 1 < nr) ? t : k1;
+    };
     int r = 0;
-    uint64_t rs = k0, nb = __shfl_sync(0xffffffffu, myp, 1 < nr ? 1 : nr);
+    uint64_t rs = k0, nb = row_end(0);
     double acc = 0.0, mine = 0.0;
     // close leading empty rows
     while (r < nr && nb <= rs) {
         if (lane == r) mine = 0.0;
         ++r;
-        nb = __shfl_sync(0xffffffffu, myp, r + 1 < nr ? r + 1 : nr);
+        nb = row_end(r);
     }
     uint2 ec[UNROLL];
 #pragma unroll
@@ -206,7 +212,7 @@ __device__ __forceinline__ double stream_rows(const uint2* __restrict__ A, const
             acc = 0.0;
             rs = nb;
             ++r;
-            nb = __shfl_sync(0xffffffffu, myp, r + 1 < nr ? r + 1 : nr);
+            nb = row_end(r);
         }
         if (r < nr) {
 #pragma unroll

@@ -6,4 +6,4 @@ WAMGPU_UNROLL=$u timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-basel
 python -c "import json;d=json.loads(open('gpurun_out/bench_cfg2_u$u.log').read().strip().splitlines()[-1]);print(d['value'],d['e2e']['value'],json.dumps(d['kernels']))"
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/launches_cfg2.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu rc=$?"
-python scripts/launches.py gpurun_out/launches_cfg2.csv | head -12
+python scripts/launches.py gpurun_out/launches_cfg2.csv > gpurun_out/launches_cfg2.txt; head -14 gpurun_out/launches_cfg2.txt
