@@ -243,7 +243,6 @@ def main():
         ctx.set_comm(uid, rank, world)
     ctx.set_geometry(g)
     ctx.set_data(d, I0)
-    nnz_total = int(plumb.max(0) if False else 0)  # placeholder for clarity
     nnz_local = ctx.nnz
 
     def step_device():
@@ -266,6 +265,7 @@ def main():
     dev_ms, fwd_ms, back_ms, launches = [], [], [], 0
     fwd_n = back_n = 0
     split_ms = upd_ms = exp_ms = comm_ms = 0.0
+    split_nnz = 0
     plumb.barrier()
     with ClockSampler(local) as clk:
         t_wall = time.perf_counter()
@@ -282,6 +282,7 @@ def main():
                 upd_ms += t["update_ms"]
                 exp_ms += t["expand_ms"]
                 comm_ms += t["comm_ms"]
+                split_nnz = t["split_nnz"]
         wall = time.perf_counter() - t_wall
     plumb.barrier()
     ms_step = plumb.max(sum(dev_ms) / len(dev_ms))
@@ -349,6 +350,8 @@ def main():
                        "parallelism": f"views/{world}"},
             "ray_voxel_updates_per_s": 2 * nnz * J / (ms_step * 1e-3),
             "final_objective": final_obj,
+            "tree": {"active_set_by_iteration": sorted({r["active_set"] for r in recs}),
+                     "coefficients": N, "phi_minus_nnz": split_nnz},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
                          "algorithmic_bytes": fwd_bytes if "forward" in dom else back_bytes},

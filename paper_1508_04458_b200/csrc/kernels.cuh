@@ -149,97 +149,67 @@ __device__ __forceinline__ double idiv_term(double d, double q) {
     return (d > 0.0 ? d * log(d / q) : 0.0) - d + q;
 }
 
-// Warp-cooperative sparse dot products of 32 consecutive rows (or columns)
-// [y0, y0+nr): row r = sum_{k in [ptr[y0+r], ptr[y0+r+1])} h_k x[idx_k].  The
-// warp streams the rows' contiguous entry range in rounds of 32*UNROLL entries
-// (predicated 8-byte streaming loads); the loads of round i+1 are issued
-// before the gathers of round i, so the pipeline never drains at row
-// boundaries and a warp keeps ~2*UNROLL*256 B in flight.  Row boundaries that
-// fall inside a round are closed with masked partial sums.  fp64 accumulation
-// (fp32 x fp32 products are exact in fp64), fixed lane-partial + xor-butterfly
-// order (deterministic).  Returns row (lane)'s value in lane `lane` (lane < nr).
-template <int UNROLL>
-__device__ __forceinline__ double stream_rows(const uint2* __restrict__ A, const float* __restrict__ x,
-                                              const unsigned long long* __restrict__ ptr, uint64_t y0, int nr,
-                                              int lane) {
-    // lane j holds ptr[y0+j] (j < nr); the end pointer ptr[y0+nr] is loaded
-    // uniformly (nr may be 32, beyond the lanes)
-    const unsigned long long myp = (lane < nr) ? __ldg(ptr + y0 + lane) : 0ull;
-    const uint64_t k0 = __shfl_sync(0xffffffffu, myp, 0), k1 = __ldg(ptr + y0 + nr);
-    auto row_end = [&](int rr) -> uint64_t {  // end of row rr (warp-uniform rr)
-        const uint64_t t = __shfl_sync(0xffffffffu, myp, rr + 1 < 32 ? rr + 1 : 31);
-        return (rr + 1 < nr) ? t : k1;
-    };
-    int r = 0;
-    uint64_t rs = k0, nb = row_end(0);
-    double acc = 0.0, mine = 0.0;
-    // close leading empty rows
-    while (r < nr && nb <= rs) {
-        if (lane == r) mine = 0.0;
-        ++r;
-        nb = row_end(r);
-    }
+// Warp-cooperative segmented sparse dot products over a contiguous entry range
+// [lo, hi) holding G consecutive segments (rows or columns) split at b[0..G-2]:
+// out[g] = sum over segment g of h_k x[idx_k].  Software-pipelined: the
+// UNROLL predicated 8-byte streaming loads of round r+1 are issued before the
+// gathers of round r, so a warp keeps ~2*UNROLL*256 B in flight and pays about
+// one memory latency per 256*UNROLL/32 entries, across segment boundaries.
+// fp64 accumulation (products of two fp32 are exact in fp64); segment
+// selection is by predicated fma with h=0 (an exact no-op); fixed
+// xor-butterfly reduction (deterministic).
+constexpr int UNROLL = 8;
+template <int G>
+__device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
+                                        const uint64_t (&b)[G > 1 ? G - 1 : 1], uint64_t hi, int lane,
+                                        double (&out)[G]) {
+    double acc[G][2];
+#pragma unroll
+    for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = 0.0;
     uint2 ec[UNROLL];
+    uint64_t base = lo + lane;
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-        const uint64_t k = k0 + lane + 32 * u;
-        ec[u] = (k < k1) ? ld_stream(A + k) : make_uint2(0u, 0u);
+        const uint64_t k = base + 32 * u;
+        ec[u] = (k < hi) ? ld_stream(A + k) : make_uint2(0u, 0u);
     }
-    for (uint64_t b0 = k0; b0 < k1; b0 += 32 * UNROLL) {
+    for (; base < hi; base += 32 * UNROLL) {
         uint2 en[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
-            const uint64_t k = b0 + 32 * UNROLL + lane + 32 * u;
-            en[u] = (k < k1) ? ld_stream(A + k) : make_uint2(0u, 0u);
+            const uint64_t k = base + 32 * (UNROLL + u);
+            en[u] = (k < hi) ? ld_stream(A + k) : make_uint2(0u, 0u);
         }
         float v[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(x + ec[u].x);
-        double p[UNROLL];
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) p[u] = hval(ec[u]) * (double)v[u];
-        const uint64_t re = b0 + 32 * UNROLL;
-        // rows that end inside this round
-        while (r < nr && nb <= re) {
-            double part = acc;
+        for (int u = 0; u < UNROLL; ++u) {
+            const double h = hval(ec[u]), xv = (double)v[u];
+            if (G == 1) {
+                acc[0][u & 1] = fma(h, xv, acc[0][u & 1]);
+            } else {
+                const uint64_t k = base + 32 * u;
+                int seg = 0;
 #pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
-                const uint64_t k = b0 + lane + 32 * u;
-                part += (k >= rs && k < nb) ? p[u] : 0.0;
-            }
-            const double tot = warp_sum(part);
-            if (lane == r) mine = tot;
-            acc = 0.0;
-            rs = nb;
-            ++r;
-            nb = row_end(r);
-        }
-        if (r < nr) {
+                for (int g = 0; g < G - 1; ++g) seg += (k >= b[g]);
 #pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
-                const uint64_t k = b0 + lane + 32 * u;
-                acc += (k >= rs) ? p[u] : 0.0;
+                for (int g = 0; g < G; ++g) acc[g][u & 1] = fma(seg == g ? h : 0.0, xv, acc[g][u & 1]);
             }
         }
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) ec[u] = en[u];
     }
-    // rows not closed inside the stream (trailing empty rows / last row)
-    while (r < nr) {
-        const double tot = warp_sum(acc);
-        if (lane == r) mine = tot;
-        acc = 0.0;
-        ++r;
-    }
-    return mine;
+#pragma unroll
+    for (int g = 0; g < G; ++g) out[g] = warp_sum(acc[g][0] + acc[g][1]);
 }
 
 // ------------------------------------------------------------ CSR forward
-// Warp task = 32 consecutive rays (contiguous CSR entries).  MODE 0: l = H mu
-// (forward_project, fp64 out).  MODE 1: fused Beer's law + I-divergence: the
-// 32 lanes finish their rays in parallel (q = fp32(I0 exp(-l)), coalesced),
-// and the per-block fp64 objective partial is summed in a fixed order.
-template <int MODE, int UNROLL>
+// Warp task = FG consecutive rays.  MODE 0: l = H mu as fp64 (forward_project).
+// MODE 1: fused Beer's law + I-divergence: q = fp32(I0 exp(-l)), per-block fp64
+// partial of the objective (deterministic block order).
+constexpr int FG = 2;  // rows per warp task in the forward kernel (measured best of 1/2/4)
+template <int MODE>
 __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long long* __restrict__ rp,
                                                  const uint2* __restrict__ A, const float* __restrict__ mu,
                                                  const float* __restrict__ I0, const float* __restrict__ d,
@@ -247,25 +217,37 @@ __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long
                                                  double* __restrict__ partial, int* __restrict__ flag) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t ntask = (M + 31) / 32;
+    const uint64_t ntask = (M + FG - 1) / FG;
     double tacc = 0.0;
     for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; t < ntask; t += W) {
-        const uint64_t y0 = t * 32;
-        const int nr = (int)((M - y0) < 32 ? (M - y0) : 32);
-        const double l = stream_rows<UNROLL>(A, mu, rp, y0, nr, lane);
+        const uint64_t y0 = t * FG;
+        const int nr = (int)((M - y0) < (uint64_t)FG ? (M - y0) : (uint64_t)FG);
+        // row extents: lane j < nr+1 loads rp[y0+j]
+        const unsigned long long myrp = (lane <= nr) ? __ldg(rp + y0 + lane) : 0ull;
+        const uint64_t lo = __shfl_sync(0xffffffffu, myrp, 0), hi = __shfl_sync(0xffffffffu, myrp, nr);
+        uint64_t bnd[FG - 1];
+#pragma unroll
+        for (int g = 0; g < FG - 1; ++g) bnd[g] = __shfl_sync(0xffffffffu, myrp, min(g + 1, nr));
+        double l[FG];
+        seg_dot<FG>(A, mu, lo, bnd, hi, lane, l);
+        // lane g finishes row y0+g: Beer's law, I-divergence term
+        double lg = l[0];
+#pragma unroll
+        for (int g = 1; g < FG; ++g) lg = (lane == g) ? l[g] : lg;
         if (lane < nr) {
             const uint64_t y = y0 + lane;
-            if (!isfinite(l)) atomicOr(flag, 1);
+            if (!isfinite(lg)) atomicOr(flag, 1);
             if (MODE == 0) {
-                lout[y] = l;
+                lout[y] = lg;
             } else {
-                const double qq = (double)I0[y] * exp(-l);
+                const double qq = (double)I0[y] * exp(-lg);
                 q[y] = (float)qq;
                 tacc += idiv_term((double)d[y], qq);
             }
         }
     }
     if (MODE == 1) {
+        // deterministic block partial: lanes, then warps, in fixed order
         __shared__ double s[32];
         double v = tacc;
 #pragma unroll
@@ -281,24 +263,22 @@ __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long
 }
 
 // ------------------------------------------------------------- CSC back
-// Warp task = 32 consecutive voxels: g(x) = sum_y h(y|x) w(y) in fp64 over each
-// voxel's CSC column (voxel-driven gather, no atomics).
+// Warp per voxel: g(x) = sum_y h(y|x) w(y) in fp64 over the voxel's CSC column.
 // MODE 0: write g (fp64).  MODE 1: fused AM update:
 // mu <- max(0, mu + ln(g/b)/Z0) where b > 0 and g > 0, otherwise frozen.
-template <int MODE, int UNROLL>
+template <int MODE>
 __global__ void __launch_bounds__(256) k_back(uint64_t N, const unsigned long long* __restrict__ cp,
                                               const uint2* __restrict__ C, const float* __restrict__ w,
                                               double* __restrict__ g, const double* __restrict__ bam,
                                               float* __restrict__ mu, double Z0, int* __restrict__ flag) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t ntask = (N + 31) / 32;
-    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; t < ntask; t += W) {
-        const uint64_t x0 = t * 32;
-        const int nr = (int)((N - x0) < 32 ? (N - x0) : 32);
-        const double c = stream_rows<UNROLL>(C, w, cp, x0, nr, lane);
-        if (lane < nr) {
-            const uint64_t x = x0 + lane;
+    for (uint64_t x = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; x < N; x += W) {
+        const uint64_t nob[1] = {0};
+        double cc[1];
+        seg_dot<1>(C, w, cp[x], nob, cp[x + 1], lane, cc);
+        const double c = cc[0];
+        if (lane == 0) {
             if (MODE == 0) {
                 g[x] = c;
             } else {

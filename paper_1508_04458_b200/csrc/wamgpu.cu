@@ -105,7 +105,6 @@ struct wamgpu_ctx {
     double Z0 = 0.0;
     DBuf<double> scal, partial;
     int nblk_row = 1, nblk_col = 1;
-    int unroll = 8;  // SpMV pipeline depth (WAMGPU_UNROLL: 4 or 8)
     DBuf<unsigned long long> counters;
     DBuf<int> flag, it;
     DBuf<double> objs;
@@ -172,7 +171,7 @@ static int bits_for(uint64_t n) {
 static void sort_pairs(Ctx* c, DBuf<unsigned>& kin, DBuf<uint2>& vin, DBuf<unsigned>& kout, DBuf<uint2>& vout,
                        uint64_t n, uint64_t maxkey) {
     kout.ensure(std::max<uint64_t>(n, 1));
-    vout.alloc(std::max<uint64_t>(n, 1));
+    vout.ensure(std::max<uint64_t>(n, 1));
     if (n == 0) return;
     const int bits = bits_for(maxkey);
     auto vi = reinterpret_cast<unsigned long long*>(vin.p);
@@ -233,8 +232,8 @@ static void finish_matrix(Ctx* c) {
     c->C.swap(vout);
     kout.release();
     c->cub_tmp.release();
-    c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>(((c->Ml + 31) / 32 + 7) / 8, (uint64_t)c->sms * 8));
-    c->nblk_col = (int)std::max<uint64_t>(1, std::min<uint64_t>(((c->N + 31) / 32 + 7) / 8, (uint64_t)c->sms * 8));
+    c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>(((c->Ml + FG - 1) / FG + 7) / 8, (uint64_t)c->sms * 16));
+    c->nblk_col = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->N + 7) / 8, (uint64_t)c->sms * 16));
     c->partial.alloc(std::max(c->nblk_row, 1024));
     c->scal.alloc(8);
     c->zrow.alloc(c->Ml + 1);
@@ -313,10 +312,7 @@ static void need_data(Ctx* c) { if (!c->have_data) throw ContractError("wamgpu: 
 
 static void back_into(Ctx* c, const float* w, double* out) {
     c->timer_begin(T_BACK);
-    if (c->unroll == 4)
-        k_back<0, 4><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
-    else
-        k_back<0, 8><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
+    k_back<0><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
     check_launch(c);
     c->timer_end(T_BACK);
     c->tm.back_launches++;
@@ -325,12 +321,8 @@ static void back_into(Ctx* c, const float* w, double* out) {
 // q = I0 exp(-H mu), objective -> scal[0] (all-reduced), record
 static void forward_fused(Ctx* c, bool record) {
     c->timer_begin(T_FWD);
-    if (c->unroll == 4)
-        k_forward<1, 4><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, c->q.p,
-                                                       nullptr, c->partial.p, c->flag.p);
-    else
-        k_forward<1, 8><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, c->q.p,
-                                                       nullptr, c->partial.p, c->flag.p);
+    k_forward<1><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, c->q.p, nullptr,
+                                                c->partial.p, c->flag.p);
     check_launch(c);
     c->timer_end(T_FWD);
     c->tm.fwd_launches++;
@@ -482,7 +474,7 @@ static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
     for (int i = 0; i < n; ++i) {
         if (c->nranks == 1) {
             c->timer_begin(T_BACK);
-            k_back<1, 8><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, c->q.p, nullptr, c->bam.p, c->mu.p,
+            k_back<1><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, c->q.p, nullptr, c->bam.p, c->mu.p,
                                                       c->Z0, c->flag.p);
             check_launch(c);
             c->timer_end(T_BACK);
@@ -557,12 +549,10 @@ static void rebuild_phi(Ctx* c) {
     if (tot) {
         launch_walk<2>(c, c->L, nullptr, c->wcnt.p, c->kin_s.p, c->vin_s.p);
     }
-    DBuf<uint2> vout;
-    sort_pairs(c, c->kin_s, c->vin_s, c->kout_s, vout, tot, c->N);
+    sort_pairs(c, c->kin_s, c->vin_s, c->kout_s, c->E, tot, c->N);
     c->np.ensure(c->N + 1);
     k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(c->kout_s.p, tot, c->N, c->np.p);
     check_launch(c);
-    c->E.swap(vout);
     c->nnz_phi = tot;
     CK(cudaStreamSynchronize(c->st));
 }
@@ -715,7 +705,6 @@ static Ctx* create(int device) {
     CK(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10) throw CudaError("wamgpu: requires an sm_100a (Blackwell) device");
     c->sms = prop.multiProcessorCount;
-    if (const char* e = std::getenv("WAMGPU_UNROLL")) c->unroll = std::atoi(e) == 4 ? 4 : 8;
     CK(cudaEventCreate(&c->ev_t0));
     CK(cudaEventCreate(&c->ev_a));
     CK(cudaEventCreate(&c->ev_b));
@@ -886,7 +875,7 @@ int wamgpu_forward_project(wamgpu_ctx* ctx, const double* mu, double* l) {
         std::vector<float> m(c->N);
         for (uint64_t x = 0; x < c->N; ++x) m[x] = (float)mu[x];
         CK(cudaMemcpyAsync(c->fscratch.p, m.data(), c->N * 4, cudaMemcpyHostToDevice, c->st));
-        k_forward<0, 8><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->fscratch.p, nullptr, nullptr,
+        k_forward<0><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->fscratch.p, nullptr, nullptr,
                                                     nullptr, c->dscratch.p, nullptr, c->flag.p);
         check_launch(c);
         CK(cudaMemcpyAsync(l, c->dscratch.p, c->Ml * 8, cudaMemcpyDeviceToHost, c->st));
