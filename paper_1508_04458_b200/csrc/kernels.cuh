@@ -707,6 +707,120 @@ __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsi
     }
 }
 
+// Expansion walk, one WARP PER LEVEL (blockDim = 32 L): the L warps of a block
+// share the same 32 rays (thread = ray), whose rows are staged once per
+// 32-entry round in shared memory by all L warps (cp.async).  Because every
+// block's phi comes from its own quadrant sums, levels are
+// independent: warp l tracks only level-l blocks, accumulates quadrant sums
+// only inside ACTIVE blocks (tree bits in shared memory), and on block exit
+// adds |phi| to its per-ray level total (MODE 1) or emits negative fp32 phi
+// (MODE 2).  Per-ray results are combined in the fixed order
+//   Z(y) = zA[y] + tot_L + ... + tot_1
+// (bit-identical to the oracle).  cnt / pos are per (ray, level): index y*L + l-1.
+template <int MODE, int L>
+__global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned long long* __restrict__ rp,
+                                                    const uint2* __restrict__ A, int nx, int ny,
+                                                    const unsigned* __restrict__ tbits, ActOff boff, int tree_words,
+                                                    const double* __restrict__ zA, double* __restrict__ zrow,
+                                                    unsigned long long* __restrict__ cnt,
+                                                    const unsigned long long* __restrict__ pos,
+                                                    unsigned* __restrict__ keys, uint2* __restrict__ vals) {
+    extern __shared__ unsigned tsm[];   // tree bits (tree_words words)
+    __shared__ uint2 buf[32][33];
+    __shared__ unsigned long long s_lo[32], s_len[32];
+    __shared__ double s_tot[L][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, l = w + 1;
+    for (int i = threadIdx.x; i < tree_words; i += blockDim.x) tsm[i] = tbits[i];
+    const uint64_t y = (uint64_t)blockIdx.x * 32 + lane;
+    if (w == 0) {
+        uint64_t lo = 0, hi = 0;
+        if (y < M) { lo = rp[y]; hi = rp[y + 1]; }
+        s_lo[lane] = lo;
+        s_len[lane] = hi - lo;
+    }
+    __syncthreads();
+    unsigned long long maxlen = s_len[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    const unsigned long long len = s_len[lane];
+    const bool pow2 = (nx & (nx - 1)) == 0;
+    const int lgx = 31 - __clz(nx);
+    const int wl = nx >> l, hl = ny >> l;
+    const unsigned bo = (unsigned)boff.off[l];
+    const double sc = 1.0 / (double)(1 << l);
+
+    int cur = -1, cbi = 0, cbj = 0;
+    bool av = false;
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, tot = 0.0;
+    unsigned long long count = 0, wp = 0;
+    if (MODE == 2 && y < M) wp = pos[y * L + (l - 1)];
+
+    auto flush = [&]() {
+        if (av) {
+            const double st = q0 + q1, sb = q2 + q3;
+            const double pH = (st - sb) * sc, pV = ((q0 + q2) - (q1 + q3)) * sc, pD = ((q0 + q3) - (q1 + q2)) * sc;
+            if (MODE == 1) tot += fabs(pH) + fabs(pV) + fabs(pD);
+            const float v[3] = {(float)pH, (float)pV, (float)pD};
+            const unsigned z[3] = {(unsigned)((hl + cbi) * nx + cbj), (unsigned)(cbi * nx + wl + cbj),
+                                   (unsigned)((hl + cbi) * nx + wl + cbj)};
+#pragma unroll
+            for (int s = 0; s < 3; ++s)
+                if (v[s] < 0.0f) {
+                    if (MODE == 1) ++count;
+                    else { keys[wp] = z[s]; vals[wp] = make_uint2((unsigned)y, __float_as_uint(v[s])); ++wp; }
+                }
+        }
+        q0 = q1 = q2 = q3 = 0.0;
+    };
+
+    for (unsigned long long base = 0; base < maxlen; base += 32) {
+        // all L warps stage the 32 rays' entries [base, base+32)
+        for (int j = w; j < 32; j += L) {
+            const unsigned long long nj = s_len[j];
+            const bool ok = base + lane < nj;
+            cp_async8(&buf[j][lane], A + (ok ? s_lo[j] + base + lane : 0), ok);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        const int n = (int)min(32ull, len > base ? len - base : 0ull);
+        for (int i = 0; i < n; ++i) {
+            const uint2 e = buf[lane][i];
+            int ix, iy;
+            if (pow2) { ix = (int)(e.x & (unsigned)(nx - 1)); iy = (int)(e.x >> lgx); }
+            else { iy = (int)(e.x / (unsigned)nx); ix = (int)(e.x % (unsigned)nx); }
+            const int bi = iy >> l, bj = ix >> l;
+            const int key = bi * wl + bj;
+            if (key != cur) {
+                flush();
+                cur = key; cbi = bi; cbj = bj;
+                const unsigned bit = bo + (unsigned)key;
+                av = (tsm[bit >> 5] >> (bit & 31)) & 1u;
+            }
+            if (av) {
+                const double h = hval(e);
+                const int quad = (((iy >> (l - 1)) & 1) << 1) | ((ix >> (l - 1)) & 1);
+                q0 += quad == 0 ? h : 0.0;
+                q1 += quad == 1 ? h : 0.0;
+                q2 += quad == 2 ? h : 0.0;
+                q3 += quad == 3 ? h : 0.0;
+            }
+        }
+        __syncthreads();
+    }
+    flush();
+    if (MODE == 1) {
+        s_tot[l - 1][lane] = tot;
+        if (y < M) cnt[y * L + (l - 1)] = count;
+        __syncthreads();
+        if (w == 0 && y < M) {
+            double z = zA[y];
+#pragma unroll
+            for (int k = L; k >= 1; --k) z += s_tot[k - 1][lane];
+            zrow[y] = z;
+        }
+    }
+}
+
 // Signed split (K5): warp per active detail coefficient,
 // b-(z) = sum over its Phi^- column of q(y) phi(y|z) in fp64.
 __global__ void __launch_bounds__(256) k_split(uint64_t nlist, const unsigned* __restrict__ list,

@@ -95,6 +95,9 @@ struct wamgpu_ctx {
     DBuf<uint2> vin_s;
     int L = 0;
     DBuf<uint8_t> act, act_new;
+    DBuf<unsigned> tbits;               // bit-packed tree for the expansion walk
+    ActOff boff{};                      // bit offset of level l in tbits
+    int tree_words = 0;
     ActOff off{};
     uint64_t act_bytes = 0;
     std::vector<uint8_t> act_host;
@@ -365,16 +368,60 @@ static void launch_walk(Ctx* c, int L, unsigned long long* cnt, const unsigned l
     check_launch(c);
 }
 
+
+static void upload_tree_bits(Ctx* c) {
+    // host act_host -> bit-packed, levels at 32-bit aligned bit offsets
+    std::vector<unsigned> w;
+    uint64_t bit = 0;
+    for (int l = 0; l <= LMAX + 1; ++l) c->boff.off[l] = 0;
+    for (int l = 1; l <= c->L; ++l) {
+        c->boff.off[l] = bit;
+        const uint64_t n = (uint64_t)(c->nx >> l) * (c->ny >> l);
+        const uint8_t* a = c->act_host.data() + c->off.off[l];
+        w.resize((bit + n + 31) / 32 + 1, 0u);
+        for (uint64_t i = 0; i < n; ++i)
+            if (a[i]) w[(bit + i) >> 5] |= 1u << ((bit + i) & 31);
+        bit = (bit + n + 31) / 32 * 32;
+    }
+    if (w.empty()) w.push_back(0u);
+    c->tree_words = (int)w.size();
+    c->tbits.ensure(w.size());
+    CK(cudaMemcpyAsync(c->tbits.p, w.data(), w.size() * 4, cudaMemcpyHostToDevice, c->st));
+}
+
+template <int MODE>
+static void launch_walk_lv(Ctx* c, unsigned long long* cnt, const unsigned long long* pos, unsigned* keys,
+                           uint2* vals) {
+    const unsigned nb = blocks_for(c->Ml, 32);
+    const size_t smem = (size_t)c->tree_words * 4;
+    if (smem > 160 * 1024) throw ConfigError("tree too large for the shared-memory walk");
+#define LV_CASE(LV)                                                                                              \
+    case LV: {                                                                                                   \
+        auto kf = k_walk_lv<MODE, LV>;                                                                           \
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        kf<<<nb, 32 * LV, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->tbits.p, c->boff, c->tree_words, \
+                                         c->zA.p, c->zrow.p, cnt, pos, keys, vals);                               \
+    } break;
+    switch (c->L) {
+        LV_CASE(1) LV_CASE(2) LV_CASE(3) LV_CASE(4) LV_CASE(5)
+        default: throw ConfigError("haar: depth beyond the device walk");
+    }
+#undef LV_CASE
+    check_launch(c);
+}
+
 // Z0 = max_y sum_{z active} |phi(y|z)| (Eq. 1.61).  init: the approximation part
 // (tree-independent, cached in zA); AM: levels = 0 -> row sums.
 static double compute_z0(Ctx* c, int levels, bool init) {
-    c->wcnt.ensure(c->Ml + 1);
+    const uint64_t ncnt = (uint64_t)c->Ml * std::max(levels, 1) + 1;
+    c->wcnt.ensure(ncnt);
     c->zA.ensure(c->Ml + 1);
     if (init) {
-        CK(cudaMemsetAsync(c->wcnt.p, 0, (c->Ml + 1) * 8, c->st));
+        CK(cudaMemsetAsync(c->wcnt.p, 0, ncnt * 8, c->st));
         if (c->Ml) launch_walk<0>(c, levels, nullptr, nullptr, nullptr, nullptr);
     } else if (c->Ml) {
-        launch_walk<1>(c, levels, c->wcnt.p, nullptr, nullptr, nullptr);
+        upload_tree_bits(c);
+        launch_walk_lv<1>(c, c->wcnt.p, nullptr, nullptr, nullptr);
     }
     double z0 = device_max(c, c->zrow.p, c->Ml);
     if (!(z0 > 0.0)) throw NumericError("Z0: no ray intersects the active set");
@@ -540,14 +587,16 @@ static void rebuild_phi(Ctx* c) {
         CK(cudaMemcpyAsync(c->list.p, lst.data(), lst.size() * 4, cudaMemcpyHostToDevice, c->st));
     // Phi^- CSC over local rays: counts (from the Z0 walk of this tree) -> scan
     // -> emit -> stable radix sort by z (rays stay ascending within a column)
-    exclusive_scan_u64(c, c->wcnt.p, c->Ml + 1);
+    const uint64_t ncnt = c->L > 0 ? (uint64_t)c->Ml * c->L : c->Ml;
+    CK(cudaMemsetAsync(c->wcnt.p + ncnt, 0, 8, c->st));
+    exclusive_scan_u64(c, c->wcnt.p, ncnt + 1);
     unsigned long long tot = 0;
-    CK(cudaMemcpyAsync(&tot, c->wcnt.p + c->Ml, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&tot, c->wcnt.p + ncnt, 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     c->kin_s.ensure(std::max<uint64_t>(tot, 1));
     c->vin_s.ensure(std::max<uint64_t>(tot, 1));
     if (tot) {
-        launch_walk<2>(c, c->L, nullptr, c->wcnt.p, c->kin_s.p, c->vin_s.p);
+        launch_walk_lv<2>(c, nullptr, c->wcnt.p, c->kin_s.p, c->vin_s.p);
     }
     sort_pairs(c, c->kin_s, c->vin_s, c->kout_s, c->E, tot, c->N);
     c->np.ensure(c->N + 1);
