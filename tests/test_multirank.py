@@ -1,0 +1,99 @@
+"""World-size-2 gloo tests of the view-sharded 2D algebra, on
+CPU: each rank owns a contiguous block of views (CSR rows), computes partial
+back projections / signed splits over its rows, and an all-reduce SUM makes the
+replicated coefficient update identical to the single-rank result.  The
+partition rule is the one libwamgpu.so uses (wamgpu.cu set_geometry)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def view_range(V, rank, nranks):
+    """libwamgpu.so: v0 = V*rank/P, v1 = V*(rank+1)/P (integer division)."""
+    return V * rank // nranks, V * (rank + 1) // nranks
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    from oracle import oracle as O
+    from wam_testutil import problem_inputs
+    cfg, p, mu_true, I0, d = problem_inputs("tiny", O, None)
+    rp, ci, v = p.csr()
+    D = cfg["detectors"]
+    v0, v1 = view_range(cfg["views"], rank, world)
+    r0, r1 = v0 * D, v1 * D
+    # one AM iteration, sharded: partial H^T q and H^T d over own rows, all-reduce
+    q = I0 * np.exp(-p.forward_project(np.zeros(p.N)))
+    def partial_back(w):
+        g = np.zeros(p.N)
+        for y in range(r0, r1):
+            sl = slice(int(rp[y]), int(rp[y + 1]))
+            np.add.at(g, ci[sl].astype(np.int64), v[sl] * w[y])
+        return g
+    gq = torch.from_numpy(partial_back(q))
+    gd = torch.from_numpy(partial_back(d))
+    dist.all_reduce(gq)
+    dist.all_reduce(gd)
+    # objective partial over own rows, all-reduced
+    obj = torch.tensor([float(np.sum(q[r0:r1] - d[r0:r1] + d[r0:r1] * np.log(np.where(d[r0:r1] > 0, d[r0:r1] / q[r0:r1], 1.0))))],
+                       dtype=torch.float64)
+    dist.all_reduce(obj)
+    # Z0 partial max over own rows, all-reduced MAX
+    rs = np.array([v[int(rp[y]):int(rp[y + 1])].sum() for y in range(r0, r1)] or [0.0])
+    z0 = torch.tensor([rs.max()], dtype=torch.float64)
+    dist.all_reduce(z0, op=dist.ReduceOp.MAX)
+    out[rank] = (gq.numpy().copy(), gd.numpy().copy(), float(obj.item()), float(z0.item()), (r0, r1))
+    dist.destroy_process_group()
+
+
+def test_view_partition_covers_rows_once():
+    for V in (180, 720, 7):
+        for P in (1, 2, 3, 4, 8):
+            rng = [view_range(V, r, P) for r in range(P)]
+            assert rng[0][0] == 0 and rng[-1][1] == V
+            assert all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
+
+
+def test_two_rank_sharded_am_step_matches_single_rank():
+    from oracle import oracle as O
+    from wam_testutil import problem_inputs
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.start_processes(_worker, args=(world, port, out), nprocs=world, join=True, start_method="fork")
+    cfg, p, mu_true, I0, d = problem_inputs("tiny", O, None)
+    q = I0 * np.exp(-p.forward_project(np.zeros(p.N)))
+    g_ref = p.back_project(q)
+    b_ref = p.back_project(d)
+    for r in range(world):
+        gq, gd, obj, z0, rows = out[r]
+        assert np.allclose(gq, g_ref, rtol=1e-12, atol=0)
+        assert np.allclose(gd, b_ref, rtol=1e-12, atol=0)
+        assert abs(obj - O.i_divergence(d, q)) <= 1e-9 * abs(obj)
+    # replicated update is identical on both ranks (same all-reduced inputs)
+    assert np.array_equal(out[0][0], out[1][0]) and out[0][3] == out[1][3]
+    p.am_init(d, I0)
+    assert out[0][3] == p.am_get()["Z0"]
+    # the replicated multiplicative AM update from the all-reduced sums equals
+    # the single-rank oracle's first iterate
+    gq, gd = out[0][0], out[0][1]
+    z0 = out[0][3]
+    mu = np.where((gd > 0) & (gq > 0), np.maximum(0.0, np.log(np.where(gd > 0, gq / np.where(gd > 0, gd, 1), 1)) / z0), 0.0)
+    p.am_iterate(1)
+    assert np.allclose(mu, p.am_get()["mu"], rtol=1e-10, atol=1e-14)
