@@ -173,6 +173,7 @@ class Context:
         _chk(lib.wamgpu_create(int(device), C.byref(h)))
         self.h = h
         self.M = self.N = self.nnz = self.row0 = self.row1 = None
+        self.nz = 1
 
     def close(self):
         if getattr(self, "h", None):
@@ -205,10 +206,12 @@ class Context:
         """build_system_matrix (projector.hpp:126-148) on the device."""
         _chk(load().wamgpu_set_geometry(self.h, C.byref(g)), self.h)
         self.geom = g
+        self.nz = g.nz
         self._info()
 
     def set_grid(self, nx, ny, nz=1):
         _chk(load().wamgpu_set_grid(self.h, int(nx), int(ny), int(nz)), self.h)
+        self.nz = nz
 
     def set_matrix_csr(self, row_ptr, col_idx, values, cols):
         """SystemMatrix(rows, cols, row_ptr, col_idx, values) (system_matrix.hpp:24-35)."""
@@ -238,13 +241,13 @@ class Context:
     # ---- core-model
     def forward_project(self, mu):
         mu = np.ascontiguousarray(mu, np.float64)
-        out = np.empty(self.row1 - self.row0)
+        out = np.empty((self.row1 - self.row0) * self.nz)
         _chk(load().wamgpu_forward_project(self.h, _p(mu), _p(out)), self.h)
         return out
 
     def back_project(self, w):
         w = np.ascontiguousarray(w, np.float64)
-        out = np.empty(self.N)
+        out = np.empty(self.N * self.nz)
         _chk(load().wamgpu_back_project(self.h, _p(w), _p(out)), self.h)
         return out
 
@@ -288,17 +291,17 @@ class Context:
 
     # ---- state
     def image(self):
-        out = np.empty(self.N)
+        out = np.empty(self.N * self.nz)
         _chk(load().wamgpu_get_image(self.h, _p(out)), self.h)
         return out
 
     def beta(self):
-        out = np.empty(self.N)
+        out = np.empty(self.N * self.nz)
         _chk(load().wamgpu_get_beta(self.h, _p(out)), self.h)
         return out
 
     def q(self):
-        out = np.empty(self.row1 - self.row0)
+        out = np.empty((self.row1 - self.row0) * self.nz)
         _chk(load().wamgpu_get_q(self.h, _p(out)), self.h)
         return out
 
@@ -310,7 +313,8 @@ class Context:
         return out[: n.value]
 
     def stats(self):
-        b, bp, bm = np.empty(self.N), np.empty(self.N), np.empty(self.N)
+        n = self.N * self.nz
+        b, bp, bm = np.empty(n), np.empty(n), np.empty(n)
         _chk(load().wamgpu_get_stats(self.h, _p(b), _p(bp), _p(bm)), self.h)
         return b, bp, bm
 

@@ -105,6 +105,10 @@ CONFIGS = {
                  phantom="bag"),
     "small": dict(nx=64, ny=64, nz=1, voxel=2.0, views=90, detectors=128, I0=1e5, L=3, J=16, seed=12,
                   phantom="bag"),
+    "tiny3d": dict(nx=32, ny=32, nz=8, voxel=4.0, views=60, detectors=64, I0=1e5, L=3, J=12, seed=21,
+                   phantom="luggage"),
+    "small3d": dict(nx=64, ny=64, nz=40, voxel=4.0, views=72, detectors=96, I0=2e5, L=3, J=10, seed=22,
+                    phantom="luggage"),
     "small_lug": dict(nx=128, ny=128, nz=1, voxel=2.0, views=120, detectors=192, I0=2e5, L=4, J=20, seed=13,
                       phantom="luggage"),
 }

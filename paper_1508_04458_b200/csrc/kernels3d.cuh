@@ -1,0 +1,259 @@
+// kernels3d.cuh — the axial 3D stack (nz > 1 slices sharing one in-plane
+// system matrix, geometry.hpp:17-20; pin P2).
+//
+// Every ray y of the in-plane matrix is traced once and reused for all nz
+// slices, so each projector pass is a sparse-matrix x dense-slab product:
+// one WARP per in-plane ray (forward) or voxel (back), the matrix entry is a
+// warp-uniform (broadcast) load and the lanes cover the slices of a z-fastest
+// slab (SPL slices per lane: nz <= 32 SPL), so every gather is one coalesced
+// nz*4-byte segment.  Device layouts: mu3/beta3 [x][s] fp32, q3/d3/I03 [y][s]
+// fp32, g3/bdata3/bm3 [z][s] fp64.  The boundary transposes to the reference
+// layouts (image.hpp:14 (z*ny+iy)*nx+ix, rays z*M+y).
+#pragma once
+#include "kernels.cuh"
+
+namespace wamgpu {
+
+template <int SPL>
+struct SliceVec { float v[SPL]; };
+
+template <int SPL>
+__device__ __forceinline__ void load_slices(const float* __restrict__ p, int nz, int lane, float (&out)[SPL]) {
+    const int s0 = lane * SPL;
+    if (SPL == 2 && s0 + 1 < nz) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(p + s0));
+        out[0] = t.x; out[SPL > 1 ? 1 : 0] = t.y;
+        return;
+    }
+    if (SPL == 4 && s0 + 3 < nz) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p + s0));
+        out[0] = t.x; out[SPL > 1 ? 1 : 0] = t.y; out[SPL > 2 ? 2 : 0] = t.z; out[SPL > 3 ? 3 : 0] = t.w;
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) out[j] = (s0 + j < nz) ? __ldg(p + s0 + j) : 0.0f;
+}
+
+// Slab SpMV of one row/column: acc[j] = sum_k h_k x[idx_k * nz + lane*SPL + j].
+// The row's entries are read 8 at a time (uniform loads, all in flight), then
+// their 8 slab gathers, then the fp64 fmas.
+template <int SPL>
+__device__ __forceinline__ void slab_dot(const uint2* __restrict__ A, const float* __restrict__ x, int nz,
+                                         uint64_t lo, uint64_t hi, int lane, double (&acc)[SPL]) {
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) acc[j] = 0.0;
+    constexpr int U = 8;
+    uint64_t k = lo;
+    for (; k + U <= hi; k += U) {
+        uint2 e[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) e[u] = __ldg(A + k + u);
+        float v[U][SPL];
+#pragma unroll
+        for (int u = 0; u < U; ++u) load_slices<SPL>(x + (uint64_t)e[u].x * nz, nz, lane, v[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const double h = hval(e[u]);
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) acc[j] = fma(h, (double)v[u][j], acc[j]);
+        }
+    }
+    for (; k < hi; ++k) {
+        const uint2 e = __ldg(A + k);
+        float v[SPL];
+        load_slices<SPL>(x + (uint64_t)e.x * nz, nz, lane, v);
+        const double h = hval(e);
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) acc[j] = fma(h, (double)v[j], acc[j]);
+    }
+}
+
+// K2 3D: l[y][s] = sum_x h(y|x) mu[x][s]; MODE 0 writes l (fp64, [y][s]);
+// MODE 1 fuses q = fp32(I0 exp(-l)) and the fp64 I-divergence partial.
+template <int MODE, int SPL>
+__global__ void __launch_bounds__(256) k_forward3(uint64_t M, int nz, const unsigned long long* __restrict__ rp,
+                                                  const uint2* __restrict__ A, const float* __restrict__ mu,
+                                                  const float* __restrict__ I0, const float* __restrict__ d,
+                                                  float* __restrict__ q, double* __restrict__ lout,
+                                                  double* __restrict__ partial, int* __restrict__ flag) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    double tacc = 0.0;
+    for (uint64_t y = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; y < M; y += W) {
+        double acc[SPL];
+        slab_dot<SPL>(A, mu, nz, rp[y], rp[y + 1], lane, acc);
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+            const int s = lane * SPL + j;
+            if (s >= nz) continue;
+            const uint64_t id = y * nz + s;
+            if (!isfinite(acc[j])) atomicOr(flag, 1);
+            if (MODE == 0) {
+                lout[id] = acc[j];
+            } else {
+                const double qq = (double)I0[id] * exp(-acc[j]);
+                q[id] = (float)qq;
+                tacc += idiv_term((double)d[id], qq);
+            }
+        }
+    }
+    if (MODE == 1) {
+        __shared__ double sm[32];
+        double v = tacc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) sm[wib] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sm[w];
+            partial[blockIdx.x] = t;
+        }
+    }
+}
+
+// K3 3D: g[x][s] = sum_y h(y|x) w[y][s] over the voxel's CSC column (no
+// atomics).  MODE 0: g (fp64).  MODE 1: fused AM update of mu[x][s]
+// (SPEC.md:303, 316-317).  Voxels are visited in 2D tile order (`order`) so the
+// concurrently processed columns share rays and the q-slab gathers hit L2.
+template <int MODE, int SPL>
+__global__ void __launch_bounds__(256) k_back3(uint64_t N, int nz, const unsigned* __restrict__ order,
+                                               const unsigned long long* __restrict__ cp, const uint2* __restrict__ C,
+                                               const float* __restrict__ w, double* __restrict__ g,
+                                               const double* __restrict__ bam, float* __restrict__ mu, double Z0,
+                                               int* __restrict__ flag) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < N; i += W) {
+        const uint64_t x = order ? order[i] : i;
+        double acc[SPL];
+        slab_dot<SPL>(C, w, nz, cp[x], cp[x + 1], lane, acc);
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+            const int s = lane * SPL + j;
+            if (s >= nz) continue;
+            const uint64_t id = x * nz + s;
+            if (MODE == 0) {
+                g[id] = acc[j];
+            } else {
+                const double b = bam[id], c = acc[j];
+                if (b > 0.0 && c > 0.0) {
+                    const double v = (double)mu[id] + log(c / b) / Z0;
+                    if (!isfinite(v)) atomicOr(flag, 2);
+                    mu[id] = (float)((0.0 < v) ? v : 0.0);
+                }
+            }
+        }
+    }
+}
+
+// K5 3D: b-[z][s] = sum over the (slice-shared) Phi^- column of z of q[y][s] phi.
+template <int SPL>
+__global__ void __launch_bounds__(256) k_split3(uint64_t nlist, int nz, const unsigned* __restrict__ list,
+                                                const unsigned long long* __restrict__ ptr,
+                                                const uint2* __restrict__ E, const float* __restrict__ q,
+                                                double* __restrict__ bm) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlist; i += W) {
+        const unsigned z = list[i];
+        double acc[SPL];
+        slab_dot<SPL>(E, q, nz, ptr[z], ptr[z + 1], lane, acc);
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+            const int s = lane * SPL + j;
+            if (s < nz) bm[(uint64_t)z * nz + s] = acc[j];
+        }
+    }
+}
+
+// Haar tiles of a slab: one CTA per (2^L x 2^L tile, chunk of SC slices).
+// Same per-2x2 operation order as k_tile, per slice.
+// mode 0: synthesis beta -> mu (and mu64); mode 1: analysis + root solve +
+// synthesis; mode 2: analysis only (g -> out).
+constexpr int SC3 = 8;  // slices per CTA
+__global__ void k_tile3(int mode, int nx, int ny, int nz, int L, const double* __restrict__ g,
+                        const double* __restrict__ bm, const double* __restrict__ bdata,
+                        const uint8_t* __restrict__ act, ActOff off, float* __restrict__ beta,
+                        float* __restrict__ mu, double* __restrict__ mu64, double* __restrict__ out,
+                        double* __restrict__ bp_out, double* __restrict__ bm_out, double Z0,
+                        unsigned long long* __restrict__ counters, int* __restrict__ flag) {
+    extern __shared__ double sm3[];
+    const int TS = 1 << L, T2 = TS * TS;
+    const int ti = blockIdx.y, tj = blockIdx.x, s0 = blockIdx.z * SC3;
+    const int ns = min(SC3, nz - s0);
+    double* xs = sm3;                 // [SC3][T2]
+    double* ts = sm3 + SC3 * T2;      // scratch
+    const uint64_t base = (uint64_t)ti * TS * nx + (uint64_t)tj * TS;
+    // load: voxel-major, slices contiguous (coalesced over the slice chunk)
+    if (mode != 0) {
+        for (int i = threadIdx.x; i < T2 * ns; i += blockDim.x) {
+            const int v = i / ns, s = i % ns;
+            xs[s * T2 + v] = g[(base + (uint64_t)(v / TS) * nx + v % TS) * nz + s0 + s];
+        }
+        __syncthreads();
+        for (int s = 0; s < ns; ++s) tile_fwd(xs + s * T2, ts, TS, L);
+    }
+    if (mode == 2) {
+        for (int i = threadIdx.x; i < T2 * ns; i += blockDim.x) {
+            const int v = i / ns, s = i % ns;
+            CoefInfo ci = coef_info(v / TS, v % TS, ti, tj, L, nx, ny, act, off);
+            out[ci.z * nz + s0 + s] = xs[s * T2 + v];
+        }
+        return;
+    }
+    unsigned long long upd = 0, deg = 0;
+    for (int i = threadIdx.x; i < T2 * ns; i += blockDim.x) {
+        const int v = i / ns, s = i % ns;
+        CoefInfo ci = coef_info(v / TS, v % TS, ti, tj, L, nx, ny, act, off);
+        const uint64_t zid = ci.z * nz + s0 + s;
+        float bo = beta[zid];
+        if (mode == 1) {
+            const double bmv = ci.approx ? 0.0 : bm[zid];
+            const double bpv = xs[s * T2 + v] - bmv;
+            if (bp_out) { bp_out[zid] = bpv; bm_out[zid] = bmv; }
+            if (ci.active) {
+                double nb;
+                const int r = solve_update(bdata[zid], bpv, bmv, Z0, (double)bo, &nb);
+                if (r == 0) {
+                    if (!isfinite(nb)) atomicOr(flag, 4);
+                    bo = (float)nb;
+                    beta[zid] = bo;
+                    ++upd;
+                } else if (r == 2) {
+                    ++deg;
+                }
+            }
+        }
+        xs[s * T2 + v] = (double)bo;
+    }
+    if (mode == 1) {
+        for (int o = 16; o > 0; o >>= 1) {
+            upd += __shfl_xor_sync(0xffffffffu, upd, o);
+            deg += __shfl_xor_sync(0xffffffffu, deg, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (upd) atomicAdd(counters + 0, upd);
+            if (deg) atomicAdd(counters + 1, deg);
+        }
+    }
+    __syncthreads();
+    for (int s = 0; s < ns; ++s) tile_inv(xs + s * T2, ts, TS, L);
+    for (int i = threadIdx.x; i < T2 * ns; i += blockDim.x) {
+        const int v = i / ns, s = i % ns;
+        const uint64_t p = (base + (uint64_t)(v / TS) * nx + v % TS) * nz + s0 + s;
+        mu[p] = (float)xs[s * T2 + v];
+        if (mu64) mu64[p] = xs[s * T2 + v];
+    }
+}
+
+// z-summed criterion image: s(p) = sum_s mu64[p][s] in slice order.
+__global__ void k_zsum(uint64_t N, int nz, const double* __restrict__ mu64, double* __restrict__ out) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    double s = 0.0;
+    for (int k = 0; k < nz; ++k) s += mu64[p * nz + k];
+    out[p] = s;
+}
+
+}  // namespace wamgpu

@@ -26,6 +26,7 @@
 #include "../../include/wamgpu.h"
 #include "host_model.hpp"
 #include "kernels.cuh"
+#include "kernels3d.cuh"
 
 namespace wamgpu {
 
@@ -79,6 +80,8 @@ struct wamgpu_ctx {
     int nx = 0, ny = 0, nz = 1;
     bool have_grid = false, have_matrix = false;
     uint64_t M = 0, N = 0, row0 = 0, row1 = 0, Ml = 0, nnz = 0;
+    int s0 = 0, nzl = 1;                // local z-slab [s0, s0+nzl) of an axial 3D stack (nz > 1)
+    DBuf<unsigned> order;               // 3D back projection: voxels in 16x16 tile order
     DBuf<unsigned long long> rp, cp;
     DBuf<uint2> A, C;
     // data
@@ -237,7 +240,7 @@ static void finish_matrix(Ctx* c) {
     c->cub_tmp.release();
     c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>(((c->Ml + FG - 1) / FG + 7) / 8, (uint64_t)c->sms * 16));
     c->nblk_col = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->N + 7) / 8, (uint64_t)c->sms * 16));
-    c->partial.alloc(std::max(c->nblk_row, 1024));
+    c->partial.alloc(std::max<size_t>(std::max(c->nblk_row, 1024), (size_t)c->sms * 16));
     c->scal.alloc(8);
     c->zrow.alloc(c->Ml + 1);
     CK(cudaStreamSynchronize(c->st));
@@ -245,18 +248,49 @@ static void finish_matrix(Ctx* c) {
     c->algo = 0;
 }
 
+// Sharding: a 2D problem (nz == 1) shards VIEWS (contiguous
+// CSR rows, row = v*D + k, projector.hpp:123-125); an axial 3D stack shards
+// z-SLABS (every rank holds the whole in-plane matrix, rays never leave their
+// slice, geometry.hpp:17-20).
+static void partition(Ctx* c, int views, int detectors) {
+    if (c->nz > 128) throw ConfigError("wamgpu: at most 128 slices per GPU slab");
+    if (c->nz == 1) {
+        const int v0 = (int)((int64_t)views * c->rank / c->nranks), v1 = (int)((int64_t)views * (c->rank + 1) / c->nranks);
+        c->row0 = (uint64_t)v0 * detectors;
+        c->row1 = (uint64_t)v1 * detectors;
+        c->s0 = 0;
+        c->nzl = 1;
+    } else {
+        c->row0 = 0;
+        c->row1 = c->M;
+        c->s0 = (int)((int64_t)c->nz * c->rank / c->nranks);
+        c->nzl = (int)((int64_t)c->nz * (c->rank + 1) / c->nranks) - c->s0;
+        if (c->nzl < 1) throw ConfigError("wamgpu: more ranks than slices");
+    }
+    c->Ml = c->row1 - c->row0;
+}
+
+static void build_tile_order(Ctx* c) {
+    if (c->nz == 1) return;
+    std::vector<unsigned> o;
+    o.reserve(c->N);
+    const int T = 16;
+    for (int ty = 0; ty < c->ny; ty += T)
+        for (int tx = 0; tx < c->nx; tx += T)
+            for (int iy = ty; iy < std::min(ty + T, c->ny); ++iy)
+                for (int ix = tx; ix < std::min(tx + T, c->nx); ++ix) o.push_back((unsigned)(iy * c->nx + ix));
+    c->order.ensure(c->N);
+    CK(cudaMemcpyAsync(c->order.p, o.data(), c->N * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+}
+
 static void set_geometry(Ctx* c, const wamgpu_geometry& g) {
     validate(g);
-    if (g.nz != 1) throw ConfigError("wamgpu: device path supports nz == 1 (2D slices) in this build");
     std::vector<RayD> rays = ray_table(g);
-    const int V = g.views, D = g.detectors;
-    const int v0 = (int)((int64_t)V * c->rank / c->nranks), v1 = (int)((int64_t)V * (c->rank + 1) / c->nranks);
     c->nx = g.nx; c->ny = g.ny; c->nz = g.nz; c->have_grid = true;
-    c->M = (uint64_t)V * D;
+    c->M = (uint64_t)g.views * g.detectors;
     c->N = (uint64_t)g.nx * g.ny;
-    c->row0 = (uint64_t)v0 * D;
-    c->row1 = (uint64_t)v1 * D;
-    c->Ml = c->row1 - c->row0;
+    partition(c, g.views, g.detectors);
     DBuf<RayDev> dr;
     dr.alloc(std::max<uint64_t>(c->Ml, 1));
     if (c->Ml)
@@ -275,6 +309,7 @@ static void set_geometry(Ctx* c, const wamgpu_geometry& g) {
         check_launch(c);
     }
     finish_matrix(c);
+    build_tile_order(c);
 }
 
 static void set_matrix_csr(Ctx* c, uint64_t rows, uint64_t cols, uint64_t nnz, const uint64_t* rp,
@@ -287,9 +322,17 @@ static void set_matrix_csr(Ctx* c, uint64_t rows, uint64_t cols, uint64_t nnz, c
         throw ContractError("SystemMatrix: cols != nx*ny of the grid");
     c->M = rows;
     c->N = cols;
-    c->row0 = rows * c->rank / c->nranks;
-    c->row1 = rows * (c->rank + 1) / c->nranks;
-    c->Ml = c->row1 - c->row0;
+    if (!c->have_grid) { c->nx = (int)cols; c->ny = 1; c->nz = 1; }
+    // explicit matrices shard by contiguous row blocks (2D) or by z-slab (3D)
+    if (c->nz == 1) {
+        c->row0 = rows * c->rank / c->nranks;
+        c->row1 = rows * (c->rank + 1) / c->nranks;
+        c->Ml = c->row1 - c->row0;
+        c->s0 = 0;
+        c->nzl = 1;
+    } else {
+        partition(c, (int)rows, 1);
+    }
     const uint64_t k0 = rp[c->row0], k1 = rp[c->row1];
     c->nnz = k1 - k0;
     std::vector<unsigned long long> lrp(c->Ml + 1);
@@ -305,31 +348,76 @@ static void set_matrix_csr(Ctx* c, uint64_t rows, uint64_t cols, uint64_t nnz, c
     c->A.alloc(std::max<uint64_t>(c->nnz, 1));
     CK(cudaMemcpyAsync(c->rp.p, lrp.data(), (c->Ml + 1) * 8, cudaMemcpyHostToDevice, c->st));
     if (c->nnz) CK(cudaMemcpyAsync(c->A.p, ent.data(), c->nnz * 8, cudaMemcpyHostToDevice, c->st));
-    if (!c->have_grid) { c->nx = (int)cols; c->ny = 1; c->nz = 1; }
     finish_matrix(c);
+    build_tile_order(c);
 }
 
 // ------------------------------------------------------------- pipeline steps
 static void need_matrix(Ctx* c) { if (!c->have_matrix) throw ContractError("wamgpu: no system matrix set"); }
 static void need_data(Ctx* c) { if (!c->have_data) throw ContractError("wamgpu: no transmission data set"); }
 
-static void back_into(Ctx* c, const float* w, double* out) {
+static int spl_of(const Ctx* c) { return c->nzl <= 32 ? 1 : (c->nzl <= 64 ? 2 : 4); }
+static unsigned nblk_warp(const Ctx* c, uint64_t n) {
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, (uint64_t)c->sms * 16));
+}
+
+// g = H^T w (fp64).  2D: CSC gather; 3D: slab gather over the tile-ordered voxels.
+// am != nullptr: fused AM update of mu instead of writing g.
+static void back_launch(Ctx* c, const float* w, double* out, const double* bam) {
     c->timer_begin(T_BACK);
-    k_back<0><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
+    if (c->nzl == 1) {
+        if (bam) k_back<1><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, nullptr, bam, c->mu.p, c->Z0, c->flag.p);
+        else k_back<0><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
+    } else {
+        const unsigned nb = nblk_warp(c, c->N);
+#define B3(S)                                                                                                     \
+    if (bam) k_back3<1, S><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p, w, nullptr, bam,     \
+                                                  c->mu.p, c->Z0, c->flag.p);                                     \
+    else k_back3<0, S><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p, w, out, nullptr, nullptr, \
+                                              0.0, c->flag.p);
+        switch (spl_of(c)) { case 1: B3(1) break; case 2: B3(2) break; default: B3(4) break; }
+#undef B3
+    }
     check_launch(c);
     c->timer_end(T_BACK);
     c->tm.back_launches++;
+}
+static void back_into(Ctx* c, const float* w, double* out) { back_launch(c, w, out, nullptr); }
+
+// plain l = H mu (fp64 out), for forward_project
+static void forward_plain(Ctx* c, const float* mu, double* l) {
+    if (c->nzl == 1) {
+        k_forward<0><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, mu, nullptr, nullptr, nullptr, l, nullptr,
+                                                    c->flag.p);
+    } else {
+        const unsigned nb = nblk_warp(c, c->Ml);
+#define F3(S) k_forward3<0, S><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu, nullptr, nullptr, nullptr, \
+                                                      l, nullptr, c->flag.p);
+        switch (spl_of(c)) { case 1: F3(1) break; case 2: F3(2) break; default: F3(4) break; }
+#undef F3
+    }
+    check_launch(c);
 }
 
 // q = I0 exp(-H mu), objective -> scal[0] (all-reduced), record
 static void forward_fused(Ctx* c, bool record) {
     c->timer_begin(T_FWD);
-    k_forward<1><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, c->q.p, nullptr,
-                                                c->partial.p, c->flag.p);
+    int nparts = c->nblk_row;
+    if (c->nzl == 1) {
+        k_forward<1><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, c->q.p, nullptr,
+                                                    c->partial.p, c->flag.p);
+    } else {
+        const unsigned nb = std::min<unsigned>(nblk_warp(c, c->Ml), (unsigned)c->partial.n);
+        nparts = (int)nb;
+#define F3(S) k_forward3<1, S><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, \
+                                                      c->q.p, nullptr, c->partial.p, c->flag.p);
+        switch (spl_of(c)) { case 1: F3(1) break; case 2: F3(2) break; default: F3(4) break; }
+#undef F3
+    }
     check_launch(c);
     c->timer_end(T_FWD);
     c->tm.fwd_launches++;
-    k_sum_partials<<<1, 1024, 0, c->st>>>(c->partial.p, c->nblk_row, c->scal.p);
+    k_sum_partials<<<1, 1024, 0, c->st>>>(c->partial.p, nparts, c->scal.p);
     check_launch(c);
     allreduce_sum(c, c->scal.p, 1);
     if (record) {
@@ -487,23 +575,42 @@ static void fill_records(Ctx* c, int n, wamgpu_record* recs, int64_t active_at_s
     }
 }
 
+// ---- boundary layout conversion: reference image/coefficient layout
+// ((s0+s)*N + x, image.hpp:14) <-> device slab [x][s]; rays (s*M + y) <-> [y][s].
+static uint64_t NV(const Ctx* c) { return c->N * (uint64_t)c->nzl; }
+static uint64_t MV(const Ctx* c) { return c->Ml * (uint64_t)c->nzl; }
+template <class T>
+static void upload_slab(Ctx* c, const double* ref, T* dev, uint64_t n_inner, uint64_t ref_stride, uint64_t ref_off,
+                        bool local = false) {
+    std::vector<T> h(std::max<uint64_t>(n_inner * c->nzl, 1));
+    const int sb = local ? 0 : c->s0;
+    for (int s = 0; s < c->nzl; ++s)
+        for (uint64_t i = 0; i < n_inner; ++i) h[i * c->nzl + s] = (T)ref[(uint64_t)(sb + s) * ref_stride + ref_off + i];
+    CK(cudaMemcpyAsync(dev, h.data(), n_inner * c->nzl * sizeof(T), cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+}
+template <class T>
+static void download_slab(Ctx* c, const T* dev, double* ref, uint64_t n_inner, uint64_t ref_stride, uint64_t ref_off,
+                          bool local = false) {
+    std::vector<T> h(std::max<uint64_t>(n_inner * c->nzl, 1));
+    CK(cudaMemcpyAsync(h.data(), dev, n_inner * c->nzl * sizeof(T), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    const int sb = local ? 0 : c->s0;
+    for (int s = 0; s < c->nzl; ++s)
+        for (uint64_t i = 0; i < n_inner; ++i) ref[(uint64_t)(sb + s) * ref_stride + ref_off + i] = (double)h[i * c->nzl + s];
+}
+
 // ------------------------------------------------------------------ AM
 static void am_init(Ctx* c, const double* init_mu) {
     need_matrix(c);
     need_data(c);
-    c->mu.ensure(c->N);
-    c->g.ensure(2 * c->N);
-    c->bam.ensure(c->N);
-    if (init_mu) {
-        std::vector<float> m(c->N);
-        for (uint64_t x = 0; x < c->N; ++x) m[x] = (float)init_mu[x];
-        CK(cudaMemcpyAsync(c->mu.p, m.data(), c->N * 4, cudaMemcpyHostToDevice, c->st));
-        CK(cudaStreamSynchronize(c->st));
-    } else {
-        CK(cudaMemsetAsync(c->mu.p, 0, c->N * 4, c->st));
-    }
+    c->mu.ensure(NV(c));
+    c->g.ensure(2 * NV(c));
+    c->bam.ensure(NV(c));
+    if (init_mu) upload_slab<float>(c, init_mu, c->mu.p, c->N, c->N, 0);
+    else CK(cudaMemsetAsync(c->mu.p, 0, NV(c) * 4, c->st));
     back_into(c, c->d.p, c->bam.p);  // b(x) = sum_y d(y) h(y|x)
-    allreduce_sum(c, c->bam.p, c->N);
+    if (c->nzl == 1) allreduce_sum(c, c->bam.p, c->N);
     if (!c->act.p) { c->act.alloc(1); }
     c->Z0 = compute_z0(c, 0, true);  // Z0 = max_y sum_x h(y|x)
     forward_fused(c, false);
@@ -512,20 +619,15 @@ static void am_init(Ctx* c, const double* init_mu) {
     check_flag(c, "am_init");
     c->algo = 1;
     c->iter = 0;
-    c->active = (int64_t)c->N;
+    c->active = (int64_t)c->N * c->nz;
 }
 
 static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
     if (c->algo != 1) throw ContractError("am: not initialised");
     ensure_records(c, n);
     for (int i = 0; i < n; ++i) {
-        if (c->nranks == 1) {
-            c->timer_begin(T_BACK);
-            k_back<1><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, c->q.p, nullptr, c->bam.p, c->mu.p,
-                                                      c->Z0, c->flag.p);
-            check_launch(c);
-            c->timer_end(T_BACK);
-            c->tm.back_launches++;
+        if (c->nranks == 1 || c->nzl > 1) {
+            back_launch(c, c->q.p, nullptr, c->bam.p);   // fused multiplicative update
         } else {
             back_into(c, c->q.p, c->g.p);
             allreduce_sum(c, c->g.p, c->N);
@@ -548,8 +650,8 @@ static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
             recs[i].iter = c->iter - n + i + 1;
             recs[i].objective = o[i];
             recs[i].elapsed_s = ms * 1e-3;
-            recs[i].active_set = (int64_t)c->N;
-            recs[i].cum_updates = (int64_t)c->N * recs[i].iter;
+            recs[i].active_set = c->active;
+            recs[i].cum_updates = c->active * recs[i].iter;
         }
     }
 }
@@ -557,12 +659,22 @@ static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
 // ------------------------------------------------------------------ WAM
 static void tile_launch(Ctx* c, int mode, double* mu64, double* out) {
     const int TS = 1 << c->L;
-    dim3 grid(c->nx >> c->L, c->ny >> c->L);
-    const int bs = std::min(1024, std::max(32, TS * TS));
-    const size_t smem = 2ull * TS * TS * sizeof(double);
-    k_tile<<<grid, bs, smem, c->st>>>(mode, c->nx, c->ny, c->L, c->g.p, c->g.p + c->N, c->bdata.p, c->act.p, c->off,
-                                      c->beta.p, c->mu.p, mu64, out, c->bp_dbg.p, c->bm_dbg.p, c->Z0,
-                                      c->counters.p, c->flag.p);
+    if (c->nzl == 1) {
+        dim3 grid(c->nx >> c->L, c->ny >> c->L);
+        const int bs = std::min(1024, std::max(32, TS * TS));
+        const size_t smem = 2ull * TS * TS * sizeof(double);
+        k_tile<<<grid, bs, smem, c->st>>>(mode, c->nx, c->ny, c->L, c->g.p, c->g.p + c->N, c->bdata.p, c->act.p,
+                                          c->off, c->beta.p, c->mu.p, mu64, out, c->bp_dbg.p, c->bm_dbg.p, c->Z0,
+                                          c->counters.p, c->flag.p);
+    } else {
+        dim3 grid(c->nx >> c->L, c->ny >> c->L, (c->nzl + SC3 - 1) / SC3);
+        const size_t smem = (size_t)(SC3 + 1) * TS * TS * sizeof(double);
+        if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_tile3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_tile3<<<grid, 256, smem, c->st>>>(mode, c->nx, c->ny, c->nzl, c->L, c->g.p, c->g.p + NV(c), c->bdata.p,
+                                            c->act.p, c->off, c->beta.p, c->mu.p, mu64, out, c->bp_dbg.p,
+                                            c->bm_dbg.p, c->Z0, c->counters.p, c->flag.p);
+    }
     check_launch(c);
 }
 
@@ -623,7 +735,7 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     if (L < 0 || L > LMAX) throw ConfigError("haar: depth must be in [0, " + std::to_string(LMAX) + "]");
     if ((c->nx % (1 << L)) || (c->ny % (1 << L))) throw ConfigError("haar: slice dimensions not divisible by 2^L");
     c->L = L;
-    const uint64_t N = c->N;
+    const uint64_t N = NV(c);  // local slab of coefficients / voxels
     c->mu.ensure(N); c->beta.ensure(N); c->g.ensure(2 * N); c->bdata.ensure(N); c->mu64.ensure(N);
     c->bp_dbg.ensure(N); c->bm_dbg.ensure(N);
     CK(cudaMemsetAsync(c->g.p, 0, 2 * N * 8, c->st));
@@ -639,16 +751,13 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     CK(cudaMemsetAsync(c->act.p, 0, std::max<uint64_t>(o, 1), c->st));
     c->act_host.assign(o, 0);
     if (init_beta) {
-        std::vector<float> b(N);
-        for (uint64_t z = 0; z < N; ++z) b[z] = (float)init_beta[z];
-        CK(cudaMemcpyAsync(c->beta.p, b.data(), N * 4, cudaMemcpyHostToDevice, c->st));
-        CK(cudaStreamSynchronize(c->st));
+        upload_slab<float>(c, init_beta, c->beta.p, c->N, c->N, 0);
     } else {
         CK(cudaMemsetAsync(c->beta.p, 0, N * 4, c->st));
     }
     // b(z) = [Omega^T H^T d](z) for every z
     back_into(c, c->d.p, c->g.p);
-    allreduce_sum(c, c->g.p, N);
+    if (c->nzl == 1) allreduce_sum(c, c->g.p, N);
     tile_launch(c, 2, nullptr, c->bdata.p);
     CK(cudaMemsetAsync(c->g.p, 0, 2 * N * 8, c->st));
     c->Z0 = compute_z0(c, L, true);
@@ -670,12 +779,19 @@ static void wam_step(Ctx* c) {
     if (c->nlist) {
         c->timer_begin(T_SPLIT);
         const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist + 7) / 8, (uint64_t)c->sms * 16);
-        k_split<<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->np.p, c->E.p, c->q.p, c->g.p + c->N);
+        if (c->nzl == 1) {
+            k_split<<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->np.p, c->E.p, c->q.p, c->g.p + c->N);
+        } else {
+            double* bm3 = c->g.p + NV(c);
+#define S3(S) k_split3<S><<<nb, 256, 0, c->st>>>(c->nlist, c->nzl, c->list.p, c->np.p, c->E.p, c->q.p, bm3);
+            switch (spl_of(c)) { case 1: S3(1) break; case 2: S3(2) break; default: S3(4) break; }
+#undef S3
+        }
         check_launch(c);
         c->timer_end(T_SPLIT);
         c->tm.split_launches++;
     }
-    allreduce_sum(c, c->g.p, 2 * c->N);
+    if (c->nzl == 1) allreduce_sum(c, c->g.p, 2 * c->N);   // view shards: partial sums
     c->timer_begin(T_UPDATE);
     tile_launch(c, 1, nullptr, nullptr);
     c->timer_end(T_UPDATE);
@@ -699,12 +815,20 @@ static int64_t wam_expand(Ctx* c, double factor) {
     if (c->algo != 2) throw ContractError("wam: not initialised");
     c->timer_begin(T_EXPAND);
     tile_launch(c, 0, c->mu64.p, nullptr);         // fp64 criterion image Omega beta
-    const double mx = device_max(c, c->mu64.p, c->N);  // nz == 1: the z-sum is the slice
+    const double* crit = c->mu64.p;                // nz == 1: the z-sum is the slice
+    if (c->nzl > 1 || c->nz > 1) {                 // z-summed image, slabs all-reduced
+        c->dscratch.ensure(c->N);
+        k_zsum<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->nzl, c->mu64.p, c->dscratch.p);
+        check_launch(c);
+        allreduce_sum(c, c->dscratch.p, c->N);
+        crit = c->dscratch.p;
+    }
+    const double mx = device_max(c, crit, c->N);
     int64_t newly = 0;
     if (mx > 0.0 && c->L > 0) {
         const double thr = factor * mx;
         CK(cudaMemcpyAsync(c->act_new.p, c->act.p, c->act_bytes, cudaMemcpyDeviceToDevice, c->st));
-        k_mark<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->nx, c->ny, c->L, c->mu64.p, thr, c->act.p, c->act_new.p,
+        k_mark<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->nx, c->ny, c->L, crit, thr, c->act.p, c->act_new.p,
                                                           c->off);
         check_launch(c);
         c->act.swap(c->act_new);
@@ -859,7 +983,7 @@ int wamgpu_set_geometry(wamgpu_ctx* ctx, const wamgpu_geometry* g) {
 int wamgpu_set_grid(wamgpu_ctx* ctx, int nx, int ny, int nz) {
     API_TRY(ctx, {
         NEED(ctx);
-        if (nx < 1 || ny < 1 || nz != 1) throw ConfigError("set_grid: invalid grid (nz must be 1)");
+        if (nx < 1 || ny < 1 || nz < 1) throw ConfigError("set_grid: invalid grid");
         if (ctx->have_matrix && (uint64_t)nx * ny != ctx->N) throw ContractError("set_grid: nx*ny != matrix cols");
         ctx->nx = nx; ctx->ny = ny; ctx->nz = nz; ctx->have_grid = true;
     })
@@ -919,16 +1043,11 @@ int wamgpu_forward_project(wamgpu_ctx* ctx, const double* mu, double* l) {
         NEED(ctx); NEED(mu); NEED(l);
         need_matrix(ctx);
         Ctx* c = ctx;
-        c->fscratch.ensure(c->N);
-        c->dscratch.ensure(std::max<uint64_t>(c->Ml, 1));
-        std::vector<float> m(c->N);
-        for (uint64_t x = 0; x < c->N; ++x) m[x] = (float)mu[x];
-        CK(cudaMemcpyAsync(c->fscratch.p, m.data(), c->N * 4, cudaMemcpyHostToDevice, c->st));
-        k_forward<0><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->fscratch.p, nullptr, nullptr,
-                                                    nullptr, c->dscratch.p, nullptr, c->flag.p);
-        check_launch(c);
-        CK(cudaMemcpyAsync(l, c->dscratch.p, c->Ml * 8, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
+        c->fscratch.ensure(NV(c));
+        c->dscratch.ensure(std::max<uint64_t>(MV(c), 1));
+        upload_slab<float>(c, mu, c->fscratch.p, c->N, c->N, 0);
+        forward_plain(c, c->fscratch.p, c->dscratch.p);
+        download_slab<double>(c, c->dscratch.p, l, c->Ml, c->Ml, 0, true);
         check_flag(c, "forward_project");
     })
 }
@@ -938,15 +1057,12 @@ int wamgpu_back_project(wamgpu_ctx* ctx, const double* w, double* out) {
         NEED(ctx); NEED(w); NEED(out);
         need_matrix(ctx);
         Ctx* c = ctx;
-        c->fscratch.ensure(std::max<uint64_t>(c->Ml, 1));
-        c->dscratch.ensure(c->N);
-        std::vector<float> m(std::max<uint64_t>(c->Ml, 1));
-        for (uint64_t y = 0; y < c->Ml; ++y) m[y] = (float)w[y];
-        CK(cudaMemcpyAsync(c->fscratch.p, m.data(), c->Ml * 4, cudaMemcpyHostToDevice, c->st));
+        c->fscratch.ensure(std::max<uint64_t>(MV(c), 1));
+        c->dscratch.ensure(NV(c));
+        upload_slab<float>(c, w, c->fscratch.p, c->Ml, c->Ml, 0, true);
         back_into(c, c->fscratch.p, c->dscratch.p);
-        allreduce_sum(c, c->dscratch.p, c->N);
-        CK(cudaMemcpyAsync(out, c->dscratch.p, c->N * 8, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
+        if (c->nzl == 1) allreduce_sum(c, c->dscratch.p, c->N);
+        download_slab<double>(c, c->dscratch.p, out, c->N, c->N, 0);
     })
 }
 
@@ -955,20 +1071,18 @@ int wamgpu_set_data(wamgpu_ctx* ctx, const double* d, const double* I0) {
         NEED(ctx); NEED(d); NEED(I0);
         need_matrix(ctx);
         Ctx* c = ctx;
-        std::vector<float> fd(std::max<uint64_t>(c->Ml, 1)), fi(std::max<uint64_t>(c->Ml, 1));
-        for (uint64_t y = 0; y < c->Ml; ++y) {
-            const double dv = d[c->row0 + y], iv = I0[c->row0 + y];
-            if (!(dv >= 0.0)) throw ContractError("TransmissionData: d must be >= 0");
-            if (!(iv > 0.0)) throw ContractError("TransmissionData: I0 must be > 0");
-            fd[y] = (float)dv;
-            fi[y] = (float)iv;
-        }
-        c->d.alloc(std::max<uint64_t>(c->Ml, 1));
-        c->I0.alloc(std::max<uint64_t>(c->Ml, 1));
-        c->q.alloc(std::max<uint64_t>(c->Ml, 1));
-        CK(cudaMemcpyAsync(c->d.p, fd.data(), c->Ml * 4, cudaMemcpyHostToDevice, c->st));
-        CK(cudaMemcpyAsync(c->I0.p, fi.data(), c->Ml * 4, cudaMemcpyHostToDevice, c->st));
-        CK(cudaStreamSynchronize(c->st));
+        for (int s = 0; s < c->nzl; ++s)
+            for (uint64_t y = 0; y < c->Ml; ++y) {
+                const uint64_t id = (uint64_t)(c->s0 + s) * c->M + c->row0 + y;
+                if (!(d[id] >= 0.0)) throw ContractError("TransmissionData: d must be >= 0");
+                if (!(I0[id] > 0.0)) throw ContractError("TransmissionData: I0 must be > 0");
+            }
+        const uint64_t n = std::max<uint64_t>(MV(c), 1);
+        c->d.ensure(n);
+        c->I0.ensure(n);
+        c->q.ensure(n);
+        upload_slab<float>(c, d, c->d.p, c->Ml, c->M, c->row0);
+        upload_slab<float>(c, I0, c->I0.p, c->Ml, c->M, c->row0);
         c->have_data = true;
         c->algo = 0;
     })
@@ -1029,10 +1143,7 @@ int wamgpu_get_image(const wamgpu_ctx* ctx, double* mu) {
         NEED(ctx); NEED(mu);
         Ctx* c = const_cast<wamgpu_ctx*>(ctx);
         if (!c->algo) throw ContractError("get_image: no solver state");
-        std::vector<float> m(c->N);
-        CK(cudaMemcpyAsync(m.data(), c->mu.p, c->N * 4, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
-        for (uint64_t x = 0; x < c->N; ++x) mu[x] = m[x];
+        download_slab<float>(c, c->mu.p, mu, c->N, c->N, 0);
     })
 }
 
@@ -1041,10 +1152,7 @@ int wamgpu_get_beta(const wamgpu_ctx* ctx, double* beta) {
         NEED(ctx); NEED(beta);
         Ctx* c = const_cast<wamgpu_ctx*>(ctx);
         if (c->algo != 2) throw ContractError("get_beta: no wavelet-AM state");
-        std::vector<float> m(c->N);
-        CK(cudaMemcpyAsync(m.data(), c->beta.p, c->N * 4, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
-        for (uint64_t x = 0; x < c->N; ++x) beta[x] = m[x];
+        download_slab<float>(c, c->beta.p, beta, c->N, c->N, 0);
     })
 }
 
@@ -1053,10 +1161,7 @@ int wamgpu_get_q(const wamgpu_ctx* ctx, double* q) {
         NEED(ctx); NEED(q);
         Ctx* c = const_cast<wamgpu_ctx*>(ctx);
         need_data(c);
-        std::vector<float> m(std::max<uint64_t>(c->Ml, 1));
-        CK(cudaMemcpyAsync(m.data(), c->q.p, c->Ml * 4, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
-        for (uint64_t y = 0; y < c->Ml; ++y) q[y] = m[y];
+        download_slab<float>(c, c->q.p, q, c->Ml, c->Ml, 0, true);
     })
 }
 
@@ -1073,10 +1178,9 @@ int wamgpu_get_stats(const wamgpu_ctx* ctx, double* b, double* bp, double* bm) {
         NEED(ctx);
         Ctx* c = const_cast<wamgpu_ctx*>(ctx);
         if (c->algo != 2) throw ContractError("get_stats: no wavelet-AM state");
-        if (b) CK(cudaMemcpyAsync(b, c->bdata.p, c->N * 8, cudaMemcpyDeviceToHost, c->st));
-        if (bp) CK(cudaMemcpyAsync(bp, c->bp_dbg.p, c->N * 8, cudaMemcpyDeviceToHost, c->st));
-        if (bm) CK(cudaMemcpyAsync(bm, c->bm_dbg.p, c->N * 8, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
+        if (b) download_slab<double>(c, c->bdata.p, b, c->N, c->N, 0);
+        if (bp) download_slab<double>(c, c->bp_dbg.p, bp, c->N, c->N, 0);
+        if (bm) download_slab<double>(c, c->bm_dbg.p, bm, c->N, c->N, 0);
     })
 }
 
@@ -1088,7 +1192,7 @@ int wamgpu_get_scalars(const wamgpu_ctx* ctx, double* Z0, int64_t* cum, int64_t*
         CK(cudaMemcpyAsync(cnt, c->counters.p, 16, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
         if (Z0) *Z0 = c->Z0;
-        if (cum) *cum = c->algo == 1 ? (int64_t)c->N * c->iter : (int64_t)cnt[0];
+        if (cum) *cum = c->algo == 1 ? c->active * c->iter : (int64_t)cnt[0];
         if (degen) *degen = (int64_t)cnt[1];
         if (active) *active = c->active;
     })

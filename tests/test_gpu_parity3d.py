@@ -1,0 +1,89 @@
+"""GPU parity of the axial 3D stack (nz > 1 slices sharing one in-plane system
+matrix, geometry.hpp:17-20; pin P2) against the CPU oracle:
+slab forward/back, the AM baseline and the wavelet AM with per-slice 2D Haar
+and the z-summed expansion criterion.  `small3d` has 40
+slices, exercising partially filled lane slabs (2 slices per lane, masked)."""
+import numpy as np
+import pytest
+
+from wam_testutil import problem_inputs, rel_l2
+
+pytestmark = pytest.mark.gpu
+TOL_F64, TOL_MIRROR = 1e-4, 1e-6
+
+
+def _ctx(W, cfg):
+    from paper_1508_04458_b200 import configs
+    c = W.Context(0)
+    c.set_geometry(configs.geometry(cfg, W.Geometry))
+    return c
+
+
+@pytest.mark.parametrize("name", ["tiny3d", "small3d"])
+def test_slab_forward_back_vs_mirror(wam, orc, name):
+    cfg, p, mu_true, I0, d = problem_inputs(name, orc, wam, mirror=True)
+    c = _ctx(wam, cfg)
+    mu32 = mu_true.astype(np.float32).astype(np.float64)
+    l_gpu, l_orc = c.forward_project(mu_true), p.forward_project(mu32)
+    assert l_gpu.shape == l_orc.shape and rel_l2(l_gpu, l_orc) < 1e-14
+    w = (I0 * np.exp(-l_orc)).astype(np.float32).astype(np.float64)
+    assert rel_l2(c.back_project(w), p.back_project(w)) < 1e-14
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal(p.N * p.nz).astype(np.float32).astype(np.float64)
+    y = rng.standard_normal(p.M * p.nz).astype(np.float32).astype(np.float64)
+    Hx, Hty = c.forward_project(x), c.back_project(y)
+    assert abs(Hx @ y - x @ Hty) <= 1e-12 * np.linalg.norm(Hx) * np.linalg.norm(y)
+
+
+@pytest.mark.parametrize("name", ["tiny3d", "small3d"])
+def test_am3d_parity(wam, orc, name):
+    cfg, p64, _, I0, d = problem_inputs(name, orc, wam)
+    p32 = orc.Problem(p64.geom, mirror=True)
+    c = _ctx(wam, cfg)
+    c.set_data(d, I0)
+    c.am_init()
+    p64.am_init(d, I0)
+    p32.am_init(d, I0)
+    J = cfg["J"]
+    og = np.array([r["objective"] for r in c.am_iterate(J)])
+    o64 = [r[1] for r in p64.am_iterate(J)]
+    o32 = [r[1] for r in p32.am_iterate(J)]
+    assert rel_l2(og, o64) < TOL_F64 and rel_l2(og, o32) < TOL_MIRROR
+    assert rel_l2(c.image(), p64.am_get()["mu"]) < TOL_F64
+    assert rel_l2(c.image(), p32.am_get()["mu"]) < TOL_MIRROR
+    assert all(b <= a * (1 + 1e-6) for a, b in zip(og, og[1:]))
+
+
+@pytest.mark.parametrize("name", ["tiny3d", "small3d"])
+def test_wam3d_parity_tree_bit_exact(wam, orc, name):
+    cfg, p64, _, I0, d = problem_inputs(name, orc, wam)
+    p32 = orc.Problem(p64.geom, mirror=True)
+    L, J, sched = cfg["L"], cfg["J"], cfg["schedule"]
+    c = _ctx(wam, cfg)
+    c.set_data(d, I0)
+    c.wam_init(L)
+    p64.wam_init(d, I0, L)
+    p32.wam_init(d, I0, L)
+    assert c.scalars()["Z0"] == p32.wam_get()["Z0"]
+    assert rel_l2(c.stats()[0], p32.wam_stats()[0]) < 1e-12
+    og, o64, o32, done = [], [], [], 0
+    for ev in sched + [J]:
+        og += [r["objective"] for r in c.wam_iterate(ev - done)]
+        o64 += [r[1] for r in p64.wam_iterate(ev - done)]
+        o32 += [r[1] for r in p32.wam_iterate(ev - done)]
+        done = ev
+        if ev == J:
+            break
+        assert c.wam_expand(0.1) == p32.wam_expand(0.1)
+        p64.wam_expand(0.1)
+        assert np.array_equal(c.tree(), p32.wam_tree()) and np.array_equal(c.tree(), p64.wam_tree())
+        assert c.scalars()["Z0"] == p32.wam_get()["Z0"]
+    assert rel_l2(og, o64) < TOL_F64 and rel_l2(og, o32) < TOL_MIRROR
+    assert rel_l2(c.image(), p64.wam_get()["mu"]) < TOL_F64
+    assert rel_l2(c.image(), p32.wam_get()["mu"]) < TOL_MIRROR
+    s, cnt = c.scalars(), p32.wam_counters()
+    assert (s["active_set"], s["cum_updates"], s["degenerate"]) == (cnt["active_set"], cnt["cum_updates"],
+                                                                      cnt["degenerate"])
+    _, bp, bm = c.stats()
+    _, bp32, bm32 = p32.wam_stats()
+    assert rel_l2(bm, bm32) < TOL_MIRROR and rel_l2(bp, bp32) < TOL_MIRROR
