@@ -147,10 +147,12 @@ def _peaks():
 
 
 def _workload_desc(cfg, nnz, algo, J):
-    return (f"{cfg['name']}: 2D fan-beam {cfg['nx']}x{cfg['ny']} @ {cfg['voxel']} mm, {cfg['views']} views x "
+    dims = (f"2D fan-beam {cfg['nx']}x{cfg['ny']}" if cfg["nz"] == 1 else
+            f"axial 3D stack {cfg['nx']}x{cfg['ny']}x{cfg['nz']} (rays in-plane, one H for all slices, pin P2)")
+    return (f"{cfg['name']}: {dims} @ {cfg['voxel']} mm, {cfg['views']} views x "
             f"{cfg['detectors']} arc detectors (SCD 500, SDD 1000), I0={cfg['I0']:g} Poisson, "
-            + (f"wavelet AM Haar L={cfg['L']}, {J} iterations, expansions {cfg['schedule']} @0.1"
-               if algo == "wam" else f"image-domain AM, {J} iterations") + f", nnz(H)={nnz}")
+            + (f"wavelet AM Haar L={cfg['L']} (2D per slice), {J} iterations, expansions {cfg['schedule']} @0.1"
+               if algo == "wam" else f"image-domain AM, {J} iterations") + f", nnz(H per slice)={nnz}")
 
 
 def _inputs(cfg, W):
@@ -298,7 +300,8 @@ def main():
         img = ctx.image()
     e2e_s = plumb.max((time.perf_counter() - t0) / args.steps)
     Ml = ctx.row1 - ctx.row0
-    h2d = 2 * 4 * Ml
+    nz = cfg["nz"]
+    h2d = 2 * 4 * Ml * nz
     d2h = 4 * img.size
 
     iters_per_s = J / (ms_step * 1e-3)
@@ -308,8 +311,11 @@ def main():
         M, N = ctx.M, ctx.N
         nnz = nnz_local * world  # approximately equal shards; exact total below on N=1
         nnz = nnz_local if world == 1 else nnz
-        fwd_bytes = 8 * nnz_local + 4 * (Ml + 1) + 4 * N + 12 * Ml
-        back_bytes = 8 * nnz_local + 4 * (N + 1) + 4 * Ml + 4 * N
+        if nz == 1:
+            fwd_bytes = 8 * nnz_local + 4 * (Ml + 1) + 4 * N + 12 * Ml
+            back_bytes = 8 * nnz_local + 4 * (N + 1) + 4 * Ml + 4 * N
+        else:
+            fwd_bytes = back_bytes = 4 * nnz_local * nz                   # SURVEY.md §8(d) K2'/K3': 4 B/update
         fwd_avg = sum(fwd_ms) / max(fwd_n, 1)
         back_avg = sum(back_ms) / max(back_n, 1)
         fwd_gbs = fwd_bytes / (fwd_avg * 1e-3) / 1e9
@@ -348,7 +354,7 @@ def main():
             "config": {"workload": _workload_desc(cfg, nnz, algo, J), "step": "init_state + run (all iterations"
                        " and expansions)", "l2": "working set (H CSR+CSC = 16 B/nnz) >> 126 MB L2; no flush needed",
                        "parallelism": f"views/{world}"},
-            "ray_voxel_updates_per_s": 2 * nnz * J / (ms_step * 1e-3),
+            "ray_voxel_updates_per_s": 2 * nnz * nz * J / (ms_step * 1e-3),
             "final_objective": final_obj,
             "tree": {"active_set_by_iteration": sorted({r["active_set"] for r in recs}),
                      "coefficients": N, "phi_minus_nnz": split_nnz},
