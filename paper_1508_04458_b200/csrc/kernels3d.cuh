@@ -5,73 +5,70 @@
 // slices, so each projector pass is a sparse-matrix x dense-slab product:
 // one WARP per in-plane ray (forward) or voxel (back), the matrix entry is a
 // warp-uniform (broadcast) load and the lanes cover the slices of a z-fastest
-// slab (SPL slices per lane: nz <= 32 SPL), so every gather is one coalesced
-// nz*4-byte segment.  Device layouts: mu3/beta3 [x][s] fp32, q3/d3/I03 [y][s]
-// fp32, g3/bdata3/bm3 [z][s] fp64.  The boundary transposes to the reference
+// slab (SPL slices per lane: nz <= P = 32 SPL), so every gather is one
+// coalesced P*4-byte segment.  Device layouts (stride P): mu3/beta3 [x][s]
+// fp32, q3/d3/I03 [y][s] fp32, g3/bdata3/bm3 [z][s] fp64.  The boundary transposes to the reference
 // layouts (image.hpp:14 (z*ny+iy)*nx+ix, rays z*M+y).
 #pragma once
 #include "kernels.cuh"
 
 namespace wamgpu {
 
-template <int SPL>
-struct SliceVec { float v[SPL]; };
+// Slab stride P = 32*SPL (device layouts are padded to it; pad slices are
+// zero and carry I0 = d = 0, so they contribute nothing): every lane owns SPL
+// consecutive slices and all slab loads are unconditional vector loads.
+template <int SPL> struct SlabVec;
+template <> struct SlabVec<1> { using T = float; };
+template <> struct SlabVec<2> { using T = float2; };
+template <> struct SlabVec<4> { using T = float4; };
+__device__ __forceinline__ void unpack(float v, float (&o)[1]) { o[0] = v; }
+__device__ __forceinline__ void unpack(float2 v, float (&o)[2]) { o[0] = v.x; o[1] = v.y; }
+__device__ __forceinline__ void unpack(float4 v, float (&o)[4]) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
 
+// Slab SpMV of one row/column: acc[j] = sum_k h_k x[idx_k*P + lane*SPL + j].
+// The warp loads 32 matrix entries with ONE coalesced load (lane j holds entry
+// base+j), prefetches the next 32 while it works, broadcasts entries by
+// shuffle, and keeps 8 slab gathers in flight per lane.
 template <int SPL>
-__device__ __forceinline__ void load_slices(const float* __restrict__ p, int nz, int lane, float (&out)[SPL]) {
-    const int s0 = lane * SPL;
-    if (SPL == 2 && s0 + 1 < nz) {
-        const float2 t = __ldg(reinterpret_cast<const float2*>(p + s0));
-        out[0] = t.x; out[SPL > 1 ? 1 : 0] = t.y;
-        return;
-    }
-    if (SPL == 4 && s0 + 3 < nz) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(p + s0));
-        out[0] = t.x; out[SPL > 1 ? 1 : 0] = t.y; out[SPL > 2 ? 2 : 0] = t.z; out[SPL > 3 ? 3 : 0] = t.w;
-        return;
-    }
-#pragma unroll
-    for (int j = 0; j < SPL; ++j) out[j] = (s0 + j < nz) ? __ldg(p + s0 + j) : 0.0f;
-}
-
-// Slab SpMV of one row/column: acc[j] = sum_k h_k x[idx_k * nz + lane*SPL + j].
-// The row's entries are read 8 at a time (uniform loads, all in flight), then
-// their 8 slab gathers, then the fp64 fmas.
-template <int SPL>
-__device__ __forceinline__ void slab_dot(const uint2* __restrict__ A, const float* __restrict__ x, int nz,
-                                         uint64_t lo, uint64_t hi, int lane, double (&acc)[SPL]) {
+__device__ __forceinline__ void slab_dot(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
+                                         uint64_t hi, int lane, double (&acc)[SPL]) {
+    using V = typename SlabVec<SPL>::T;
+    constexpr int P = 32 * SPL;
 #pragma unroll
     for (int j = 0; j < SPL; ++j) acc[j] = 0.0;
-    constexpr int U = 8;
-    uint64_t k = lo;
-    for (; k + U <= hi; k += U) {
-        uint2 e[U];
+    uint2 cur = (lo + lane < hi) ? ld_stream(A + lo + lane) : make_uint2(0u, 0u);
+    for (uint64_t base = lo; base < hi; base += 32) {
+        const uint64_t nb = base + 32;
+        const uint2 nxt = (nb + lane < hi) ? ld_stream(A + nb + lane) : make_uint2(0u, 0u);
+        const int n = (int)((hi - base) < 32 ? (hi - base) : 32);
+        for (int j0 = 0; j0 < n; j0 += 8) {
+            unsigned c[8];
+            float h[8];
 #pragma unroll
-        for (int u = 0; u < U; ++u) e[u] = __ldg(A + k + u);
-        float v[U][SPL];
+            for (int u = 0; u < 8; ++u) {
+                c[u] = __shfl_sync(0xffffffffu, cur.x, j0 + u);
+                h[u] = __uint_as_float(__shfl_sync(0xffffffffu, cur.y, j0 + u));
+            }
+            V v[8];
 #pragma unroll
-        for (int u = 0; u < U; ++u) load_slices<SPL>(x + (uint64_t)e[u].x * nz, nz, lane, v[u]);
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(reinterpret_cast<const V*>(x + (uint64_t)c[u] * P) + lane);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const double h = hval(e[u]);
+            for (int u = 0; u < 8; ++u) {
+                float f[SPL];
+                unpack(v[u], f);
+                const double hh = (double)h[u];
 #pragma unroll
-            for (int j = 0; j < SPL; ++j) acc[j] = fma(h, (double)v[u][j], acc[j]);
+                for (int j = 0; j < SPL; ++j) acc[j] = fma(hh, (double)f[j], acc[j]);
+            }
         }
-    }
-    for (; k < hi; ++k) {
-        const uint2 e = __ldg(A + k);
-        float v[SPL];
-        load_slices<SPL>(x + (uint64_t)e.x * nz, nz, lane, v);
-        const double h = hval(e);
-#pragma unroll
-        for (int j = 0; j < SPL; ++j) acc[j] = fma(h, (double)v[j], acc[j]);
+        cur = nxt;
     }
 }
 
 // K2 3D: l[y][s] = sum_x h(y|x) mu[x][s]; MODE 0 writes l (fp64, [y][s]);
 // MODE 1 fuses q = fp32(I0 exp(-l)) and the fp64 I-divergence partial.
 template <int MODE, int SPL>
-__global__ void __launch_bounds__(256) k_forward3(uint64_t M, int nz, const unsigned long long* __restrict__ rp,
+__global__ void __launch_bounds__(256, 4) k_forward3(uint64_t M, int nz, const unsigned long long* __restrict__ rp,
                                                   const uint2* __restrict__ A, const float* __restrict__ mu,
                                                   const float* __restrict__ I0, const float* __restrict__ d,
                                                   float* __restrict__ q, double* __restrict__ lout,
@@ -81,12 +78,12 @@ __global__ void __launch_bounds__(256) k_forward3(uint64_t M, int nz, const unsi
     double tacc = 0.0;
     for (uint64_t y = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; y < M; y += W) {
         double acc[SPL];
-        slab_dot<SPL>(A, mu, nz, rp[y], rp[y + 1], lane, acc);
+        slab_dot<SPL>(A, mu, rp[y], rp[y + 1], lane, acc);
 #pragma unroll
         for (int j = 0; j < SPL; ++j) {
             const int s = lane * SPL + j;
             if (s >= nz) continue;
-            const uint64_t id = y * nz + s;
+            const uint64_t id = y * (32 * SPL) + s;
             if (!isfinite(acc[j])) atomicOr(flag, 1);
             if (MODE == 0) {
                 lout[id] = acc[j];
@@ -117,7 +114,7 @@ __global__ void __launch_bounds__(256) k_forward3(uint64_t M, int nz, const unsi
 // (SPEC.md:303, 316-317).  Voxels are visited in 2D tile order (`order`) so the
 // concurrently processed columns share rays and the q-slab gathers hit L2.
 template <int MODE, int SPL>
-__global__ void __launch_bounds__(256) k_back3(uint64_t N, int nz, const unsigned* __restrict__ order,
+__global__ void __launch_bounds__(256, 4) k_back3(uint64_t N, int nz, const unsigned* __restrict__ order,
                                                const unsigned long long* __restrict__ cp, const uint2* __restrict__ C,
                                                const float* __restrict__ w, double* __restrict__ g,
                                                const double* __restrict__ bam, float* __restrict__ mu, double Z0,
@@ -127,12 +124,12 @@ __global__ void __launch_bounds__(256) k_back3(uint64_t N, int nz, const unsigne
     for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < N; i += W) {
         const uint64_t x = order ? order[i] : i;
         double acc[SPL];
-        slab_dot<SPL>(C, w, nz, cp[x], cp[x + 1], lane, acc);
+        slab_dot<SPL>(C, w, cp[x], cp[x + 1], lane, acc);
 #pragma unroll
         for (int j = 0; j < SPL; ++j) {
             const int s = lane * SPL + j;
             if (s >= nz) continue;
-            const uint64_t id = x * nz + s;
+            const uint64_t id = x * (32 * SPL) + s;
             if (MODE == 0) {
                 g[id] = acc[j];
             } else {
@@ -149,7 +146,7 @@ __global__ void __launch_bounds__(256) k_back3(uint64_t N, int nz, const unsigne
 
 // K5 3D: b-[z][s] = sum over the (slice-shared) Phi^- column of z of q[y][s] phi.
 template <int SPL>
-__global__ void __launch_bounds__(256) k_split3(uint64_t nlist, int nz, const unsigned* __restrict__ list,
+__global__ void __launch_bounds__(256, 4) k_split3(uint64_t nlist, int nz, const unsigned* __restrict__ list,
                                                 const unsigned long long* __restrict__ ptr,
                                                 const uint2* __restrict__ E, const float* __restrict__ q,
                                                 double* __restrict__ bm) {
@@ -158,11 +155,11 @@ __global__ void __launch_bounds__(256) k_split3(uint64_t nlist, int nz, const un
     for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlist; i += W) {
         const unsigned z = list[i];
         double acc[SPL];
-        slab_dot<SPL>(E, q, nz, ptr[z], ptr[z + 1], lane, acc);
+        slab_dot<SPL>(E, q, ptr[z], ptr[z + 1], lane, acc);
 #pragma unroll
         for (int j = 0; j < SPL; ++j) {
             const int s = lane * SPL + j;
-            if (s < nz) bm[(uint64_t)z * nz + s] = acc[j];
+            if (s < nz) bm[(uint64_t)z * (32 * SPL) + s] = acc[j];
         }
     }
 }
@@ -172,7 +169,7 @@ __global__ void __launch_bounds__(256) k_split3(uint64_t nlist, int nz, const un
 // mode 0: synthesis beta -> mu (and mu64); mode 1: analysis + root solve +
 // synthesis; mode 2: analysis only (g -> out).
 constexpr int SC3 = 8;  // slices per CTA
-__global__ void k_tile3(int mode, int nx, int ny, int nz, int L, const double* __restrict__ g,
+__global__ void k_tile3(int mode, int nx, int ny, int nz, int P, int L, const double* __restrict__ g,
                         const double* __restrict__ bm, const double* __restrict__ bdata,
                         const uint8_t* __restrict__ act, ActOff off, float* __restrict__ beta,
                         float* __restrict__ mu, double* __restrict__ mu64, double* __restrict__ out,
@@ -189,7 +186,7 @@ __global__ void k_tile3(int mode, int nx, int ny, int nz, int L, const double* _
     if (mode != 0) {
         for (int i = threadIdx.x; i < T2 * ns; i += blockDim.x) {
             const int v = i / ns, s = i % ns;
-            xs[s * T2 + v] = g[(base + (uint64_t)(v / TS) * nx + v % TS) * nz + s0 + s];
+            xs[s * T2 + v] = g[(base + (uint64_t)(v / TS) * nx + v % TS) * P + s0 + s];
         }
         __syncthreads();
         for (int s = 0; s < ns; ++s) tile_fwd(xs + s * T2, ts, TS, L);
@@ -198,7 +195,7 @@ __global__ void k_tile3(int mode, int nx, int ny, int nz, int L, const double* _
         for (int i = threadIdx.x; i < T2 * ns; i += blockDim.x) {
             const int v = i / ns, s = i % ns;
             CoefInfo ci = coef_info(v / TS, v % TS, ti, tj, L, nx, ny, act, off);
-            out[ci.z * nz + s0 + s] = xs[s * T2 + v];
+            out[ci.z * P + s0 + s] = xs[s * T2 + v];
         }
         return;
     }
@@ -206,7 +203,7 @@ __global__ void k_tile3(int mode, int nx, int ny, int nz, int L, const double* _
     for (int i = threadIdx.x; i < T2 * ns; i += blockDim.x) {
         const int v = i / ns, s = i % ns;
         CoefInfo ci = coef_info(v / TS, v % TS, ti, tj, L, nx, ny, act, off);
-        const uint64_t zid = ci.z * nz + s0 + s;
+        const uint64_t zid = ci.z * P + s0 + s;
         float bo = beta[zid];
         if (mode == 1) {
             const double bmv = ci.approx ? 0.0 : bm[zid];
@@ -241,18 +238,18 @@ __global__ void k_tile3(int mode, int nx, int ny, int nz, int L, const double* _
     for (int s = 0; s < ns; ++s) tile_inv(xs + s * T2, ts, TS, L);
     for (int i = threadIdx.x; i < T2 * ns; i += blockDim.x) {
         const int v = i / ns, s = i % ns;
-        const uint64_t p = (base + (uint64_t)(v / TS) * nx + v % TS) * nz + s0 + s;
+        const uint64_t p = (base + (uint64_t)(v / TS) * nx + v % TS) * P + s0 + s;
         mu[p] = (float)xs[s * T2 + v];
         if (mu64) mu64[p] = xs[s * T2 + v];
     }
 }
 
 // z-summed criterion image: s(p) = sum_s mu64[p][s] in slice order.
-__global__ void k_zsum(uint64_t N, int nz, const double* __restrict__ mu64, double* __restrict__ out) {
+__global__ void k_zsum(uint64_t N, int nz, int P, const double* __restrict__ mu64, double* __restrict__ out) {
     const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= N) return;
     double s = 0.0;
-    for (int k = 0; k < nz; ++k) s += mu64[p * nz + k];
+    for (int k = 0; k < nz; ++k) s += mu64[p * P + k];
     out[p] = s;
 }
 

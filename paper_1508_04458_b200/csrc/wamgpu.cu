@@ -577,27 +577,30 @@ static void fill_records(Ctx* c, int n, wamgpu_record* recs, int64_t active_at_s
 
 // ---- boundary layout conversion: reference image/coefficient layout
 // ((s0+s)*N + x, image.hpp:14) <-> device slab [x][s]; rays (s*M + y) <-> [y][s].
-static uint64_t NV(const Ctx* c) { return c->N * (uint64_t)c->nzl; }
-static uint64_t MV(const Ctx* c) { return c->Ml * (uint64_t)c->nzl; }
+static int slab_stride(const Ctx* c) { return c->nzl == 1 ? 1 : 32 * (c->nzl <= 32 ? 1 : (c->nzl <= 64 ? 2 : 4)); }
+static uint64_t NV(const Ctx* c) { return c->N * (uint64_t)slab_stride(c); }
+static uint64_t MV(const Ctx* c) { return c->Ml * (uint64_t)slab_stride(c); }
 template <class T>
 static void upload_slab(Ctx* c, const double* ref, T* dev, uint64_t n_inner, uint64_t ref_stride, uint64_t ref_off,
                         bool local = false) {
-    std::vector<T> h(std::max<uint64_t>(n_inner * c->nzl, 1));
+    const int P = slab_stride(c);
+    std::vector<T> h(std::max<uint64_t>(n_inner * P, 1), (T)0);   // pad slices are zero
     const int sb = local ? 0 : c->s0;
     for (int s = 0; s < c->nzl; ++s)
-        for (uint64_t i = 0; i < n_inner; ++i) h[i * c->nzl + s] = (T)ref[(uint64_t)(sb + s) * ref_stride + ref_off + i];
-    CK(cudaMemcpyAsync(dev, h.data(), n_inner * c->nzl * sizeof(T), cudaMemcpyHostToDevice, c->st));
+        for (uint64_t i = 0; i < n_inner; ++i) h[i * P + s] = (T)ref[(uint64_t)(sb + s) * ref_stride + ref_off + i];
+    CK(cudaMemcpyAsync(dev, h.data(), n_inner * P * sizeof(T), cudaMemcpyHostToDevice, c->st));
     CK(cudaStreamSynchronize(c->st));
 }
 template <class T>
 static void download_slab(Ctx* c, const T* dev, double* ref, uint64_t n_inner, uint64_t ref_stride, uint64_t ref_off,
                           bool local = false) {
-    std::vector<T> h(std::max<uint64_t>(n_inner * c->nzl, 1));
-    CK(cudaMemcpyAsync(h.data(), dev, n_inner * c->nzl * sizeof(T), cudaMemcpyDeviceToHost, c->st));
+    const int P = slab_stride(c);
+    std::vector<T> h(std::max<uint64_t>(n_inner * P, 1));
+    CK(cudaMemcpyAsync(h.data(), dev, n_inner * P * sizeof(T), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     const int sb = local ? 0 : c->s0;
     for (int s = 0; s < c->nzl; ++s)
-        for (uint64_t i = 0; i < n_inner; ++i) ref[(uint64_t)(sb + s) * ref_stride + ref_off + i] = (double)h[i * c->nzl + s];
+        for (uint64_t i = 0; i < n_inner; ++i) ref[(uint64_t)(sb + s) * ref_stride + ref_off + i] = (double)h[i * P + s];
 }
 
 // ------------------------------------------------------------------ AM
@@ -671,7 +674,7 @@ static void tile_launch(Ctx* c, int mode, double* mu64, double* out) {
         const size_t smem = (size_t)(SC3 + 1) * TS * TS * sizeof(double);
         if (smem > 48 * 1024)
             CK(cudaFuncSetAttribute(k_tile3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_tile3<<<grid, 256, smem, c->st>>>(mode, c->nx, c->ny, c->nzl, c->L, c->g.p, c->g.p + NV(c), c->bdata.p,
+        k_tile3<<<grid, 256, smem, c->st>>>(mode, c->nx, c->ny, c->nzl, slab_stride(c), c->L, c->g.p, c->g.p + NV(c), c->bdata.p,
                                             c->act.p, c->off, c->beta.p, c->mu.p, mu64, out, c->bp_dbg.p,
                                             c->bm_dbg.p, c->Z0, c->counters.p, c->flag.p);
     }
@@ -818,7 +821,7 @@ static int64_t wam_expand(Ctx* c, double factor) {
     const double* crit = c->mu64.p;                // nz == 1: the z-sum is the slice
     if (c->nzl > 1 || c->nz > 1) {                 // z-summed image, slabs all-reduced
         c->dscratch.ensure(c->N);
-        k_zsum<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->nzl, c->mu64.p, c->dscratch.p);
+        k_zsum<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->nzl, slab_stride(c), c->mu64.p, c->dscratch.p);
         check_launch(c);
         allreduce_sum(c, c->dscratch.p, c->N);
         crit = c->dscratch.p;
