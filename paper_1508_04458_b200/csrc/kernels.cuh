@@ -158,8 +158,7 @@ __device__ __forceinline__ double idiv_term(double d, double q) {
 // fp64 accumulation (products of two fp32 are exact in fp64); segment
 // selection is by predicated fma with h=0 (an exact no-op); fixed
 // xor-butterfly reduction (deterministic).
-constexpr int UNROLL = 8;
-template <int G>
+template <int G, int UNROLL = 8>
 __device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
                                         const uint64_t (&b)[G > 1 ? G - 1 : 1], uint64_t hi, int lane,
                                         double (&out)[G]) {
@@ -208,9 +207,9 @@ __device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float
 // Warp task = FG consecutive rays.  MODE 0: l = H mu as fp64 (forward_project).
 // MODE 1: fused Beer's law + I-divergence: q = fp32(I0 exp(-l)), per-block fp64
 // partial of the objective (deterministic block order).
-constexpr int FG = 2;  // rows per warp task in the forward kernel (measured best of 1/2/4)
-template <int MODE>
-__global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long long* __restrict__ rp,
+constexpr int FG_DEFAULT = 2;  // rows per warp task in the forward kernel (measured best of 1/2/4)
+template <int MODE, int FG = FG_DEFAULT, int UNR = 8, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_forward(uint64_t M, const unsigned long long* __restrict__ rp,
                                                  const uint2* __restrict__ A, const float* __restrict__ mu,
                                                  const float* __restrict__ I0, const float* __restrict__ d,
                                                  float* __restrict__ q, double* __restrict__ lout,
@@ -225,11 +224,12 @@ __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long
         // row extents: lane j < nr+1 loads rp[y0+j]
         const unsigned long long myrp = (lane <= nr) ? __ldg(rp + y0 + lane) : 0ull;
         const uint64_t lo = __shfl_sync(0xffffffffu, myrp, 0), hi = __shfl_sync(0xffffffffu, myrp, nr);
-        uint64_t bnd[FG - 1];
+        uint64_t bnd[FG > 1 ? FG - 1 : 1];
+        bnd[0] = 0;
 #pragma unroll
         for (int g = 0; g < FG - 1; ++g) bnd[g] = __shfl_sync(0xffffffffu, myrp, min(g + 1, nr));
         double l[FG];
-        seg_dot<FG>(A, mu, lo, bnd, hi, lane, l);
+        seg_dot<FG, UNR>(A, mu, lo, bnd, hi, lane, l);
         // lane g finishes row y0+g: Beer's law, I-divergence term
         double lg = l[0];
 #pragma unroll
@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(256) k_forward(uint64_t M, const unsigned long
 // Warp per voxel: g(x) = sum_y h(y|x) w(y) in fp64 over the voxel's CSC column.
 // MODE 0: write g (fp64).  MODE 1: fused AM update:
 // mu <- max(0, mu + ln(g/b)/Z0) where b > 0 and g > 0, otherwise frozen.
-template <int MODE>
-__global__ void __launch_bounds__(256) k_back(uint64_t N, const unsigned long long* __restrict__ cp,
+template <int MODE, int UNR = 8, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_back(uint64_t N, const unsigned long long* __restrict__ cp,
                                               const uint2* __restrict__ C, const float* __restrict__ w,
                                               double* __restrict__ g, const double* __restrict__ bam,
                                               float* __restrict__ mu, double Z0, int* __restrict__ flag) {
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256) k_back(uint64_t N, const unsigned long lo
     for (uint64_t x = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; x < N; x += W) {
         const uint64_t nob[1] = {0};
         double cc[1];
-        seg_dot<1>(C, w, cp[x], nob, cp[x + 1], lane, cc);
+        seg_dot<1, UNR>(C, w, cp[x], nob, cp[x + 1], lane, cc);
         const double c = cc[0];
         if (lane == 0) {
             if (MODE == 0) {
@@ -719,7 +719,7 @@ __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsi
 // (bit-identical to the oracle).  cnt / pos are per (ray, level): index y*L + l-1.
 template <int MODE, int L>
 __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned long long* __restrict__ rp,
-                                                    const uint2* __restrict__ A, int nx, int ny,
+                                                    const uint2* __restrict__ A, int nx, int ny, int nlev,
                                                     const unsigned* __restrict__ tbits, ActOff boff, int tree_words,
                                                     const double* __restrict__ zA, double* __restrict__ zrow,
                                                     unsigned long long* __restrict__ cnt,
@@ -729,7 +729,9 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
     __shared__ uint2 buf[32][33];
     __shared__ unsigned long long s_lo[32], s_len[32];
     __shared__ double s_tot[L][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, l = w + 1;
+    // warp w tracks level L - w; levels below L - nlev + 1 hold no active block
+    // (tree closure), so their warps are not launched at all
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, l = L - w;
     for (int i = threadIdx.x; i < tree_words; i += blockDim.x) tsm[i] = tbits[i];
     const uint64_t y = (uint64_t)blockIdx.x * 32 + lane;
     if (w == 0) {
@@ -754,6 +756,7 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
     double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, tot = 0.0;
     unsigned long long count = 0, wp = 0;
     if (MODE == 2 && y < M) wp = pos[y * L + (l - 1)];
+    (void)nlev;
 
     auto flush = [&]() {
         if (av) {
@@ -775,7 +778,7 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
 
     for (unsigned long long base = 0; base < maxlen; base += 32) {
         // all L warps stage the 32 rays' entries [base, base+32)
-        for (int j = w; j < 32; j += L) {
+        for (int j = w; j < 32; j += nlev) {
             const unsigned long long nj = s_len[j];
             const bool ok = base + lane < nj;
             cp_async8(&buf[j][lane], A + (ok ? s_lo[j] + base + lane : 0), ok);
@@ -815,8 +818,10 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
         if (w == 0 && y < M) {
             double z = zA[y];
 #pragma unroll
-            for (int k = L; k >= 1; --k) z += s_tot[k - 1][lane];
+            for (int k = L; k >= 1; --k)
+                if (k > L - nlev) z += s_tot[k - 1][lane];
             zrow[y] = z;
+            for (int k = 1; k <= L - nlev; ++k) cnt[y * L + (k - 1)] = 0;
         }
     }
 }

@@ -111,6 +111,7 @@ struct wamgpu_ctx {
     double Z0 = 0.0;
     DBuf<double> scal, partial;
     int nblk_row = 1, nblk_col = 1;
+    int fwd_variant = 0, back_variant = 0;  // SpMV tuning knobs (WAMGPU_FWD_VARIANT / WAMGPU_BACK_VARIANT)
     DBuf<unsigned long long> counters;
     DBuf<int> flag, it;
     DBuf<double> objs;
@@ -238,7 +239,7 @@ static void finish_matrix(Ctx* c) {
     c->C.swap(vout);
     kout.release();
     c->cub_tmp.release();
-    c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>(((c->Ml + FG - 1) / FG + 7) / 8, (uint64_t)c->sms * 16));
+    c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->Ml + 7) / 8, (uint64_t)c->sms * 16));
     c->nblk_col = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->N + 7) / 8, (uint64_t)c->sms * 16));
     c->partial.alloc(std::max<size_t>(std::max(c->nblk_row, 1024), (size_t)c->sms * 16));
     c->scal.alloc(8);
@@ -366,8 +367,19 @@ static unsigned nblk_warp(const Ctx* c, uint64_t n) {
 static void back_launch(Ctx* c, const float* w, double* out, const double* bam) {
     c->timer_begin(T_BACK);
     if (c->nzl == 1) {
-        if (bam) k_back<1><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, nullptr, bam, c->mu.p, c->Z0, c->flag.p);
-        else k_back<0><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
+#define BV(U, MB)                                                                                                 \
+    if (bam) k_back<1, U, MB><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, nullptr, bam, c->mu.p,     \
+                                                              c->Z0, c->flag.p);                                  \
+    else k_back<0, U, MB><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0,   \
+                                                          c->flag.p);
+        switch (c->back_variant) {
+            case 1: BV(4, 1) break;
+            case 2: BV(4, 8) break;
+            case 3: BV(12, 1) break;
+            case 4: BV(8, 6) break;
+            default: BV(8, 1) break;
+        }
+#undef BV
     } else {
         const unsigned nb = nblk_warp(c, c->N);
 #define B3(S)                                                                                                     \
@@ -404,8 +416,20 @@ static void forward_fused(Ctx* c, bool record) {
     c->timer_begin(T_FWD);
     int nparts = c->nblk_row;
     if (c->nzl == 1) {
-        k_forward<1><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, c->q.p, nullptr,
-                                                    c->partial.p, c->flag.p);
+#define FV(FGv, U, MB)                                                                                              \
+    k_forward<1, FGv, U, MB><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p,     \
+                                                            c->q.p, nullptr, c->partial.p, c->flag.p);
+        switch (c->fwd_variant) {
+            case 1: FV(1, 8, 1) break;
+            case 2: FV(2, 4, 1) break;
+            case 3: FV(2, 4, 6) break;
+            case 4: FV(1, 4, 8) break;
+            case 5: FV(2, 12, 1) break;
+            case 6: FV(4, 4, 1) break;
+            case 7: FV(1, 8, 6) break;
+            default: FV(2, 8, 1) break;
+        }
+#undef FV
     } else {
         const unsigned nb = std::min<unsigned>(nblk_warp(c, c->Ml), (unsigned)c->partial.n);
         nparts = (int)nb;
@@ -482,12 +506,24 @@ static void launch_walk_lv(Ctx* c, unsigned long long* cnt, const unsigned long 
                            uint2* vals) {
     const unsigned nb = blocks_for(c->Ml, 32);
     const size_t smem = (size_t)c->tree_words * 4;
+    // levels that hold active blocks: L down to the finest active level
+    int nlev = 0;
+    for (int l = c->L; l >= 1; --l) {
+        const uint64_t n = (uint64_t)(c->nx >> l) * (c->ny >> l);
+        const uint8_t* a = c->act_host.data() + c->off.off[l];
+        bool any = false;
+        for (uint64_t i = 0; i < n && !any; ++i) any = a[i] != 0;
+        if (!any) break;
+        ++nlev;
+    }
+    if (nlev == 0) nlev = 1;
     if (smem > 160 * 1024) throw ConfigError("tree too large for the shared-memory walk");
 #define LV_CASE(LV)                                                                                              \
     case LV: {                                                                                                   \
         auto kf = k_walk_lv<MODE, LV>;                                                                           \
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        kf<<<nb, 32 * LV, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->tbits.p, c->boff, c->tree_words, \
+        kf<<<nb, 32 * nlev, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, nlev, c->tbits.p, c->boff,      \
+                                           c->tree_words, \
                                          c->zA.p, c->zrow.p, cnt, pos, keys, vals);                               \
     } break;
     switch (c->L) {
@@ -881,6 +917,8 @@ static Ctx* create(int device) {
     CK(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10) throw CudaError("wamgpu: requires an sm_100a (Blackwell) device");
     c->sms = prop.multiProcessorCount;
+    if (const char* e = std::getenv("WAMGPU_FWD_VARIANT")) c->fwd_variant = std::atoi(e);
+    if (const char* e = std::getenv("WAMGPU_BACK_VARIANT")) c->back_variant = std::atoi(e);
     CK(cudaEventCreate(&c->ev_t0));
     CK(cudaEventCreate(&c->ev_a));
     CK(cudaEventCreate(&c->ev_b));
