@@ -751,15 +751,26 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
     const unsigned bo = (unsigned)boff.off[l];
     const double sc = 1.0 / (double)(1 << l);
 
-    int cur = -1, cbi = 0, cbj = 0;
+    int cur = -1, cbi = 0, cbj = 0, cq = -1;
     bool av = false;
-    double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, tot = 0.0;
+    // quadrant sums of the current block; quadrants are convex, so a ray visits
+    // each quadrant in one contiguous sub-run: one running accumulator qa for
+    // the current quadrant cq, parked into q0..q3 when the quadrant changes
+    // (the same sequential ray-order sums as four accumulators).
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, qa = 0.0, tot = 0.0;
     unsigned long long count = 0, wp = 0;
     if (MODE == 2 && y < M) wp = pos[y * L + (l - 1)];
     (void)nlev;
 
+    auto park = [&]() {
+        q0 = cq == 0 ? qa : q0;
+        q1 = cq == 1 ? qa : q1;
+        q2 = cq == 2 ? qa : q2;
+        q3 = cq == 3 ? qa : q3;
+    };
     auto flush = [&]() {
         if (av) {
+            park();
             const double st = q0 + q1, sb = q2 + q3;
             const double pH = (st - sb) * sc, pV = ((q0 + q2) - (q1 + q3)) * sc, pD = ((q0 + q3) - (q1 + q2)) * sc;
             if (MODE == 1) tot += fabs(pH) + fabs(pV) + fabs(pD);
@@ -772,8 +783,10 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
                     if (MODE == 1) ++count;
                     else { keys[wp] = z[s]; vals[wp] = make_uint2((unsigned)y, __float_as_uint(v[s])); ++wp; }
                 }
+            q0 = q1 = q2 = q3 = 0.0;
         }
-        q0 = q1 = q2 = q3 = 0.0;
+        cq = -1;
+        qa = 0.0;
     };
 
     for (unsigned long long base = 0; base < maxlen; base += 32) {
@@ -800,12 +813,13 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
                 av = (tsm[bit >> 5] >> (bit & 31)) & 1u;
             }
             if (av) {
-                const double h = hval(e);
                 const int quad = (((iy >> (l - 1)) & 1) << 1) | ((ix >> (l - 1)) & 1);
-                q0 += quad == 0 ? h : 0.0;
-                q1 += quad == 1 ? h : 0.0;
-                q2 += quad == 2 ? h : 0.0;
-                q3 += quad == 3 ? h : 0.0;
+                if (quad != cq) {
+                    if (cq >= 0) park();
+                    cq = quad;
+                    qa = 0.0;
+                }
+                qa += hval(e);
             }
         }
         __syncthreads();

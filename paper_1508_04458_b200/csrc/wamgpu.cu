@@ -15,12 +15,14 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/wamgpu.h"
@@ -375,9 +377,9 @@ static void back_launch(Ctx* c, const float* w, double* out, const double* bam) 
         switch (c->back_variant) {
             case 1: BV(4, 1) break;
             case 2: BV(4, 8) break;
-            case 3: BV(12, 1) break;
             case 4: BV(8, 6) break;
-            default: BV(8, 1) break;
+            case 5: BV(8, 1) break;
+            default: BV(12, 1) break;     // measured best at cfg2 (round 1 sweep, profiles/)
         }
 #undef BV
     } else {
@@ -423,11 +425,11 @@ static void forward_fused(Ctx* c, bool record) {
             case 1: FV(1, 8, 1) break;
             case 2: FV(2, 4, 1) break;
             case 3: FV(2, 4, 6) break;
-            case 4: FV(1, 4, 8) break;
             case 5: FV(2, 12, 1) break;
             case 6: FV(4, 4, 1) break;
             case 7: FV(1, 8, 6) break;
-            default: FV(2, 8, 1) break;
+            case 8: FV(2, 8, 1) break;
+            default: FV(1, 4, 8) break;   // measured best at cfg2 (round 1 sweep, profiles/)
         }
 #undef FV
     } else {
@@ -614,6 +616,20 @@ static void fill_records(Ctx* c, int n, wamgpu_record* recs, int64_t active_at_s
 // ---- boundary layout conversion: reference image/coefficient layout
 // ((s0+s)*N + x, image.hpp:14) <-> device slab [x][s]; rays (s*M + y) <-> [y][s].
 static int slab_stride(const Ctx* c) { return c->nzl == 1 ? 1 : 32 * (c->nzl <= 32 ? 1 : (c->nzl <= 64 ? 2 : 4)); }
+// host-side data-parallel loop for the boundary conversions (large 3D slabs)
+template <class Fn>
+static void host_par(uint64_t n, Fn&& fn) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const uint64_t nt = n < (1u << 20) ? 1 : std::min<uint64_t>(hw, 32);
+    if (nt == 1) { fn(0, n); return; }
+    std::vector<std::thread> pool;
+    const uint64_t chunk = (n + nt - 1) / nt;
+    for (uint64_t t = 0; t < nt; ++t) {
+        const uint64_t lo = t * chunk, hi = std::min(n, lo + chunk);
+        if (lo < hi) pool.emplace_back([&fn, lo, hi] { fn(lo, hi); });
+    }
+    for (auto& th : pool) th.join();
+}
 static uint64_t NV(const Ctx* c) { return c->N * (uint64_t)slab_stride(c); }
 static uint64_t MV(const Ctx* c) { return c->Ml * (uint64_t)slab_stride(c); }
 template <class T>
@@ -622,8 +638,11 @@ static void upload_slab(Ctx* c, const double* ref, T* dev, uint64_t n_inner, uin
     const int P = slab_stride(c);
     std::vector<T> h(std::max<uint64_t>(n_inner * P, 1), (T)0);   // pad slices are zero
     const int sb = local ? 0 : c->s0;
-    for (int s = 0; s < c->nzl; ++s)
-        for (uint64_t i = 0; i < n_inner; ++i) h[i * P + s] = (T)ref[(uint64_t)(sb + s) * ref_stride + ref_off + i];
+    const int nzl = c->nzl;
+    host_par(n_inner, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t i = lo; i < hi; ++i)
+            for (int s = 0; s < nzl; ++s) h[i * P + s] = (T)ref[(uint64_t)(sb + s) * ref_stride + ref_off + i];
+    });
     CK(cudaMemcpyAsync(dev, h.data(), n_inner * P * sizeof(T), cudaMemcpyHostToDevice, c->st));
     CK(cudaStreamSynchronize(c->st));
 }
@@ -635,8 +654,11 @@ static void download_slab(Ctx* c, const T* dev, double* ref, uint64_t n_inner, u
     CK(cudaMemcpyAsync(h.data(), dev, n_inner * P * sizeof(T), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     const int sb = local ? 0 : c->s0;
-    for (int s = 0; s < c->nzl; ++s)
-        for (uint64_t i = 0; i < n_inner; ++i) ref[(uint64_t)(sb + s) * ref_stride + ref_off + i] = (double)h[i * P + s];
+    const int nzl = c->nzl;
+    host_par(n_inner, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t i = lo; i < hi; ++i)
+            for (int s = 0; s < nzl; ++s) ref[(uint64_t)(sb + s) * ref_stride + ref_off + i] = (double)h[i * P + s];
+    });
 }
 
 // ------------------------------------------------------------------ AM
@@ -1112,12 +1134,19 @@ int wamgpu_set_data(wamgpu_ctx* ctx, const double* d, const double* I0) {
         NEED(ctx); NEED(d); NEED(I0);
         need_matrix(ctx);
         Ctx* c = ctx;
-        for (int s = 0; s < c->nzl; ++s)
-            for (uint64_t y = 0; y < c->Ml; ++y) {
-                const uint64_t id = (uint64_t)(c->s0 + s) * c->M + c->row0 + y;
-                if (!(d[id] >= 0.0)) throw ContractError("TransmissionData: d must be >= 0");
-                if (!(I0[id] > 0.0)) throw ContractError("TransmissionData: I0 must be > 0");
-            }
+        std::atomic<int> bad{0};
+        host_par(c->Ml, [&](uint64_t lo, uint64_t hi) {
+            int b = 0;
+            for (int s = 0; s < c->nzl; ++s)
+                for (uint64_t y = lo; y < hi; ++y) {
+                    const uint64_t id = (uint64_t)(c->s0 + s) * c->M + c->row0 + y;
+                    if (!(d[id] >= 0.0)) b |= 1;
+                    if (!(I0[id] > 0.0)) b |= 2;
+                }
+            bad.fetch_or(b);
+        });
+        if (bad & 1) throw ContractError("TransmissionData: d must be >= 0");
+        if (bad & 2) throw ContractError("TransmissionData: I0 must be > 0");
         const uint64_t n = std::max<uint64_t>(MV(c), 1);
         c->d.ensure(n);
         c->I0.ensure(n);
