@@ -164,12 +164,61 @@ __global__ void __launch_bounds__(256, 4) k_split3(uint64_t nlist, int nz, const
     }
 }
 
-// Haar tiles of a slab: one CTA per (2^L x 2^L tile, chunk of SC slices).
-// Same per-2x2 operation order as k_tile, per slice.
+// Haar tiles of a slab: one CTA per (2^L x 2^L tile, chunk of sc slices); every
+// level step works on all sc slices at once (one __syncthreads per step, not
+// per slice).  Same per-2x2 operation order as k_tile.
 // mode 0: synthesis beta -> mu (and mu64); mode 1: analysis + root solve +
-// synthesis; mode 2: analysis only (g -> out).
-constexpr int SC3 = 8;  // slices per CTA
-__global__ void k_tile3(int mode, int nx, int ny, int nz, int P, int L, const double* __restrict__ g,
+// synthesis; mode 2: analysis only (g -> out).  Slab stride P.
+__device__ __forceinline__ void tiles_fwd(double* x, double* t, int TS, int L, int ns) {
+    const int T2 = TS * TS;
+    for (int l = 1; l <= L; ++l) {
+        const int s = TS >> (l - 1), h2 = s >> 1, g2 = h2 * h2;
+        for (int i = threadIdx.x; i < g2 * ns; i += blockDim.x) {
+            const int sl = i / g2, r = i % g2, gi = r / h2, gj = r % h2;
+            const double* xs = x + sl * T2;
+            double* ts = t + sl * T2;
+            const double a = xs[(2 * gi) * TS + 2 * gj], b = xs[(2 * gi) * TS + 2 * gj + 1];
+            const double c = xs[(2 * gi + 1) * TS + 2 * gj], d = xs[(2 * gi + 1) * TS + 2 * gj + 1];
+            const double s1 = a + b, s2 = c + d, d1 = a - b, d2 = c - d;
+            ts[gi * TS + gj] = (s1 + s2) * 0.5;
+            ts[(gi + h2) * TS + gj] = (s1 - s2) * 0.5;
+            ts[gi * TS + gj + h2] = (d1 + d2) * 0.5;
+            ts[(gi + h2) * TS + gj + h2] = (d1 - d2) * 0.5;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < s * s * ns; i += blockDim.x) {
+            const int sl = i / (s * s), r = i % (s * s);
+            x[sl * T2 + (r / s) * TS + r % s] = t[sl * T2 + (r / s) * TS + r % s];
+        }
+        __syncthreads();
+    }
+}
+__device__ __forceinline__ void tiles_inv(double* x, double* t, int TS, int L, int ns) {
+    const int T2 = TS * TS;
+    for (int l = L; l >= 1; --l) {
+        const int s = TS >> (l - 1), h2 = s >> 1, g2 = h2 * h2;
+        for (int i = threadIdx.x; i < g2 * ns; i += blockDim.x) {
+            const int sl = i / g2, r = i % g2, gi = r / h2, gj = r % h2;
+            const double* xs = x + sl * T2;
+            double* ts = t + sl * T2;
+            const double A = xs[gi * TS + gj], H = xs[(gi + h2) * TS + gj];
+            const double V = xs[gi * TS + gj + h2], D = xs[(gi + h2) * TS + gj + h2];
+            const double p = A + H, m = A - H, r2 = V + D, u = V - D;
+            ts[(2 * gi) * TS + 2 * gj] = (p + r2) * 0.5;
+            ts[(2 * gi) * TS + 2 * gj + 1] = (p - r2) * 0.5;
+            ts[(2 * gi + 1) * TS + 2 * gj] = (m + u) * 0.5;
+            ts[(2 * gi + 1) * TS + 2 * gj + 1] = (m - u) * 0.5;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < s * s * ns; i += blockDim.x) {
+            const int sl = i / (s * s), r = i % (s * s);
+            x[sl * T2 + (r / s) * TS + r % s] = t[sl * T2 + (r / s) * TS + r % s];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_tile3(int mode, int nx, int ny, int nz, int P, int L, int sc, const double* __restrict__ g,
                         const double* __restrict__ bm, const double* __restrict__ bdata,
                         const uint8_t* __restrict__ act, ActOff off, float* __restrict__ beta,
                         float* __restrict__ mu, double* __restrict__ mu64, double* __restrict__ out,
@@ -177,19 +226,19 @@ __global__ void k_tile3(int mode, int nx, int ny, int nz, int P, int L, const do
                         unsigned long long* __restrict__ counters, int* __restrict__ flag) {
     extern __shared__ double sm3[];
     const int TS = 1 << L, T2 = TS * TS;
-    const int ti = blockIdx.y, tj = blockIdx.x, s0 = blockIdx.z * SC3;
-    const int ns = min(SC3, nz - s0);
-    double* xs = sm3;                 // [SC3][T2]
-    double* ts = sm3 + SC3 * T2;      // scratch
+    const int ti = blockIdx.y, tj = blockIdx.x, s0 = blockIdx.z * sc;
+    const int ns = min(sc, nz - s0);
+    double* xs = sm3;                 // [sc][T2]
+    double* ts = sm3 + sc * T2;       // [sc][T2] scratch
     const uint64_t base = (uint64_t)ti * TS * nx + (uint64_t)tj * TS;
-    // load: voxel-major, slices contiguous (coalesced over the slice chunk)
+    // voxel-major, slices fastest: contiguous ns*8-byte runs per voxel
     if (mode != 0) {
         for (int i = threadIdx.x; i < T2 * ns; i += blockDim.x) {
             const int v = i / ns, s = i % ns;
             xs[s * T2 + v] = g[(base + (uint64_t)(v / TS) * nx + v % TS) * P + s0 + s];
         }
         __syncthreads();
-        for (int s = 0; s < ns; ++s) tile_fwd(xs + s * T2, ts, TS, L);
+        tiles_fwd(xs, ts, TS, L, ns);
     }
     if (mode == 2) {
         for (int i = threadIdx.x; i < T2 * ns; i += blockDim.x) {
@@ -235,7 +284,7 @@ __global__ void k_tile3(int mode, int nx, int ny, int nz, int P, int L, const do
         }
     }
     __syncthreads();
-    for (int s = 0; s < ns; ++s) tile_inv(xs + s * T2, ts, TS, L);
+    tiles_inv(xs, ts, TS, L, ns);
     for (int i = threadIdx.x; i < T2 * ns; i += blockDim.x) {
         const int v = i / ns, s = i % ns;
         const uint64_t p = (base + (uint64_t)(v / TS) * nx + v % TS) * P + s0 + s;

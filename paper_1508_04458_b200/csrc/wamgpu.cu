@@ -728,11 +728,12 @@ static void tile_launch(Ctx* c, int mode, double* mu64, double* out) {
                                           c->off, c->beta.p, c->mu.p, mu64, out, c->bp_dbg.p, c->bm_dbg.p, c->Z0,
                                           c->counters.p, c->flag.p);
     } else {
-        dim3 grid(c->nx >> c->L, c->ny >> c->L, (c->nzl + SC3 - 1) / SC3);
-        const size_t smem = (size_t)(SC3 + 1) * TS * TS * sizeof(double);
+        const int sc = std::max(1, std::min({32, c->nzl, 4096 / (TS * TS)}));   // slices per CTA
+        dim3 grid(c->nx >> c->L, c->ny >> c->L, (c->nzl + sc - 1) / sc);
+        const size_t smem = 2ull * sc * TS * TS * sizeof(double);
         if (smem > 48 * 1024)
             CK(cudaFuncSetAttribute(k_tile3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_tile3<<<grid, 256, smem, c->st>>>(mode, c->nx, c->ny, c->nzl, slab_stride(c), c->L, c->g.p, c->g.p + NV(c), c->bdata.p,
+        k_tile3<<<grid, 256, smem, c->st>>>(mode, c->nx, c->ny, c->nzl, slab_stride(c), c->L, sc, c->g.p, c->g.p + NV(c), c->bdata.p,
                                             c->act.p, c->off, c->beta.p, c->mu.p, mu64, out, c->bp_dbg.p,
                                             c->bm_dbg.p, c->Z0, c->counters.p, c->flag.p);
     }

@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
+timeout 1200 python bench.py --config cfg3 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_cfg3.log 2>&1; echo "bench cfg3 rc=$?"
+tail -1 gpurun_out/bench_cfg3.log | python -c "import json,sys;d=json.loads(sys.stdin.read());print(d['value'],d['e2e']['value'],d['ray_voxel_updates_per_s'],json.dumps(d['kernels']['per_step_ms']))"
+timeout 1200 python bench.py --config cfg5 --steps 2 --warmup 1 --cpu-iters 1 > gpurun_out/bench_cfg5.log 2>&1; echo "bench cfg5 rc=$?"
+tail -1 gpurun_out/bench_cfg5.log | python -c "import json,sys;d=json.loads(sys.stdin.read());print(d['value'],d['e2e']['value'],json.dumps(d['cpu_baseline']))"
+nvidia-smi --query-gpu=memory.used,memory.total --format=csv
+/usr/bin/time -v timeout 1800 python bench.py --config cfg4 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/bench_cfg4.log 2> gpurun_out/bench_cfg4.err; echo "bench cfg4 rc=$?"
+tail -1 gpurun_out/bench_cfg4.log | cut -c1-1500; grep -E "Maximum resident|Elapsed" gpurun_out/bench_cfg4.err; tail -3 gpurun_out/bench_cfg4.err
