@@ -523,7 +523,8 @@ static void launch_walk_lv(Ctx* c, unsigned long long* cnt, const unsigned long 
 #define LV_CASE(LV)                                                                                              \
     case LV: {                                                                                                   \
         auto kf = k_walk_lv<MODE, LV>;                                                                           \
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        /* static smem (~10 KB) + the bit-packed tree may exceed the 48 KB default */                            \
+        if (smem > 32 * 1024) CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
         kf<<<nb, 32 * nlev, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, nlev, c->tbits.p, c->boff,      \
                                            c->tree_words, \
                                          c->zA.p, c->zrow.p, cnt, pos, keys, vals);                               \
