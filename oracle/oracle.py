@@ -210,6 +210,9 @@ class Problem:
         return dict(mu=mu, q=q, Z0=z0.value, b=b)
 
     # --- WAM
+    def set_haar_dim(self, dim):
+        _chk(lib().orc_set_haar_dim(self.h, int(dim)))
+
     def wam_init(self, d, I0, L, init_beta=None):
         self._d = np.ascontiguousarray(d, np.float64)
         self._I0 = np.ascontiguousarray(I0, np.float64)
@@ -288,6 +291,20 @@ def idwt2(x, nx, ny, L):
     ns = x.size // (nx * ny)
     out = np.empty_like(x)
     _chk(lib().orc_idwt2(nx, ny, ns, int(L), P(x), P(out)))
+    return out
+
+
+def dwt3(x, nx, ny, nz, L):
+    x = np.ascontiguousarray(x, np.float64)
+    out = np.empty_like(x)
+    _chk(lib().orc_dwt3(nx, ny, nz, int(L), P(x), P(out)))
+    return out
+
+
+def idwt3(x, nx, ny, nz, L):
+    x = np.ascontiguousarray(x, np.float64)
+    out = np.empty_like(x)
+    _chk(lib().orc_idwt3(nx, ny, nz, int(L), P(x), P(out)))
     return out
 
 

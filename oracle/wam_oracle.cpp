@@ -42,6 +42,7 @@
 #include "wam_oracle.h"
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -285,6 +286,12 @@ struct orc_problem {
     double Z0 = 0.0;
     int64_t cum = 0, degen = 0;
     int wam_iter = 0;
+    // separable 3D Haar (pin P3): act[l] is over (nz>>l, ny>>l, nx>>l) blocks
+    bool haar3 = false;
+    // mirror mode, 3D: Psi lists per (level, in-plane block) with any active z-block
+    std::vector<std::vector<uint64_t>> psi_ptr;            // [l][b + 1]
+    std::vector<std::vector<uint32_t>> psi_ray;            // [l][entry]
+    std::vector<std::vector<std::array<float, 4>>> psi_val; // [l][entry] A, H, V, D (2^-l scaled)
     // mirror mode: explicit negative-phi columns for active details, per slice-0 Mallat z
     std::vector<uint64_t> nphi_ptr;
     std::vector<uint32_t> nphi_row;
@@ -464,7 +471,8 @@ static inline BlockIdx mallat(int nx, int ny, int l, int bi, int bj) {
 //   D = (TL+BR)-(TR+BL);  phi = 2^-l * (A | H | V | D)   (A only at l == L).
 // Sign patterns: H + on the top half, V + on the left half, D + on TL/BR
 // (Haar analysis of DESIGN.md §3).  cb(level, bi, bj, phiA, phiH, phiV, phiD)
-// fires for every block in ray order within each level.
+// fires for every block in ray order within each level (phiA = 2^-l A at every
+// level; the 2D model uses it at l == L, the separable 3D model at all levels).
 template <typename CB>
 static void phi_walk(const orc_problem* p, int L, uint64_t y, CB&& cb) {
     const int nx = p->g.nx;
@@ -483,7 +491,7 @@ static void phi_walk(const orc_problem* p, int L, uint64_t y, CB&& cb) {
         const double st = TL + TR, sb = BL + BR;
         const double H = st - sb, V = (TL + BL) - (TR + BR), D = (TL + BR) - (TR + BL);
         const double sc = std::ldexp(1.0, -l);
-        cb(l, cbi[l], cbj[l], (l == L) ? (st + sb) * sc : 0.0, H * sc, V * sc, D * sc);
+        cb(l, cbi[l], cbj[l], (st + sb) * sc, H * sc, V * sc, D * sc);
         q[l][0] = q[l][1] = q[l][2] = q[l][3] = 0.0;
     };
     for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) {
@@ -522,10 +530,11 @@ static double z_row(const orc_problem* p, uint64_t y) {
     return z;
 }
 
+static double z_row3(const orc_problem* p, uint64_t y);
 static void compute_z0(orc_problem* p) {
     std::vector<double> zr(p->Ms);
     parallel_for(p->Ms, p->threads, [&](std::size_t lo, std::size_t hi, int) {
-        for (std::size_t y = lo; y < hi; ++y) zr[y] = z_row(p, y);
+        for (std::size_t y = lo; y < hi; ++y) zr[y] = p->haar3 ? z_row3(p, y) : z_row(p, y);
     });
     double m = 0.0;
     for (double v : zr) m = std::max(m, v);
@@ -671,12 +680,278 @@ static void set_data(orc_problem* p, const double* d, const double* I0) {
     }
 }
 
+static void idwt3(int nx, int ny, int nz, int L, const double* in, double* out);
 static std::vector<double> image_of_beta(const orc_problem* p, bool round_storage) {
     std::vector<double> mu(p->beta.size());
-    idwt2(p->g.nx, p->g.ny, p->nz, p->L, p->beta.data(), mu.data());
+    if (p->haar3) idwt3(p->g.nx, p->g.ny, p->g.nz, p->L, p->beta.data(), mu.data());
+    else idwt2(p->g.nx, p->g.ny, p->nz, p->L, p->beta.data(), mu.data());
     if (round_storage)
         for (auto& v : mu) v = p->st(v);
     return mu;
+}
+
+
+// ======================================================================
+// Separable 3D Haar (pin P3): the same 1D orthonormal step
+// along z on top of the in-plane 2D step.  One level on the leading
+// d x h x w region of the volume (z-major, row stride nx, plane stride N):
+// each z-plane pair (2k, 2k+1) gets the in-plane 2D step (DESIGN.md §3 order)
+// giving (A,H,V,D)_0 and (A,H,V,D)_1, then low = (P0+P1)*c, high = (P0-P1)*c
+// with c = 1/sqrt(2) rounded to double.  Mallat positions: low at plane k,
+// high at plane k + d/2; in-plane positions as in 2D.
+static constexpr double kC3 = 0.70710678118654752440;
+
+static inline double cpow3(int l) {  // c^l by repeated multiplication (GPU mirrors this)
+    double c = 1.0;
+    for (int i = 0; i < l; ++i) c *= kC3;
+    return c;
+}
+
+static void haar3_fwd_level(double* x, int nx, int N, int d, int h, int w, std::vector<double>& tmp) {
+    tmp.assign((std::size_t)d * h * w, 0.0);
+    const int d2 = d / 2, h2 = h / 2, w2 = w / 2;
+    auto at = [&](int z, int i, int j) -> double& { return x[(std::size_t)z * N + (std::size_t)i * nx + j]; };
+    auto tt = [&](int z, int i, int j) -> double& { return tmp[((std::size_t)z * h + i) * w + j]; };
+    for (int k = 0; k < d2; ++k)
+        for (int i = 0; i < h2; ++i)
+            for (int j = 0; j < w2; ++j) {
+                double P[2][4];
+                for (int e = 0; e < 2; ++e) {
+                    const int z = 2 * k + e;
+                    const double a = at(z, 2 * i, 2 * j), b = at(z, 2 * i, 2 * j + 1);
+                    const double c = at(z, 2 * i + 1, 2 * j), dd = at(z, 2 * i + 1, 2 * j + 1);
+                    const double s1 = a + b, s2 = c + dd, d1 = a - b, d2v = c - dd;
+                    P[e][0] = (s1 + s2) * 0.5; P[e][1] = (s1 - s2) * 0.5;
+                    P[e][2] = (d1 + d2v) * 0.5; P[e][3] = (d1 - d2v) * 0.5;
+                }
+                const int pi[4] = {i, i + h2, i, i + h2}, pj[4] = {j, j, j + w2, j + w2};
+                for (int t = 0; t < 4; ++t) {
+                    tt(k, pi[t], pj[t]) = (P[0][t] + P[1][t]) * kC3;
+                    tt(k + d2, pi[t], pj[t]) = (P[0][t] - P[1][t]) * kC3;
+                }
+            }
+    for (int z = 0; z < d; ++z)
+        for (int i = 0; i < h; ++i)
+            for (int j = 0; j < w; ++j) at(z, i, j) = tt(z, i, j);
+}
+
+static void haar3_inv_level(double* x, int nx, int N, int d, int h, int w, std::vector<double>& tmp) {
+    tmp.assign((std::size_t)d * h * w, 0.0);
+    const int d2 = d / 2, h2 = h / 2, w2 = w / 2;
+    auto at = [&](int z, int i, int j) -> double& { return x[(std::size_t)z * N + (std::size_t)i * nx + j]; };
+    auto tt = [&](int z, int i, int j) -> double& { return tmp[((std::size_t)z * h + i) * w + j]; };
+    for (int k = 0; k < d2; ++k)
+        for (int i = 0; i < h2; ++i)
+            for (int j = 0; j < w2; ++j) {
+                const int pi[4] = {i, i + h2, i, i + h2}, pj[4] = {j, j, j + w2, j + w2};
+                double P[2][4];
+                for (int t = 0; t < 4; ++t) {
+                    const double lo = at(k, pi[t], pj[t]), hi = at(k + d2, pi[t], pj[t]);
+                    P[0][t] = (lo + hi) * kC3;
+                    P[1][t] = (lo - hi) * kC3;
+                }
+                for (int e = 0; e < 2; ++e) {
+                    const int z = 2 * k + e;
+                    const double A = P[e][0], H = P[e][1], V = P[e][2], D = P[e][3];
+                    const double pp = A + H, mm = A - H, r = V + D, t2 = V - D;
+                    tt(z, 2 * i, 2 * j) = (pp + r) * 0.5;
+                    tt(z, 2 * i, 2 * j + 1) = (pp - r) * 0.5;
+                    tt(z, 2 * i + 1, 2 * j) = (mm + t2) * 0.5;
+                    tt(z, 2 * i + 1, 2 * j + 1) = (mm - t2) * 0.5;
+                }
+            }
+    for (int z = 0; z < d; ++z)
+        for (int i = 0; i < h; ++i)
+            for (int j = 0; j < w; ++j) at(z, i, j) = tt(z, i, j);
+}
+
+static void check_haar3_dims(int nx, int ny, int nz, int L) {
+    check_haar_dims(nx, ny, L);
+    if ((nz % (1 << L)) != 0) throw config_error("haar3: nz not divisible by 2^L");
+}
+static void dwt3(int nx, int ny, int nz, int L, const double* in, double* out) {
+    check_haar3_dims(nx, ny, nz, L);
+    const std::size_t N = (std::size_t)nx * ny;
+    std::copy(in, in + N * nz, out);
+    std::vector<double> tmp;
+    for (int l = 1; l <= L; ++l) haar3_fwd_level(out, nx, (int)N, nz >> (l - 1), ny >> (l - 1), nx >> (l - 1), tmp);
+}
+static void idwt3(int nx, int ny, int nz, int L, const double* in, double* out) {
+    check_haar3_dims(nx, ny, nz, L);
+    const std::size_t N = (std::size_t)nx * ny;
+    std::copy(in, in + N * nz, out);
+    std::vector<double> tmp;
+    for (int l = L; l >= 1; --l) haar3_inv_level(out, nx, (int)N, nz >> (l - 1), ny >> (l - 1), nx >> (l - 1), tmp);
+}
+
+// 3D Mallat indices of level-l block (bk, bi, bj): [0] approx (l == L), then the
+// 7 details in the fixed order Hl, Vl, Dl, Ah, Hh, Vh, Dh (l = z low / h = z high).
+static inline void mallat3(int nx, int ny, int nz, int l, int bk, int bi, int bj, uint64_t (&z)[8]) {
+    const uint64_t N = (uint64_t)nx * ny;
+    const int dl = nz >> l, hl = ny >> l, wl = nx >> l;
+    auto ix3 = [&](int zz, int yy, int xx) { return (uint64_t)zz * N + (uint64_t)yy * nx + xx; };
+    z[0] = ix3(bk, bi, bj);
+    z[1] = ix3(bk, hl + bi, bj); z[2] = ix3(bk, bi, wl + bj); z[3] = ix3(bk, hl + bi, wl + bj);
+    z[4] = ix3(dl + bk, bi, bj); z[5] = ix3(dl + bk, hl + bi, bj); z[6] = ix3(dl + bk, bi, wl + bj);
+    z[7] = ix3(dl + bk, hl + bi, wl + bj);
+}
+static inline std::size_t blk3(const orc_problem* p, int l, int bk, int bi, int bj) {
+    return ((std::size_t)bk * (p->g.ny >> l) + bi) * (p->g.nx >> l) + bj;
+}
+static inline bool active3(const orc_problem* p, int l, int bk, int bi, int bj) {
+    return p->act[l][blk3(p, l, bk, bi, bj)] != 0;
+}
+
+// Z(y, s) = zA(y) + tot_L(y, k_L(s)) + ... + tot_1(y, k_1(s)) with
+//   zA = sum over level-L in-plane blocks (ray order) of |psi_A c^L|,
+//   tot_l(y, k) = sum over level-l in-plane blocks b (ray order) with (k, b)
+//   active of t(b) = |Hl|+|Vl|+|Dl|+|Ah|+|Hh|+|Vh|+|Dh| (that order, each psi c^l).
+// Returns max_s Z(y, s) (Eq. 1.61 over the rays of every slice).
+static double z_row3(const orc_problem* p, uint64_t y) {
+    const int L = p->L, nz = p->g.nz;
+    double zA = 0.0;
+    std::vector<std::vector<double>> tot(L + 1);
+    for (int l = 1; l <= L; ++l) tot[l].assign(nz >> l, 0.0);
+    const double cL = cpow3(L);
+    phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {
+        const double cl = cpow3(l);
+        if (l == L) zA += std::fabs(pA * cL);
+        const double h = std::fabs(pH * cl), v = std::fabs(pV * cl), dd = std::fabs(pD * cl), a = std::fabs(pA * cl);
+        const double t = (((((h + v) + dd) + a) + h) + v) + dd;
+        for (int k = 0; k < (nz >> l); ++k)
+            if (active3(p, l, k, bi, bj)) tot[l][k] += t;
+    });
+    double best = 0.0;
+    for (int s = 0; s < nz; ++s) {
+        double z = zA;
+        for (int l = L; l >= 1; --l) z += tot[l][s >> l];
+        best = std::max(best, z);
+    }
+    return best;
+}
+
+// Psi lists (mirror mode): per (level l, in-plane block b) with ANY active z-block,
+// the rays crossing b (ascending) with fp32 psi_A, psi_H, psi_V, psi_D.
+static void build_psi3(orc_problem* p) {
+    const int L = p->L, nx = p->g.nx, ny = p->g.ny, nz = p->g.nz;
+    p->psi_ptr.assign(L + 1, {});
+    p->psi_ray.assign(L + 1, {});
+    p->psi_val.assign(L + 1, {});
+    std::vector<std::vector<uint8_t>> anyk(L + 1);
+    for (int l = 1; l <= L; ++l) {
+        const int hl = ny >> l, wl = nx >> l;
+        anyk[l].assign((std::size_t)hl * wl, 0);
+        for (int k = 0; k < (nz >> l); ++k)
+            for (int bi = 0; bi < hl; ++bi)
+                for (int bj = 0; bj < wl; ++bj)
+                    if (active3(p, l, k, bi, bj)) anyk[l][(std::size_t)bi * wl + bj] = 1;
+    }
+    std::vector<std::vector<std::vector<std::pair<uint32_t, std::array<float, 4>>>>> cols(L + 1);
+    for (int l = 1; l <= L; ++l) cols[l].resize((std::size_t)(ny >> l) * (nx >> l));
+    for (uint64_t y = 0; y < p->Ms; ++y)
+        phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {
+            const std::size_t b = (std::size_t)bi * (nx >> l) + bj;
+            if (!anyk[l][b]) return;
+            cols[l][b].push_back({(uint32_t)y, {(float)pA, (float)pH, (float)pV, (float)pD}});
+        });
+    for (int l = 1; l <= L; ++l) {
+        const std::size_t nb = cols[l].size();
+        p->psi_ptr[l].assign(nb + 1, 0);
+        for (std::size_t b = 0; b < nb; ++b) p->psi_ptr[l][b + 1] = p->psi_ptr[l][b] + cols[l][b].size();
+        for (std::size_t b = 0; b < nb; ++b)
+            for (auto& e : cols[l][b]) { p->psi_ray[l].push_back(e.first); p->psi_val[l].push_back(e.second); }
+    }
+}
+
+// b-(z) of every active 3D detail (mirror mode, from the Psi lists):
+//   z-low  subband p: sum_y [psi_p < 0] psi_p c^l (Qlo + Qhi)
+//   z-high subband p: sum_y psi_p < 0 ? psi_p c^l Qlo : (psi_p > 0 ? -psi_p c^l Qhi : 0)
+// with Qlo / Qhi the ray-wise sums of q over the lower / upper half of the
+// z-block's slices (ascending slice order).  Rays ascending within a list.
+static void split3_mirror(const orc_problem* p, const std::vector<double>& q, std::vector<double>& bm) {
+    const int L = p->L, nx = p->g.nx, ny = p->g.ny, nz = p->g.nz;
+    const uint64_t M = p->Ms;
+    bm.assign(p->Ns * nz, 0.0);
+    for (int l = 1; l <= L; ++l) {
+        const double cl = cpow3(l);
+        const int hw = 1 << (l - 1);
+        for (int bi = 0; bi < (ny >> l); ++bi)
+            for (int bj = 0; bj < (nx >> l); ++bj) {
+                const std::size_t b = (std::size_t)bi * (nx >> l) + bj;
+                for (int k = 0; k < (nz >> l); ++k) {
+                    if (!active3(p, l, k, bi, bj)) continue;
+                    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+                    for (uint64_t e = p->psi_ptr[l][b]; e < p->psi_ptr[l][b + 1]; ++e) {
+                        const uint64_t y = p->psi_ray[l][e];
+                        const auto& ps = p->psi_val[l][e];
+                        double qlo = 0.0, qhi = 0.0;
+                        for (int s = 0; s < hw; ++s) qlo += q[(uint64_t)(k * 2 * hw + s) * M + y];
+                        for (int s = 0; s < hw; ++s) qhi += q[(uint64_t)(k * 2 * hw + hw + s) * M + y];
+                        const double qall = qlo + qhi;
+                        const double A = (double)ps[0] * cl, H = (double)ps[1] * cl, V = (double)ps[2] * cl,
+                                     D = (double)ps[3] * cl;
+                        const double lowp[3] = {H, V, D}, highp[4] = {A, H, V, D};
+                        for (int t = 0; t < 3; ++t)
+                            if (lowp[t] < 0.0) acc[t] += lowp[t] * qall;
+                        for (int t = 0; t < 4; ++t) {
+                            if (highp[t] < 0.0) acc[3 + t] += highp[t] * qlo;
+                            else if (highp[t] > 0.0) acc[3 + t] += -highp[t] * qhi;
+                        }
+                    }
+                    uint64_t z[8];
+                    mallat3(nx, ny, nz, l, k, bi, bj, z);
+                    for (int t = 0; t < 7; ++t) bm[z[1 + t]] = acc[t];
+                }
+            }
+    }
+}
+
+// Direct signed split (reference precision, 3D): b+ / b- for every active z
+// (or every z with all_coeffs) from the exact phi(y_s|z) = psi c^l sigma_z(s).
+static void direct_split3(const orc_problem* p, const std::vector<double>& w, std::vector<double>& bp,
+                          std::vector<double>& bm, bool all_coeffs) {
+    const int L = p->L, nx = p->g.nx, ny = p->g.ny, nz = p->g.nz;
+    const uint64_t M = p->Ms, NT = p->Ns * nz;
+    int nt = resolve_threads(p->threads);
+    std::vector<std::vector<double>> tp(nt), tm(nt);
+    parallel_for(M, nt, [&](std::size_t lo, std::size_t hi, int bt) {
+        tp[bt].assign(NT, 0.0); tm[bt].assign(NT, 0.0);
+        auto& P = tp[bt]; auto& Mn = tm[bt];
+        auto add = [&](uint64_t z, double t, double phi) {
+            if (phi > 0.0) P[z] += t; else if (phi < 0.0) Mn[z] += t;
+        };
+        for (std::size_t y = lo; y < hi; ++y)
+            phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {
+                const double cl = cpow3(l), cL = cpow3(L);
+                const int hw = 1 << (l - 1);
+                for (int s = 0; s < nz; ++s) {
+                    const double qy = w[(uint64_t)s * M + y];
+                    const int k = s >> l;
+                    const double sg = ((s >> (l - 1)) & 1) ? -1.0 : 1.0;
+                    (void)hw;
+                    uint64_t z[8];
+                    mallat3(nx, ny, nz, l, k, bi, bj, z);
+                    if (l == L) { const double ph = pA * cL; add(z[0], qy * ph, ph); }
+                    if (!all_coeffs && !active3(p, l, k, bi, bj)) continue;
+                    const double ph[7] = {pH * cl, pV * cl, pD * cl, pA * cl * sg, pH * cl * sg, pV * cl * sg,
+                                          pD * cl * sg};
+                    for (int t = 0; t < 7; ++t) add(z[1 + t], qy * ph[t], ph[t]);
+                }
+            });
+    });
+    bp.assign(NT, 0.0); bm.assign(NT, 0.0);
+    for (int b = 0; b < nt; ++b) {
+        if (tp[b].empty()) continue;
+        for (uint64_t z = 0; z < NT; ++z) { bp[z] += tp[b][z]; bm[z] += tm[b][z]; }
+    }
+}
+
+static int64_t active_count3(const orc_problem* p) {
+    const int L = p->L, nx = p->g.nx, ny = p->g.ny, nz = p->g.nz;
+    int64_t c = (int64_t)(nx >> L) * (ny >> L) * (nz >> L);
+    for (int l = 1; l <= L; ++l)
+        for (uint8_t a : p->act[l]) c += 7 * (int64_t)(a != 0);
+    return c;
 }
 
 }  // namespace orc
@@ -864,6 +1139,13 @@ int orc_idwt2(int nx, int ny, int ns, int L, const double* in, double* out) {
     ORC_TRY({ idwt2(nx, ny, ns, L, in, out); })
 }
 
+int orc_dwt3(int nx, int ny, int nz, int L, const double* in, double* out) {
+    ORC_TRY({ dwt3(nx, ny, nz, L, in, out); })
+}
+int orc_idwt3(int nx, int ny, int nz, int L, const double* in, double* out) {
+    ORC_TRY({ idwt3(nx, ny, nz, L, in, out); })
+}
+
 int orc_solve_update(double b, double bp, double bm, double Z0, double beta, double* out) {
     try { return solve_update(b, bp, bm, Z0, beta, out); }
     catch (const orc::Error& e) { g_err = e.what(); return -e.code; }
@@ -931,14 +1213,24 @@ int orc_am_get(const orc_problem* p, double* mu, double* q, double* Z0, double* 
 }
 
 // ---------------- wavelet-am, SPEC.md:353-389 ----------------
+int orc_set_haar_dim(orc_problem* p, int dim) {
+    ORC_TRY({
+        if (dim != 2 && dim != 3) throw config_error("haar: dimension must be 2 or 3");
+        p->haar3 = dim == 3;
+        p->wam_ready = false;
+    })
+}
+
 int orc_wam_init(orc_problem* p, const double* d, const double* I0, int L, const double* init_beta) {
     ORC_TRY({
-        check_haar_dims(p->g.nx, p->g.ny, L);
+        if (p->haar3) check_haar3_dims(p->g.nx, p->g.ny, p->g.nz, L);
+        else check_haar_dims(p->g.nx, p->g.ny, L);
         set_data(p, d, I0);
         p->L = L;
         const uint64_t NT = p->Ns * p->nz;
         p->act.assign(L + 1, {});
-        for (int l = 1; l <= L; ++l) p->act[l].assign((std::size_t)(p->g.nx >> l) * (p->g.ny >> l), 0);
+        for (int l = 1; l <= L; ++l)
+            p->act[l].assign((std::size_t)(p->g.nx >> l) * (p->g.ny >> l) * (p->haar3 ? (p->g.nz >> l) : 1), 0);
         p->beta.assign(NT, 0.0);
         if (init_beta)
             for (uint64_t z = 0; z < NT; ++z) p->beta[z] = p->st(init_beta[z]);
@@ -947,11 +1239,12 @@ int orc_wam_init(orc_problem* p, const double* d, const double* I0, int L, const
             std::vector<double> g(NT);
             back(p, p->d.data(), g.data());
             p->bdata.resize(NT);
-            dwt2(p->g.nx, p->g.ny, p->nz, L, g.data(), p->bdata.data());
-            build_nphi(p);
+            if (p->haar3) { dwt3(p->g.nx, p->g.ny, p->g.nz, L, g.data(), p->bdata.data()); build_psi3(p); }
+            else { dwt2(p->g.nx, p->g.ny, p->nz, L, g.data(), p->bdata.data()); build_nphi(p); }
         } else {
             std::vector<double> bp, bm;
-            direct_split(p, p->d, bp, bm, true);
+            if (p->haar3) direct_split3(p, p->d, bp, bm, true);
+            else direct_split(p, p->d, bp, bm, true);
             p->bdata.resize(NT);
             for (uint64_t z = 0; z < NT; ++z) p->bdata[z] = bp[z] + bm[z];
         }
@@ -968,24 +1261,31 @@ int orc_wam_init(orc_problem* p, const double* d, const double* I0, int L, const
 int orc_wam_iterate(orc_problem* p, int n, orc_record* recs) {
     ORC_TRY({
         if (!p->wam_ready) throw contract_error("wam: not initialised");
-        const int L = p->L, nx = p->g.nx, ny = p->g.ny;
+        const int L = p->L, nx = p->g.nx, ny = p->g.ny, nz = p->g.nz;
         const uint64_t N = p->Ns, NT = N * p->nz;
         for (int it = 0; it < n; ++it) {
             std::vector<double> bp, bm;
             if (p->mirror) {
                 std::vector<double> g(NT), S(NT);
                 back(p, p->q.data(), g.data());
-                dwt2(nx, ny, p->nz, L, g.data(), S.data());
-                bm.assign(NT, 0.0);
-                for (int s = 0; s < p->nz; ++s)
-                    for (uint64_t z = 0; z < N; ++z) {
-                        double acc = 0.0;
-                        for (uint64_t k = p->nphi_ptr[z]; k < p->nphi_ptr[z + 1]; ++k)
-                            acc += p->q[(uint64_t)s * p->Ms + p->nphi_row[k]] * p->nphi_val[k];
-                        bm[(uint64_t)s * N + z] = acc;
-                    }
+                if (p->haar3) {
+                    dwt3(nx, ny, nz, L, g.data(), S.data());
+                    split3_mirror(p, p->q, bm);
+                } else {
+                    dwt2(nx, ny, p->nz, L, g.data(), S.data());
+                    bm.assign(NT, 0.0);
+                    for (int s = 0; s < p->nz; ++s)
+                        for (uint64_t z = 0; z < N; ++z) {
+                            double acc = 0.0;
+                            for (uint64_t k = p->nphi_ptr[z]; k < p->nphi_ptr[z + 1]; ++k)
+                                acc += p->q[(uint64_t)s * p->Ms + p->nphi_row[k]] * p->nphi_val[k];
+                            bm[(uint64_t)s * N + z] = acc;
+                        }
+                }
                 bp.resize(NT);
                 for (uint64_t z = 0; z < NT; ++z) bp[z] = S[z] - bm[z];
+            } else if (p->haar3) {
+                direct_split3(p, p->q, bp, bm, false);
             } else {
                 direct_split(p, p->q, bp, bm, false);
             }
@@ -997,17 +1297,32 @@ int orc_wam_iterate(orc_problem* p, int n, orc_record* recs) {
                 if (r == 0) { p->beta[z] = p->st(nb); ++upd; }
                 else if (r == 2) ++deg;
             };
-            for (int s = 0; s < p->nz; ++s) {
-                const uint64_t off = (uint64_t)s * N;
-                for (int bi = 0; bi < (ny >> L); ++bi)
-                    for (int bj = 0; bj < (nx >> L); ++bj) visit(off + (uint64_t)bi * nx + bj);
+            if (p->haar3) {
+                for (int k = 0; k < (nz >> L); ++k)
+                    for (int bi = 0; bi < (ny >> L); ++bi)
+                        for (int bj = 0; bj < (nx >> L); ++bj) visit((uint64_t)k * N + (uint64_t)bi * nx + bj);
                 for (int l = 1; l <= L; ++l)
-                    for (int bi = 0; bi < (ny >> l); ++bi)
-                        for (int bj = 0; bj < (nx >> l); ++bj) {
-                            if (!is_active(p, l, bi, bj)) continue;
-                            BlockIdx z = mallat(nx, ny, l, bi, bj);
-                            visit(off + z.H); visit(off + z.V); visit(off + z.D);
-                        }
+                    for (int k = 0; k < (nz >> l); ++k)
+                        for (int bi = 0; bi < (ny >> l); ++bi)
+                            for (int bj = 0; bj < (nx >> l); ++bj) {
+                                if (!active3(p, l, k, bi, bj)) continue;
+                                uint64_t z[8];
+                                mallat3(nx, ny, nz, l, k, bi, bj, z);
+                                for (int t = 1; t < 8; ++t) visit(z[t]);
+                            }
+            } else {
+                for (int s = 0; s < p->nz; ++s) {
+                    const uint64_t off = (uint64_t)s * N;
+                    for (int bi = 0; bi < (ny >> L); ++bi)
+                        for (int bj = 0; bj < (nx >> L); ++bj) visit(off + (uint64_t)bi * nx + bj);
+                    for (int l = 1; l <= L; ++l)
+                        for (int bi = 0; bi < (ny >> l); ++bi)
+                            for (int bj = 0; bj < (nx >> l); ++bj) {
+                                if (!is_active(p, l, bi, bj)) continue;
+                                BlockIdx z = mallat(nx, ny, l, bi, bj);
+                                visit(off + z.H); visit(off + z.V); visit(off + z.D);
+                            }
+                }
             }
             p->bp_last = bp; p->bm_last = bm;
             p->cum += upd; p->degen += deg;
@@ -1018,44 +1333,54 @@ int orc_wam_iterate(orc_problem* p, int n, orc_record* recs) {
                 recs[it].iter = p->wam_iter;
                 recs[it].objective = obj;
                 recs[it].elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - p->t0).count();
-                recs[it].active_set = active_count(p);
+                recs[it].active_set = p->haar3 ? active_count3(p) : active_count(p);
                 recs[it].cum_updates = p->cum;
             }
         }
     })
 }
 
-// expand_tree, SPEC.md:248-256, 267-268 (z-summed criterion, one level per event).
+// expand_tree.  2D model: z-summed criterion image
+// and a 2D mask shared by all slices.  3D model (pin P3): criterion on every
+// voxel, no z-sum; activation of the coarsest inactive 3D block.
 int orc_wam_expand(orc_problem* p, double factor, int64_t* newly) {
     ORC_TRY({
         if (!p->wam_ready) throw contract_error("wam: not initialised");
         const int L = p->L, nx = p->g.nx, ny = p->g.ny;
         const uint64_t N = p->Ns;
         std::vector<double> mu = image_of_beta(p, false);   // fp64 criterion image
-        std::vector<double> s(N, 0.0);
-        for (int sl = 0; sl < p->nz; ++sl)
-            for (uint64_t x = 0; x < N; ++x) s[x] += mu[(uint64_t)sl * N + x];
+        std::vector<double> s;
+        if (p->haar3) {
+            s = mu;
+        } else {
+            s.assign(N, 0.0);
+            for (int sl = 0; sl < p->nz; ++sl)
+                for (uint64_t x = 0; x < N; ++x) s[x] += mu[(uint64_t)sl * N + x];
+        }
         double mx = -std::numeric_limits<double>::infinity();
         for (double v : s) mx = std::max(mx, v);
         int64_t cnt = 0;
         if (mx > 0.0 && L > 0) {
             const double thr = factor * mx;
             auto na = p->act;
-            for (int iy = 0; iy < ny; ++iy)
-                for (int ix = 0; ix < nx; ++ix) {
-                    if (!(s[(uint64_t)iy * nx + ix] > thr)) continue;
-                    for (int l = L; l >= 1; --l) {
-                        std::size_t bidx = (std::size_t)(iy >> l) * (nx >> l) + (ix >> l);
-                        if (!p->act[l][bidx]) {
-                            if (!na[l][bidx]) { na[l][bidx] = 1; ++cnt; }
-                            break;
+            const int nzs = p->haar3 ? p->g.nz : 1;
+            for (int iz = 0; iz < nzs; ++iz)
+                for (int iy = 0; iy < ny; ++iy)
+                    for (int ix = 0; ix < nx; ++ix) {
+                        if (!(s[((uint64_t)iz * ny + iy) * nx + ix] > thr)) continue;
+                        for (int l = L; l >= 1; --l) {
+                            const std::size_t bidx = p->haar3 ? blk3(p, l, iz >> l, iy >> l, ix >> l)
+                                                              : (std::size_t)(iy >> l) * (nx >> l) + (ix >> l);
+                            if (!p->act[l][bidx]) {
+                                if (!na[l][bidx]) { na[l][bidx] = 1; ++cnt; }
+                                break;
+                            }
                         }
                     }
-                }
             p->act = na;
             if (cnt > 0) {
                 compute_z0(p);
-                if (p->mirror) build_nphi(p);
+                if (p->mirror) { if (p->haar3) build_psi3(p); else build_nphi(p); }
             }
         }
         if (newly) *newly = cnt;
@@ -1109,13 +1434,13 @@ int orc_wam_counters(const orc_problem* p, int64_t* cum, int64_t* degen, int64_t
     ORC_TRY({
         if (cum) *cum = p->cum;
         if (degen) *degen = p->degen;
-        if (act) *act = active_count(p);
+        if (act) *act = p->haar3 ? active_count3(p) : active_count(p);
     })
 }
 
 int orc_wam_z0_rows(const orc_problem* p, double* zrow) {
     ORC_TRY({
-        for (uint64_t y = 0; y < p->Ms; ++y) zrow[y] = z_row(p, y);
+        for (uint64_t y = 0; y < p->Ms; ++y) zrow[y] = p->haar3 ? z_row3(p, y) : z_row(p, y);
     })
 }
 

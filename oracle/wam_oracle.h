@@ -86,6 +86,12 @@ double orc_poisson(uint64_t seed, uint64_t stream, double mean);
 int orc_dwt2(int nx, int ny, int nslices, int L, const double* in, double* out);
 int orc_idwt2(int nx, int ny, int nslices, int L, const double* in, double* out);
 
+/* separable 3D Haar (pin P3): volume z-major, 3D Mallat layout */
+int orc_dwt3(int nx, int ny, int nz, int L, const double* in, double* out);
+int orc_idwt3(int nx, int ny, int nz, int L, const double* in, double* out);
+/* wavelet model: 2 = per-slice 2D Haar, 3 = separable 3D Haar (pin P3) */
+int orc_set_haar_dim(orc_problem* p, int dim);
+
 /* root solver (errata E1/E2); returns 0 updated, 1 skipped, 2 degenerate */
 int orc_solve_update(double b, double bp, double bm, double Z0, double beta, double* out);
 
