@@ -151,7 +151,7 @@ def _workload_desc(cfg, nnz, algo, J):
             f"axial 3D stack {cfg['nx']}x{cfg['ny']}x{cfg['nz']} (rays in-plane, one H for all slices, pin P2)")
     return (f"{cfg['name']}: {dims} @ {cfg['voxel']} mm, {cfg['views']} views x "
             f"{cfg['detectors']} arc detectors (SCD 500, SDD 1000), I0={cfg['I0']:g} Poisson, "
-            + (f"wavelet AM Haar L={cfg['L']} (2D per slice), {J} iterations, expansions {cfg['schedule']} @0.1"
+            + (f"wavelet AM Haar L={cfg['L']} ({'separable 3D' if cfg['haar'] == 3 and cfg['nz'] > 1 else '2D per slice'}), {J} iterations, expansions {cfg['schedule']} @0.1"
                if algo == "wam" else f"image-domain AM, {J} iterations") + f", nnz(H per slice)={nnz}")
 
 
@@ -183,6 +183,8 @@ def cpu_reference(cfg, algo, iters, threads=0, inputs=None):
         I0, d = inputs
     t0 = time.perf_counter()
     if algo == "wam":
+        if cfg["nz"] > 1:
+            p.set_haar_dim(cfg["haar"])
         p.wam_init(d, I0, cfg["L"])
     else:
         p.am_init(d, I0)
@@ -244,6 +246,8 @@ def main():
         uid = plumb.bcast_bytes(W.nccl_unique_id() if rank == 0 else b"")
         ctx.set_comm(uid, rank, world)
     ctx.set_geometry(g)
+    if cfg["nz"] > 1 and algo == "wam":
+        ctx.set_haar_dim(cfg["haar"])
     ctx.set_data(d, I0)
     nnz_local = ctx.nnz
 

@@ -131,6 +131,11 @@ int wamgpu_set_data(wamgpu_ctx* ctx, const double* d, const double* I0);
 int wamgpu_am_init(wamgpu_ctx* ctx, const double* init_mu);
 int wamgpu_am_iterate(wamgpu_ctx* ctx, int n, wamgpu_record* recs);
 
+/* wavelet model for nz > 1: 2 = per-slice 2D Haar with the z-summed criterion
+ * (default), 3 = separable 3D Haar octree with the per-voxel
+ * criterion (pin P3, BASELINE cfg3/cfg4).  Takes effect at the next wam_init. */
+int wamgpu_set_haar_dim(wamgpu_ctx* ctx, int dim);
+
 /* wavelet-am: init_state, wam_iterate, expand_tree, run. */
 int wamgpu_wam_init(wamgpu_ctx* ctx, int levels, const double* init_beta);
 int wamgpu_wam_iterate(wamgpu_ctx* ctx, int n, wamgpu_record* recs);

@@ -58,7 +58,7 @@ EXPORTED = [
     "wamgpu_set_data", "wamgpu_am_init", "wamgpu_am_iterate", "wamgpu_wam_init", "wamgpu_wam_iterate",
     "wamgpu_wam_expand", "wamgpu_wam_run", "wamgpu_get_image", "wamgpu_get_beta", "wamgpu_get_q",
     "wamgpu_get_tree", "wamgpu_get_stats", "wamgpu_get_scalars", "wamgpu_get_z_rows", "wamgpu_get_timing",
-    "wamgpu_set_kernel_timing", "wamgpu_rasterize", "wamgpu_simulate", "wamgpu_host_rays",
+    "wamgpu_set_kernel_timing", "wamgpu_rasterize", "wamgpu_simulate", "wamgpu_host_rays", "wamgpu_set_haar_dim",
 ]
 
 
@@ -267,6 +267,10 @@ class Context:
         return _records(recs[:n])
 
     # ---- wavelet AM
+    def set_haar_dim(self, dim):
+        """2: per-slice 2D Haar (SPEC model); 3: separable 3D Haar (pin P3)."""
+        _chk(load().wamgpu_set_haar_dim(self.h, int(dim)), self.h)
+
     def wam_init(self, levels, init_beta=None):
         b = None if init_beta is None else np.ascontiguousarray(init_beta, np.float64)
         _chk(load().wamgpu_wam_init(self.h, int(levels), _p(b)), self.h)

@@ -95,9 +95,9 @@ CONFIGS = {
     "cfg2": dict(nx=512, ny=512, nz=1, voxel=0.5, views=720, detectors=1024, I0=2e5, L=4, J=50, seed=2,
                  phantom="luggage"),
     "cfg3": dict(nx=512, ny=512, nz=64, voxel=1.0, views=720, detectors=1024, I0=2e5, L=3, J=30, seed=3,
-                 phantom="luggage"),
+                 phantom="luggage", haar=3),
     "cfg4": dict(nx=1024, ny=1024, nz=128, voxel=0.5, views=1440, detectors=1024, I0=1e5, L=4, J=40, seed=4,
-                 phantom="luggage", gain=0.2),
+                 phantom="luggage", gain=0.2, haar=3),
     "cfg5": dict(nx=512, ny=512, nz=64, voxel=1.0, views=720, detectors=1024, I0=2e5, L=0, J=30, seed=3,
                  phantom="luggage", algo="am"),
     # small parity cases (oracle finishes in seconds)
@@ -118,6 +118,7 @@ def get(name):
     c = dict(CONFIGS[name])
     c["name"] = name
     c.setdefault("algo", "wam")
+    c.setdefault("haar", 2)   # 3: separable 3D Haar (pin P3, BASELINE cfg3/cfg4)
     c["schedule"] = schedule(c["J"], c["L"]) if c["L"] > 0 else []
     return c
 

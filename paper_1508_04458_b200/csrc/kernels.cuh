@@ -566,7 +566,7 @@ __device__ __forceinline__ void add_quad(double (&q)[4], int quad, double v) {
 template <int MODE, int L>
 __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsigned long long* __restrict__ rp,
                                                           const uint2* __restrict__ A, int nx, int ny,
-                                                          const uint8_t* __restrict__ act, ActOff off,
+                                                          const uint8_t* __restrict__ act, ActOff off, double cz,
                                                           double* __restrict__ zA, double* __restrict__ zrow,
                                                           unsigned long long* __restrict__ cnt,
                                                           const unsigned long long* __restrict__ pos,
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsi
         const double TL = q[l][0], TR = q[l][1], BL = q[l][2], BR = q[l][3];
         const double st = TL + TR, sb = BL + BR;
         const double sc = 1.0 / (double)(1 << l);
-        if (MODE == 0 && l == L) totA += fabs((st + sb) * sc);
+        if (MODE == 0 && l == L) totA += fabs(((st + sb) * sc) * cz);
         if (MODE != 0 && av[l]) {
             const double pH = (st - sb) * sc, pV = ((TL + BL) - (TR + BR)) * sc, pD = ((TL + BR) - (TR + BL)) * sc;
             if (MODE == 1) tot[l] += fabs(pH) + fabs(pV) + fabs(pD);

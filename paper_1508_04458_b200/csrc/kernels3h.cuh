@@ -1,0 +1,458 @@
+// kernels3h.cuh — separable 3D Haar model of the wavelet AM (pin P3,
+// SURVEY.md App. A) on the axial 3D stack: octree of 2^l x 2^l x 2^l blocks, 7
+// details per node, criterion on every voxel (no z-sum).
+//
+// A level-l coefficient's column factorises (rays never leave their slice):
+//   phi(y_s | z) = psi_p(y | b) * c^l * sigma(s)
+// with psi_p (p in A,H,V,D) the in-plane quadrant combination of the 2D model
+// (DESIGN.md §4), c = 1/sqrt(2) and sigma = +1 (z low-pass) or +-1 on the two
+// z-halves of the block (z high-pass).  So the expansion walk stays in-plane,
+// one Psi entry (ray, psi_A, psi_H, psi_V, psi_D) per (ray, in-plane block b)
+// serves every z-block of b, and the split needs slab sums of q over z-halves.
+// Coefficients use the slab-local 3D Mallat layout stored as [yy*nx+xx][zz]
+// (stride P), like images.
+#pragma once
+#include "kernels3d.cuh"
+
+namespace wamgpu {
+
+constexpr double kC3 = 0.70710678118654752440;
+__device__ __forceinline__ double cpow3(int l) {  // c^l by repeated multiplication (oracle: cpow3)
+    double c = 1.0;
+    for (int i = 0; i < l; ++i) c *= kC3;
+    return c;
+}
+
+// ------------------------------------------------------------ 3D Haar tiles
+// smem cube x[z][i][j] (TS^3).  One level on the leading s^3 region: per
+// 2x2x2 group the in-plane step on both z-planes (DESIGN.md §3 order), then
+// low = (P0+P1)*c, high = (P0-P1)*c at planes k and k + s/2.
+__device__ __forceinline__ void cube_fwd(double* x, double* t, int TS, int L) {
+    for (int l = 1; l <= L; ++l) {
+        const int s = TS >> (l - 1), h2 = s >> 1, g3 = h2 * h2 * h2;
+        for (int i = threadIdx.x; i < g3; i += blockDim.x) {
+            const int k = i / (h2 * h2), r = i % (h2 * h2), gi = r / h2, gj = r % h2;
+            double P[2][4];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double* xp = x + (2 * k + e) * TS * TS;
+                const double a = xp[(2 * gi) * TS + 2 * gj], b = xp[(2 * gi) * TS + 2 * gj + 1];
+                const double c = xp[(2 * gi + 1) * TS + 2 * gj], d = xp[(2 * gi + 1) * TS + 2 * gj + 1];
+                const double s1 = a + b, s2 = c + d, d1 = a - b, d2 = c - d;
+                P[e][0] = (s1 + s2) * 0.5; P[e][1] = (s1 - s2) * 0.5;
+                P[e][2] = (d1 + d2) * 0.5; P[e][3] = (d1 - d2) * 0.5;
+            }
+            const int pi[4] = {gi, gi + h2, gi, gi + h2}, pj[4] = {gj, gj, gj + h2, gj + h2};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                t[(k * TS + pi[q]) * TS + pj[q]] = (P[0][q] + P[1][q]) * kC3;
+                t[((k + h2) * TS + pi[q]) * TS + pj[q]] = (P[0][q] - P[1][q]) * kC3;
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < s * s * s; i += blockDim.x) {
+            const int z = i / (s * s), r = i % (s * s), ii = r / s, jj = r % s;
+            x[(z * TS + ii) * TS + jj] = t[(z * TS + ii) * TS + jj];
+        }
+        __syncthreads();
+    }
+}
+__device__ __forceinline__ void cube_inv(double* x, double* t, int TS, int L) {
+    for (int l = L; l >= 1; --l) {
+        const int s = TS >> (l - 1), h2 = s >> 1, g3 = h2 * h2 * h2;
+        for (int i = threadIdx.x; i < g3; i += blockDim.x) {
+            const int k = i / (h2 * h2), r = i % (h2 * h2), gi = r / h2, gj = r % h2;
+            const int pi[4] = {gi, gi + h2, gi, gi + h2}, pj[4] = {gj, gj, gj + h2, gj + h2};
+            double P[2][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double lo = x[(k * TS + pi[q]) * TS + pj[q]], hi = x[((k + h2) * TS + pi[q]) * TS + pj[q]];
+                P[0][q] = (lo + hi) * kC3;
+                P[1][q] = (lo - hi) * kC3;
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double* tp = t + (2 * k + e) * TS * TS;
+                const double A = P[e][0], H = P[e][1], V = P[e][2], D = P[e][3];
+                const double p = A + H, m = A - H, r2 = V + D, u = V - D;
+                tp[(2 * gi) * TS + 2 * gj] = (p + r2) * 0.5;
+                tp[(2 * gi) * TS + 2 * gj + 1] = (p - r2) * 0.5;
+                tp[(2 * gi + 1) * TS + 2 * gj] = (m + u) * 0.5;
+                tp[(2 * gi + 1) * TS + 2 * gj + 1] = (m - u) * 0.5;
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < s * s * s; i += blockDim.x) {
+            const int z = i / (s * s), r = i % (s * s), ii = r / s, jj = r % s;
+            x[(z * TS + ii) * TS + jj] = t[(z * TS + ii) * TS + jj];
+        }
+        __syncthreads();
+    }
+}
+
+// Device index ((yy*nx + xx)*P + zz) of local cube position (z, i, j) of tile
+// (kt, ti, tj), its level and activity (slab-local 3D Mallat layout).
+struct CoefInfo3 { uint64_t idx; bool approx; bool active; };
+__device__ __forceinline__ CoefInfo3 coef_info3(int z, int i, int j, int kt, int ti, int tj, int L, int nx, int ny,
+                                                int nzl, int P, const uint8_t* __restrict__ act, const ActOff& off) {
+    CoefInfo3 ci;
+    const int m = max(z, max(i, j));
+    if (m == 0) {
+        ci.idx = ((uint64_t)ti * nx + tj) * P + kt;
+        ci.approx = true; ci.active = true;
+        return ci;
+    }
+    const int lg = 31 - __clz(m), l = L - lg, half = 1 << lg;
+    const int bk = kt * half + (z & (half - 1)), bi = ti * half + (i & (half - 1)), bj = tj * half + (j & (half - 1));
+    const int dl = nzl >> l, hl = ny >> l, wl = nx >> l;
+    const int zz = (z >= half ? dl : 0) + bk, yy = (i >= half ? hl : 0) + bi, xx = (j >= half ? wl : 0) + bj;
+    ci.idx = ((uint64_t)yy * nx + xx) * P + zz;
+    ci.approx = false;
+    ci.active = act[off.off[l] + ((uint64_t)bk * hl + bi) * wl + bj] != 0;
+    return ci;
+}
+
+// One CTA per (TS x TS x TS) tile.  mode 0: synthesis (beta -> mu, mu64);
+// mode 1: analysis of g, root solve of active z, synthesis; mode 2: analysis only.
+__global__ void k_tile3h(int mode, int nx, int ny, int nzl, int P, int L, const double* __restrict__ g,
+                         const double* __restrict__ bm, const double* __restrict__ bdata,
+                         const uint8_t* __restrict__ act, ActOff off, float* __restrict__ beta,
+                         float* __restrict__ mu, double* __restrict__ mu64, double* __restrict__ out,
+                         double* __restrict__ bp_out, double* __restrict__ bm_out, double Z0,
+                         unsigned long long* __restrict__ counters, int* __restrict__ flag) {
+    extern __shared__ double smh[];
+    const int TS = 1 << L, T3 = TS * TS * TS;
+    double* x = smh;
+    double* t = smh + T3;
+    const int tj = blockIdx.x, ti = blockIdx.y, kt = blockIdx.z;
+    auto vox = [&](int z, int i, int j) -> uint64_t {
+        return ((uint64_t)(ti * TS + i) * nx + (tj * TS + j)) * P + (kt * TS + z);
+    };
+    if (mode != 0) {
+        for (int e = threadIdx.x; e < T3; e += blockDim.x) {  // z fastest: contiguous slab runs
+            const int z = e % TS, r = e / TS, i = r / TS, j = r % TS;
+            x[(z * TS + i) * TS + j] = g[vox(z, i, j)];
+        }
+        __syncthreads();
+        cube_fwd(x, t, TS, L);
+    }
+    if (mode == 2) {
+        for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+            const int z = e % TS, r = e / TS, i = r / TS, j = r % TS;
+            const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, L, nx, ny, nzl, P, act, off);
+            out[ci.idx] = x[(z * TS + i) * TS + j];
+        }
+        return;
+    }
+    unsigned long long upd = 0, deg = 0;
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, r = e / TS, i = r / TS, j = r % TS;
+        const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, L, nx, ny, nzl, P, act, off);
+        float bo = beta[ci.idx];
+        if (mode == 1) {
+            const double bmv = ci.approx ? 0.0 : bm[ci.idx];
+            const double bpv = x[(z * TS + i) * TS + j] - bmv;
+            if (bp_out) { bp_out[ci.idx] = bpv; bm_out[ci.idx] = bmv; }
+            if (ci.active) {
+                double nb;
+                const int rr = solve_update(bdata[ci.idx], bpv, bmv, Z0, (double)bo, &nb);
+                if (rr == 0) {
+                    if (!isfinite(nb)) atomicOr(flag, 4);
+                    bo = (float)nb;
+                    beta[ci.idx] = bo;
+                    ++upd;
+                } else if (rr == 2) {
+                    ++deg;
+                }
+            }
+        }
+        x[(z * TS + i) * TS + j] = (double)bo;
+    }
+    if (mode == 1) {
+        for (int o = 16; o > 0; o >>= 1) {
+            upd += __shfl_xor_sync(0xffffffffu, upd, o);
+            deg += __shfl_xor_sync(0xffffffffu, deg, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (upd) atomicAdd(counters + 0, upd);
+            if (deg) atomicAdd(counters + 1, deg);
+        }
+    }
+    __syncthreads();
+    cube_inv(x, t, TS, L);
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, r = e / TS, i = r / TS, j = r % TS;
+        const uint64_t p = vox(z, i, j);
+        mu[p] = (float)x[(z * TS + i) * TS + j];
+        if (mu64) mu64[p] = x[(z * TS + i) * TS + j];
+    }
+}
+
+// ------------------------------------------------------------ criterion
+__global__ void k_max_slab(const double* __restrict__ v, uint64_t n, int nzl, int P, double* __restrict__ part) {
+    double m = -DBL_MAX;
+    const uint64_t tot = n * (uint64_t)nzl;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (uint64_t)gridDim.x * blockDim.x)
+        m = fmax(m, v[(i / nzl) * P + i % nzl]);
+    m = warp_max(m);
+    __shared__ double s[32];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = -DBL_MAX;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, s[w]);
+        part[blockIdx.x] = r;
+    }
+}
+
+// voxel (x, s) with mu > thr activates the coarsest inactive 3D block (OLD tree)
+__global__ void k_mark3h(int nx, int ny, int nzl, int P, int L, const double* __restrict__ mu64, double thr,
+                         const uint8_t* __restrict__ act_old, uint8_t* __restrict__ act_new, ActOff off) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t N = (uint64_t)nx * ny;
+    if (e >= N * (uint64_t)nzl) return;
+    const uint64_t xv = e / nzl;
+    const int s = (int)(e % nzl);
+    if (!(mu64[xv * P + s] > thr)) return;
+    const int iy = (int)(xv / nx), ix = (int)(xv % nx);
+    for (int l = L; l >= 1; --l) {
+        const uint64_t b = off.off[l] + ((uint64_t)(s >> l) * (ny >> l) + (iy >> l)) * (nx >> l) + (ix >> l);
+        if (!act_old[b]) { act_new[b] = 1; return; }
+    }
+}
+
+// ------------------------------------------------------------ expansion walk
+// One warp per level over 32 staged rays (as k_walk_lv).  Tree: anyb bits (one
+// per (l, in-plane block)) in shared memory; per-block z-bit words in global
+// (W_l words per block, bit k = z-block k of the slab).
+// MODE 1: Z(y) = max_s [zA(y) + tot_L(k_L(s)) + ... + tot_1(k_1(s))] with
+//   tot_l(k) = sum over (ray-order) level-l blocks b with (k, b) active of
+//   t = |Hl|+|Vl|+|Dl|+|Ah|+|Hh|+|Vh|+|Dh| (each psi c^l) — oracle z_row3;
+//   cnt[y*L + l-1] = number of level-l blocks b crossed with any active k.
+// MODE 2: emit one Psi entry per such (y, b): key = koff[l] + b, payload at pos.
+template <int MODE, int L>
+__global__ void __launch_bounds__(32 * 5) k_walk3h(uint64_t M, const unsigned long long* __restrict__ rp,
+                                                   const uint2* __restrict__ A, int nx, int ny, int nzl,
+                                                   const unsigned* __restrict__ tbits, ActOff boff, int tree_words,
+                                                   const unsigned* __restrict__ zbits, ActOff zoff, ActOff koff,
+                                                   const double* __restrict__ zA, double* __restrict__ zrow,
+                                                   unsigned long long* __restrict__ cnt,
+                                                   const unsigned long long* __restrict__ pos,
+                                                   unsigned* __restrict__ keys, uint2* __restrict__ vidx,
+                                                   unsigned* __restrict__ pray, float4* __restrict__ ppsi) {
+    extern __shared__ unsigned char dsm[];
+    unsigned* tsm = reinterpret_cast<unsigned*>(dsm);                                // tree_words
+    double* stot = reinterpret_cast<double*>(dsm + ((tree_words * 4 + 15) / 16) * 16);  // sum_l (nzl>>l)*32
+    __shared__ uint2 buf[32][33];
+    __shared__ unsigned long long s_lo[32], s_len[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, l = L - w, nlev = blockDim.x >> 5;
+    for (int i = threadIdx.x; i < tree_words; i += blockDim.x) tsm[i] = tbits[i];
+    int toff = 0;  // offset of this level's tot block in stot
+    for (int k = L; k > l; --k) toff += (nzl >> k) * 32;
+    const int nk = nzl >> l;
+    if (MODE == 1)
+        for (int i = lane; i < nk * 32; i += 32) stot[toff + i] = 0.0;
+    const uint64_t y = (uint64_t)blockIdx.x * 32 + lane;
+    if (w == 0) {
+        uint64_t lo = 0, hi = 0;
+        if (y < M) { lo = rp[y]; hi = rp[y + 1]; }
+        s_lo[lane] = lo;
+        s_len[lane] = hi - lo;
+    }
+    __syncthreads();
+    unsigned long long maxlen = s_len[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    const unsigned long long len = s_len[lane];
+    const bool pow2 = (nx & (nx - 1)) == 0;
+    const int lgx = 31 - __clz(nx);
+    const int wl = nx >> l;
+    const unsigned bo = (unsigned)boff.off[l];
+    const double sc = 1.0 / (double)(1 << l), cl = cpow3(l);
+    const int W = (nk + 31) >> 5;
+
+    int cur = -1, cq = -1;
+    bool av = false;
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, qa = 0.0;
+    unsigned long long count = 0, wp = 0;
+    if (MODE == 2 && y < M) wp = pos[y * L + (l - 1)];
+
+    auto park = [&]() {
+        q0 = cq == 0 ? qa : q0;
+        q1 = cq == 1 ? qa : q1;
+        q2 = cq == 2 ? qa : q2;
+        q3 = cq == 3 ? qa : q3;
+    };
+    auto flush = [&]() {
+        if (av) {
+            park();
+            const double st = q0 + q1, sb = q2 + q3;
+            const double pA = (st + sb) * sc, pH = (st - sb) * sc, pV = ((q0 + q2) - (q1 + q3)) * sc,
+                         pD = ((q0 + q3) - (q1 + q2)) * sc;
+            if (MODE == 1) {
+                const double hh = fabs(pH * cl), vv = fabs(pV * cl), dd = fabs(pD * cl), aa = fabs(pA * cl);
+                const double t = (((((hh + vv) + dd) + aa) + hh) + vv) + dd;
+                const unsigned* zb = zbits + zoff.off[l] + (uint64_t)cur * W;
+                for (int wi = 0; wi < W; ++wi) {
+                    unsigned m = zb[wi];
+                    while (m) {
+                        const int k = wi * 32 + __ffs(m) - 1;
+                        m &= m - 1;
+                        stot[toff + k * 32 + lane] += t;
+                    }
+                }
+                ++count;
+            } else {
+                keys[wp] = (unsigned)(koff.off[l] + cur);
+                vidx[wp] = make_uint2((unsigned)wp, 0u);
+                pray[wp] = (unsigned)y;
+                ppsi[wp] = make_float4((float)pA, (float)pH, (float)pV, (float)pD);
+                ++wp;
+            }
+            q0 = q1 = q2 = q3 = 0.0;
+        }
+        cq = -1;
+        qa = 0.0;
+    };
+
+    for (unsigned long long base = 0; base < maxlen; base += 32) {
+        for (int j = w; j < 32; j += nlev) {
+            const unsigned long long nj = s_len[j];
+            const bool ok = base + lane < nj;
+            cp_async8(&buf[j][lane], A + (ok ? s_lo[j] + base + lane : 0), ok);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        const int n = (int)min(32ull, len > base ? len - base : 0ull);
+        for (int i = 0; i < n; ++i) {
+            const uint2 e = buf[lane][i];
+            int ix, iy;
+            if (pow2) { ix = (int)(e.x & (unsigned)(nx - 1)); iy = (int)(e.x >> lgx); }
+            else { iy = (int)(e.x / (unsigned)nx); ix = (int)(e.x % (unsigned)nx); }
+            const int key = (iy >> l) * wl + (ix >> l);
+            if (key != cur) {
+                flush();
+                cur = key;
+                const unsigned bit = bo + (unsigned)key;
+                av = (tsm[bit >> 5] >> (bit & 31)) & 1u;
+            }
+            if (av) {
+                const int quad = (((iy >> (l - 1)) & 1) << 1) | ((ix >> (l - 1)) & 1);
+                if (quad != cq) {
+                    if (cq >= 0) park();
+                    cq = quad;
+                    qa = 0.0;
+                }
+                qa += hval(e);
+            }
+        }
+        __syncthreads();
+    }
+    flush();
+    if (MODE == 1) {
+        if (y < M) cnt[y * L + (l - 1)] = count;
+        __syncthreads();
+        if (w == 0 && y < M) {
+            for (int k = 1; k <= L - nlev; ++k) cnt[y * L + (k - 1)] = 0;
+            double best = 0.0;
+            for (int s = 0; s < nzl; ++s) {
+                double z = zA[y];
+                int o = 0;
+                for (int k = L; k >= 1; --k) {
+                    if (k > L - nlev) z += stot[o + (s >> k) * 32 + lane];
+                    o += (nzl >> k) * 32;
+                }
+                best = fmax(best, z);
+            }
+            zrow[y] = best;
+        }
+    }
+}
+
+// Payload gather after the key sort: E3 entries in (key, ray-insertion) order.
+__global__ void k_gather_psi(uint64_t n, const uint2* __restrict__ sidx, const unsigned* __restrict__ pray,
+                             const float4* __restrict__ ppsi, unsigned* __restrict__ eray,
+                             float4* __restrict__ epsi) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned j = sidx[i].x;
+    eray[i] = pray[j];
+    epsi[i] = ppsi[j];
+}
+
+// ------------------------------------------------------------ split (3D)
+// Warp per (level l, in-plane block b) with any active z-block: over its Psi
+// list, lanes own SPL slices; per slice s (z-block k = s>>l, half (s>>(l-1))&1):
+//   z-low p in H,V,D:   psi_p c^l q  if psi_p < 0
+//   z-high p in A,H,V,D: psi_p c^l q if psi_p < 0 and s in the low half;
+//                       -psi_p c^l q if psi_p > 0 and s in the high half.
+// Per-slice partials are then summed over each block's 2^l slices (ascending)
+// and written for the active (k, b).  bm is indexed like beta (slab stride P).
+template <int SPL>
+__global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __restrict__ list, int nx, int ny,
+                                                 int nzl, const unsigned long long* __restrict__ ptr,
+                                                 const unsigned* __restrict__ eray, const float4* __restrict__ epsi,
+                                                 const float* __restrict__ q, const uint8_t* __restrict__ act,
+                                                 ActOff off, ActOff koff, double* __restrict__ bm) {
+    using V = typename SlabVec<SPL>::T;
+    constexpr int P = 32 * SPL;
+    __shared__ double red[4][7][P];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nlist; it += W) {
+        const unsigned b = list[it].x;
+        const int l = (int)list[it].y;
+        const double cl = cpow3(l);
+        const uint64_t key = koff.off[l] + b;
+        double acc[SPL][7];
+#pragma unroll
+        for (int j = 0; j < SPL; ++j)
+#pragma unroll
+            for (int t = 0; t < 7; ++t) acc[j][t] = 0.0;
+        for (uint64_t e = ptr[key]; e < ptr[key + 1]; ++e) {
+            const unsigned yv = eray[e];
+            const float4 ps = epsi[e];
+            const double pA = (double)ps.x * cl, pH = (double)ps.y * cl, pV = (double)ps.z * cl,
+                         pD = (double)ps.w * cl;
+            float f[SPL];
+            unpack(__ldg(reinterpret_cast<const V*>(q + (uint64_t)yv * P) + lane), f);
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) {
+                const double qv = (double)f[j];
+                const int s = lane * SPL + j;
+                const bool hi = ((s >> (l - 1)) & 1) != 0;
+                if (pH < 0.0) acc[j][0] += pH * qv;
+                if (pV < 0.0) acc[j][1] += pV * qv;
+                if (pD < 0.0) acc[j][2] += pD * qv;
+                const double hp[4] = {pA, pH, pV, pD};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if (!hi && hp[t] < 0.0) acc[j][3 + t] += hp[t] * qv;
+                    else if (hi && hp[t] > 0.0) acc[j][3 + t] += -hp[t] * qv;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < SPL; ++j)
+#pragma unroll
+            for (int t = 0; t < 7; ++t) red[wib][t][lane * SPL + j] = acc[j][t];
+        __syncwarp();
+        const int nk = nzl >> l, hl = ny >> l, wl = nx >> l, dl = nk;
+        const int bi = (int)(b / wl), bj = (int)(b % wl);
+        for (int k = lane; k < nk; k += 32) {
+            if (!act[off.off[l] + ((uint64_t)k * hl + bi) * wl + bj]) continue;
+            const int zz[7] = {k, k, k, dl + k, dl + k, dl + k, dl + k};
+            const int yy[7] = {hl + bi, bi, hl + bi, bi, hl + bi, bi, hl + bi};
+            const int xx[7] = {bj, wl + bj, wl + bj, bj, bj, wl + bj, wl + bj};
+#pragma unroll
+            for (int t = 0; t < 7; ++t) {
+                double sum = 0.0;
+                for (int s = k << l; s < (k + 1) << l; ++s) sum += red[wib][t][s];
+                bm[((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]] = sum;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace wamgpu

@@ -29,6 +29,7 @@
 #include "host_model.hpp"
 #include "kernels.cuh"
 #include "kernels3d.cuh"
+#include "kernels3h.cuh"
 
 namespace wamgpu {
 
@@ -103,6 +104,16 @@ struct wamgpu_ctx {
     DBuf<unsigned> tbits;               // bit-packed tree for the expansion walk
     ActOff boff{};                      // bit offset of level l in tbits
     int tree_words = 0;
+    // separable 3D Haar model (pin P3)
+    bool haar3 = false;
+    DBuf<unsigned> zbits;               // per (level, in-plane block): z-block activity words
+    ActOff zoff{}, koff{};              // word offset of level l in zbits; key offset of level l
+    uint64_t nkeys3 = 0;
+    DBuf<unsigned> E3ray, pray_s;
+    DBuf<float4> E3psi, ppsi_s;
+    DBuf<uint2> list3;                  // (in-plane block, level) with any active z-block
+    uint64_t nlist3 = 0;
+    int walk_nlev = 1;
     ActOff off{};
     uint64_t act_bytes = 0;
     std::vector<uint8_t> act_host;
@@ -153,6 +164,11 @@ using Ctx = ::wamgpu_ctx;
 static thread_local std::string g_err;
 
 // ------------------------------------------------------------- utilities
+static double cpow3_host(int l) {  // c^l, same sequence of multiplications as the device / oracle
+    double c = 1.0;
+    for (int i = 0; i < l; ++i) c *= 0.70710678118654752440;
+    return c;
+}
 static inline unsigned blocks_for(uint64_t n, unsigned bs) { return (unsigned)((n + bs - 1) / bs); }
 
 static void launched(Ctx* c, int n = 1) { c->launches += n; }
@@ -472,7 +488,8 @@ static void launch_walk(Ctx* c, int L, unsigned long long* cnt, const unsigned l
 #define WALK_CASE(LV)                                                                                        \
     case LV:                                                                                                 \
         k_walk<MODE, LV><<<nb, 32 * WALK_WARPS, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->act.p, \
-                                                             c->off, c->zA.p, c->zrow.p, cnt, pos, keys, vals); \
+                                                             c->off, c->haar3 ? cpow3_host(LV) : 1.0, c->zA.p,  \
+                                                             c->zrow.p, cnt, pos, keys, vals);                 \
         break;
     switch (L) {
         WALK_CASE(0) WALK_CASE(1) WALK_CASE(2) WALK_CASE(3) WALK_CASE(4) WALK_CASE(5)
@@ -537,6 +554,110 @@ static void launch_walk_lv(Ctx* c, unsigned long long* cnt, const unsigned long 
     check_launch(c);
 }
 
+
+// ---- separable 3D Haar (pin P3) helpers -------------------------------------
+static uint64_t blocks2(const Ctx* c, int l) { return (uint64_t)(c->nx >> l) * (c->ny >> l); }
+static int zwords(const Ctx* c, int l) { return ((c->nzl >> l) + 31) >> 5; }
+
+// act_host (3D bytes, level l: (nzl>>l, ny>>l, nx>>l)) -> any-bits per in-plane
+// block (shared memory of the walk) + z-activity words per in-plane block.
+static void upload_tree3(Ctx* c, int* nlev_out) {
+    std::vector<unsigned> w, zw;
+    uint64_t bit = 0, zo = 0, ko = 0;
+    for (int l = 0; l <= LMAX + 1; ++l) c->boff.off[l] = c->zoff.off[l] = c->koff.off[l] = 0;
+    int nlev = 0;
+    bool chain = true;
+    std::vector<uint2> lst;
+    for (int l = c->L; l >= 1; --l) {
+        const uint64_t nb = blocks2(c, l);
+        const int nk = c->nzl >> l, W = zwords(c, l);
+        c->boff.off[l] = bit;
+        c->zoff.off[l] = zo;
+        c->koff.off[l] = ko;
+        w.resize((bit + nb + 31) / 32 + 1, 0u);
+        zw.resize(zo + nb * W, 0u);
+        const uint8_t* a = c->act_host.data() + c->off.off[l];
+        bool any_l = false;
+        for (int k = 0; k < nk; ++k)
+            for (uint64_t b = 0; b < nb; ++b)
+                if (a[(uint64_t)k * nb + b]) {
+                    zw[zo + b * W + (k >> 5)] |= 1u << (k & 31);
+                    w[(bit + b) >> 5] |= 1u << ((bit + b) & 31);
+                    any_l = true;
+                }
+        for (uint64_t b = 0; b < nb; ++b)
+            if ((w[(bit + b) >> 5] >> ((bit + b) & 31)) & 1u) lst.push_back(make_uint2((unsigned)b, (unsigned)l));
+        if (chain && any_l) ++nlev; else chain = false;
+        bit = (bit + nb + 31) / 32 * 32;
+        zo += nb * W;
+        ko += nb;
+    }
+    if (w.empty()) w.push_back(0u);
+    if (zw.empty()) zw.push_back(0u);
+    c->tree_words = (int)w.size();
+    c->nkeys3 = ko;
+    c->tbits.ensure(w.size());
+    c->zbits.ensure(zw.size());
+    CK(cudaMemcpyAsync(c->tbits.p, w.data(), w.size() * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->zbits.p, zw.data(), zw.size() * 4, cudaMemcpyHostToDevice, c->st));
+    c->nlist3 = lst.size();
+    c->list3.ensure(std::max<size_t>(lst.size(), 1));
+    if (!lst.empty()) CK(cudaMemcpyAsync(c->list3.p, lst.data(), lst.size() * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    *nlev_out = std::max(nlev, 1);
+}
+
+template <int MODE>
+static void launch_walk3h(Ctx* c, int nlev, unsigned long long* cnt, const unsigned long long* pos) {
+    const unsigned nb = blocks_for(c->Ml, 32);
+    size_t stot = 0;
+    for (int l = 1; l <= c->L; ++l) stot += (size_t)(c->nzl >> l) * 32 * 8;
+    const size_t smem = ((size_t)c->tree_words * 4 + 15) / 16 * 16 + stot;
+    if (smem > 200 * 1024) throw ConfigError("tree too large for the shared-memory 3D walk");
+#define W3(LV)                                                                                                   \
+    case LV: {                                                                                                   \
+        auto kf = k_walk3h<MODE, LV>;                                                                            \
+        if (smem > 32 * 1024) CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        kf<<<nb, 32 * nlev, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->nzl, c->tbits.p, c->boff,     \
+                                           c->tree_words, c->zbits.p, c->zoff, c->koff, c->zA.p, c->zrow.p, cnt,  \
+                                           pos, c->kin_s.p, c->vin_s.p, c->pray_s.p, c->ppsi_s.p);                \
+    } break;
+    switch (c->L) {
+        W3(1) W3(2) W3(3) W3(4) W3(5)
+        default: throw ConfigError("haar3: depth beyond the device walk");
+    }
+#undef W3
+    check_launch(c);
+}
+
+// Psi lists (per in-plane block with any active z-block): count -> scan ->
+// emit -> stable radix sort by key -> payload gather -> CSC by key.
+static void rebuild_psi3(Ctx* c, int nlev) {
+    const uint64_t ncnt = (uint64_t)c->Ml * c->L;
+    CK(cudaMemsetAsync(c->wcnt.p + ncnt, 0, 8, c->st));
+    exclusive_scan_u64(c, c->wcnt.p, ncnt + 1);
+    unsigned long long tot = 0;
+    CK(cudaMemcpyAsync(&tot, c->wcnt.p + ncnt, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    const uint64_t n1 = std::max<uint64_t>(tot, 1);
+    c->kin_s.ensure(n1); c->vin_s.ensure(n1); c->pray_s.ensure(n1); c->ppsi_s.ensure(n1);
+    if (tot) launch_walk3h<2>(c, nlev, nullptr, c->wcnt.p);
+    DBuf<uint2> sidx;
+    sort_pairs(c, c->kin_s, c->vin_s, c->kout_s, sidx, tot, c->nkeys3);
+    c->E3ray.ensure(n1);
+    c->E3psi.ensure(n1);
+    if (tot) {
+        k_gather_psi<<<blocks_for(tot, 256), 256, 0, c->st>>>(tot, sidx.p, c->pray_s.p, c->ppsi_s.p, c->E3ray.p,
+                                                               c->E3psi.p);
+        check_launch(c);
+    }
+    c->np.ensure(c->nkeys3 + 1);
+    k_bounds<<<blocks_for(c->nkeys3 + 1, 256), 256, 0, c->st>>>(c->kout_s.p, tot, c->nkeys3, c->np.p);
+    check_launch(c);
+    c->nnz_phi = tot;
+    CK(cudaStreamSynchronize(c->st));
+}
+
 // Z0 = max_y sum_{z active} |phi(y|z)| (Eq. 1.61).  init: the approximation part
 // (tree-independent, cached in zA); AM: levels = 0 -> row sums.
 static double compute_z0(Ctx* c, int levels, bool init) {
@@ -546,6 +667,11 @@ static double compute_z0(Ctx* c, int levels, bool init) {
     if (init) {
         CK(cudaMemsetAsync(c->wcnt.p, 0, ncnt * 8, c->st));
         if (c->Ml) launch_walk<0>(c, levels, nullptr, nullptr, nullptr, nullptr);
+    } else if (c->Ml && c->haar3) {
+        int nlev = 1;
+        upload_tree3(c, &nlev);
+        c->walk_nlev = nlev;
+        launch_walk3h<1>(c, nlev, c->wcnt.p, nullptr);
     } else if (c->Ml) {
         upload_tree_bits(c);
         launch_walk_lv<1>(c, c->wcnt.p, nullptr, nullptr, nullptr);
@@ -721,6 +847,17 @@ static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
 // ------------------------------------------------------------------ WAM
 static void tile_launch(Ctx* c, int mode, double* mu64, double* out) {
     const int TS = 1 << c->L;
+    if (c->haar3) {
+        dim3 grid(c->nx >> c->L, c->ny >> c->L, c->nzl >> c->L);
+        const size_t smem = 2ull * TS * TS * TS * sizeof(double);
+        if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_tile3h, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_tile3h<<<grid, 256, smem, c->st>>>(mode, c->nx, c->ny, c->nzl, slab_stride(c), c->L, c->g.p, c->g.p + NV(c),
+                                             c->bdata.p, c->act.p, c->off, c->beta.p, c->mu.p, mu64, out, c->bp_dbg.p,
+                                             c->bm_dbg.p, c->Z0, c->counters.p, c->flag.p);
+        check_launch(c);
+        return;
+    }
     if (c->nzl == 1) {
         dim3 grid(c->nx >> c->L, c->ny >> c->L);
         const int bs = std::min(1024, std::max(32, TS * TS));
@@ -782,6 +919,15 @@ static void rebuild_phi(Ctx* c) {
 }
 
 static int64_t count_active(const Ctx* c) {
+    if (c->haar3) {
+        int64_t a = (int64_t)(c->nx >> c->L) * (c->ny >> c->L) * (c->nzl >> c->L);
+        for (int l = 1; l <= c->L; ++l) {
+            const uint64_t n = blocks2(c, l) * (uint64_t)(c->nzl >> l);
+            const uint8_t* p = c->act_host.data() + c->off.off[l];
+            for (uint64_t i = 0; i < n; ++i) a += 7 * (p[i] != 0);
+        }
+        return a;
+    }
     int64_t a = (int64_t)(c->nx >> c->L) * (c->ny >> c->L);
     for (int l = 1; l <= c->L; ++l) {
         const uint64_t n = (uint64_t)(c->nx >> l) * (c->ny >> l);
@@ -797,6 +943,9 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     if (!c->have_grid) throw ContractError("wam: image grid unknown (set_geometry or set_grid)");
     if (L < 0 || L > LMAX) throw ConfigError("haar: depth must be in [0, " + std::to_string(LMAX) + "]");
     if ((c->nx % (1 << L)) || (c->ny % (1 << L))) throw ConfigError("haar: slice dimensions not divisible by 2^L");
+    if (c->haar3 && (c->nzl % (1 << L) || c->s0 % (1 << L)))
+        throw ConfigError("haar3: the slab's slices must be divisible by 2^L (and slab-aligned)");
+    if (c->haar3 && L < 1) throw ConfigError("haar3: depth must be >= 1");
     c->L = L;
     const uint64_t N = NV(c);  // local slab of coefficients / voxels
     c->mu.ensure(N); c->beta.ensure(N); c->g.ensure(2 * N); c->bdata.ensure(N); c->mu64.ensure(N);
@@ -807,7 +956,10 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     // tree bitmaps, level l at off[l]
     uint64_t o = 0;
     for (int l = 0; l <= LMAX + 1; ++l) c->off.off[l] = 0;
-    for (int l = 1; l <= L; ++l) { c->off.off[l] = o; o += (uint64_t)(c->nx >> l) * (c->ny >> l); }
+    for (int l = 1; l <= L; ++l) {
+        c->off.off[l] = o;
+        o += (uint64_t)(c->nx >> l) * (c->ny >> l) * (c->haar3 ? (uint64_t)(c->nzl >> l) : 1);
+    }
     c->act_bytes = o;
     c->act.ensure(std::max<uint64_t>(o, 1));
     c->act_new.ensure(std::max<uint64_t>(o, 1));
@@ -825,8 +977,9 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     CK(cudaMemsetAsync(c->g.p, 0, 2 * N * 8, c->st));
     c->Z0 = compute_z0(c, L, true);
     c->nlist = 0;
+    c->nlist3 = 0;
     c->nnz_phi = 0;
-    rebuild_phi(c);
+    if (!c->haar3) rebuild_phi(c);       // 3D: the tree is empty, no Psi lists yet
     tile_launch(c, 0, nullptr, nullptr);  // mu = Omega beta
     forward_fused(c, false);
     CK(cudaMemsetAsync(c->counters.p, 0, 16, c->st));
@@ -839,7 +992,18 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
 
 static void wam_step(Ctx* c) {
     back_into(c, c->q.p, c->g.p);
-    if (c->nlist) {
+    if (c->haar3 && c->nlist3) {
+        c->timer_begin(T_SPLIT);
+        const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist3 + 3) / 4, (uint64_t)c->sms * 16);
+        double* bm3 = c->g.p + NV(c);
+#define S3H(S) k_split3h<S><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p, c->E3ray.p, \
+                                                   c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3);
+        switch (spl_of(c)) { case 1: S3H(1) break; case 2: S3H(2) break; default: S3H(4) break; }
+#undef S3H
+        check_launch(c);
+        c->timer_end(T_SPLIT);
+        c->tm.split_launches++;
+    } else if (!c->haar3 && c->nlist) {
         c->timer_begin(T_SPLIT);
         const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist + 7) / 8, (uint64_t)c->sms * 16);
         if (c->nzl == 1) {
@@ -878,6 +1042,39 @@ static int64_t wam_expand(Ctx* c, double factor) {
     if (c->algo != 2) throw ContractError("wam: not initialised");
     c->timer_begin(T_EXPAND);
     tile_launch(c, 0, c->mu64.p, nullptr);         // fp64 criterion image Omega beta
+    if (c->haar3) {                                 // pin P3: every voxel, no z-sum
+        int64_t newly = 0;
+        const int nb = 1024;
+        k_max_slab<<<nb, 256, 0, c->st>>>(c->mu64.p, c->N, c->nzl, slab_stride(c), c->partial.p);
+        check_launch(c);
+        k_max_partials<<<1, 256, 0, c->st>>>(c->partial.p, (uint64_t)nb, c->scal.p + 1);
+        check_launch(c);
+        allreduce_max(c, c->scal.p + 1, 1);
+        double mx = 0.0;
+        CK(cudaMemcpyAsync(&mx, c->scal.p + 1, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        if (mx > 0.0 && c->L > 0) {
+            CK(cudaMemcpyAsync(c->act_new.p, c->act.p, c->act_bytes, cudaMemcpyDeviceToDevice, c->st));
+            k_mark3h<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->nx, c->ny, c->nzl, slab_stride(c), c->L,
+                                                                         c->mu64.p, factor * mx, c->act.p,
+                                                                         c->act_new.p, c->off);
+            check_launch(c);
+            c->act.swap(c->act_new);
+            std::vector<uint8_t> h(c->act_bytes);
+            CK(cudaMemcpyAsync(h.data(), c->act.p, c->act_bytes, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            for (uint64_t i = 0; i < c->act_bytes; ++i) newly += (h[i] != 0) - (c->act_host[i] != 0);
+            c->act_host.swap(h);
+            if (newly > 0) {
+                c->Z0 = compute_z0(c, c->L, false);
+                rebuild_psi3(c, c->walk_nlev);
+                c->active = count_active(c);
+            }
+        }
+        c->timer_end(T_EXPAND);
+        c->tm.expand_events++;
+        return newly;
+    }
     const double* crit = c->mu64.p;                // nz == 1: the z-sum is the slice
     if (c->nzl > 1 || c->nz > 1) {                 // z-summed image, slabs all-reduced
         c->dscratch.ensure(c->N);
@@ -1038,6 +1235,15 @@ int wamgpu_set_comm(wamgpu_ctx* ctx, const void* id128, int rank, int nranks) {
             std::memcpy(&id, id128, sizeof(id));
             NK(ncclCommInitRank(&ctx->comm, nranks, id, rank));
         }
+    })
+}
+
+int wamgpu_set_haar_dim(wamgpu_ctx* ctx, int dim) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (dim != 2 && dim != 3) throw ConfigError("haar: dimension must be 2 or 3");
+        ctx->haar3 = dim == 3;
+        ctx->algo = 0;
     })
 }
 
@@ -1275,7 +1481,7 @@ int wamgpu_get_z_rows(wamgpu_ctx* ctx, double* zrow) {
         NEED(ctx); NEED(zrow);
         Ctx* c = ctx;
         need_matrix(c);
-        if (c->algo == 2) compute_z0(c, c->L, false); else compute_z0(c, 0, true);
+        if (c->algo == 2 && c->L > 0) compute_z0(c, c->L, false); else compute_z0(c, c->algo == 2 ? c->L : 0, true);
         CK(cudaMemcpyAsync(zrow, c->zrow.p, c->Ml * 8, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
     })

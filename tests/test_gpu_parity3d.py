@@ -87,3 +87,43 @@ def test_wam3d_parity_tree_bit_exact(wam, orc, name):
     _, bp, bm = c.stats()
     _, bp32, bm32 = p32.wam_stats()
     assert rel_l2(bm, bm32) < TOL_MIRROR and rel_l2(bp, bp32) < TOL_MIRROR
+
+
+@pytest.mark.parametrize("name", ["tiny3d", "small3d"])
+def test_wam3d_separable_haar_parity(wam, orc, name):
+    """Separable 3D Haar model (pin P3): octree tree bit-exact vs both oracles
+    after every expansion, Z0 bit-exact vs the mirror, mu / I-div within bars."""
+    cfg, p64, _, I0, d = problem_inputs(name, orc, wam)
+    p32 = orc.Problem(p64.geom, mirror=True)
+    L, J, sched = cfg["L"], cfg["J"], cfg["schedule"]
+    c = _ctx(wam, cfg)
+    c.set_haar_dim(3)
+    c.set_data(d, I0)
+    c.wam_init(L)
+    for p in (p64, p32):
+        p.set_haar_dim(3)
+        p.wam_init(d, I0, L)
+    assert c.scalars()["Z0"] == p32.wam_get()["Z0"]
+    assert rel_l2(c.stats()[0], p32.wam_stats()[0]) < 1e-12
+    og, o64, o32, done = [], [], [], 0
+    for ev in sched + [J]:
+        og += [r["objective"] for r in c.wam_iterate(ev - done)]
+        o64 += [r[1] for r in p64.wam_iterate(ev - done)]
+        o32 += [r[1] for r in p32.wam_iterate(ev - done)]
+        done = ev
+        if ev == J:
+            break
+        assert c.wam_expand(0.1) == p32.wam_expand(0.1)
+        p64.wam_expand(0.1)
+        assert np.array_equal(c.tree(), p32.wam_tree()) and np.array_equal(c.tree(), p64.wam_tree())
+        assert c.scalars()["Z0"] == p32.wam_get()["Z0"]
+        assert np.array_equal(c.z_rows(), p32.wam_z0_rows())
+    assert rel_l2(og, o64) < TOL_F64 and rel_l2(og, o32) < TOL_MIRROR
+    assert rel_l2(c.image(), p64.wam_get()["mu"]) < TOL_F64
+    assert rel_l2(c.image(), p32.wam_get()["mu"]) < TOL_MIRROR
+    s, cnt = c.scalars(), p32.wam_counters()
+    assert (s["active_set"], s["cum_updates"], s["degenerate"]) == (cnt["active_set"], cnt["cum_updates"],
+                                                                      cnt["degenerate"])
+    _, bp, bm = c.stats()
+    _, bp32, bm32 = p32.wam_stats()
+    assert rel_l2(bm, bm32) < TOL_MIRROR and rel_l2(bp, bp32) < TOL_MIRROR
