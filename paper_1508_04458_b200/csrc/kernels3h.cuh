@@ -382,12 +382,13 @@ __global__ void k_gather_psi(uint64_t n, const uint2* __restrict__ sidx, const u
 
 // ------------------------------------------------------------ split (3D)
 // Warp per (level l, in-plane block b) with any active z-block: over its Psi
-// list, lanes own SPL slices; per slice s (z-block k = s>>l, half (s>>(l-1))&1):
-//   z-low p in H,V,D:   psi_p c^l q  if psi_p < 0
-//   z-high p in A,H,V,D: psi_p c^l q if psi_p < 0 and s in the low half;
-//                       -psi_p c^l q if psi_p > 0 and s in the high half.
-// Per-slice partials are then summed over each block's 2^l slices (ascending)
-// and written for the active (k, b).  bm is indexed like beta (slab stride P).
+// list, lanes own SPL slices; per entry the negative-part multipliers are
+//   z-low p in H,V,D:    m_lo = m_hi = min(psi_p c^l, 0)
+//   z-high p in A,H,V,D: m_lo = min(psi_p c^l, 0), m_hi = -max(psi_p c^l, 0)
+// and slice s (z-block k = s>>l, half (s>>(l-1))&1) adds m_half * q(y, s).
+// Consecutive slice pairs (2m, 2m+1) share a half for l >= 2 (one fma on
+// q0+q1) and split one block's halves for l == 1.  Pair partials are summed
+// over each block's slices (ascending) and written for the active (k, b).
 template <int SPL>
 __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __restrict__ list, int nx, int ny,
                                                  int nzl, const unsigned long long* __restrict__ ptr,
@@ -396,7 +397,8 @@ __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __
                                                  ActOff off, ActOff koff, double* __restrict__ bm) {
     using V = typename SlabVec<SPL>::T;
     constexpr int P = 32 * SPL;
-    __shared__ double red[4][7][P];
+    constexpr int NG = SPL >= 2 ? SPL / 2 : 1;   // slice groups per lane (pairs, or the single slice)
+    __shared__ double red[4][7][32 * NG];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nlist; it += W) {
@@ -404,50 +406,86 @@ __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __
         const int l = (int)list[it].y;
         const double cl = cpow3(l);
         const uint64_t key = koff.off[l] + b;
-        double acc[SPL][7];
+        // half of each of this lane's slices (SPL == 1: the single slice)
+        bool hi1 = false;
+        if (SPL == 1) hi1 = ((lane >> (l - 1)) & 1) != 0;
+        double acc[NG][7];
 #pragma unroll
-        for (int j = 0; j < SPL; ++j)
+        for (int g = 0; g < NG; ++g)
 #pragma unroll
-            for (int t = 0; t < 7; ++t) acc[j][t] = 0.0;
-        for (uint64_t e = ptr[key]; e < ptr[key + 1]; ++e) {
-            const unsigned yv = eray[e];
-            const float4 ps = epsi[e];
-            const double pA = (double)ps.x * cl, pH = (double)ps.y * cl, pV = (double)ps.z * cl,
-                         pD = (double)ps.w * cl;
-            float f[SPL];
-            unpack(__ldg(reinterpret_cast<const V*>(q + (uint64_t)yv * P) + lane), f);
+            for (int t = 0; t < 7; ++t) acc[g][t] = 0.0;
+        constexpr int U = 4;
+        const uint64_t e0 = ptr[key], e1 = ptr[key + 1];
+        for (uint64_t e = e0; e < e1; e += U) {
+            unsigned yv[U];
+            float4 ps[U];
 #pragma unroll
-            for (int j = 0; j < SPL; ++j) {
-                const double qv = (double)f[j];
-                const int s = lane * SPL + j;
-                const bool hi = ((s >> (l - 1)) & 1) != 0;
-                if (pH < 0.0) acc[j][0] += pH * qv;
-                if (pV < 0.0) acc[j][1] += pV * qv;
-                if (pD < 0.0) acc[j][2] += pD * qv;
+            for (int u = 0; u < U; ++u) {
+                const bool ok = e + u < e1;
+                yv[u] = ok ? __ldg(eray + e + u) : 0u;
+                ps[u] = ok ? __ldg(epsi + e + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            V qv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) qv[u] = __ldg(reinterpret_cast<const V*>(q + (uint64_t)yv[u] * P) + lane);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const double pA = (double)ps[u].x * cl, pH = (double)ps[u].y * cl, pV = (double)ps[u].z * cl,
+                             pD = (double)ps[u].w * cl;
+                const double lowm[3] = {fmin(pH, 0.0), fmin(pV, 0.0), fmin(pD, 0.0)};
                 const double hp[4] = {pA, pH, pV, pD};
+                double mlo[4], mhi[4];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    if (!hi && hp[t] < 0.0) acc[j][3 + t] += hp[t] * qv;
-                    else if (hi && hp[t] > 0.0) acc[j][3 + t] += -hp[t] * qv;
+                for (int t = 0; t < 4; ++t) { mlo[t] = fmin(hp[t], 0.0); mhi[t] = -fmax(hp[t], 0.0); }
+                float f[SPL];
+                unpack(qv[u], f);
+                if (SPL == 1) {
+                    const double qq = (double)f[0];
+#pragma unroll
+                    for (int t = 0; t < 3; ++t) acc[0][t] = fma(lowm[t], qq, acc[0][t]);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) acc[0][3 + t] = fma(hi1 ? mhi[t] : mlo[t], qq, acc[0][3 + t]);
+                } else if (l >= 2) {
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        const int s = lane * SPL + 2 * g;
+                        const bool hh = ((s >> (l - 1)) & 1) != 0;
+                        const double qq = (double)f[2 * g] + (double)f[2 * g + 1];
+#pragma unroll
+                        for (int t = 0; t < 3; ++t) acc[g][t] = fma(lowm[t], qq, acc[g][t]);
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) acc[g][3 + t] = fma(hh ? mhi[t] : mlo[t], qq, acc[g][3 + t]);
+                    }
+                } else {  // l == 1: the pair is one z-block, slice 2g its low half, 2g+1 its high half
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        const double q0 = (double)f[2 * g], q1 = (double)f[2 * g + 1], qq = q0 + q1;
+#pragma unroll
+                        for (int t = 0; t < 3; ++t) acc[g][t] = fma(lowm[t], qq, acc[g][t]);
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) acc[g][3 + t] = fma(mhi[t], q1, fma(mlo[t], q0, acc[g][3 + t]));
+                    }
                 }
             }
         }
 #pragma unroll
-        for (int j = 0; j < SPL; ++j)
+        for (int g = 0; g < NG; ++g)
 #pragma unroll
-            for (int t = 0; t < 7; ++t) red[wib][t][lane * SPL + j] = acc[j][t];
+            for (int t = 0; t < 7; ++t) red[wib][t][lane * NG + g] = acc[g][t];
         __syncwarp();
         const int nk = nzl >> l, hl = ny >> l, wl = nx >> l, dl = nk;
         const int bi = (int)(b / wl), bj = (int)(b % wl);
+        const int gper = SPL == 1 ? 1 : 2;   // slices per group
         for (int k = lane; k < nk; k += 32) {
             if (!act[off.off[l] + ((uint64_t)k * hl + bi) * wl + bj]) continue;
             const int zz[7] = {k, k, k, dl + k, dl + k, dl + k, dl + k};
             const int yy[7] = {hl + bi, bi, hl + bi, bi, hl + bi, bi, hl + bi};
             const int xx[7] = {bj, wl + bj, wl + bj, bj, bj, wl + bj, wl + bj};
+            const int g0 = (k << l) / gper, g1 = ((k + 1) << l) / gper;
 #pragma unroll
             for (int t = 0; t < 7; ++t) {
                 double sum = 0.0;
-                for (int s = k << l; s < (k + 1) << l; ++s) sum += red[wib][t][s];
+                for (int gg = g0; gg < g1; ++gg) sum += red[wib][t][gg];
                 bm[((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]] = sum;
             }
         }
