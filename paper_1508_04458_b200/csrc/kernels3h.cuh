@@ -422,8 +422,10 @@ __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const bool ok = e + u < e1;
-                yv[u] = ok ? __ldg(eray + e + u) : 0u;
-                ps[u] = ok ? __ldg(epsi + e + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const uint64_t ei = ok ? e + u : e;   // always a valid index
+                yv[u] = __ldg(eray + ei);
+                ps[u] = __ldg(epsi + ei);
+                if (!ok) ps[u] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
             V qv[U];
 #pragma unroll
@@ -439,13 +441,14 @@ __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __
                 for (int t = 0; t < 4; ++t) { mlo[t] = fmin(hp[t], 0.0); mhi[t] = -fmax(hp[t], 0.0); }
                 float f[SPL];
                 unpack(qv[u], f);
-                if (SPL == 1) {
+                if constexpr (SPL == 1) {
                     const double qq = (double)f[0];
 #pragma unroll
                     for (int t = 0; t < 3; ++t) acc[0][t] = fma(lowm[t], qq, acc[0][t]);
 #pragma unroll
                     for (int t = 0; t < 4; ++t) acc[0][3 + t] = fma(hi1 ? mhi[t] : mlo[t], qq, acc[0][3 + t]);
-                } else if (l >= 2) {
+                } else {
+                  if (l >= 2) {
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
                         const int s = lane * SPL + 2 * g;
@@ -465,6 +468,7 @@ __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __
 #pragma unroll
                         for (int t = 0; t < 4; ++t) acc[g][3 + t] = fma(mhi[t], q1, fma(mlo[t], q0, acc[g][3 + t]));
                     }
+                  }
                 }
             }
         }

@@ -58,6 +58,10 @@ struct DBuf {
         n = n_;
     }
     void ensure(size_t n_) { if (n < n_) alloc(n_); }
+    // streamed arrays get a 64-element tail so predicated vector/prefetch
+    // loads just past the logical end stay inside the allocation
+    void alloc_padded(size_t n_) { alloc(n_ + 64); n = n_ + 64; }
+    void ensure_padded(size_t n_) { if (n < n_ + 64) alloc_padded(n_); }
     void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
     void swap(DBuf& o) { std::swap(p, o.p); std::swap(n, o.n); }
 };
@@ -173,8 +177,13 @@ static inline unsigned blocks_for(uint64_t n, unsigned bs) { return (unsigned)((
 
 static void launched(Ctx* c, int n = 1) { c->launches += n; }
 
-static void check_launch(Ctx* c) {
+static bool g_sync_check = std::getenv("WAMGPU_SYNC_CHECK") != nullptr;  // debug: sync + check every launch
+static void check_launch(Ctx* c, const char* what = "kernel") {
     CK(cudaGetLastError());
+    if (g_sync_check) {
+        const cudaError_t e = cudaStreamSynchronize(c->st);
+        if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+    }
     launched(c);
 }
 
@@ -195,8 +204,8 @@ static int bits_for(uint64_t n) {
 // stable sort of (key, value) pairs by key; output in keys_out / vals_out
 static void sort_pairs(Ctx* c, DBuf<unsigned>& kin, DBuf<uint2>& vin, DBuf<unsigned>& kout, DBuf<uint2>& vout,
                        uint64_t n, uint64_t maxkey) {
-    kout.ensure(std::max<uint64_t>(n, 1));
-    vout.ensure(std::max<uint64_t>(n, 1));
+    kout.ensure_padded(std::max<uint64_t>(n, 1));
+    vout.ensure_padded(std::max<uint64_t>(n, 1));
     if (n == 0) return;
     const int bits = bits_for(maxkey);
     auto vi = reinterpret_cast<unsigned long long*>(vin.p);
@@ -246,14 +255,14 @@ static void finish_matrix(Ctx* c) {
     c->cub_tmp.release();
     if (c->nnz) {
         k_csr_to_pairs<<<c->sms * 8, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, kin.p, vin.p);
-        check_launch(c);
+        check_launch(c, "k_csr_to_pairs");
     }
     sort_pairs(c, kin, vin, kout, vout, c->nnz, c->N);
     kin.release();
     vin.release();
     c->cp.alloc(c->N + 1);
     k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(kout.p, c->nnz, c->N, c->cp.p);
-    check_launch(c);
+    check_launch(c, "k_bounds");
     c->C.swap(vout);
     kout.release();
     c->cub_tmp.release();
@@ -316,16 +325,16 @@ static void set_geometry(Ctx* c, const wamgpu_geometry& g) {
         CK(cudaMemcpyAsync(dr.p, rays.data() + c->row0, c->Ml * sizeof(RayDev), cudaMemcpyHostToDevice, c->st));
     c->rp.alloc(c->Ml + 1);
     k_trace_count<<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(dr.p, c->Ml, g.nx, g.ny, g.voxel_size, c->rp.p);
-    check_launch(c);
+    check_launch(c, "k_trace_count");
     exclusive_scan_u64(c, c->rp.p, c->Ml + 1);
     unsigned long long nnz = 0;
     CK(cudaMemcpyAsync(&nnz, c->rp.p + c->Ml, sizeof(nnz), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     c->nnz = nnz;
-    c->A.alloc(std::max<uint64_t>(nnz, 1));
+    c->A.alloc_padded(std::max<uint64_t>(nnz, 1));
     if (c->Ml) {
         k_trace_fill<<<blocks_for(c->Ml, 128), 128, 0, c->st>>>(dr.p, c->Ml, g.nx, g.ny, g.voxel_size, c->rp.p, c->A.p);
-        check_launch(c);
+        check_launch(c, "k_trace_fill");
     }
     finish_matrix(c);
     build_tile_order(c);
@@ -364,7 +373,7 @@ static void set_matrix_csr(Ctx* c, uint64_t rows, uint64_t cols, uint64_t nnz, c
         std::memcpy(&ent[k].y, &f, 4);
     }
     c->rp.alloc(c->Ml + 1);
-    c->A.alloc(std::max<uint64_t>(c->nnz, 1));
+    c->A.alloc_padded(std::max<uint64_t>(c->nnz, 1));
     CK(cudaMemcpyAsync(c->rp.p, lrp.data(), (c->Ml + 1) * 8, cudaMemcpyHostToDevice, c->st));
     if (c->nnz) CK(cudaMemcpyAsync(c->A.p, ent.data(), c->nnz * 8, cudaMemcpyHostToDevice, c->st));
     finish_matrix(c);
@@ -408,7 +417,7 @@ static void back_launch(Ctx* c, const float* w, double* out, const double* bam) 
         switch (spl_of(c)) { case 1: B3(1) break; case 2: B3(2) break; default: B3(4) break; }
 #undef B3
     }
-    check_launch(c);
+    check_launch(c, "k_back3");
     c->timer_end(T_BACK);
     c->tm.back_launches++;
 }
@@ -426,7 +435,7 @@ static void forward_plain(Ctx* c, const float* mu, double* l) {
         switch (spl_of(c)) { case 1: F3(1) break; case 2: F3(2) break; default: F3(4) break; }
 #undef F3
     }
-    check_launch(c);
+    check_launch(c, "k_forward3");
 }
 
 // q = I0 exp(-H mu), objective -> scal[0] (all-reduced), record
@@ -456,24 +465,24 @@ static void forward_fused(Ctx* c, bool record) {
         switch (spl_of(c)) { case 1: F3(1) break; case 2: F3(2) break; default: F3(4) break; }
 #undef F3
     }
-    check_launch(c);
+    check_launch(c, "k_forward3");
     c->timer_end(T_FWD);
     c->tm.fwd_launches++;
     k_sum_partials<<<1, 1024, 0, c->st>>>(c->partial.p, nparts, c->scal.p);
-    check_launch(c);
+    check_launch(c, "k_sum_partials");
     allreduce_sum(c, c->scal.p, 1);
     if (record) {
         k_record<<<1, 32, 0, c->st>>>(c->scal.p, c->counters.p, c->objs.p, c->cums.p, c->it.p);
-        check_launch(c);
+        check_launch(c, "k_record");
     }
 }
 
 static double device_max(Ctx* c, const double* v, uint64_t n) {
     const int nb = (int)std::min<uint64_t>(std::max<uint64_t>(1, (n + 255) / 256), 1024);
     k_max_partials<<<nb, 256, 0, c->st>>>(v, n, c->partial.p);
-    check_launch(c);
+    check_launch(c, "k_max_partials");
     k_max_partials<<<1, 256, 0, c->st>>>(c->partial.p, (uint64_t)nb, c->scal.p + 1);
-    check_launch(c);
+    check_launch(c, "k_max_partials");
     allreduce_max(c, c->scal.p + 1, 1);
     double m = 0.0;
     CK(cudaMemcpyAsync(&m, c->scal.p + 1, 8, cudaMemcpyDeviceToHost, c->st));
@@ -496,7 +505,7 @@ static void launch_walk(Ctx* c, int L, unsigned long long* cnt, const unsigned l
         default: throw ConfigError("haar: depth beyond the device walk");
     }
 #undef WALK_CASE
-    check_launch(c);
+    check_launch(c, "k_walk");
 }
 
 
@@ -551,7 +560,7 @@ static void launch_walk_lv(Ctx* c, unsigned long long* cnt, const unsigned long 
         default: throw ConfigError("haar: depth beyond the device walk");
     }
 #undef LV_CASE
-    check_launch(c);
+    check_launch(c, "k_walk_lv");
 }
 
 
@@ -627,7 +636,7 @@ static void launch_walk3h(Ctx* c, int nlev, unsigned long long* cnt, const unsig
         default: throw ConfigError("haar3: depth beyond the device walk");
     }
 #undef W3
-    check_launch(c);
+    check_launch(c, "k_walk3h");
 }
 
 // Psi lists (per in-plane block with any active z-block): count -> scan ->
@@ -644,16 +653,16 @@ static void rebuild_psi3(Ctx* c, int nlev) {
     if (tot) launch_walk3h<2>(c, nlev, nullptr, c->wcnt.p);
     DBuf<uint2> sidx;
     sort_pairs(c, c->kin_s, c->vin_s, c->kout_s, sidx, tot, c->nkeys3);
-    c->E3ray.ensure(n1);
-    c->E3psi.ensure(n1);
+    c->E3ray.ensure_padded(n1);
+    c->E3psi.ensure_padded(n1);
     if (tot) {
         k_gather_psi<<<blocks_for(tot, 256), 256, 0, c->st>>>(tot, sidx.p, c->pray_s.p, c->ppsi_s.p, c->E3ray.p,
                                                                c->E3psi.p);
-        check_launch(c);
+        check_launch(c, "k_gather_psi");
     }
     c->np.ensure(c->nkeys3 + 1);
     k_bounds<<<blocks_for(c->nkeys3 + 1, 256), 256, 0, c->st>>>(c->kout_s.p, tot, c->nkeys3, c->np.p);
-    check_launch(c);
+    check_launch(c, "k_bounds");
     c->nnz_phi = tot;
     CK(cudaStreamSynchronize(c->st));
 }
@@ -820,7 +829,7 @@ static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
             back_into(c, c->q.p, c->g.p);
             allreduce_sum(c, c->g.p, c->N);
             k_am_update<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->g.p, c->bam.p, c->mu.p, c->Z0, c->flag.p);
-            check_launch(c);
+            check_launch(c, "k_am_update");
         }
         CK(cudaMemsetAsync(c->counters.p, 0, 8, c->st));
         forward_fused(c, true);
@@ -855,7 +864,7 @@ static void tile_launch(Ctx* c, int mode, double* mu64, double* out) {
         k_tile3h<<<grid, 256, smem, c->st>>>(mode, c->nx, c->ny, c->nzl, slab_stride(c), c->L, c->g.p, c->g.p + NV(c),
                                              c->bdata.p, c->act.p, c->off, c->beta.p, c->mu.p, mu64, out, c->bp_dbg.p,
                                              c->bm_dbg.p, c->Z0, c->counters.p, c->flag.p);
-        check_launch(c);
+        check_launch(c, "k_tile3h");
         return;
     }
     if (c->nzl == 1) {
@@ -875,7 +884,7 @@ static void tile_launch(Ctx* c, int mode, double* mu64, double* out) {
                                             c->act.p, c->off, c->beta.p, c->mu.p, mu64, out, c->bp_dbg.p,
                                             c->bm_dbg.p, c->Z0, c->counters.p, c->flag.p);
     }
-    check_launch(c);
+    check_launch(c, "k_tile3");
 }
 
 static void rebuild_phi(Ctx* c) {
@@ -913,7 +922,7 @@ static void rebuild_phi(Ctx* c) {
     sort_pairs(c, c->kin_s, c->vin_s, c->kout_s, c->E, tot, c->N);
     c->np.ensure(c->N + 1);
     k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(c->kout_s.p, tot, c->N, c->np.p);
-    check_launch(c);
+    check_launch(c, "k_bounds");
     c->nnz_phi = tot;
     CK(cudaStreamSynchronize(c->st));
 }
@@ -1000,7 +1009,7 @@ static void wam_step(Ctx* c) {
                                                    c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3);
         switch (spl_of(c)) { case 1: S3H(1) break; case 2: S3H(2) break; default: S3H(4) break; }
 #undef S3H
-        check_launch(c);
+        check_launch(c, "k_split3h");
         c->timer_end(T_SPLIT);
         c->tm.split_launches++;
     } else if (!c->haar3 && c->nlist) {
@@ -1014,7 +1023,7 @@ static void wam_step(Ctx* c) {
             switch (spl_of(c)) { case 1: S3(1) break; case 2: S3(2) break; default: S3(4) break; }
 #undef S3
         }
-        check_launch(c);
+        check_launch(c, "k_split3");
         c->timer_end(T_SPLIT);
         c->tm.split_launches++;
     }
@@ -1046,9 +1055,9 @@ static int64_t wam_expand(Ctx* c, double factor) {
         int64_t newly = 0;
         const int nb = 1024;
         k_max_slab<<<nb, 256, 0, c->st>>>(c->mu64.p, c->N, c->nzl, slab_stride(c), c->partial.p);
-        check_launch(c);
+        check_launch(c, "k_max_slab");
         k_max_partials<<<1, 256, 0, c->st>>>(c->partial.p, (uint64_t)nb, c->scal.p + 1);
-        check_launch(c);
+        check_launch(c, "k_max_partials");
         allreduce_max(c, c->scal.p + 1, 1);
         double mx = 0.0;
         CK(cudaMemcpyAsync(&mx, c->scal.p + 1, 8, cudaMemcpyDeviceToHost, c->st));
@@ -1058,7 +1067,7 @@ static int64_t wam_expand(Ctx* c, double factor) {
             k_mark3h<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->nx, c->ny, c->nzl, slab_stride(c), c->L,
                                                                          c->mu64.p, factor * mx, c->act.p,
                                                                          c->act_new.p, c->off);
-            check_launch(c);
+            check_launch(c, "k_mark3h");
             c->act.swap(c->act_new);
             std::vector<uint8_t> h(c->act_bytes);
             CK(cudaMemcpyAsync(h.data(), c->act.p, c->act_bytes, cudaMemcpyDeviceToHost, c->st));
@@ -1079,7 +1088,7 @@ static int64_t wam_expand(Ctx* c, double factor) {
     if (c->nzl > 1 || c->nz > 1) {                 // z-summed image, slabs all-reduced
         c->dscratch.ensure(c->N);
         k_zsum<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->nzl, slab_stride(c), c->mu64.p, c->dscratch.p);
-        check_launch(c);
+        check_launch(c, "k_zsum");
         allreduce_sum(c, c->dscratch.p, c->N);
         crit = c->dscratch.p;
     }
@@ -1090,7 +1099,7 @@ static int64_t wam_expand(Ctx* c, double factor) {
         CK(cudaMemcpyAsync(c->act_new.p, c->act.p, c->act_bytes, cudaMemcpyDeviceToDevice, c->st));
         k_mark<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->nx, c->ny, c->L, crit, thr, c->act.p, c->act_new.p,
                                                           c->off);
-        check_launch(c);
+        check_launch(c, "k_mark");
         c->act.swap(c->act_new);
         std::vector<uint8_t> h(c->act_bytes);
         CK(cudaMemcpyAsync(h.data(), c->act.p, c->act_bytes, cudaMemcpyDeviceToHost, c->st));
