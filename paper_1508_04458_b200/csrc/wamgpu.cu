@@ -218,13 +218,13 @@ static void sort_pairs(Ctx* c, DBuf<unsigned>& kin, DBuf<uint2>& vin, DBuf<unsig
 }
 
 static void allreduce_sum(Ctx* c, double* buf, size_t n) {
-    if (c->nranks <= 1) return;
+    if (!c->comm) return;   // single GPU without a communicator
     c->timer_begin(T_COMM);
     NK(ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, c->comm, c->st));
     c->timer_end(T_COMM);
 }
 static void allreduce_max(Ctx* c, double* buf, size_t n) {
-    if (c->nranks <= 1) return;
+    if (!c->comm) return;
     c->timer_begin(T_COMM);
     NK(ncclAllReduce(buf, buf, n, ncclDouble, ncclMax, c->comm, c->st));
     c->timer_end(T_COMM);
@@ -823,7 +823,7 @@ static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
     if (c->algo != 1) throw ContractError("am: not initialised");
     ensure_records(c, n);
     for (int i = 0; i < n; ++i) {
-        if (c->nranks == 1 || c->nzl > 1) {
+        if (!c->comm || c->nzl > 1) {
             back_launch(c, c->q.p, nullptr, c->bam.p);   // fused multiplicative update
         } else {
             back_into(c, c->q.p, c->g.p);
@@ -1238,11 +1238,12 @@ int wamgpu_set_comm(wamgpu_ctx* ctx, const void* id128, int rank, int nranks) {
         if (ctx->comm) { ncclCommDestroy(ctx->comm); ctx->comm = nullptr; }
         ctx->rank = rank;
         ctx->nranks = nranks;
-        if (nranks > 1) {
-            NEED(id128);
+        if (id128) {   // nranks == 1 with an id: a 1-rank communicator (exercises the NCCL path)
             ncclUniqueId id;
             std::memcpy(&id, id128, sizeof(id));
             NK(ncclCommInitRank(&ctx->comm, nranks, id, rank));
+        } else if (nranks > 1) {
+            throw ContractError("set_comm: an ncclUniqueId is required for nranks > 1");
         }
     })
 }
