@@ -32,6 +32,16 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 __device__ __forceinline__ double hval(uint2 e) { return (double)__uint_as_float(e.y); }
 
+// Device layout of the 2D image mu: 8 x 4 voxel tiles (one 128-byte line per
+// tile) when lgx = log2(nx) >= 3, so the gathers along a ray -- which step by
+// +-1 or +-nx in the reference layout (image.hpp:14) -- stay inside a line for
+// several steps in every direction.  lgx < 0: reference row-major layout.
+__device__ __host__ __forceinline__ unsigned mu_addr(unsigned col, int lgx) {
+    if (lgx < 0) return col;
+    const unsigned ix = col & ((1u << lgx) - 1u), iy = col >> lgx;
+    return ((((iy >> 2) << (lgx - 3)) + (ix >> 3)) << 5) + ((iy & 3u) << 3) + (ix & 7u);
+}
+
 // Streaming (evict-first) 8-byte load of a matrix entry: the matrix is read
 // once per pass, keep L2 for the gathered vectors.
 __device__ __forceinline__ uint2 ld_stream(const uint2* p) { return __ldcs(p); }
@@ -161,7 +171,7 @@ __device__ __forceinline__ double idiv_term(double d, double q) {
 template <int G, int UNROLL = 8>
 __device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
                                         const uint64_t (&b)[G > 1 ? G - 1 : 1], uint64_t hi, int lane,
-                                        double (&out)[G]) {
+                                        double (&out)[G], int lgx = -1) {
     double acc[G][2];
 #pragma unroll
     for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = 0.0;
@@ -181,7 +191,7 @@ __device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float
         }
         float v[UNROLL];
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(x + ec[u].x);
+        for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(x + mu_addr(ec[u].x, lgx));
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
             const double h = hval(ec[u]), xv = (double)v[u];
@@ -213,7 +223,7 @@ __global__ void __launch_bounds__(256, MINB) k_forward(uint64_t M, const unsigne
                                                  const uint2* __restrict__ A, const float* __restrict__ mu,
                                                  const float* __restrict__ I0, const float* __restrict__ d,
                                                  float* __restrict__ q, double* __restrict__ lout,
-                                                 double* __restrict__ partial, int* __restrict__ flag) {
+                                                 double* __restrict__ partial, int* __restrict__ flag, int lgx) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t ntask = (M + FG - 1) / FG;
@@ -229,7 +239,7 @@ __global__ void __launch_bounds__(256, MINB) k_forward(uint64_t M, const unsigne
 #pragma unroll
         for (int g = 0; g < FG - 1; ++g) bnd[g] = __shfl_sync(0xffffffffu, myrp, min(g + 1, nr));
         double l[FG];
-        seg_dot<FG, UNR>(A, mu, lo, bnd, hi, lane, l);
+        seg_dot<FG, UNR>(A, mu, lo, bnd, hi, lane, l, lgx);
         // lane g finishes row y0+g: Beer's law, I-divergence term
         double lg = l[0];
 #pragma unroll
@@ -270,7 +280,7 @@ template <int MODE, int UNR = 8, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) k_back(uint64_t N, const unsigned long long* __restrict__ cp,
                                               const uint2* __restrict__ C, const float* __restrict__ w,
                                               double* __restrict__ g, const double* __restrict__ bam,
-                                              float* __restrict__ mu, double Z0, int* __restrict__ flag) {
+                                              float* __restrict__ mu, double Z0, int* __restrict__ flag, int lgx) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t x = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; x < N; x += W) {
@@ -284,9 +294,10 @@ __global__ void __launch_bounds__(256, MINB) k_back(uint64_t N, const unsigned l
             } else {
                 const double b = bam[x];
                 if (b > 0.0 && c > 0.0) {
-                    const double v = (double)mu[x] + log(c / b) / Z0;
+                    const unsigned mx = mu_addr((unsigned)x, lgx);
+                    const double v = (double)mu[mx] + log(c / b) / Z0;
                     if (!isfinite(v)) atomicOr(flag, 2);
-                    mu[x] = (float)((0.0 < v) ? v : 0.0);
+                    mu[mx] = (float)((0.0 < v) ? v : 0.0);
                 }
             }
         }
@@ -295,14 +306,15 @@ __global__ void __launch_bounds__(256, MINB) k_back(uint64_t N, const unsigned l
 
 // AM update from an (all-reduced) back projection g (multi-GPU path).
 __global__ void k_am_update(uint64_t N, const double* __restrict__ g, const double* __restrict__ bam,
-                            float* __restrict__ mu, double Z0, int* __restrict__ flag) {
+                            float* __restrict__ mu, double Z0, int* __restrict__ flag, int lgx) {
     uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= N) return;
     const double b = bam[x], c = g[x];
     if (b > 0.0 && c > 0.0) {
-        const double v = (double)mu[x] + log(c / b) / Z0;
+        const unsigned mx = mu_addr((unsigned)x, lgx);
+        const double v = (double)mu[mx] + log(c / b) / Z0;
         if (!isfinite(v)) atomicOr(flag, 2);
-        mu[x] = (float)((0.0 < v) ? v : 0.0);
+        mu[mx] = (float)((0.0 < v) ? v : 0.0);
     }
 }
 
@@ -447,7 +459,7 @@ __global__ void k_tile(int mode, int nx, int ny, int L, const double* __restrict
                        const double* __restrict__ bdata, const uint8_t* __restrict__ act, ActOff off,
                        float* __restrict__ beta, float* __restrict__ mu, double* __restrict__ mu64,
                        double* __restrict__ out, double* __restrict__ bp_out, double* __restrict__ bm_out,
-                       double Z0, unsigned long long* __restrict__ counters, int* __restrict__ flag) {
+                       double Z0, unsigned long long* __restrict__ counters, int* __restrict__ flag, int lgx) {
     extern __shared__ double sm[];
     const int TS = 1 << L, T2 = TS * TS;
     double* x = sm;
@@ -505,7 +517,7 @@ __global__ void k_tile(int mode, int nx, int ny, int L, const double* __restrict
     tile_inv(x, t, TS, L);
     for (int i = threadIdx.x; i < T2; i += blockDim.x) {
         const uint64_t p = base + (uint64_t)(i / TS) * nx + i % TS;
-        mu[p] = (float)x[i];
+        mu[mu_addr((unsigned)p, lgx)] = (float)x[i];
         if (mu64) mu64[p] = x[i];
     }
 }

@@ -128,6 +128,7 @@ struct wamgpu_ctx {
     double Z0 = 0.0;
     DBuf<double> scal, partial;
     int nblk_row = 1, nblk_col = 1;
+    int lgx = -1;   // 2D mu in 8x4 tiles (mu_addr) when >= 0
     int fwd_variant = 0, back_variant = 0;  // SpMV tuning knobs (WAMGPU_FWD_VARIANT / WAMGPU_BACK_VARIANT)
     DBuf<unsigned long long> counters;
     DBuf<int> flag, it;
@@ -265,6 +266,12 @@ static void finish_matrix(Ctx* c) {
     check_launch(c, "k_bounds");
     c->C.swap(vout);
     kout.release();
+    {   // tiled 2D image layout for the forward gathers (knob WAMGPU_MU_TILED=0 disables)
+        const char* e = std::getenv("WAMGPU_MU_TILED");
+        const bool want = !(e && e[0] == '0');
+        const bool pow2 = c->nx >= 8 && (c->nx & (c->nx - 1)) == 0 && c->ny % 4 == 0;
+        c->lgx = (want && pow2 && c->nz == 1) ? 31 - __builtin_clz((unsigned)c->nx) : -1;
+    }
     c->cub_tmp.release();
     c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->Ml + 7) / 8, (uint64_t)c->sms * 16));
     c->nblk_col = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->N + 7) / 8, (uint64_t)c->sms * 16));
@@ -396,9 +403,9 @@ static void back_launch(Ctx* c, const float* w, double* out, const double* bam) 
     if (c->nzl == 1) {
 #define BV(U, MB)                                                                                                 \
     if (bam) k_back<1, U, MB><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, nullptr, bam, c->mu.p,     \
-                                                              c->Z0, c->flag.p);                                  \
+                                                              c->Z0, c->flag.p, c->lgx);                          \
     else k_back<0, U, MB><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0,   \
-                                                          c->flag.p);
+                                                          c->flag.p, -1);
         switch (c->back_variant) {
             case 1: BV(4, 1) break;
             case 2: BV(4, 8) break;
@@ -427,7 +434,7 @@ static void back_into(Ctx* c, const float* w, double* out) { back_launch(c, w, o
 static void forward_plain(Ctx* c, const float* mu, double* l) {
     if (c->nzl == 1) {
         k_forward<0><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, mu, nullptr, nullptr, nullptr, l, nullptr,
-                                                    c->flag.p);
+                                                    c->flag.p, c->lgx);
     } else {
         const unsigned nb = nblk_warp(c, c->Ml);
 #define F3(S) k_forward3<0, S><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu, nullptr, nullptr, nullptr, \
@@ -445,7 +452,7 @@ static void forward_fused(Ctx* c, bool record) {
     if (c->nzl == 1) {
 #define FV(FGv, U, MB)                                                                                              \
     k_forward<1, FGv, U, MB><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p,     \
-                                                            c->q.p, nullptr, c->partial.p, c->flag.p);
+                                                            c->q.p, nullptr, c->partial.p, c->flag.p, c->lgx);
         switch (c->fwd_variant) {
             case 1: FV(1, 8, 1) break;
             case 2: FV(2, 4, 1) break;
@@ -768,6 +775,20 @@ static void host_par(uint64_t n, Fn&& fn) {
 }
 static uint64_t NV(const Ctx* c) { return c->N * (uint64_t)slab_stride(c); }
 static uint64_t MV(const Ctx* c) { return c->Ml * (uint64_t)slab_stride(c); }
+// 2D image upload/download through the tiled device layout (mu_addr)
+static void upload_image2(Ctx* c, const double* ref, float* dev) {
+    std::vector<float> h(c->N);
+    for (uint64_t x = 0; x < c->N; ++x) h[mu_addr((unsigned)x, c->lgx)] = (float)ref[x];
+    CK(cudaMemcpyAsync(dev, h.data(), c->N * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+}
+static void download_image2(Ctx* c, const float* dev, double* ref) {
+    std::vector<float> h(c->N);
+    CK(cudaMemcpyAsync(h.data(), dev, c->N * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (uint64_t x = 0; x < c->N; ++x) ref[x] = h[mu_addr((unsigned)x, c->lgx)];
+}
+
 template <class T>
 static void upload_slab(Ctx* c, const double* ref, T* dev, uint64_t n_inner, uint64_t ref_stride, uint64_t ref_off,
                         bool local = false) {
@@ -804,8 +825,12 @@ static void am_init(Ctx* c, const double* init_mu) {
     c->mu.ensure(NV(c));
     c->g.ensure(2 * NV(c));
     c->bam.ensure(NV(c));
-    if (init_mu) upload_slab<float>(c, init_mu, c->mu.p, c->N, c->N, 0);
-    else CK(cudaMemsetAsync(c->mu.p, 0, NV(c) * 4, c->st));
+    if (init_mu) {
+        if (c->nzl == 1) upload_image2(c, init_mu, c->mu.p);
+        else upload_slab<float>(c, init_mu, c->mu.p, c->N, c->N, 0);
+    } else {
+        CK(cudaMemsetAsync(c->mu.p, 0, NV(c) * 4, c->st));
+    }
     back_into(c, c->d.p, c->bam.p);  // b(x) = sum_y d(y) h(y|x)
     if (c->nzl == 1) allreduce_sum(c, c->bam.p, c->N);
     if (!c->act.p) { c->act.alloc(1); }
@@ -828,7 +853,8 @@ static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
         } else {
             back_into(c, c->q.p, c->g.p);
             allreduce_sum(c, c->g.p, c->N);
-            k_am_update<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->g.p, c->bam.p, c->mu.p, c->Z0, c->flag.p);
+            k_am_update<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->g.p, c->bam.p, c->mu.p, c->Z0, c->flag.p,
+                                                                   c->lgx);
             check_launch(c, "k_am_update");
         }
         CK(cudaMemsetAsync(c->counters.p, 0, 8, c->st));
@@ -873,7 +899,7 @@ static void tile_launch(Ctx* c, int mode, double* mu64, double* out) {
         const size_t smem = 2ull * TS * TS * sizeof(double);
         k_tile<<<grid, bs, smem, c->st>>>(mode, c->nx, c->ny, c->L, c->g.p, c->g.p + c->N, c->bdata.p, c->act.p,
                                           c->off, c->beta.p, c->mu.p, mu64, out, c->bp_dbg.p, c->bm_dbg.p, c->Z0,
-                                          c->counters.p, c->flag.p);
+                                          c->counters.p, c->flag.p, c->lgx);
     } else {
         const int sc = std::max(1, std::min({32, c->nzl, 4096 / (TS * TS)}));   // slices per CTA
         dim3 grid(c->nx >> c->L, c->ny >> c->L, (c->nzl + sc - 1) / sc);
@@ -1326,7 +1352,8 @@ int wamgpu_forward_project(wamgpu_ctx* ctx, const double* mu, double* l) {
         Ctx* c = ctx;
         c->fscratch.ensure(NV(c));
         c->dscratch.ensure(std::max<uint64_t>(MV(c), 1));
-        upload_slab<float>(c, mu, c->fscratch.p, c->N, c->N, 0);
+        if (c->nzl == 1) upload_image2(c, mu, c->fscratch.p);
+        else upload_slab<float>(c, mu, c->fscratch.p, c->N, c->N, 0);
         forward_plain(c, c->fscratch.p, c->dscratch.p);
         download_slab<double>(c, c->dscratch.p, l, c->Ml, c->Ml, 0, true);
         check_flag(c, "forward_project");
@@ -1431,7 +1458,8 @@ int wamgpu_get_image(const wamgpu_ctx* ctx, double* mu) {
         NEED(ctx); NEED(mu);
         Ctx* c = const_cast<wamgpu_ctx*>(ctx);
         if (!c->algo) throw ContractError("get_image: no solver state");
-        download_slab<float>(c, c->mu.p, mu, c->N, c->N, 0);
+        if (c->nzl == 1) download_image2(c, c->mu.p, mu);
+        else download_slab<float>(c, c->mu.p, mu, c->N, c->N, 0);
     })
 }
 
