@@ -168,7 +168,7 @@ __device__ __forceinline__ double idiv_term(double d, double q) {
 // fp64 accumulation (products of two fp32 are exact in fp64); segment
 // selection is by predicated fma with h=0 (an exact no-op); fixed
 // xor-butterfly reduction (deterministic).
-template <int G, int UNROLL = 8>
+template <int G, int UNROLL = 8, bool TILED = false>
 __device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
                                         const uint64_t (&b)[G > 1 ? G - 1 : 1], uint64_t hi, int lane,
                                         double (&out)[G], int lgx = -1) {
@@ -191,7 +191,14 @@ __device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float
         }
         float v[UNROLL];
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) v[u] = __ldg(x + mu_addr(ec[u].x, lgx));
+        for (int u = 0; u < UNROLL; ++u) {
+            if constexpr (TILED) {
+                const unsigned col = ec[u].x, ix = col & ((1u << lgx) - 1u), iy = col >> lgx;
+                v[u] = __ldg(x + (((((iy >> 2) << (lgx - 3)) + (ix >> 3)) << 5) + ((iy & 3u) << 3) + (ix & 7u)));
+            } else {
+                v[u] = __ldg(x + ec[u].x);
+            }
+        }
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
             const double h = hval(ec[u]), xv = (double)v[u];
@@ -218,7 +225,7 @@ __device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float
 // MODE 1: fused Beer's law + I-divergence: q = fp32(I0 exp(-l)), per-block fp64
 // partial of the objective (deterministic block order).
 constexpr int FG_DEFAULT = 2;  // rows per warp task in the forward kernel (measured best of 1/2/4)
-template <int MODE, int FG = FG_DEFAULT, int UNR = 8, int MINB = 1>
+template <int MODE, int FG = FG_DEFAULT, int UNR = 8, int MINB = 1, bool TILED = false>
 __global__ void __launch_bounds__(256, MINB) k_forward(uint64_t M, const unsigned long long* __restrict__ rp,
                                                  const uint2* __restrict__ A, const float* __restrict__ mu,
                                                  const float* __restrict__ I0, const float* __restrict__ d,
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__(256, MINB) k_forward(uint64_t M, const unsigne
 #pragma unroll
         for (int g = 0; g < FG - 1; ++g) bnd[g] = __shfl_sync(0xffffffffu, myrp, min(g + 1, nr));
         double l[FG];
-        seg_dot<FG, UNR>(A, mu, lo, bnd, hi, lane, l, lgx);
+        seg_dot<FG, UNR, TILED>(A, mu, lo, bnd, hi, lane, l, lgx);
         // lane g finishes row y0+g: Beer's law, I-divergence term
         double lg = l[0];
 #pragma unroll

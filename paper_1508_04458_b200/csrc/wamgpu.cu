@@ -433,8 +433,13 @@ static void back_into(Ctx* c, const float* w, double* out) { back_launch(c, w, o
 // plain l = H mu (fp64 out), for forward_project
 static void forward_plain(Ctx* c, const float* mu, double* l) {
     if (c->nzl == 1) {
-        k_forward<0><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, mu, nullptr, nullptr, nullptr, l, nullptr,
-                                                    c->flag.p, c->lgx);
+        if (c->lgx >= 0)
+            k_forward<0, FG_DEFAULT, 8, 1, true><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, mu, nullptr,
+                                                                              nullptr, nullptr, l, nullptr, c->flag.p,
+                                                                              c->lgx);
+        else
+            k_forward<0><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, mu, nullptr, nullptr, nullptr, l,
+                                                        nullptr, c->flag.p, -1);
     } else {
         const unsigned nb = nblk_warp(c, c->Ml);
 #define F3(S) k_forward3<0, S><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu, nullptr, nullptr, nullptr, \
@@ -451,8 +456,14 @@ static void forward_fused(Ctx* c, bool record) {
     int nparts = c->nblk_row;
     if (c->nzl == 1) {
 #define FV(FGv, U, MB)                                                                                              \
-    k_forward<1, FGv, U, MB><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p,     \
-                                                            c->q.p, nullptr, c->partial.p, c->flag.p, c->lgx);
+    if (c->lgx >= 0)                                                                                               \
+        k_forward<1, FGv, U, MB, true><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p,    \
+                                                                    c->d.p, c->q.p, nullptr, c->partial.p,         \
+                                                                    c->flag.p, c->lgx);                            \
+    else                                                                                                           \
+        k_forward<1, FGv, U, MB, false><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p,   \
+                                                                     c->d.p, c->q.p, nullptr, c->partial.p,        \
+                                                                     c->flag.p, -1);
         switch (c->fwd_variant) {
             case 1: FV(1, 8, 1) break;
             case 2: FV(2, 4, 1) break;
