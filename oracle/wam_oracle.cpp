@@ -1274,12 +1274,16 @@ int orc_wam_iterate(orc_problem* p, int n, orc_record* recs) {
                 } else {
                     dwt2(nx, ny, p->nz, L, g.data(), S.data());
                     bm.assign(NT, 0.0);
+                    // b-(z): exact fixed-point sum (2^-20 units) of q*phi over the
+                    // Phi^- column -- order-independent, mirrored bit-for-bit by
+                    // the GPU split whatever order its columns hold
                     for (int s = 0; s < p->nz; ++s)
                         for (uint64_t z = 0; z < N; ++z) {
-                            double acc = 0.0;
+                            long long acc = 0;
                             for (uint64_t k = p->nphi_ptr[z]; k < p->nphi_ptr[z + 1]; ++k)
-                                acc += p->q[(uint64_t)s * p->Ms + p->nphi_row[k]] * p->nphi_val[k];
-                            bm[(uint64_t)s * N + z] = acc;
+                                acc += std::llrint(p->q[(uint64_t)s * p->Ms + p->nphi_row[k]] * p->nphi_val[k] *
+                                                   1048576.0);
+                            bm[(uint64_t)s * N + z] = (double)acc * (1.0 / 1048576.0);
                         }
                 }
                 bp.resize(NT);

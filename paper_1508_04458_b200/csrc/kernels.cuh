@@ -742,12 +742,28 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
                                                     const unsigned* __restrict__ tbits, ActOff boff, int tree_words,
                                                     const double* __restrict__ zA, double* __restrict__ zrow,
                                                     unsigned long long* __restrict__ cnt,
-                                                    const unsigned long long* __restrict__ pos,
+                                                    unsigned long long* __restrict__ cursor,
+                                                    unsigned long long cap,
                                                     unsigned* __restrict__ keys, uint2* __restrict__ vals) {
+    // MODE 1: Z(y) + per-(ray, level) negative counts.  MODE 2: Z(y) + emission
+    // of every negative phi in the same pass.  Emission has no atomics in the
+    // hot loop: each lane appends (z, phi) to a private ring in shared memory;
+    // the inner loop is warp-uniform, and when any lane's ring could overflow
+    // on the next entry the WARP drains: warp scan of the ring counts, the
+    // warp's output goes to its private chunk of the global array (reserved
+    // from *cursor in chunks, one atomicAdd per chunk), and at the end the
+    // unused chunk tail is filled with the sentinel key nx*ny (sorted past every
+    // column, excluded by k_bounds).  Output: unsorted (z, y, phi) triples.
+    // The signed split sums in exact fixed point (k_split), so the order of rays
+    // inside a column is irrelevant and this one pass replaces count + scan +
+    // emit.  Slots past cap are reserved but not stored (the host retries; the
+    // reserved total is deterministic per warp, so the retry fits).
+    constexpr int kR = MODE == 2 ? 12 : 1;   // ring slots per lane
     extern __shared__ unsigned tsm[];   // tree bits (tree_words words)
     __shared__ uint2 buf[32][33];
     __shared__ unsigned long long s_lo[32], s_len[32];
     __shared__ double s_tot[L][32];
+    __shared__ uint2 ring[kR][32 * 5];   // slot-major: lanes' k-th slots are adjacent
     // warp w tracks level L - w; levels below L - nlev + 1 hold no active block
     // (tree closure), so their warps are not launched at all
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, l = L - w;
@@ -777,8 +793,10 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
     // the current quadrant cq, parked into q0..q3 when the quadrant changes
     // (the same sequential ray-order sums as four accumulators).
     double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, qa = 0.0, tot = 0.0;
-    unsigned long long count = 0, wp = 0;
-    if (MODE == 2 && y < M) wp = pos[y * L + (l - 1)];
+    unsigned long long count = 0;
+    int rc = 0;                              // ring fill (MODE 2)
+    unsigned long long cb = 0, ce = 0;       // the warp's current output chunk [cb, ce)
+    const unsigned long long chunk = (unsigned long long)max(32, 512 >> l);
     (void)nlev;
 
     auto park = [&]() {
@@ -792,20 +810,49 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
             park();
             const double st = q0 + q1, sb = q2 + q3;
             const double pH = (st - sb) * sc, pV = ((q0 + q2) - (q1 + q3)) * sc, pD = ((q0 + q3) - (q1 + q2)) * sc;
-            if (MODE == 1) tot += fabs(pH) + fabs(pV) + fabs(pD);
-            const float v[3] = {(float)pH, (float)pV, (float)pD};
-            const unsigned z[3] = {(unsigned)((hl + cbi) * nx + cbj), (unsigned)(cbi * nx + wl + cbj),
-                                   (unsigned)((hl + cbi) * nx + wl + cbj)};
-#pragma unroll
-            for (int s = 0; s < 3; ++s)
-                if (v[s] < 0.0f) {
-                    if (MODE == 1) ++count;
-                    else { keys[wp] = z[s]; vals[wp] = make_uint2((unsigned)y, __float_as_uint(v[s])); ++wp; }
-                }
+            tot += fabs(pH) + fabs(pV) + fabs(pD);
+            const float vH = (float)pH, vV = (float)pV, vD = (float)pD;
+            if constexpr (MODE == 1) {
+                count += (vH < 0.0f) + (vV < 0.0f) + (vD < 0.0f);
+            } else {
+                if (vH < 0.0f) ring[rc++][threadIdx.x] = make_uint2((unsigned)((hl + cbi) * nx + cbj), __float_as_uint(vH));
+                if (vV < 0.0f) ring[rc++][threadIdx.x] = make_uint2((unsigned)(cbi * nx + wl + cbj), __float_as_uint(vV));
+                if (vD < 0.0f)
+                    ring[rc++][threadIdx.x] = make_uint2((unsigned)((hl + cbi) * nx + wl + cbj), __float_as_uint(vD));
+            }
             q0 = q1 = q2 = q3 = 0.0;
         }
         cq = -1;
         qa = 0.0;
+    };
+
+    // warp-converged: move every lane's ring to the warp's output chunk
+    auto wdrain = [&]() {
+        unsigned pre = (unsigned)rc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += t;
+        }
+        const unsigned T = __shfl_sync(0xffffffffu, pre, 31);
+        pre -= (unsigned)rc;
+        if (T == 0) return;
+        const unsigned long long rem = ce - cb;
+        unsigned long long nb = 0, need = 0;
+        if (T > rem) {   // the rest of the current chunk, then a fresh chunk
+            need = max(chunk, (unsigned long long)T - rem);
+            if (lane == 0) nb = atomicAdd(cursor, need);
+            nb = __shfl_sync(0xffffffffu, nb, 0);
+        }
+        for (int k = 0; k < rc; ++k) {
+            const unsigned long long j = pre + (unsigned)k;
+            const unsigned long long p = j < rem ? cb + j : nb + (j - rem);
+            const uint2 r = ring[k][threadIdx.x];
+            if (p < cap) { keys[p] = r.x; vals[p] = make_uint2((unsigned)y, r.y); }
+        }
+        if (T > rem) { cb = nb + (T - rem); ce = nb + need; }
+        else cb += T;
+        rc = 0;
     };
 
     for (unsigned long long base = 0; base < maxlen; base += 32) {
@@ -818,35 +865,47 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
         cp_async_wait_all();
         __syncthreads();
         const int n = (int)min(32ull, len > base ? len - base : 0ull);
-        for (int i = 0; i < n; ++i) {
-            const uint2 e = buf[lane][i];
-            int ix, iy;
-            if (pow2) { ix = (int)(e.x & (unsigned)(nx - 1)); iy = (int)(e.x >> lgx); }
-            else { iy = (int)(e.x / (unsigned)nx); ix = (int)(e.x % (unsigned)nx); }
-            const int bi = iy >> l, bj = ix >> l;
-            const int key = bi * wl + bj;
-            if (key != cur) {
-                flush();
-                cur = key; cbi = bi; cbj = bj;
-                const unsigned bit = bo + (unsigned)key;
-                av = (tsm[bit >> 5] >> (bit & 31)) & 1u;
-            }
-            if (av) {
-                const int quad = (((iy >> (l - 1)) & 1) << 1) | ((ix >> (l - 1)) & 1);
-                if (quad != cq) {
-                    if (cq >= 0) park();
-                    cq = quad;
-                    qa = 0.0;
+        // MODE 2 keeps the warp converged (uniform trip count) for the drains
+        const int nit = MODE == 2 ? (int)min(32ull, maxlen - base) : n;
+        for (int i = 0; i < nit; ++i) {
+            if (MODE == 1 || i < n) {
+                const uint2 e = buf[lane][i];
+                int ix, iy;
+                if (pow2) { ix = (int)(e.x & (unsigned)(nx - 1)); iy = (int)(e.x >> lgx); }
+                else { iy = (int)(e.x / (unsigned)nx); ix = (int)(e.x % (unsigned)nx); }
+                const int bi = iy >> l, bj = ix >> l;
+                const int key = bi * wl + bj;
+                if (key != cur) {
+                    flush();
+                    cur = key; cbi = bi; cbj = bj;
+                    const unsigned bit = bo + (unsigned)key;
+                    av = (tsm[bit >> 5] >> (bit & 31)) & 1u;
                 }
-                qa += hval(e);
+                if (av) {
+                    const int quad = (((iy >> (l - 1)) & 1) << 1) | ((ix >> (l - 1)) & 1);
+                    if (quad != cq) {
+                        if (cq >= 0) park();
+                        cq = quad;
+                        qa = 0.0;
+                    }
+                    qa += hval(e);
+                }
             }
+            if constexpr (MODE == 2)
+                if (__any_sync(0xffffffffu, rc > kR - 3)) wdrain();
         }
         __syncthreads();
     }
     flush();
-    if (MODE == 1) {
+    if constexpr (MODE == 2) {
+        wdrain();
+        const unsigned sent = (unsigned)(nx * ny);
+        for (unsigned long long p = cb + lane; p < ce; p += 32)
+            if (p < cap) { keys[p] = sent; vals[p] = make_uint2(0u, 0u); }
+    }
+    {
         s_tot[l - 1][lane] = tot;
-        if (y < M) cnt[y * L + (l - 1)] = count;
+        if (MODE == 1 && y < M) cnt[y * L + (l - 1)] = count;
         __syncthreads();
         if (w == 0 && y < M) {
             double z = zA[y];
@@ -854,13 +913,25 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
             for (int k = L; k >= 1; --k)
                 if (k > L - nlev) z += s_tot[k - 1][lane];
             zrow[y] = z;
-            for (int k = 1; k <= L - nlev; ++k) cnt[y * L + (k - 1)] = 0;
+            if (MODE == 1)
+                for (int k = 1; k <= L - nlev; ++k) cnt[y * L + (k - 1)] = 0;
         }
     }
 }
 
 // Signed split (K5): warp per active detail coefficient,
-// b-(z) = sum over its Phi^- column of q(y) phi(y|z) in fp64.
+// b-(z) = sum over its Phi^- column of q(y) phi(y|z).  Each product (exact in
+// fp64) is rounded to a 2^-20 fixed-point integer and summed in int64: the
+// result is exact and independent of the column's entry order (so Phi^- may
+// be built in any order, and view-sharded partial sums are rank-count
+// independent).  Range: |q phi| <= ~1e7, columns <= ~1e5 entries -> < 2^61.
+constexpr double kFix = 1048576.0, kFixInv = 1.0 / 1048576.0;
+__device__ __forceinline__ long long fix_term(double q, double phi) { return __double2ll_rn(q * phi * kFix); }
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 __global__ void __launch_bounds__(256) k_split(uint64_t nlist, const unsigned* __restrict__ list,
                                                const unsigned long long* __restrict__ ptr,
                                                const uint2* __restrict__ E, const float* __restrict__ q,
@@ -870,19 +941,19 @@ __global__ void __launch_bounds__(256) k_split(uint64_t nlist, const unsigned* _
     for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlist; i += W) {
         const unsigned z = list[i];
         const uint64_t lo = ptr[z], hi = ptr[z + 1];
-        double a0 = 0.0, a1 = 0.0;
+        long long a0 = 0, a1 = 0;
         uint64_t k = lo + lane;
         for (; k + 32 < hi; k += 64) {
             const uint2 e0 = ld_stream(E + k), e1 = ld_stream(E + k + 32);
-            a0 = fma(hval(e0), (double)__ldg(q + e0.x), a0);
-            a1 = fma(hval(e1), (double)__ldg(q + e1.x), a1);
+            a0 += fix_term((double)__ldg(q + e0.x), hval(e0));
+            a1 += fix_term((double)__ldg(q + e1.x), hval(e1));
         }
         for (; k < hi; k += 32) {
             const uint2 e0 = ld_stream(E + k);
-            a0 = fma(hval(e0), (double)__ldg(q + e0.x), a0);
+            a0 += fix_term((double)__ldg(q + e0.x), hval(e0));
         }
-        const double s = warp_sum(a0 + a1);
-        if (lane == 0) bm[z] = s;
+        const long long s = warp_sum_ll(a0 + a1);
+        if (lane == 0) bm[z] = (double)s * kFixInv;
     }
 }
 

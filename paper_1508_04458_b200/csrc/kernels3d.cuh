@@ -144,22 +144,45 @@ __global__ void __launch_bounds__(256, 4) k_back3(uint64_t N, int nz, const unsi
     }
 }
 
-// K5 3D: b-[z][s] = sum over the (slice-shared) Phi^- column of z of q[y][s] phi.
+// K5 3D: b-[z][s] = sum over the (slice-shared) Phi^- column of z of q[y][s] phi,
+// exact 2^-20 fixed-point accumulation per slice (order-independent, as k_split).
 template <int SPL>
 __global__ void __launch_bounds__(256, 4) k_split3(uint64_t nlist, int nz, const unsigned* __restrict__ list,
                                                 const unsigned long long* __restrict__ ptr,
                                                 const uint2* __restrict__ E, const float* __restrict__ q,
                                                 double* __restrict__ bm) {
+    using V = typename SlabVec<SPL>::T;
+    constexpr int P = 32 * SPL;
     const int lane = threadIdx.x & 31;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlist; i += W) {
         const unsigned z = list[i];
-        double acc[SPL];
-        slab_dot<SPL>(E, q, ptr[z], ptr[z + 1], lane, acc);
+        const uint64_t lo = ptr[z], hi = ptr[z + 1];
+        long long acc[SPL];
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) acc[j] = 0;
+        constexpr int U = 8;
+        for (uint64_t k0 = lo; k0 < hi; k0 += U) {
+            uint2 e[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) e[u] = __ldg(E + (k0 + u < hi ? k0 + u : lo));
+            V v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const V*>(q + (uint64_t)e[u].x * P) + lane);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (k0 + u >= hi) break;
+                float f[SPL];
+                unpack(v[u], f);
+                const double ph = hval(e[u]);
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) acc[j] += fix_term((double)f[j], ph);
+            }
+        }
 #pragma unroll
         for (int j = 0; j < SPL; ++j) {
             const int s = lane * SPL + j;
-            if (s < nz) bm[(uint64_t)z * (32 * SPL) + s] = acc[j];
+            if (s < nz) bm[(uint64_t)z * P + s] = (double)acc[j] * kFixInv;
         }
     }
 }

@@ -98,7 +98,8 @@ struct wamgpu_ctx {
     int algo = 0;  // 1 AM, 2 WAM
     DBuf<float> mu, beta, fscratch;
     DBuf<double> g, bdata, bam, mu64, bp_dbg, bm_dbg, zrow, dscratch;
-    DBuf<unsigned long long> wcnt;      // per-ray Phi^- counts from the Z0 walk (then scanned)
+    DBuf<unsigned long long> wcnt;      // per-(ray, level) Phi^- counts (MODE 1 walk; z-row diagnostics)
+    DBuf<unsigned long long> cursor;    // Phi^- emission cursor of the merged walk
     DBuf<double> zA;                    // per-ray approximation part of Z (tree-independent)
     DBuf<uint8_t> cub_tmp;
     DBuf<unsigned> kin_s, kout_s;
@@ -550,8 +551,8 @@ static void upload_tree_bits(Ctx* c) {
 }
 
 template <int MODE>
-static void launch_walk_lv(Ctx* c, unsigned long long* cnt, const unsigned long long* pos, unsigned* keys,
-                           uint2* vals) {
+static void launch_walk_lv(Ctx* c, unsigned long long* cnt, unsigned long long* cursor, unsigned long long cap,
+                           unsigned* keys, uint2* vals) {
     const unsigned nb = blocks_for(c->Ml, 32);
     const size_t smem = (size_t)c->tree_words * 4;
     // levels that hold active blocks: L down to the finest active level
@@ -569,11 +570,10 @@ static void launch_walk_lv(Ctx* c, unsigned long long* cnt, const unsigned long 
 #define LV_CASE(LV)                                                                                              \
     case LV: {                                                                                                   \
         auto kf = k_walk_lv<MODE, LV>;                                                                           \
-        /* static smem (~10 KB) + the bit-packed tree may exceed the 48 KB default */                            \
-        if (smem > 32 * 1024) CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        /* static smem (10-35 KB) + the bit-packed tree may exceed the 48 KB default */                         \
+        if (smem > 12 * 1024) CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
         kf<<<nb, 32 * nlev, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, nlev, c->tbits.p, c->boff,      \
-                                           c->tree_words, \
-                                         c->zA.p, c->zrow.p, cnt, pos, keys, vals);                               \
+                                           c->tree_words, c->zA.p, c->zrow.p, cnt, cursor, cap, keys, vals);       \
     } break;
     switch (c->L) {
         LV_CASE(1) LV_CASE(2) LV_CASE(3) LV_CASE(4) LV_CASE(5)
@@ -703,7 +703,7 @@ static double compute_z0(Ctx* c, int levels, bool init) {
         launch_walk3h<1>(c, nlev, c->wcnt.p, nullptr);
     } else if (c->Ml) {
         upload_tree_bits(c);
-        launch_walk_lv<1>(c, c->wcnt.p, nullptr, nullptr, nullptr);
+        launch_walk_lv<1>(c, c->wcnt.p, nullptr, 0, nullptr, nullptr);
     }
     double z0 = device_max(c, c->zrow.p, c->Ml);
     if (!(z0 > 0.0)) throw NumericError("Z0: no ray intersects the active set");
@@ -945,25 +945,40 @@ static void rebuild_phi(Ctx* c) {
     c->list.ensure(std::max<size_t>(lst.size(), 1));
     if (!lst.empty())
         CK(cudaMemcpyAsync(c->list.p, lst.data(), lst.size() * 4, cudaMemcpyHostToDevice, c->st));
-    // Phi^- CSC over local rays: counts (from the Z0 walk of this tree) -> scan
-    // -> emit -> stable radix sort by z (rays stay ascending within a column)
-    const uint64_t ncnt = c->L > 0 ? (uint64_t)c->Ml * c->L : c->Ml;
-    CK(cudaMemsetAsync(c->wcnt.p + ncnt, 0, 8, c->st));
-    exclusive_scan_u64(c, c->wcnt.p, ncnt + 1);
+    // Phi^- CSC over local rays in ONE walk (k_walk_lv MODE 2, which also yields
+    // Z(y) for this tree): unsorted (z, y, phi) triples through a device cursor,
+    // retried once with the exact size if the capacity guess was short, then a
+    // radix sort by z.  Within a column the ray order is arbitrary; the split
+    // is exact fixed point, so it does not matter.
     unsigned long long tot = 0;
-    CK(cudaMemcpyAsync(&tot, c->wcnt.p + ncnt, 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    c->kin_s.ensure(std::max<uint64_t>(tot, 1));
-    c->vin_s.ensure(std::max<uint64_t>(tot, 1));
-    if (tot) {
-        launch_walk_lv<2>(c, nullptr, c->wcnt.p, c->kin_s.p, c->vin_s.p);
+    if (!lst.empty()) {
+        upload_tree_bits(c);
+        c->cursor.ensure(1);
+        // capacity guess: the active set grows several-fold per expansion and the
+        // final Phi^- holds ~nnz(H)/2 entries (cfg2: 209 M of 450 M), so start at
+        // nnz/2 -- a short guess costs a second walk
+        uint64_t cap = std::max<uint64_t>({c->kin_s.n, 4 * c->nnz_phi, c->nnz / 2, (uint64_t)1 << 20});
+        for (int attempt = 0;; ++attempt) {
+            c->kin_s.ensure(cap);
+            c->vin_s.ensure(cap);
+            CK(cudaMemsetAsync(c->cursor.p, 0, 8, c->st));
+            launch_walk_lv<2>(c, nullptr, c->cursor.p, c->kin_s.n, c->kin_s.p, c->vin_s.p);
+            CK(cudaMemcpyAsync(&tot, c->cursor.p, 8, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            if (tot <= c->kin_s.n) break;
+            if (attempt) throw NumericError("phi-: emission count changed between walks");
+            cap = tot + tot / 4;
+        }
     }
     sort_pairs(c, c->kin_s, c->vin_s, c->kout_s, c->E, tot, c->N);
     c->np.ensure(c->N + 1);
     k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(c->kout_s.p, tot, c->N, c->np.p);
     check_launch(c, "k_bounds");
-    c->nnz_phi = tot;
+    // chunk tails carry the sentinel key N (sorted last): np[N] counts the rest
+    unsigned long long valid = 0;
+    CK(cudaMemcpyAsync(&valid, c->np.p + c->N, 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
+    c->nnz_phi = valid;
 }
 
 static int64_t count_active(const Ctx* c) {
@@ -1146,8 +1161,10 @@ static int64_t wam_expand(Ctx* c, double factor) {
         for (uint64_t i = 0; i < c->act_bytes; ++i) newly += (h[i] != 0) - (c->act_host[i] != 0);
         c->act_host.swap(h);
         if (newly > 0) {
-            c->Z0 = compute_z0(c, c->L, false);
-            rebuild_phi(c);
+            rebuild_phi(c);   // the merged walk also leaves Z(y) of the new tree in zrow
+            const double z0 = device_max(c, c->zrow.p, c->Ml);
+            if (!(z0 > 0.0)) throw NumericError("Z0: no ray intersects the active set");
+            c->Z0 = z0;
             c->active = count_active(c);
         }
     }
