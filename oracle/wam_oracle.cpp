@@ -515,10 +515,29 @@ static inline bool is_active(const orc_problem* p, int l, int bi, int bj) {
     return p->act[l][(std::size_t)bi * (p->g.nx >> l) + bj] != 0;
 }
 
-// Z(y) = sum_{z in Zs} |phi(y|z)|, Eq. (1.61).  Order: per level running sums in
-// ray order; Z = totA + tot_L + ... + tot_1 (mirrored by the GPU kernel).
+// Z(y) = sum_{z in Zs} |phi(y|z)|, Eq. (1.61).
+//   mirror = 0: f64, per level running sums in ray order;
+//               Z = totA + tot_L + ... + tot_1.
+//   mirror = 1 (== the GPU, pin P8): int64 multiples of 2^-32 with every term
+//               rounded UP, Z = F(totA) + sum over active detail blocks of
+//               F(|phi_H|) + F(|phi_V|) + F(|phi_D|), F(x) = ceil(x 2^32).  Exact
+//               integer sums are order-independent, so the GPU keeps Z(y)
+//               incrementally across expansions; rounding up keeps Z >= the
+//               true sum (the majorization Eq. 1.61 needs), at most 2^-32 per
+//               term above it.
+static inline long long zfix_up(double x) { return (long long)std::ceil(x * 4294967296.0); }
 static double z_row(const orc_problem* p, uint64_t y) {
     const int L = p->L;
+    if (p->mirror) {
+        double totA = 0.0;
+        long long zf = 0;
+        phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {
+            if (l == L) totA += std::fabs(pA);
+            if (l >= 1 && is_active(p, l, bi, bj))
+                zf += zfix_up(std::fabs(pH)) + zfix_up(std::fabs(pV)) + zfix_up(std::fabs(pD));
+        });
+        return (double)(zfix_up(totA) + zf) * (1.0 / 4294967296.0);
+    }
     double totA = 0.0, tot[24];
     for (int l = 0; l <= L; ++l) tot[l] = 0.0;
     phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {

@@ -726,60 +726,79 @@ __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsi
     }
 }
 
-// Expansion walk, one WARP PER LEVEL (blockDim = 32 L): the L warps of a block
-// share the same 32 rays (thread = ray), whose rows are staged once per
-// 32-entry round in shared memory by all L warps (cp.async).  Because every
-// block's phi comes from its own quadrant sums, levels are
-// independent: warp l tracks only level-l blocks, accumulates quadrant sums
-// only inside ACTIVE blocks (tree bits in shared memory), and on block exit
-// adds |phi| to its per-ray level total (MODE 1) or emits negative fp32 phi
-// (MODE 2).  Per-ray results are combined in the fixed order
-//   Z(y) = zA[y] + tot_L + ... + tot_1
-// (bit-identical to the oracle).  cnt / pos are per (ray, level): index y*L + l-1.
-template <int MODE, int L>
+// Fixed-point Z(y) (pin P8): int64 multiples of 2^-32, every term rounded UP.
+constexpr double kZFix = 4294967296.0, kZFixInv = 1.0 / 4294967296.0;
+__device__ __forceinline__ long long zfix_up(double x) { return __double2ll_ru(x * kZFix); }
+__global__ void k_zfix_init(uint64_t n, const double* __restrict__ zA, long long* __restrict__ zf) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) zf[i] = zfix_up(zA[i]);
+}
+__global__ void k_zfix_to_d(uint64_t n, const long long* __restrict__ zf, double* __restrict__ z) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) z[i] = (double)zf[i] * kZFixInv;
+}
+
+// set the [lo, hi) Phi^- ranges of the columns present in a freshly sorted batch
+// appended at offset off (columns of one batch are new, disjoint from older ones)
+__global__ void k_cols_set(uint64_t n, const unsigned long long* __restrict__ ptr, unsigned long long off,
+                           ulonglong2* __restrict__ col) {
+    const uint64_t z = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (z >= n) return;
+    const unsigned long long lo = ptr[z], hi = ptr[z + 1];
+    if (hi > lo) col[z] = make_ulonglong2(off + lo, off + hi);
+}
+
+// Incremental expansion walk, one WARP PER LEVEL: the warps of a block share
+// the same 32 rays (thread = ray), whose rows are staged once per 32-entry
+// round in shared memory (cp.async).  Only NEWLY active blocks are walked
+// (tree bits of act_new & ~act_old in shared memory): Phi^- columns of blocks
+// that were already active never change, so an expansion emits just the new
+// columns and adds the new blocks' |phi| to Z(y).  Because every block's phi
+// comes from its own quadrant sums, levels are independent:
+// warp w tracks level lv(w) = (lvpack >> 4w) & 15, accumulates quadrant sums
+// only inside new blocks, and on block exit
+//   * adds F(|phi_H|) + F(|phi_V|) + F(|phi_D|) to the ray's fixed-point Z,
+//     F(x) = ceil(x 2^32) (exact int64 sums: order-independent, so the
+//     incremental update is bit-identical to a full recomputation and to the
+//     oracle; rounding up keeps Z0 a majorizer, pin P8);
+//   * appends every negative fp32 phi to a private per-lane ring in shared
+//     memory (no atomics in the hot loop).  The inner loop is warp-uniform;
+//     when any lane's ring could overflow on the next entry, the WARP drains:
+//     warp scan of ring counts, output to the warp's private chunk of the
+//     global triple array (chunks reserved from *cursor, one atomicAdd each);
+//     unused chunk tails get the sentinel key nx*ny (sorted past every column).
+// Output: zout[y] = zin[y] + new terms, and unsorted (z, y, phi) triples.
+// Slots past cap are reserved but not stored (the host retries; a warp's
+// reserved total is deterministic, so the retry fits exactly).
 __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned long long* __restrict__ rp,
                                                     const uint2* __restrict__ A, int nx, int ny, int nlev,
-                                                    const unsigned* __restrict__ tbits, ActOff boff, int tree_words,
-                                                    const double* __restrict__ zA, double* __restrict__ zrow,
-                                                    unsigned long long* __restrict__ cnt,
-                                                    unsigned long long* __restrict__ cursor,
-                                                    unsigned long long cap,
+                                                    unsigned lvpack, const unsigned* __restrict__ tbits, ActOff boff,
+                                                    int tree_words, const long long* __restrict__ zin,
+                                                    long long* __restrict__ zout,
+                                                    unsigned long long* __restrict__ cursor, unsigned long long cap,
                                                     unsigned* __restrict__ keys, uint2* __restrict__ vals) {
-    // MODE 1: Z(y) + per-(ray, level) negative counts.  MODE 2: Z(y) + emission
-    // of every negative phi in the same pass.  Emission has no atomics in the
-    // hot loop: each lane appends (z, phi) to a private ring in shared memory;
-    // the inner loop is warp-uniform, and when any lane's ring could overflow
-    // on the next entry the WARP drains: warp scan of the ring counts, the
-    // warp's output goes to its private chunk of the global array (reserved
-    // from *cursor in chunks, one atomicAdd per chunk), and at the end the
-    // unused chunk tail is filled with the sentinel key nx*ny (sorted past every
-    // column, excluded by k_bounds).  Output: unsorted (z, y, phi) triples.
-    // The signed split sums in exact fixed point (k_split), so the order of rays
-    // inside a column is irrelevant and this one pass replaces count + scan +
-    // emit.  Slots past cap are reserved but not stored (the host retries; the
-    // reserved total is deterministic per warp, so the retry fits).
-    constexpr int kR = MODE == 2 ? 12 : 1;   // ring slots per lane
+    constexpr int kR = 12;              // ring slots per lane
     extern __shared__ unsigned tsm[];   // tree bits (tree_words words)
     __shared__ uint2 buf[32][33];
-    __shared__ unsigned long long s_lo[32], s_len[32];
-    __shared__ double s_tot[L][32];
-    __shared__ uint2 ring[kR][32 * 5];   // slot-major: lanes' k-th slots are adjacent
-    // warp w tracks level L - w; levels below L - nlev + 1 hold no active block
-    // (tree closure), so their warps are not launched at all
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, l = L - w;
+    __shared__ unsigned long long s_lo[32];
+    __shared__ int s_len[32];
+    __shared__ long long s_zf[5][32];
+    __shared__ uint2 ring[kR][32 * 5];  // slot-major: the lanes' k-th slots are adjacent
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int l = (int)((lvpack >> (4 * w)) & 15u);
     for (int i = threadIdx.x; i < tree_words; i += blockDim.x) tsm[i] = tbits[i];
     const uint64_t y = (uint64_t)blockIdx.x * 32 + lane;
     if (w == 0) {
         uint64_t lo = 0, hi = 0;
         if (y < M) { lo = rp[y]; hi = rp[y + 1]; }
         s_lo[lane] = lo;
-        s_len[lane] = hi - lo;
+        s_len[lane] = (int)(hi - lo);
     }
     __syncthreads();
-    unsigned long long maxlen = s_len[lane];
+    const int len = s_len[lane];
+    int maxlen = len;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
-    const unsigned long long len = s_len[lane];
     const bool pow2 = (nx & (nx - 1)) == 0;
     const int lgx = 31 - __clz(nx);
     const int wl = nx >> l, hl = ny >> l;
@@ -792,12 +811,11 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
     // each quadrant in one contiguous sub-run: one running accumulator qa for
     // the current quadrant cq, parked into q0..q3 when the quadrant changes
     // (the same sequential ray-order sums as four accumulators).
-    double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, qa = 0.0, tot = 0.0;
-    unsigned long long count = 0;
-    int rc = 0;                              // ring fill (MODE 2)
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, qa = 0.0;
+    long long zf = 0;
+    int rc = 0;                              // ring fill
     unsigned long long cb = 0, ce = 0;       // the warp's current output chunk [cb, ce)
     const unsigned long long chunk = (unsigned long long)max(32, 512 >> l);
-    (void)nlev;
 
     auto park = [&]() {
         q0 = cq == 0 ? qa : q0;
@@ -810,16 +828,12 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
             park();
             const double st = q0 + q1, sb = q2 + q3;
             const double pH = (st - sb) * sc, pV = ((q0 + q2) - (q1 + q3)) * sc, pD = ((q0 + q3) - (q1 + q2)) * sc;
-            tot += fabs(pH) + fabs(pV) + fabs(pD);
+            zf += zfix_up(fabs(pH)) + zfix_up(fabs(pV)) + zfix_up(fabs(pD));
             const float vH = (float)pH, vV = (float)pV, vD = (float)pD;
-            if constexpr (MODE == 1) {
-                count += (vH < 0.0f) + (vV < 0.0f) + (vD < 0.0f);
-            } else {
-                if (vH < 0.0f) ring[rc++][threadIdx.x] = make_uint2((unsigned)((hl + cbi) * nx + cbj), __float_as_uint(vH));
-                if (vV < 0.0f) ring[rc++][threadIdx.x] = make_uint2((unsigned)(cbi * nx + wl + cbj), __float_as_uint(vV));
-                if (vD < 0.0f)
-                    ring[rc++][threadIdx.x] = make_uint2((unsigned)((hl + cbi) * nx + wl + cbj), __float_as_uint(vD));
-            }
+            if (vH < 0.0f) ring[rc++][threadIdx.x] = make_uint2((unsigned)((hl + cbi) * nx + cbj), __float_as_uint(vH));
+            if (vV < 0.0f) ring[rc++][threadIdx.x] = make_uint2((unsigned)(cbi * nx + wl + cbj), __float_as_uint(vV));
+            if (vD < 0.0f)
+                ring[rc++][threadIdx.x] = make_uint2((unsigned)((hl + cbi) * nx + wl + cbj), __float_as_uint(vD));
             q0 = q1 = q2 = q3 = 0.0;
         }
         cq = -1;
@@ -855,20 +869,19 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
         rc = 0;
     };
 
-    for (unsigned long long base = 0; base < maxlen; base += 32) {
-        // all L warps stage the 32 rays' entries [base, base+32)
+    for (int base = 0; base < maxlen; base += 32) {
+        // all warps stage the 32 rays' entries [base, base+32)
         for (int j = w; j < 32; j += nlev) {
-            const unsigned long long nj = s_len[j];
+            const int nj = s_len[j];
             const bool ok = base + lane < nj;
-            cp_async8(&buf[j][lane], A + (ok ? s_lo[j] + base + lane : 0), ok);
+            cp_async8(&buf[j][lane], A + (ok ? s_lo[j] + (unsigned)(base + lane) : 0ull), ok);
         }
         cp_async_wait_all();
         __syncthreads();
-        const int n = (int)min(32ull, len > base ? len - base : 0ull);
-        // MODE 2 keeps the warp converged (uniform trip count) for the drains
-        const int nit = MODE == 2 ? (int)min(32ull, maxlen - base) : n;
+        const int n = min(32, len - base);      // may be <= 0
+        const int nit = min(32, maxlen - base);  // warp-uniform trip count (drains need convergence)
         for (int i = 0; i < nit; ++i) {
-            if (MODE == 1 || i < n) {
+            if (i < n) {
                 const uint2 e = buf[lane][i];
                 int ix, iy;
                 if (pow2) { ix = (int)(e.x & (unsigned)(nx - 1)); iy = (int)(e.x >> lgx); }
@@ -891,31 +904,21 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
                     qa += hval(e);
                 }
             }
-            if constexpr (MODE == 2)
-                if (__any_sync(0xffffffffu, rc > kR - 3)) wdrain();
+            if (__any_sync(0xffffffffu, rc > kR - 3)) wdrain();
         }
         __syncthreads();
     }
     flush();
-    if constexpr (MODE == 2) {
-        wdrain();
-        const unsigned sent = (unsigned)(nx * ny);
-        for (unsigned long long p = cb + lane; p < ce; p += 32)
-            if (p < cap) { keys[p] = sent; vals[p] = make_uint2(0u, 0u); }
-    }
-    {
-        s_tot[l - 1][lane] = tot;
-        if (MODE == 1 && y < M) cnt[y * L + (l - 1)] = count;
-        __syncthreads();
-        if (w == 0 && y < M) {
-            double z = zA[y];
-#pragma unroll
-            for (int k = L; k >= 1; --k)
-                if (k > L - nlev) z += s_tot[k - 1][lane];
-            zrow[y] = z;
-            if (MODE == 1)
-                for (int k = 1; k <= L - nlev; ++k) cnt[y * L + (k - 1)] = 0;
-        }
+    wdrain();
+    const unsigned sent = (unsigned)(nx * ny);
+    for (unsigned long long p = cb + lane; p < ce; p += 32)
+        if (p < cap) { keys[p] = sent; vals[p] = make_uint2(0u, 0u); }
+    s_zf[w][lane] = zf;
+    __syncthreads();
+    if (w == 0 && y < M) {
+        long long z = zin[y];
+        for (int k = 0; k < nlev; ++k) z += s_zf[k][lane];
+        zout[y] = z;
     }
 }
 
@@ -933,14 +936,15 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
     return v;
 }
 __global__ void __launch_bounds__(256) k_split(uint64_t nlist, const unsigned* __restrict__ list,
-                                               const unsigned long long* __restrict__ ptr,
+                                               const ulonglong2* __restrict__ col,
                                                const uint2* __restrict__ E, const float* __restrict__ q,
                                                double* __restrict__ bm) {
     const int lane = threadIdx.x & 31;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlist; i += W) {
         const unsigned z = list[i];
-        const uint64_t lo = ptr[z], hi = ptr[z + 1];
+        const ulonglong2 cr = col[z];
+        const uint64_t lo = cr.x, hi = cr.y;
         long long a0 = 0, a1 = 0;
         uint64_t k = lo + lane;
         for (; k + 32 < hi; k += 64) {

@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256, 4) k_back3(uint64_t N, int nz, const unsi
 // exact 2^-20 fixed-point accumulation per slice (order-independent, as k_split).
 template <int SPL>
 __global__ void __launch_bounds__(256, 4) k_split3(uint64_t nlist, int nz, const unsigned* __restrict__ list,
-                                                const unsigned long long* __restrict__ ptr,
+                                                const ulonglong2* __restrict__ col,
                                                 const uint2* __restrict__ E, const float* __restrict__ q,
                                                 double* __restrict__ bm) {
     using V = typename SlabVec<SPL>::T;
@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(256, 4) k_split3(uint64_t nlist, int nz, const
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlist; i += W) {
         const unsigned z = list[i];
-        const uint64_t lo = ptr[z], hi = ptr[z + 1];
+        const ulonglong2 cr = col[z];
+        const uint64_t lo = cr.x, hi = cr.y;
         long long acc[SPL];
 #pragma unroll
         for (int j = 0; j < SPL; ++j) acc[j] = 0;

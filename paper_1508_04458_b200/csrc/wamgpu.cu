@@ -99,7 +99,11 @@ struct wamgpu_ctx {
     DBuf<float> mu, beta, fscratch;
     DBuf<double> g, bdata, bam, mu64, bp_dbg, bm_dbg, zrow, dscratch;
     DBuf<unsigned long long> wcnt;      // per-(ray, level) Phi^- counts (MODE 1 walk; z-row diagnostics)
-    DBuf<unsigned long long> cursor;    // Phi^- emission cursor of the merged walk
+    DBuf<unsigned long long> cursor;    // Phi^- emission cursor of the expansion walk
+    DBuf<long long> zfix, zfix2;        // 2D tree: per-ray Z(y) in 2^-32 fixed point (pin P8)
+    DBuf<ulonglong2> cols;              // 2D tree: Phi^- range [lo, hi) of column z inside E
+    DBuf<unsigned long long> ptmp;      // column bounds of one sorted batch
+    std::vector<uint8_t> act_phi;       // tree that Phi^- / zfix currently cover
     DBuf<double> zA;                    // per-ray approximation part of Z (tree-independent)
     DBuf<uint8_t> cub_tmp;
     DBuf<unsigned> kin_s, kout_s;
@@ -125,7 +129,7 @@ struct wamgpu_ctx {
     DBuf<unsigned long long> np;
     DBuf<uint2> E;
     DBuf<unsigned> list;
-    uint64_t nlist = 0, nnz_phi = 0;
+    uint64_t nlist = 0, nnz_phi = 0, phi_batch = 0;
     double Z0 = 0.0;
     DBuf<double> scal, partial;
     int nblk_row = 1, nblk_col = 1;
@@ -530,15 +534,15 @@ static void launch_walk(Ctx* c, int L, unsigned long long* cnt, const unsigned l
 }
 
 
-static void upload_tree_bits(Ctx* c) {
-    // host act_host -> bit-packed, levels at 32-bit aligned bit offsets
+static void upload_tree_bits(Ctx* c, const std::vector<uint8_t>& src) {
+    // host tree bytes -> bit-packed, levels at 32-bit aligned bit offsets
     std::vector<unsigned> w;
     uint64_t bit = 0;
     for (int l = 0; l <= LMAX + 1; ++l) c->boff.off[l] = 0;
     for (int l = 1; l <= c->L; ++l) {
         c->boff.off[l] = bit;
         const uint64_t n = (uint64_t)(c->nx >> l) * (c->ny >> l);
-        const uint8_t* a = c->act_host.data() + c->off.off[l];
+        const uint8_t* a = src.data() + c->off.off[l];
         w.resize((bit + n + 31) / 32 + 1, 0u);
         for (uint64_t i = 0; i < n; ++i)
             if (a[i]) w[(bit + i) >> 5] |= 1u << ((bit + i) & 31);
@@ -550,36 +554,17 @@ static void upload_tree_bits(Ctx* c) {
     CK(cudaMemcpyAsync(c->tbits.p, w.data(), w.size() * 4, cudaMemcpyHostToDevice, c->st));
 }
 
-template <int MODE>
-static void launch_walk_lv(Ctx* c, unsigned long long* cnt, unsigned long long* cursor, unsigned long long cap,
-                           unsigned* keys, uint2* vals) {
+// incremental expansion walk over the new-block bits in tbits: levels in
+// lvpack (4 bits each, nlev warps), zfix -> zfix2, triples -> kin_s / vin_s
+static void launch_walk_lv(Ctx* c, int nlev, unsigned lvpack, unsigned long long cap) {
     const unsigned nb = blocks_for(c->Ml, 32);
     const size_t smem = (size_t)c->tree_words * 4;
-    // levels that hold active blocks: L down to the finest active level
-    int nlev = 0;
-    for (int l = c->L; l >= 1; --l) {
-        const uint64_t n = (uint64_t)(c->nx >> l) * (c->ny >> l);
-        const uint8_t* a = c->act_host.data() + c->off.off[l];
-        bool any = false;
-        for (uint64_t i = 0; i < n && !any; ++i) any = a[i] != 0;
-        if (!any) break;
-        ++nlev;
-    }
-    if (nlev == 0) nlev = 1;
-    if (smem > 160 * 1024) throw ConfigError("tree too large for the shared-memory walk");
-#define LV_CASE(LV)                                                                                              \
-    case LV: {                                                                                                   \
-        auto kf = k_walk_lv<MODE, LV>;                                                                           \
-        /* static smem (10-35 KB) + the bit-packed tree may exceed the 48 KB default */                         \
-        if (smem > 12 * 1024) CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        kf<<<nb, 32 * nlev, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, nlev, c->tbits.p, c->boff,      \
-                                           c->tree_words, c->zA.p, c->zrow.p, cnt, cursor, cap, keys, vals);       \
-    } break;
-    switch (c->L) {
-        LV_CASE(1) LV_CASE(2) LV_CASE(3) LV_CASE(4) LV_CASE(5)
-        default: throw ConfigError("haar: depth beyond the device walk");
-    }
-#undef LV_CASE
+    if (smem > 192 * 1024) throw ConfigError("tree too large for the shared-memory walk");
+    // ~26 KB static shared memory + the bit-packed tree may exceed the 48 KB default
+    if (smem > 12 * 1024) CK(cudaFuncSetAttribute(k_walk_lv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_walk_lv<<<nb, 32 * nlev, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, nlev, lvpack, c->tbits.p, c->boff,
+                                             c->tree_words, c->zfix.p, c->zfix2.p, c->cursor.p, cap, c->kin_s.p,
+                                             c->vin_s.p);
     check_launch(c, "k_walk_lv");
 }
 
@@ -702,8 +687,7 @@ static double compute_z0(Ctx* c, int levels, bool init) {
         c->walk_nlev = nlev;
         launch_walk3h<1>(c, nlev, c->wcnt.p, nullptr);
     } else if (c->Ml) {
-        upload_tree_bits(c);
-        launch_walk_lv<1>(c, c->wcnt.p, nullptr, 0, nullptr, nullptr);
+        throw std::logic_error("compute_z0: the 2D tree keeps Z(y) incrementally (zfix)");
     }
     double z0 = device_max(c, c->zrow.p, c->Ml);
     if (!(z0 > 0.0)) throw NumericError("Z0: no ray intersects the active set");
@@ -926,59 +910,109 @@ static void tile_launch(Ctx* c, int mode, double* mu64, double* out) {
     check_launch(c, "k_tile3");
 }
 
-static void rebuild_phi(Ctx* c) {
-    // active detail list from the host tree (ascending Mallat index)
+// Z0 = max_y Z(y) from the fixed-point rows (zrow receives the doubles)
+static void z0_from_zfix(Ctx* c) {
+    if (c->Ml) {
+        k_zfix_to_d<<<blocks_for(c->Ml, 256), 256, 0, c->st>>>(c->Ml, c->zfix.p, c->zrow.p);
+        check_launch(c, "k_zfix_to_d");
+    }
+    const double z0 = device_max(c, c->zrow.p, c->Ml);
+    if (!(z0 > 0.0)) throw NumericError("Z0: no ray intersects the active set");
+    c->Z0 = z0;
+}
+
+// Bring Phi^- (CSC over local rays, active details) and Z(y) up to the current
+// tree act_host from the tree act_phi they cover.  Columns of blocks that were
+// already active never change: one walk over the NEW blocks (k_walk_lv) emits
+// their negative phi as unsorted triples and adds their |phi| terms to the
+// fixed-point Z; the batch is radix-sorted by z straight into E after the
+// existing entries, and k_cols_set records each new column's [lo, hi).  Within
+// a column the ray order is arbitrary: the split sums in exact fixed point.
+static void phi_append(Ctx* c) {
+    // active detail list from the host tree (ascending Mallat index), new bits
     std::vector<unsigned> lst;
+    std::vector<uint8_t> nw(c->act_bytes, 0);
+    bool lv_new[LMAX + 2] = {};
     for (int l = 1; l <= c->L; ++l) {
         const int wl = c->nx >> l, hl = c->ny >> l;
-        const uint8_t* a = c->act_host.data() + c->off.off[l];
+        const uint64_t o = c->off.off[l];
+        const uint8_t* a = c->act_host.data() + o;
         for (int bi = 0; bi < hl; ++bi)
-            for (int bj = 0; bj < wl; ++bj)
-                if (a[(uint64_t)bi * wl + bj]) {
-                    lst.push_back((unsigned)((hl + bi) * c->nx + bj));
-                    lst.push_back((unsigned)(bi * c->nx + wl + bj));
-                    lst.push_back((unsigned)((hl + bi) * c->nx + wl + bj));
-                }
+            for (int bj = 0; bj < wl; ++bj) {
+                const uint64_t i = (uint64_t)bi * wl + bj;
+                if (!a[i]) continue;
+                lst.push_back((unsigned)((hl + bi) * c->nx + bj));
+                lst.push_back((unsigned)(bi * c->nx + wl + bj));
+                lst.push_back((unsigned)((hl + bi) * c->nx + wl + bj));
+                if (!c->act_phi[o + i]) { nw[o + i] = 1; lv_new[l] = true; }
+            }
     }
     std::sort(lst.begin(), lst.end());
     c->nlist = lst.size();
     c->list.ensure(std::max<size_t>(lst.size(), 1));
     if (!lst.empty())
         CK(cudaMemcpyAsync(c->list.p, lst.data(), lst.size() * 4, cudaMemcpyHostToDevice, c->st));
-    // Phi^- CSC over local rays in ONE walk (k_walk_lv MODE 2, which also yields
-    // Z(y) for this tree): unsorted (z, y, phi) triples through a device cursor,
-    // retried once with the exact size if the capacity guess was short, then a
-    // radix sort by z.  Within a column the ray order is arbitrary; the split
-    // is exact fixed point, so it does not matter.
-    unsigned long long tot = 0;
-    if (!lst.empty()) {
-        upload_tree_bits(c);
-        c->cursor.ensure(1);
-        // capacity guess: the active set grows several-fold per expansion and the
-        // final Phi^- holds ~nnz(H)/2 entries (cfg2: 209 M of 450 M), so start at
-        // nnz/2 -- a short guess costs a second walk
-        uint64_t cap = std::max<uint64_t>({c->kin_s.n, 4 * c->nnz_phi, c->nnz / 2, (uint64_t)1 << 20});
-        for (int attempt = 0;; ++attempt) {
-            c->kin_s.ensure(cap);
-            c->vin_s.ensure(cap);
-            CK(cudaMemsetAsync(c->cursor.p, 0, 8, c->st));
-            launch_walk_lv<2>(c, nullptr, c->cursor.p, c->kin_s.n, c->kin_s.p, c->vin_s.p);
-            CK(cudaMemcpyAsync(&tot, c->cursor.p, 8, cudaMemcpyDeviceToHost, c->st));
-            CK(cudaStreamSynchronize(c->st));
-            if (tot <= c->kin_s.n) break;
-            if (attempt) throw NumericError("phi-: emission count changed between walks");
-            cap = tot + tot / 4;
-        }
+    int nlev = 0;
+    unsigned lvpack = 0;
+    for (int l = c->L; l >= 1; --l)
+        if (lv_new[l]) { lvpack |= (unsigned)l << (4 * nlev); ++nlev; }
+    if (nlev == 0 || c->Ml == 0) {
+        c->act_phi = c->act_host;
+        if (nlev) z0_from_zfix(c);   // collective: every rank takes part
+        CK(cudaStreamSynchronize(c->st));
+        return;
     }
-    sort_pairs(c, c->kin_s, c->vin_s, c->kout_s, c->E, tot, c->N);
-    c->np.ensure(c->N + 1);
-    k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(c->kout_s.p, tot, c->N, c->np.p);
+    upload_tree_bits(c, nw);
+    c->cursor.ensure(1);
+    c->zfix2.ensure(c->Ml + 1);
+    // capacity guess for the batch (a short guess costs a second walk)
+    unsigned long long tot = 0;
+    uint64_t cap = std::max<uint64_t>({c->kin_s.n, 2 * c->phi_batch, c->nnz / 4, (uint64_t)1 << 20});
+    for (int attempt = 0;; ++attempt) {
+        c->kin_s.ensure(cap);
+        c->vin_s.ensure(cap);
+        CK(cudaMemsetAsync(c->cursor.p, 0, 8, c->st));
+        launch_walk_lv(c, nlev, lvpack, c->kin_s.n);
+        CK(cudaMemcpyAsync(&tot, c->cursor.p, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        if (tot <= c->kin_s.n) break;
+        if (attempt) throw NumericError("phi-: emission count changed between walks");
+        cap = tot + tot / 8;
+    }
+    c->phi_batch = tot;
+    // append: E keeps the first nnz_phi entries, the sorted batch follows
+    const uint64_t off = c->nnz_phi;
+    if (c->E.n < off + tot + 64) {
+        DBuf<uint2> t;
+        t.alloc(off + tot + (off + tot) / 2 + 64);
+        if (off) CK(cudaMemcpyAsync(t.p, c->E.p, off * sizeof(uint2), cudaMemcpyDeviceToDevice, c->st));
+        c->E.swap(t);
+    }
+    c->kout_s.ensure(std::max<uint64_t>(tot, 1));
+    c->ptmp.ensure(c->N + 1);
+    if (tot) {
+        const int bits = bits_for(c->N);
+        auto vi = reinterpret_cast<unsigned long long*>(c->vin_s.p);
+        auto vo = reinterpret_cast<unsigned long long*>(c->E.p + off);
+        size_t tb = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, c->kin_s.p, c->kout_s.p, vi, vo, (int64_t)tot, 0, bits,
+                                           c->st));
+        c->cub_tmp.ensure(tb + 1);
+        CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tb, c->kin_s.p, c->kout_s.p, vi, vo, (int64_t)tot, 0, bits,
+                                           c->st));
+        launched(c, 4);
+    }
+    k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(c->kout_s.p, tot, c->N, c->ptmp.p);
     check_launch(c, "k_bounds");
-    // chunk tails carry the sentinel key N (sorted last): np[N] counts the rest
+    k_cols_set<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->ptmp.p, off, c->cols.p);
+    check_launch(c, "k_cols_set");
+    // batch tails carry the sentinel key N (sorted last): ptmp[N] counts the rest
     unsigned long long valid = 0;
-    CK(cudaMemcpyAsync(&valid, c->np.p + c->N, 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    c->nnz_phi = valid;
+    CK(cudaMemcpyAsync(&valid, c->ptmp.p + c->N, 8, cudaMemcpyDeviceToHost, c->st));
+    c->zfix.swap(c->zfix2);
+    z0_from_zfix(c);
+    c->nnz_phi = off + valid;
+    c->act_phi = c->act_host;
 }
 
 static int64_t count_active(const Ctx* c) {
@@ -1042,7 +1076,19 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     c->nlist = 0;
     c->nlist3 = 0;
     c->nnz_phi = 0;
-    if (!c->haar3) rebuild_phi(c);       // 3D: the tree is empty, no Psi lists yet
+    c->phi_batch = 0;
+    if (!c->haar3) {                     // 3D: the tree is empty, no Psi lists yet
+        // empty tree: Z(y) = F(zA(y)) in fixed point, Phi^- empty
+        c->zfix.ensure(c->Ml + 1);
+        if (c->Ml) {
+            k_zfix_init<<<blocks_for(c->Ml, 256), 256, 0, c->st>>>(c->Ml, c->zA.p, c->zfix.p);
+            check_launch(c, "k_zfix_init");
+        }
+        z0_from_zfix(c);
+        c->cols.ensure(c->N);
+        CK(cudaMemsetAsync(c->cols.p, 0, c->N * sizeof(ulonglong2), c->st));
+        c->act_phi.assign(c->act_bytes, 0);
+    }
     tile_launch(c, 0, nullptr, nullptr);  // mu = Omega beta
     forward_fused(c, false);
     CK(cudaMemsetAsync(c->counters.p, 0, 16, c->st));
@@ -1070,10 +1116,10 @@ static void wam_step(Ctx* c) {
         c->timer_begin(T_SPLIT);
         const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist + 7) / 8, (uint64_t)c->sms * 16);
         if (c->nzl == 1) {
-            k_split<<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->np.p, c->E.p, c->q.p, c->g.p + c->N);
+            k_split<<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
         } else {
             double* bm3 = c->g.p + NV(c);
-#define S3(S) k_split3<S><<<nb, 256, 0, c->st>>>(c->nlist, c->nzl, c->list.p, c->np.p, c->E.p, c->q.p, bm3);
+#define S3(S) k_split3<S><<<nb, 256, 0, c->st>>>(c->nlist, c->nzl, c->list.p, c->cols.p, c->E.p, c->q.p, bm3);
             switch (spl_of(c)) { case 1: S3(1) break; case 2: S3(2) break; default: S3(4) break; }
 #undef S3
         }
@@ -1161,10 +1207,7 @@ static int64_t wam_expand(Ctx* c, double factor) {
         for (uint64_t i = 0; i < c->act_bytes; ++i) newly += (h[i] != 0) - (c->act_host[i] != 0);
         c->act_host.swap(h);
         if (newly > 0) {
-            rebuild_phi(c);   // the merged walk also leaves Z(y) of the new tree in zrow
-            const double z0 = device_max(c, c->zrow.p, c->Ml);
-            if (!(z0 > 0.0)) throw NumericError("Z0: no ray intersects the active set");
-            c->Z0 = z0;
+            phi_append(c);    // new columns of Phi^-, Z(y) and Z0 of the grown tree
             c->active = count_active(c);
         }
     }
@@ -1549,7 +1592,16 @@ int wamgpu_get_z_rows(wamgpu_ctx* ctx, double* zrow) {
         NEED(ctx); NEED(zrow);
         Ctx* c = ctx;
         need_matrix(c);
-        if (c->algo == 2 && c->L > 0) compute_z0(c, c->L, false); else compute_z0(c, c->algo == 2 ? c->L : 0, true);
+        if (c->algo == 2 && !c->haar3) {
+            if (c->Ml) {
+                k_zfix_to_d<<<blocks_for(c->Ml, 256), 256, 0, c->st>>>(c->Ml, c->zfix.p, c->zrow.p);
+                check_launch(c, "k_zfix_to_d");
+            }
+        } else if (c->algo == 2 && c->L > 0) {
+            compute_z0(c, c->L, false);
+        } else {
+            compute_z0(c, c->algo == 2 ? c->L : 0, true);
+        }
         CK(cudaMemcpyAsync(zrow, c->zrow.p, c->Ml * 8, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
     })
