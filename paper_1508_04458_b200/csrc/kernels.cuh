@@ -770,33 +770,60 @@ __global__ void k_cols_set(uint64_t n, const unsigned long long* __restrict__ pt
 // Output: zout[y] = zin[y] + new terms, and unsorted (z, y, phi) triples.
 // Slots past cap are reserved but not stored (the host retries; a warp's
 // reserved total is deterministic, so the retry fits exactly).
-__global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned long long* __restrict__ rp,
-                                                    const uint2* __restrict__ A, int nx, int ny, int nlev,
+// Dynamic shared-memory layout of k_walk_lv for G ray groups x nlev level warps
+// (host and device agree on it through walk_smem).
+constexpr int WLV_D = 16;   // entries per ray staged per round
+constexpr int WLV_R = 8;    // ring slots per lane
+struct WalkSmem {
+    size_t buf, lo, len, zf, ring, tree, total;
+};
+__host__ __device__ inline WalkSmem walk_smem(int G, int nlev, int tree_words) {
+    WalkSmem m;
+    const size_t T = (size_t)32 * G * nlev;
+    m.buf = 0;                                                   // uint2 [G*32][D+1]
+    m.lo = m.buf + (size_t)G * 32 * (WLV_D + 1) * 8;             // u64   [G*32]
+    m.len = m.lo + (size_t)G * 32 * 8;                           // int   [G*32]
+    m.zf = (m.len + (size_t)G * 32 * 4 + 7) & ~(size_t)7;        // i64   [T]
+    m.ring = m.zf + T * 8;                                       // uint2 [R][T]
+    m.tree = m.ring + (size_t)WLV_R * T * 8;                     // u32   [tree_words]
+    m.total = m.tree + (size_t)tree_words * 4;
+    return m;
+}
+
+__global__ void __launch_bounds__(32 * 8) k_walk_lv(uint64_t M, const unsigned long long* __restrict__ rp,
+                                                    const uint2* __restrict__ A, int nx, int ny, int nlev, int G,
                                                     unsigned lvpack, const unsigned* __restrict__ tbits, ActOff boff,
                                                     int tree_words, const long long* __restrict__ zin,
                                                     long long* __restrict__ zout,
                                                     unsigned long long* __restrict__ cursor, unsigned long long cap,
                                                     unsigned* __restrict__ keys, uint2* __restrict__ vals) {
-    constexpr int kR = 12;              // ring slots per lane
-    extern __shared__ unsigned tsm[];   // tree bits (tree_words words)
-    __shared__ uint2 buf[32][33];
-    __shared__ unsigned long long s_lo[32];
-    __shared__ int s_len[32];
-    __shared__ long long s_zf[5][32];
-    __shared__ uint2 ring[kR][32 * 5];  // slot-major: the lanes' k-th slots are adjacent
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int l = (int)((lvpack >> (4 * w)) & 15u);
-    for (int i = threadIdx.x; i < tree_words; i += blockDim.x) tsm[i] = tbits[i];
-    const uint64_t y = (uint64_t)blockIdx.x * 32 + lane;
-    if (w == 0) {
+    constexpr int kR = WLV_R, D = WLV_D;
+    extern __shared__ __align__(16) unsigned char wsm[];
+    const WalkSmem L_ = walk_smem(G, nlev, tree_words);
+    uint2 (*buf)[D + 1] = reinterpret_cast<uint2 (*)[D + 1]>(wsm + L_.buf);
+    unsigned long long* s_lo = reinterpret_cast<unsigned long long*>(wsm + L_.lo);
+    int* s_len = reinterpret_cast<int*>(wsm + L_.len);
+    long long* s_zf = reinterpret_cast<long long*>(wsm + L_.zf);
+    uint2* ring = reinterpret_cast<uint2*>(wsm + L_.ring);   // [kR][blockDim]: lanes' k-th slots adjacent
+    unsigned* tsm = reinterpret_cast<unsigned*>(wsm + L_.tree);
+    const int TB = blockDim.x;   // (T inside wdrain is the warp total)
+    // warp w: ray group g = w / nlev, level l = lvpack nibble (w % nlev)
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = w / nlev, lvi = w - g * nlev;
+    const int l = (int)((lvpack >> (4 * lvi)) & 15u);
+    for (int i = threadIdx.x; i < tree_words; i += TB) tsm[i] = tbits[i];
+    const int nrays = 32 * G;
+    const uint64_t y0 = (uint64_t)blockIdx.x * nrays;
+    const uint64_t y = y0 + (uint64_t)g * 32 + lane;
+    for (int r = threadIdx.x; r < nrays; r += TB) {
         uint64_t lo = 0, hi = 0;
-        if (y < M) { lo = rp[y]; hi = rp[y + 1]; }
-        s_lo[lane] = lo;
-        s_len[lane] = (int)(hi - lo);
+        if (y0 + r < M) { lo = rp[y0 + r]; hi = rp[y0 + r + 1]; }
+        s_lo[r] = lo;
+        s_len[r] = (int)(hi - lo);
     }
     __syncthreads();
-    const int len = s_len[lane];
-    int maxlen = len;
+    const int len = s_len[g * 32 + lane];
+    int maxlen = 0;   // CTA-uniform round count (barriers inside the loop)
+    for (int r = lane; r < nrays; r += 32) maxlen = max(maxlen, s_len[r]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
     const bool pow2 = (nx & (nx - 1)) == 0;
@@ -830,10 +857,10 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
             const double pH = (st - sb) * sc, pV = ((q0 + q2) - (q1 + q3)) * sc, pD = ((q0 + q3) - (q1 + q2)) * sc;
             zf += zfix_up(fabs(pH)) + zfix_up(fabs(pV)) + zfix_up(fabs(pD));
             const float vH = (float)pH, vV = (float)pV, vD = (float)pD;
-            if (vH < 0.0f) ring[rc++][threadIdx.x] = make_uint2((unsigned)((hl + cbi) * nx + cbj), __float_as_uint(vH));
-            if (vV < 0.0f) ring[rc++][threadIdx.x] = make_uint2((unsigned)(cbi * nx + wl + cbj), __float_as_uint(vV));
+            if (vH < 0.0f) ring[(rc++) * TB + threadIdx.x] = make_uint2((unsigned)((hl + cbi) * nx + cbj), __float_as_uint(vH));
+            if (vV < 0.0f) ring[(rc++) * TB + threadIdx.x] = make_uint2((unsigned)(cbi * nx + wl + cbj), __float_as_uint(vV));
             if (vD < 0.0f)
-                ring[rc++][threadIdx.x] = make_uint2((unsigned)((hl + cbi) * nx + wl + cbj), __float_as_uint(vD));
+                ring[(rc++) * TB + threadIdx.x] = make_uint2((unsigned)((hl + cbi) * nx + wl + cbj), __float_as_uint(vD));
             q0 = q1 = q2 = q3 = 0.0;
         }
         cq = -1;
@@ -861,7 +888,7 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
         for (int k = 0; k < rc; ++k) {
             const unsigned long long j = pre + (unsigned)k;
             const unsigned long long p = j < rem ? cb + j : nb + (j - rem);
-            const uint2 r = ring[k][threadIdx.x];
+            const uint2 r = ring[k * TB + threadIdx.x];
             if (p < cap) { keys[p] = r.x; vals[p] = make_uint2((unsigned)y, r.y); }
         }
         if (T > rem) { cb = nb + (T - rem); ce = nb + need; }
@@ -869,20 +896,24 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
         rc = 0;
     };
 
-    for (int base = 0; base < maxlen; base += 32) {
-        // all warps stage the 32 rays' entries [base, base+32)
-        for (int j = w; j < 32; j += nlev) {
+    const int nw = TB >> 5, half = lane >> 4, sub = lane & 15;
+    for (int base = 0; base < maxlen; base += D) {
+        // all warps stage the CTA's rays' entries [base, base+D): two rows per
+        // warp instruction (half-warps), coalesced 128 B per row
+        for (int j = 2 * w + half; j < nrays; j += 2 * nw) {
             const int nj = s_len[j];
-            const bool ok = base + lane < nj;
-            cp_async8(&buf[j][lane], A + (ok ? s_lo[j] + (unsigned)(base + lane) : 0ull), ok);
+            const bool ok = base + sub < nj;
+            cp_async8(&buf[j][sub], A + (ok ? s_lo[j] + (unsigned)(base + sub) : 0ull), ok);
         }
         cp_async_wait_all();
         __syncthreads();
-        const int n = min(32, len - base);      // may be <= 0
-        const int nit = min(32, maxlen - base);  // warp-uniform trip count (drains need convergence)
+        const int n = min(D, len - base);       // may be <= 0
+        int nit = min(D, max(0, len - base));   // warp-uniform trip count (drains need convergence)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nit = max(nit, __shfl_xor_sync(0xffffffffu, nit, o));
         for (int i = 0; i < nit; ++i) {
             if (i < n) {
-                const uint2 e = buf[lane][i];
+                const uint2 e = buf[g * 32 + lane][i];
                 int ix, iy;
                 if (pow2) { ix = (int)(e.x & (unsigned)(nx - 1)); iy = (int)(e.x >> lgx); }
                 else { iy = (int)(e.x / (unsigned)nx); ix = (int)(e.x % (unsigned)nx); }
@@ -913,11 +944,11 @@ __global__ void __launch_bounds__(32 * 5) k_walk_lv(uint64_t M, const unsigned l
     const unsigned sent = (unsigned)(nx * ny);
     for (unsigned long long p = cb + lane; p < ce; p += 32)
         if (p < cap) { keys[p] = sent; vals[p] = make_uint2(0u, 0u); }
-    s_zf[w][lane] = zf;
+    s_zf[threadIdx.x] = zf;
     __syncthreads();
-    if (w == 0 && y < M) {
+    if (lvi == 0 && y < M) {
         long long z = zin[y];
-        for (int k = 0; k < nlev; ++k) z += s_zf[k][lane];
+        for (int k = 0; k < nlev; ++k) z += s_zf[(g * nlev + k) * 32 + lane];
         zout[y] = z;
     }
 }

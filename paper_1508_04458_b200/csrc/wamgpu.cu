@@ -540,9 +540,12 @@ static void upload_tree_bits(Ctx* c, const std::vector<uint8_t>& src) {
     uint64_t bit = 0;
     for (int l = 0; l <= LMAX + 1; ++l) c->boff.off[l] = 0;
     for (int l = 1; l <= c->L; ++l) {
-        c->boff.off[l] = bit;
         const uint64_t n = (uint64_t)(c->nx >> l) * (c->ny >> l);
         const uint8_t* a = src.data() + c->off.off[l];
+        bool any = false;   // levels without bits are never looked up: not uploaded
+        for (uint64_t i = 0; i < n && !any; ++i) any = a[i] != 0;
+        if (!any) continue;
+        c->boff.off[l] = bit;
         w.resize((bit + n + 31) / 32 + 1, 0u);
         for (uint64_t i = 0; i < n; ++i)
             if (a[i]) w[(bit + i) >> 5] |= 1u << ((bit + i) & 31);
@@ -557,14 +560,15 @@ static void upload_tree_bits(Ctx* c, const std::vector<uint8_t>& src) {
 // incremental expansion walk over the new-block bits in tbits: levels in
 // lvpack (4 bits each, nlev warps), zfix -> zfix2, triples -> kin_s / vin_s
 static void launch_walk_lv(Ctx* c, int nlev, unsigned lvpack, unsigned long long cap) {
-    const unsigned nb = blocks_for(c->Ml, 32);
-    const size_t smem = (size_t)c->tree_words * 4;
-    if (smem > 192 * 1024) throw ConfigError("tree too large for the shared-memory walk");
-    // ~26 KB static shared memory + the bit-packed tree may exceed the 48 KB default
-    if (smem > 12 * 1024) CK(cudaFuncSetAttribute(k_walk_lv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_walk_lv<<<nb, 32 * nlev, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, nlev, lvpack, c->tbits.p, c->boff,
-                                             c->tree_words, c->zfix.p, c->zfix2.p, c->cursor.p, cap, c->kin_s.p,
-                                             c->vin_s.p);
+    // G ray groups of 32 per CTA so that a CTA has ~4 warps whatever nlev is
+    const int G = std::max(1, 4 / nlev);
+    const unsigned nb = blocks_for(c->Ml, 32 * G);
+    const size_t smem = walk_smem(G, nlev, c->tree_words).total;
+    if (smem > 200 * 1024) throw ConfigError("tree too large for the shared-memory walk");
+    CK(cudaFuncSetAttribute(k_walk_lv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_walk_lv<<<nb, 32 * nlev * G, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, nlev, G, lvpack, c->tbits.p,
+                                                 c->boff, c->tree_words, c->zfix.p, c->zfix2.p, c->cursor.p, cap,
+                                                 c->kin_s.p, c->vin_s.p);
     check_launch(c, "k_walk_lv");
 }
 
