@@ -279,6 +279,88 @@ __global__ void __launch_bounds__(256, MINB) k_forward(uint64_t M, const unsigne
     }
 }
 
+// Patch-mapped forward: a warp takes R ADJACENT rays (neighbouring detectors of
+// one view), LPR = 32/R lanes per ray, each lane striding its ray by LPR.  One
+// gather instruction then touches a compact ~LPR x R patch of cells (the rays
+// run side by side) instead of a 32-cell line along one ray, which cuts the L1
+// sectors per gathered entry (the forward's limiter is the L1 data pipe,
+// profiles/) while the A stream stays coalesced (LPR*8 B per ray per load).
+// Software-pipelined like seg_dot; fp64 accumulation; fixed strided partials +
+// xor butterfly inside each LPR-lane group (deterministic).  MODE as k_forward.
+template <int MODE, int R, int UNR, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fwd_patch(uint64_t M, const unsigned long long* __restrict__ rp,
+                                                    const uint2* __restrict__ A, const float* __restrict__ mu,
+                                                    const float* __restrict__ I0, const float* __restrict__ d,
+                                                    float* __restrict__ q, double* __restrict__ lout,
+                                                    double* __restrict__ partial, int* __restrict__ flag) {
+    constexpr int LPR = 32 / R;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, sub = lane % LPR;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t ntask = (M + R - 1) / R;
+    double tacc = 0.0;
+    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; t < ntask; t += W) {
+        const uint64_t y = t * R + lane / LPR;
+        const bool has = y < M;
+        uint64_t lo = 0, hi = 0;
+        if (has) { lo = __ldg(rp + y); hi = __ldg(rp + y + 1); }
+        unsigned maxlen = (unsigned)(hi - lo);
+#pragma unroll
+        for (int o = 16; o >= LPR; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+        double acc0 = 0.0, acc1 = 0.0;
+        uint2 ec[UNR];
+        const uint64_t b0 = lo + sub;
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint64_t k = b0 + LPR * u;
+            ec[u] = k < hi ? ld_stream(A + k) : make_uint2(0u, 0u);
+        }
+        for (unsigned off = 0; off < maxlen; off += LPR * UNR) {
+            uint2 en[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint64_t k = b0 + off + LPR * (UNR + u);
+                en[u] = k < hi ? ld_stream(A + k) : make_uint2(0u, 0u);
+            }
+            float v[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) v[u] = (b0 + off + LPR * u < hi) ? __ldg(mu + ec[u].x) : 0.0f;
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const double h = hval(ec[u]), xv = (double)v[u];
+                if (u & 1) acc1 = fma(h, xv, acc1); else acc0 = fma(h, xv, acc0);
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) ec[u] = en[u];
+        }
+        double lg = acc0 + acc1;
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
+        if (has && sub == 0) {
+            if (!isfinite(lg)) atomicOr(flag, 1);
+            if (MODE == 0) {
+                lout[y] = lg;
+            } else {
+                const double qq = (double)I0[y] * exp(-lg);
+                q[y] = (float)qq;
+                tacc += idiv_term((double)d[y], qq);
+            }
+        }
+    }
+    if (MODE == 1) {
+        __shared__ double s[32];
+        double v = tacc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s[wib] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+            partial[blockIdx.x] = t;
+        }
+    }
+}
+
 // ------------------------------------------------------------- CSC back
 // Warp per voxel: g(x) = sum_y h(y|x) w(y) in fp64 over the voxel's CSC column.
 // MODE 0: write g (fp64).  MODE 1: fused AM update:
@@ -305,6 +387,71 @@ __global__ void __launch_bounds__(256, MINB) k_back(uint64_t N, const unsigned l
                     const double v = (double)mu[mx] + log(c / b) / Z0;
                     if (!isfinite(v)) atomicOr(flag, 2);
                     mu[mx] = (float)((0.0 < v) ? v : 0.0);
+                }
+            }
+        }
+    }
+}
+
+// Patch-mapped back projection (see k_fwd_patch): a warp takes R ADJACENT
+// voxels of an image row, LPR = 32/R lanes per CSC column.  Neighbouring
+// voxels are crossed by nearly the same rays (same views, neighbouring
+// detectors), so one gather of w touches few sectors.  MODE as k_back.
+template <int MODE, int R, int UNR, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_back_patch(uint64_t N, const unsigned long long* __restrict__ cp,
+                                                     const uint2* __restrict__ C, const float* __restrict__ w,
+                                                     double* __restrict__ g, const double* __restrict__ bam,
+                                                     float* __restrict__ mu, double Z0, int* __restrict__ flag) {
+    constexpr int LPR = 32 / R;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, sub = lane % LPR;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t ntask = (N + R - 1) / R;
+    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; t < ntask; t += W) {
+        const uint64_t x = t * R + lane / LPR;
+        const bool has = x < N;
+        uint64_t lo = 0, hi = 0;
+        if (has) { lo = __ldg(cp + x); hi = __ldg(cp + x + 1); }
+        unsigned maxlen = (unsigned)(hi - lo);
+#pragma unroll
+        for (int o = 16; o >= LPR; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+        double acc0 = 0.0, acc1 = 0.0;
+        uint2 ec[UNR];
+        const uint64_t b0 = lo + sub;
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint64_t k = b0 + LPR * u;
+            ec[u] = k < hi ? ld_stream(C + k) : make_uint2(0u, 0u);
+        }
+        for (unsigned off = 0; off < maxlen; off += LPR * UNR) {
+            uint2 en[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint64_t k = b0 + off + LPR * (UNR + u);
+                en[u] = k < hi ? ld_stream(C + k) : make_uint2(0u, 0u);
+            }
+            float v[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) v[u] = (b0 + off + LPR * u < hi) ? __ldg(w + ec[u].x) : 0.0f;
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const double h = hval(ec[u]), xv = (double)v[u];
+                if (u & 1) acc1 = fma(h, xv, acc1); else acc0 = fma(h, xv, acc0);
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) ec[u] = en[u];
+        }
+        double c = acc0 + acc1;
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (has && sub == 0) {
+            if (MODE == 0) {
+                g[x] = c;
+            } else {
+                const double b = bam[x];
+                if (b > 0.0 && c > 0.0) {
+                    const double v = (double)mu[x] + log(c / b) / Z0;
+                    if (!isfinite(v)) atomicOr(flag, 2);
+                    mu[x] = (float)((0.0 < v) ? v : 0.0);
                 }
             }
         }

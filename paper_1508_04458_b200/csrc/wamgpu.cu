@@ -418,6 +418,19 @@ static void back_launch(Ctx* c, const float* w, double* out, const double* bam) 
             case 2: BV(4, 8) break;
             case 4: BV(8, 6) break;
             case 5: BV(8, 1) break;
+#define BP(R, U, MB)                                                                                              \
+    if (c->lgx >= 0) throw ConfigError("patch back projection: row-major mu only");                              \
+    if (bam) k_back_patch<1, R, U, MB><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, nullptr, bam,    \
+                                                                       c->mu.p, c->Z0, c->flag.p);               \
+    else k_back_patch<0, R, U, MB><<<c->nblk_col, 256, 0, c->st>>>(c->N, c->cp.p, c->C.p, w, out, nullptr,        \
+                                                                   nullptr, 0.0, c->flag.p);
+            case 10: BP(4, 8, 5) break;
+            case 11: BP(4, 12, 3) break;
+            case 12: BP(2, 8, 5) break;
+            case 13: BP(4, 8, 4) break;
+            case 14: BP(8, 8, 4) break;
+            case 15: BP(2, 12, 3) break;
+#undef BP
             default: BV(12, 1) break;     // measured best at cfg2 (round 1 sweep, profiles/)
         }
 #undef BV
@@ -479,8 +492,30 @@ static void forward_fused(Ctx* c, bool record) {
             case 6: FV(4, 4, 1) break;
             case 7: FV(1, 8, 6) break;
             case 8: FV(2, 8, 1) break;
-            default: FV(1, 4, 8) break;   // measured best at cfg2 (round 1 sweep, profiles/)
+#define FP(R, U, MB)                                                                                               \
+    k_fwd_patch<1, R, U, MB><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p,      \
+                                                            c->q.p, nullptr, c->partial.p, c->flag.p);
+            case 10: FP(4, 4, 8) break;
+            case 11: FP(4, 8, 4) break;
+            case 12: FP(2, 4, 8) break;
+            case 13: FP(8, 4, 8) break;
+            case 14: FP(4, 6, 6) break;
+            case 15: FP(8, 8, 4) break;
+            case 16: FP(4, 2, 8) break;
+            case 17: FP(4, 12, 3) break;
+            case 18: FP(4, 8, 5) break;
+            case 19: FP(2, 8, 4) break;
+            case 20: FP(4, 16, 2) break;
+            case 21: FP(4, 10, 4) break;
+            case 22: FP(8, 12, 3) break;
+            case 23: FP(4, 8, 6) break;
+            case 24: FP(8, 8, 5) break;
+            case 25: FP(4, 6, 5) break;
+            case 26: FP(2, 8, 5) break;
+            case 9: FV(1, 4, 8) break;    // round-1 default (row-per-warp)
+            default: FP(4, 8, 5) break;   // measured best at cfg2 (patch sweep, profiles/r02_fwd_patch_sweep.txt)
         }
+#undef FP
 #undef FV
     } else {
         const unsigned nb = std::min<unsigned>(nblk_warp(c, c->Ml), (unsigned)c->partial.n);
