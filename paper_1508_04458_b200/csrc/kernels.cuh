@@ -722,6 +722,9 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void add_quad(double (&q)[4], int quad, double v) {
     q[0] += quad == 0 ? v : 0.0;
     q[1] += quad == 1 ? v : 0.0;
@@ -919,16 +922,16 @@ __global__ void k_cols_set(uint64_t n, const unsigned long long* __restrict__ pt
 // reserved total is deterministic, so the retry fits exactly).
 // Dynamic shared-memory layout of k_walk_lv for G ray groups x nlev level warps
 // (host and device agree on it through walk_smem).
-constexpr int WLV_D = 16;   // entries per ray staged per round
 constexpr int WLV_R = 8;    // ring slots per lane
 struct WalkSmem {
     size_t buf, lo, len, zf, ring, tree, total;
 };
-__host__ __device__ inline WalkSmem walk_smem(int G, int nlev, int tree_words) {
+// D entries per ray staged per round, NS staging buffers (2: double-buffered)
+__host__ __device__ inline WalkSmem walk_smem(int G, int nlev, int tree_words, int D, int NS) {
     WalkSmem m;
     const size_t T = (size_t)32 * G * nlev;
-    m.buf = 0;                                                   // uint2 [G*32][D+1]
-    m.lo = m.buf + (size_t)G * 32 * (WLV_D + 1) * 8;             // u64   [G*32]
+    m.buf = 0;                                                   // uint2 [NS][G*32][D+1]
+    m.lo = m.buf + (size_t)NS * G * 32 * (D + 1) * 8;            // u64   [G*32]
     m.len = m.lo + (size_t)G * 32 * 8;                           // int   [G*32]
     m.zf = (m.len + (size_t)G * 32 * 4 + 7) & ~(size_t)7;        // i64   [T]
     m.ring = m.zf + T * 8;                                       // uint2 [R][T]
@@ -937,6 +940,7 @@ __host__ __device__ inline WalkSmem walk_smem(int G, int nlev, int tree_words) {
     return m;
 }
 
+template <int D, int NS>
 __global__ void __launch_bounds__(32 * 8) k_walk_lv(uint64_t M, const unsigned long long* __restrict__ rp,
                                                     const uint2* __restrict__ A, int nx, int ny, int nlev, int G,
                                                     unsigned lvpack, const unsigned* __restrict__ tbits, ActOff boff,
@@ -944,9 +948,9 @@ __global__ void __launch_bounds__(32 * 8) k_walk_lv(uint64_t M, const unsigned l
                                                     long long* __restrict__ zout,
                                                     unsigned long long* __restrict__ cursor, unsigned long long cap,
                                                     unsigned* __restrict__ keys, uint2* __restrict__ vals) {
-    constexpr int kR = WLV_R, D = WLV_D;
+    constexpr int kR = WLV_R;
     extern __shared__ __align__(16) unsigned char wsm[];
-    const WalkSmem L_ = walk_smem(G, nlev, tree_words);
+    const WalkSmem L_ = walk_smem(G, nlev, tree_words, D, NS);
     uint2 (*buf)[D + 1] = reinterpret_cast<uint2 (*)[D + 1]>(wsm + L_.buf);
     unsigned long long* s_lo = reinterpret_cast<unsigned long long*>(wsm + L_.lo);
     int* s_len = reinterpret_cast<int*>(wsm + L_.len);
@@ -1043,24 +1047,40 @@ __global__ void __launch_bounds__(32 * 8) k_walk_lv(uint64_t M, const unsigned l
         rc = 0;
     };
 
-    const int nw = TB >> 5, half = lane >> 4, sub = lane & 15;
-    for (int base = 0; base < maxlen; base += D) {
-        // all warps stage the CTA's rays' entries [base, base+D): two rows per
-        // warp instruction (half-warps), coalesced 128 B per row
-        for (int j = 2 * w + half; j < nrays; j += 2 * nw) {
+    constexpr int RPI = 32 / D;   // rows staged per warp instruction
+    const int nw = TB >> 5, half = lane / D, sub = lane % D;
+    // all warps stage the CTA's rays' entries [base, base+D) into stage st: 32/D
+    // rows per warp instruction, coalesced 8D bytes per row.  Double
+    // buffered: round r+1 is in flight while round r is processed.
+    auto stage = [&](int base, int st) {
+        uint2 (*bs)[D + 1] = buf + st * nrays;
+        for (int j = RPI * w + half; j < nrays; j += RPI * nw) {
             const int nj = s_len[j];
             const bool ok = base + sub < nj;
-            cp_async8(&buf[j][sub], A + (ok ? s_lo[j] + (unsigned)(base + sub) : 0ull), ok);
+            cp_async8(&bs[j][sub], A + (ok ? s_lo[j] + (unsigned)(base + sub) : 0ull), ok);
         }
-        cp_async_wait_all();
+        cp_async_commit();
+    };
+    if (NS == 2 && maxlen > 0) stage(0, 0);
+    for (int base = 0, rnd = 0; base < maxlen; base += D, ++rnd) {
+        if (NS == 1) {
+            stage(base, 0);
+            cp_async_wait<0>();
+        } else if (base + D < maxlen) {
+            stage(base + D, (rnd + 1) & 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
         __syncthreads();
+        uint2 (*bcur)[D + 1] = buf + (NS == 2 ? (rnd & 1) * nrays : 0);
         const int n = min(D, len - base);       // may be <= 0
         int nit = min(D, max(0, len - base));   // warp-uniform trip count (drains need convergence)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nit = max(nit, __shfl_xor_sync(0xffffffffu, nit, o));
         for (int i = 0; i < nit; ++i) {
             if (i < n) {
-                const uint2 e = buf[g * 32 + lane][i];
+                const uint2 e = bcur[g * 32 + lane][i];
                 int ix, iy;
                 if (pow2) { ix = (int)(e.x & (unsigned)(nx - 1)); iy = (int)(e.x >> lgx); }
                 else { iy = (int)(e.x / (unsigned)nx); ix = (int)(e.x % (unsigned)nx); }
@@ -1113,28 +1133,42 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
+template <int UNR>
 __global__ void __launch_bounds__(256) k_split(uint64_t nlist, const unsigned* __restrict__ list,
                                                const ulonglong2* __restrict__ col,
                                                const uint2* __restrict__ E, const float* __restrict__ q,
                                                double* __restrict__ bm) {
+    // warp per column, software-pipelined: the UNR streaming loads of round
+    // r+1 are issued before the q gathers of round r (as seg_dot)
     const int lane = threadIdx.x & 31;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlist; i += W) {
         const unsigned z = list[i];
         const ulonglong2 cr = col[z];
         const uint64_t lo = cr.x, hi = cr.y;
-        long long a0 = 0, a1 = 0;
-        uint64_t k = lo + lane;
-        for (; k + 32 < hi; k += 64) {
-            const uint2 e0 = ld_stream(E + k), e1 = ld_stream(E + k + 32);
-            a0 += fix_term((double)__ldg(q + e0.x), hval(e0));
-            a1 += fix_term((double)__ldg(q + e1.x), hval(e1));
+        long long a = 0;
+        uint2 ec[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint64_t k = lo + lane + 32 * u;
+            ec[u] = k < hi ? ld_stream(E + k) : make_uint2(0u, 0u);
         }
-        for (; k < hi; k += 32) {
-            const uint2 e0 = ld_stream(E + k);
-            a0 += fix_term((double)__ldg(q + e0.x), hval(e0));
+        for (uint64_t base = lo + lane; base < hi; base += 32 * UNR) {
+            uint2 en[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint64_t k = base + 32 * (UNR + u);
+                en[u] = k < hi ? ld_stream(E + k) : make_uint2(0u, 0u);
+            }
+            float v[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) v[u] = (base + 32 * u < hi) ? __ldg(q + ec[u].x) : 0.0f;
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) a += fix_term((double)v[u], hval(ec[u]));
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) ec[u] = en[u];
         }
-        const long long s = warp_sum_ll(a0 + a1);
+        const long long s = warp_sum_ll(a);
         if (lane == 0) bm[z] = (double)s * kFixInv;
     }
 }

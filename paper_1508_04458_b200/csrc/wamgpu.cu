@@ -135,6 +135,9 @@ struct wamgpu_ctx {
     int nblk_row = 1, nblk_col = 1;
     int lgx = -1;   // 2D mu in 8x4 tiles (mu_addr) when >= 0
     int fwd_variant = 0, back_variant = 0;  // SpMV tuning knobs (WAMGPU_FWD_VARIANT / WAMGPU_BACK_VARIANT)
+    int split_variant = 0;                  // WAMGPU_SPLIT_VARIANT
+    int walk_variant = 0;                   // WAMGPU_WALK_VARIANT
+    double t_trace = 0.0;                   // WAMGPU_TRACE_HOST phase clock
     DBuf<unsigned long long> counters;
     DBuf<int> flag, it;
     DBuf<double> objs;
@@ -458,8 +461,8 @@ static void forward_plain(Ctx* c, const float* mu, double* l) {
                                                                               nullptr, nullptr, l, nullptr, c->flag.p,
                                                                               c->lgx);
         else
-            k_forward<0><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, mu, nullptr, nullptr, nullptr, l,
-                                                        nullptr, c->flag.p, -1);
+            k_fwd_patch<0, 4, 8, 5><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, mu, nullptr, nullptr,
+                                                                   nullptr, l, nullptr, c->flag.p);
     } else {
         const unsigned nb = nblk_warp(c, c->Ml);
 #define F3(S) k_forward3<0, S><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu, nullptr, nullptr, nullptr, \
@@ -598,12 +601,23 @@ static void launch_walk_lv(Ctx* c, int nlev, unsigned lvpack, unsigned long long
     // G ray groups of 32 per CTA so that a CTA has ~4 warps whatever nlev is
     const int G = std::max(1, 4 / nlev);
     const unsigned nb = blocks_for(c->Ml, 32 * G);
-    const size_t smem = walk_smem(G, nlev, c->tree_words).total;
-    if (smem > 200 * 1024) throw ConfigError("tree too large for the shared-memory walk");
-    CK(cudaFuncSetAttribute(k_walk_lv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_walk_lv<<<nb, 32 * nlev * G, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, nlev, G, lvpack, c->tbits.p,
-                                                 c->boff, c->tree_words, c->zfix.p, c->zfix2.p, c->cursor.p, cap,
-                                                 c->kin_s.p, c->vin_s.p);
+#define WL(D, NS)                                                                                                 \
+    {                                                                                                             \
+        const size_t smem = walk_smem(G, nlev, c->tree_words, D, NS).total;                                       \
+        if (smem > 200 * 1024) throw ConfigError("tree too large for the shared-memory walk");                    \
+        CK(cudaFuncSetAttribute(k_walk_lv<D, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
+        k_walk_lv<D, NS><<<nb, 32 * nlev * G, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, nlev, G, lvpack, \
+                                                            c->tbits.p, c->boff, c->tree_words, c->zfix.p,        \
+                                                            c->zfix2.p, c->cursor.p, cap, c->kin_s.p, c->vin_s.p); \
+    }
+    switch (c->walk_variant) {
+        case 1: WL(8, 2) break;
+        case 2: WL(16, 2) break;
+        case 3: WL(32, 1) break;
+        case 4: WL(4, 2) break;
+        default: WL(16, 1) break;   // measured best at cfg2 (expand 17.6 ms vs 19.0 for (8,2))
+    }
+#undef WL
     check_launch(c, "k_walk_lv");
 }
 
@@ -967,8 +981,26 @@ static void z0_from_zfix(Ctx* c) {
 // fixed-point Z; the batch is radix-sorted by z straight into E after the
 // existing entries, and k_cols_set records each new column's [lo, hi).  Within
 // a column the ray order is arbitrary: the split sums in exact fixed point.
+static double host_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static bool trace_host() {
+    static const bool on = std::getenv("WAMGPU_TRACE_HOST") != nullptr;
+    return on;
+}
+#define HTRACE(label)                                                                  \
+    do {                                                                               \
+        if (trace_host()) {                                                            \
+            CK(cudaStreamSynchronize(c->st));                                          \
+            const double t_ = host_ms();                                               \
+            std::fprintf(stderr, "[wamgpu] %-28s %8.3f ms\n", label, t_ - c->t_trace); \
+            c->t_trace = t_;                                                           \
+        }                                                                              \
+    } while (0)
+
 static void phi_append(Ctx* c) {
-    // active detail list from the host tree (ascending Mallat index), new bits
+    // active detail list from the host tree (level by level, the H, V, D of a
+    // block adjacent: the split is order-free and they share rays), new bits
     std::vector<unsigned> lst;
     std::vector<uint8_t> nw(c->act_bytes, 0);
     bool lv_new[LMAX + 2] = {};
@@ -986,7 +1018,7 @@ static void phi_append(Ctx* c) {
                 if (!c->act_phi[o + i]) { nw[o + i] = 1; lv_new[l] = true; }
             }
     }
-    std::sort(lst.begin(), lst.end());
+    HTRACE("expand: list + new bits");
     c->nlist = lst.size();
     c->list.ensure(std::max<size_t>(lst.size(), 1));
     if (!lst.empty())
@@ -1002,6 +1034,7 @@ static void phi_append(Ctx* c) {
         return;
     }
     upload_tree_bits(c, nw);
+    HTRACE("expand: list/tree upload");
     c->cursor.ensure(1);
     c->zfix2.ensure(c->Ml + 1);
     // capacity guess for the batch (a short guess costs a second walk)
@@ -1019,6 +1052,7 @@ static void phi_append(Ctx* c) {
         cap = tot + tot / 8;
     }
     c->phi_batch = tot;
+    HTRACE("expand: walk");
     // append: E keeps the first nnz_phi entries, the sorted batch follows
     const uint64_t off = c->nnz_phi;
     if (c->E.n < off + tot + 64) {
@@ -1029,6 +1063,7 @@ static void phi_append(Ctx* c) {
     }
     c->kout_s.ensure(std::max<uint64_t>(tot, 1));
     c->ptmp.ensure(c->N + 1);
+    HTRACE("expand: E grow");
     if (tot) {
         const int bits = bits_for(c->N);
         auto vi = reinterpret_cast<unsigned long long*>(c->vin_s.p);
@@ -1041,6 +1076,7 @@ static void phi_append(Ctx* c) {
                                            c->st));
         launched(c, 4);
     }
+    HTRACE("expand: sort");
     k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(c->kout_s.p, tot, c->N, c->ptmp.p);
     check_launch(c, "k_bounds");
     k_cols_set<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->ptmp.p, off, c->cols.p);
@@ -1052,6 +1088,7 @@ static void phi_append(Ctx* c) {
     z0_from_zfix(c);
     c->nnz_phi = off + valid;
     c->act_phi = c->act_host;
+    HTRACE("expand: bounds + Z0");
 }
 
 static int64_t count_active(const Ctx* c) {
@@ -1155,7 +1192,14 @@ static void wam_step(Ctx* c) {
         c->timer_begin(T_SPLIT);
         const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist + 7) / 8, (uint64_t)c->sms * 16);
         if (c->nzl == 1) {
-            k_split<<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
+            if (c->split_variant == 1)
+                k_split<4><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
+            else if (c->split_variant == 2)
+                k_split<8><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
+            else if (c->split_variant == 3)
+                k_split<16><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
+            else   // measured best at cfg2 (profiles/r02_fwd_patch_sweep.txt)
+                k_split<12><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
         } else {
             double* bm3 = c->g.p + NV(c);
 #define S3(S) k_split3<S><<<nb, 256, 0, c->st>>>(c->nlist, c->nzl, c->list.p, c->cols.p, c->E.p, c->q.p, bm3);
@@ -1188,6 +1232,7 @@ static void wam_iterate(Ctx* c, int n, wamgpu_record* recs) {
 
 static int64_t wam_expand(Ctx* c, double factor) {
     if (c->algo != 2) throw ContractError("wam: not initialised");
+    if (trace_host()) { CK(cudaStreamSynchronize(c->st)); c->t_trace = host_ms(); }
     c->timer_begin(T_EXPAND);
     tile_launch(c, 0, c->mu64.p, nullptr);         // fp64 criterion image Omega beta
     if (c->haar3) {                                 // pin P3: every voxel, no z-sum
@@ -1246,8 +1291,10 @@ static int64_t wam_expand(Ctx* c, double factor) {
         for (uint64_t i = 0; i < c->act_bytes; ++i) newly += (h[i] != 0) - (c->act_host[i] != 0);
         c->act_host.swap(h);
         if (newly > 0) {
+            HTRACE("expand: criterion + mark");
             phi_append(c);    // new columns of Phi^-, Z(y) and Z0 of the grown tree
             c->active = count_active(c);
+            HTRACE("expand: count active");
         }
     }
     c->timer_end(T_EXPAND);
@@ -1286,6 +1333,8 @@ static Ctx* create(int device) {
     if (prop.major < 10) throw CudaError("wamgpu: requires an sm_100a (Blackwell) device");
     c->sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("WAMGPU_FWD_VARIANT")) c->fwd_variant = std::atoi(e);
+    if (const char* e = std::getenv("WAMGPU_SPLIT_VARIANT")) c->split_variant = std::atoi(e);
+    if (const char* e = std::getenv("WAMGPU_WALK_VARIANT")) c->walk_variant = std::atoi(e);
     if (const char* e = std::getenv("WAMGPU_BACK_VARIANT")) c->back_variant = std::atoi(e);
     CK(cudaEventCreate(&c->ev_t0));
     CK(cudaEventCreate(&c->ev_a));
