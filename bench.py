@@ -324,8 +324,10 @@ def main():
         back_avg = sum(back_ms) / max(back_n, 1)
         fwd_gbs = fwd_bytes / (fwd_avg * 1e-3) / 1e9
         back_gbs = back_bytes / (back_avg * 1e-3) / 1e9
-        dom = "k_forward<1> (K2 CSR forward + Beer + I-div)" if sum(fwd_ms) >= sum(back_ms) else \
-            "k_back (K3 CSC back projection)"
+        fwd_name = ("k_fwd_patch<1,4,8,5> (K2 CSR forward + Beer + I-div, 4 rays/warp)" if nz == 1 else
+                    "k_forward3<1> (K2' slab forward + Beer + I-div)")
+        back_name = "k_back<1,12,1> (K3 CSC back projection)" if nz == 1 else "k_back3 (K3' slab back projection)"
+        dom = fwd_name if sum(fwd_ms) >= sum(back_ms) else back_name
         ach = fwd_gbs if sum(fwd_ms) >= sum(back_ms) else back_gbs
         traffic = None
         try:

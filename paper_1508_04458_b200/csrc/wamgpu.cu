@@ -516,7 +516,7 @@ static void forward_fused(Ctx* c, bool record) {
             case 25: FP(4, 6, 5) break;
             case 26: FP(2, 8, 5) break;
             case 9: FV(1, 4, 8) break;    // round-1 default (row-per-warp)
-            default: FP(4, 8, 5) break;   // measured best at cfg2 (patch sweep, profiles/r02_fwd_patch_sweep.txt)
+            default: FP(4, 8, 5) break;   // measured best at cfg2 (patch sweep, profiles/r01_fwd_patch_sweep.txt)
         }
 #undef FP
 #undef FV
@@ -1198,7 +1198,7 @@ static void wam_step(Ctx* c) {
                 k_split<8><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
             else if (c->split_variant == 3)
                 k_split<16><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
-            else   // measured best at cfg2 (profiles/r02_fwd_patch_sweep.txt)
+            else   // measured best at cfg2 (profiles/r01_fwd_patch_sweep.txt)
                 k_split<12><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
         } else {
             double* bm3 = c->g.p + NV(c);

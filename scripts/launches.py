@@ -9,7 +9,7 @@ for i, r in enumerate(rows):
         hdr, start = r, i + 1
         break
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 agg = collections.OrderedDict()
 for r in rows[start:]:
     if len(r) <= vi:
