@@ -93,6 +93,36 @@ def test_z0_validity_and_definition():  # SPEC.md:396, acceptance 5, Eq. 1.61
     assert abs(acc.max() - z0) <= 1e-9 * z0
 
 
+def test_fixed_point_z_majorizes():  # pin P8: mirror Z(y) in 2^-32 fixed point, terms rounded up
+    cfg, p64, _, I0, d = problem_inputs("tiny", O, None)
+    p = O.Problem(p64.geom, mirror=True)
+    p.wam_init(d, I0, cfg["L"])
+    p.wam_run(12, [4, 8], 0.1)
+    zr = p.wam_z0_rows()
+    assert p.wam_get()["Z0"] == zr.max()
+    assert np.all(zr * 2.0**32 == np.round(zr * 2.0**32))      # exact multiples of 2^-32
+    tree = p.wam_tree()
+    L, n = cfg["L"], cfg["nx"]
+    acc, nterm = np.zeros(p.M), np.zeros(p.M)
+    zs = [i * n + j for i in range(n >> L) for j in range(n >> L)]
+    off = 0
+    for lvl in range(1, L + 1):
+        m = n >> lvl
+        for bi in range(m):
+            for bj in range(m):
+                if tree[off + bi * m + bj]:
+                    zs += [(m + bi) * n + bj, bi * n + m + bj, (m + bi) * n + m + bj]
+        off += m * m
+    for z in zs:
+        rows, vals = p.phi_column(L, z)
+        np.add.at(acc, rows.astype(np.int64), np.abs(vals))
+        np.add.at(nterm, rows.astype(np.int64), 1.0)
+    # majorizes the exact sum (up to the f64 rounding of acc itself) and stays
+    # within one 2^-32 per term (+1 for the approximation part) above it
+    assert np.all(zr >= acc * (1 - 1e-14))
+    assert np.all(zr - acc <= (nterm + 1) * 2.0**-32 + 1e-12 * acc)
+
+
 def test_expand_tree_bright_block_oracle():  # SPEC.md:256, acceptance 8
     g = _geom(32, 30, 48, 1.0)
     p = O.Problem(g)
