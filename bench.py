@@ -319,7 +319,12 @@ def main():
             fwd_bytes = 8 * nnz_local + 4 * (Ml + 1) + 4 * N + 12 * Ml
             back_bytes = 8 * nnz_local + 4 * (N + 1) + 4 * Ml + 4 * N
         else:
-            fwd_bytes = back_bytes = 4 * nnz_local * nz                   # SURVEY.md §8(d) K2'/K3': 4 B/update
+            # slab kernels read H once per pass for all nz slices: the minimal
+            # HBM traffic is H + the slab vectors; the 4 B/update SURVEY figure
+            # (SURVEY.md §8(d) K2'/K3') is served from L1/L2 and reported as
+            # gather_gbs
+            fwd_bytes = 8 * nnz_local + 4 * (Ml + 1) + 4 * N * nz + 12 * Ml * nz
+            back_bytes = 8 * nnz_local + 4 * (N + 1) + 4 * Ml * nz + 16 * N * nz
         fwd_avg = sum(fwd_ms) / max(fwd_n, 1)
         back_avg = sum(back_ms) / max(back_n, 1)
         fwd_gbs = fwd_bytes / (fwd_avg * 1e-3) / 1e9
@@ -368,6 +373,7 @@ def main():
                          "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
                          "algorithmic_bytes": fwd_bytes if "forward" in dom else back_bytes},
             "kernels": {"fwd_avg_ms": fwd_avg, "fwd_gbs": fwd_gbs, "fwd_frac": fwd_gbs / hbm,
+                        "gather_gbs": (4 * nnz_local * nz / (fwd_avg * 1e-3) / 1e9) if nz > 1 else None,
                         "back_avg_ms": back_avg, "back_gbs": back_gbs, "back_frac": back_gbs / hbm,
                         "per_step_ms": {"forward": sum(fwd_ms) / args.steps, "back": sum(back_ms) / args.steps,
                                         "split": split_ms / args.steps, "update": upd_ms / args.steps,
