@@ -78,6 +78,13 @@ class Plumbing:
         self.dist.broadcast_object_list(obj, src=0)
         return obj[0]
 
+    def all_gather_bytes(self, b: bytes):
+        if not self.dist:
+            return [b]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, b)
+        return out
+
     def max(self, v: float):
         if not self.dist:
             return v
@@ -246,6 +253,15 @@ def main():
         uid = plumb.bcast_bytes(W.nccl_unique_id() if rank == 0 else b"")
         ctx.set_comm(uid, rank, world)
     ctx.set_geometry(g)
+    collective = "none" if world == 1 else "nccl"
+    if world > 1 and cfg["nz"] == 1 and os.environ.get("WAMGPU_P2P", "1") != "0":
+        # fused back projection + all-reduce over NVLink peer memory: exchange
+        # the CUDA IPC handles over the host plumbing
+        try:
+            blobs = plumb.all_gather_bytes(ctx.p2p_export())
+            collective = "fused-p2p" if ctx.p2p_import(b"".join(blobs)) else "nccl (p2p self-check failed)"
+        except Exception as e:  # no peer access: stay on NCCL
+            collective = f"nccl (p2p unavailable: {e})"
     if cfg["nz"] > 1 and algo == "wam":
         ctx.set_haar_dim(cfg["haar"])
     ctx.set_data(d, I0)
@@ -364,7 +380,8 @@ def main():
             "data": "synthetic (seeded luggage phantom, seeded Poisson counts; product host simulator)",
             "config": {"workload": _workload_desc(cfg, nnz, algo, J), "step": "init_state + run (all iterations"
                        " and expansions)", "l2": "working set (H CSR+CSC = 16 B/nnz) >> 126 MB L2; no flush needed",
-                       "parallelism": f"views/{world}"},
+                       "parallelism": f"views/{world}" if cfg["nz"] == 1 else f"z-slabs/{world}",
+                       "collective": collective},
             "ray_voxel_updates_per_s": 2 * nnz * nz * J / (ms_step * 1e-3),
             "final_objective": final_obj,
             "tree": {"active_set_by_iteration": sorted({r["active_set"] for r in recs}),

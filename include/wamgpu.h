@@ -98,6 +98,25 @@ int wamgpu_destroy(wamgpu_ctx* ctx);
 int wamgpu_nccl_unique_id(void* id128);
 int wamgpu_set_comm(wamgpu_ctx* ctx, const void* id128, int rank, int nranks);
 
+/* Fused back projection + all-reduce over NVLink peer memory (view-sharded 2D,
+ * DESIGN.md §7): replaces the back-projection kernel + ncclAllReduce of
+ * [g || b-] by one kernel per rank.  After set_comm and the matrix: every rank
+ * exports a WAMGPU_P2P_BLOB-byte blob of CUDA IPC handles, the caller gathers
+ * them in rank order (any host transport), and every rank imports the
+ * concatenation.  import runs a collective self-check; *ok = 1 when the fused
+ * path is active, 0 when the library stays on NCCL. */
+#define WAMGPU_P2P_BLOB 256
+int wamgpu_p2p_export(wamgpu_ctx* ctx, void* blob);
+int wamgpu_p2p_import(wamgpu_ctx* ctx, const void* blobs, int* ok);
+/* Test hooks (emulate R ranks in one cooperative grid on one GPU): synthetic
+ * partials (R x n -> R x n results), and the production back-projection
+ * producer over R contexts holding the R row shards (w[k]: shard k's local rows,
+ * extra[k]: N doubles or NULL; out: R x 2N). */
+int wamgpu_selftest_fused_allreduce(int device, int R, uint64_t n, const double* partials, double* out,
+                                    int epochs);
+int wamgpu_selftest_fused_back(wamgpu_ctx* const* ctxs, int R, const double* const* w,
+                               const double* const* extra, double* out);
+
 /* System model.  set_geometry replaces build_system_matrix(g)
  * (projector.hpp:126-148): the ray table is built on the host with the
  * reference's make_ray arithmetic (projector.hpp:22-49) and the Siddon traversal

@@ -50,6 +50,18 @@ class Context {
     wamgpu_ctx* raw() const { return c_; }
 
     void set_comm(const void* nccl_id128, int rank, int nranks) { check(wamgpu_set_comm(c_, nccl_id128, rank, nranks), c_); }
+    // fused back projection + all-reduce over NVLink peer memory (wamgpu.h):
+    // export, all-gather the blobs in rank order, import (collective)
+    std::vector<char> p2p_export() {
+        std::vector<char> b(WAMGPU_P2P_BLOB);
+        check(wamgpu_p2p_export(c_, b.data()), c_);
+        return b;
+    }
+    bool p2p_import(const std::vector<char>& all_blobs) {
+        int ok = 0;
+        check(wamgpu_p2p_import(c_, all_blobs.data(), &ok), c_);
+        return ok != 0;
+    }
 
     /// build_system_matrix(g) on the device (projector.hpp:126-148).
     void set_geometry(const wamgpu_geometry& g) { check(wamgpu_set_geometry(c_, &g), c_); }

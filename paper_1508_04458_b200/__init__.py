@@ -59,7 +59,9 @@ EXPORTED = [
     "wamgpu_wam_expand", "wamgpu_wam_run", "wamgpu_get_image", "wamgpu_get_beta", "wamgpu_get_q",
     "wamgpu_get_tree", "wamgpu_get_stats", "wamgpu_get_scalars", "wamgpu_get_z_rows", "wamgpu_get_timing",
     "wamgpu_set_kernel_timing", "wamgpu_rasterize", "wamgpu_simulate", "wamgpu_host_rays", "wamgpu_set_haar_dim",
+    "wamgpu_p2p_export", "wamgpu_p2p_import", "wamgpu_selftest_fused_allreduce", "wamgpu_selftest_fused_back",
 ]
+P2P_BLOB = 256   # WAMGPU_P2P_BLOB
 
 
 # ---------------------------------------------------------------- C structs
@@ -157,6 +159,33 @@ def _records(arr):
                  cum_updates=r.cum_updates) for r in arr]
 
 
+def selftest_fused_allreduce(partials, epochs=2, device=0):
+    """R logical ranks of the fused all-reduce in one cooperative grid on one
+    GPU: partials (R, n) -> every rank's result (R, n)."""
+    p = np.ascontiguousarray(partials, np.float64)
+    R, n = p.shape
+    out = np.empty_like(p)
+    _chk(load().wamgpu_selftest_fused_allreduce(int(device), int(R), C.c_uint64(n), _p(p), _p(out), int(epochs)))
+    return out
+
+
+def selftest_fused_back(ctxs, ws, extras=None):
+    """The fused back projection + all-reduce over R contexts (context k plays
+    rank k with its own row shard) on one GPU: returns (R, 2N)."""
+    R = len(ctxs)
+    hs = (C.c_void_p * R)(*[c.h for c in ctxs])
+    wk = [np.ascontiguousarray(w, np.float64) for w in ws]
+    wp = (C.POINTER(C.c_double) * R)(*[_p(w) for w in wk])
+    ek = None
+    ep = None
+    if extras is not None:
+        ek = [np.ascontiguousarray(e, np.float64) for e in extras]
+        ep = (C.POINTER(C.c_double) * R)(*[_p(e) for e in ek])
+    out = np.empty((R, 2 * ctxs[0].N), np.float64)
+    _chk(load().wamgpu_selftest_fused_back(hs, int(R), wp, ep, _p(out)))
+    return out
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _chk(load().wamgpu_nccl_unique_id(buf))
@@ -195,6 +224,20 @@ class Context:
     # ---- setup
     def set_comm(self, uid: bytes, rank: int, nranks: int):
         _chk(load().wamgpu_set_comm(self.h, C.c_char_p(uid) if uid else None, int(rank), int(nranks)), self.h)
+
+    def p2p_export(self) -> bytes:
+        """This rank's CUDA IPC handles for the fused back projection +
+        all-reduce over NVLink peer memory (after set_comm and the matrix)."""
+        buf = C.create_string_buffer(P2P_BLOB)
+        _chk(load().wamgpu_p2p_export(self.h, buf), self.h)
+        return buf.raw
+
+    def p2p_import(self, blobs: bytes) -> bool:
+        """blobs: every rank's p2p_export() concatenated in rank order.  Runs a
+        collective self-check; True when the fused path is active."""
+        ok = C.c_int(0)
+        _chk(load().wamgpu_p2p_import(self.h, C.c_char_p(blobs), C.byref(ok)), self.h)
+        return bool(ok.value)
 
     def _info(self):
         M, N, nnz, r0, r1 = (C.c_uint64() for _ in range(5))

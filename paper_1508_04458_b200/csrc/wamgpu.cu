@@ -30,6 +30,7 @@
 #include "kernels.cuh"
 #include "kernels3d.cuh"
 #include "kernels3h.cuh"
+#include "kernels_ar.cuh"
 
 namespace wamgpu {
 
@@ -138,6 +139,15 @@ struct wamgpu_ctx {
     int split_variant = 0;                  // WAMGPU_SPLIT_VARIANT
     int walk_variant = 0;                   // WAMGPU_WALK_VARIANT
     double t_trace = 0.0;                   // WAMGPU_TRACE_HOST phase clock
+    // fused back projection + all-reduce over NVLink peer memory (kernels_ar.cuh)
+    struct {
+        bool on = false;                    // set by wamgpu_p2p_import after its self-check
+        DBuf<double> slot, res, extra, ones;
+        DBuf<unsigned long long> cnt, rdy;
+        wamgpu::ArArgs args{};
+        std::vector<void*> opened;          // peer pointers from cudaIpcOpenMemHandle
+        uint64_t n = 0;
+    } ar;
     DBuf<unsigned long long> counters;
     DBuf<int> flag, it;
     DBuf<double> objs;
@@ -249,6 +259,7 @@ static void check_flag(Ctx* c, const char* where) {
         if (f & 1) what += "non-finite line integral; ";
         if (f & 2) what += "non-finite AM update; ";
         if (f & 4) what += "non-finite coefficient update; ";
+        if (f & 256) what += "fused all-reduce: a peer did not arrive within 10 s; ";
         throw NumericError(what);
     }
 }
@@ -452,6 +463,41 @@ static void back_launch(Ctx* c, const float* w, double* out, const double* bam) 
     c->tm.back_launches++;
 }
 static void back_into(Ctx* c, const float* w, double* out) { back_launch(c, w, out, nullptr); }
+
+// one cooperative launch of the fused back projection + all-reduce (kernels_ar.cuh);
+// rexec logical ranks [a.r0, a.r0 + rexec) run in this grid
+template <class Prod>
+static void launch_fused_ar(int sms, cudaStream_t st, ArArgs a, const Prod& prod, int rexec) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_allreduce<Prod>, 256, 0));
+    const uint64_t ntiles = (a.n + AR_TILE - 1) / AR_TILE;
+    const int per = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)per_sm * sms / rexec, ntiles));
+    if (per * rexec > per_sm * sms) throw ConfigError("fused all-reduce: ranks exceed the co-resident CTAs");
+    a.rexec = rexec;
+    Prod p = prod;
+    void* args[] = {&a, &p};
+    CK(cudaLaunchCooperativeKernel((void*)k_fused_allreduce<Prod>, dim3(per * rexec), dim3(256), args, 0, st));
+}
+
+// [g || extra] = sum over ranks of (H_r^T w || extra_r): one fused kernel per
+// rank; the result is left in c->ar.res (n = 2N) on every rank
+static void back_allreduce(Ctx* c, const float* w, const double* extra) {
+    c->timer_begin(T_BACK);
+    ArProdBack pb{};
+    pb.cp[c->rank] = c->cp.p;
+    pb.C[c->rank] = c->C.p;
+    pb.w[c->rank] = w;
+    pb.extra[c->rank] = extra;
+    pb.N = c->N;
+    ArArgs a = c->ar.args;
+    a.epoch = ++c->ar.args.epoch;
+    a.r0 = c->rank;
+    a.err = c->flag.p;
+    launch_fused_ar(c->sms, c->st, a, pb, 1);
+    check_launch(c, "k_fused_allreduce");
+    c->timer_end(T_BACK);
+    c->tm.back_launches++;
+}
 
 // plain l = H mu (fp64 out), for forward_project
 static void forward_plain(Ctx* c, const float* mu, double* l) {
@@ -901,9 +947,15 @@ static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
         if (!c->comm || c->nzl > 1) {
             back_launch(c, c->q.p, nullptr, c->bam.p);   // fused multiplicative update
         } else {
-            back_into(c, c->q.p, c->g.p);
-            allreduce_sum(c, c->g.p, c->N);
-            k_am_update<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->g.p, c->bam.p, c->mu.p, c->Z0, c->flag.p,
+            const double* g = c->g.p;
+            if (c->ar.on) {   // fused back projection + all-reduce over NVLink peer memory
+                back_allreduce(c, c->q.p, c->ar.extra.p);   // extra = zeros here
+                g = c->ar.res.p;
+            } else {
+                back_into(c, c->q.p, c->g.p);
+                allreduce_sum(c, c->g.p, c->N);
+            }
+            k_am_update<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, g, c->bam.p, c->mu.p, c->Z0, c->flag.p,
                                                                    c->lgx);
             check_launch(c, "k_am_update");
         }
@@ -1148,6 +1200,7 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     if (c->nzl == 1) allreduce_sum(c, c->g.p, N);
     tile_launch(c, 2, nullptr, c->bdata.p);
     CK(cudaMemsetAsync(c->g.p, 0, 2 * N * 8, c->st));
+    if (c->ar.extra.p) CK(cudaMemsetAsync(c->ar.extra.p, 0, c->N * 8, c->st));   // fused path: no stale b-
     c->Z0 = compute_z0(c, L, true);
     c->nlist = 0;
     c->nlist3 = 0;
@@ -1176,7 +1229,11 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
 }
 
 static void wam_step(Ctx* c) {
-    back_into(c, c->q.p, c->g.p);
+    // view-sharded 2D with peer memory: split first (its partial b- rides along
+    // as the second half of the fused back projection + all-reduce)
+    const bool fused = c->ar.on && c->nzl == 1 && !c->haar3;
+    double* bm2 = fused ? c->ar.extra.p : c->g.p + c->N;
+    if (!fused) back_into(c, c->q.p, c->g.p);
     if (c->haar3 && c->nlist3) {
         c->timer_begin(T_SPLIT);
         const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist3 + 3) / 4, (uint64_t)c->sms * 16);
@@ -1193,13 +1250,13 @@ static void wam_step(Ctx* c) {
         const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist + 7) / 8, (uint64_t)c->sms * 16);
         if (c->nzl == 1) {
             if (c->split_variant == 1)
-                k_split<4><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
+                k_split<4><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, bm2);
             else if (c->split_variant == 2)
-                k_split<8><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
+                k_split<8><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, bm2);
             else if (c->split_variant == 3)
-                k_split<16><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
+                k_split<16><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, bm2);
             else   // measured best at cfg2 (profiles/r01_fwd_patch_sweep.txt)
-                k_split<12><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, c->g.p + c->N);
+                k_split<12><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, bm2);
         } else {
             double* bm3 = c->g.p + NV(c);
 #define S3(S) k_split3<S><<<nb, 256, 0, c->st>>>(c->nlist, c->nzl, c->list.p, c->cols.p, c->E.p, c->q.p, bm3);
@@ -1210,7 +1267,15 @@ static void wam_step(Ctx* c) {
         c->timer_end(T_SPLIT);
         c->tm.split_launches++;
     }
-    if (c->nzl == 1) allreduce_sum(c, c->g.p, 2 * c->N);   // view shards: partial sums
+    if (fused) {
+        // inactive details keep b- = 0 (k_tile reads only active ones); the
+        // extra half must still be the split's output or zeros
+        if (!c->nlist) CK(cudaMemsetAsync(c->ar.extra.p, 0, c->N * 8, c->st));
+        back_allreduce(c, c->q.p, c->ar.extra.p);
+        CK(cudaMemcpyAsync(c->g.p, c->ar.res.p, 2 * c->N * 8, cudaMemcpyDeviceToDevice, c->st));
+    } else if (c->nzl == 1) {
+        allreduce_sum(c, c->g.p, 2 * c->N);   // view shards: partial sums
+    }
     c->timer_begin(T_UPDATE);
     tile_launch(c, 1, nullptr, nullptr);
     c->timer_end(T_UPDATE);
@@ -1359,6 +1424,7 @@ static void destroy(Ctx* c) {
     if (c->ev_t0) cudaEventDestroy(c->ev_t0);
     if (c->ev_a) cudaEventDestroy(c->ev_a);
     if (c->ev_b) cudaEventDestroy(c->ev_b);
+    for (void* p : c->ar.opened) cudaIpcCloseMemHandle(p);
     if (c->comm) ncclCommDestroy(c->comm);
     c->A.release(); c->C.release(); c->E.release();
     cudaStreamDestroy(c->st);
@@ -1432,6 +1498,205 @@ int wamgpu_set_comm(wamgpu_ctx* ctx, const void* id128, int rank, int nranks) {
         } else if (nranks > 1) {
             throw ContractError("set_comm: an ncclUniqueId is required for nranks > 1");
         }
+    })
+}
+
+// ---- fused back projection + all-reduce over NVLink peer memory ------------
+// buffers of this rank: staging R x n, result n, per-tile counters, ready counter
+static void ar_alloc(Ctx* c) {
+    const int R = c->nranks;
+    const uint64_t n = 2 * c->N, ntiles = (n + AR_TILE - 1) / AR_TILE;
+    c->ar.n = n;
+    c->ar.slot.alloc((uint64_t)R * n);
+    c->ar.res.alloc(n);
+    c->ar.extra.alloc(c->N);
+    c->ar.cnt.alloc(ntiles);
+    c->ar.rdy.alloc(1);
+    CK(cudaMemsetAsync(c->ar.extra.p, 0, c->N * 8, c->st));
+    CK(cudaMemsetAsync(c->ar.cnt.p, 0, ntiles * 8, c->st));
+    CK(cudaMemsetAsync(c->ar.rdy.p, 0, 8, c->st));
+    CK(cudaStreamSynchronize(c->st));
+}
+
+int wamgpu_p2p_export(wamgpu_ctx* ctx, void* blob) {
+    API_TRY(ctx, {
+        NEED(ctx); NEED(blob);
+        Ctx* c = ctx;
+        if (c->nranks < 2 || c->nranks > AR_MAX) throw ContractError("p2p: needs 2..8 ranks (set_comm)");
+        need_matrix(c);
+        if (c->nz != 1) throw ContractError("p2p: the fused all-reduce serves the view-sharded 2D path");
+        CK(cudaSetDevice(c->device));
+        ar_alloc(c);
+        cudaIpcMemHandle_t h[4];
+        CK(cudaIpcGetMemHandle(&h[0], c->ar.slot.p));
+        CK(cudaIpcGetMemHandle(&h[1], c->ar.res.p));
+        CK(cudaIpcGetMemHandle(&h[2], c->ar.cnt.p));
+        CK(cudaIpcGetMemHandle(&h[3], c->ar.rdy.p));
+        static_assert(sizeof(h) == WAMGPU_P2P_BLOB, "blob size");
+        std::memcpy(blob, h, sizeof(h));
+    })
+}
+
+int wamgpu_p2p_import(wamgpu_ctx* ctx, const void* blobs, int* ok) {
+    API_TRY(ctx, {
+        NEED(ctx); NEED(blobs);
+        Ctx* c = ctx;
+        if (!c->ar.slot.p) throw ContractError("p2p_import: p2p_export first");
+        CK(cudaSetDevice(c->device));
+        // every local failure becomes good = 0; every rank always reaches the
+        // agreement all-reduce below (no rank may block in NCCL on another)
+        double good = 1.0;
+        std::string why;
+        try {
+            const int R = c->nranks;
+            ArArgs a{};
+            a.n = c->ar.n;
+            a.R = R;
+            auto get = [&](int k, int i) {
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, (const char*)blobs + (size_t)k * WAMGPU_P2P_BLOB + (size_t)i * sizeof(h), sizeof(h));
+                void* p = nullptr;
+                CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+                c->ar.opened.push_back(p);
+                return p;
+            };
+            for (int k = 0; k < R; ++k) {
+                if (k == c->rank) {
+                    a.slot[k] = c->ar.slot.p; a.res[k] = c->ar.res.p; a.cnt[k] = c->ar.cnt.p; a.rdy[k] = c->ar.rdy.p;
+                } else {
+                    a.slot[k] = (double*)get(k, 0); a.res[k] = (double*)get(k, 1);
+                    a.cnt[k] = (unsigned long long*)get(k, 2); a.rdy[k] = (unsigned long long*)get(k, 3);
+                }
+            }
+            c->ar.args = a;
+            // self-check (collective, epoch 1): every rank contributes rank+1;
+            // a peer that never arrives makes the kernel time out (10 s), not hang
+            c->ar.ones.alloc(a.n);
+            std::vector<double> v(a.n, (double)(c->rank + 1));
+            CK(cudaMemcpyAsync(c->ar.ones.p, v.data(), a.n * 8, cudaMemcpyHostToDevice, c->st));
+            ArProdCopy pc{};
+            pc.in[c->rank] = c->ar.ones.p;
+            ArArgs a1 = a;
+            a1.epoch = c->ar.args.epoch = 1;
+            a1.r0 = c->rank;
+            a1.err = c->flag.p;
+            launch_fused_ar(c->sms, c->st, a1, pc, 1);
+            check_launch(c, "k_fused_allreduce");
+            check_flag(c, "p2p self-check");
+            CK(cudaMemcpyAsync(v.data(), c->ar.res.p, a.n * 8, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            const double want = 0.5 * R * (R + 1);
+            for (double x : v)
+                if (x != want) { good = 0.0; why = "wrong self-check sum"; break; }
+            c->ar.ones.release();
+        } catch (const std::exception& e) {
+            good = 0.0;
+            why = e.what();
+        }
+        double* d = nullptr;
+        CK(cudaMalloc(&d, 8));
+        CK(cudaMemcpyAsync(d, &good, 8, cudaMemcpyHostToDevice, c->st));
+        if (c->comm) NK(ncclAllReduce(d, d, 1, ncclDouble, ncclMin, c->comm, c->st));
+        CK(cudaMemcpyAsync(&good, d, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        cudaFree(d);
+        c->ar.on = good == 1.0;
+        if (ok) *ok = c->ar.on ? 1 : 0;
+        if (!c->ar.on && !why.empty()) c->err = "p2p disabled on this rank: " + why;
+    })
+}
+
+// R logical ranks emulated in ONE cooperative grid on one GPU (B200_PROFILING.md):
+// partials R x n -> out R x n (every rank's result)
+int wamgpu_selftest_fused_allreduce(int device, int R, uint64_t n, const double* partials, double* out,
+                                    int epochs) {
+    const wamgpu_ctx* none = nullptr;
+    API_TRY(none, {
+        NEED(partials); NEED(out);
+        if (R < 1 || R > AR_MAX || n == 0 || epochs < 1) throw ContractError("selftest: bad R / n / epochs");
+        CK(cudaSetDevice(device));
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        cudaStream_t st;
+        CK(cudaStreamCreate(&st));
+        const uint64_t ntiles = (n + AR_TILE - 1) / AR_TILE;
+        std::vector<DBuf<double>> slot(R), res(R), in(R);
+        std::vector<DBuf<unsigned long long>> cnt(R), rdy(R);
+        DBuf<int> err;
+        err.alloc(1);
+        CK(cudaMemsetAsync(err.p, 0, 4, st));
+        ArArgs a{};
+        ArProdCopy pc{};
+        a.n = n; a.R = R; a.r0 = 0; a.err = err.p;
+        for (int k = 0; k < R; ++k) {
+            slot[k].alloc((uint64_t)R * n); res[k].alloc(n); in[k].alloc(n); cnt[k].alloc(ntiles); rdy[k].alloc(1);
+            CK(cudaMemsetAsync(cnt[k].p, 0, ntiles * 8, st));
+            CK(cudaMemsetAsync(rdy[k].p, 0, 8, st));
+            CK(cudaMemcpyAsync(in[k].p, partials + (uint64_t)k * n, n * 8, cudaMemcpyHostToDevice, st));
+            a.slot[k] = slot[k].p; a.res[k] = res[k].p; a.cnt[k] = cnt[k].p; a.rdy[k] = rdy[k].p;
+            pc.in[k] = in[k].p;
+        }
+        for (int e = 1; e <= epochs; ++e) {
+            a.epoch = (unsigned long long)e;
+            for (int k = 0; k < R; ++k) CK(cudaMemsetAsync(res[k].p, 0xff, n * 8, st));   // NaN: must be rewritten
+            launch_fused_ar(sms, st, a, pc, R);
+            CK(cudaGetLastError());
+        }
+        for (int k = 0; k < R; ++k) CK(cudaMemcpyAsync(out + (uint64_t)k * n, res[k].p, n * 8, cudaMemcpyDeviceToHost, st));
+        int e = 0;
+        CK(cudaMemcpyAsync(&e, err.p, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaStreamDestroy(st));
+        if (e) throw NumericError("fused all-reduce self-test: a logical rank did not arrive within 10 s");
+    })
+}
+
+// The production producer (CSC back projection of each rank's own rays + its
+// split partial) emulated over R contexts on one GPU: context k plays rank k
+// with its own matrix (rows = rank k's shard).  out: R x 2N results.
+int wamgpu_selftest_fused_back(wamgpu_ctx* const* ctxs, int R, const double* const* w,
+                               const double* const* extra, double* out) {
+    const wamgpu_ctx* none = nullptr;
+    API_TRY(none, {
+        NEED(ctxs); NEED(w); NEED(out);
+        if (R < 1 || R > AR_MAX) throw ContractError("selftest: bad R");
+        Ctx* c0 = ctxs[0];
+        need_matrix(c0);
+        CK(cudaSetDevice(c0->device));
+        const uint64_t N = c0->N, n = 2 * N, ntiles = (n + AR_TILE - 1) / AR_TILE;
+        std::vector<DBuf<double>> slot(R), res(R), ex(R);
+        std::vector<DBuf<float>> wf(R);
+        std::vector<DBuf<unsigned long long>> cnt(R), rdy(R);
+        DBuf<int> err;
+        err.alloc(1);
+        CK(cudaMemsetAsync(err.p, 0, 4, c0->st));
+        ArArgs a{};
+        ArProdBack pb{};
+        a.n = n; a.R = R; a.r0 = 0; a.epoch = 1; a.err = err.p;
+        pb.N = N;
+        for (int k = 0; k < R; ++k) {
+            Ctx* c = ctxs[k];
+            need_matrix(c);
+            if (c->N != N || c->device != c0->device) throw ContractError("selftest: contexts must share N and device");
+            slot[k].alloc((uint64_t)R * n); res[k].alloc(n); ex[k].alloc(N); cnt[k].alloc(ntiles); rdy[k].alloc(1);
+            wf[k].alloc(c->Ml + 1);
+            std::vector<float> wv(c->Ml);
+            for (uint64_t y = 0; y < c->Ml; ++y) wv[y] = (float)w[k][y];
+            CK(cudaMemcpyAsync(wf[k].p, wv.data(), c->Ml * 4, cudaMemcpyHostToDevice, c0->st));
+            if (extra && extra[k]) CK(cudaMemcpyAsync(ex[k].p, extra[k], N * 8, cudaMemcpyHostToDevice, c0->st));
+            else CK(cudaMemsetAsync(ex[k].p, 0, N * 8, c0->st));
+            CK(cudaMemsetAsync(cnt[k].p, 0, ntiles * 8, c0->st));
+            CK(cudaMemsetAsync(rdy[k].p, 0, 8, c0->st));
+            a.slot[k] = slot[k].p; a.res[k] = res[k].p; a.cnt[k] = cnt[k].p; a.rdy[k] = rdy[k].p;
+            pb.cp[k] = c->cp.p; pb.C[k] = c->C.p; pb.w[k] = wf[k].p; pb.extra[k] = ex[k].p;
+        }
+        launch_fused_ar(c0->sms, c0->st, a, pb, R);
+        CK(cudaGetLastError());
+        for (int k = 0; k < R; ++k) CK(cudaMemcpyAsync(out + (uint64_t)k * n, res[k].p, n * 8, cudaMemcpyDeviceToHost, c0->st));
+        int e = 0;
+        CK(cudaMemcpyAsync(&e, err.p, 4, cudaMemcpyDeviceToHost, c0->st));
+        CK(cudaStreamSynchronize(c0->st));
+        if (e) throw NumericError("fused back + all-reduce self-test: a logical rank did not arrive within 10 s");
     })
 }
 

@@ -97,3 +97,62 @@ def test_two_rank_sharded_am_step_matches_single_rank():
     mu = np.where((gd > 0) & (gq > 0), np.maximum(0.0, np.log(np.where(gd > 0, gq / np.where(gd > 0, gd, 1), 1)) / z0), 0.0)
     p.am_iterate(1)
     assert np.allclose(mu, p.am_get()["mu"], rtol=1e-10, atol=1e-14)
+
+
+def _p2p_worker(rank, world, port, out):
+    """bench.Plumbing over gloo: the IPC-handle blobs every rank exports are
+    gathered in RANK ORDER and concatenated (wamgpu_p2p_import's layout), and
+    the tile protocol of kernels_ar.cuh (owner = tile % R, owner sums the R
+    contributions in rank order, broadcasts) gives every rank the same result."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import torch
+    pl = bench.Plumbing(rank, world)
+    blob = bytes([rank]) * 256                            # WAMGPU_P2P_BLOB bytes
+    blobs = b"".join(pl.all_gather_bytes(blob))
+    # host model of the protocol over gloo: staging = all_gather of partials
+    n, T = 1000, 256
+    rng = np.random.default_rng(rank)
+    part = rng.standard_normal(n)
+    parts = [torch.zeros(n, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(parts, torch.from_numpy(part))
+    res = np.empty(n)
+    owned = []
+    for t in range((n + T - 1) // T):
+        if t % world != rank:
+            continue
+        owned.append(t)
+        sl = slice(t * T, min(n, (t + 1) * T))
+        s = np.zeros(sl.stop - sl.start)
+        for k in range(world):                               # rank order
+            s = s + parts[k].numpy()[sl]
+        res[sl] = s
+    # broadcast of owned tiles: every rank assembles the full result
+    full = torch.zeros(n, dtype=torch.float64)
+    mine = torch.zeros(n, dtype=torch.float64)
+    for t in owned:
+        sl = slice(t * T, min(n, (t + 1) * T))
+        mine[sl] = torch.from_numpy(res[sl])
+    dist.all_reduce(mine)                                    # disjoint tiles: a gather
+    full += mine
+    out[rank] = (blobs, full.numpy().copy(), [p.numpy().copy() for p in parts])
+    pl.close()
+
+
+def test_two_rank_p2p_blob_exchange_and_tile_protocol():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.start_processes(_p2p_worker, args=(world, port, out), nprocs=world, join=True, start_method="fork")
+    want_blobs = bytes([0]) * 256 + bytes([1]) * 256
+    for r in range(world):
+        assert out[r][0] == want_blobs
+    parts = out[0][2]
+    s = np.zeros_like(parts[0])
+    for p in parts:
+        s = s + p
+    assert np.array_equal(out[0][1], s) and np.array_equal(out[1][1], s)
