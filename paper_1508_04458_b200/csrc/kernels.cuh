@@ -45,6 +45,8 @@ __device__ __host__ __forceinline__ unsigned mu_addr(unsigned col, int lgx) {
 // Streaming (evict-first) 8-byte load of a matrix entry: the matrix is read
 // once per pass, keep L2 for the gathered vectors.
 __device__ __forceinline__ uint2 ld_stream(const uint2* p) { return __ldcs(p); }
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
+__device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
 
 // ------------------------------------------------------------------ Siddon
 // projector.hpp:52-119 on the device, fp64, every operation an explicit
@@ -331,6 +333,159 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_patch(uint64_t M, const unsig
             }
 #pragma unroll
             for (int u = 0; u < UNR; ++u) ec[u] = en[u];
+        }
+        double lg = acc0 + acc1;
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
+        if (has && sub == 0) {
+            if (!isfinite(lg)) atomicOr(flag, 1);
+            if (MODE == 0) {
+                lout[y] = lg;
+            } else {
+                const double qq = (double)I0[y] * exp(-lg);
+                q[y] = (float)qq;
+                tacc += idiv_term((double)d[y], qq);
+            }
+        }
+    }
+    if (MODE == 1) {
+        __shared__ double s[32];
+        double v = tacc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s[wib] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+            partial[blockIdx.x] = t;
+        }
+    }
+}
+
+// ---------------------------------------------- compressed CSR forward (C2)
+// A Siddon ray (projector.hpp:52-119) visits cells monotonically: every step
+// from one entry to the next moves by sx in x, sy in y, or both (a corner), with
+// sx, sy fixed per ray.  So a row is fully described by its first cell, the two
+// signs and 2 bits per entry.  C2 stores, per row, rh = {col0 | sign bits,
+// offset of the row's step codes} and, per group of 8 entries, one u16 code
+// (low byte: entries with an x step, high byte: with a y step), padded to 8
+// groups (16 B) per row; h is fp32 in the same 64-entry blocks, lane-major
+// (entry 8u + j at 8j + u) so a lane reads its 8 values with two 16-B loads.
+// ~4.4 B per entry instead of 8 (uint2 {col, h}).  k_c2_build derives it from the CSR on the device and
+// verifies every step; any row that does not fit disables C2 (flag).
+__global__ void k_c2_count(uint64_t M, const unsigned long long* __restrict__ rp, unsigned long long* __restrict__ nb) {
+    const uint64_t y = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= M) return;
+    const uint64_t len = rp[y + 1] - rp[y], groups = (len + 7) / 8;
+    nb[y] = (groups + 7) / 8;   // 16-byte blocks of 8 group codes
+}
+__global__ void k_c2_build(uint64_t M, const unsigned long long* __restrict__ rp, const uint2* __restrict__ A, int nx,
+                           const unsigned long long* __restrict__ boff, uint2* __restrict__ rh,
+                           unsigned short* __restrict__ codes, float* __restrict__ hv, int* __restrict__ bad) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t y = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; y < M; y += W) {
+        const uint64_t lo = rp[y], hi = rp[y + 1], len = hi - lo;
+        const uint64_t go = boff[y] * 8;   // in u16 group codes
+        int sx = 1, sy = 1;
+        unsigned col0 = 0;
+        if (len) {
+            const unsigned c0 = A[lo].x, c1 = A[hi - 1].x;
+            col0 = c0;
+            sx = (int)(c1 % (unsigned)nx) >= (int)(c0 % (unsigned)nx) ? 1 : -1;
+            sy = (int)(c1 / (unsigned)nx) >= (int)(c0 / (unsigned)nx) ? 1 : -1;
+        }
+        if (lane == 0) {
+            if (col0 >= (1u << 30)) atomicOr(bad, 1);
+            rh[y] = make_uint2(col0 | (sx < 0 ? 1u << 30 : 0u) | (sy < 0 ? 1u << 31 : 0u), (unsigned)boff[y]);
+        }
+        const uint64_t groups = (len + 7) / 8, padded = ((groups + 7) / 8) * 8;
+        for (uint64_t g = lane; g < padded; g += 32) {
+            unsigned mx = 0, my = 0;
+            for (int i = 0; i < 8; ++i) {
+                const uint64_t e = g * 8 + i;
+                if (e >= len) break;
+                const uint2 cur = A[lo + e];
+                // h lane-major inside each 64-entry block: entry 8u + j (group
+                // u, element j) at 8j + u, so lane j's 8 values are contiguous
+                hv[(boff[y] + g / 8) * 64 + 8 * i + (g % 8)] = __uint_as_float(cur.y);
+                if (e == 0) continue;
+                const unsigned prev = A[lo + e - 1].x;
+                const int dx = (int)(cur.x % (unsigned)nx) - (int)(prev % (unsigned)nx);
+                const int dy = (int)(cur.x / (unsigned)nx) - (int)(prev / (unsigned)nx);
+                if (!((dx == 0 || dx == sx) && (dy == 0 || dy == sy) && (dx | dy))) atomicOr(bad, 2);
+                mx |= (dx != 0 ? 1u : 0u) << i;
+                my |= (dy != 0 ? 1u : 0u) << i;
+            }
+            codes[go + g] = (unsigned short)(mx | (my << 8));
+        }
+    }
+}
+
+// Forward over C2: the lane mapping and summation of k_fwd_patch<MODE,4,8,MINB>
+// (4 adjacent rays per warp, 8 lanes per ray, round of 64 entries = 8 groups),
+// so the result is bit-identical; lane j's column in group u is
+// base_u + popc(mx & mask_j) sx + popc(my & mask_j) sy nx.
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fwd_c2(uint64_t M, const unsigned long long* __restrict__ rp,
+                                                 const uint2* __restrict__ rh,
+                                                 const unsigned short* __restrict__ codes,
+                                                 const float* __restrict__ hv, int nx, const float* __restrict__ mu,
+                                                 const float* __restrict__ I0, const float* __restrict__ d,
+                                                 float* __restrict__ q, double* __restrict__ lout,
+                                                 double* __restrict__ partial, int* __restrict__ flag) {
+    constexpr int R = 4, LPR = 8, UNR = 8;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, sub = lane & 7;
+    const unsigned pm = (2u << sub) - 1u;   // steps into entries 0..sub of a group
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t ntask = (M + R - 1) / R;
+    double tacc = 0.0;
+    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; t < ntask; t += W) {
+        const uint64_t y = t * R + (lane >> 3);
+        const bool has = y < M;
+        uint64_t lo = 0, hi = 0;
+        uint2 hd = make_uint2(0u, 0u);
+        if (has) { lo = __ldg(rp + y); hi = __ldg(rp + y + 1); hd = __ldg(rh + y); }
+        const unsigned len = (unsigned)(hi - lo);
+        unsigned maxlen = len;
+#pragma unroll
+        for (int o = 16; o >= LPR; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+        const int sx = (hd.x >> 30) & 1u ? -1 : 1;
+        const int sy = (hd.x >> 31) ? -nx : nx;
+        int base = (int)(hd.x & 0x3fffffffu);
+        const uint4* cblk = reinterpret_cast<const uint4*>(codes) + hd.y;            // 8 codes per block
+        const uint4* hblk = reinterpret_cast<const uint4*>(hv) + (uint64_t)hd.y * 16 + 2 * sub;   // lane's 8 h
+        const unsigned nblk = (len + 63) / 64;
+        double acc0 = 0.0, acc1 = 0.0;
+        uint4 ha = make_uint4(0u, 0u, 0u, 0u), hb = ha, cc = ha;   // padding entries hold h = 0
+        if (nblk) { cc = ld_stream(cblk); ha = ld_stream(hblk); hb = ld_stream(hblk + 1); }
+        for (unsigned off = 0, blk = 0; off < maxlen; off += LPR * UNR, ++blk) {
+            uint4 cn = make_uint4(0u, 0u, 0u, 0u), han = cn, hbn = cn;
+            if (blk + 1 < nblk) {
+                cn = ld_stream(cblk + blk + 1);
+                han = ld_stream(hblk + 16 * (blk + 1));
+                hbn = ld_stream(hblk + 16 * (blk + 1) + 1);
+            }
+            const unsigned hw[8] = {ha.x, ha.y, ha.z, ha.w, hb.x, hb.y, hb.z, hb.w};
+            const unsigned cw[4] = {cc.x, cc.y, cc.z, cc.w};
+            float v[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const unsigned code = (cw[u >> 1] >> (16 * (u & 1))) & 0xffffu;
+                const unsigned mx = code & 0xffu, my = code >> 8;
+                const int col = base + __popc(mx & pm) * sx + __popc(my & pm) * sy;
+                v[u] = (off + LPR * u + sub < len) ? __ldg(mu + col) : 0.0f;
+                base += __popc(mx) * sx + __popc(my) * sy;
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const double h = (double)__uint_as_float(hw[u]), xv = (double)v[u];
+                if (u & 1) acc1 = fma(h, xv, acc1); else acc0 = fma(h, xv, acc0);
+            }
+            ha = han;
+            hb = hbn;
+            cc = cn;
         }
         double lg = acc0 + acc1;
 #pragma unroll

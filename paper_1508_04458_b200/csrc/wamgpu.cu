@@ -92,6 +92,12 @@ struct wamgpu_ctx {
     DBuf<unsigned> order;               // 3D back projection: voxels in 16x16 tile order
     DBuf<unsigned long long> rp, cp;
     DBuf<uint2> A, C;
+    // compressed CSR for the 2D forward (C2, kernels.cuh): per-row header, 2-bit
+    // step codes, fp32 h; c2_ok = built and verified
+    DBuf<uint2> c2_rh;
+    DBuf<unsigned short> c2_codes;
+    DBuf<float> c2_h;
+    bool c2_ok = false;
     // data
     DBuf<float> d, I0, q;
     bool have_data = false;
@@ -292,6 +298,41 @@ static void finish_matrix(Ctx* c) {
         const bool want = e && e[0] == '1';
         const bool pow2 = c->nx >= 8 && (c->nx & (c->nx - 1)) == 0 && c->ny % 4 == 0;
         c->lgx = (want && pow2 && c->nz == 1) ? 31 - __builtin_clz((unsigned)c->nx) : -1;
+    }
+    // C2 compressed forward (2D only), OPT-IN (WAMGPU_C2=1): it halves the
+    // forward's DRAM bytes (1.96 vs 3.67 GB at cfg2) but the decode makes it
+    // slower (0.81 vs 0.68-0.70 ms, profiles/r01_fwd_patch_sweep.txt), so the
+    // uint2 CSR patch forward stays the default
+    c->c2_ok = false;
+    c->c2_rh.release(); c->c2_codes.release(); c->c2_h.release();
+    {
+        const char* e = std::getenv("WAMGPU_C2");
+        if (c->nz == 1 && c->Ml && e && e[0] == '1' && c->N < (1ull << 30)) {
+            DBuf<unsigned long long> nb;
+            nb.alloc(c->Ml + 1);
+            k_c2_count<<<blocks_for(c->Ml, 256), 256, 0, c->st>>>(c->Ml, c->rp.p, nb.p);
+            check_launch(c, "k_c2_count");
+            CK(cudaMemsetAsync(nb.p + c->Ml, 0, 8, c->st));
+            exclusive_scan_u64(c, nb.p, c->Ml + 1);
+            unsigned long long blocks = 0;
+            CK(cudaMemcpyAsync(&blocks, nb.p + c->Ml, 8, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            c->c2_codes.alloc(std::max<unsigned long long>(blocks, 1) * 8);
+            c->c2_rh.alloc(c->Ml);
+            c->c2_h.alloc(std::max<unsigned long long>(blocks, 1) * 64);
+            CK(cudaMemsetAsync(c->c2_h.p, 0, std::max<unsigned long long>(blocks, 1) * 64 * 4, c->st));
+            CK(cudaMemsetAsync(c->c2_codes.p, 0, std::max<unsigned long long>(blocks, 1) * 16, c->st));
+            CK(cudaMemsetAsync(c->flag.p, 0, 4, c->st));
+            k_c2_build<<<c->sms * 8, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, nb.p, c->c2_rh.p,
+                                                       c->c2_codes.p, c->c2_h.p, c->flag.p);
+            check_launch(c, "k_c2_build");
+            int bad = 0;
+            CK(cudaMemcpyAsync(&bad, c->flag.p, 4, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaMemsetAsync(c->flag.p, 0, 4, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            c->c2_ok = bad == 0;
+            if (!c->c2_ok) { c->c2_rh.release(); c->c2_codes.release(); c->c2_h.release(); }
+        }
     }
     c->cub_tmp.release();
     c->nblk_row = (int)std::max<uint64_t>(1, std::min<uint64_t>((c->Ml + 7) / 8, (uint64_t)c->sms * 16));
@@ -506,6 +547,9 @@ static void forward_plain(Ctx* c, const float* mu, double* l) {
             k_forward<0, FG_DEFAULT, 8, 1, true><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, mu, nullptr,
                                                                               nullptr, nullptr, l, nullptr, c->flag.p,
                                                                               c->lgx);
+        else if (c->c2_ok)
+            k_fwd_c2<0, 5><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->c2_rh.p, c->c2_codes.p, c->c2_h.p,
+                                                          c->nx, mu, nullptr, nullptr, nullptr, l, nullptr, c->flag.p);
         else
             k_fwd_patch<0, 4, 8, 5><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, mu, nullptr, nullptr,
                                                                    nullptr, l, nullptr, c->flag.p);
@@ -562,7 +606,16 @@ static void forward_fused(Ctx* c, bool record) {
             case 25: FP(4, 6, 5) break;
             case 26: FP(2, 8, 5) break;
             case 9: FV(1, 4, 8) break;    // round-1 default (row-per-warp)
-            default: FP(4, 8, 5) break;   // measured best at cfg2 (patch sweep, profiles/r01_fwd_patch_sweep.txt)
+#define FC2(MB)                                                                                                  \
+    if (c->c2_ok) k_fwd_c2<1, MB><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->c2_rh.p, c->c2_codes.p,       \
+                                                                  c->c2_h.p, c->nx, c->mu.p, c->I0.p, c->d.p,     \
+                                                                  c->q.p, nullptr, c->partial.p, c->flag.p);      \
+    else FP(4, 8, 5)
+            case 40: FC2(4) break;
+            case 41: FC2(6) break;
+            case 42: FC2(8) break;
+            default: FC2(5) break;        // C2 when built (WAMGPU_C2=1), else FP(4,8,5): the measured best
+#undef FC2
         }
 #undef FP
 #undef FV
