@@ -868,7 +868,6 @@ __global__ void k_mark(int nx, int ny, int L, const double* __restrict__ s, doub
 //        cnt[y] = number of negative fp32 phi of active detail coefficients
 // MODE 2 (fill): emit those entries (key = Mallat z, value = {ray, f32}) at pos[y]
 constexpr int WALK_WARPS = 4;
-constexpr int WALK_TREE_SMEM = 4096;  // level-L activity bytes staged in smem
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     const int sz = valid ? 8 : 0;
@@ -887,26 +886,20 @@ __device__ __forceinline__ void add_quad(double (&q)[4], int quad, double v) {
     q[3] += quad == 3 ? v : 0.0;
 }
 
-template <int MODE, int L>
+// Init walk (K8 at wam_init): the tree-independent approximation part of Z,
+// zA(y) = sum over the level-L blocks the ray crosses, in ray order, of
+// |phi_A| * cz (cz = 1 for the 2D model, c^L for the separable 3D one), with
+// phi_A = 2^-L ((TL + TR) + (BL + BR)) from the four sequential ray-order
+// quadrant sums.  L = 0: zA = sum |h| (Omega = I).  Thread per
+// ray; a warp's 32 rows are staged 32 entries per round with cp.async.
+template <int L>
 __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsigned long long* __restrict__ rp,
-                                                          const uint2* __restrict__ A, int nx, int ny,
-                                                          const uint8_t* __restrict__ act, ActOff off, double cz,
-                                                          double* __restrict__ zA, double* __restrict__ zrow,
-                                                          unsigned long long* __restrict__ cnt,
-                                                          const unsigned long long* __restrict__ pos,
-                                                          unsigned* __restrict__ keys, uint2* __restrict__ vals) {
+                                                          const uint2* __restrict__ A, int nx, double cz,
+                                                          double* __restrict__ zA, double* __restrict__ zrow) {
     __shared__ uint2 buf[WALK_WARPS][32][33];
-    __shared__ uint8_t treeL[WALK_TREE_SMEM];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint64_t y = ((uint64_t)blockIdx.x * WALK_WARPS + w) * 32 + lane;
-    const int WLv = (L > 0) ? (nx >> L) : nx, HLv = (L > 0) ? (ny >> L) : ny;
-    const int nL = WLv * HLv;
-    const bool tree_smem = (MODE != 0) && L > 0 && nL <= WALK_TREE_SMEM;
-    if (tree_smem) {
-        for (int i = threadIdx.x; i < nL; i += blockDim.x) treeL[i] = act[off.off[L] + i];
-        __syncthreads();
-    }
-    if (MODE == 1 && y == M) cnt[M] = 0;
+    const int WLv = (L > 0) ? (nx >> L) : nx;
     uint64_t lo = 0, hi = 0;
     if (y < M) { lo = rp[y]; hi = rp[y + 1]; }
     const unsigned long long len = hi - lo;
@@ -916,49 +909,15 @@ __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsi
     if (maxlen == 0 && y >= M) return;
     const bool pow2 = (nx & (nx - 1)) == 0;
     const int lgx = 31 - __clz(nx);
-
-    constexpr int NL = L + 1;
-    int cur[NL], cbi[NL], cbj[NL];
-    bool av[NL + 1];
-    double q[NL][4], tot[NL];
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-        cur[l] = -1; cbi[l] = cbj[l] = 0; av[l] = false; tot[l] = 0.0;
-        q[l][0] = q[l][1] = q[l][2] = q[l][3] = 0.0;
-    }
-    av[NL] = true;
+    int cur = -1;
+    double q[4] = {0.0, 0.0, 0.0, 0.0};
     double totA = 0.0;
-    unsigned long long count = 0, wp = (MODE == 2 && y < M) ? pos[y] : 0;
-
-    // block exit at level l (compile-time after unrolling)
-    auto flush = [&](int l) {
-        const double TL = q[l][0], TR = q[l][1], BL = q[l][2], BR = q[l][3];
-        const double st = TL + TR, sb = BL + BR;
-        const double sc = 1.0 / (double)(1 << l);
-        if (MODE == 0 && l == L) totA += fabs(((st + sb) * sc) * cz);
-        if (MODE != 0 && av[l]) {
-            const double pH = (st - sb) * sc, pV = ((TL + BL) - (TR + BR)) * sc, pD = ((TL + BR) - (TR + BL)) * sc;
-            if (MODE == 1) tot[l] += fabs(pH) + fabs(pV) + fabs(pD);
-            const int wl = nx >> l, hl = ny >> l;
-            const float v[3] = {(float)pH, (float)pV, (float)pD};
-            const unsigned z[3] = {(unsigned)((hl + cbi[l]) * nx + cbj[l]), (unsigned)(cbi[l] * nx + wl + cbj[l]),
-                                   (unsigned)((hl + cbi[l]) * nx + wl + cbj[l])};
-#pragma unroll
-            for (int s = 0; s < 3; ++s)
-                if (v[s] < 0.0f) {
-                    if (MODE == 1) ++count;
-                    else { keys[wp] = z[s]; vals[wp] = make_uint2((unsigned)y, __float_as_uint(v[s])); ++wp; }
-                }
-        }
-        q[l][0] = q[l][1] = q[l][2] = q[l][3] = 0.0;
-        cur[l] = -1;
-        av[l] = false;
+    constexpr double sc = 1.0 / (double)(1 << L);
+    auto flush = [&]() {
+        const double st = q[0] + q[1], sb = q[2] + q[3];
+        totA += fabs(((st + sb) * sc) * cz);
+        q[0] = q[1] = q[2] = q[3] = 0.0;
     };
-    auto is_act = [&](int l, int key) -> bool {
-        if (l == L && tree_smem) return treeL[key] != 0;
-        return act[off.off[l] + (uint64_t)key] != 0;
-    };
-
     for (unsigned long long base = 0; base < maxlen; base += 32) {
         for (int j = 0; j < 32; ++j) {
             const unsigned long long lj = __shfl_sync(0xffffffffu, lo, j);
@@ -972,63 +931,23 @@ __global__ void __launch_bounds__(32 * WALK_WARPS) k_walk(uint64_t M, const unsi
         for (int i = 0; i < n; ++i) {
             const uint2 e = buf[w][lane][i];
             const double h = hval(e);
-            if (L == 0) { if (MODE == 0) totA += fabs(h); continue; }
+            if (L == 0) { totA += fabs(h); continue; }
             int ix, iy;
             if (pow2) { ix = (int)(e.x & (unsigned)(nx - 1)); iy = (int)(e.x >> lgx); }
             else { iy = (int)(e.x / (unsigned)nx); ix = (int)(e.x % (unsigned)nx); }
-            if (MODE == 0) {
-                // approximation only: level-L quadrant sums of every crossed block
-                const int key = (iy >> L) * WLv + (ix >> L);
-                if (key != cur[L]) {
-                    if (cur[L] >= 0) flush(L);
-                    cur[L] = key;
-                }
-                add_quad(q[L], (((iy >> (L - 1)) & 1) << 1) | ((ix >> (L - 1)) & 1), h);
-                continue;
+            const int key = (iy >> L) * WLv + (ix >> L);
+            if (key != cur) {
+                if (cur >= 0) flush();
+                cur = key;
             }
-            // coarsest tracked level whose block changes at this cell
-            int m = 0;
-#pragma unroll
-            for (int l = L; l >= 1; --l) {
-                if (l < L && !av[l + 1]) break;       // untracked below an inactive block
-                const int key = (iy >> l) * (nx >> l) + (ix >> l);
-                if (key != cur[l]) { m = l; break; }
-            }
-            if (m) {
-#pragma unroll
-                for (int l = 1; l <= L; ++l)
-                    if (l <= m && cur[l] >= 0) flush(l);
-#pragma unroll
-                for (int l = L; l >= 1; --l) {
-                    if (l > m) continue;
-                    if (l < L && !av[l + 1]) break;
-                    cbi[l] = iy >> l; cbj[l] = ix >> l;
-                    cur[l] = cbi[l] * (nx >> l) + cbj[l];
-                    av[l] = is_act(l, cur[l]);
-                }
-            }
-#pragma unroll
-            for (int l = L; l >= 1; --l) {
-                if (!av[l]) break;                     // details only inside active blocks
-                add_quad(q[l], (((iy >> (l - 1)) & 1) << 1) | ((ix >> (l - 1)) & 1), h);
-            }
+            add_quad(q, (((iy >> (L - 1)) & 1) << 1) | ((ix >> (L - 1)) & 1), h);
         }
         __syncwarp();
     }
     if (y >= M) return;
-#pragma unroll
-    for (int l = 1; l <= L; ++l)
-        if (cur[l] >= 0) flush(l);
-    if (MODE == 0) {
-        zA[y] = totA;
-        zrow[y] = totA;
-    } else if (MODE == 1) {
-        double z = zA[y];
-#pragma unroll
-        for (int l = L; l >= 1; --l) z += tot[l];
-        zrow[y] = z;
-        cnt[y] = count;
-    }
+    if (L > 0 && cur >= 0) flush();
+    zA[y] = totA;
+    zrow[y] = totA;
 }
 
 // Fixed-point Z(y) (pin P8): int64 multiples of 2^-32, every term rounded UP.

@@ -105,7 +105,7 @@ struct wamgpu_ctx {
     int algo = 0;  // 1 AM, 2 WAM
     DBuf<float> mu, beta, fscratch;
     DBuf<double> g, bdata, bam, mu64, bp_dbg, bm_dbg, zrow, dscratch;
-    DBuf<unsigned long long> wcnt;      // per-(ray, level) Phi^- counts (MODE 1 walk; z-row diagnostics)
+    DBuf<unsigned long long> wcnt;      // separable 3D: per-(ray, level) Psi counts of the walk
     DBuf<unsigned long long> cursor;    // Phi^- emission cursor of the expansion walk
     DBuf<long long> zfix, zfix2;        // 2D tree: per-ray Z(y) in 2^-32 fixed point (pin P8)
     DBuf<ulonglong2> cols;              // 2D tree: Phi^- range [lo, hi) of column z inside E
@@ -652,15 +652,12 @@ static double device_max(Ctx* c, const double* v, uint64_t n) {
     return m;
 }
 
-template <int MODE>
-static void launch_walk(Ctx* c, int L, unsigned long long* cnt, const unsigned long long* pos, unsigned* keys,
-                        uint2* vals) {
+static void launch_walk(Ctx* c, int L) {
     const unsigned nb = blocks_for(c->Ml + 1, 32 * WALK_WARPS);
 #define WALK_CASE(LV)                                                                                        \
     case LV:                                                                                                 \
-        k_walk<MODE, LV><<<nb, 32 * WALK_WARPS, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->act.p, \
-                                                             c->off, c->haar3 ? cpow3_host(LV) : 1.0, c->zA.p,  \
-                                                             c->zrow.p, cnt, pos, keys, vals);                 \
+        k_walk<LV><<<nb, 32 * WALK_WARPS, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx,                        \
+                                                      c->haar3 ? cpow3_host(LV) : 1.0, c->zA.p, c->zrow.p); \
         break;
     switch (L) {
         WALK_CASE(0) WALK_CASE(1) WALK_CASE(2) WALK_CASE(3) WALK_CASE(4) WALK_CASE(5)
@@ -826,14 +823,14 @@ static void rebuild_psi3(Ctx* c, int nlev) {
 
 // Z0 = max_y sum_{z active} |phi(y|z)| (Eq. 1.61).  init: the approximation part
 // (tree-independent, cached in zA); AM: levels = 0 -> row sums.
+// (The 2D tree's Z(y) is kept incrementally in fixed point by phi_append; the
+// non-init path here is the separable 3D model's.)
 static double compute_z0(Ctx* c, int levels, bool init) {
-    const uint64_t ncnt = (uint64_t)c->Ml * std::max(levels, 1) + 1;
-    c->wcnt.ensure(ncnt);
     c->zA.ensure(c->Ml + 1);
     if (init) {
-        CK(cudaMemsetAsync(c->wcnt.p, 0, ncnt * 8, c->st));
-        if (c->Ml) launch_walk<0>(c, levels, nullptr, nullptr, nullptr, nullptr);
+        if (c->Ml) launch_walk(c, levels);
     } else if (c->Ml && c->haar3) {
+        c->wcnt.ensure((uint64_t)c->Ml * std::max(levels, 1) + 1);
         int nlev = 1;
         upload_tree3(c, &nlev);
         c->walk_nlev = nlev;
