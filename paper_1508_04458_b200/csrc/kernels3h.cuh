@@ -497,4 +497,119 @@ __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __
     }
 }
 
+// k_split3h with E Psi entries in flight per warp: 32/E lanes per entry, each
+// lane owning S = SPL*E consecutive slices (S/2 slice pairs).  The per-entry
+// multipliers are computed by 32/E lanes instead of 32 (fp64 work per slice
+// roughly halves at E = 4); the E entry groups' partials are combined by a
+// fixed xor butterfly, then per-block sums as in k_split3h.
+template <int SPL, int E>
+__global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* __restrict__ list, int nx, int ny,
+                                                   int nzl, const unsigned long long* __restrict__ ptr,
+                                                   const unsigned* __restrict__ eray, const float4* __restrict__ epsi,
+                                                   const float* __restrict__ q, const uint8_t* __restrict__ act,
+                                                   ActOff off, ActOff koff, double* __restrict__ bm) {
+    constexpr int P = 32 * SPL, LPE = 32 / E, S = SPL * E, NG = S / 2;
+    static_assert(S >= 2 && S % 4 == 0, "slices per lane: a multiple of 4");
+    __shared__ double red[4][7][P / 2];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, grp = lane / LPE, j = lane % LPE;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nlist; it += W) {
+        const unsigned b = list[it].x;
+        const int l = (int)list[it].y;
+        const double cl = cpow3(l);
+        const uint64_t key = koff.off[l] + b;
+        double acc[NG][7];
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+#pragma unroll
+            for (int t = 0; t < 7; ++t) acc[g][t] = 0.0;
+        constexpr int U = 2;
+        const uint64_t e0 = ptr[key], e1 = ptr[key + 1];
+        for (uint64_t e = e0; e < e1; e += (uint64_t)E * U) {
+            unsigned yv[U];
+            float4 ps[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t ee = e + grp + (uint64_t)E * u;
+                const bool ok = ee < e1;
+                const uint64_t ei = ok ? ee : e0;   // always a valid index
+                yv[u] = __ldg(eray + ei);
+                ps[u] = ok ? __ldg(epsi + ei) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            float4 qv[U][S / 4];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int v = 0; v < S / 4; ++v)
+                    qv[u][v] = __ldg(reinterpret_cast<const float4*>(q + (uint64_t)yv[u] * P + j * S) + v);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const double pA = (double)ps[u].x * cl, pH = (double)ps[u].y * cl, pV = (double)ps[u].z * cl,
+                             pD = (double)ps[u].w * cl;
+                const double lowm[3] = {fmin(pH, 0.0), fmin(pV, 0.0), fmin(pD, 0.0)};
+                const double hp[4] = {pA, pH, pV, pD};
+                double mlo[4], mhi[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) { mlo[t] = fmin(hp[t], 0.0); mhi[t] = -fmax(hp[t], 0.0); }
+                float f[S];
+#pragma unroll
+                for (int v = 0; v < S / 4; ++v) {
+                    f[4 * v] = qv[u][v].x; f[4 * v + 1] = qv[u][v].y; f[4 * v + 2] = qv[u][v].z; f[4 * v + 3] = qv[u][v].w;
+                }
+                if (l >= 2) {
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        const int sl = j * S + 2 * g;
+                        const bool hh = ((sl >> (l - 1)) & 1) != 0;
+                        const double qq = (double)f[2 * g] + (double)f[2 * g + 1];
+#pragma unroll
+                        for (int t = 0; t < 3; ++t) acc[g][t] = fma(lowm[t], qq, acc[g][t]);
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) acc[g][3 + t] = fma(hh ? mhi[t] : mlo[t], qq, acc[g][3 + t]);
+                    }
+                } else {   // l == 1: a pair is one z-block (low half, high half)
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        const double q0 = (double)f[2 * g], q1 = (double)f[2 * g + 1], qq = q0 + q1;
+#pragma unroll
+                        for (int t = 0; t < 3; ++t) acc[g][t] = fma(lowm[t], qq, acc[g][t]);
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) acc[g][3 + t] = fma(mhi[t], q1, fma(mlo[t], q0, acc[g][3 + t]));
+                    }
+                }
+            }
+        }
+        // combine the E entry groups (same slices: lanes j, j+LPE, ...), fixed order
+#pragma unroll
+        for (int o = LPE; o < 32; o <<= 1)
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
+#pragma unroll
+                for (int t = 0; t < 7; ++t) acc[g][t] += __shfl_xor_sync(0xffffffffu, acc[g][t], o);
+        if (grp == 0) {
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
+#pragma unroll
+                for (int t = 0; t < 7; ++t) red[wib][t][j * NG + g] = acc[g][t];
+        }
+        __syncwarp();
+        const int nk = nzl >> l, hl = ny >> l, wl = nx >> l, dl = nk;
+        const int bi = (int)(b / wl), bj = (int)(b % wl);
+        for (int k = lane; k < nk; k += 32) {
+            if (!act[off.off[l] + ((uint64_t)k * hl + bi) * wl + bj]) continue;
+            const int zz[7] = {k, k, k, dl + k, dl + k, dl + k, dl + k};
+            const int yy[7] = {hl + bi, bi, hl + bi, bi, hl + bi, bi, hl + bi};
+            const int xx[7] = {bj, wl + bj, wl + bj, bj, bj, wl + bj, wl + bj};
+            const int g0 = (k << l) / 2, g1 = ((k + 1) << l) / 2;
+#pragma unroll
+            for (int t = 0; t < 7; ++t) {
+                double sum = 0.0;
+                for (int gg = g0; gg < g1; ++gg) sum += red[wib][t][gg];
+                bm[((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]] = sum;
+            }
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace wamgpu

@@ -126,6 +126,7 @@ struct wamgpu_ctx {
     ActOff zoff{}, koff{};              // word offset of level l in zbits; key offset of level l
     uint64_t nkeys3 = 0;
     DBuf<unsigned> E3ray, pray_s;
+    DBuf<uint2> sidx3;                  // Psi sort output (persistent)
     DBuf<float4> E3psi, ppsi_s;
     DBuf<uint2> list3;                  // (in-plane block, level) with any active z-block
     uint64_t nlist3 = 0;
@@ -189,6 +190,23 @@ struct wamgpu_ctx {
 
 namespace wamgpu {
 using Ctx = ::wamgpu_ctx;
+
+static double host_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static bool trace_host() {
+    static const bool on = std::getenv("WAMGPU_TRACE_HOST") != nullptr;
+    return on;
+}
+#define HTRACE(label)                                                                  \
+    do {                                                                               \
+        if (trace_host()) {                                                            \
+            CK(cudaStreamSynchronize(c->st));                                          \
+            const double t_ = host_ms();                                               \
+            std::fprintf(stderr, "[wamgpu] %-28s %8.3f ms\n", label, t_ - c->t_trace); \
+            c->t_trace = t_;                                                           \
+        }                                                                              \
+    } while (0)
 
 static thread_local std::string g_err;
 
@@ -805,8 +823,12 @@ static void rebuild_psi3(Ctx* c, int nlev) {
     const uint64_t n1 = std::max<uint64_t>(tot, 1);
     c->kin_s.ensure(n1); c->vin_s.ensure(n1); c->pray_s.ensure(n1); c->ppsi_s.ensure(n1);
     if (tot) launch_walk3h<2>(c, nlev, nullptr, c->wcnt.p);
-    DBuf<uint2> sidx;
+    HTRACE("expand3: Psi count scan + emit walk");
+    // persistent sort output: a per-call buffer meant a GB-sized cudaMalloc +
+    // cudaFree (which synchronizes) in every expansion
+    DBuf<uint2>& sidx = c->sidx3;
     sort_pairs(c, c->kin_s, c->vin_s, c->kout_s, sidx, tot, c->nkeys3);
+    HTRACE("expand3: Psi sort");
     c->E3ray.ensure_padded(n1);
     c->E3psi.ensure_padded(n1);
     if (tot) {
@@ -1083,22 +1105,6 @@ static void z0_from_zfix(Ctx* c) {
 // fixed-point Z; the batch is radix-sorted by z straight into E after the
 // existing entries, and k_cols_set records each new column's [lo, hi).  Within
 // a column the ray order is arbitrary: the split sums in exact fixed point.
-static double host_ms() {
-    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
-static bool trace_host() {
-    static const bool on = std::getenv("WAMGPU_TRACE_HOST") != nullptr;
-    return on;
-}
-#define HTRACE(label)                                                                  \
-    do {                                                                               \
-        if (trace_host()) {                                                            \
-            CK(cudaStreamSynchronize(c->st));                                          \
-            const double t_ = host_ms();                                               \
-            std::fprintf(stderr, "[wamgpu] %-28s %8.3f ms\n", label, t_ - c->t_trace); \
-            c->t_trace = t_;                                                           \
-        }                                                                              \
-    } while (0)
 
 static void phi_append(Ctx* c) {
     // active detail list from the host tree (level by level, the H, V, D of a
@@ -1290,7 +1296,17 @@ static void wam_step(Ctx* c) {
         double* bm3 = c->g.p + NV(c);
 #define S3H(S) k_split3h<S><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p, c->E3ray.p, \
                                                    c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3);
-        switch (spl_of(c)) { case 1: S3H(1) break; case 2: S3H(2) break; default: S3H(4) break; }
+#define S3E(S, EE) k_split3h_e<S, EE><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p,   \
+                                                             c->E3ray.p, c->E3psi.p, c->q.p, c->act.p, c->off,      \
+                                                             c->koff, bm3);
+        if (c->split_variant == 1) {
+            switch (spl_of(c)) { case 1: S3H(1) break; case 2: S3H(2) break; default: S3H(4) break; }
+        } else if (c->split_variant == 2) {
+            switch (spl_of(c)) { case 1: S3E(1, 8) break; case 2: S3E(2, 2) break; default: S3E(4, 2) break; }
+        } else {
+            switch (spl_of(c)) { case 1: S3E(1, 4) break; case 2: S3E(2, 4) break; default: S3E(4, 4) break; }
+        }
+#undef S3E
 #undef S3H
         check_launch(c, "k_split3h");
         c->timer_end(T_SPLIT);
@@ -1374,9 +1390,13 @@ static int64_t wam_expand(Ctx* c, double factor) {
             for (uint64_t i = 0; i < c->act_bytes; ++i) newly += (h[i] != 0) - (c->act_host[i] != 0);
             c->act_host.swap(h);
             if (newly > 0) {
+                HTRACE("expand3: criterion + mark");
                 c->Z0 = compute_z0(c, c->L, false);
+                HTRACE("expand3: Z walk + Z0");
                 rebuild_psi3(c, c->walk_nlev);
+                HTRACE("expand3: Psi rebuild");
                 c->active = count_active(c);
+                HTRACE("expand3: count active");
             }
         }
         c->timer_end(T_EXPAND);

@@ -10,6 +10,8 @@ cfg = configs.get(sys.argv[1] if len(sys.argv) > 1 else "cfg2")
 g, I0, d = bench._inputs(cfg, W)
 ctx = W.Context(0)
 ctx.set_geometry(g)
+if cfg["nz"] > 1:
+    ctx.set_haar_dim(cfg["haar"])
 ctx.set_data(d, I0)
 for rep in range(2):
     t0 = time.perf_counter(); ctx.wam_init(cfg["L"]); t1 = time.perf_counter()
