@@ -1303,8 +1303,8 @@ static void wam_step(Ctx* c) {
             switch (spl_of(c)) { case 1: S3H(1) break; case 2: S3H(2) break; default: S3H(4) break; }
         } else if (c->split_variant == 2) {
             switch (spl_of(c)) { case 1: S3E(1, 8) break; case 2: S3E(2, 2) break; default: S3E(4, 2) break; }
-        } else {
-            switch (spl_of(c)) { case 1: S3E(1, 4) break; case 2: S3E(2, 4) break; default: S3E(4, 4) break; }
+        } else {   // measured: cfg3 (64 slices) E=4 188 ms/run vs 364; cfg4 (128) E=2 1888 vs 2157 (E=4) / 2500
+            switch (spl_of(c)) { case 1: S3E(1, 4) break; case 2: S3E(2, 4) break; default: S3E(4, 2) break; }
         }
 #undef S3E
 #undef S3H
