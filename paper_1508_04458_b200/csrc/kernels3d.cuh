@@ -65,6 +65,257 @@ __device__ __forceinline__ void slab_dot(const uint2* __restrict__ A, const floa
     }
 }
 
+// ------------------------------------------------------------ slab SpMM v2
+// ncu of slab_dot (profiles/r02_ncu_3d.txt): the XU pipe is 85% busy.  Every
+// update converts its fp32 slab value to fp64 with F2F.F64.F32, which runs at
+// 4 lanes/clk/SMSP on the XU pipe, and the broadcast h takes one more per
+// entry.  v2 removes most of them without changing one bit of the result:
+//  * h is converted once per staged entry (per-warp smem), not per lane;
+//  * a slab value f is moved into fp64 by integer bit moves, exactly:
+//    f2d_scaled(f) = f * 2^-896 for every finite f (normal, zero, denormal:
+//    f32 denormals land on fp64 denormals with the same mantissa), and
+//    fma(h * 2^896, f2d_scaled(f), acc) == fma(h, (double)f, acc) bit for bit
+//    (both products are exactly h*f; FMA rounds once).  NF of every 4 values
+//    still take F2F so the XU and ALU pipes share the conversions.
+//  * a warp owns G = 32/LPR adjacent rays (voxels), LPR lanes x SPL slices
+//    each, stepped in lockstep so neighbouring rays meet the same slab lines
+//    close together in time (L1 reuse).
+// Summation stays sequential per (ray, slice) in Siddon / CSC order.
+template <bool SIGNED>
+__device__ __forceinline__ double f2d_scaled(float f) {
+    const unsigned u = __float_as_uint(f);
+    const unsigned hi = SIGNED ? (((u & 0x7fffffffu) >> 3) | (u & 0x80000000u)) : (u >> 3);
+    return __hiloint2double((int)hi, (int)(u << 29));
+}
+constexpr double kTwo896 = 0x1p896;
+
+template <int SPL> struct SlabLd {  // SPL consecutive floats as vector loads
+    static constexpr int NV = SPL >= 4 ? SPL / 4 : 1;
+    using T = typename SlabVec<(SPL >= 4 ? 4 : SPL)>::T;
+};
+// Lane-to-slice map of the v2 kernels.  SPL <= 2: lane lig owns the SPL
+// consecutive slices lig*SPL.. (one load).  SPL >= 4: load i of lane lig is
+// the float4 at slice 4*LPR*i + 4*lig, so each load instruction of a group
+// covers one contiguous 16*LPR-byte run (full sectors, no sector fetched twice).
+template <int LPR, int SPL>
+__device__ __forceinline__ int slab_slice(int lig, int j) {
+    return SPL >= 4 ? (j / 4) * 4 * LPR + 4 * lig + (j % 4) : lig * SPL + j;
+}
+template <int LPR, int SPL>
+__device__ __forceinline__ void slab_load(const float* p, typename SlabLd<SPL>::T (&v)[SlabLd<SPL>::NV]) {
+#pragma unroll
+    for (int i = 0; i < SlabLd<SPL>::NV; ++i)
+        v[i] = __ldg(reinterpret_cast<const typename SlabLd<SPL>::T*>(p + (SPL >= 4 ? 4 * LPR * i : 0)));
+}
+template <int SPL>
+__device__ __forceinline__ void slab_unpack(const typename SlabLd<SPL>::T (&v)[SlabLd<SPL>::NV], float (&f)[SPL]) {
+    if constexpr (SPL >= 4) {
+#pragma unroll
+        for (int i = 0; i < SPL / 4; ++i) { f[4 * i] = v[i].x; f[4 * i + 1] = v[i].y; f[4 * i + 2] = v[i].z; f[4 * i + 3] = v[i].w; }
+    } else {
+        float t[SPL];
+        unpack(v[0], t);
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) f[j] = t[j];
+    }
+}
+
+// per-warp staging: 2 chunk buffers x G groups x K entries (K = 32, 16 for
+// G = 8 to stay in 48 KB of static smem per CTA); strides K+4 / K+2 keep the
+// G 16-byte broadcasts of a load in distinct bank quads
+template <int G> struct SlabStage {
+    static constexpr int K = G >= 8 ? 16 : 32, CS = K + 4, HS = K + 2;
+    unsigned c[2][G][CS];
+    double h[2][G][HS];
+};
+
+// acc[j] = sum over entries [lo, hi) of h_k x[idx_k*P + lig*SPL + j]; the
+// warp-uniform maxlen is the longest of the warp's G segments (shorter ones
+// are padded with h = 0, idx = 0: an exact no-op for finite x).
+// Software pipeline: the U gathers of round r+1 are issued before round r is
+// consumed (a loop-carried register set, so ptxas cannot sink them), and the
+// chunk after the current one is staged into the other smem buffer from
+// registers prefetched a whole chunk ahead.
+template <int LPR, int SPL, int U, int NF, bool SIGNED, int P>
+__device__ __forceinline__ void slab_dot_g(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
+                                           uint64_t hi, int maxlen, int lig, int g,
+                                           SlabStage<32 / LPR>& st, double (&acc)[SPL]) {
+    constexpr int kSlabK = SlabStage<32 / LPR>::K, NL = kSlabK / LPR, RPC = kSlabK / U;
+    static_assert(kSlabK % U == 0 && U % 4 == 0 && NL >= 1, "unroll");
+    using L = SlabLd<SPL>;
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) acc[j] = 0.0;
+    if (maxlen <= 0) return;
+    const float* xl = x + slab_slice<LPR, SPL>(lig, 0);
+    uint2 nx[NL];
+    auto fetch = [&](int base) {
+#pragma unroll
+        for (int t = 0; t < NL; ++t) {
+            const uint64_t k = lo + base + lig + LPR * t;
+            nx[t] = k < hi ? ld_stream(A + k) : make_uint2(0u, 0u);
+        }
+    };
+    auto stage = [&](int buf) {
+#pragma unroll
+        for (int t = 0; t < NL; ++t) {
+            st.c[buf][g][lig + LPR * t] = nx[t].x;
+            st.h[buf][g][lig + LPR * t] = (double)__uint_as_float(nx[t].y);
+        }
+    };
+    typename L::T v[U][L::NV];
+    double h[U];
+    auto issue = [&](int buf, int j0) {   // gathers of the round at entries j0.. of buffer buf
+        const unsigned* sc = st.c[buf][g];
+        const double* sh = st.h[buf][g];
+#pragma unroll
+        for (int u = 0; u < U; u += 4) {
+            const uint4 c4 = *reinterpret_cast<const uint4*>(sc + j0 + u);
+            const double2 h01 = *reinterpret_cast<const double2*>(sh + j0 + u);
+            const double2 h23 = *reinterpret_cast<const double2*>(sh + j0 + u + 2);
+            h[u] = h01.x; h[u + 1] = h01.y; h[u + 2] = h23.x; h[u + 3] = h23.y;
+            slab_load<LPR, SPL>(xl + (uint64_t)c4.x * P, v[u]);
+            slab_load<LPR, SPL>(xl + (uint64_t)c4.y * P, v[u + 1]);
+            slab_load<LPR, SPL>(xl + (uint64_t)c4.z * P, v[u + 2]);
+            slab_load<LPR, SPL>(xl + (uint64_t)c4.w * P, v[u + 3]);
+        }
+    };
+    fetch(0);
+    __syncwarp();
+    stage(0);
+    if (kSlabK < maxlen) fetch(kSlabK);
+    __syncwarp();
+    issue(0, 0);
+    const int nr = (maxlen + U - 1) / U;
+    // (an explicit two-set ping-pong without these copies was measured slower:
+    // 156 registers uncapped, 8.77 vs 8.04 ms at cfg5 with a 128 cap)
+    for (int r = 0; r < nr; ++r) {
+        typename L::T vc[U][L::NV];
+        double hc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            hc[u] = h[u];
+#pragma unroll
+            for (int i = 0; i < L::NV; ++i) vc[u][i] = v[u][i];
+        }
+        const int r1 = r + 1;
+        if (r1 < nr) {
+            const int chunk = r1 / RPC, j0 = (r1 % RPC) * U;
+            if (j0 == 0) {   // first round of a new chunk: stage it, prefetch the one after
+                stage(chunk & 1);
+                if ((chunk + 1) * kSlabK < maxlen) fetch((chunk + 1) * kSlabK);
+                __syncwarp();
+            }
+            issue(chunk & 1, j0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            float f[SPL];
+            slab_unpack<SPL>(vc[u], f);
+            const double hs = hc[u] * kTwo896;
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) {
+                if (((u * SPL + j) & 3) < NF) acc[j] = fma(hc[u], (double)f[j], acc[j]);
+                else acc[j] = fma(hs, f2d_scaled<SIGNED>(f[j]), acc[j]);
+            }
+        }
+    }
+}
+
+// K2 3D v2: one warp = G adjacent rays (groups of LPR lanes); MODE as k_forward3.
+// The warp covers LPR*SPL slices of the stride-P slab per part and loops over
+// the P/(LPR*SPL) parts (the ray's entries are re-read from L1/L2 per part).
+template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P>
+__global__ void __launch_bounds__(256) k_fwd3s(uint64_t M, int nz, const unsigned long long* __restrict__ rp,
+                                               const uint2* __restrict__ A, const float* __restrict__ mu,
+                                               const float* __restrict__ I0, const float* __restrict__ d,
+                                               float* __restrict__ q, double* __restrict__ lout,
+                                               double* __restrict__ partial, int* __restrict__ flag) {
+    constexpr int G = 32 / LPR, SB = LPR * SPL;
+    static_assert(P % SB == 0, "slab parts");
+    __shared__ __align__(16) SlabStage<G> s_st[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, g = lane / LPR, lig = lane % LPR;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    double tacc = 0.0;
+    for (uint64_t y0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + wib) * G; y0 < M; y0 += W * G)
+    for (int s0 = 0; s0 < nz; s0 += SB) {
+        const uint64_t y = y0 + g;
+        const bool ok = y < M;
+        const uint64_t lo = ok ? rp[y] : 0, hi = ok ? rp[y + 1] : 0;
+        const int maxlen = (int)__reduce_max_sync(0xffffffffu, (unsigned)(hi - lo));
+        double acc[SPL];
+        slab_dot_g<LPR, SPL, U, NF, SIGNED, P>(A, mu + s0, lo, hi, maxlen, lig, g, s_st[wib], acc);
+        if (!ok) continue;
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+            const int s = s0 + slab_slice<LPR, SPL>(lig, j);
+            if (s >= nz) continue;
+            const uint64_t id = y * P + s;
+            if (!isfinite(acc[j])) atomicOr(flag, 1);
+            if (MODE == 0) {
+                lout[id] = acc[j];
+            } else {
+                const double qq = (double)I0[id] * exp(-acc[j]);
+                q[id] = (float)qq;
+                tacc += idiv_term((double)d[id], qq);
+            }
+        }
+    }
+    if (MODE == 1) {
+        __shared__ double sm[32];
+        double v = tacc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) sm[wib] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sm[w];
+            partial[blockIdx.x] = t;
+        }
+    }
+}
+
+// K3 3D v2: one warp = G voxels of the tile order; MODE as k_back3.
+template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P>
+__global__ void __launch_bounds__(256) k_back3s(uint64_t N, int nz, const unsigned* __restrict__ order,
+                                                const unsigned long long* __restrict__ cp,
+                                                const uint2* __restrict__ C, const float* __restrict__ w,
+                                                double* __restrict__ g, const double* __restrict__ bam,
+                                                float* __restrict__ mu, double Z0, int* __restrict__ flag) {
+    constexpr int G = 32 / LPR, SB = LPR * SPL;
+    static_assert(P % SB == 0, "slab parts");
+    __shared__ __align__(16) SlabStage<G> s_st[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, gr = lane / LPR, lig = lane % LPR;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + wib) * G; i0 < N; i0 += W * G)
+    for (int s0 = 0; s0 < nz; s0 += SB) {
+        const uint64_t i = i0 + gr;
+        const bool ok = i < N;
+        const uint64_t x = ok ? (order ? order[i] : i) : 0;
+        const uint64_t lo = ok ? cp[x] : 0, hi = ok ? cp[x + 1] : 0;
+        const int maxlen = (int)__reduce_max_sync(0xffffffffu, (unsigned)(hi - lo));
+        double acc[SPL];
+        slab_dot_g<LPR, SPL, U, NF, SIGNED, P>(C, w + s0, lo, hi, maxlen, lig, gr, s_st[wib], acc);
+        if (!ok) continue;
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+            const int s = s0 + slab_slice<LPR, SPL>(lig, j);
+            if (s >= nz) continue;
+            const uint64_t id = x * P + s;
+            if (MODE == 0) {
+                g[id] = acc[j];
+            } else {
+                const double b = bam[id], c = acc[j];
+                if (b > 0.0 && c > 0.0) {
+                    const double v = (double)mu[id] + log(c / b) / Z0;
+                    if (!isfinite(v)) atomicOr(flag, 2);
+                    mu[id] = (float)((0.0 < v) ? v : 0.0);
+                }
+            }
+        }
+    }
+}
+
 // K2 3D: l[y][s] = sum_x h(y|x) mu[x][s]; MODE 0 writes l (fp64, [y][s]);
 // MODE 1 fuses q = fp32(I0 exp(-l)) and the fp64 I-divergence partial.
 template <int MODE, int SPL>

@@ -145,6 +145,8 @@ struct wamgpu_ctx {
     int fwd_variant = 0, back_variant = 0;  // SpMV tuning knobs (WAMGPU_FWD_VARIANT / WAMGPU_BACK_VARIANT)
     int split_variant = 0;                  // WAMGPU_SPLIT_VARIANT
     int walk_variant = 0;                   // WAMGPU_WALK_VARIANT
+    int slab_variant = 112;                 // WAMGPU_SLAB_VARIANT (3D slab SpMM)
+    bool mu_nonneg = false;                 // AM: mu has no sign bit set (see am_init)
     double t_trace = 0.0;                   // WAMGPU_TRACE_HOST phase clock
     // fused back projection + all-reduce over NVLink peer memory (kernels_ar.cuh)
     struct {
@@ -476,9 +478,108 @@ static unsigned nblk_warp(const Ctx* c, uint64_t n) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, (uint64_t)c->sms * 16));
 }
 
+// 3D slab SpMM launches (kernels3d.cuh).  WAMGPU_SLAB_VARIANT picks the
+// conversion share NF (of 4 values, F2F; the rest by bit moves) of the v2
+// kernel (SLAB_LPR lanes per ray, 4 gathers per round):
+//   12 = NF 3 (default), 3 = NF 2, 8 = NF 0, 9 = NF 4, 11 = NF 1;
+//   1 = round-1 k_forward3/k_back3 (warp per ray, shuffles, F2F only).
+// Variant + 100 (default 112): the unsigned bit move for vectors known to be
+// non-negative.  cfg5 sweep (profiles/r02_slab_sweep.txt): 1 -> 11.3 ms per
+// pass, 9 -> 8.45, 12 -> 8.25, 112 -> 8.04 (forward) / 7.89 (back).
+// Lanes per ray: 8 for P <= 64 (4 rays per warp), 16 for P = 128 (2 rays per
+// warp; 8 slices per lane either way at P >= 64).
+#define SLAB_LPR (SPL == 4 ? 16 : 8)
+#define SLAB_SWITCH(X, V)                                                                                          \
+    switch (V) {                                                                                                   \
+        case 3: X(SLAB_LPR, P / SLAB_LPR, 4, 2) break;                                                             \
+        case 8: X(SLAB_LPR, P / SLAB_LPR, 4, 0) break;                                                             \
+        case 9: X(SLAB_LPR, P / SLAB_LPR, 4, 4) break;                                                             \
+        case 11: X(SLAB_LPR, P / SLAB_LPR, 4, 1) break;                                                            \
+        default: X(SLAB_LPR, P / SLAB_LPR, 4, 3) break;                                                            \
+    }
+template <int MODE, int SPL>
+static unsigned fwd3_launch_s(Ctx* c, const float* mu, double* l, unsigned maxblk, bool nonneg) {
+    constexpr int P = 32 * SPL;
+    unsigned nb = 0;
+    const int v = c->slab_variant % 100;
+    const bool uns = nonneg && c->slab_variant >= 100;
+    if (v == 1) {
+        nb = std::min<unsigned>(nblk_warp(c, c->Ml), maxblk);
+        k_forward3<MODE, SPL><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l,
+                                                     c->partial.p, c->flag.p);
+        return nb;
+    }
+#define FX(LPR, S2, U, NF)                                                                                         \
+    {                                                                                                              \
+        constexpr int G = 32 / LPR;                                                                                \
+        nb = std::min<unsigned>(nblk_warp(c, (c->Ml + G - 1) / G), maxblk);                                        \
+        if (uns)                                                                                                   \
+            k_fwd3s<MODE, LPR, S2, U, NF, false, P><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu,     \
+                                                                          c->I0.p, c->d.p, c->q.p, l, c->partial.p, \
+                                                                          c->flag.p);                             \
+        else                                                                                                       \
+            k_fwd3s<MODE, LPR, S2, U, NF, true, P><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu,      \
+                                                                         c->I0.p, c->d.p, c->q.p, l, c->partial.p, \
+                                                                         c->flag.p);                              \
+    }
+    SLAB_SWITCH(FX, v)
+#undef FX
+    return nb;
+}
+// nonneg: the caller guarantees mu >= 0 (AM iterate: mu starts at 0 and every
+// update clamps at 0)
+template <int MODE>
+static unsigned fwd3_launch(Ctx* c, const float* mu, double* l, unsigned maxblk, bool nonneg) {
+    unsigned nb = 0;
+    switch (spl_of(c)) {
+        case 1: nb = fwd3_launch_s<MODE, 1>(c, mu, l, maxblk, nonneg); break;
+        case 2: nb = fwd3_launch_s<MODE, 2>(c, mu, l, maxblk, nonneg); break;
+        default: nb = fwd3_launch_s<MODE, 4>(c, mu, l, maxblk, nonneg); break;
+    }
+    check_launch(c, "k_fwd3s");
+    return nb;
+}
+template <int SPL>
+static void back3_launch_s(Ctx* c, const float* w, double* out, const double* bam, bool nonneg) {
+    constexpr int P = 32 * SPL;
+    const int v = c->slab_variant % 100;
+    const bool uns = nonneg && c->slab_variant >= 100;
+    if (v == 1) {
+        const unsigned nb = nblk_warp(c, c->N);
+        if (bam) k_back3<1, SPL><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p, w, nullptr, bam,
+                                                        c->mu.p, c->Z0, c->flag.p);
+        else k_back3<0, SPL><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p, w, out, nullptr,
+                                                    nullptr, 0.0, c->flag.p);
+        return;
+    }
+#define BX1(LPR, S2, U, NF, SG)                                                                                    \
+    {                                                                                                              \
+        constexpr int G = 32 / LPR;                                                                                \
+        const unsigned nb = nblk_warp(c, (c->N + G - 1) / G);                                                      \
+        if (bam) k_back3s<1, LPR, S2, U, NF, SG, P><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p,      \
+                                                                          c->C.p, w, nullptr, bam, c->mu.p, c->Z0, \
+                                                                          c->flag.p);                             \
+        else k_back3s<0, LPR, S2, U, NF, SG, P><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p,  \
+                                                                      w, out, nullptr, nullptr, 0.0, c->flag.p);  \
+    }
+#define BX(LPR, S2, U, NF)                                                                                         \
+    if (uns) BX1(LPR, S2, U, NF, false) else BX1(LPR, S2, U, NF, true)
+    SLAB_SWITCH(BX, v)
+#undef BX
+#undef BX1
+}
+// nonneg: w >= 0 (the iteration's q and d; not the public back_project)
+static void back3_launch(Ctx* c, const float* w, double* out, const double* bam, bool nonneg) {
+    switch (spl_of(c)) {
+        case 1: back3_launch_s<1>(c, w, out, bam, nonneg); break;
+        case 2: back3_launch_s<2>(c, w, out, bam, nonneg); break;
+        default: back3_launch_s<4>(c, w, out, bam, nonneg); break;
+    }
+}
+
 // g = H^T w (fp64).  2D: CSC gather; 3D: slab gather over the tile-ordered voxels.
 // am != nullptr: fused AM update of mu instead of writing g.
-static void back_launch(Ctx* c, const float* w, double* out, const double* bam) {
+static void back_launch(Ctx* c, const float* w, double* out, const double* bam, bool nonneg = true) {
     c->timer_begin(T_BACK);
     if (c->nzl == 1) {
 #define BV(U, MB)                                                                                                 \
@@ -508,20 +609,16 @@ static void back_launch(Ctx* c, const float* w, double* out, const double* bam) 
         }
 #undef BV
     } else {
-        const unsigned nb = nblk_warp(c, c->N);
-#define B3(S)                                                                                                     \
-    if (bam) k_back3<1, S><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p, w, nullptr, bam,     \
-                                                  c->mu.p, c->Z0, c->flag.p);                                     \
-    else k_back3<0, S><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p, w, out, nullptr, nullptr, \
-                                              0.0, c->flag.p);
-        switch (spl_of(c)) { case 1: B3(1) break; case 2: B3(2) break; default: B3(4) break; }
-#undef B3
+        back3_launch(c, w, out, bam, nonneg);
     }
     check_launch(c, "k_back3");
     c->timer_end(T_BACK);
     c->tm.back_launches++;
 }
-static void back_into(Ctx* c, const float* w, double* out) { back_launch(c, w, out, nullptr); }
+// nonneg: w >= 0 with no -0.0 (q, d); false for caller-supplied vectors
+static void back_into(Ctx* c, const float* w, double* out, bool nonneg = true) {
+    back_launch(c, w, out, nullptr, nonneg);
+}
 
 // one cooperative launch of the fused back projection + all-reduce (kernels_ar.cuh);
 // rexec logical ranks [a.r0, a.r0 + rexec) run in this grid
@@ -572,11 +669,7 @@ static void forward_plain(Ctx* c, const float* mu, double* l) {
             k_fwd_patch<0, 4, 8, 5><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, mu, nullptr, nullptr,
                                                                    nullptr, l, nullptr, c->flag.p);
     } else {
-        const unsigned nb = nblk_warp(c, c->Ml);
-#define F3(S) k_forward3<0, S><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu, nullptr, nullptr, nullptr, \
-                                                      l, nullptr, c->flag.p);
-        switch (spl_of(c)) { case 1: F3(1) break; case 2: F3(2) break; default: F3(4) break; }
-#undef F3
+        fwd3_launch<0>(c, mu, l, nblk_warp(c, c->Ml), false);
     }
     check_launch(c, "k_forward3");
 }
@@ -638,12 +731,7 @@ static void forward_fused(Ctx* c, bool record) {
 #undef FP
 #undef FV
     } else {
-        const unsigned nb = std::min<unsigned>(nblk_warp(c, c->Ml), (unsigned)c->partial.n);
-        nparts = (int)nb;
-#define F3(S) k_forward3<1, S><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, c->mu.p, c->I0.p, c->d.p, \
-                                                      c->q.p, nullptr, c->partial.p, c->flag.p);
-        switch (spl_of(c)) { case 1: F3(1) break; case 2: F3(2) break; default: F3(4) break; }
-#undef F3
+        nparts = (int)fwd3_launch<1>(c, c->mu.p, nullptr, (unsigned)c->partial.n, c->algo == 1 && c->mu_nonneg);
     }
     check_launch(c, "k_forward3");
     c->timer_end(T_FWD);
@@ -993,7 +1081,11 @@ static void am_init(Ctx* c, const double* init_mu) {
     c->mu.ensure(NV(c));
     c->g.ensure(2 * NV(c));
     c->bam.ensure(NV(c));
+    // the AM update clamps at +0, so mu stays sign-bit-free when
+    // it starts so: the 3D forward may then use the unsigned bit move
+    c->mu_nonneg = true;
     if (init_mu) {
+        for (uint64_t i = 0; i < c->N * (uint64_t)c->nz && c->mu_nonneg; ++i) c->mu_nonneg = !std::signbit(init_mu[i]);
         if (c->nzl == 1) upload_image2(c, init_mu, c->mu.p);
         else upload_slab<float>(c, init_mu, c->mu.p, c->N, c->N, 0);
     } else {
@@ -1470,6 +1562,7 @@ static Ctx* create(int device) {
     if (const char* e = std::getenv("WAMGPU_FWD_VARIANT")) c->fwd_variant = std::atoi(e);
     if (const char* e = std::getenv("WAMGPU_SPLIT_VARIANT")) c->split_variant = std::atoi(e);
     if (const char* e = std::getenv("WAMGPU_WALK_VARIANT")) c->walk_variant = std::atoi(e);
+    if (const char* e = std::getenv("WAMGPU_SLAB_VARIANT")) c->slab_variant = std::atoi(e);
     if (const char* e = std::getenv("WAMGPU_BACK_VARIANT")) c->back_variant = std::atoi(e);
     CK(cudaEventCreate(&c->ev_t0));
     CK(cudaEventCreate(&c->ev_a));
@@ -1864,7 +1957,7 @@ int wamgpu_back_project(wamgpu_ctx* ctx, const double* w, double* out) {
         c->fscratch.ensure(std::max<uint64_t>(MV(c), 1));
         c->dscratch.ensure(NV(c));
         upload_slab<float>(c, w, c->fscratch.p, c->Ml, c->Ml, 0, true);
-        back_into(c, c->fscratch.p, c->dscratch.p);
+        back_into(c, c->fscratch.p, c->dscratch.p, false);
         if (c->nzl == 1) allreduce_sum(c, c->dscratch.p, c->N);
         download_slab<double>(c, c->dscratch.p, out, c->N, c->N, 0);
     })
