@@ -223,9 +223,12 @@ __device__ __forceinline__ void slab_dot_g(const uint2* __restrict__ A, const fl
 
 // K2 3D v2: one warp = G adjacent rays (groups of LPR lanes); MODE as k_forward3.
 // The warp covers LPR*SPL slices of the stride-P slab per part and loops over
-// the P/(LPR*SPL) parts (the ray's entries are re-read from L1/L2 per part).
+// the parts in [sbeg, nz) (the ray's entries are re-read from L1/L2 per part);
+// the host may instead launch once per part (sbeg = part start, nz = its end)
+// so that one part's slab columns stay L2-resident (cfg4: 1M voxels x 32 slices
+// = 128 MB per part against the 512 MB whole slab).
 template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P>
-__global__ void __launch_bounds__(256) k_fwd3s(uint64_t M, int nz, const unsigned long long* __restrict__ rp,
+__global__ void __launch_bounds__(256) k_fwd3s(uint64_t M, int sbeg, int nz, const unsigned long long* __restrict__ rp,
                                                const uint2* __restrict__ A, const float* __restrict__ mu,
                                                const float* __restrict__ I0, const float* __restrict__ d,
                                                float* __restrict__ q, double* __restrict__ lout,
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(256) k_fwd3s(uint64_t M, int nz, const unsigne
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     double tacc = 0.0;
     for (uint64_t y0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + wib) * G; y0 < M; y0 += W * G)
-    for (int s0 = 0; s0 < nz; s0 += SB) {
+    for (int s0 = sbeg; s0 < nz; s0 += SB) {
         const uint64_t y = y0 + g;
         const bool ok = y < M;
         const uint64_t lo = ok ? rp[y] : 0, hi = ok ? rp[y + 1] : 0;
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(256) k_fwd3s(uint64_t M, int nz, const unsigne
 
 // K3 3D v2: one warp = G voxels of the tile order; MODE as k_back3.
 template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P>
-__global__ void __launch_bounds__(256) k_back3s(uint64_t N, int nz, const unsigned* __restrict__ order,
+__global__ void __launch_bounds__(256) k_back3s(uint64_t N, int sbeg, int nz, const unsigned* __restrict__ order,
                                                 const unsigned long long* __restrict__ cp,
                                                 const uint2* __restrict__ C, const float* __restrict__ w,
                                                 double* __restrict__ g, const double* __restrict__ bam,
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__(256) k_back3s(uint64_t N, int nz, const unsign
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, gr = lane / LPR, lig = lane % LPR;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t i0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + wib) * G; i0 < N; i0 += W * G)
-    for (int s0 = 0; s0 < nz; s0 += SB) {
+    for (int s0 = sbeg; s0 < nz; s0 += SB) {
         const uint64_t i = i0 + gr;
         const bool ok = i < N;
         const uint64_t x = ok ? (order ? order[i] : i) : 0;

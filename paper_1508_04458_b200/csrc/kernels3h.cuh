@@ -502,7 +502,10 @@ __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __
 // multipliers are computed by 32/E lanes instead of 32 (fp64 work per slice
 // roughly halves at E = 4); the E entry groups' partials are combined by a
 // fixed xor butterfly, then per-block sums as in k_split3h.
-template <int SPL, int E>
+// U rounds of E entries: the q rows of round r+1 are loaded before round r is
+// consumed (software pipeline; ncu at cfg4 showed 44% of the stall samples on
+// the first use of the q gathers with only the current round in flight).
+template <int SPL, int E, int U = 2>
 __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* __restrict__ list, int nx, int ny,
                                                    int nzl, const unsigned long long* __restrict__ ptr,
                                                    const unsigned* __restrict__ eray, const float4* __restrict__ epsi,
@@ -523,11 +526,11 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
         for (int g = 0; g < NG; ++g)
 #pragma unroll
             for (int t = 0; t < 7; ++t) acc[g][t] = 0.0;
-        constexpr int U = 2;
         const uint64_t e0 = ptr[key], e1 = ptr[key + 1];
-        for (uint64_t e = e0; e < e1; e += (uint64_t)E * U) {
-            unsigned yv[U];
-            float4 ps[U];
+        unsigned yv[U];
+        float4 ps[U];
+        float4 qv[U][S / 4];
+        auto load = [&](uint64_t e) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const uint64_t ee = e + grp + (uint64_t)E * u;
@@ -536,16 +539,27 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
                 yv[u] = __ldg(eray + ei);
                 ps[u] = ok ? __ldg(epsi + ei) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            float4 qv[U][S / 4];
 #pragma unroll
             for (int u = 0; u < U; ++u)
 #pragma unroll
                 for (int v = 0; v < S / 4; ++v)
                     qv[u][v] = __ldg(reinterpret_cast<const float4*>(q + (uint64_t)yv[u] * P + j * S) + v);
+        };
+        if (e0 < e1) load(e0);
+        for (uint64_t e = e0; e < e1; e += (uint64_t)E * U) {
+            float4 pc[U];
+            float4 qc[U][S / 4];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const double pA = (double)ps[u].x * cl, pH = (double)ps[u].y * cl, pV = (double)ps[u].z * cl,
-                             pD = (double)ps[u].w * cl;
+                pc[u] = ps[u];
+#pragma unroll
+                for (int v = 0; v < S / 4; ++v) qc[u][v] = qv[u][v];
+            }
+            if (e + (uint64_t)E * U < e1) load(e + (uint64_t)E * U);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const double pA = (double)pc[u].x * cl, pH = (double)pc[u].y * cl, pV = (double)pc[u].z * cl,
+                             pD = (double)pc[u].w * cl;
                 const double lowm[3] = {fmin(pH, 0.0), fmin(pV, 0.0), fmin(pD, 0.0)};
                 const double hp[4] = {pA, pH, pV, pD};
                 double mlo[4], mhi[4];
@@ -554,7 +568,7 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
                 float f[S];
 #pragma unroll
                 for (int v = 0; v < S / 4; ++v) {
-                    f[4 * v] = qv[u][v].x; f[4 * v + 1] = qv[u][v].y; f[4 * v + 2] = qv[u][v].z; f[4 * v + 3] = qv[u][v].w;
+                    f[4 * v] = qc[u][v].x; f[4 * v + 1] = qc[u][v].y; f[4 * v + 2] = qc[u][v].z; f[4 * v + 3] = qc[u][v].w;
                 }
                 if (l >= 2) {
 #pragma unroll

@@ -483,6 +483,8 @@ static unsigned nblk_warp(const Ctx* c, uint64_t n) {
 // kernel (SLAB_LPR lanes per ray, 4 gathers per round):
 //   12 = NF 3 (default), 3 = NF 2, 8 = NF 0, 9 = NF 4, 11 = NF 1;
 //   1 = round-1 k_forward3/k_back3 (warp per ray, shuffles, F2F only).
+//   20/21 = 32-slice parts (8 lanes x 4 slices, 4 rays per warp), one launch
+//   per part (NF 3/2) so a part's slab columns stay L2-resident.
 // Variant + 100 (default 112): the unsigned bit move for vectors known to be
 // non-negative.  cfg5 sweep (profiles/r02_slab_sweep.txt): 1 -> 11.3 ms per
 // pass, 9 -> 8.45, 12 -> 8.25, 112 -> 8.04 (forward) / 7.89 (back).
@@ -495,6 +497,8 @@ static unsigned nblk_warp(const Ctx* c, uint64_t n) {
         case 8: X(SLAB_LPR, P / SLAB_LPR, 4, 0) break;                                                             \
         case 9: X(SLAB_LPR, P / SLAB_LPR, 4, 4) break;                                                             \
         case 11: X(SLAB_LPR, P / SLAB_LPR, 4, 1) break;                                                            \
+        case 20: X(8, 4, 4, 3) break;                                                                              \
+        case 21: X(8, 4, 4, 2) break;                                                                              \
         default: X(SLAB_LPR, P / SLAB_LPR, 4, 3) break;                                                            \
     }
 template <int MODE, int SPL>
@@ -503,6 +507,7 @@ static unsigned fwd3_launch_s(Ctx* c, const float* mu, double* l, unsigned maxbl
     unsigned nb = 0;
     const int v = c->slab_variant % 100;
     const bool uns = nonneg && c->slab_variant >= 100;
+    const bool parts = v >= 20 && P > 32;
     if (v == 1) {
         nb = std::min<unsigned>(nblk_warp(c, c->Ml), maxblk);
         k_forward3<MODE, SPL><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l,
@@ -512,15 +517,20 @@ static unsigned fwd3_launch_s(Ctx* c, const float* mu, double* l, unsigned maxbl
 #define FX(LPR, S2, U, NF)                                                                                         \
     {                                                                                                              \
         constexpr int G = 32 / LPR;                                                                                \
-        nb = std::min<unsigned>(nblk_warp(c, (c->Ml + G - 1) / G), maxblk);                                        \
-        if (uns)                                                                                                   \
-            k_fwd3s<MODE, LPR, S2, U, NF, false, P><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu,     \
-                                                                          c->I0.p, c->d.p, c->q.p, l, c->partial.p, \
-                                                                          c->flag.p);                             \
-        else                                                                                                       \
-            k_fwd3s<MODE, LPR, S2, U, NF, true, P><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu,      \
-                                                                         c->I0.p, c->d.p, c->q.p, l, c->partial.p, \
-                                                                         c->flag.p);                              \
+        const int np = parts ? (c->nzl + 31) / 32 : 1;                                                             \
+        nb = std::min<unsigned>(nblk_warp(c, (c->Ml + G - 1) / G), maxblk / np);                                   \
+        for (int pi = 0; pi < np; ++pi) {                                                                          \
+            const int sb = parts ? 32 * pi : 0, se = parts ? std::min(c->nzl, sb + 32) : c->nzl;                   \
+            if (uns)                                                                                               \
+                k_fwd3s<MODE, LPR, S2, U, NF, false, P><<<nb, 256, 0, c->st>>>(                                    \
+                    c->Ml, sb, se, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l, c->partial.p + pi * nb,        \
+                    c->flag.p);                                                                                    \
+            else                                                                                                   \
+                k_fwd3s<MODE, LPR, S2, U, NF, true, P><<<nb, 256, 0, c->st>>>(                                     \
+                    c->Ml, sb, se, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l, c->partial.p + pi * nb,        \
+                    c->flag.p);                                                                                    \
+        }                                                                                                          \
+        nb *= np;                                                                                                  \
     }
     SLAB_SWITCH(FX, v)
 #undef FX
@@ -544,6 +554,7 @@ static void back3_launch_s(Ctx* c, const float* w, double* out, const double* ba
     constexpr int P = 32 * SPL;
     const int v = c->slab_variant % 100;
     const bool uns = nonneg && c->slab_variant >= 100;
+    const bool parts = v >= 20 && P > 32;
     if (v == 1) {
         const unsigned nb = nblk_warp(c, c->N);
         if (bam) k_back3<1, SPL><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p, w, nullptr, bam,
@@ -556,11 +567,14 @@ static void back3_launch_s(Ctx* c, const float* w, double* out, const double* ba
     {                                                                                                              \
         constexpr int G = 32 / LPR;                                                                                \
         const unsigned nb = nblk_warp(c, (c->N + G - 1) / G);                                                      \
-        if (bam) k_back3s<1, LPR, S2, U, NF, SG, P><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p,      \
-                                                                          c->C.p, w, nullptr, bam, c->mu.p, c->Z0, \
-                                                                          c->flag.p);                             \
-        else k_back3s<0, LPR, S2, U, NF, SG, P><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p,  \
-                                                                      w, out, nullptr, nullptr, 0.0, c->flag.p);  \
+        const int np = parts ? (c->nzl + 31) / 32 : 1;                                                             \
+        for (int pi = 0; pi < np; ++pi) {                                                                          \
+            const int sb = parts ? 32 * pi : 0, se = parts ? std::min(c->nzl, sb + 32) : c->nzl;                   \
+            if (bam) k_back3s<1, LPR, S2, U, NF, SG, P><<<nb, 256, 0, c->st>>>(                                    \
+                c->N, sb, se, c->order.p, c->cp.p, c->C.p, w, nullptr, bam, c->mu.p, c->Z0, c->flag.p);            \
+            else k_back3s<0, LPR, S2, U, NF, SG, P><<<nb, 256, 0, c->st>>>(                                        \
+                c->N, sb, se, c->order.p, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);              \
+        }                                                                                                          \
     }
 #define BX(LPR, S2, U, NF)                                                                                         \
     if (uns) BX1(LPR, S2, U, NF, false) else BX1(LPR, S2, U, NF, true)
@@ -1388,16 +1402,23 @@ static void wam_step(Ctx* c) {
         double* bm3 = c->g.p + NV(c);
 #define S3H(S) k_split3h<S><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p, c->E3ray.p, \
                                                    c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3);
-#define S3E(S, EE) k_split3h_e<S, EE><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p,   \
-                                                             c->E3ray.p, c->E3psi.p, c->q.p, c->act.p, c->off,      \
-                                                             c->koff, bm3);
+#define S3E(S, EE) S3EU(S, EE, 2)
+#define S3EU(S, EE, UU) k_split3h_e<S, EE, UU><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl,  \
+                                                                     c->np.p, c->E3ray.p, c->E3psi.p, c->q.p,     \
+                                                                     c->act.p, c->off, c->koff, bm3);
         if (c->split_variant == 1) {
             switch (spl_of(c)) { case 1: S3H(1) break; case 2: S3H(2) break; default: S3H(4) break; }
         } else if (c->split_variant == 2) {
             switch (spl_of(c)) { case 1: S3E(1, 8) break; case 2: S3E(2, 2) break; default: S3E(4, 2) break; }
-        } else {   // measured: cfg3 (64 slices) E=4 188 ms/run vs 364; cfg4 (128) E=2 1888 vs 2157 (E=4) / 2500
+        } else if (c->split_variant == 3) {   // two pipelined rounds of E entries
             switch (spl_of(c)) { case 1: S3E(1, 4) break; case 2: S3E(2, 4) break; default: S3E(4, 2) break; }
+        } else if (c->split_variant == 4) {
+            switch (spl_of(c)) { case 1: S3EU(1, 4, 4) break; case 2: S3EU(2, 4, 4) break; default: S3EU(4, 2, 4) break; }
+        } else {   // measured: cfg3 (64 slices) E=4 188 ms/run vs 364; cfg4 (128) E=2 1888 vs 2157 (E=4) / 2500;
+                   // one pipelined round (U = 1) 182 ms/run at cfg3 vs 188 (U = 2) / 189 (U = 4)
+            switch (spl_of(c)) { case 1: S3EU(1, 4, 1) break; case 2: S3EU(2, 4, 1) break; default: S3EU(4, 2, 1) break; }
         }
+#undef S3EU
 #undef S3E
 #undef S3H
         check_launch(c, "k_split3h");
