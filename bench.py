@@ -45,6 +45,8 @@ def _args():
     ap.add_argument("--iters", type=int, default=None, help="override J")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--nz", type=int, default=None,
+                    help="override the slice count of a 3D config (one z-slab shard of an R-GPU run = nz/R)")
     return ap.parse_args()
 
 
@@ -242,6 +244,11 @@ def main():
     import paper_1508_04458_b200 as W
     from paper_1508_04458_b200 import configs
     cfg = configs.get(args.config)
+    if args.nz:
+        if cfg["nz"] == 1:
+            raise SystemExit("--nz applies to 3D configs only")
+        cfg["nz"] = args.nz
+        cfg["name"] += f" (nz override {args.nz}: one z-slab shard)"
     algo = args.algo or cfg["algo"]
     J = args.iters or cfg["J"]
     sched = [s for s in cfg["schedule"] if s < J] if algo == "wam" else []

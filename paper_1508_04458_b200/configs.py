@@ -109,6 +109,11 @@ CONFIGS = {
                    phantom="luggage"),
     "small3d": dict(nx=64, ny=64, nz=40, voxel=4.0, views=72, detectors=96, I0=2e5, L=3, J=10, seed=22,
                     phantom="luggage"),
+    # slab strides 16 and 32 (with 8 pad slices): the sharded small-slab layouts
+    "tiny3d16": dict(nx=32, ny=32, nz=16, voxel=4.0, views=60, detectors=64, I0=1e5, L=3, J=10, seed=23,
+                     phantom="luggage"),
+    "tiny3d24": dict(nx=32, ny=32, nz=24, voxel=4.0, views=60, detectors=64, I0=1e5, L=3, J=10, seed=24,
+                     phantom="luggage"),
     "small_lug": dict(nx=128, ny=128, nz=1, voxel=2.0, views=120, detectors=192, I0=2e5, L=4, J=20, seed=13,
                       phantom="luggage"),
 }

@@ -400,14 +400,17 @@ __global__ void __launch_bounds__(256, 4) k_back3(uint64_t N, int nz, const unsi
 
 // K5 3D: b-[z][s] = sum over the (slice-shared) Phi^- column of z of q[y][s] phi,
 // exact 2^-20 fixed-point accumulation per slice (order-independent, as k_split).
+// Slab stride P = 32*SPL, or for SPL = 1 any Pr <= 32 (sharded small slabs:
+// lanes >= Pr idle).
 template <int SPL>
-__global__ void __launch_bounds__(256, 4) k_split3(uint64_t nlist, int nz, const unsigned* __restrict__ list,
+__global__ void __launch_bounds__(256, 4) k_split3(uint64_t nlist, int nz, int Pr, const unsigned* __restrict__ list,
                                                 const ulonglong2* __restrict__ col,
                                                 const uint2* __restrict__ E, const float* __restrict__ q,
                                                 double* __restrict__ bm) {
     using V = typename SlabVec<SPL>::T;
-    constexpr int P = 32 * SPL;
+    const int P = SPL == 1 ? Pr : 32 * SPL;
     const int lane = threadIdx.x & 31;
+    const bool live = lane * SPL < P;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nlist; i += W) {
         const unsigned z = list[i];
@@ -423,7 +426,8 @@ __global__ void __launch_bounds__(256, 4) k_split3(uint64_t nlist, int nz, const
             for (int u = 0; u < U; ++u) e[u] = __ldg(E + (k0 + u < hi ? k0 + u : lo));
             V v[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const V*>(q + (uint64_t)e[u].x * P) + lane);
+            for (int u = 0; u < U; ++u)
+                v[u] = live ? __ldg(reinterpret_cast<const V*>(q + (uint64_t)e[u].x * P) + lane) : V{};
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (k0 + u >= hi) break;
@@ -580,4 +584,43 @@ __global__ void k_zsum(uint64_t N, int nz, int P, const double* __restrict__ mu6
     out[p] = s;
 }
 
+// ---- boundary layout transposes on the device (the host only streams
+// contiguous rows): reference order [s][i] (n per slice) <-> slab [i][P],
+// pad slices zero.  32x32 smem tiles, coalesced on both sides.
+template <class T>
+__global__ void k_ref_to_slab(const T* __restrict__ src, T* __restrict__ dst, uint64_t n, int nzl, int P) {
+    __shared__ T t[32][33];
+    const uint64_t i0 = (uint64_t)blockIdx.x * 32;
+    const int s0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {   // r: slice within the tile
+        const int s = s0 + r;
+        const uint64_t i = i0 + threadIdx.x;
+        t[r][threadIdx.x] = (s < nzl && i < n) ? src[(uint64_t)s * n + i] : (T)0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {   // r: element within the tile
+        const uint64_t i = i0 + r;
+        const int s = s0 + threadIdx.x;
+        if (i < n && s < P) dst[i * P + s] = t[threadIdx.x][r];
+    }
+}
+template <class T>
+__global__ void k_slab_to_ref(const T* __restrict__ src, T* __restrict__ dst, uint64_t n, int nzl, int P) {
+    __shared__ T t[32][33];
+    const uint64_t i0 = (uint64_t)blockIdx.x * 32;
+    const int s0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const uint64_t i = i0 + r;
+        const int s = s0 + threadIdx.x;
+        t[threadIdx.x][r] = (i < n && s < nzl) ? src[i * P + s] : (T)0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int s = s0 + r;
+        const uint64_t i = i0 + threadIdx.x;
+        if (s < nzl && i < n) dst[(uint64_t)s * n + i] = t[r][threadIdx.x];
+    }
+}
+
 }  // namespace wamgpu
+

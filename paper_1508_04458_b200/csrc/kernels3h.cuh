@@ -505,13 +505,14 @@ __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __
 // U rounds of E entries: the q rows of round r+1 are loaded before round r is
 // consumed (software pipeline; ncu at cfg4 showed 44% of the stall samples on
 // the first use of the q gathers with only the current round in flight).
-template <int SPL, int E, int U = 2>
+// Templated on the slab stride P (8 .. 128): S = P*E/32 slices per lane.
+template <int P, int E, int U = 2>
 __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* __restrict__ list, int nx, int ny,
                                                    int nzl, const unsigned long long* __restrict__ ptr,
                                                    const unsigned* __restrict__ eray, const float4* __restrict__ epsi,
                                                    const float* __restrict__ q, const uint8_t* __restrict__ act,
                                                    ActOff off, ActOff koff, double* __restrict__ bm) {
-    constexpr int P = 32 * SPL, LPE = 32 / E, S = SPL * E, NG = S / 2;
+    constexpr int LPE = 32 / E, S = P * E / 32, NG = S / 2;
     static_assert(S >= 2 && S % 4 == 0, "slices per lane: a multiple of 4");
     __shared__ double red[4][7][P / 2];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, grp = lane / LPE, j = lane % LPE;

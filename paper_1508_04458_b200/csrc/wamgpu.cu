@@ -104,6 +104,9 @@ struct wamgpu_ctx {
     // state
     int algo = 0;  // 1 AM, 2 WAM
     DBuf<float> mu, beta, fscratch;
+    DBuf<char> xfer;                        // device side of the boundary transposes
+    void* pin[2] = {nullptr, nullptr};      // pinned host staging, double-buffered
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     DBuf<double> g, bdata, bam, mu64, bp_dbg, bm_dbg, zrow, dscratch;
     DBuf<unsigned long long> wcnt;      // separable 3D: per-(ray, level) Psi counts of the walk
     DBuf<unsigned long long> cursor;    // Phi^- emission cursor of the expansion walk
@@ -473,6 +476,15 @@ static void set_matrix_csr(Ctx* c, uint64_t rows, uint64_t cols, uint64_t nnz, c
 static void need_matrix(Ctx* c) { if (!c->have_matrix) throw ContractError("wamgpu: no system matrix set"); }
 static void need_data(Ctx* c) { if (!c->have_data) throw ContractError("wamgpu: no transmission data set"); }
 
+// Slab stride P of the z-fastest 3D layouts: the local slice count rounded up
+// to 8, 16, 32, 64 or 128, so a z-slab shard of a few slices (cfg3 on 8 GPUs:
+// 8 slices) costs its own slices, not a 32-slice minimum.
+static int slab_stride(const Ctx* c) {
+    if (c->nzl == 1) return 1;
+    int P = 8;
+    while (P < c->nzl) P *= 2;
+    return P;
+}
 static int spl_of(const Ctx* c) { return c->nzl <= 32 ? 1 : (c->nzl <= 64 ? 2 : 4); }
 static unsigned nblk_warp(const Ctx* c, uint64_t n) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, (uint64_t)c->sms * 16));
@@ -480,58 +492,49 @@ static unsigned nblk_warp(const Ctx* c, uint64_t n) {
 
 // 3D slab SpMM launches (kernels3d.cuh).  WAMGPU_SLAB_VARIANT picks the
 // conversion share NF (of 4 values, F2F; the rest by bit moves) of the v2
-// kernel (SLAB_LPR lanes per ray, 4 gathers per round):
+// kernel:
 //   12 = NF 3 (default), 3 = NF 2, 8 = NF 0, 9 = NF 4, 11 = NF 1;
-//   1 = round-1 k_forward3/k_back3 (warp per ray, shuffles, F2F only).
-//   20/21 = 32-slice parts (8 lanes x 4 slices, 4 rays per warp), one launch
-//   per part (NF 3/2) so a part's slab columns stay L2-resident.
+//   1 = round-1 k_forward3/k_back3 (warp per ray, shuffles, F2F only; P >= 32).
 // Variant + 100 (default 112): the unsigned bit move for vectors known to be
 // non-negative.  cfg5 sweep (profiles/r02_slab_sweep.txt): 1 -> 11.3 ms per
-// pass, 9 -> 8.45, 12 -> 8.25, 112 -> 8.04 (forward) / 7.89 (back).
-// Lanes per ray: 8 for P <= 64 (4 rays per warp), 16 for P = 128 (2 rays per
-// warp; 8 slices per lane either way at P >= 64).
-#define SLAB_LPR (SPL == 4 ? 16 : 8)
+// pass, 9 -> 8.45, 12 -> 8.25, 112 -> 8.04 (forward) / 7.89 (back).  One launch
+// per 32-slice part (L2-resident part columns at cfg4) was measured slower
+// (117 / 111 vs 100 / 70 ms at cfg4) and dropped.
+// Lanes per ray by slab stride P: 4 (P = 8, 16: 8 rays per warp), 8 (P = 32,
+// 64: 4 rays per warp), 16 (P = 128: 2 rays per warp).
+template <int P> struct SlabShape {
+    static constexpr int LPR = P <= 16 ? 4 : (P <= 64 ? 8 : 16), SPL = P / LPR, G = 32 / LPR;
+};
 #define SLAB_SWITCH(X, V)                                                                                          \
     switch (V) {                                                                                                   \
-        case 3: X(SLAB_LPR, P / SLAB_LPR, 4, 2) break;                                                             \
-        case 8: X(SLAB_LPR, P / SLAB_LPR, 4, 0) break;                                                             \
-        case 9: X(SLAB_LPR, P / SLAB_LPR, 4, 4) break;                                                             \
-        case 11: X(SLAB_LPR, P / SLAB_LPR, 4, 1) break;                                                            \
-        case 20: X(8, 4, 4, 3) break;                                                                              \
-        case 21: X(8, 4, 4, 2) break;                                                                              \
-        default: X(SLAB_LPR, P / SLAB_LPR, 4, 3) break;                                                            \
+        case 3: X(2) break;                                                                                        \
+        case 8: X(0) break;                                                                                        \
+        case 9: X(4) break;                                                                                        \
+        case 11: X(1) break;                                                                                       \
+        default: X(3) break;                                                                                       \
     }
-template <int MODE, int SPL>
-static unsigned fwd3_launch_s(Ctx* c, const float* mu, double* l, unsigned maxblk, bool nonneg) {
-    constexpr int P = 32 * SPL;
+template <int MODE, int P>
+static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxblk, bool nonneg) {
+    using S = SlabShape<P>;
     unsigned nb = 0;
     const int v = c->slab_variant % 100;
     const bool uns = nonneg && c->slab_variant >= 100;
-    const bool parts = v >= 20 && P > 32;
-    if (v == 1) {
-        nb = std::min<unsigned>(nblk_warp(c, c->Ml), maxblk);
-        k_forward3<MODE, SPL><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l,
-                                                     c->partial.p, c->flag.p);
-        return nb;
+    if constexpr (P >= 32) {
+        if (v == 1) {
+            nb = std::min<unsigned>(nblk_warp(c, c->Ml), maxblk);
+            k_forward3<MODE, P / 32><<<nb, 256, 0, c->st>>>(c->Ml, c->nzl, c->rp.p, c->A.p, mu, c->I0.p, c->d.p,
+                                                            c->q.p, l, c->partial.p, c->flag.p);
+            return nb;
+        }
     }
-#define FX(LPR, S2, U, NF)                                                                                         \
-    {                                                                                                              \
-        constexpr int G = 32 / LPR;                                                                                \
-        const int np = parts ? (c->nzl + 31) / 32 : 1;                                                             \
-        nb = std::min<unsigned>(nblk_warp(c, (c->Ml + G - 1) / G), maxblk / np);                                   \
-        for (int pi = 0; pi < np; ++pi) {                                                                          \
-            const int sb = parts ? 32 * pi : 0, se = parts ? std::min(c->nzl, sb + 32) : c->nzl;                   \
-            if (uns)                                                                                               \
-                k_fwd3s<MODE, LPR, S2, U, NF, false, P><<<nb, 256, 0, c->st>>>(                                    \
-                    c->Ml, sb, se, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l, c->partial.p + pi * nb,        \
-                    c->flag.p);                                                                                    \
-            else                                                                                                   \
-                k_fwd3s<MODE, LPR, S2, U, NF, true, P><<<nb, 256, 0, c->st>>>(                                     \
-                    c->Ml, sb, se, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l, c->partial.p + pi * nb,        \
-                    c->flag.p);                                                                                    \
-        }                                                                                                          \
-        nb *= np;                                                                                                  \
-    }
+    nb = std::min<unsigned>(nblk_warp(c, (c->Ml + S::G - 1) / S::G), maxblk);
+#define FX(NF)                                                                                                     \
+    if (uns)                                                                                                       \
+        k_fwd3s<MODE, S::LPR, S::SPL, 4, NF, false, P><<<nb, 256, 0, c->st>>>(                                     \
+            c->Ml, 0, c->nzl, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l, c->partial.p, c->flag.p);           \
+    else                                                                                                           \
+        k_fwd3s<MODE, S::LPR, S::SPL, 4, NF, true, P><<<nb, 256, 0, c->st>>>(                                      \
+            c->Ml, 0, c->nzl, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l, c->partial.p, c->flag.p);
     SLAB_SWITCH(FX, v)
 #undef FX
     return nb;
@@ -541,53 +544,50 @@ static unsigned fwd3_launch_s(Ctx* c, const float* mu, double* l, unsigned maxbl
 template <int MODE>
 static unsigned fwd3_launch(Ctx* c, const float* mu, double* l, unsigned maxblk, bool nonneg) {
     unsigned nb = 0;
-    switch (spl_of(c)) {
-        case 1: nb = fwd3_launch_s<MODE, 1>(c, mu, l, maxblk, nonneg); break;
-        case 2: nb = fwd3_launch_s<MODE, 2>(c, mu, l, maxblk, nonneg); break;
-        default: nb = fwd3_launch_s<MODE, 4>(c, mu, l, maxblk, nonneg); break;
+    switch (slab_stride(c)) {
+        case 8: nb = fwd3_launch_p<MODE, 8>(c, mu, l, maxblk, nonneg); break;
+        case 16: nb = fwd3_launch_p<MODE, 16>(c, mu, l, maxblk, nonneg); break;
+        case 32: nb = fwd3_launch_p<MODE, 32>(c, mu, l, maxblk, nonneg); break;
+        case 64: nb = fwd3_launch_p<MODE, 64>(c, mu, l, maxblk, nonneg); break;
+        default: nb = fwd3_launch_p<MODE, 128>(c, mu, l, maxblk, nonneg); break;
     }
     check_launch(c, "k_fwd3s");
     return nb;
 }
-template <int SPL>
-static void back3_launch_s(Ctx* c, const float* w, double* out, const double* bam, bool nonneg) {
-    constexpr int P = 32 * SPL;
+template <int P>
+static void back3_launch_p(Ctx* c, const float* w, double* out, const double* bam, bool nonneg) {
+    using S = SlabShape<P>;
     const int v = c->slab_variant % 100;
     const bool uns = nonneg && c->slab_variant >= 100;
-    const bool parts = v >= 20 && P > 32;
-    if (v == 1) {
-        const unsigned nb = nblk_warp(c, c->N);
-        if (bam) k_back3<1, SPL><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p, w, nullptr, bam,
-                                                        c->mu.p, c->Z0, c->flag.p);
-        else k_back3<0, SPL><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p, w, out, nullptr,
-                                                    nullptr, 0.0, c->flag.p);
-        return;
+    if constexpr (P >= 32) {
+        if (v == 1) {
+            const unsigned nb = nblk_warp(c, c->N);
+            if (bam) k_back3<1, P / 32><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p, w, nullptr,
+                                                               bam, c->mu.p, c->Z0, c->flag.p);
+            else k_back3<0, P / 32><<<nb, 256, 0, c->st>>>(c->N, c->nzl, c->order.p, c->cp.p, c->C.p, w, out,
+                                                           nullptr, nullptr, 0.0, c->flag.p);
+            return;
+        }
     }
-#define BX1(LPR, S2, U, NF, SG)                                                                                    \
-    {                                                                                                              \
-        constexpr int G = 32 / LPR;                                                                                \
-        const unsigned nb = nblk_warp(c, (c->N + G - 1) / G);                                                      \
-        const int np = parts ? (c->nzl + 31) / 32 : 1;                                                             \
-        for (int pi = 0; pi < np; ++pi) {                                                                          \
-            const int sb = parts ? 32 * pi : 0, se = parts ? std::min(c->nzl, sb + 32) : c->nzl;                   \
-            if (bam) k_back3s<1, LPR, S2, U, NF, SG, P><<<nb, 256, 0, c->st>>>(                                    \
-                c->N, sb, se, c->order.p, c->cp.p, c->C.p, w, nullptr, bam, c->mu.p, c->Z0, c->flag.p);            \
-            else k_back3s<0, LPR, S2, U, NF, SG, P><<<nb, 256, 0, c->st>>>(                                        \
-                c->N, sb, se, c->order.p, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);              \
-        }                                                                                                          \
-    }
-#define BX(LPR, S2, U, NF)                                                                                         \
-    if (uns) BX1(LPR, S2, U, NF, false) else BX1(LPR, S2, U, NF, true)
+    const unsigned nb = nblk_warp(c, (c->N + S::G - 1) / S::G);
+#define BX1(NF, SG)                                                                                                \
+    if (bam) k_back3s<1, S::LPR, S::SPL, 4, NF, SG, P><<<nb, 256, 0, c->st>>>(                                     \
+        c->N, 0, c->nzl, c->order.p, c->cp.p, c->C.p, w, nullptr, bam, c->mu.p, c->Z0, c->flag.p);                 \
+    else k_back3s<0, S::LPR, S::SPL, 4, NF, SG, P><<<nb, 256, 0, c->st>>>(                                         \
+        c->N, 0, c->nzl, c->order.p, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
+#define BX(NF) if (uns) { BX1(NF, false) } else { BX1(NF, true) }
     SLAB_SWITCH(BX, v)
 #undef BX
 #undef BX1
 }
 // nonneg: w >= 0 (the iteration's q and d; not the public back_project)
 static void back3_launch(Ctx* c, const float* w, double* out, const double* bam, bool nonneg) {
-    switch (spl_of(c)) {
-        case 1: back3_launch_s<1>(c, w, out, bam, nonneg); break;
-        case 2: back3_launch_s<2>(c, w, out, bam, nonneg); break;
-        default: back3_launch_s<4>(c, w, out, bam, nonneg); break;
+    switch (slab_stride(c)) {
+        case 8: back3_launch_p<8>(c, w, out, bam, nonneg); break;
+        case 16: back3_launch_p<16>(c, w, out, bam, nonneg); break;
+        case 32: back3_launch_p<32>(c, w, out, bam, nonneg); break;
+        case 64: back3_launch_p<64>(c, w, out, bam, nonneg); break;
+        default: back3_launch_p<128>(c, w, out, bam, nonneg); break;
     }
 }
 
@@ -1028,7 +1028,7 @@ static void fill_records(Ctx* c, int n, wamgpu_record* recs, int64_t active_at_s
 
 // ---- boundary layout conversion: reference image/coefficient layout
 // ((s0+s)*N + x, image.hpp:14) <-> device slab [x][s]; rays (s*M + y) <-> [y][s].
-static int slab_stride(const Ctx* c) { return c->nzl == 1 ? 1 : 32 * (c->nzl <= 32 ? 1 : (c->nzl <= 64 ? 2 : 4)); }
+
 // host-side data-parallel loop for the boundary conversions (large 3D slabs)
 template <class Fn>
 static void host_par(uint64_t n, Fn&& fn) {
@@ -1059,32 +1059,99 @@ static void download_image2(Ctx* c, const float* dev, double* ref) {
     for (uint64_t x = 0; x < c->N; ++x) ref[x] = h[mu_addr((unsigned)x, c->lgx)];
 }
 
+// Streamed host<->device transfers through two pinned 32 MB staging buffers:
+// the host fills (drains) one while the other is in flight.  The strided
+// reference<->slab reorder runs on the device (k_ref_to_slab / k_slab_to_ref);
+// the host only converts contiguous runs between double and the device type.
+constexpr size_t kPinChunk = 32u << 20;
+static void ensure_pinned(Ctx* c) {
+    if (c->pin[0]) return;
+    for (int k = 0; k < 2; ++k) {
+        CK(cudaMallocHost(&c->pin[k], kPinChunk));
+        CK(cudaEventCreateWithFlags(&c->pin_ev[k], cudaEventDisableTiming));
+    }
+}
+// fill(h, lo, hi): write elements [lo, hi) of the host-side sequence to h[0 ..)
+template <class T, class Fill>
+static void h2d_streamed(Ctx* c, T* dev, uint64_t count, Fill&& fill) {
+    ensure_pinned(c);
+    const uint64_t per = kPinChunk / sizeof(T);
+    int k = 0;
+    for (uint64_t lo = 0; lo < count; lo += per, k ^= 1) {
+        const uint64_t hi = std::min(count, lo + per);
+        CK(cudaEventSynchronize(c->pin_ev[k]));   // this buffer's previous copy has left
+        T* h = static_cast<T*>(c->pin[k]);
+        host_par(hi - lo, [&](uint64_t a, uint64_t b) { fill(h + a, lo + a, lo + b); });
+        CK(cudaMemcpyAsync(dev + lo, h, (hi - lo) * sizeof(T), cudaMemcpyHostToDevice, c->st));
+        CK(cudaEventRecord(c->pin_ev[k], c->st));
+    }
+}
+// drain(h, lo, hi): consume elements [lo, hi) of the device sequence from h[0 ..)
+template <class T, class Drain>
+static void d2h_streamed(Ctx* c, const T* dev, uint64_t count, Drain&& drain) {
+    ensure_pinned(c);
+    const uint64_t per = kPinChunk / sizeof(T);
+    const uint64_t nch = (count + per - 1) / per;
+    auto issue = [&](uint64_t ch) {
+        const uint64_t lo = ch * per, hi = std::min(count, lo + per);
+        CK(cudaMemcpyAsync(c->pin[ch & 1], dev + lo, (hi - lo) * sizeof(T), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaEventRecord(c->pin_ev[ch & 1], c->st));
+    };
+    if (nch) issue(0);
+    for (uint64_t ch = 0; ch < nch; ++ch) {
+        if (ch + 1 < nch) issue(ch + 1);           // its buffer was drained in the previous round
+        CK(cudaEventSynchronize(c->pin_ev[ch & 1]));
+        const uint64_t lo = ch * per, hi = std::min(count, lo + per);
+        const T* h = static_cast<const T*>(c->pin[ch & 1]);
+        host_par(hi - lo, [&](uint64_t a, uint64_t b) { drain(h + a, lo + a, lo + b); });
+    }
+}
+
 template <class T>
 static void upload_slab(Ctx* c, const double* ref, T* dev, uint64_t n_inner, uint64_t ref_stride, uint64_t ref_off,
                         bool local = false) {
     const int P = slab_stride(c);
-    std::vector<T> h(std::max<uint64_t>(n_inner * P, 1), (T)0);   // pad slices are zero
     const int sb = local ? 0 : c->s0;
     const int nzl = c->nzl;
-    host_par(n_inner, [&](uint64_t lo, uint64_t hi) {
-        for (uint64_t i = lo; i < hi; ++i)
-            for (int s = 0; s < nzl; ++s) h[i * P + s] = (T)ref[(uint64_t)(sb + s) * ref_stride + ref_off + i];
+    const uint64_t count = (uint64_t)nzl * n_inner;
+    c->xfer.ensure(std::max<uint64_t>(count, 1) * sizeof(T));
+    T* xs = reinterpret_cast<T*>(c->xfer.p);
+    h2d_streamed<T>(c, xs, count, [&](T* h, uint64_t lo, uint64_t hi) {
+        uint64_t s = lo / n_inner, i = lo % n_inner;
+        const double* r = ref + (uint64_t)(sb + s) * ref_stride + ref_off;
+        for (uint64_t e = lo; e < hi; ++e) {
+            *h++ = (T)r[i];
+            if (++i == n_inner) { i = 0; ++s; r = ref + (uint64_t)(sb + s) * ref_stride + ref_off; }
+        }
     });
-    CK(cudaMemcpyAsync(dev, h.data(), n_inner * P * sizeof(T), cudaMemcpyHostToDevice, c->st));
+    if (n_inner) {
+        k_ref_to_slab<T><<<dim3((unsigned)((n_inner + 31) / 32), (unsigned)((P + 31) / 32)), dim3(32, 8), 0, c->st>>>(
+            xs, dev, n_inner, nzl, P);
+        check_launch(c, "k_ref_to_slab");
+    }
     CK(cudaStreamSynchronize(c->st));
 }
 template <class T>
 static void download_slab(Ctx* c, const T* dev, double* ref, uint64_t n_inner, uint64_t ref_stride, uint64_t ref_off,
                           bool local = false) {
     const int P = slab_stride(c);
-    std::vector<T> h(std::max<uint64_t>(n_inner * P, 1));
-    CK(cudaMemcpyAsync(h.data(), dev, n_inner * P * sizeof(T), cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
     const int sb = local ? 0 : c->s0;
     const int nzl = c->nzl;
-    host_par(n_inner, [&](uint64_t lo, uint64_t hi) {
-        for (uint64_t i = lo; i < hi; ++i)
-            for (int s = 0; s < nzl; ++s) ref[(uint64_t)(sb + s) * ref_stride + ref_off + i] = (double)h[i * P + s];
+    const uint64_t count = (uint64_t)nzl * n_inner;
+    c->xfer.ensure(std::max<uint64_t>(count, 1) * sizeof(T));
+    T* xs = reinterpret_cast<T*>(c->xfer.p);
+    if (n_inner) {
+        k_slab_to_ref<T><<<dim3((unsigned)((n_inner + 31) / 32), (unsigned)((P + 31) / 32)), dim3(32, 8), 0, c->st>>>(
+            dev, xs, n_inner, nzl, P);
+        check_launch(c, "k_slab_to_ref");
+    }
+    d2h_streamed<T>(c, xs, count, [&](const T* h, uint64_t lo, uint64_t hi) {
+        uint64_t s = lo / n_inner, i = lo % n_inner;
+        double* r = ref + (uint64_t)(sb + s) * ref_stride + ref_off;
+        for (uint64_t e = lo; e < hi; ++e) {
+            r[i] = (double)*h++;
+            if (++i == n_inner) { i = 0; ++s; r = ref + (uint64_t)(sb + s) * ref_stride + ref_off; }
+        }
     });
 }
 
@@ -1406,17 +1473,25 @@ static void wam_step(Ctx* c) {
 #define S3EU(S, EE, UU) k_split3h_e<S, EE, UU><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl,  \
                                                                      c->np.p, c->E3ray.p, c->E3psi.p, c->q.p,     \
                                                                      c->act.p, c->off, c->koff, bm3);
-        if (c->split_variant == 1) {
+        const int P = slab_stride(c);
+        if (c->split_variant == 1 && P >= 32) {
             switch (spl_of(c)) { case 1: S3H(1) break; case 2: S3H(2) break; default: S3H(4) break; }
-        } else if (c->split_variant == 2) {
-            switch (spl_of(c)) { case 1: S3E(1, 8) break; case 2: S3E(2, 2) break; default: S3E(4, 2) break; }
-        } else if (c->split_variant == 3) {   // two pipelined rounds of E entries
-            switch (spl_of(c)) { case 1: S3E(1, 4) break; case 2: S3E(2, 4) break; default: S3E(4, 2) break; }
-        } else if (c->split_variant == 4) {
-            switch (spl_of(c)) { case 1: S3EU(1, 4, 4) break; case 2: S3EU(2, 4, 4) break; default: S3EU(4, 2, 4) break; }
+        } else if (c->split_variant == 2 && P >= 32) {
+            switch (P) { case 32: S3E(32, 8) break; case 64: S3E(64, 2) break; default: S3E(128, 2) break; }
+        } else if (c->split_variant == 3 && P >= 32) {   // two pipelined rounds of E entries
+            switch (P) { case 32: S3E(32, 4) break; case 64: S3E(64, 4) break; default: S3E(128, 2) break; }
+        } else if (c->split_variant == 4 && P >= 32) {
+            switch (P) { case 32: S3EU(32, 4, 4) break; case 64: S3EU(64, 4, 4) break; default: S3EU(128, 2, 4) break; }
         } else {   // measured: cfg3 (64 slices) E=4 188 ms/run vs 364; cfg4 (128) E=2 1888 vs 2157 (E=4) / 2500;
-                   // one pipelined round (U = 1) 182 ms/run at cfg3 vs 188 (U = 2) / 189 (U = 4)
-            switch (spl_of(c)) { case 1: S3EU(1, 4, 1) break; case 2: S3EU(2, 4, 1) break; default: S3EU(4, 2, 1) break; }
+                   // one pipelined round (U = 1) 182 ms/run at cfg3 vs 188 (U = 2) / 189 (U = 4).
+                   // Sharded small slabs: S = P*E/32 = 4 slices per lane.
+            switch (P) {
+                case 8: S3EU(8, 16, 1) break;
+                case 16: S3EU(16, 8, 1) break;
+                case 32: S3EU(32, 4, 1) break;
+                case 64: S3EU(64, 4, 1) break;
+                default: S3EU(128, 2, 1) break;
+            }
         }
 #undef S3EU
 #undef S3E
@@ -1438,7 +1513,8 @@ static void wam_step(Ctx* c) {
                 k_split<12><<<nb, 256, 0, c->st>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, bm2);
         } else {
             double* bm3 = c->g.p + NV(c);
-#define S3(S) k_split3<S><<<nb, 256, 0, c->st>>>(c->nlist, c->nzl, c->list.p, c->cols.p, c->E.p, c->q.p, bm3);
+#define S3(S) k_split3<S><<<nb, 256, 0, c->st>>>(c->nlist, c->nzl, slab_stride(c), c->list.p, c->cols.p, c->E.p, \
+                                                c->q.p, bm3);
             switch (spl_of(c)) { case 1: S3(1) break; case 2: S3(2) break; default: S3(4) break; }
 #undef S3
         }
@@ -1611,6 +1687,10 @@ static void destroy(Ctx* c) {
     for (void* p : c->ar.opened) cudaIpcCloseMemHandle(p);
     if (c->comm) ncclCommDestroy(c->comm);
     c->A.release(); c->C.release(); c->E.release();
+    for (int k = 0; k < 2; ++k) {
+        if (c->pin[k]) cudaFreeHost(c->pin[k]);
+        if (c->pin_ev[k]) cudaEventDestroy(c->pin_ev[k]);
+    }
     cudaStreamDestroy(c->st);
     delete c;
 }

@@ -2,7 +2,9 @@
 matrix, geometry.hpp:17-20; pin P2) against the CPU oracle:
 slab forward/back, the AM baseline and the wavelet AM with per-slice 2D Haar
 and the z-summed expansion criterion.  `small3d` has 40
-slices, exercising partially filled lane slabs (2 slices per lane, masked)."""
+slices, exercising partially filled lane slabs (2 slices per lane, masked);
+`tiny3d` / `tiny3d16` / `tiny3d24` use the slab strides 8, 16 and 32 (8 pad
+slices) of z-slab shards."""
 import numpy as np
 import pytest
 
@@ -19,7 +21,7 @@ def _ctx(W, cfg):
     return c
 
 
-@pytest.mark.parametrize("name", ["tiny3d", "small3d"])
+@pytest.mark.parametrize("name", ["tiny3d", "tiny3d16", "tiny3d24", "small3d"])
 def test_slab_forward_back_vs_mirror(wam, orc, name):
     cfg, p, mu_true, I0, d = problem_inputs(name, orc, wam, mirror=True)
     c = _ctx(wam, cfg)
@@ -89,7 +91,7 @@ def test_wam3d_parity_tree_bit_exact(wam, orc, name):
     assert rel_l2(bm, bm32) < TOL_MIRROR and rel_l2(bp, bp32) < TOL_MIRROR
 
 
-@pytest.mark.parametrize("name", ["tiny3d", "small3d"])
+@pytest.mark.parametrize("name", ["tiny3d", "tiny3d16", "tiny3d24", "small3d"])
 def test_wam3d_separable_haar_parity(wam, orc, name):
     """Separable 3D Haar model (pin P3): octree tree bit-exact vs both oracles
     after every expansion, Z0 bit-exact vs the mirror, mu / I-div within bars."""
