@@ -141,7 +141,7 @@ __device__ __forceinline__ void slab_dot_g(const uint2* __restrict__ A, const fl
                                            uint64_t hi, int maxlen, int lig, int g,
                                            SlabStage<32 / LPR>& st, double (&acc)[SPL]) {
     constexpr int kSlabK = SlabStage<32 / LPR>::K, NL = kSlabK / LPR, RPC = kSlabK / U;
-    static_assert(kSlabK % U == 0 && U % 4 == 0 && NL >= 1, "unroll");
+    static_assert(kSlabK % U == 0 && (U % 4 == 0 || U == 2) && NL >= 1, "unroll");
     using L = SlabLd<SPL>;
 #pragma unroll
     for (int j = 0; j < SPL; ++j) acc[j] = 0.0;
@@ -167,16 +167,24 @@ __device__ __forceinline__ void slab_dot_g(const uint2* __restrict__ A, const fl
     auto issue = [&](int buf, int j0) {   // gathers of the round at entries j0.. of buffer buf
         const unsigned* sc = st.c[buf][g];
         const double* sh = st.h[buf][g];
+        if constexpr (U == 2) {
+            const uint2 c2 = *reinterpret_cast<const uint2*>(sc + j0);
+            const double2 h01 = *reinterpret_cast<const double2*>(sh + j0);
+            h[0] = h01.x; h[1] = h01.y;
+            slab_load<LPR, SPL>(xl + (uint64_t)c2.x * P, v[0]);
+            slab_load<LPR, SPL>(xl + (uint64_t)c2.y * P, v[1]);
+        } else {
 #pragma unroll
-        for (int u = 0; u < U; u += 4) {
-            const uint4 c4 = *reinterpret_cast<const uint4*>(sc + j0 + u);
-            const double2 h01 = *reinterpret_cast<const double2*>(sh + j0 + u);
-            const double2 h23 = *reinterpret_cast<const double2*>(sh + j0 + u + 2);
-            h[u] = h01.x; h[u + 1] = h01.y; h[u + 2] = h23.x; h[u + 3] = h23.y;
-            slab_load<LPR, SPL>(xl + (uint64_t)c4.x * P, v[u]);
-            slab_load<LPR, SPL>(xl + (uint64_t)c4.y * P, v[u + 1]);
-            slab_load<LPR, SPL>(xl + (uint64_t)c4.z * P, v[u + 2]);
-            slab_load<LPR, SPL>(xl + (uint64_t)c4.w * P, v[u + 3]);
+            for (int u = 0; u < U; u += 4) {
+                const uint4 c4 = *reinterpret_cast<const uint4*>(sc + j0 + u);
+                const double2 h01 = *reinterpret_cast<const double2*>(sh + j0 + u);
+                const double2 h23 = *reinterpret_cast<const double2*>(sh + j0 + u + 2);
+                h[u] = h01.x; h[u + 1] = h01.y; h[u + 2] = h23.x; h[u + 3] = h23.y;
+                slab_load<LPR, SPL>(xl + (uint64_t)c4.x * P, v[u]);
+                slab_load<LPR, SPL>(xl + (uint64_t)c4.y * P, v[u + 1]);
+                slab_load<LPR, SPL>(xl + (uint64_t)c4.z * P, v[u + 2]);
+                slab_load<LPR, SPL>(xl + (uint64_t)c4.w * P, v[u + 3]);
+            }
         }
     };
     fetch(0);
@@ -227,15 +235,15 @@ __device__ __forceinline__ void slab_dot_g(const uint2* __restrict__ A, const fl
 // the host may instead launch once per part (sbeg = part start, nz = its end)
 // so that one part's slab columns stay L2-resident (cfg4: 1M voxels x 32 slices
 // = 128 MB per part against the 512 MB whole slab).
-template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P>
-__global__ void __launch_bounds__(256) k_fwd3s(uint64_t M, int sbeg, int nz, const unsigned long long* __restrict__ rp,
+template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P, int WPB = 8, int MINB = 1>
+__global__ void __launch_bounds__(32 * WPB, MINB) k_fwd3s(uint64_t M, int sbeg, int nz, const unsigned long long* __restrict__ rp,
                                                const uint2* __restrict__ A, const float* __restrict__ mu,
                                                const float* __restrict__ I0, const float* __restrict__ d,
                                                float* __restrict__ q, double* __restrict__ lout,
                                                double* __restrict__ partial, int* __restrict__ flag) {
     constexpr int G = 32 / LPR, SB = LPR * SPL;
     static_assert(P % SB == 0, "slab parts");
-    __shared__ __align__(16) SlabStage<G> s_st[8];
+    __shared__ __align__(16) SlabStage<G> s_st[WPB];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, g = lane / LPR, lig = lane % LPR;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     double tacc = 0.0;
@@ -279,15 +287,15 @@ __global__ void __launch_bounds__(256) k_fwd3s(uint64_t M, int sbeg, int nz, con
 }
 
 // K3 3D v2: one warp = G voxels of the tile order; MODE as k_back3.
-template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P>
-__global__ void __launch_bounds__(256) k_back3s(uint64_t N, int sbeg, int nz, const unsigned* __restrict__ order,
+template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P, int WPB = 8, int MINB = 1>
+__global__ void __launch_bounds__(32 * WPB, MINB) k_back3s(uint64_t N, int sbeg, int nz, const unsigned* __restrict__ order,
                                                 const unsigned long long* __restrict__ cp,
                                                 const uint2* __restrict__ C, const float* __restrict__ w,
                                                 double* __restrict__ g, const double* __restrict__ bam,
                                                 float* __restrict__ mu, double Z0, int* __restrict__ flag) {
     constexpr int G = 32 / LPR, SB = LPR * SPL;
     static_assert(P % SB == 0, "slab parts");
-    __shared__ __align__(16) SlabStage<G> s_st[8];
+    __shared__ __align__(16) SlabStage<G> s_st[WPB];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, gr = lane / LPR, lig = lane % LPR;
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t i0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + wib) * G; i0 < N; i0 += W * G)

@@ -505,13 +505,18 @@ static unsigned nblk_warp(const Ctx* c, uint64_t n) {
 template <int P> struct SlabShape {
     static constexpr int LPR = P <= 16 ? 4 : (P <= 64 ? 8 : 16), SPL = P / LPR, G = 32 / LPR;
 };
+// X(NF, U, WPB, MINB): F2F share, gathers per round, warps per CTA, min CTAs per SM
 #define SLAB_SWITCH(X, V)                                                                                          \
     switch (V) {                                                                                                   \
-        case 3: X(2) break;                                                                                        \
-        case 8: X(0) break;                                                                                        \
-        case 9: X(4) break;                                                                                        \
-        case 11: X(1) break;                                                                                       \
-        default: X(3) break;                                                                                       \
+        case 3: X(2, 4, 8, 1) break;                                                                               \
+        case 8: X(0, 4, 8, 1) break;                                                                               \
+        case 9: X(4, 4, 8, 1) break;                                                                               \
+        case 11: X(1, 4, 8, 1) break;                                                                              \
+        case 13: X(3, 2, 8, 1) break;                                                                              \
+        case 14: X(3, 2, 4, 5) break;                                                                              \
+        case 15: X(3, 4, 4, 1) break;                                                                              \
+        case 16: X(3, 2, 4, 6) break;                                                                              \
+        default: X(3, 4, 8, 1) break;                                                                              \
     }
 template <int MODE, int P>
 static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxblk, bool nonneg) {
@@ -527,14 +532,16 @@ static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxbl
             return nb;
         }
     }
-    nb = std::min<unsigned>(nblk_warp(c, (c->Ml + S::G - 1) / S::G), maxblk);
-#define FX(NF)                                                                                                     \
-    if (uns)                                                                                                       \
-        k_fwd3s<MODE, S::LPR, S::SPL, 4, NF, false, P><<<nb, 256, 0, c->st>>>(                                     \
-            c->Ml, 0, c->nzl, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l, c->partial.p, c->flag.p);           \
-    else                                                                                                           \
-        k_fwd3s<MODE, S::LPR, S::SPL, 4, NF, true, P><<<nb, 256, 0, c->st>>>(                                      \
-            c->Ml, 0, c->nzl, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l, c->partial.p, c->flag.p);
+#define FX(NF, U, WPB, MINB)                                                                                       \
+    {                                                                                                              \
+        nb = std::min<unsigned>(nblk_warp(c, (c->Ml + S::G - 1) / S::G) * (8 / WPB), maxblk);                      \
+        if (uns)                                                                                                   \
+            k_fwd3s<MODE, S::LPR, S::SPL, U, NF, false, P, WPB, MINB><<<nb, 32 * WPB, 0, c->st>>>(                 \
+                c->Ml, 0, c->nzl, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l, c->partial.p, c->flag.p);       \
+        else                                                                                                       \
+            k_fwd3s<MODE, S::LPR, S::SPL, U, NF, true, P, WPB, MINB><<<nb, 32 * WPB, 0, c->st>>>(                  \
+                c->Ml, 0, c->nzl, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l, c->partial.p, c->flag.p);       \
+    }
     SLAB_SWITCH(FX, v)
 #undef FX
     return nb;
@@ -569,13 +576,15 @@ static void back3_launch_p(Ctx* c, const float* w, double* out, const double* ba
             return;
         }
     }
-    const unsigned nb = nblk_warp(c, (c->N + S::G - 1) / S::G);
-#define BX1(NF, SG)                                                                                                \
-    if (bam) k_back3s<1, S::LPR, S::SPL, 4, NF, SG, P><<<nb, 256, 0, c->st>>>(                                     \
-        c->N, 0, c->nzl, c->order.p, c->cp.p, c->C.p, w, nullptr, bam, c->mu.p, c->Z0, c->flag.p);                 \
-    else k_back3s<0, S::LPR, S::SPL, 4, NF, SG, P><<<nb, 256, 0, c->st>>>(                                         \
-        c->N, 0, c->nzl, c->order.p, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);
-#define BX(NF) if (uns) { BX1(NF, false) } else { BX1(NF, true) }
+#define BX1(NF, U, WPB, MINB, SG)                                                                                  \
+    {                                                                                                              \
+        const unsigned nb = nblk_warp(c, (c->N + S::G - 1) / S::G) * (8 / WPB);                                    \
+        if (bam) k_back3s<1, S::LPR, S::SPL, U, NF, SG, P, WPB, MINB><<<nb, 32 * WPB, 0, c->st>>>(                 \
+            c->N, 0, c->nzl, c->order.p, c->cp.p, c->C.p, w, nullptr, bam, c->mu.p, c->Z0, c->flag.p);             \
+        else k_back3s<0, S::LPR, S::SPL, U, NF, SG, P, WPB, MINB><<<nb, 32 * WPB, 0, c->st>>>(                     \
+            c->N, 0, c->nzl, c->order.p, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);               \
+    }
+#define BX(NF, U, WPB, MINB) if (uns) { BX1(NF, U, WPB, MINB, false) } else { BX1(NF, U, WPB, MINB, true) }
     SLAB_SWITCH(BX, v)
 #undef BX
 #undef BX1
@@ -1480,6 +1489,8 @@ static void wam_step(Ctx* c) {
             switch (P) { case 32: S3E(32, 8) break; case 64: S3E(64, 2) break; default: S3E(128, 2) break; }
         } else if (c->split_variant == 3 && P >= 32) {   // two pipelined rounds of E entries
             switch (P) { case 32: S3E(32, 4) break; case 64: S3E(64, 4) break; default: S3E(128, 2) break; }
+        } else if (c->split_variant == 5 && P >= 32) {   // half the entries in flight, half the registers
+            switch (P) { case 32: S3EU(32, 4, 1) break; case 64: S3EU(64, 2, 1) break; default: S3EU(128, 1, 1) break; }
         } else if (c->split_variant == 4 && P >= 32) {
             switch (P) { case 32: S3EU(32, 4, 4) break; case 64: S3EU(64, 4, 4) break; default: S3EU(128, 2, 4) break; }
         } else {   // measured: cfg3 (64 slices) E=4 188 ms/run vs 364; cfg4 (128) E=2 1888 vs 2157 (E=4) / 2500;
