@@ -97,6 +97,22 @@ int wamgpu_destroy(wamgpu_ctx* ctx);
  * 128-byte ncclUniqueId shared by the caller.  Must precede the matrix. */
 int wamgpu_nccl_unique_id(void* id128);
 int wamgpu_set_comm(wamgpu_ctx* ctx, const void* id128, int rank, int nranks);
+/* In-process ranks: R contexts (any devices, one host thread each) joined
+ * under the same group key; collectives are rank-order device reductions
+ * between host barriers (bit-identical on every member).  group < 0: a
+ * DETACHED shard -- the context computes rank's share of an nranks-way
+ * partition alone and skips every exchange (timing one rank's work on one
+ * GPU; its results are not a reconstruction).  Must precede the matrix. */
+int wamgpu_set_comm_local(wamgpu_ctx* ctx, int group, int rank, int nranks);
+/* Rank grid: view_groups Rv x z groups
+ * Rz = nranks / Rv, rank = zg*Rv + vg.  2D: views only (Rv = nranks, the
+ * default).  Axial 3D: default Rv = 1 (z-slabs, scalars cross GPUs); Rv > 1
+ * also splits the views of each slab, whose ranks then sum their partial back
+ * projections [H^T q || b-] (fp64) every iteration.  After set_comm, before
+ * the matrix. */
+int wamgpu_set_partition(wamgpu_ctx* ctx, int view_groups);
+int wamgpu_get_partition(const wamgpu_ctx* ctx, int* view_groups, int* z_groups, int* slab_begin,
+                         int* slab_slices);
 
 /* Fused back projection + all-reduce over NVLink peer memory (view-sharded 2D,
  * DESIGN.md §7): replaces the back-projection kernel + ncclAllReduce of

@@ -60,6 +60,7 @@ EXPORTED = [
     "wamgpu_get_tree", "wamgpu_get_stats", "wamgpu_get_scalars", "wamgpu_get_z_rows", "wamgpu_get_timing",
     "wamgpu_set_kernel_timing", "wamgpu_rasterize", "wamgpu_simulate", "wamgpu_host_rays", "wamgpu_set_haar_dim",
     "wamgpu_p2p_export", "wamgpu_p2p_import", "wamgpu_selftest_fused_allreduce", "wamgpu_selftest_fused_back",
+    "wamgpu_set_comm_local", "wamgpu_set_partition", "wamgpu_get_partition",
 ]
 P2P_BLOB = 256   # WAMGPU_P2P_BLOB
 
@@ -224,6 +225,20 @@ class Context:
     # ---- setup
     def set_comm(self, uid: bytes, rank: int, nranks: int):
         _chk(load().wamgpu_set_comm(self.h, C.c_char_p(uid) if uid else None, int(rank), int(nranks)), self.h)
+
+    def set_comm_local(self, group: int, rank: int, nranks: int):
+        """In-process ranks (one host thread per context) joined under `group`;
+        group < 0: a detached shard (this rank's share alone, no exchange)."""
+        _chk(load().wamgpu_set_comm_local(self.h, int(group), int(rank), int(nranks)), self.h)
+
+    def set_partition(self, view_groups: int):
+        """Rank grid: view_groups x (nranks / view_groups) z groups (3D); 0 = default."""
+        _chk(load().wamgpu_set_partition(self.h, int(view_groups)), self.h)
+
+    def partition(self):
+        v = [C.c_int() for _ in range(4)]
+        _chk(load().wamgpu_get_partition(self.h, *[C.byref(x) for x in v]), self.h)
+        return dict(view_groups=v[0].value, z_groups=v[1].value, slab_begin=v[2].value, slab_slices=v[3].value)
 
     def p2p_export(self) -> bytes:
         """This rank's CUDA IPC handles for the fused back projection +

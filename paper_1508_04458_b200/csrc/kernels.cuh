@@ -627,6 +627,24 @@ __global__ void k_am_update(uint64_t N, const double* __restrict__ g, const doub
     }
 }
 
+// ------------------------------------------------ in-process rank groups
+// out[i] = p[0][i] (+|max) p[1][i] ... in rank order: the same result on every
+// member of an in-process group (wamgpu_set_comm_local).
+constexpr int GROUP_MAX = 16;
+struct GroupPtrs {
+    const double* p[GROUP_MAX];
+};
+__global__ void k_group_reduce(double* __restrict__ out, GroupPtrs g, int k, uint64_t n, int op) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        double a = g.p[0][i];
+        for (int j = 1; j < k; ++j) {
+            const double b = g.p[j][i];
+            a = op ? (b > a ? b : a) : a + b;
+        }
+        out[i] = a;
+    }
+}
+
 // ------------------------------------------------------- reductions / records
 // Single block: fixed-order sum of n partials -> out[0].
 __global__ void k_sum_partials(const double* __restrict__ part, int n, double* __restrict__ out) {

@@ -20,7 +20,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -69,6 +72,19 @@ struct DBuf {
 
 enum Cat { T_FWD = 0, T_BACK, T_SPLIT, T_UPDATE, T_EXPAND, T_COMM, T_NCAT };
 
+// In-process rank group (wamgpu_set_comm_local): R contexts driven by R host
+// threads of one process.  Collectives are a device-side rank-order reduction
+// over the members' staging buffers between two host barriers.
+struct LocalGroup {
+    std::mutex m;
+    std::condition_variable cv;
+    int n = 0, joined = 0, arrived = 0;
+    uint64_t gen = 0;
+    bool broken = false;
+    std::vector<double*> stage;   // per-rank device staging
+    std::vector<int> dev;
+};
+
 }  // namespace wamgpu
 
 using wamgpu::DBuf;
@@ -84,6 +100,16 @@ struct wamgpu_ctx {
     std::string err;
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1;
+    // rank grid (partition): Rv view groups x Rz z-slab groups, rank = zg*Rv + vg.
+    // comm_v: ranks sharing my slab (partial back projections are summed over
+    // it); comm_z: ranks sharing my views (z-summed criterion).  nullptr = the
+    // global comm (or no exchange when that group has one rank).
+    int vgroups_req = 0, Rv = 1, Rz = 1, vg = 0, zg = 0;
+    ncclComm_t comm_v = nullptr, comm_z = nullptr;
+    int comm_kind = 0;                  // 0 none, 1 NCCL, 2 in-process group, 3 detached shard
+    std::shared_ptr<wamgpu::LocalGroup> lg;
+    DBuf<double> gstage;                // in-process group staging
+    std::vector<int> peers_on;          // devices peer access was enabled to
     // grid / matrix
     int nx = 0, ny = 0, nz = 1;
     bool have_grid = false, have_matrix = false;
@@ -214,6 +240,8 @@ static bool trace_host() {
     } while (0)
 
 static thread_local std::string g_err;
+static std::mutex g_groups_m;
+static std::map<int, std::shared_ptr<LocalGroup>> g_groups;   // in-process rank groups by key
 
 // ------------------------------------------------------------- utilities
 static double cpow3_host(int l) {  // c^l, same sequence of multiplications as the device / oracle
@@ -265,18 +293,104 @@ static void sort_pairs(Ctx* c, DBuf<unsigned>& kin, DBuf<uint2>& vin, DBuf<unsig
     launched(c, 4);
 }
 
-static void allreduce_sum(Ctx* c, double* buf, size_t n) {
-    if (!c->comm) return;   // single GPU without a communicator
+// ---- collectives ------------------------------------------------------------
+// Scope of a reduction in the rank grid (partition()):
+//   ALL    every rank (objective, Z0, criterion max);
+//   VIEWS  the ranks holding the same z-slab and different views: the partial
+//          back projections [g || b-] of view shards are summed over it;
+//   SLABS  the ranks holding the same views and different z-slabs: the
+//          z-summed criterion image of the per-slice Haar model.
+enum Scope { S_ALL = 0, S_VIEWS, S_SLABS };
+
+static int scope_size(const Ctx* c, Scope s) {
+    return s == S_ALL ? c->nranks : (s == S_VIEWS ? c->Rv : c->Rz);
+}
+static std::vector<int> scope_members(const Ctx* c, Scope s) {
+    std::vector<int> m;
+    if (s == S_ALL) for (int r = 0; r < c->nranks; ++r) m.push_back(r);
+    else if (s == S_VIEWS) for (int v = 0; v < c->Rv; ++v) m.push_back(c->zg * c->Rv + v);
+    else for (int z = 0; z < c->Rz; ++z) m.push_back(z * c->Rv + c->vg);
+    return m;
+}
+
+static void group_barrier(LocalGroup& g) {
+    std::unique_lock<std::mutex> lk(g.m);
+    if (g.broken) throw CudaError("local group: broken by an earlier failure of a peer rank");
+    const uint64_t my = g.gen;
+    if (++g.arrived == g.n) {
+        g.arrived = 0;
+        ++g.gen;
+        g.cv.notify_all();
+        return;
+    }
+    const bool ok = g.cv.wait_for(lk, std::chrono::seconds(120), [&] { return g.gen != my || g.broken; });
+    if (!ok || g.broken) {
+        g.broken = true;
+        g.cv.notify_all();
+        throw CudaError("local group: a peer rank did not arrive within 120 s");
+    }
+}
+
+// in-process group: copy to my staging, barrier, rank-order reduction of the
+// members' staging into buf (identical on every member), barrier
+static void local_allreduce(Ctx* c, double* buf, size_t n, int op, const std::vector<int>& mem) {
+    LocalGroup& g = *c->lg;
+    if ((int)mem.size() > GROUP_MAX) throw ConfigError("local group: at most 16 ranks per reduction");
+    if (c->gstage.n < n) c->gstage.alloc(n);
+    {
+        std::lock_guard<std::mutex> lk(g.m);
+        g.stage[c->rank] = c->gstage.p;
+    }
+    CK(cudaMemcpyAsync(c->gstage.p, buf, n * 8, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    group_barrier(g);
+    GroupPtrs gp{};
+    {
+        std::lock_guard<std::mutex> lk(g.m);
+        for (size_t j = 0; j < mem.size(); ++j) {
+            gp.p[j] = g.stage[mem[j]];
+            const int d = g.dev[mem[j]];
+            if (d != c->device && std::find(c->peers_on.begin(), c->peers_on.end(), d) == c->peers_on.end()) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    throw CudaError(std::string("local group: no peer access: ") + cudaGetErrorString(e));
+                cudaGetLastError();
+                c->peers_on.push_back(d);
+            }
+        }
+    }
+    k_group_reduce<<<std::max<unsigned>(1, std::min<unsigned>(blocks_for(n, 256), c->sms * 8)), 256, 0, c->st>>>(
+        buf, gp, (int)mem.size(), n, op);
+    check_launch(c, "k_group_reduce");
+    CK(cudaStreamSynchronize(c->st));
+    group_barrier(g);
+}
+
+static void allreduce(Ctx* c, double* buf, size_t n, int op, Scope s) {
+    if (c->comm_kind == 0 || c->comm_kind == 3) return;   // single rank / detached shard
+    if (c->comm_kind == 1) {
+        ncclComm_t cm = s == S_ALL ? c->comm : (s == S_VIEWS ? c->comm_v : c->comm_z);
+        if (!cm) {
+            if (scope_size(c, s) == 1 && c->nranks > 1) return;   // a one-rank group: nothing to exchange
+            cm = c->comm;                                          // the group is the whole communicator
+        }
+        c->timer_begin(T_COMM);
+        NK(ncclAllReduce(buf, buf, n, ncclDouble, op ? ncclMax : ncclSum, cm, c->st));
+        c->timer_end(T_COMM);
+        return;
+    }
+    // in-process group: every rank calls every collective; one-rank scopes are
+    // skipped identically on all of them
+    if (scope_size(c, s) == 1) return;
     c->timer_begin(T_COMM);
-    NK(ncclAllReduce(buf, buf, n, ncclDouble, ncclSum, c->comm, c->st));
+    local_allreduce(c, buf, n, op, scope_members(c, s));
     c->timer_end(T_COMM);
 }
-static void allreduce_max(Ctx* c, double* buf, size_t n) {
-    if (!c->comm) return;
-    c->timer_begin(T_COMM);
-    NK(ncclAllReduce(buf, buf, n, ncclDouble, ncclMax, c->comm, c->st));
-    c->timer_end(T_COMM);
-}
+static void allreduce_sum(Ctx* c, double* buf, size_t n, Scope s = S_ALL) { allreduce(c, buf, n, 0, s); }
+static void allreduce_max(Ctx* c, double* buf, size_t n) { allreduce(c, buf, n, 1, S_ALL); }
+// view-sharded (partial back projections to sum); a 1-rank NCCL communicator
+// on a 2D problem also takes this path (tests the NCCL route bit-exactly)
+static bool view_sharded(const Ctx* c) { return c->Rv > 1 || (c->comm_kind == 1 && c->nz == 1); }
 
 static void check_flag(Ctx* c, const char* where) {
     int f = 0;
@@ -368,24 +482,43 @@ static void finish_matrix(Ctx* c) {
     c->algo = 0;
 }
 
-// Sharding: a 2D problem (nz == 1) shards VIEWS (contiguous
-// CSR rows, row = v*D + k, projector.hpp:123-125); an axial 3D stack shards
-// z-SLABS (every rank holds the whole in-plane matrix, rays never leave their
-// slice, geometry.hpp:17-20).
+// Sharding.  The ranks form an Rv x Rz grid, rank = zg*Rv + vg:
+// view group vg owns the contiguous CSR rows of views [V*vg/Rv, V*(vg+1)/Rv)
+// (row = v*D + k, projector.hpp:123-125) and z group zg owns slices
+// [nz*zg/Rz, nz*(zg+1)/Rz) (rays never leave their slice, geometry.hpp:17-20).
+// A 2D problem shards views only (Rv = R).  An axial 3D stack defaults to
+// z-slabs only (Rv = 1, scalars cross GPUs); wamgpu_set_partition picks Rv > 1
+// (view shards of a slab sum their partial back projections over comm_v).
+static void resolve_grid(Ctx* c) {
+    const int R = c->nranks;
+    int Rv = c->nz == 1 ? R : (c->vgroups_req > 0 ? c->vgroups_req : 1);
+    if (c->nz == 1 && c->vgroups_req > 0 && c->vgroups_req != R)
+        throw ConfigError("partition: a 2D problem shards views across all ranks");
+    if (Rv < 1 || R % Rv) throw ConfigError("partition: view groups must divide the rank count");
+    c->Rv = Rv;
+    c->Rz = R / Rv;
+    c->vg = c->rank % Rv;
+    c->zg = c->rank / Rv;
+    if (c->comm_kind == 1 && c->Rv > 1 && c->Rz > 1 && !c->comm_v) {   // collective over the whole comm
+        NK(ncclCommSplit(c->comm, c->zg, c->vg, &c->comm_v, nullptr));
+        NK(ncclCommSplit(c->comm, c->vg, c->zg, &c->comm_z, nullptr));
+    }
+}
+
 static void partition(Ctx* c, int views, int detectors) {
-    if (c->nz > 128) throw ConfigError("wamgpu: at most 128 slices per GPU slab");
+    if (c->nz > 128 * c->Rz) throw ConfigError("wamgpu: at most 128 slices per GPU slab");
+    resolve_grid(c);
+    const int v0 = (int)((int64_t)views * c->vg / c->Rv), v1 = (int)((int64_t)views * (c->vg + 1) / c->Rv);
+    c->row0 = (uint64_t)v0 * detectors;
+    c->row1 = (uint64_t)v1 * detectors;
     if (c->nz == 1) {
-        const int v0 = (int)((int64_t)views * c->rank / c->nranks), v1 = (int)((int64_t)views * (c->rank + 1) / c->nranks);
-        c->row0 = (uint64_t)v0 * detectors;
-        c->row1 = (uint64_t)v1 * detectors;
         c->s0 = 0;
         c->nzl = 1;
     } else {
-        c->row0 = 0;
-        c->row1 = c->M;
-        c->s0 = (int)((int64_t)c->nz * c->rank / c->nranks);
-        c->nzl = (int)((int64_t)c->nz * (c->rank + 1) / c->nranks) - c->s0;
-        if (c->nzl < 1) throw ConfigError("wamgpu: more ranks than slices");
+        c->s0 = (int)((int64_t)c->nz * c->zg / c->Rz);
+        c->nzl = (int)((int64_t)c->nz * (c->zg + 1) / c->Rz) - c->s0;
+        if (c->nzl < 1) throw ConfigError("wamgpu: more z groups than slices");
+        if (c->nzl > 128) throw ConfigError("wamgpu: at most 128 slices per GPU slab");
     }
     c->Ml = c->row1 - c->row0;
 }
@@ -443,16 +576,8 @@ static void set_matrix_csr(Ctx* c, uint64_t rows, uint64_t cols, uint64_t nnz, c
     c->M = rows;
     c->N = cols;
     if (!c->have_grid) { c->nx = (int)cols; c->ny = 1; c->nz = 1; }
-    // explicit matrices shard by contiguous row blocks (2D) or by z-slab (3D)
-    if (c->nz == 1) {
-        c->row0 = rows * c->rank / c->nranks;
-        c->row1 = rows * (c->rank + 1) / c->nranks;
-        c->Ml = c->row1 - c->row0;
-        c->s0 = 0;
-        c->nzl = 1;
-    } else {
-        partition(c, (int)rows, 1);
-    }
+    // explicit matrices shard by contiguous row blocks (views) and/or z-slab (3D)
+    partition(c, (int)rows, 1);
     const uint64_t k0 = rp[c->row0], k1 = rp[c->row1];
     c->nnz = k1 - k0;
     std::vector<unsigned long long> lrp(c->Ml + 1);
@@ -1182,7 +1307,7 @@ static void am_init(Ctx* c, const double* init_mu) {
         CK(cudaMemsetAsync(c->mu.p, 0, NV(c) * 4, c->st));
     }
     back_into(c, c->d.p, c->bam.p);  // b(x) = sum_y d(y) h(y|x)
-    if (c->nzl == 1) allreduce_sum(c, c->bam.p, c->N);
+    if (view_sharded(c)) allreduce_sum(c, c->bam.p, NV(c), S_VIEWS);
     if (!c->act.p) { c->act.alloc(1); }
     c->Z0 = compute_z0(c, 0, true);  // Z0 = max_y sum_x h(y|x)
     forward_fused(c, false);
@@ -1198,19 +1323,19 @@ static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
     if (c->algo != 1) throw ContractError("am: not initialised");
     ensure_records(c, n);
     for (int i = 0; i < n; ++i) {
-        if (!c->comm || c->nzl > 1) {
+        if (!view_sharded(c)) {
             back_launch(c, c->q.p, nullptr, c->bam.p);   // fused multiplicative update
         } else {
             const double* g = c->g.p;
-            if (c->ar.on) {   // fused back projection + all-reduce over NVLink peer memory
+            if (c->ar.on && c->nz == 1) {   // fused back projection + all-reduce over NVLink peer memory
                 back_allreduce(c, c->q.p, c->ar.extra.p);   // extra = zeros here
                 g = c->ar.res.p;
             } else {
                 back_into(c, c->q.p, c->g.p);
-                allreduce_sum(c, c->g.p, c->N);
+                allreduce_sum(c, c->g.p, NV(c), S_VIEWS);
             }
-            k_am_update<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, g, c->bam.p, c->mu.p, c->Z0, c->flag.p,
-                                                                   c->lgx);
+            k_am_update<<<blocks_for(NV(c), 256), 256, 0, c->st>>>(NV(c), g, c->bam.p, c->mu.p, c->Z0, c->flag.p,
+                                                                    c->nz == 1 ? c->lgx : -1);
             check_launch(c, "k_am_update");
         }
         CK(cudaMemsetAsync(c->counters.p, 0, 8, c->st));
@@ -1435,7 +1560,7 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     }
     // b(z) = [Omega^T H^T d](z) for every z
     back_into(c, c->d.p, c->g.p);
-    if (c->nzl == 1) allreduce_sum(c, c->g.p, N);
+    if (view_sharded(c)) allreduce_sum(c, c->g.p, N, S_VIEWS);
     tile_launch(c, 2, nullptr, c->bdata.p);
     CK(cudaMemsetAsync(c->g.p, 0, 2 * N * 8, c->st));
     if (c->ar.extra.p) CK(cudaMemsetAsync(c->ar.extra.p, 0, c->N * 8, c->st));   // fused path: no stale b-
@@ -1469,7 +1594,7 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
 static void wam_step(Ctx* c) {
     // view-sharded 2D with peer memory: split first (its partial b- rides along
     // as the second half of the fused back projection + all-reduce)
-    const bool fused = c->ar.on && c->nzl == 1 && !c->haar3;
+    const bool fused = c->ar.on && c->nz == 1 && !c->haar3;
     double* bm2 = fused ? c->ar.extra.p : c->g.p + c->N;
     if (!fused) back_into(c, c->q.p, c->g.p);
     if (c->haar3 && c->nlist3) {
@@ -1539,8 +1664,8 @@ static void wam_step(Ctx* c) {
         if (!c->nlist) CK(cudaMemsetAsync(c->ar.extra.p, 0, c->N * 8, c->st));
         back_allreduce(c, c->q.p, c->ar.extra.p);
         CK(cudaMemcpyAsync(c->g.p, c->ar.res.p, 2 * c->N * 8, cudaMemcpyDeviceToDevice, c->st));
-    } else if (c->nzl == 1) {
-        allreduce_sum(c, c->g.p, 2 * c->N);   // view shards: partial sums
+    } else if (view_sharded(c)) {
+        allreduce_sum(c, c->g.p, 2 * NV(c), S_VIEWS);   // view shards: partial sums of [g || b-]
     }
     c->timer_begin(T_UPDATE);
     tile_launch(c, 1, nullptr, nullptr);
@@ -1608,7 +1733,7 @@ static int64_t wam_expand(Ctx* c, double factor) {
         c->dscratch.ensure(c->N);
         k_zsum<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->nzl, slab_stride(c), c->mu64.p, c->dscratch.p);
         check_launch(c, "k_zsum");
-        allreduce_sum(c, c->dscratch.p, c->N);
+        allreduce_sum(c, c->dscratch.p, c->N, S_SLABS);
         crit = c->dscratch.p;
     }
     const double mx = device_max(c, crit, c->N);
@@ -1696,7 +1821,11 @@ static void destroy(Ctx* c) {
     if (c->ev_a) cudaEventDestroy(c->ev_a);
     if (c->ev_b) cudaEventDestroy(c->ev_b);
     for (void* p : c->ar.opened) cudaIpcCloseMemHandle(p);
+    if (c->comm_v) ncclCommDestroy(c->comm_v);
+    if (c->comm_z) ncclCommDestroy(c->comm_z);
     if (c->comm) ncclCommDestroy(c->comm);
+    c->gstage.release();
+    c->lg.reset();
     c->A.release(); c->C.release(); c->E.release();
     for (int k = 0; k < 2; ++k) {
         if (c->pin[k]) cudaFreeHost(c->pin[k]);
@@ -1758,21 +1887,85 @@ int wamgpu_nccl_unique_id(void* id128) {
     })
 }
 
+static void reset_comm(Ctx* c) {
+    if (c->comm_v) { ncclCommDestroy(c->comm_v); c->comm_v = nullptr; }
+    if (c->comm_z) { ncclCommDestroy(c->comm_z); c->comm_z = nullptr; }
+    if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
+    c->lg.reset();
+    c->comm_kind = 0;
+    c->rank = 0;
+    c->nranks = 1;
+}
+
 int wamgpu_set_comm(wamgpu_ctx* ctx, const void* id128, int rank, int nranks) {
     API_TRY(ctx, {
         NEED(ctx);
         if (nranks < 1 || rank < 0 || rank >= nranks) throw ContractError("set_comm: bad rank/nranks");
         if (ctx->have_matrix) throw ContractError("set_comm must precede the system matrix");
-        if (ctx->comm) { ncclCommDestroy(ctx->comm); ctx->comm = nullptr; }
-        ctx->rank = rank;
-        ctx->nranks = nranks;
+        reset_comm(ctx);
         if (id128) {   // nranks == 1 with an id: a 1-rank communicator (exercises the NCCL path)
             ncclUniqueId id;
             std::memcpy(&id, id128, sizeof(id));
             NK(ncclCommInitRank(&ctx->comm, nranks, id, rank));
+            ctx->comm_kind = 1;
         } else if (nranks > 1) {
             throw ContractError("set_comm: an ncclUniqueId is required for nranks > 1");
         }
+        ctx->rank = rank;
+        ctx->nranks = nranks;
+    })
+}
+
+int wamgpu_set_comm_local(wamgpu_ctx* ctx, int group, int rank, int nranks) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw ContractError("set_comm_local: bad rank/nranks");
+        if (ctx->have_matrix) throw ContractError("set_comm_local must precede the system matrix");
+        reset_comm(ctx);
+        ctx->rank = rank;
+        ctx->nranks = nranks;
+        if (group < 0) {          // detached shard: this rank's share alone, no exchange
+            ctx->comm_kind = nranks > 1 ? 3 : 0;
+            return WAMGPU_OK;
+        }
+        std::shared_ptr<LocalGroup> g;
+        {
+            std::lock_guard<std::mutex> lk(g_groups_m);
+            auto& slot = g_groups[group];
+            if (!slot || slot->broken || slot->joined == slot->n) {   // a fresh group under this key
+                slot = std::make_shared<LocalGroup>();
+                slot->n = nranks;
+                slot->stage.assign(nranks, nullptr);
+                slot->dev.assign(nranks, -1);
+            }
+            if (slot->n != nranks) throw ContractError("set_comm_local: nranks differs from the group's");
+            if (slot->dev[rank] != -1) throw ContractError("set_comm_local: rank already joined");
+            slot->dev[rank] = ctx->device;
+            slot->joined++;
+            g = slot;
+        }
+        ctx->lg = g;
+        ctx->comm_kind = nranks > 1 ? 2 : 0;
+    })
+}
+
+int wamgpu_set_partition(wamgpu_ctx* ctx, int view_groups) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (ctx->have_matrix) throw ContractError("set_partition must precede the system matrix");
+        if (view_groups < 0 || (view_groups > 0 && ctx->nranks % view_groups))
+            throw ConfigError("set_partition: view groups must divide the rank count");
+        ctx->vgroups_req = view_groups;
+    })
+}
+
+int wamgpu_get_partition(const wamgpu_ctx* ctx, int* rv, int* rz, int* s0, int* nzl) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (rv) *rv = ctx->Rv;
+        if (rz) *rz = ctx->Rz;
+        if (s0) *s0 = ctx->s0;
+        if (nzl) *nzl = ctx->nzl;
     })
 }
 
@@ -2070,7 +2263,7 @@ int wamgpu_back_project(wamgpu_ctx* ctx, const double* w, double* out) {
         c->dscratch.ensure(NV(c));
         upload_slab<float>(c, w, c->fscratch.p, c->Ml, c->Ml, 0, true);
         back_into(c, c->fscratch.p, c->dscratch.p, false);
-        if (c->nzl == 1) allreduce_sum(c, c->dscratch.p, c->N);
+        if (view_sharded(c)) allreduce_sum(c, c->dscratch.p, NV(c), S_VIEWS);
         download_slab<double>(c, c->dscratch.p, out, c->N, c->N, 0);
     })
 }
