@@ -47,6 +47,12 @@ def _args():
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--nz", type=int, default=None,
                     help="override the slice count of a 3D config (one z-slab shard of an R-GPU run = nz/R)")
+    ap.add_argument("--view-groups", type=int, default=None,
+                    help="3D rank grid: Rv view groups x R/Rv z-slab groups (default 1: z-slabs only)")
+    ap.add_argument("--shard", type=int, default=None,
+                    help="N=1: time rank --shard-rank of an R-rank grid ALONE on this GPU (detached shard: "
+                         "its views/slab, no exchange) and project the R-GPU step with a modelled all-reduce")
+    ap.add_argument("--shard-rank", type=int, default=0)
     return ap.parse_args()
 
 
@@ -236,6 +242,48 @@ def run_reference(args):
     return 0
 
 
+# NCCL all-reduce bus bandwidth of 8 B200 ranks over NVSwitch at 1 GiB
+# (/opt/skills/guides/B200_PROFILING.md) and a small-message latency allowance
+ALLREDUCE_BUSBW_GBS = 725.0
+SMALL_COLLECTIVE_US = 20.0
+
+
+def _shard_projection(args, cfg, algo, J, part, ctx, ms_step, comm_ms):
+    """Projected R-GPU step of the rank grid from one detached shard timed alone:
+    t_R = t_shard + J * (t_collectives of the view group + scalars).
+    NCCL times of S total bytes over n ranks at bus bandwidth B: all-reduce
+    S*2(n-1)/n/B; reduce-scatter and all-gather S*(n-1)/n/B.  With the split
+    update (wamgpu.cu tile_update_split / am_split_update) the view group
+    reduce-scatters [g || b-] (fp64) and all-gathers {mu, beta} (fp32); without
+    it, it all-reduces [g || b-]."""
+    R, Rv = args.shard, part["view_groups"]
+    nzl = part["slab_slices"]
+    P = 1 if cfg["nz"] == 1 else max(8, 1 << (nzl - 1).bit_length())
+    B = ALLREDUCE_BUSBW_GBS * 1e9
+    split = (os.environ.get("WAMGPU_VIEW_UPDATE") != "allreduce" and cfg["nz"] > 1 and Rv > 1 and
+             ((algo == "am" and cfg["ny"] % Rv == 0) or
+              (algo == "wam" and cfg["haar"] == 3 and (cfg["ny"] >> cfg["L"]) % Rv == 0)))
+    if Rv == 1:
+        S, kind, t_c = 0, "none", 0.0
+    elif split:
+        ne = ctx.N * (P if algo == "am" else nzl)
+        s_rs, s_ag = (8 * ne, 4 * ne) if algo == "am" else (16 * ne, 8 * ne)
+        S, kind = s_rs + s_ag, "reduce-scatter [g || b-] fp64 + all-gather {mu, beta} fp32"
+        t_c = (s_rs + s_ag) * (Rv - 1) / Rv / B * 1e3
+    else:
+        S, kind = (2 if algo == "wam" else 1) * 8 * ctx.N * P, "all-reduce [g || b-] fp64"
+        t_c = S * 2 * (Rv - 1) / Rv / B * 1e3
+    t_small = SMALL_COLLECTIVE_US * 1e-3   # the objective SUM every iteration
+    proj = ms_step + J * (t_c + t_small)
+    return {"ranks": R, "rank": args.shard_rank, "view_groups": Rv, "z_groups": part["z_groups"],
+            "slab": [part["slab_begin"], nzl], "rows": [ctx.row0, ctx.row1], "collective": kind,
+            "collective_bytes_per_iter": S, "collective_ms_model": t_c, "small_collective_ms_model": t_small,
+            "projected_ms_per_step": proj,
+            "model": f"t_shard + J*(NCCL time at {ALLREDUCE_BUSBW_GBS:g} GB/s bus bandwidth + {SMALL_COLLECTIVE_US:g} us)",
+            "note": "detached shard: this rank's views and slab timed alone on one B200; the tree it grows "
+                    "follows its partial data, not the joint reconstruction's"}
+
+
 def main():
     args = _args()
     if args.impl == "reference":
@@ -259,7 +307,12 @@ def main():
     if world > 1:
         uid = plumb.bcast_bytes(W.nccl_unique_id() if rank == 0 else b"")
         ctx.set_comm(uid, rank, world)
+    elif args.shard:
+        ctx.set_comm_local(-1, args.shard_rank, args.shard)
+    if cfg["nz"] > 1 and args.view_groups:
+        ctx.set_partition(args.view_groups)
     ctx.set_geometry(g)
+    part = ctx.partition()
     collective = "none" if world == 1 else "nccl"
     if world > 1 and cfg["nz"] == 1 and os.environ.get("WAMGPU_P2P", "1") != "0":
         # fused back projection + all-reduce over NVLink peer memory: exchange
@@ -365,7 +418,7 @@ def main():
         except Exception:
             pass
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and not args.shard:
             try:
                 cores = os.cpu_count() or 1
                 p, tb, tinit = cpu_reference(cfg, algo, args.cpu_iters, threads=cores, inputs=(I0, d))
@@ -387,7 +440,8 @@ def main():
             "data": "synthetic (seeded luggage phantom, seeded Poisson counts; product host simulator)",
             "config": {"workload": _workload_desc(cfg, nnz, algo, J), "step": "init_state + run (all iterations"
                        " and expansions)", "l2": "working set (H CSR+CSC = 16 B/nnz) >> 126 MB L2; no flush needed",
-                       "parallelism": f"views/{world}" if cfg["nz"] == 1 else f"z-slabs/{world}",
+                       "parallelism": (f"views/{world}" if cfg["nz"] == 1 else
+                                       f"views/{part['view_groups']} x z-slabs/{part['z_groups']}"),
                        "collective": collective},
             "ray_voxel_updates_per_s": 2 * nnz * nz * J / (ms_step * 1e-3),
             "final_objective": final_obj,
@@ -409,6 +463,8 @@ def main():
             "wall_s_timed": wall,
             "cpu_baseline": cpu,
         }
+        if args.shard:
+            line["shard"] = _shard_projection(args, cfg, algo, J, part, ctx, ms_step, comm_ms)
         print(json.dumps(line), flush=True)
     ctx.close()
     plumb.close()

@@ -188,6 +188,123 @@ __global__ void k_tile3h(int mode, int nx, int ny, int nzl, int P, int L, const 
     }
 }
 
+// ------------------------------------------ view-group update (RS / AG)
+// The Rv ranks of a slab split its tiles by tile rows: member r owns tile rows
+// [r*TY/Rv, (r+1)*TY/Rv).  Chunk r of the tile-major exchange buffers holds
+// those tiles, tile (kt, ti, tj) at local index ((ti - t0)*TX + tj)*TZ + kt,
+// element e = (i*TS + j)*TS + z (z fastest, like the voxel slab).
+//   reduce-scatter buffer T: chunk r = [g of its tiles (CT) || b- of its tiles (CT)]
+//   all-gather buffer U: chunk r = [float2 {mu, beta} of its tiles (CT) || 2 u64 counts]
+struct TileChunks { int TX, TZ, rows; uint64_t CT; };   // rows = tile rows per member
+
+// T <- (g voxel slab, b- Mallat) of every tile; one CTA per tile
+__global__ void k_pack3h(int nx, int ny, int nzl, int P, int L, TileChunks tc, const double* __restrict__ g,
+                         const double* __restrict__ bm, const uint8_t* __restrict__ act, ActOff off,
+                         double* __restrict__ T) {
+    const int TS = 1 << L, T3 = TS * TS * TS;
+    const int tj = blockIdx.x, ti = blockIdx.y, kt = blockIdx.z;
+    const int r = ti / tc.rows;
+    const uint64_t base = (uint64_t)r * 2 * tc.CT + ((uint64_t)((ti - r * tc.rows) * tc.TX + tj) * tc.TZ + kt) * T3;
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
+        T[base + e] = g[((uint64_t)(ti * TS + i) * nx + (tj * TS + j)) * P + (kt * TS + z)];
+        const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, L, nx, ny, nzl, P, act, off);
+        T[base + tc.CT + e] = ci.approx ? 0.0 : bm[ci.idx];
+    }
+}
+
+// k_tile3h mode 1 over this member's tiles, inputs from its summed chunk Ts,
+// outputs {mu, beta} + counts into its U chunk (beta and mu land everywhere
+// through the all-gather and k_unpack3h)
+__global__ void k_tile3h_own(int nx, int ny, int nzl, int P, int L, TileChunks tc, int t0,
+                             const double* __restrict__ Ts, const double* __restrict__ bdata,
+                             const uint8_t* __restrict__ act, ActOff off, const float* __restrict__ beta,
+                             float2* __restrict__ U, double* __restrict__ bp_out, double* __restrict__ bm_out,
+                             double Z0, int* __restrict__ flag) {
+    extern __shared__ double smh[];
+    const int TS = 1 << L, T3 = TS * TS * TS;
+    double* x = smh;
+    double* t = smh + T3;
+    const int tj = blockIdx.x, ti = t0 + blockIdx.y, kt = blockIdx.z;
+    const uint64_t lt = ((uint64_t)blockIdx.y * tc.TX + tj) * tc.TZ + kt;
+    const double* gs = Ts + lt * T3;
+    const double* bs = Ts + tc.CT + lt * T3;
+    float2* u = U + lt * T3;
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
+        x[(z * TS + i) * TS + j] = gs[e];
+    }
+    __syncthreads();
+    cube_fwd(x, t, TS, L);
+    unsigned long long upd = 0, deg = 0;
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
+        const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, L, nx, ny, nzl, P, act, off);
+        float bo = beta[ci.idx];
+        const double bmv = ci.approx ? 0.0 : bs[e];
+        const double bpv = x[(z * TS + i) * TS + j] - bmv;
+        if (bp_out) { bp_out[ci.idx] = bpv; bm_out[ci.idx] = bmv; }
+        if (ci.active) {
+            double nb;
+            const int rr = solve_update(bdata[ci.idx], bpv, bmv, Z0, (double)bo, &nb);
+            if (rr == 0) {
+                if (!isfinite(nb)) atomicOr(flag, 4);
+                bo = (float)nb;
+                ++upd;
+            } else if (rr == 2) {
+                ++deg;
+            }
+        }
+        u[e].y = bo;
+        x[(z * TS + i) * TS + j] = (double)bo;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        upd += __shfl_xor_sync(0xffffffffu, upd, o);
+        deg += __shfl_xor_sync(0xffffffffu, deg, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long* cnt = reinterpret_cast<unsigned long long*>(U + tc.CT);
+        if (upd) atomicAdd(cnt + 0, upd);
+        if (deg) atomicAdd(cnt + 1, deg);
+    }
+    __syncthreads();
+    cube_inv(x, t, TS, L);
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
+        u[e].x = (float)x[(z * TS + i) * TS + j];
+    }
+}
+
+// every tile: U -> mu (voxel slab) and beta (Mallat); block (0,0,0) adds the
+// members' counts (rank order) to the cumulative counters
+__global__ void k_unpack3h(int nx, int ny, int nzl, int P, int L, TileChunks tc, int members,
+                           const float2* __restrict__ U, const uint8_t* __restrict__ act, ActOff off,
+                           float* __restrict__ mu, float* __restrict__ beta,
+                           unsigned long long* __restrict__ counters) {
+    const int TS = 1 << L, T3 = TS * TS * TS;
+    const int tj = blockIdx.x, ti = blockIdx.y, kt = blockIdx.z;
+    const int r = ti / tc.rows;
+    const uint64_t CU = tc.CT + 2;   // float2 units per chunk (2 for the counts)
+    const float2* u = U + r * CU + ((uint64_t)((ti - r * tc.rows) * tc.TX + tj) * tc.TZ + kt) * T3;
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
+        const float2 v = u[e];
+        mu[((uint64_t)(ti * TS + i) * nx + (tj * TS + j)) * P + (kt * TS + z)] = v.x;
+        const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, L, nx, ny, nzl, P, act, off);
+        beta[ci.idx] = v.y;
+    }
+    if (threadIdx.x == 0 && tj == 0 && ti == 0 && kt == 0) {
+        unsigned long long a = 0, b = 0;
+        for (int m = 0; m < members; ++m) {
+            const unsigned long long* cnt = reinterpret_cast<const unsigned long long*>(U + m * CU + tc.CT);
+            a += cnt[0];
+            b += cnt[1];
+        }
+        counters[0] += a;
+        counters[1] += b;
+    }
+}
+
 // ------------------------------------------------------------ criterion
 __global__ void k_max_slab(const double* __restrict__ v, uint64_t n, int nzl, int P, double* __restrict__ part) {
     double m = -DBL_MAX;

@@ -109,6 +109,8 @@ struct wamgpu_ctx {
     int comm_kind = 0;                  // 0 none, 1 NCCL, 2 in-process group, 3 detached shard
     std::shared_ptr<wamgpu::LocalGroup> lg;
     DBuf<double> gstage;                // in-process group staging
+    DBuf<double> rs_send, rs_recv;      // view-group update: reduce-scatter buffers (tile-major)
+    DBuf<float2> ag_send, ag_recv;      // view-group update: all-gather buffers {mu, beta}
     std::vector<int> peers_on;          // devices peer access was enabled to
     // grid / matrix
     int nx = 0, ny = 0, nz = 1;
@@ -331,6 +333,17 @@ static void group_barrier(LocalGroup& g) {
     }
 }
 
+// the reduction kernels read the members' staging directly: peer access to
+// every other device of the group
+static void ensure_peer(Ctx* c, int d) {
+    if (d == c->device || std::find(c->peers_on.begin(), c->peers_on.end(), d) != c->peers_on.end()) return;
+    const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        throw CudaError(std::string("local group: no peer access: ") + cudaGetErrorString(e));
+    cudaGetLastError();
+    c->peers_on.push_back(d);
+}
+
 // in-process group: copy to my staging, barrier, rank-order reduction of the
 // members' staging into buf (identical on every member), barrier
 static void local_allreduce(Ctx* c, double* buf, size_t n, int op, const std::vector<int>& mem) {
@@ -349,14 +362,7 @@ static void local_allreduce(Ctx* c, double* buf, size_t n, int op, const std::ve
         std::lock_guard<std::mutex> lk(g.m);
         for (size_t j = 0; j < mem.size(); ++j) {
             gp.p[j] = g.stage[mem[j]];
-            const int d = g.dev[mem[j]];
-            if (d != c->device && std::find(c->peers_on.begin(), c->peers_on.end(), d) == c->peers_on.end()) {
-                const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
-                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
-                    throw CudaError(std::string("local group: no peer access: ") + cudaGetErrorString(e));
-                cudaGetLastError();
-                c->peers_on.push_back(d);
-            }
+            ensure_peer(c, g.dev[mem[j]]);
         }
     }
     k_group_reduce<<<std::max<unsigned>(1, std::min<unsigned>(blocks_for(n, 256), c->sms * 8)), 256, 0, c->st>>>(
@@ -386,6 +392,86 @@ static void allreduce(Ctx* c, double* buf, size_t n, int op, Scope s) {
     local_allreduce(c, buf, n, op, scope_members(c, s));
     c->timer_end(T_COMM);
 }
+// my index in the members of scope s (rank order)
+static int scope_index(const Ctx* c, Scope s) { return s == S_ALL ? c->rank : (s == S_VIEWS ? c->vg : c->zg); }
+
+static ncclComm_t scope_comm(const Ctx* c, Scope s) {
+    ncclComm_t cm = s == S_ALL ? c->comm : (s == S_VIEWS ? c->comm_v : c->comm_z);
+    return cm ? cm : c->comm;   // nullptr: the group is the whole communicator (or has one rank)
+}
+
+// recv (chunk doubles) = rank-order sum over the scope's members of their
+// send[idx*chunk, (idx+1)*chunk) -- idx = my index in the scope
+static void reduce_scatter(Ctx* c, const double* send, double* recv, size_t chunk, Scope s) {
+    const int n = scope_size(c, s);
+    if (n == 1 || c->comm_kind == 0 || c->comm_kind == 3) {
+        CK(cudaMemcpyAsync(recv, send + (size_t)scope_index(c, s) * chunk, chunk * 8, cudaMemcpyDeviceToDevice, c->st));
+        return;
+    }
+    c->timer_begin(T_COMM);
+    if (c->comm_kind == 1) {
+        NK(ncclReduceScatter(send, recv, chunk, ncclDouble, ncclSum, scope_comm(c, s), c->st));
+    } else {
+        LocalGroup& g = *c->lg;
+        const std::vector<int> mem = scope_members(c, s);
+        if ((int)mem.size() > GROUP_MAX) throw ConfigError("local group: at most 16 ranks per reduction");
+        const size_t tot = chunk * mem.size();
+        if (c->gstage.n < tot) c->gstage.alloc(tot);
+        { std::lock_guard<std::mutex> lk(g.m); g.stage[c->rank] = c->gstage.p; }
+        CK(cudaMemcpyAsync(c->gstage.p, send, tot * 8, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        group_barrier(g);
+        GroupPtrs gp{};
+        {
+            std::lock_guard<std::mutex> lk(g.m);
+            for (size_t j = 0; j < mem.size(); ++j) {
+                gp.p[j] = g.stage[mem[j]] + (size_t)scope_index(c, s) * chunk;
+                ensure_peer(c, g.dev[mem[j]]);
+            }
+        }
+        k_group_reduce<<<std::max<unsigned>(1, std::min<unsigned>(blocks_for(chunk, 256), c->sms * 8)), 256, 0,
+                         c->st>>>(recv, gp, (int)mem.size(), chunk, 0);
+        check_launch(c, "k_group_reduce");
+        CK(cudaStreamSynchronize(c->st));
+        group_barrier(g);
+    }
+    c->timer_end(T_COMM);
+}
+
+// recv (n x bytes) = the members' send (bytes each) in rank order
+static void all_gather(Ctx* c, const void* send, void* recv, size_t bytes, Scope s) {
+    const int n = scope_size(c, s);
+    char* rb = static_cast<char*>(recv);
+    if (n == 1 || c->comm_kind == 0 || c->comm_kind == 3) {
+        if (rb + (size_t)scope_index(c, s) * bytes != send)
+            CK(cudaMemcpyAsync(rb + (size_t)scope_index(c, s) * bytes, send, bytes, cudaMemcpyDeviceToDevice, c->st));
+        return;
+    }
+    c->timer_begin(T_COMM);
+    if (c->comm_kind == 1) {
+        NK(ncclAllGather(send, recv, bytes, ncclUint8, scope_comm(c, s), c->st));
+    } else {
+        LocalGroup& g = *c->lg;
+        const std::vector<int> mem = scope_members(c, s);
+        const size_t nd = (bytes + 7) / 8;
+        if (c->gstage.n < nd) c->gstage.alloc(nd);
+        { std::lock_guard<std::mutex> lk(g.m); g.stage[c->rank] = c->gstage.p; }
+        CK(cudaMemcpyAsync(c->gstage.p, send, bytes, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        group_barrier(g);
+        std::vector<const double*> src;
+        {
+            std::lock_guard<std::mutex> lk(g.m);
+            for (int m : mem) src.push_back(g.stage[m]);
+        }
+        for (size_t j = 0; j < src.size(); ++j)
+            CK(cudaMemcpyAsync(rb + j * bytes, src[j], bytes, cudaMemcpyDefault, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        group_barrier(g);
+    }
+    c->timer_end(T_COMM);
+}
+
 static void allreduce_sum(Ctx* c, double* buf, size_t n, Scope s = S_ALL) { allreduce(c, buf, n, 0, s); }
 static void allreduce_max(Ctx* c, double* buf, size_t n) { allreduce(c, buf, n, 1, S_ALL); }
 // view-sharded (partial back projections to sum); a 1-rank NCCL communicator
@@ -630,7 +716,9 @@ static unsigned nblk_warp(const Ctx* c, uint64_t n) {
 template <int P> struct SlabShape {
     static constexpr int LPR = P <= 16 ? 4 : (P <= 64 ? 8 : 16), SPL = P / LPR, G = 32 / LPR;
 };
-// X(NF, U, WPB, MINB): F2F share, gathers per round, warps per CTA, min CTAs per SM
+// X(NF, U, WPB, MINB): F2F share, gathers per round, warps per CTA, min CTAs per SM.
+// The default needs MINB = 2: (256, 1) lets ptxas take 170 registers (1 CTA, 8 warps
+// per SM) and the slab passes ran 1.65x slower (cfg5 13.5 vs 8.1 ms per forward).
 #define SLAB_SWITCH(X, V)                                                                                          \
     switch (V) {                                                                                                   \
         case 3: X(2, 4, 8, 1) break;                                                                               \
@@ -641,7 +729,7 @@ template <int P> struct SlabShape {
         case 14: X(3, 2, 4, 5) break;                                                                              \
         case 15: X(3, 4, 4, 1) break;                                                                              \
         case 16: X(3, 2, 4, 6) break;                                                                              \
-        default: X(3, 4, 8, 1) break;                                                                              \
+        default: X(3, 4, 8, 2) break;                                                                              \
     }
 template <int MODE, int P>
 static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxblk, bool nonneg) {
@@ -1319,6 +1407,26 @@ static void am_init(Ctx* c, const double* init_mu) {
     c->active = (int64_t)c->N * c->nz;
 }
 
+// View groups of a 3D slab (Rv > 1) can split the update instead of
+// replicating it: reduce-scatter the partial back projections by image rows,
+// update only the member's rows (AM) or tile rows (3D Haar), all-gather the
+// result.  Moves 24 instead of 32 bytes per coefficient (WAM) and 12 instead of
+// 16 (AM) through the collective, and divides the update by Rv.
+// WAMGPU_VIEW_UPDATE=allreduce keeps the all-reduce + replicated update.
+static bool split_update_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("WAMGPU_VIEW_UPDATE");
+        return !(e && std::strcmp(e, "allreduce") == 0);
+    }();
+    return on;
+}
+static bool am_split_update(const Ctx* c) {
+    return c->nz > 1 && c->Rv > 1 && split_update_enabled() && c->ny % c->Rv == 0;
+}
+static bool wam_split_update(const Ctx* c) {
+    return c->nz > 1 && c->haar3 && c->Rv > 1 && split_update_enabled() && ((c->ny >> c->L) % c->Rv) == 0;
+}
+
 static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
     if (c->algo != 1) throw ContractError("am: not initialised");
     ensure_records(c, n);
@@ -1327,6 +1435,21 @@ static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
             back_launch(c, c->q.p, nullptr, c->bam.p);   // fused multiplicative update
         } else {
             const double* g = c->g.p;
+            if (am_split_update(c)) {   // 3D view group: reduce-scatter g, own rows, all-gather mu
+                back_into(c, c->q.p, c->g.p);
+                const uint64_t CA = NV(c) / c->Rv, o = CA * c->vg;
+                c->rs_recv.ensure(CA);
+                reduce_scatter(c, c->g.p, c->rs_recv.p, CA, S_VIEWS);
+                k_am_update<<<blocks_for(CA, 256), 256, 0, c->st>>>(CA, c->rs_recv.p, c->bam.p + o, c->mu.p + o,
+                                                                     c->Z0, c->flag.p, -1);
+                check_launch(c, "k_am_update");
+                all_gather(c, c->mu.p + o, c->mu.p, CA * 4, S_VIEWS);
+                CK(cudaMemsetAsync(c->counters.p, 0, 8, c->st));
+                forward_fused(c, true);
+                CK(cudaEventRecord(c->ev_iter[i], c->st));
+                c->iter++;
+                continue;
+            }
             if (c->ar.on && c->nz == 1) {   // fused back projection + all-reduce over NVLink peer memory
                 back_allreduce(c, c->q.p, c->ar.extra.p);   // extra = zeros here
                 g = c->ar.res.p;
@@ -1591,6 +1714,47 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     c->active = count_active(c);
 }
 
+// separable 3D Haar update split over the view group (kernels3h.cuh k_pack3h,
+// k_tile3h_own, k_unpack3h): pack [g || b-] tile-major, reduce-scatter by tile
+// rows, update own tiles, all-gather {mu, beta} + counts, unpack everywhere
+static void tile_update_split(Ctx* c) {
+    const int TS = 1 << c->L;
+    TileChunks tc;
+    tc.TX = c->nx >> c->L;
+    tc.TZ = c->nzl >> c->L;
+    const int TY = c->ny >> c->L;
+    tc.rows = TY / c->Rv;
+    tc.CT = (uint64_t)tc.rows * tc.TX * tc.TZ * TS * TS * TS;
+    const uint64_t CU = tc.CT + 2;
+    c->rs_send.ensure(2 * tc.CT * c->Rv);
+    c->rs_recv.ensure(2 * tc.CT);
+    c->ag_send.ensure(CU);
+    c->ag_recv.ensure(CU * c->Rv);
+    const int P = slab_stride(c);
+    c->timer_begin(T_UPDATE);
+    k_pack3h<<<dim3(tc.TX, TY, tc.TZ), 256, 0, c->st>>>(c->nx, c->ny, c->nzl, P, c->L, tc, c->g.p, c->g.p + NV(c),
+                                                        c->act.p, c->off, c->rs_send.p);
+    check_launch(c, "k_pack3h");
+    c->timer_end(T_UPDATE);
+    reduce_scatter(c, c->rs_send.p, c->rs_recv.p, 2 * tc.CT, S_VIEWS);
+    c->timer_begin(T_UPDATE);
+    CK(cudaMemsetAsync(c->ag_send.p + tc.CT, 0, 16, c->st));
+    const size_t smem = 2ull * TS * TS * TS * sizeof(double);
+    if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(k_tile3h_own, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_tile3h_own<<<dim3(tc.TX, tc.rows, tc.TZ), 256, smem, c->st>>>(
+        c->nx, c->ny, c->nzl, P, c->L, tc, c->vg * tc.rows, c->rs_recv.p, c->bdata.p, c->act.p, c->off, c->beta.p,
+        c->ag_send.p, c->bp_dbg.p, c->bm_dbg.p, c->Z0, c->flag.p);
+    check_launch(c, "k_tile3h_own");
+    c->timer_end(T_UPDATE);
+    all_gather(c, c->ag_send.p, c->ag_recv.p, CU * sizeof(float2), S_VIEWS);
+    c->timer_begin(T_UPDATE);
+    k_unpack3h<<<dim3(tc.TX, TY, tc.TZ), 256, 0, c->st>>>(c->nx, c->ny, c->nzl, P, c->L, tc, c->Rv, c->ag_recv.p,
+                                                          c->act.p, c->off, c->mu.p, c->beta.p, c->counters.p);
+    check_launch(c, "k_unpack3h");
+    c->timer_end(T_UPDATE);
+}
+
 static void wam_step(Ctx* c) {
     // view-sharded 2D with peer memory: split first (its partial b- rides along
     // as the second half of the fused back projection + all-reduce)
@@ -1664,6 +1828,11 @@ static void wam_step(Ctx* c) {
         if (!c->nlist) CK(cudaMemsetAsync(c->ar.extra.p, 0, c->N * 8, c->st));
         back_allreduce(c, c->q.p, c->ar.extra.p);
         CK(cudaMemcpyAsync(c->g.p, c->ar.res.p, 2 * c->N * 8, cudaMemcpyDeviceToDevice, c->st));
+    } else if (wam_split_update(c)) {
+        tile_update_split(c);
+        c->tm.update_launches++;
+        forward_fused(c, true);
+        return;
     } else if (view_sharded(c)) {
         allreduce_sum(c, c->g.p, 2 * NV(c), S_VIEWS);   // view shards: partial sums of [g || b-]
     }

@@ -74,6 +74,7 @@ def _run(wam, cfg, I0, d, algo, haar, grid, sched):
                 res["obj"] = obj
             res["mu"] = c.image()
             res["part"] = c.partition()
+            res["scal"] = c.scalars()
             out[r] = res
         except Exception as e:  # re-raised below
             errs.append(e)
@@ -93,12 +94,14 @@ def _run(wam, cfg, I0, d, algo, haar, grid, sched):
 CASES = [
     ("tiny3d16", "am", 2, (2, 1)),
     ("tiny3d16", "am", 2, (2, 2)),
+    ("tiny3d16", "am", 2, (3, 1)),          # 32 rows % 3: all-reduce + replicated update
     ("tiny3d16", "wam", 2, (3, 1)),
     ("tiny3d16", "wam", 2, (2, 2)),
     ("tiny3d16", "wam", 3, (2, 1)),
     ("tiny3d16", "wam", 3, (4, 1)),
     ("tiny3d16", "wam", 3, (2, 2)),
     ("tiny3d16", "wam", 3, (1, 2)),
+    ("tiny3d24", "wam", 3, (3, 1)),         # 4 tile rows % 3: all-reduce + replicated update
 ]
 
 
@@ -119,6 +122,9 @@ def test_sharded3d_matches_unsharded(wam, orc, name, algo, haar, grid):
         # every rank reports the global objective
         assert rel_l2(res["obj"], ref["obj"]) < TOL, f"rank {r}"
         assert res["obj"] == out[0]["obj"]
+        if Rz == 1:   # slab-local counters: the whole stack here
+            for k in ("cum_updates", "degenerate", "active_set"):
+                assert res["scal"][k] == ref["scal"][k], (r, k)
         if algo == "wam":
             assert res["z0"] == ref["z0"], f"rank {r}: Z0 differs"
             for t, tref in zip(res["trees"], ref["trees"]):
