@@ -248,7 +248,7 @@ ALLREDUCE_BUSBW_GBS = 725.0
 SMALL_COLLECTIVE_US = 20.0
 
 
-def _shard_projection(args, cfg, algo, J, part, ctx, ms_step, comm_ms):
+def _shard_projection(args, cfg, algo, J, part, ctx, ms_step, split_ms_step):
     """Projected R-GPU step of the rank grid from one detached shard timed alone:
     t_R = t_shard + J * (t_collectives of the view group + scalars).
     NCCL times of S total bytes over n ranks at bus bandwidth B: all-reduce
@@ -270,6 +270,12 @@ def _shard_projection(args, cfg, algo, J, part, ctx, ms_step, comm_ms):
         s_rs, s_ag = (8 * ne, 4 * ne) if algo == "am" else (16 * ne, 8 * ne)
         S, kind = s_rs + s_ag, "reduce-scatter [g || b-] fp64 + all-gather {mu, beta} fp32"
         t_c = (s_rs + s_ag) * (Rv - 1) / Rv / B * 1e3
+        if algo == "wam":
+            # the g half of the reduce-scatter runs on a side stream during the
+            # signed split (wamgpu.cu wam_step): only what the split cannot hide counts
+            t_g = 8 * ne * (Rv - 1) / Rv / B * 1e3
+            t_c -= min(t_g, split_ms_step / J)
+            kind += " (g half overlapped with the split)"
     else:
         S, kind = (2 if algo == "wam" else 1) * 8 * ctx.N * P, "all-reduce [g || b-] fp64"
         t_c = S * 2 * (Rv - 1) / Rv / B * 1e3
@@ -280,8 +286,47 @@ def _shard_projection(args, cfg, algo, J, part, ctx, ms_step, comm_ms):
             "collective_bytes_per_iter": S, "collective_ms_model": t_c, "small_collective_ms_model": t_small,
             "projected_ms_per_step": proj,
             "model": f"t_shard + J*(NCCL time at {ALLREDUCE_BUSBW_GBS:g} GB/s bus bandwidth + {SMALL_COLLECTIVE_US:g} us)",
-            "note": "detached shard: this rank's views and slab timed alone on one B200; the tree it grows "
-                    "follows its partial data, not the joint reconstruction's"}
+            "note": "detached shard: this rank's views and slab timed alone on one B200, replaying the "
+                    "joint reconstruction's tree at each scheduled expansion (criterion still computed)"}
+
+
+def _joint_trees(W, cfg, g, I0, d, device, sched):
+    """Trees after each scheduled expansion of the unsharded run on this GPU."""
+    c = W.Context(device)
+    c.set_geometry(g)
+    if cfg["nz"] > 1:
+        c.set_haar_dim(cfg["haar"])
+    c.set_data(d, I0)
+    c.wam_init(cfg["L"])
+    trees, done = [], 0
+    for ev in sched:
+        c.wam_iterate(ev - done)
+        done = ev
+        c.wam_expand(0.1)
+        trees.append(c.tree())
+    c.close()
+    return trees
+
+
+def _slab_tree(tree, cfg, s0, nzl):
+    """z-slab [s0, s0+nzl) of a separable-3D tree (level l: (nz>>l, ny>>l, nx>>l))."""
+    out, o = [], 0
+    for l in range(1, cfg["L"] + 1):
+        nb = (cfg["nx"] >> l) * (cfg["ny"] >> l)
+        lv = tree[o:o + nb * (cfg["nz"] >> l)].reshape(cfg["nz"] >> l, nb)
+        out.append(lv[s0 >> l:(s0 + nzl) >> l].ravel())
+        o += nb * (cfg["nz"] >> l)
+    return np.concatenate(out)
+
+
+def _sum_timing(ts):
+    out = dict(ts[0])
+    for t in ts[1:]:
+        for k, v in t.items():
+            if k != "split_nnz":
+                out[k] += v
+    out["split_nnz"] = ts[-1]["split_nnz"]
+    return out
 
 
 def main():
@@ -303,6 +348,12 @@ def main():
     plumb = Plumbing(rank, world)
 
     g, I0, d = _inputs(cfg, W)
+    joint_trees = None
+    if args.shard and algo == "wam":
+        # the joint reconstruction's trees (the R-rank run reproduces the
+        # unsharded tree bit-exactly, tests/test_gpu_sharded3d.py): the shard
+        # replays them instead of growing its own from partial data
+        joint_trees = _joint_trees(W, cfg, g, I0, d, local, sched)
     ctx = W.Context(local)
     if world > 1:
         uid = plumb.bcast_bytes(W.nccl_unique_id() if rank == 0 else b"")
@@ -327,7 +378,23 @@ def main():
     ctx.set_data(d, I0)
     nnz_local = ctx.nnz
 
+    if joint_trees is not None and cfg["nz"] > 1 and cfg["haar"] == 3:
+        joint_trees = [_slab_tree(t, cfg, part["slab_begin"], part["slab_slices"]) for t in joint_trees]
+
     def step_device():
+        if algo == "wam" and joint_trees is not None:   # shard: replay the joint tree
+            ctx.wam_init(cfg["L"])
+            t_init = ctx.timing()
+            recs, tms, done = [], [], 0
+            for k, ev in enumerate(sched + [J]):
+                recs += ctx.wam_iterate(ev - done)
+                tms.append(ctx.timing())
+                done = ev
+                if ev == J:
+                    break
+                ctx.wam_expand(float("inf"), add_tree=joint_trees[k])
+                tms.append(ctx.timing())
+            return t_init, _sum_timing(tms), recs
         if algo == "wam":
             ctx.wam_init(cfg["L"])
             t_init = ctx.timing()
@@ -464,7 +531,7 @@ def main():
             "cpu_baseline": cpu,
         }
         if args.shard:
-            line["shard"] = _shard_projection(args, cfg, algo, J, part, ctx, ms_step, comm_ms)
+            line["shard"] = _shard_projection(args, cfg, algo, J, part, ctx, ms_step, split_ms / args.steps)
         print(json.dumps(line), flush=True)
     ctx.close()
     plumb.close()

@@ -177,6 +177,13 @@ int wamgpu_wam_iterate(wamgpu_ctx* ctx, int n, wamgpu_record* recs);
 int wamgpu_wam_expand(wamgpu_ctx* ctx, double factor, int64_t* newly_active_blocks);
 int wamgpu_wam_run(wamgpu_ctx* ctx, int iters, const int* schedule, int nsched, double factor,
                    wamgpu_record* recs);
+/* expand_tree with extra blocks: the union of the criterion's marks and the
+ * caller's tree `bits` (layout of wamgpu_get_tree, nbytes = its size; it must
+ * satisfy the parent closure, as any tree from get_tree does).  Resumes a tree
+ * manifest, or replays another run's tree (factor = +inf: the given blocks
+ * only, with the criterion still computed). */
+int wamgpu_wam_expand_with(wamgpu_ctx* ctx, double factor, const uint8_t* bits, uint64_t nbytes,
+                           int64_t* newly_active_blocks);
 
 /* state read-back */
 int wamgpu_get_image(const wamgpu_ctx* ctx, double* mu);   /* AM: mu; WAM: Omega*beta (fp32 storage) */

@@ -60,7 +60,7 @@ EXPORTED = [
     "wamgpu_get_tree", "wamgpu_get_stats", "wamgpu_get_scalars", "wamgpu_get_z_rows", "wamgpu_get_timing",
     "wamgpu_set_kernel_timing", "wamgpu_rasterize", "wamgpu_simulate", "wamgpu_host_rays", "wamgpu_set_haar_dim",
     "wamgpu_p2p_export", "wamgpu_p2p_import", "wamgpu_selftest_fused_allreduce", "wamgpu_selftest_fused_back",
-    "wamgpu_set_comm_local", "wamgpu_set_partition", "wamgpu_get_partition",
+    "wamgpu_set_comm_local", "wamgpu_set_partition", "wamgpu_get_partition", "wamgpu_wam_expand_with",
 ]
 P2P_BLOB = 256   # WAMGPU_P2P_BLOB
 
@@ -339,9 +339,16 @@ class Context:
         _chk(load().wamgpu_wam_iterate(self.h, int(n), recs), self.h)
         return _records(recs[:n])
 
-    def wam_expand(self, factor=0.1):
+    def wam_expand(self, factor=0.1, add_tree=None):
+        """expand_tree; add_tree: blocks of another tree (get_tree
+        layout) activated together with the criterion's marks."""
         n = C.c_int64()
-        _chk(load().wamgpu_wam_expand(self.h, C.c_double(factor), C.byref(n)), self.h)
+        if add_tree is None:
+            _chk(load().wamgpu_wam_expand(self.h, C.c_double(factor), C.byref(n)), self.h)
+        else:
+            t = np.ascontiguousarray(add_tree, np.uint8)
+            _chk(load().wamgpu_wam_expand_with(self.h, C.c_double(factor), _p(t, C.c_uint8), C.c_uint64(t.size),
+                                               C.byref(n)), self.h)
         return n.value
 
     def wam_run(self, iters, schedule=(), factor=0.1):

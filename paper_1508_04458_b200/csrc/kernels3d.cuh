@@ -286,13 +286,45 @@ __global__ void __launch_bounds__(32 * WPB, MINB) k_fwd3s(uint64_t M, int sbeg, 
     }
 }
 
+// Tile-major layout of the view-group split update (wamgpu.cu tile_update_split):
+// the Rv members of a slab own tile rows [r*rows, (r+1)*rows) of the 2^L-cube
+// tiles; chunk r of a tile-major buffer holds them, tile (kt, ti, tj) at local
+// index ((ti - r*rows)*TX + tj)*TZ + kt, element (i*TS + j)*TS + z.  L = 0: off
+// (plain voxel slab / Mallat layout).
+struct TileMap {
+    int L = 0, TX = 0, TZ = 0, rows = 1, nx = 0, ny = 0, nzl = 0;
+    uint64_t CT = 0;   // elements per chunk
+};
+__device__ __forceinline__ uint64_t tile_elem(const TileMap& m, int iy, int ix, int s) {
+    const int TS = 1 << m.L;
+    const int ti = iy >> m.L, tj = ix >> m.L, kt = s >> m.L;
+    const int r = ti / m.rows;
+    const uint64_t lt = ((uint64_t)(ti - r * m.rows) * m.TX + tj) * m.TZ + kt;
+    return (uint64_t)r * m.CT + lt * (uint64_t)(TS * TS * TS) +
+           (uint64_t)(((iy & (TS - 1)) * TS + (ix & (TS - 1))) * TS + (s & (TS - 1)));
+}
+// voxel x (= iy*nx + ix), slice s
+__device__ __forceinline__ uint64_t tile_pos(const TileMap& m, uint64_t x, int s) {
+    return tile_elem(m, (int)(x / (unsigned)m.nx), (int)(x % (unsigned)m.nx), s);
+}
+// level-l detail coefficient at slab Mallat coordinates (yy, xx, zz): its cube
+// position inside the tile holding it (the inverse of kernels3h coef_info3)
+__device__ __forceinline__ uint64_t coef_tile_pos(const TileMap& m, int l, int yy, int xx, int zz) {
+    const int hl = m.ny >> l, wl = m.nx >> l, dl = m.nzl >> l, sh = m.L - l, half = 1 << sh;
+    const int yh = yy >= hl, xh = xx >= wl, zh = zz >= dl;
+    const int bi = yy - yh * hl, bj = xx - xh * wl, bk = zz - zh * dl;
+    const int i = yh * half + (bi & (half - 1)), j = xh * half + (bj & (half - 1)), z = zh * half + (bk & (half - 1));
+    return tile_elem(m, ((bi >> sh) << m.L) + i, ((bj >> sh) << m.L) + j, ((bk >> sh) << m.L) + z);
+}
+
 // K3 3D v2: one warp = G voxels of the tile order; MODE as k_back3.
 template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P, int WPB = 8, int MINB = 1>
 __global__ void __launch_bounds__(32 * WPB, MINB) k_back3s(uint64_t N, int sbeg, int nz, const unsigned* __restrict__ order,
                                                 const unsigned long long* __restrict__ cp,
                                                 const uint2* __restrict__ C, const float* __restrict__ w,
                                                 double* __restrict__ g, const double* __restrict__ bam,
-                                                float* __restrict__ mu, double Z0, int* __restrict__ flag) {
+                                                float* __restrict__ mu, double Z0, int* __restrict__ flag,
+                                                TileMap tmap) {
     constexpr int G = 32 / LPR, SB = LPR * SPL;
     static_assert(P % SB == 0, "slab parts");
     __shared__ __align__(16) SlabStage<G> s_st[WPB];
@@ -314,7 +346,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB) k_back3s(uint64_t N, int sbeg,
             if (s >= nz) continue;
             const uint64_t id = x * P + s;
             if (MODE == 0) {
-                g[id] = acc[j];
+                g[tmap.L ? tile_pos(tmap, x, s) : id] = acc[j];   // tile-major: view-group split update
             } else {
                 const double b = bam[id], c = acc[j];
                 if (b > 0.0 && c > 0.0) {

@@ -189,47 +189,32 @@ __global__ void k_tile3h(int mode, int nx, int ny, int nzl, int P, int L, const 
 }
 
 // ------------------------------------------ view-group update (RS / AG)
-// The Rv ranks of a slab split its tiles by tile rows: member r owns tile rows
-// [r*TY/Rv, (r+1)*TY/Rv).  Chunk r of the tile-major exchange buffers holds
-// those tiles, tile (kt, ti, tj) at local index ((ti - t0)*TX + tj)*TZ + kt,
-// element e = (i*TS + j)*TS + z (z fastest, like the voxel slab).
-//   reduce-scatter buffer T: chunk r = [g of its tiles (CT) || b- of its tiles (CT)]
-//   all-gather buffer U: chunk r = [float2 {mu, beta} of its tiles (CT) || 2 u64 counts]
-struct TileChunks { int TX, TZ, rows; uint64_t CT; };   // rows = tile rows per member
+// Exchange buffers in the tile-major chunk layout of TileMap (kernels3d.cuh):
+//   T (reduce-scatter): [g of all chunks (Rv*CT) || b- of all chunks (Rv*CT)],
+//     written directly by k_back3s / k_split3h_e (tmap.L != 0);
+//   U (all-gather), float chunks of CU = 2*CT + 4: [mu plane (CT) || beta
+//     plane (CT) || 2 u64 counts].  The member's own U chunk is where its
+//     tiles' beta lives between iterations; the slab-Mallat beta is refreshed
+//     from the gathered planes only when read (expansion, get_beta).
+__host__ __device__ inline uint64_t u_chunk(const TileMap& m) { return 2 * m.CT + 4; }
 
-// T <- (g voxel slab, b- Mallat) of every tile; one CTA per tile
-__global__ void k_pack3h(int nx, int ny, int nzl, int P, int L, TileChunks tc, const double* __restrict__ g,
-                         const double* __restrict__ bm, const uint8_t* __restrict__ act, ActOff off,
-                         double* __restrict__ T) {
-    const int TS = 1 << L, T3 = TS * TS * TS;
-    const int tj = blockIdx.x, ti = blockIdx.y, kt = blockIdx.z;
-    const int r = ti / tc.rows;
-    const uint64_t base = (uint64_t)r * 2 * tc.CT + ((uint64_t)((ti - r * tc.rows) * tc.TX + tj) * tc.TZ + kt) * T3;
-    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
-        const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
-        T[base + e] = g[((uint64_t)(ti * TS + i) * nx + (tj * TS + j)) * P + (kt * TS + z)];
-        const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, L, nx, ny, nzl, P, act, off);
-        T[base + tc.CT + e] = ci.approx ? 0.0 : bm[ci.idx];
-    }
-}
-
-// k_tile3h mode 1 over this member's tiles, inputs from its summed chunk Ts,
-// outputs {mu, beta} + counts into its U chunk (beta and mu land everywhere
-// through the all-gather and k_unpack3h)
-__global__ void k_tile3h_own(int nx, int ny, int nzl, int P, int L, TileChunks tc, int t0,
-                             const double* __restrict__ Ts, const double* __restrict__ bdata,
-                             const uint8_t* __restrict__ act, ActOff off, const float* __restrict__ beta,
-                             float2* __restrict__ U, double* __restrict__ bp_out, double* __restrict__ bm_out,
-                             double Z0, int* __restrict__ flag) {
+// k_tile3h mode 1 over this member's tiles: inputs from its summed chunks
+// (gs = g part, bs = b- part), beta from / to its U chunk, mu into its U chunk
+__global__ void k_tile3h_own(TileMap tm, int P, int t0, const double* __restrict__ gs,
+                             const double* __restrict__ bs, const double* __restrict__ bdata,
+                             const uint8_t* __restrict__ act, ActOff off, float* __restrict__ U,
+                             double* __restrict__ bp_out, double* __restrict__ bm_out, double Z0,
+                             int* __restrict__ flag) {
     extern __shared__ double smh[];
-    const int TS = 1 << L, T3 = TS * TS * TS;
+    const int L = tm.L, TS = 1 << L, T3 = TS * TS * TS;
     double* x = smh;
     double* t = smh + T3;
     const int tj = blockIdx.x, ti = t0 + blockIdx.y, kt = blockIdx.z;
-    const uint64_t lt = ((uint64_t)blockIdx.y * tc.TX + tj) * tc.TZ + kt;
-    const double* gs = Ts + lt * T3;
-    const double* bs = Ts + tc.CT + lt * T3;
-    float2* u = U + lt * T3;
+    const uint64_t lt = ((uint64_t)blockIdx.y * tm.TX + tj) * tm.TZ + kt;
+    gs += lt * T3;
+    bs += lt * T3;
+    float* um = U + lt * T3;
+    float* ub = U + tm.CT + lt * T3;
     for (int e = threadIdx.x; e < T3; e += blockDim.x) {
         const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
         x[(z * TS + i) * TS + j] = gs[e];
@@ -239,8 +224,8 @@ __global__ void k_tile3h_own(int nx, int ny, int nzl, int P, int L, TileChunks t
     unsigned long long upd = 0, deg = 0;
     for (int e = threadIdx.x; e < T3; e += blockDim.x) {
         const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
-        const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, L, nx, ny, nzl, P, act, off);
-        float bo = beta[ci.idx];
+        const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, L, tm.nx, tm.ny, tm.nzl, P, act, off);
+        float bo = ub[e];
         const double bmv = ci.approx ? 0.0 : bs[e];
         const double bpv = x[(z * TS + i) * TS + j] - bmv;
         if (bp_out) { bp_out[ci.idx] = bpv; bm_out[ci.idx] = bmv; }
@@ -250,12 +235,12 @@ __global__ void k_tile3h_own(int nx, int ny, int nzl, int P, int L, TileChunks t
             if (rr == 0) {
                 if (!isfinite(nb)) atomicOr(flag, 4);
                 bo = (float)nb;
+                ub[e] = bo;
                 ++upd;
             } else if (rr == 2) {
                 ++deg;
             }
         }
-        u[e].y = bo;
         x[(z * TS + i) * TS + j] = (double)bo;
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -263,7 +248,7 @@ __global__ void k_tile3h_own(int nx, int ny, int nzl, int P, int L, TileChunks t
         deg += __shfl_xor_sync(0xffffffffu, deg, o);
     }
     if ((threadIdx.x & 31) == 0) {
-        unsigned long long* cnt = reinterpret_cast<unsigned long long*>(U + tc.CT);
+        unsigned long long* cnt = reinterpret_cast<unsigned long long*>(U + 2 * tm.CT);
         if (upd) atomicAdd(cnt + 0, upd);
         if (deg) atomicAdd(cnt + 1, deg);
     }
@@ -271,37 +256,53 @@ __global__ void k_tile3h_own(int nx, int ny, int nzl, int P, int L, TileChunks t
     cube_inv(x, t, TS, L);
     for (int e = threadIdx.x; e < T3; e += blockDim.x) {
         const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
-        u[e].x = (float)x[(z * TS + i) * TS + j];
+        um[e] = (float)x[(z * TS + i) * TS + j];
     }
 }
 
-// every tile: U -> mu (voxel slab) and beta (Mallat); block (0,0,0) adds the
-// members' counts (rank order) to the cumulative counters
-__global__ void k_unpack3h(int nx, int ny, int nzl, int P, int L, TileChunks tc, int members,
-                           const float2* __restrict__ U, const uint8_t* __restrict__ act, ActOff off,
-                           float* __restrict__ mu, float* __restrict__ beta,
-                           unsigned long long* __restrict__ counters) {
-    const int TS = 1 << L, T3 = TS * TS * TS;
-    const int tj = blockIdx.x, ti = blockIdx.y, kt = blockIdx.z;
-    const int r = ti / tc.rows;
-    const uint64_t CU = tc.CT + 2;   // float2 units per chunk (2 for the counts)
-    const float2* u = U + r * CU + ((uint64_t)((ti - r * tc.rows) * tc.TX + tj) * tc.TZ + kt) * T3;
-    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+// every chunk's mu plane -> the voxel slab (grid-stride over elements, z
+// fastest on both sides); thread 0 adds the members' counts (rank order)
+__global__ void k_unpack_mu(TileMap tm, int P, int members, const float* __restrict__ U, float* __restrict__ mu,
+                            unsigned long long* __restrict__ counters) {
+    const int TS = 1 << tm.L, T3 = TS * TS * TS;
+    const uint64_t CU = u_chunk(tm), n = tm.CT * (uint64_t)members;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = k / tm.CT, w = k % tm.CT, lt = w / T3;
+        const int e = (int)(w % T3);
+        const int kt = (int)(lt % tm.TZ), tj = (int)((lt / tm.TZ) % tm.TX), ti = (int)(lt / ((uint64_t)tm.TZ * tm.TX)) +
+                       (int)r * tm.rows;
         const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
-        const float2 v = u[e];
-        mu[((uint64_t)(ti * TS + i) * nx + (tj * TS + j)) * P + (kt * TS + z)] = v.x;
-        const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, L, nx, ny, nzl, P, act, off);
-        beta[ci.idx] = v.y;
+        mu[((uint64_t)(ti * TS + i) * tm.nx + (tj * TS + j)) * P + (kt * TS + z)] = U[r * CU + w];
     }
-    if (threadIdx.x == 0 && tj == 0 && ti == 0 && kt == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long a = 0, b = 0;
         for (int m = 0; m < members; ++m) {
-            const unsigned long long* cnt = reinterpret_cast<const unsigned long long*>(U + m * CU + tc.CT);
+            const unsigned long long* cnt = reinterpret_cast<const unsigned long long*>(U + m * CU + 2 * tm.CT);
             a += cnt[0];
             b += cnt[1];
         }
         counters[0] += a;
         counters[1] += b;
+    }
+}
+
+// beta planes <-> slab Mallat beta.  dir 0: every chunk's plane -> beta (the
+// lazy refresh); dir 1: beta -> the member's own plane (at wam_init)
+__global__ void k_beta_planes(TileMap tm, int P, int r0, int nchunks, float* __restrict__ U, float* __restrict__ beta,
+                              const uint8_t* __restrict__ act, ActOff off, int dir) {
+    const int TS = 1 << tm.L, T3 = TS * TS * TS;
+    const uint64_t CU = u_chunk(tm), n = tm.CT * (uint64_t)nchunks;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t rr = k / tm.CT, w = k % tm.CT, lt = w / T3;
+        const int r = r0 + (int)rr;
+        const int e = (int)(w % T3);
+        const int kt = (int)(lt % tm.TZ), tj = (int)((lt / tm.TZ) % tm.TX), ti = (int)(lt / ((uint64_t)tm.TZ * tm.TX)) +
+                       r * tm.rows;
+        const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
+        const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, tm.L, tm.nx, tm.ny, tm.nzl, P, act, off);
+        float* up = U + (dir ? 0 : (uint64_t)r * CU) + tm.CT + w;
+        if (dir) *up = beta[ci.idx];
+        else beta[ci.idx] = *up;
     }
 }
 
@@ -511,7 +512,7 @@ __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __
                                                  int nzl, const unsigned long long* __restrict__ ptr,
                                                  const unsigned* __restrict__ eray, const float4* __restrict__ epsi,
                                                  const float* __restrict__ q, const uint8_t* __restrict__ act,
-                                                 ActOff off, ActOff koff, double* __restrict__ bm) {
+                                                 ActOff off, ActOff koff, double* __restrict__ bm, TileMap tmap) {
     using V = typename SlabVec<SPL>::T;
     constexpr int P = 32 * SPL;
     constexpr int NG = SPL >= 2 ? SPL / 2 : 1;   // slice groups per lane (pairs, or the single slice)
@@ -607,7 +608,8 @@ __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __
             for (int t = 0; t < 7; ++t) {
                 double sum = 0.0;
                 for (int gg = g0; gg < g1; ++gg) sum += red[wib][t][gg];
-                bm[((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]] = sum;
+                bm[tmap.L ? coef_tile_pos(tmap, l, yy[t], xx[t], zz[t]) : ((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]] =
+                    sum;
             }
         }
         __syncwarp();
@@ -628,7 +630,8 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
                                                    int nzl, const unsigned long long* __restrict__ ptr,
                                                    const unsigned* __restrict__ eray, const float4* __restrict__ epsi,
                                                    const float* __restrict__ q, const uint8_t* __restrict__ act,
-                                                   ActOff off, ActOff koff, double* __restrict__ bm) {
+                                                   ActOff off, ActOff koff, double* __restrict__ bm,
+                                                   TileMap tmap) {
     constexpr int LPE = 32 / E, S = P * E / 32, NG = S / 2;
     static_assert(S >= 2 && S % 4 == 0, "slices per lane: a multiple of 4");
     __shared__ double red[4][7][P / 2];
@@ -737,7 +740,8 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
             for (int t = 0; t < 7; ++t) {
                 double sum = 0.0;
                 for (int gg = g0; gg < g1; ++gg) sum += red[wib][t][gg];
-                bm[((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]] = sum;
+                bm[tmap.L ? coef_tile_pos(tmap, l, yy[t], xx[t], zz[t]) : ((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]] =
+                    sum;
             }
         }
         __syncwarp();

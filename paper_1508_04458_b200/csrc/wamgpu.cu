@@ -110,8 +110,12 @@ struct wamgpu_ctx {
     std::shared_ptr<wamgpu::LocalGroup> lg;
     DBuf<double> gstage;                // in-process group staging
     DBuf<double> rs_send, rs_recv;      // view-group update: reduce-scatter buffers (tile-major)
-    DBuf<float2> ag_send, ag_recv;      // view-group update: all-gather buffers {mu, beta}
+    DBuf<float> ag_send, ag_recv;       // view-group update: all-gather buffers {mu, beta planes, counts}
+    bool beta_dirty = false;            // slab-Mallat beta behind the gathered beta planes
+    cudaStream_t st2 = nullptr;         // side stream (overlapped reduce-scatter)
+    cudaEvent_t ev_x = nullptr, ev_y = nullptr;
     std::vector<int> peers_on;          // devices peer access was enabled to
+    const uint8_t* add_tree = nullptr;  // wamgpu_wam_expand_with: caller blocks (host, act_bytes)
     // grid / matrix
     int nx = 0, ny = 0, nz = 1;
     bool have_grid = false, have_matrix = false;
@@ -402,15 +406,17 @@ static ncclComm_t scope_comm(const Ctx* c, Scope s) {
 
 // recv (chunk doubles) = rank-order sum over the scope's members of their
 // send[idx*chunk, (idx+1)*chunk) -- idx = my index in the scope
-static void reduce_scatter(Ctx* c, const double* send, double* recv, size_t chunk, Scope s) {
+static void reduce_scatter(Ctx* c, const double* send, double* recv, size_t chunk, Scope s, cudaStream_t st = nullptr) {
+    if (!st) st = c->st;
+    const bool timed = st == c->st;   // device timers live on the main stream
     const int n = scope_size(c, s);
     if (n == 1 || c->comm_kind == 0 || c->comm_kind == 3) {
-        CK(cudaMemcpyAsync(recv, send + (size_t)scope_index(c, s) * chunk, chunk * 8, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(recv, send + (size_t)scope_index(c, s) * chunk, chunk * 8, cudaMemcpyDeviceToDevice, st));
         return;
     }
-    c->timer_begin(T_COMM);
+    if (timed) c->timer_begin(T_COMM);
     if (c->comm_kind == 1) {
-        NK(ncclReduceScatter(send, recv, chunk, ncclDouble, ncclSum, scope_comm(c, s), c->st));
+        NK(ncclReduceScatter(send, recv, chunk, ncclDouble, ncclSum, scope_comm(c, s), st));
     } else {
         LocalGroup& g = *c->lg;
         const std::vector<int> mem = scope_members(c, s);
@@ -418,8 +424,8 @@ static void reduce_scatter(Ctx* c, const double* send, double* recv, size_t chun
         const size_t tot = chunk * mem.size();
         if (c->gstage.n < tot) c->gstage.alloc(tot);
         { std::lock_guard<std::mutex> lk(g.m); g.stage[c->rank] = c->gstage.p; }
-        CK(cudaMemcpyAsync(c->gstage.p, send, tot * 8, cudaMemcpyDeviceToDevice, c->st));
-        CK(cudaStreamSynchronize(c->st));
+        CK(cudaMemcpyAsync(c->gstage.p, send, tot * 8, cudaMemcpyDeviceToDevice, st));
+        CK(cudaStreamSynchronize(st));
         group_barrier(g);
         GroupPtrs gp{};
         {
@@ -430,21 +436,27 @@ static void reduce_scatter(Ctx* c, const double* send, double* recv, size_t chun
             }
         }
         k_group_reduce<<<std::max<unsigned>(1, std::min<unsigned>(blocks_for(chunk, 256), c->sms * 8)), 256, 0,
-                         c->st>>>(recv, gp, (int)mem.size(), chunk, 0);
+                         st>>>(recv, gp, (int)mem.size(), chunk, 0);
         check_launch(c, "k_group_reduce");
-        CK(cudaStreamSynchronize(c->st));
+        CK(cudaStreamSynchronize(st));
         group_barrier(g);
     }
-    c->timer_end(T_COMM);
+    if (timed) c->timer_end(T_COMM);
 }
 
 // recv (n x bytes) = the members' send (bytes each) in rank order
 static void all_gather(Ctx* c, const void* send, void* recv, size_t bytes, Scope s) {
     const int n = scope_size(c, s);
     char* rb = static_cast<char*>(recv);
-    if (n == 1 || c->comm_kind == 0 || c->comm_kind == 3) {
+    if (n == 1 || c->comm_kind == 0) {
         if (rb + (size_t)scope_index(c, s) * bytes != send)
             CK(cudaMemcpyAsync(rb + (size_t)scope_index(c, s) * bytes, send, bytes, cudaMemcpyDeviceToDevice, c->st));
+        return;
+    }
+    if (c->comm_kind == 3) {   // detached shard: own chunk into every slot (finite, locally timed data)
+        for (int j = 0; j < n; ++j)
+            if (rb + (size_t)j * bytes != send)
+                CK(cudaMemcpyAsync(rb + (size_t)j * bytes, send, bytes, cudaMemcpyDeviceToDevice, c->st));
         return;
     }
     c->timer_begin(T_COMM);
@@ -775,7 +787,7 @@ static unsigned fwd3_launch(Ctx* c, const float* mu, double* l, unsigned maxblk,
     return nb;
 }
 template <int P>
-static void back3_launch_p(Ctx* c, const float* w, double* out, const double* bam, bool nonneg) {
+static void back3_launch_p(Ctx* c, const float* w, double* out, const double* bam, bool nonneg, const TileMap& tm) {
     using S = SlabShape<P>;
     const int v = c->slab_variant % 100;
     const bool uns = nonneg && c->slab_variant >= 100;
@@ -793,9 +805,9 @@ static void back3_launch_p(Ctx* c, const float* w, double* out, const double* ba
     {                                                                                                              \
         const unsigned nb = nblk_warp(c, (c->N + S::G - 1) / S::G) * (8 / WPB);                                    \
         if (bam) k_back3s<1, S::LPR, S::SPL, U, NF, SG, P, WPB, MINB><<<nb, 32 * WPB, 0, c->st>>>(                 \
-            c->N, 0, c->nzl, c->order.p, c->cp.p, c->C.p, w, nullptr, bam, c->mu.p, c->Z0, c->flag.p);             \
+            c->N, 0, c->nzl, c->order.p, c->cp.p, c->C.p, w, nullptr, bam, c->mu.p, c->Z0, c->flag.p, tm);         \
         else k_back3s<0, S::LPR, S::SPL, U, NF, SG, P, WPB, MINB><<<nb, 32 * WPB, 0, c->st>>>(                     \
-            c->N, 0, c->nzl, c->order.p, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p);               \
+            c->N, 0, c->nzl, c->order.p, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p, tm);           \
     }
 #define BX(NF, U, WPB, MINB) if (uns) { BX1(NF, U, WPB, MINB, false) } else { BX1(NF, U, WPB, MINB, true) }
     SLAB_SWITCH(BX, v)
@@ -803,19 +815,21 @@ static void back3_launch_p(Ctx* c, const float* w, double* out, const double* ba
 #undef BX1
 }
 // nonneg: w >= 0 (the iteration's q and d; not the public back_project)
-static void back3_launch(Ctx* c, const float* w, double* out, const double* bam, bool nonneg) {
+static void back3_launch(Ctx* c, const float* w, double* out, const double* bam, bool nonneg, const TileMap& tm) {
     switch (slab_stride(c)) {
-        case 8: back3_launch_p<8>(c, w, out, bam, nonneg); break;
-        case 16: back3_launch_p<16>(c, w, out, bam, nonneg); break;
-        case 32: back3_launch_p<32>(c, w, out, bam, nonneg); break;
-        case 64: back3_launch_p<64>(c, w, out, bam, nonneg); break;
-        default: back3_launch_p<128>(c, w, out, bam, nonneg); break;
+        case 8: back3_launch_p<8>(c, w, out, bam, nonneg, tm); break;
+        case 16: back3_launch_p<16>(c, w, out, bam, nonneg, tm); break;
+        case 32: back3_launch_p<32>(c, w, out, bam, nonneg, tm); break;
+        case 64: back3_launch_p<64>(c, w, out, bam, nonneg, tm); break;
+        default: back3_launch_p<128>(c, w, out, bam, nonneg, tm); break;
     }
 }
 
 // g = H^T w (fp64).  2D: CSC gather; 3D: slab gather over the tile-ordered voxels.
 // am != nullptr: fused AM update of mu instead of writing g.
-static void back_launch(Ctx* c, const float* w, double* out, const double* bam, bool nonneg = true) {
+// tm (3D only): write g in the tile-major chunk layout of the split update
+static void back_launch(Ctx* c, const float* w, double* out, const double* bam, bool nonneg = true,
+                        const TileMap& tm = TileMap{}) {
     c->timer_begin(T_BACK);
     if (c->nzl == 1) {
 #define BV(U, MB)                                                                                                 \
@@ -845,7 +859,7 @@ static void back_launch(Ctx* c, const float* w, double* out, const double* bam, 
         }
 #undef BV
     } else {
-        back3_launch(c, w, out, bam, nonneg);
+        back3_launch(c, w, out, bam, nonneg, tm);
     }
     check_launch(c, "k_back3");
     c->timer_end(T_BACK);
@@ -1066,6 +1080,9 @@ static int zwords(const Ctx* c, int l) { return ((c->nzl >> l) + 31) >> 5; }
 
 // act_host (3D bytes, level l: (nzl>>l, ny>>l, nx>>l)) -> any-bits per in-plane
 // block (shared memory of the walk) + z-activity words per in-plane block.
+template <class Fn>
+static void host_par_chunks(uint64_t n, uint64_t align, Fn&& fn);
+
 static void upload_tree3(Ctx* c, int* nlev_out) {
     std::vector<unsigned> w, zw;
     uint64_t bit = 0, zo = 0, ko = 0;
@@ -1082,16 +1099,31 @@ static void upload_tree3(Ctx* c, int* nlev_out) {
         w.resize((bit + nb + 31) / 32 + 1, 0u);
         zw.resize(zo + nb * W, 0u);
         const uint8_t* a = c->act_host.data() + c->off.off[l];
-        bool any_l = false;
-        for (int k = 0; k < nk; ++k)
-            for (uint64_t b = 0; b < nb; ++b)
-                if (a[(uint64_t)k * nb + b]) {
-                    zw[zo + b * W + (k >> 5)] |= 1u << (k & 31);
-                    w[(bit + b) >> 5] |= 1u << ((bit + b) & 31);
-                    any_l = true;
-                }
-        for (uint64_t b = 0; b < nb; ++b)
-            if ((w[(bit + b) >> 5] >> ((bit + b) & 31)) & 1u) lst.push_back(make_uint2((unsigned)b, (unsigned)l));
+        // parallel over in-plane block ranges aligned to 32 (each thread owns
+        // its tbits words and its blocks' z words); lists concatenate in order
+        std::vector<std::vector<uint2>> parts;
+        std::mutex pm;
+        std::atomic<bool> any_l{false};
+        host_par_chunks(nb, 32, [&](uint64_t lo, uint64_t hi, int t) {
+            bool any = false;
+            for (int k = 0; k < nk; ++k) {
+                const uint8_t* ak = a + (uint64_t)k * nb;
+                for (uint64_t b = lo; b < hi; ++b)
+                    if (ak[b]) {
+                        zw[zo + b * W + (k >> 5)] |= 1u << (k & 31);
+                        w[(bit + b) >> 5] |= 1u << ((bit + b) & 31);
+                        any = true;
+                    }
+            }
+            std::vector<uint2> mine;
+            for (uint64_t b = lo; b < hi; ++b)
+                if ((w[(bit + b) >> 5] >> ((bit + b) & 31)) & 1u) mine.push_back(make_uint2((unsigned)b, (unsigned)l));
+            std::lock_guard<std::mutex> lk(pm);
+            if ((int)parts.size() <= t) parts.resize(t + 1);
+            parts[t].swap(mine);
+            if (any) any_l = true;
+        });
+        for (auto& v : parts) lst.insert(lst.end(), v.begin(), v.end());
         if (chain && any_l) ++nlev; else chain = false;
         bit = (bit + nb + 31) / 32 * 32;
         zo += nb * W;
@@ -1265,6 +1297,31 @@ static void host_par(uint64_t n, Fn&& fn) {
     }
     for (auto& th : pool) th.join();
 }
+// chunks aligned to `align` elements, fn(lo, hi, chunk index); serial below 64K
+template <class Fn>
+static void host_par_chunks(uint64_t n, uint64_t align, Fn&& fn) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const uint64_t nt = n < (1u << 16) ? 1 : std::min<uint64_t>(hw, 16);
+    if (nt == 1) { fn(0, n, 0); return; }
+    const uint64_t chunk = ((n + nt - 1) / nt + align - 1) / align * align;
+    std::vector<std::thread> pool;
+    for (uint64_t t = 0; t * chunk < n; ++t) {
+        const uint64_t lo = t * chunk, hi = std::min(n, lo + chunk);
+        pool.emplace_back([&fn, lo, hi, t] { fn(lo, hi, (int)t); });
+    }
+    for (auto& th : pool) th.join();
+}
+// number of bytes set in a[lo, hi) minus those set in b (host, parallel)
+static int64_t count_diff(const uint8_t* a, const uint8_t* b, uint64_t n) {
+    std::atomic<int64_t> tot{0};
+    host_par_chunks(n, 64, [&](uint64_t lo, uint64_t hi, int) {
+        int64_t s = 0;
+        for (uint64_t i = lo; i < hi; ++i) s += (a[i] != 0) - (b ? (b[i] != 0) : 0);
+        tot += s;
+    });
+    return tot.load();
+}
+
 static uint64_t NV(const Ctx* c) { return c->N * (uint64_t)slab_stride(c); }
 static uint64_t MV(const Ctx* c) { return c->Ml * (uint64_t)slab_stride(c); }
 // 2D image upload/download through the tiled device layout (mu_addr)
@@ -1425,6 +1482,18 @@ static bool am_split_update(const Ctx* c) {
 }
 static bool wam_split_update(const Ctx* c) {
     return c->nz > 1 && c->haar3 && c->Rv > 1 && split_update_enabled() && ((c->ny >> c->L) % c->Rv) == 0;
+}
+static TileMap make_tilemap(const Ctx* c) {
+    TileMap m;
+    m.L = c->L;
+    m.TX = c->nx >> c->L;
+    m.TZ = c->nzl >> c->L;
+    m.rows = (c->ny >> c->L) / c->Rv;
+    m.nx = c->nx;
+    m.ny = c->ny;
+    m.nzl = c->nzl;
+    m.CT = (uint64_t)m.rows * m.TX * m.TZ << (3 * c->L);
+    return m;
 }
 
 static void am_iterate(Ctx* c, int n, wamgpu_record* recs) {
@@ -1631,13 +1700,9 @@ static void phi_append(Ctx* c) {
 
 static int64_t count_active(const Ctx* c) {
     if (c->haar3) {
-        int64_t a = (int64_t)(c->nx >> c->L) * (c->ny >> c->L) * (c->nzl >> c->L);
-        for (int l = 1; l <= c->L; ++l) {
-            const uint64_t n = blocks2(c, l) * (uint64_t)(c->nzl >> l);
-            const uint8_t* p = c->act_host.data() + c->off.off[l];
-            for (uint64_t i = 0; i < n; ++i) a += 7 * (p[i] != 0);
-        }
-        return a;
+        // levels 1..L are contiguous in act_host (wam_init): 7 details per set byte
+        const int64_t a = (int64_t)(c->nx >> c->L) * (c->ny >> c->L) * (c->nzl >> c->L);
+        return a + 7 * count_diff(c->act_host.data(), nullptr, c->act_bytes);
     }
     int64_t a = (int64_t)(c->nx >> c->L) * (c->ny >> c->L);
     for (int l = 1; l <= c->L; ++l) {
@@ -1647,6 +1712,8 @@ static int64_t count_active(const Ctx* c) {
     }
     return a * c->nz;
 }
+
+static void split_init(Ctx* c);
 
 static void wam_init(Ctx* c, int L, const double* init_beta) {
     need_matrix(c);
@@ -1705,6 +1772,7 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
         c->act_phi.assign(c->act_bytes, 0);
     }
     tile_launch(c, 0, nullptr, nullptr);  // mu = Omega beta
+    split_init(c);
     forward_fused(c, false);
     CK(cudaMemsetAsync(c->counters.p, 0, 16, c->st));
     CK(cudaEventRecord(c->ev_t0, c->st));
@@ -1714,63 +1782,86 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     c->active = count_active(c);
 }
 
-// separable 3D Haar update split over the view group (kernels3h.cuh k_pack3h,
-// k_tile3h_own, k_unpack3h): pack [g || b-] tile-major, reduce-scatter by tile
-// rows, update own tiles, all-gather {mu, beta} + counts, unpack everywhere
-static void tile_update_split(Ctx* c) {
-    const int TS = 1 << c->L;
-    TileChunks tc;
-    tc.TX = c->nx >> c->L;
-    tc.TZ = c->nzl >> c->L;
-    const int TY = c->ny >> c->L;
-    tc.rows = TY / c->Rv;
-    tc.CT = (uint64_t)tc.rows * tc.TX * tc.TZ * TS * TS * TS;
-    const uint64_t CU = tc.CT + 2;
-    c->rs_send.ensure(2 * tc.CT * c->Rv);
-    c->rs_recv.ensure(2 * tc.CT);
-    c->ag_send.ensure(CU);
-    c->ag_recv.ensure(CU * c->Rv);
-    const int P = slab_stride(c);
+// separable 3D Haar update split over the view group (kernels3h.cuh): the
+// summed chunks [g || b-] of the member's tile rows feed k_tile3h_own, whose
+// {mu, beta} planes + counts are all-gathered and unpacked into the mu slab
+// (beta stays in the planes until read: sync_beta)
+static void tile_update_split(Ctx* c, const TileMap& tm) {
+    const int TS = 1 << c->L, P = slab_stride(c);
+    const uint64_t CU = u_chunk(tm);
     c->timer_begin(T_UPDATE);
-    k_pack3h<<<dim3(tc.TX, TY, tc.TZ), 256, 0, c->st>>>(c->nx, c->ny, c->nzl, P, c->L, tc, c->g.p, c->g.p + NV(c),
-                                                        c->act.p, c->off, c->rs_send.p);
-    check_launch(c, "k_pack3h");
-    c->timer_end(T_UPDATE);
-    reduce_scatter(c, c->rs_send.p, c->rs_recv.p, 2 * tc.CT, S_VIEWS);
-    c->timer_begin(T_UPDATE);
-    CK(cudaMemsetAsync(c->ag_send.p + tc.CT, 0, 16, c->st));
+    CK(cudaMemsetAsync(c->ag_send.p + 2 * tm.CT, 0, 16, c->st));
     const size_t smem = 2ull * TS * TS * TS * sizeof(double);
     if (smem > 48 * 1024)
         CK(cudaFuncSetAttribute(k_tile3h_own, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_tile3h_own<<<dim3(tc.TX, tc.rows, tc.TZ), 256, smem, c->st>>>(
-        c->nx, c->ny, c->nzl, P, c->L, tc, c->vg * tc.rows, c->rs_recv.p, c->bdata.p, c->act.p, c->off, c->beta.p,
-        c->ag_send.p, c->bp_dbg.p, c->bm_dbg.p, c->Z0, c->flag.p);
+    k_tile3h_own<<<dim3(tm.TX, tm.rows, tm.TZ), 256, smem, c->st>>>(tm, P, c->vg * tm.rows, c->rs_recv.p,
+                                                                     c->rs_recv.p + tm.CT, c->bdata.p, c->act.p,
+                                                                     c->off, c->ag_send.p, c->bp_dbg.p, c->bm_dbg.p,
+                                                                     c->Z0, c->flag.p);
     check_launch(c, "k_tile3h_own");
     c->timer_end(T_UPDATE);
-    all_gather(c, c->ag_send.p, c->ag_recv.p, CU * sizeof(float2), S_VIEWS);
+    all_gather(c, c->ag_send.p, c->ag_recv.p, CU * sizeof(float), S_VIEWS);
     c->timer_begin(T_UPDATE);
-    k_unpack3h<<<dim3(tc.TX, TY, tc.TZ), 256, 0, c->st>>>(c->nx, c->ny, c->nzl, P, c->L, tc, c->Rv, c->ag_recv.p,
-                                                          c->act.p, c->off, c->mu.p, c->beta.p, c->counters.p);
-    check_launch(c, "k_unpack3h");
+    const uint64_t n = tm.CT * c->Rv;
+    k_unpack_mu<<<(unsigned)std::min<uint64_t>(blocks_for(n, 256), (uint64_t)c->sms * 16), 256, 0, c->st>>>(
+        tm, P, c->Rv, c->ag_recv.p, c->mu.p, c->counters.p);
+    check_launch(c, "k_unpack_mu");
     c->timer_end(T_UPDATE);
+    c->beta_dirty = true;
+}
+
+// slab-Mallat beta from the gathered planes (after split updates)
+static void sync_beta(Ctx* c) {
+    if (!c->beta_dirty) return;
+    const TileMap tm = make_tilemap(c);
+    const uint64_t n = tm.CT * c->Rv;
+    k_beta_planes<<<(unsigned)std::min<uint64_t>(blocks_for(n, 256), (uint64_t)c->sms * 16), 256, 0, c->st>>>(
+        tm, slab_stride(c), 0, c->Rv, c->ag_recv.p, c->beta.p, c->act.p, c->off, 0);
+    check_launch(c, "k_beta_planes");
+    c->beta_dirty = false;
+}
+
+// split-update buffers at wam_init: T zeroed (b- entries the split never
+// writes stay 0), the member's beta plane from the initial beta
+static void split_init(Ctx* c) {
+    c->beta_dirty = false;
+    if (!wam_split_update(c)) return;
+    const TileMap tm = make_tilemap(c);
+    const uint64_t CU = u_chunk(tm);
+    c->rs_send.ensure(2 * tm.CT * c->Rv);
+    c->rs_recv.ensure(2 * tm.CT);
+    c->ag_send.ensure(CU);
+    c->ag_recv.ensure(CU * c->Rv);
+    CK(cudaMemsetAsync(c->rs_send.p, 0, 2 * tm.CT * c->Rv * 8, c->st));
+    CK(cudaMemsetAsync(c->ag_send.p, 0, CU * 4, c->st));
+    k_beta_planes<<<(unsigned)std::min<uint64_t>(blocks_for(tm.CT, 256), (uint64_t)c->sms * 16), 256, 0, c->st>>>(
+        tm, slab_stride(c), c->vg, 1, c->ag_send.p, c->beta.p, c->act.p, c->off, 1);
+    check_launch(c, "k_beta_planes");
 }
 
 static void wam_step(Ctx* c) {
     // view-sharded 2D with peer memory: split first (its partial b- rides along
     // as the second half of the fused back projection + all-reduce)
     const bool fused = c->ar.on && c->nz == 1 && !c->haar3;
+    const bool split = wam_split_update(c);   // 3D view group: reduce-scatter / own tiles / all-gather
+    const TileMap tm = split ? make_tilemap(c) : TileMap{};
     double* bm2 = fused ? c->ar.extra.p : c->g.p + c->N;
-    if (!fused) back_into(c, c->q.p, c->g.p);
+    if (split) {
+        back_launch(c, c->q.p, c->rs_send.p, nullptr, true, tm);   // g straight into the tile-major T
+        CK(cudaEventRecord(c->ev_x, c->st));
+    } else if (!fused) {
+        back_into(c, c->q.p, c->g.p);
+    }
     if (c->haar3 && c->nlist3) {
         c->timer_begin(T_SPLIT);
         const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist3 + 3) / 4, (uint64_t)c->sms * 16);
-        double* bm3 = c->g.p + NV(c);
+        double* bm3 = split ? c->rs_send.p + tm.CT * c->Rv : c->g.p + NV(c);   // split: tile-major b- part
 #define S3H(S) k_split3h<S><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p, c->E3ray.p, \
-                                                   c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3);
+                                                   c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3, tm);
 #define S3E(S, EE) S3EU(S, EE, 2)
 #define S3EU(S, EE, UU) k_split3h_e<S, EE, UU><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl,  \
                                                                      c->np.p, c->E3ray.p, c->E3psi.p, c->q.p,     \
-                                                                     c->act.p, c->off, c->koff, bm3);
+                                                                     c->act.p, c->off, c->koff, bm3, tm);
         const int P = slab_stride(c);
         if (c->split_variant == 1 && P >= 32) {
             switch (spl_of(c)) { case 1: S3H(1) break; case 2: S3H(2) break; default: S3H(4) break; }
@@ -1828,8 +1919,15 @@ static void wam_step(Ctx* c) {
         if (!c->nlist) CK(cudaMemsetAsync(c->ar.extra.p, 0, c->N * 8, c->st));
         back_allreduce(c, c->q.p, c->ar.extra.p);
         CK(cudaMemcpyAsync(c->g.p, c->ar.res.p, 2 * c->N * 8, cudaMemcpyDeviceToDevice, c->st));
-    } else if (wam_split_update(c)) {
-        tile_update_split(c);
+    } else if (split) {
+        // the g part's reduce-scatter runs on the side stream, overlapping the
+        // split (already enqueued on the main stream); the b- part follows it
+        CK(cudaStreamWaitEvent(c->st2, c->ev_x, 0));
+        reduce_scatter(c, c->rs_send.p, c->rs_recv.p, tm.CT, S_VIEWS, c->st2);
+        CK(cudaEventRecord(c->ev_y, c->st2));
+        CK(cudaStreamWaitEvent(c->st, c->ev_y, 0));
+        reduce_scatter(c, c->rs_send.p + tm.CT * c->Rv, c->rs_recv.p + tm.CT, tm.CT, S_VIEWS, c->st);
+        tile_update_split(c, tm);
         c->tm.update_launches++;
         forward_fused(c, true);
         return;
@@ -1855,10 +1953,29 @@ static void wam_iterate(Ctx* c, int n, wamgpu_record* recs) {
     fill_records(c, n, recs, c->active);
 }
 
+// expand_with: blocks of a caller-given tree (e.g. the manifest of another run,
+// or the joint tree replayed on one shard) join the criterion's marks; the
+// device tree is updated when they add anything
+static void merge_add_tree(Ctx* c, std::vector<uint8_t>& h) {
+    if (!c->add_tree) return;
+    std::atomic<bool> changed{false};
+    host_par_chunks(c->act_bytes, 64, [&](uint64_t lo, uint64_t hi, int) {
+        bool ch = false;
+        for (uint64_t i = lo; i < hi; ++i)
+            if (c->add_tree[i] && !h[i]) { h[i] = 1; ch = true; }
+        if (ch) changed = true;
+    });
+    if (changed) {
+        CK(cudaMemcpyAsync(c->act.p, h.data(), c->act_bytes, cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    }
+}
+
 static int64_t wam_expand(Ctx* c, double factor) {
     if (c->algo != 2) throw ContractError("wam: not initialised");
     if (trace_host()) { CK(cudaStreamSynchronize(c->st)); c->t_trace = host_ms(); }
     c->timer_begin(T_EXPAND);
+    sync_beta(c);
     tile_launch(c, 0, c->mu64.p, nullptr);         // fp64 criterion image Omega beta
     if (c->haar3) {                                 // pin P3: every voxel, no z-sum
         int64_t newly = 0;
@@ -1871,17 +1988,22 @@ static int64_t wam_expand(Ctx* c, double factor) {
         double mx = 0.0;
         CK(cudaMemcpyAsync(&mx, c->scal.p + 1, 8, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
-        if (mx > 0.0 && c->L > 0) {
-            CK(cudaMemcpyAsync(c->act_new.p, c->act.p, c->act_bytes, cudaMemcpyDeviceToDevice, c->st));
-            k_mark3h<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->nx, c->ny, c->nzl, slab_stride(c), c->L,
-                                                                         c->mu64.p, factor * mx, c->act.p,
-                                                                         c->act_new.p, c->off);
-            check_launch(c, "k_mark3h");
-            c->act.swap(c->act_new);
+        if ((mx > 0.0 || c->add_tree) && c->L > 0) {
             std::vector<uint8_t> h(c->act_bytes);
-            CK(cudaMemcpyAsync(h.data(), c->act.p, c->act_bytes, cudaMemcpyDeviceToHost, c->st));
-            CK(cudaStreamSynchronize(c->st));
-            for (uint64_t i = 0; i < c->act_bytes; ++i) newly += (h[i] != 0) - (c->act_host[i] != 0);
+            if (mx > 0.0) {
+                CK(cudaMemcpyAsync(c->act_new.p, c->act.p, c->act_bytes, cudaMemcpyDeviceToDevice, c->st));
+                k_mark3h<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->nx, c->ny, c->nzl, slab_stride(c),
+                                                                             c->L, c->mu64.p, factor * mx, c->act.p,
+                                                                             c->act_new.p, c->off);
+                check_launch(c, "k_mark3h");
+                c->act.swap(c->act_new);
+                CK(cudaMemcpyAsync(h.data(), c->act.p, c->act_bytes, cudaMemcpyDeviceToHost, c->st));
+                CK(cudaStreamSynchronize(c->st));
+            } else {
+                h = c->act_host;
+            }
+            merge_add_tree(c, h);
+            newly = count_diff(h.data(), c->act_host.data(), c->act_bytes);
             c->act_host.swap(h);
             if (newly > 0) {
                 HTRACE("expand3: criterion + mark");
@@ -1907,17 +2029,22 @@ static int64_t wam_expand(Ctx* c, double factor) {
     }
     const double mx = device_max(c, crit, c->N);
     int64_t newly = 0;
-    if (mx > 0.0 && c->L > 0) {
-        const double thr = factor * mx;
-        CK(cudaMemcpyAsync(c->act_new.p, c->act.p, c->act_bytes, cudaMemcpyDeviceToDevice, c->st));
-        k_mark<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->nx, c->ny, c->L, crit, thr, c->act.p, c->act_new.p,
-                                                          c->off);
-        check_launch(c, "k_mark");
-        c->act.swap(c->act_new);
+    if ((mx > 0.0 || c->add_tree) && c->L > 0) {
         std::vector<uint8_t> h(c->act_bytes);
-        CK(cudaMemcpyAsync(h.data(), c->act.p, c->act_bytes, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
-        for (uint64_t i = 0; i < c->act_bytes; ++i) newly += (h[i] != 0) - (c->act_host[i] != 0);
+        if (mx > 0.0) {
+            const double thr = factor * mx;
+            CK(cudaMemcpyAsync(c->act_new.p, c->act.p, c->act_bytes, cudaMemcpyDeviceToDevice, c->st));
+            k_mark<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->nx, c->ny, c->L, crit, thr, c->act.p, c->act_new.p,
+                                                              c->off);
+            check_launch(c, "k_mark");
+            c->act.swap(c->act_new);
+            CK(cudaMemcpyAsync(h.data(), c->act.p, c->act_bytes, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+        } else {
+            h = c->act_host;
+        }
+        merge_add_tree(c, h);
+        newly = count_diff(h.data(), c->act_host.data(), c->act_bytes);
         c->act_host.swap(h);
         if (newly > 0) {
             HTRACE("expand: criterion + mark");
@@ -1957,6 +2084,9 @@ static Ctx* create(int device) {
     c->device = device;
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_y, cudaEventDisableTiming));
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10) throw CudaError("wamgpu: requires an sm_100a (Blackwell) device");
@@ -2000,6 +2130,10 @@ static void destroy(Ctx* c) {
         if (c->pin[k]) cudaFreeHost(c->pin[k]);
         if (c->pin_ev[k]) cudaEventDestroy(c->pin_ev[k]);
     }
+    cudaStreamSynchronize(c->st2);
+    if (c->ev_x) cudaEventDestroy(c->ev_x);
+    if (c->ev_y) cudaEventDestroy(c->ev_y);
+    cudaStreamDestroy(c->st2);
     cudaStreamDestroy(c->st);
     delete c;
 }
@@ -2504,6 +2638,26 @@ int wamgpu_wam_expand(wamgpu_ctx* ctx, double factor, int64_t* newly) {
     })
 }
 
+int wamgpu_wam_expand_with(wamgpu_ctx* ctx, double factor, const uint8_t* bits, uint64_t nbytes, int64_t* newly) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (ctx->algo != 2) throw ContractError("wam: not initialised");
+        if (bits && nbytes != ctx->act_bytes) throw ContractError("expand_with: tree size differs from the state's");
+        begin_call(ctx);
+        ctx->add_tree = bits;
+        int64_t n = 0;
+        try {
+            n = wam_expand(ctx, factor);
+        } catch (...) {
+            ctx->add_tree = nullptr;
+            throw;
+        }
+        ctx->add_tree = nullptr;
+        end_call(ctx);
+        if (newly) *newly = n;
+    })
+}
+
 int wamgpu_wam_run(wamgpu_ctx* ctx, int iters, const int* sched, int nsched, double factor, wamgpu_record* recs) {
     API_TRY(ctx, {
         NEED(ctx);
@@ -2531,6 +2685,7 @@ int wamgpu_get_beta(const wamgpu_ctx* ctx, double* beta) {
         NEED(ctx); NEED(beta);
         Ctx* c = const_cast<wamgpu_ctx*>(ctx);
         if (c->algo != 2) throw ContractError("get_beta: no wavelet-AM state");
+        sync_beta(c);
         download_slab<float>(c, c->beta.p, beta, c->N, c->N, 0);
     })
 }

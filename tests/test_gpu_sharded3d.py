@@ -160,3 +160,42 @@ def test_detached_shard_runs_its_share(wam, orc):
     recs = c.wam_run(4, [2], 0.1)
     assert len(recs) == 4 and all(np.isfinite(r["objective"]) for r in recs)
     c.close()
+
+
+@pytest.mark.parametrize("name,haar", [("tiny", 2), ("tiny3d16", 2), ("tiny3d16", 3)])
+def test_expand_with_replays_a_tree(wam, orc, name, haar):
+    """wamgpu_wam_expand_with(+inf, tree): a second run that only replays the
+    first run's trees reproduces its trajectory bit-exactly (same data, same
+    tree, same kernels); a tree of the wrong size is a ContractError."""
+    from paper_1508_04458_b200 import configs
+    cfg, _, _, I0, d = problem_inputs(name, orc, wam)
+    g = configs.geometry(cfg, wam.Geometry)
+    runs = []
+    trees = None
+    for replay in (False, True):
+        c = wam.Context(0)
+        c.set_geometry(g)
+        if cfg["nz"] > 1:
+            c.set_haar_dim(haar)
+        c.set_data(d, I0)
+        c.wam_init(cfg["L"])
+        obj, got, done = [], [], 0
+        for k, ev in enumerate(cfg["schedule"] + [cfg["J"]]):
+            obj += [r["objective"] for r in c.wam_iterate(ev - done)]
+            done = ev
+            if ev == cfg["J"]:
+                break
+            if replay:
+                c.wam_expand(float("inf"), add_tree=trees[k])
+            else:
+                c.wam_expand(0.1)
+            got.append(c.tree())
+        if replay:
+            with pytest.raises(wam.ContractError):
+                c.wam_expand(0.1, add_tree=np.zeros(3, np.uint8))
+        runs.append((obj, got, c.image()))
+        trees = got
+        c.close()
+    (o1, t1, m1), (o2, t2, m2) = runs
+    assert all(np.array_equal(a, b) for a, b in zip(t1, t2))
+    assert o1 == o2 and np.array_equal(m1, m2)
