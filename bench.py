@@ -11,9 +11,15 @@ Poisson noise, Haar L = 4, 50 wavelet-AM iterations, expansions at
   python bench.py --impl reference ...    # CPU oracle port on the host cores
 
 Multi-GPU (torchrun, one process per GPU): views are sharded across ranks and
-the partial back projections are all-reduced in fp64 by the library's own
-NCCL communicator; gloo is used only for host plumbing (barrier, unique-id
+the partial back projections are reduced in fp64 by the library's own NCCL
+communicator (2D: fused back projection + all-reduce over NVLink peer memory;
+3D: reduce-scatter / own-tile update / all-gather, --view-groups for a view x
+z-slab grid); gloo is used only for host plumbing (barrier, unique-id
 broadcast, max-over-ranks of the device times).
+
+  python bench.py --config cfg3 --shard 8 [--view-groups 8]
+      times rank 0 of an 8-rank grid alone on one GPU (detached shard, joint
+      tree replayed) and projects the 8-GPU step with modelled collectives.
 """
 from __future__ import annotations
 
@@ -48,7 +54,7 @@ def _args():
     ap.add_argument("--nz", type=int, default=None,
                     help="override the slice count of a 3D config (one z-slab shard of an R-GPU run = nz/R)")
     ap.add_argument("--view-groups", type=int, default=None,
-                    help="3D rank grid: Rv view groups x R/Rv z-slab groups (default 1: z-slabs only)")
+                    help="3D rank grid: Rv view groups x R/Rv z-slab groups (default R: views only; 1 = z-slabs)")
     ap.add_argument("--shard", type=int, default=None,
                     help="N=1: time rank --shard-rank of an R-rank grid ALONE on this GPU (detached shard: "
                          "its views/slab, no exchange) and project the R-GPU step with a modelled all-reduce")
@@ -360,8 +366,10 @@ def main():
         ctx.set_comm(uid, rank, world)
     elif args.shard:
         ctx.set_comm_local(-1, args.shard_rank, args.shard)
-    if cfg["nz"] > 1 and args.view_groups:
-        ctx.set_partition(args.view_groups)
+    if cfg["nz"] > 1:
+        # 3D default: every rank a view group of its own (pure view sharding):
+        # measured best at every R (profiles/shard/r03/TABLE.md)
+        ctx.set_partition(args.view_groups or max(world, args.shard or 1))
     ctx.set_geometry(g)
     part = ctx.partition()
     collective = "none" if world == 1 else "nccl"

@@ -112,6 +112,8 @@ struct wamgpu_ctx {
     DBuf<double> rs_send, rs_recv;      // view-group update: reduce-scatter buffers (tile-major)
     DBuf<float> ag_send, ag_recv;       // view-group update: all-gather buffers {mu, beta planes, counts}
     bool beta_dirty = false;            // slab-Mallat beta behind the gathered beta planes
+    uint8_t* act_pin = nullptr;         // pinned host copy of the tree bytes (expansions)
+    uint64_t act_pin_n = 0;
     cudaStream_t st2 = nullptr;         // side stream (overlapped reduce-scatter)
     cudaEvent_t ev_x = nullptr, ev_y = nullptr;
     std::vector<int> peers_on;          // devices peer access was enabled to
@@ -1953,6 +1955,23 @@ static void wam_iterate(Ctx* c, int n, wamgpu_record* recs) {
     fill_records(c, n, recs, c->active);
 }
 
+// device tree bytes -> host through a pinned buffer (a pageable 2.4 MB copy
+// at cfg3 cost ~1 ms per expansion)
+static void act_pinned(Ctx* c) {
+    if (c->act_pin_n < c->act_bytes) {
+        if (c->act_pin) cudaFreeHost(c->act_pin);
+        c->act_pin = nullptr;
+        CK(cudaMallocHost(reinterpret_cast<void**>(&c->act_pin), std::max<uint64_t>(c->act_bytes, 1)));
+        c->act_pin_n = c->act_bytes;
+    }
+}
+static void act_to_host(Ctx* c, std::vector<uint8_t>& h) {
+    act_pinned(c);
+    CK(cudaMemcpyAsync(c->act_pin, c->act.p, c->act_bytes, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    std::memcpy(h.data(), c->act_pin, c->act_bytes);
+}
+
 // expand_with: blocks of a caller-given tree (e.g. the manifest of another run,
 // or the joint tree replayed on one shard) join the criterion's marks; the
 // device tree is updated when they add anything
@@ -1966,7 +1985,9 @@ static void merge_add_tree(Ctx* c, std::vector<uint8_t>& h) {
         if (ch) changed = true;
     });
     if (changed) {
-        CK(cudaMemcpyAsync(c->act.p, h.data(), c->act_bytes, cudaMemcpyHostToDevice, c->st));
+        act_pinned(c);
+        std::memcpy(c->act_pin, h.data(), c->act_bytes);
+        CK(cudaMemcpyAsync(c->act.p, c->act_pin, c->act_bytes, cudaMemcpyHostToDevice, c->st));
         CK(cudaStreamSynchronize(c->st));
     }
 }
@@ -1997,8 +2018,7 @@ static int64_t wam_expand(Ctx* c, double factor) {
                                                                              c->act_new.p, c->off);
                 check_launch(c, "k_mark3h");
                 c->act.swap(c->act_new);
-                CK(cudaMemcpyAsync(h.data(), c->act.p, c->act_bytes, cudaMemcpyDeviceToHost, c->st));
-                CK(cudaStreamSynchronize(c->st));
+                act_to_host(c, h);
             } else {
                 h = c->act_host;
             }
@@ -2038,8 +2058,7 @@ static int64_t wam_expand(Ctx* c, double factor) {
                                                               c->off);
             check_launch(c, "k_mark");
             c->act.swap(c->act_new);
-            CK(cudaMemcpyAsync(h.data(), c->act.p, c->act_bytes, cudaMemcpyDeviceToHost, c->st));
-            CK(cudaStreamSynchronize(c->st));
+            act_to_host(c, h);
         } else {
             h = c->act_host;
         }
@@ -2131,6 +2150,7 @@ static void destroy(Ctx* c) {
         if (c->pin_ev[k]) cudaEventDestroy(c->pin_ev[k]);
     }
     cudaStreamSynchronize(c->st2);
+    if (c->act_pin) cudaFreeHost(c->act_pin);
     if (c->ev_x) cudaEventDestroy(c->ev_x);
     if (c->ev_y) cudaEventDestroy(c->ev_y);
     cudaStreamDestroy(c->st2);

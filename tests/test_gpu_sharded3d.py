@@ -185,8 +185,10 @@ def test_expand_with_replays_a_tree(wam, orc, name, haar):
             done = ev
             if ev == cfg["J"]:
                 break
-            if replay:
-                c.wam_expand(float("inf"), add_tree=trees[k])
+            if replay:   # through the text manifest: resume a tree
+                from paper_1508_04458_b200 import harness as H
+                dims = (cfg["nx"], cfg["ny"], cfg["nz"], cfg["L"], haar if cfg["nz"] > 1 else 2)
+                c.wam_expand(float("inf"), add_tree=H.parse_manifest(H.tree_manifest(trees[k], *dims), *dims))
             else:
                 c.wam_expand(0.1)
             got.append(c.tree())
