@@ -273,10 +273,18 @@ def _shard_projection(args, cfg, algo, J, part, ctx, ms_step, split_ms_step):
         S, kind, t_c = 0, "none", 0.0
     elif split:
         ne = ctx.N * (P if algo == "am" else nzl)
-        s_rs, s_ag = (8 * ne, 4 * ne) if algo == "am" else (16 * ne, 8 * ne)
-        S, kind = s_rs + s_ag, "reduce-scatter [g || b-] fp64 + all-gather {mu, beta} fp32"
+        s_rs, s_ag = (8 * ne, 4 * ne) if algo == "am" else (16 * ne, 4 * ne)
+        S, kind = s_rs + s_ag, "reduce-scatter [g || b-] fp64 + all-gather mu fp32"
         t_c = (s_rs + s_ag) * (Rv - 1) / Rv / B * 1e3
         if algo == "wam":
+            # once per run (wam_run's end, wamgpu.cu sync_beta): the beta
+            # planes (fp32) all-gathered; per expansion: the members' marks
+            # merged by an fp64 MAX all-reduce over the tree bytes
+            nexp = len([x for x in cfg["schedule"] if x < J])
+            L = cfg["L"]
+            act_bytes = sum((cfg["nx"] >> l) * (cfg["ny"] >> l) * (nzl >> l) for l in range(1, L + 1))
+            t_c += (4 * ne * (Rv - 1) / Rv + nexp * 8 * act_bytes * 2 * (Rv - 1) / Rv) / B * 1e3 / J
+            kind += "; beta planes once per run; tree MAX per expansion"
             # the g half of the reduce-scatter runs on a side stream during the
             # signed split (wamgpu.cu wam_step): only what the split cannot hide counts
             t_g = 8 * ne * (Rv - 1) / Rv / B * 1e3

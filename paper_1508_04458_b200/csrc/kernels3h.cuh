@@ -192,17 +192,20 @@ __global__ void k_tile3h(int mode, int nx, int ny, int nzl, int P, int L, const 
 // Exchange buffers in the tile-major chunk layout of TileMap (kernels3d.cuh):
 //   T (reduce-scatter): [g of all chunks (Rv*CT) || b- of all chunks (Rv*CT)],
 //     written directly by k_back3s / k_split3h_e (tmap.L != 0);
-//   U (all-gather), float chunks of CU = 2*CT + 4: [mu plane (CT) || beta
-//     plane (CT) || 2 u64 counts].  The member's own U chunk is where its
-//     tiles' beta lives between iterations; the slab-Mallat beta is refreshed
-//     from the gathered planes only when read (expansion, get_beta).
-__host__ __device__ inline uint64_t u_chunk(const TileMap& m) { return 2 * m.CT + 4; }
+//   U (all-gather every iteration), float chunks of CU = CT + 4: [mu plane
+//     (CT) || 2 u64 counts];
+//   B: the member's beta plane (CT floats, tile-major), where its tiles' beta
+//     lives between iterations.  The planes are all-gathered and scattered to
+//     the slab-Mallat beta only at expansions and at the end of each
+//     iterate/run call (wamgpu.cu sync_beta), not every iteration.
+__host__ __device__ inline uint64_t u_chunk(const TileMap& m) { return m.CT + 4; }
 
 // k_tile3h mode 1 over this member's tiles: inputs from its summed chunks
-// (gs = g part, bs = b- part), beta from / to its U chunk, mu into its U chunk
+// (gs = g part, bs = b- part), beta from / to its plane B, mu into its U chunk
 __global__ void k_tile3h_own(TileMap tm, int P, int t0, const double* __restrict__ gs,
                              const double* __restrict__ bs, const double* __restrict__ bdata,
                              const uint8_t* __restrict__ act, ActOff off, float* __restrict__ U,
+                             float* __restrict__ B,
                              double* __restrict__ bp_out, double* __restrict__ bm_out, double Z0,
                              int* __restrict__ flag) {
     extern __shared__ double smh[];
@@ -214,7 +217,7 @@ __global__ void k_tile3h_own(TileMap tm, int P, int t0, const double* __restrict
     gs += lt * T3;
     bs += lt * T3;
     float* um = U + lt * T3;
-    float* ub = U + tm.CT + lt * T3;
+    float* ub = B + lt * T3;
     for (int e = threadIdx.x; e < T3; e += blockDim.x) {
         const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
         x[(z * TS + i) * TS + j] = gs[e];
@@ -248,7 +251,7 @@ __global__ void k_tile3h_own(TileMap tm, int P, int t0, const double* __restrict
         deg += __shfl_xor_sync(0xffffffffu, deg, o);
     }
     if ((threadIdx.x & 31) == 0) {
-        unsigned long long* cnt = reinterpret_cast<unsigned long long*>(U + 2 * tm.CT);
+        unsigned long long* cnt = reinterpret_cast<unsigned long long*>(U + tm.CT);
         if (upd) atomicAdd(cnt + 0, upd);
         if (deg) atomicAdd(cnt + 1, deg);
     }
@@ -277,7 +280,7 @@ __global__ void k_unpack_mu(TileMap tm, int P, int members, const float* __restr
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long a = 0, b = 0;
         for (int m = 0; m < members; ++m) {
-            const unsigned long long* cnt = reinterpret_cast<const unsigned long long*>(U + m * CU + 2 * tm.CT);
+            const unsigned long long* cnt = reinterpret_cast<const unsigned long long*>(U + m * CU + tm.CT);
             a += cnt[0];
             b += cnt[1];
         }
@@ -286,12 +289,13 @@ __global__ void k_unpack_mu(TileMap tm, int P, int members, const float* __restr
     }
 }
 
-// beta planes <-> slab Mallat beta.  dir 0: every chunk's plane -> beta (the
-// lazy refresh); dir 1: beta -> the member's own plane (at wam_init)
-__global__ void k_beta_planes(TileMap tm, int P, int r0, int nchunks, float* __restrict__ U, float* __restrict__ beta,
-                              const uint8_t* __restrict__ act, ActOff off, int dir) {
+// beta planes <-> slab Mallat beta.  dir 0: the gathered planes of chunks
+// [r0, r0+nchunks) -> beta; dir 1: beta -> the member's own plane (r0 = its
+// index, nchunks = 1; at wam_init)
+__global__ void k_beta_planes(TileMap tm, int P, int r0, int nchunks, float* __restrict__ planes,
+                              float* __restrict__ beta, const uint8_t* __restrict__ act, ActOff off, int dir) {
     const int TS = 1 << tm.L, T3 = TS * TS * TS;
-    const uint64_t CU = u_chunk(tm), n = tm.CT * (uint64_t)nchunks;
+    const uint64_t n = tm.CT * (uint64_t)nchunks;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t rr = k / tm.CT, w = k % tm.CT, lt = w / T3;
         const int r = r0 + (int)rr;
@@ -300,9 +304,54 @@ __global__ void k_beta_planes(TileMap tm, int P, int r0, int nchunks, float* __r
                        r * tm.rows;
         const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
         const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, tm.L, tm.nx, tm.ny, tm.nzl, P, act, off);
-        float* up = U + (dir ? 0 : (uint64_t)r * CU) + tm.CT + w;
+        float* up = planes + rr * tm.CT + w;
         if (dir) *up = beta[ci.idx];
         else beta[ci.idx] = *up;
+    }
+}
+
+// Expansion criterion of the split update: each member synthesises only its
+// own tiles from its beta plane (fp64, the same cube_inv as k_tile3h mode 0,
+// so mu64 is bit-identical) into mu64 and one max per tile in part[].
+__global__ void k_crit_own(TileMap tm, int P, int t0, const float* __restrict__ B, double* __restrict__ mu64,
+                           double* __restrict__ part) {
+    extern __shared__ double smh[];
+    const int L = tm.L, TS = 1 << L, T3 = TS * TS * TS;
+    double* x = smh;
+    double* t = smh + T3;
+    const int tj = blockIdx.x, ti = t0 + blockIdx.y, kt = blockIdx.z;
+    const uint64_t lt = ((uint64_t)blockIdx.y * tm.TX + tj) * tm.TZ + kt;
+    const float* ub = B + lt * T3;
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
+        x[(z * TS + i) * TS + j] = (double)ub[e];
+    }
+    __syncthreads();
+    cube_inv(x, t, TS, L);
+    double m = -DBL_MAX;
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, q = e / TS, i = q / TS, j = q % TS;
+        const double v = x[(z * TS + i) * TS + j];
+        mu64[((uint64_t)(ti * TS + i) * tm.nx + (tj * TS + j)) * P + (kt * TS + z)] = v;
+        m = fmax(m, v);
+    }
+    m = warp_max(m);
+    __shared__ double sm[32];
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = -DBL_MAX;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, sm[w]);
+        part[lt] = r;
+    }
+}
+
+// tree bytes <-> doubles (the view group merges its members' marks with a MAX)
+__global__ void k_bytes_d(const uint8_t* __restrict__ a, double* __restrict__ d, uint8_t* __restrict__ out,
+                          uint64_t n, int dir) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (dir == 0) d[i] = a[i] ? 1.0 : 0.0;
+        else out[i] = d[i] > 0.0 ? 1 : 0;
     }
 }
 
@@ -324,11 +373,13 @@ __global__ void k_max_slab(const double* __restrict__ v, uint64_t n, int nzl, in
 }
 
 // voxel (x, s) with mu > thr activates the coarsest inactive 3D block (OLD tree)
+// (voxels e0 .. e1-1 of the slab, e = x*nzl + s: the split update marks only
+// its own tile rows)
 __global__ void k_mark3h(int nx, int ny, int nzl, int P, int L, const double* __restrict__ mu64, double thr,
-                         const uint8_t* __restrict__ act_old, uint8_t* __restrict__ act_new, ActOff off) {
-    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t N = (uint64_t)nx * ny;
-    if (e >= N * (uint64_t)nzl) return;
+                         const uint8_t* __restrict__ act_old, uint8_t* __restrict__ act_new, ActOff off,
+                         uint64_t e0, uint64_t e1) {
+    const uint64_t e = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= e1) return;
     const uint64_t xv = e / nzl;
     const int s = (int)(e % nzl);
     if (!(mu64[xv * P + s] > thr)) return;

@@ -110,7 +110,8 @@ struct wamgpu_ctx {
     std::shared_ptr<wamgpu::LocalGroup> lg;
     DBuf<double> gstage;                // in-process group staging
     DBuf<double> rs_send, rs_recv;      // view-group update: reduce-scatter buffers (tile-major)
-    DBuf<float> ag_send, ag_recv;       // view-group update: all-gather buffers {mu, beta planes, counts}
+    DBuf<float> ag_send, ag_recv;       // view-group update: all-gather buffers {mu plane, counts}
+    DBuf<float> bown, ball;             // view-group update: own beta plane, gathered planes
     bool beta_dirty = false;            // slab-Mallat beta behind the gathered beta planes
     uint8_t* act_pin = nullptr;         // pinned host copy of the tree bytes (expansions)
     uint64_t act_pin_n = 0;
@@ -488,6 +489,7 @@ static void all_gather(Ctx* c, const void* send, void* recv, size_t bytes, Scope
 
 static void allreduce_sum(Ctx* c, double* buf, size_t n, Scope s = S_ALL) { allreduce(c, buf, n, 0, s); }
 static void allreduce_max(Ctx* c, double* buf, size_t n) { allreduce(c, buf, n, 1, S_ALL); }
+static void allreduce_max_scope(Ctx* c, double* buf, size_t n, Scope s) { allreduce(c, buf, n, 1, s); }
 // view-sharded (partial back projections to sum); a 1-rank NCCL communicator
 // on a 2D problem also takes this path (tests the NCCL route bit-exactly)
 static bool view_sharded(const Ctx* c) { return c->Rv > 1 || (c->comm_kind == 1 && c->nz == 1); }
@@ -1792,13 +1794,14 @@ static void tile_update_split(Ctx* c, const TileMap& tm) {
     const int TS = 1 << c->L, P = slab_stride(c);
     const uint64_t CU = u_chunk(tm);
     c->timer_begin(T_UPDATE);
-    CK(cudaMemsetAsync(c->ag_send.p + 2 * tm.CT, 0, 16, c->st));
+    CK(cudaMemsetAsync(c->ag_send.p + tm.CT, 0, 16, c->st));
     const size_t smem = 2ull * TS * TS * TS * sizeof(double);
     if (smem > 48 * 1024)
         CK(cudaFuncSetAttribute(k_tile3h_own, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_tile3h_own<<<dim3(tm.TX, tm.rows, tm.TZ), 256, smem, c->st>>>(tm, P, c->vg * tm.rows, c->rs_recv.p,
                                                                      c->rs_recv.p + tm.CT, c->bdata.p, c->act.p,
-                                                                     c->off, c->ag_send.p, c->bp_dbg.p, c->bm_dbg.p,
+                                                                     c->off, c->ag_send.p, c->bown.p, c->bp_dbg.p,
+                                                                     c->bm_dbg.p,
                                                                      c->Z0, c->flag.p);
     check_launch(c, "k_tile3h_own");
     c->timer_end(T_UPDATE);
@@ -1812,13 +1815,16 @@ static void tile_update_split(Ctx* c, const TileMap& tm) {
     c->beta_dirty = true;
 }
 
-// slab-Mallat beta from the gathered planes (after split updates)
+// slab-Mallat beta from the members' planes (after split updates).  Collective
+// over the view group: called at expansions and at the end of every
+// iterate/run call, so beta is current at every ABI boundary.
 static void sync_beta(Ctx* c) {
     if (!c->beta_dirty) return;
     const TileMap tm = make_tilemap(c);
+    all_gather(c, c->bown.p, c->ball.p, tm.CT * sizeof(float), S_VIEWS);
     const uint64_t n = tm.CT * c->Rv;
     k_beta_planes<<<(unsigned)std::min<uint64_t>(blocks_for(n, 256), (uint64_t)c->sms * 16), 256, 0, c->st>>>(
-        tm, slab_stride(c), 0, c->Rv, c->ag_recv.p, c->beta.p, c->act.p, c->off, 0);
+        tm, slab_stride(c), 0, c->Rv, c->ball.p, c->beta.p, c->act.p, c->off, 0);
     check_launch(c, "k_beta_planes");
     c->beta_dirty = false;
 }
@@ -1834,10 +1840,12 @@ static void split_init(Ctx* c) {
     c->rs_recv.ensure(2 * tm.CT);
     c->ag_send.ensure(CU);
     c->ag_recv.ensure(CU * c->Rv);
+    c->bown.ensure(tm.CT);
+    c->ball.ensure(tm.CT * c->Rv);
     CK(cudaMemsetAsync(c->rs_send.p, 0, 2 * tm.CT * c->Rv * 8, c->st));
     CK(cudaMemsetAsync(c->ag_send.p, 0, CU * 4, c->st));
     k_beta_planes<<<(unsigned)std::min<uint64_t>(blocks_for(tm.CT, 256), (uint64_t)c->sms * 16), 256, 0, c->st>>>(
-        tm, slab_stride(c), c->vg, 1, c->ag_send.p, c->beta.p, c->act.p, c->off, 1);
+        tm, slab_stride(c), c->vg, 1, c->bown.p, c->beta.p, c->act.p, c->off, 1);
     check_launch(c, "k_beta_planes");
 }
 
@@ -1951,6 +1959,7 @@ static void wam_iterate(Ctx* c, int n, wamgpu_record* recs) {
         CK(cudaEventRecord(c->ev_iter[i], c->st));
         c->iter++;
     }
+    sync_beta(c);
     check_flag(c, "wam_iterate");
     fill_records(c, n, recs, c->active);
 }
@@ -1996,15 +2005,34 @@ static int64_t wam_expand(Ctx* c, double factor) {
     if (c->algo != 2) throw ContractError("wam: not initialised");
     if (trace_host()) { CK(cudaStreamSynchronize(c->st)); c->t_trace = host_ms(); }
     c->timer_begin(T_EXPAND);
-    sync_beta(c);
-    tile_launch(c, 0, c->mu64.p, nullptr);         // fp64 criterion image Omega beta
+    const bool split = wam_split_update(c);
+    TileMap tm;
+    if (split) {   // criterion of the member's own tiles from its beta plane
+        tm = make_tilemap(c);
+        const int TS = 1 << c->L;
+        const uint64_t ntl = (uint64_t)tm.TX * tm.rows * tm.TZ;
+        c->dscratch.ensure(std::max<uint64_t>(ntl, c->act_bytes));
+        const size_t smem = 2ull * TS * TS * TS * sizeof(double);
+        if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_crit_own, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_crit_own<<<dim3(tm.TX, tm.rows, tm.TZ), 256, smem, c->st>>>(tm, slab_stride(c), c->vg * tm.rows,
+                                                                      c->bown.p, c->mu64.p, c->dscratch.p);
+        check_launch(c, "k_crit_own");
+        k_max_partials<<<1, 256, 0, c->st>>>(c->dscratch.p, ntl, c->scal.p + 1);
+        check_launch(c, "k_max_partials");
+    } else {
+        sync_beta(c);
+        tile_launch(c, 0, c->mu64.p, nullptr);     // fp64 criterion image Omega beta
+    }
     if (c->haar3) {                                 // pin P3: every voxel, no z-sum
         int64_t newly = 0;
         const int nb = 1024;
-        k_max_slab<<<nb, 256, 0, c->st>>>(c->mu64.p, c->N, c->nzl, slab_stride(c), c->partial.p);
-        check_launch(c, "k_max_slab");
-        k_max_partials<<<1, 256, 0, c->st>>>(c->partial.p, (uint64_t)nb, c->scal.p + 1);
-        check_launch(c, "k_max_partials");
+        if (!split) {
+            k_max_slab<<<nb, 256, 0, c->st>>>(c->mu64.p, c->N, c->nzl, slab_stride(c), c->partial.p);
+            check_launch(c, "k_max_slab");
+            k_max_partials<<<1, 256, 0, c->st>>>(c->partial.p, (uint64_t)nb, c->scal.p + 1);
+            check_launch(c, "k_max_partials");
+        }
         allreduce_max(c, c->scal.p + 1, 1);
         double mx = 0.0;
         CK(cudaMemcpyAsync(&mx, c->scal.p + 1, 8, cudaMemcpyDeviceToHost, c->st));
@@ -2013,11 +2041,25 @@ static int64_t wam_expand(Ctx* c, double factor) {
             std::vector<uint8_t> h(c->act_bytes);
             if (mx > 0.0) {
                 CK(cudaMemcpyAsync(c->act_new.p, c->act.p, c->act_bytes, cudaMemcpyDeviceToDevice, c->st));
-                k_mark3h<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->nx, c->ny, c->nzl, slab_stride(c),
-                                                                             c->L, c->mu64.p, factor * mx, c->act.p,
-                                                                             c->act_new.p, c->off);
+                uint64_t e0 = 0, e1 = c->N * c->nzl;
+                if (split) {   // own tile rows only; the view group merges the marks
+                    const uint64_t rowv = (uint64_t)c->nx * c->nzl << c->L;   // voxels per tile row
+                    e0 = rowv * (uint64_t)(c->vg * tm.rows);
+                    e1 = e0 + rowv * tm.rows;
+                }
+                k_mark3h<<<blocks_for(e1 - e0, 256), 256, 0, c->st>>>(c->nx, c->ny, c->nzl, slab_stride(c), c->L,
+                                                                       c->mu64.p, factor * mx, c->act.p,
+                                                                       c->act_new.p, c->off, e0, e1);
                 check_launch(c, "k_mark3h");
                 c->act.swap(c->act_new);
+                if (split) {
+                    const unsigned nbk = (unsigned)std::min<uint64_t>(blocks_for(c->act_bytes, 256), c->sms * 16);
+                    k_bytes_d<<<nbk, 256, 0, c->st>>>(c->act.p, c->dscratch.p, nullptr, c->act_bytes, 0);
+                    check_launch(c, "k_bytes_d");
+                    allreduce_max_scope(c, c->dscratch.p, c->act_bytes, S_VIEWS);
+                    k_bytes_d<<<nbk, 256, 0, c->st>>>(nullptr, c->dscratch.p, c->act.p, c->act_bytes, 1);
+                    check_launch(c, "k_bytes_d");
+                }
                 act_to_host(c, h);
             } else {
                 h = c->act_host;
@@ -2091,6 +2133,7 @@ static void wam_run(Ctx* c, int iters, const int* sched, int nsched, double fact
         for (int k = 0; k < nsched; ++k)
             if (sched[k] == it) { wam_expand(c, factor); break; }
     }
+    sync_beta(c);
     check_flag(c, "wam_run");
     if (recs) {
         fill_records(c, iters, recs, 0);
@@ -2705,7 +2748,6 @@ int wamgpu_get_beta(const wamgpu_ctx* ctx, double* beta) {
         NEED(ctx); NEED(beta);
         Ctx* c = const_cast<wamgpu_ctx*>(ctx);
         if (c->algo != 2) throw ContractError("get_beta: no wavelet-AM state");
-        sync_beta(c);
         download_slab<float>(c, c->beta.p, beta, c->N, c->N, 0);
     })
 }
