@@ -176,14 +176,15 @@ def _workload_desc(cfg, nnz, algo, J):
                if algo == "wam" else f"image-domain AM, {J} iterations") + f", nnz(H per slice)={nnz}")
 
 
-def _inputs(cfg, W):
-    """Seeded phantom + Poisson data from the PRODUCT host simulator."""
+def _inputs(cfg, W, device=0):
+    """Seeded phantom + Poisson data from the product's device simulator (the
+    same counts as its host simulator, tests/test_gpu_simulate.py)."""
     from paper_1508_04458_b200 import configs
     g = configs.geometry(cfg, W.Geometry)
     mu_true = W.rasterize(g, configs.phantom(cfg))
     M = cfg["views"] * cfg["detectors"]
     I0 = configs.incident(cfg, M)
-    d = W.simulate(g, mu_true, I0, cfg["seed"])
+    d = W.simulate_device(g, mu_true, I0, cfg["seed"], device=device)
     return g, I0, d
 
 
@@ -361,7 +362,7 @@ def main():
     sched = [s for s in cfg["schedule"] if s < J] if algo == "wam" else []
     plumb = Plumbing(rank, world)
 
-    g, I0, d = _inputs(cfg, W)
+    g, I0, d = _inputs(cfg, W, local)
     joint_trees = None
     if args.shard and algo == "wam":
         # the joint reconstruction's trees (the R-rank run reproduces the
@@ -520,7 +521,7 @@ def main():
             "value": iters_per_s, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 storage / f64 accumulation",
-            "data": "synthetic (seeded luggage phantom, seeded Poisson counts; product host simulator)",
+            "data": "synthetic (seeded luggage phantom, seeded Poisson counts; product device simulator)",
             "config": {"workload": _workload_desc(cfg, nnz, algo, J), "step": "init_state + run (all iterations"
                        " and expansions)", "l2": "working set (H CSR+CSC = 16 B/nnz) >> 126 MB L2; no flush needed",
                        "parallelism": (f"views/{world}" if cfg["nz"] == 1 else

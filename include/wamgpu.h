@@ -202,6 +202,11 @@ int wamgpu_rasterize(const wamgpu_geometry* g, const wamgpu_primitive* prims, in
                      double* mu);
 int wamgpu_simulate(const wamgpu_geometry* g, const double* mu_true, const double* I0, uint64_t seed,
                     int noisy, int threads, double* d);
+/* the same simulation on a CUDA device: identical
+ * trace, sums and counter-based Poisson generator, one warp per ray; the
+ * counts equal wamgpu_simulate's (tests/test_gpu_simulate.py). */
+int wamgpu_simulate_device(int device, const wamgpu_geometry* g, const double* mu_true, const double* I0,
+                           uint64_t seed, int noisy, double* d);
 /* the host ray table used by set_geometry (6 doubles per in-plane ray) */
 int wamgpu_host_rays(const wamgpu_geometry* g, double* rays6);
 

@@ -60,7 +60,7 @@ EXPORTED = [
     "wamgpu_get_tree", "wamgpu_get_stats", "wamgpu_get_scalars", "wamgpu_get_z_rows", "wamgpu_get_timing",
     "wamgpu_set_kernel_timing", "wamgpu_rasterize", "wamgpu_simulate", "wamgpu_host_rays", "wamgpu_set_haar_dim",
     "wamgpu_p2p_export", "wamgpu_p2p_import", "wamgpu_selftest_fused_allreduce", "wamgpu_selftest_fused_back",
-    "wamgpu_set_comm_local", "wamgpu_set_partition", "wamgpu_get_partition", "wamgpu_wam_expand_with",
+    "wamgpu_set_comm_local", "wamgpu_set_partition", "wamgpu_get_partition", "wamgpu_wam_expand_with", "wamgpu_simulate_device",
 ]
 P2P_BLOB = 256   # WAMGPU_P2P_BLOB
 
@@ -426,6 +426,17 @@ def simulate(g: Geometry, mu_true, I0, seed, noisy=True, threads=0):
     d = np.empty(I0.size)
     _chk(load().wamgpu_simulate(C.byref(g), _p(mu_true), _p(I0), C.c_uint64(seed), int(noisy), int(threads),
                                 _p(d)))
+    return d
+
+
+def simulate_device(g: Geometry, mu_true, I0, seed, noisy=True, device=0):
+    """simulate_counts on a CUDA device: the host simulator's trace, sums and
+    counter-based Poisson generator, one warp per ray."""
+    mu_true = np.ascontiguousarray(mu_true, np.float64)
+    I0 = np.ascontiguousarray(I0, np.float64)
+    d = np.empty(I0.size)
+    _chk(load().wamgpu_simulate_device(int(device), C.byref(g), _p(mu_true), _p(I0), C.c_uint64(seed), int(noisy),
+                                       _p(d)))
     return d
 
 

@@ -123,6 +123,96 @@ __global__ void k_trace_fill(const RayDev* __restrict__ rays, uint64_t M, int nx
     });
 }
 
+// ------------------------------------------------------- seeded simulation
+// simulate_counts on the device, restating host_model.cpp
+// simulate() operation for operation: the same fp64 Siddon trace (trace_dev),
+// the same ray-order fp64 sums (mul then add: --fmad=false), I0*exp(-l), and the
+// same counter-based generator (splitmix64 keyed by (seed, ray id, draw);
+// inversion below mean 12, PTRS above).  Counts equal the host's except where
+// the device exp/log/lgamma round differently from the host's AND that flips a
+// sampling comparison (never seen in the parity tests).
+__device__ __forceinline__ uint64_t mix64_dev(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ double uniform01_dev(uint64_t seed, uint64_t stream, uint64_t k) {
+    const uint64_t x = mix64_dev(mix64_dev(seed) ^ mix64_dev(stream * 0x100000001B3ull + k));
+    return __dmul_rn(__dadd_rn((double)(x >> 11), 0.5), 0x1.0p-53);
+}
+// returns -1 for an invalid mean (the host throws NumericError)
+__device__ double poisson_dev(uint64_t seed, uint64_t stream, double m) {
+    if (!(m >= 0.0) || !isfinite(m)) return -1.0;
+    if (m == 0.0) return 0.0;
+    if (m < 12.0) {
+        const double u = uniform01_dev(seed, stream, 0);
+        double p = exp(-m), F = p, k = 0.0;
+        while (u > F && k < 1000.0) {
+            k = __dadd_rn(k, 1.0);
+            p = __dmul_rn(p, __ddiv_rn(m, k));
+            F = __dadd_rn(F, p);
+        }
+        return k;
+    }
+    const double slam = sqrt(m), loglam = log(m);
+    const double b = __dadd_rn(0.931, __dmul_rn(2.53, slam)), a = __dadd_rn(-0.059, __dmul_rn(0.02483, b));
+    const double invalpha = __dadd_rn(1.1239, __ddiv_rn(1.1328, __dsub_rn(b, 3.4)));
+    const double vr = __dsub_rn(0.9277, __ddiv_rn(3.6224, __dsub_rn(b, 2.0)));
+    for (uint64_t j = 0;; ++j) {
+        const double U = __dsub_rn(uniform01_dev(seed, stream, 2 * j + 1), 0.5);
+        const double V = uniform01_dev(seed, stream, 2 * j + 2);
+        const double us = __dsub_rn(0.5, fabs(U));
+        const double k = floor(__dadd_rn(__dadd_rn(__dmul_rn(__dadd_rn(__ddiv_rn(__dmul_rn(2.0, a), us), b), U), m), 0.43));
+        if (us >= 0.07 && V <= vr) return k;
+        if (k < 0.0 || (us < 0.013 && V > us)) continue;
+        const double lhs = __dsub_rn(__dadd_rn(log(V), log(invalpha)), log(__dadd_rn(__ddiv_rn(a, __dmul_rn(us, us)), b)));
+        const double rhs = __dsub_rn(__dadd_rn(-m, __dmul_rn(k, loglam)), lgamma(__dadd_rn(k, 1.0)));
+        if (lhs <= rhs) return k;
+    }
+}
+
+// One warp per in-plane ray; every lane traces it (identical control flow) and
+// owns slices s0 + lane + 32 j.  mu: fp64 [x][nz] (voxel-major); I0, d: rays
+// in the reference layout s*M + y.
+template <int SJ>
+__global__ void __launch_bounds__(256) k_simulate(const RayDev* __restrict__ rays, uint64_t M, int nx, int ny, int nz,
+                                                  double h, const double* __restrict__ mu,
+                                                  const double* __restrict__ I0, uint64_t seed, int noisy,
+                                                  double* __restrict__ d, int* __restrict__ flag) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t y = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; y < M; y += W) {
+        const RayDev r = rays[y];
+        for (int s0 = 0; s0 < nz; s0 += 32 * SJ) {
+            double acc[SJ];
+#pragma unroll
+            for (int j = 0; j < SJ; ++j) acc[j] = 0.0;
+            trace_dev(nx, ny, h, r, [&](int ix, int iy, double len) {
+                const double* col = mu + ((uint64_t)iy * nx + ix) * nz;
+#pragma unroll
+                for (int j = 0; j < SJ; ++j) {
+                    const int s = s0 + lane + 32 * j;
+                    if (s < nz) acc[j] = __dadd_rn(acc[j], __dmul_rn(len, col[s]));
+                }
+            });
+#pragma unroll
+            for (int j = 0; j < SJ; ++j) {
+                const int s = s0 + lane + 32 * j;
+                if (s >= nz) continue;
+                const uint64_t id = (uint64_t)s * M + y;
+                const double m = __dmul_rn(I0[id], exp(-acc[j]));
+                double v = m;
+                if (noisy) {
+                    v = poisson_dev(seed, id, m);
+                    if (v < 0.0) atomicOr(flag, 1);
+                }
+                d[id] = v;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------- CSC transpose helpers
 // warp per row: key = column, value = {row, f32 bits} (coalesced writes).
 __global__ void k_csr_to_pairs(uint64_t M, const unsigned long long* __restrict__ rp, const uint2* __restrict__ A,

@@ -2833,6 +2833,52 @@ int wamgpu_simulate(const wamgpu_geometry* g, const double* mu, const double* I0
     API_TRY(none, { NEED(g); NEED(mu); NEED(I0); NEED(d); simulate(*g, mu, I0, seed, noisy != 0, threads, d); })
 }
 
+int wamgpu_simulate_device(int device, const wamgpu_geometry* g, const double* mu, const double* I0, uint64_t seed,
+                           int noisy, double* d) {
+    const wamgpu_ctx* none = nullptr;
+    API_TRY(none, {
+        NEED(g); NEED(mu); NEED(I0); NEED(d);
+        CK(cudaSetDevice(device));
+        const std::vector<RayD> rays = ray_table(*g);
+        const uint64_t M = rays.size(), N = (uint64_t)g->nx * g->ny, nz = (uint64_t)g->nz;
+        std::vector<double> mt(N * nz);   // voxel-major [x][s]: lanes read consecutive slices
+        host_par(N, [&](uint64_t lo, uint64_t hi) {
+            for (uint64_t x = lo; x < hi; ++x)
+                for (uint64_t s = 0; s < nz; ++s) mt[x * nz + s] = mu[s * N + x];
+        });
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        DBuf<RayDev> dr;
+        DBuf<double> dmu, dI0, dd;
+        DBuf<int> flag;
+        dr.alloc(std::max<uint64_t>(M, 1));
+        dmu.alloc(std::max<uint64_t>(N * nz, 1));
+        dI0.alloc(std::max<uint64_t>(M * nz, 1));
+        dd.alloc(std::max<uint64_t>(M * nz, 1));
+        flag.alloc(1);
+        CK(cudaMemcpyAsync(dr.p, rays.data(), M * sizeof(RayDev), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dmu.p, mt.data(), N * nz * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dI0.p, I0, M * nz * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(flag.p, 0, 4, st));
+        int dev_sms = 148;
+        CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
+        const unsigned nb = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((M + 7) / 8, (uint64_t)dev_sms * 32));
+        if (nz <= 32)
+            k_simulate<1><<<nb, 256, 0, st>>>(dr.p, M, g->nx, g->ny, g->nz, g->voxel_size, dmu.p, dI0.p, seed, noisy,
+                                              dd.p, flag.p);
+        else
+            k_simulate<4><<<nb, 256, 0, st>>>(dr.p, M, g->nx, g->ny, g->nz, g->voxel_size, dmu.p, dI0.p, seed, noisy,
+                                              dd.p, flag.p);
+        CK(cudaGetLastError());
+        int f = 0;
+        CK(cudaMemcpyAsync(&f, flag.p, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(d, dd.p, M * nz * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaStreamDestroy(st));
+        if (f) throw NumericError("simulate: invalid Poisson mean");
+    })
+}
+
 int wamgpu_host_rays(const wamgpu_geometry* g, double* rays6) {
     const wamgpu_ctx* none = nullptr;
     API_TRY(none, {
