@@ -63,6 +63,11 @@ class Context {
         return ok != 0;
     }
 
+    /// 3D rank grid: view groups x z-slab groups (after set_comm, before the matrix).
+    void set_partition(int view_groups) { check(wamgpu_set_partition(c_, view_groups), c_); }
+    /// in-process ranks (one host thread per Context); group < 0: detached shard
+    void set_comm_local(int group, int rank, int nranks) { check(wamgpu_set_comm_local(c_, group, rank, nranks), c_); }
+
     /// build_system_matrix(g) on the device (projector.hpp:126-148).
     void set_geometry(const wamgpu_geometry& g) { check(wamgpu_set_geometry(c_, &g), c_); }
 
@@ -125,6 +130,12 @@ class Context {
     int64_t expand_tree(double factor = 0.1) {
         int64_t n = 0;
         check(wamgpu_wam_expand(c_, factor, &n), c_);
+        return n;
+    }
+    /// expand_tree plus the blocks of a given tree (get_tree layout): resume a manifest
+    int64_t expand_tree_with(double factor, const std::vector<uint8_t>& tree) {
+        int64_t n = 0;
+        check(wamgpu_wam_expand_with(c_, factor, tree.data(), tree.size(), &n), c_);
         return n;
     }
     std::vector<Record> run(int iters, const std::vector<int>& schedule, double factor = 0.1) {
