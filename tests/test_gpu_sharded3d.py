@@ -44,7 +44,7 @@ def _run(wam, cfg, I0, d, algo, haar, grid, sched):
             c.set_comm_local(key, r, R)
             c.set_partition(Rv)
         c.set_geometry(g)
-        if algo == "wam":
+        if algo == "wam" and cfg["nz"] > 1:
             c.set_haar_dim(haar)
         c.set_data(d, I0)
         ctxs.append(c)
@@ -102,6 +102,9 @@ CASES = [
     ("tiny3d16", "wam", 3, (2, 2)),
     ("tiny3d16", "wam", 3, (1, 2)),
     ("tiny3d24", "wam", 3, (3, 1)),         # 4 tile rows % 3: all-reduce + replicated update
+    ("tiny", "wam", 2, (2, 1)),             # 2D view shards: all-reduce of [g || b-] (NCCL's path)
+    ("tiny", "wam", 2, (3, 1)),
+    ("tiny", "am", 2, (2, 1)),
 ]
 
 
