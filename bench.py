@@ -430,7 +430,8 @@ def main():
     ctx.set_kernel_timing(True)
     dev_ms, fwd_ms, back_ms, launches = [], [], [], 0
     fwd_n = back_n = 0
-    split_ms = upd_ms = exp_ms = comm_ms = 0.0
+    split_ms = upd_ms = exp_ms = comm_ms = phi_ms = 0.0
+    phi_n = 0
     split_nnz = 0
     plumb.barrier()
     with ClockSampler(local) as clk:
@@ -448,6 +449,8 @@ def main():
                 upd_ms += t["update_ms"]
                 exp_ms += t["expand_ms"]
                 comm_ms += t["comm_ms"]
+                phi_ms += t["phi_ms"]
+                phi_n += t["phi_launches"]
                 split_nnz = t["split_nnz"]
         wall = time.perf_counter() - t_wall
     plumb.barrier()
@@ -539,7 +542,9 @@ def main():
                         "back_avg_ms": back_avg, "back_gbs": back_gbs, "back_frac": back_gbs / hbm,
                         "per_step_ms": {"forward": sum(fwd_ms) / args.steps, "back": sum(back_ms) / args.steps,
                                         "split": split_ms / args.steps, "update": upd_ms / args.steps,
-                                        "expand": exp_ms / args.steps, "comm": comm_ms / args.steps}},
+                                        "expand": exp_ms / args.steps, "comm": comm_ms / args.steps,
+                                        "phi_a": phi_ms / args.steps},
+                        "phi_a_iterations_per_step": phi_n / args.steps},
             "e2e": {"value": J / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,

@@ -83,6 +83,8 @@ typedef struct {
     int64_t fwd_launches, back_launches, split_launches, update_launches, expand_events;
     int64_t kernel_launches; /* every kernel of this library launched in the call */
     int64_t split_nnz;       /* Phi^- entries gathered per split launch (last) */
+    double phi_ms;           /* iterations over the approximation columns (root-only tree) */
+    int64_t phi_launches;    /* such iterations (their back / update / forward are not in the above) */
 } wamgpu_timing;
 
 int wamgpu_version(void);

@@ -98,7 +98,8 @@ class Timing(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("total_ms", "fwd_ms", "back_ms", "split_ms", "update_ms",
                                           "expand_ms", "comm_ms")] + \
                [(n, C.c_int64) for n in ("fwd_launches", "back_launches", "split_launches", "update_launches",
-                                         "expand_events", "kernel_launches", "split_nnz")]
+                                         "expand_events", "kernel_launches", "split_nnz")] + \
+               [("phi_ms", C.c_double), ("phi_launches", C.c_int64)]
 
     def asdict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -34,6 +34,7 @@
 #include "kernels3d.cuh"
 #include "kernels3h.cuh"
 #include "kernels_ar.cuh"
+#include "kernels_phi.cuh"
 
 namespace wamgpu {
 
@@ -70,7 +71,7 @@ struct DBuf {
     void swap(DBuf& o) { std::swap(p, o.p); std::swap(n, o.n); }
 };
 
-enum Cat { T_FWD = 0, T_BACK, T_SPLIT, T_UPDATE, T_EXPAND, T_COMM, T_NCAT };
+enum Cat { T_FWD = 0, T_BACK, T_SPLIT, T_UPDATE, T_EXPAND, T_COMM, T_PHI, T_NCAT };
 
 // In-process rank group (wamgpu_set_comm_local): R contexts driven by R host
 // threads of one process.  Collectives are a device-side rank-order reduction
@@ -114,6 +115,14 @@ struct wamgpu_ctx {
     DBuf<float> bown, ball;             // view-group update: own beta plane, gathered planes
     bool beta_dirty = false;            // slab-Mallat beta behind the gathered beta planes
     uint8_t* act_pin = nullptr;         // pinned host copy of the tree bytes (expansions)
+    // Φ_A (kernels_phi.cuh): approximation columns of the 2D tree, CSR + CSC,
+    // built once per (matrix, L); used while no detail coefficient is active
+    bool phiA_ok = false, mu_stale = false;
+    int phiA_L = -1;
+    uint64_t phiA_nnz = 0;
+    DBuf<unsigned long long> phiA_rp, phiA_cp;
+    DBuf<unsigned> phiA_col, phiA_row;
+    DBuf<double> phiA_val, phiA_valC, phiA_part;
     uint64_t act_pin_n = 0;
     cudaStream_t st2 = nullptr;         // side stream (overlapped reduce-scatter)
     cudaEvent_t ev_x = nullptr, ev_y = nullptr;
@@ -511,6 +520,10 @@ static void check_flag(Ctx* c, const char* where) {
 
 // ------------------------------------------------------------- system model
 static void finish_matrix(Ctx* c) {
+    c->phiA_ok = false;
+    c->phiA_L = -1;
+    c->phiA_rp.release(); c->phiA_cp.release(); c->phiA_col.release(); c->phiA_row.release();
+    c->phiA_val.release(); c->phiA_valC.release(); c->phiA_part.release();
     // CSC mirror (system_matrix.hpp:61-75): stable radix sort of CSR entries by
     // column keeps rows ascending within every column.
     DBuf<unsigned> kin, kout;
@@ -1252,7 +1265,7 @@ static void end_call(Ctx* c) {
     CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
     c->tm.total_ms = ms;
     double* dst[T_NCAT] = {&c->tm.fwd_ms, &c->tm.back_ms, &c->tm.split_ms, &c->tm.update_ms, &c->tm.expand_ms,
-                           &c->tm.comm_ms};
+                           &c->tm.comm_ms, &c->tm.phi_ms};
     for (int k = 0; k < T_NCAT; ++k) {
         double s = 0.0;
         for (size_t i = 0; i < c->tev_used[k]; ++i) {
@@ -1718,6 +1731,8 @@ static int64_t count_active(const Ctx* c) {
 }
 
 static void split_init(Ctx* c);
+static bool phiA_applicable(const Ctx* c);
+static void build_phiA(Ctx* c);
 
 static void wam_init(Ctx* c, int L, const double* init_beta) {
     need_matrix(c);
@@ -1776,6 +1791,8 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
         c->act_phi.assign(c->act_bytes, 0);
     }
     tile_launch(c, 0, nullptr, nullptr);  // mu = Omega beta
+    c->mu_stale = false;
+    if (phiA_applicable(c)) build_phiA(c);
     split_init(c);
     forward_fused(c, false);
     CK(cudaMemsetAsync(c->counters.p, 0, 16, c->st));
@@ -1784,6 +1801,95 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     c->algo = 2;
     c->iter = 0;
     c->active = count_active(c);
+}
+
+// ---- Φ_A projections while the tree holds only the approximation roots ----
+constexpr int kPhiSeg = 8;
+static bool phiA_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("WAMGPU_PHI_A");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+static bool phiA_applicable(const Ctx* c) {
+    return phiA_enabled() && c->nz == 1 && !c->haar3 && c->L >= 1;
+}
+// CSR by ray (count, scan, fill) and CSC by coefficient (stable key sort)
+static void build_phiA(Ctx* c) {
+    if (c->phiA_ok && c->phiA_L == c->L) return;
+    c->phiA_ok = false;
+    c->phiA_rp.alloc(c->Ml + 1);
+    k_phiA_count<<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->L, c->phiA_rp.p);
+    check_launch(c, "k_phiA_count");
+    exclusive_scan_u64(c, c->phiA_rp.p, c->Ml + 1);
+    unsigned long long nnz = 0;
+    CK(cudaMemcpyAsync(&nnz, c->phiA_rp.p + c->Ml, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    const uint64_t n1 = std::max<unsigned long long>(nnz, 1);
+    c->phiA_col.alloc(n1);
+    c->phiA_val.alloc(n1);
+    DBuf<unsigned> kin, kout;
+    DBuf<uint2> vin, vout;
+    kin.alloc(n1);
+    vin.alloc(n1);
+    k_phiA_fill<<<blocks_for(c->Ml, 128), 128, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->L, c->phiA_rp.p,
+                                                            c->phiA_col.p, c->phiA_val.p, kin.p, vin.p);
+    check_launch(c, "k_phiA_fill");
+    sort_pairs(c, kin, vin, kout, vout, nnz, c->N);
+    kin.release();
+    vin.release();
+    c->phiA_row.alloc(n1);
+    c->phiA_valC.alloc(n1);
+    if (nnz) {
+        k_phiA_gather<<<blocks_for(nnz, 256), 256, 0, c->st>>>(nnz, vout.p, c->phiA_val.p, c->phiA_row.p,
+                                                              c->phiA_valC.p);
+        check_launch(c, "k_phiA_gather");
+    }
+    c->phiA_cp.alloc(c->N + 1);
+    k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(kout.p, nnz, c->N, c->phiA_cp.p);
+    check_launch(c, "k_bounds");
+    const uint64_t nA = (uint64_t)(c->nx >> c->L) * (c->ny >> c->L);
+    c->phiA_part.alloc(nA * kPhiSeg);
+    CK(cudaStreamSynchronize(c->st));
+    c->phiA_nnz = nnz;
+    c->phiA_L = c->L;
+    c->phiA_ok = true;
+}
+// one wavelet-AM iteration with only the roots active: S = Φ_Aᵀ q̂, root
+// solves, ℓ = Φ_A β fused with q̂ and the I-divergence (mu is left stale)
+static void phiA_step(Ctx* c) {
+    const int wA = c->nx >> c->L, nA = wA * (c->ny >> c->L);
+    c->timer_begin(T_PHI);
+    const unsigned nbb = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(blocks_for((uint64_t)nA * kPhiSeg * 32, 256),
+                                                                              (uint64_t)c->sms * 16));
+    k_phiA_back<kPhiSeg><<<nbb, 256, 0, c->st>>>(nA, wA, c->nx, c->phiA_cp.p, c->phiA_row.p, c->phiA_valC.p, c->q.p,
+                                                 c->phiA_part.p);
+    check_launch(c, "k_phiA_back");
+    // view shards: the partials of each (coefficient, segment) over the ranks'
+    // own rays are summed (64 KB at cfg2); the update then runs replicated
+    if (view_sharded(c)) allreduce_sum(c, c->phiA_part.p, (size_t)nA * kPhiSeg, S_VIEWS);
+    k_phiA_update<kPhiSeg><<<blocks_for(nA, 256), 256, 0, c->st>>>(nA, wA, c->nx, c->phiA_part.p, c->bdata.p,
+                                                                   c->beta.p, c->Z0, c->bp_dbg.p, c->bm_dbg.p,
+                                                                   c->counters.p, c->flag.p);
+    check_launch(c, "k_phiA_update");
+    const int nparts = (int)std::min<uint64_t>(c->nblk_row, c->partial.n);
+    k_phiA_fwd<<<nparts, 256, 0, c->st>>>(c->Ml, c->phiA_rp.p, c->phiA_col.p, c->phiA_val.p, c->beta.p, c->I0.p,
+                                          c->d.p, c->q.p, c->partial.p, c->flag.p);
+    check_launch(c, "k_phiA_fwd");
+    c->timer_end(T_PHI);
+    c->tm.phi_launches++;
+    k_sum_partials<<<1, 1024, 0, c->st>>>(c->partial.p, nparts, c->scal.p);
+    check_launch(c, "k_sum_partials");
+    allreduce_sum(c, c->scal.p, 1);
+    k_record<<<1, 32, 0, c->st>>>(c->scal.p, c->counters.p, c->objs.p, c->cums.p, c->it.p);
+    check_launch(c, "k_record");
+    c->mu_stale = true;
+}
+static void sync_mu(Ctx* c) {
+    if (!c->mu_stale) return;
+    tile_launch(c, 0, nullptr, nullptr);   // mu = Omega beta
+    c->mu_stale = false;
 }
 
 // separable 3D Haar update split over the view group (kernels3h.cuh): the
@@ -1850,6 +1956,11 @@ static void split_init(Ctx* c) {
 }
 
 static void wam_step(Ctx* c) {
+    if (c->nlist == 0 && c->phiA_ok && c->phiA_L == c->L && phiA_applicable(c)) {
+        phiA_step(c);
+        return;
+    }
+    c->mu_stale = false;   // the update below synthesises mu
     // view-sharded 2D with peer memory: split first (its partial b- rides along
     // as the second half of the fused back projection + all-reduce)
     const bool fused = c->ar.on && c->nz == 1 && !c->haar3;
@@ -2022,7 +2133,8 @@ static int64_t wam_expand(Ctx* c, double factor) {
         check_launch(c, "k_max_partials");
     } else {
         sync_beta(c);
-        tile_launch(c, 0, c->mu64.p, nullptr);     // fp64 criterion image Omega beta
+        tile_launch(c, 0, c->mu64.p, nullptr);     // fp64 criterion image Omega beta (and mu)
+        c->mu_stale = false;
     }
     if (c->haar3) {                                 // pin P3: every voxel, no z-sum
         int64_t newly = 0;
@@ -2738,6 +2850,7 @@ int wamgpu_get_image(const wamgpu_ctx* ctx, double* mu) {
         NEED(ctx); NEED(mu);
         Ctx* c = const_cast<wamgpu_ctx*>(ctx);
         if (!c->algo) throw ContractError("get_image: no solver state");
+        if (c->algo == 2) sync_mu(c);
         if (c->nzl == 1) download_image2(c, c->mu.p, mu);
         else download_slab<float>(c, c->mu.p, mu, c->N, c->N, 0);
     })

@@ -212,3 +212,28 @@ def test_error_mapping(wam):
         c.wam_init(4)                      # 24 not divisible by 16
     with pytest.raises(wam.ContractError):
         c.set_data(-np.ones(c.M), np.ones(c.M))
+
+
+def test_root_only_iterations_use_phi_a(wam, orc):
+    """While no detail coefficient is active, the 2D iteration runs over the
+    approximation columns Φ_A (kernels_phi.cuh) instead of H; its trajectory and
+    tree stay within the mirror bars (test_wam_parity_tree_bit_exact runs the
+    same phase), and the first expansion still matches the oracle bit-exactly."""
+    cfg, p64, _, I0, d = problem_inputs("small", orc, wam)
+    p32 = orc.Problem(p64.geom, mirror=True)
+    c = _ctx(wam, p64, cfg)
+    c.set_data(d, I0)
+    c.wam_init(cfg["L"])
+    p32.wam_init(d, I0, cfg["L"])
+    n = cfg["schedule"][0]
+    og = [r["objective"] for r in c.wam_iterate(n)]
+    t = c.timing()
+    assert t["phi_launches"] == n and t["fwd_launches"] == 0 and t["back_launches"] == 0
+    o32 = [r[1] for r in p32.wam_iterate(n)]
+    assert rel_l2(og, o32) < TOL_MIRROR
+    assert rel_l2(c.image(), p32.wam_get()["mu"]) < TOL_MIRROR      # mu synthesised on read
+    assert c.wam_expand(0.1) == p32.wam_expand(0.1)
+    assert np.array_equal(c.tree(), p32.wam_tree())
+    og2 = [r["objective"] for r in c.wam_iterate(2)]
+    assert c.timing()["phi_launches"] == 0                          # details active: the H path
+    assert rel_l2(og2, [r[1] for r in p32.wam_iterate(2)]) < TOL_MIRROR
