@@ -117,7 +117,8 @@ struct wamgpu_ctx {
     uint8_t* act_pin = nullptr;         // pinned host copy of the tree bytes (expansions)
     // Φ_A (kernels_phi.cuh): approximation columns of the 2D tree, CSR + CSC,
     // built once per (matrix, L); used while no detail coefficient is active
-    bool phiA_ok = false, mu_stale = false;
+    bool phiA_ok = false, mu_stale = false, phiA_beta_ok = true, bown_stale = false;
+    DBuf<float> phiA_mblk;              // 3D: fp32 synthesis of each root (forward multiplier)
     int phiA_L = -1;
     uint64_t phiA_nnz = 0;
     DBuf<unsigned long long> phiA_rp, phiA_cp;
@@ -1792,6 +1793,8 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     }
     tile_launch(c, 0, nullptr, nullptr);  // mu = Omega beta
     c->mu_stale = false;
+    c->bown_stale = false;
+    c->phiA_beta_ok = init_beta == nullptr;   // Φ_A covers the roots only: inactive details must be 0
     if (phiA_applicable(c)) build_phiA(c);
     split_init(c);
     forward_fused(c, false);
@@ -1812,8 +1815,12 @@ static bool phiA_enabled() {
     }();
     return on;
 }
+// slices per lane of the 3D Φ_A kernels (lane-owned slices stay in one z-block)
+static int phiA3_spl(const Ctx* c) { return std::max(1, slab_stride(c) / 32); }
 static bool phiA_applicable(const Ctx* c) {
-    return phiA_enabled() && c->nz == 1 && !c->haar3 && c->L >= 1;
+    if (!phiA_enabled() || c->L < 1 || !c->phiA_beta_ok) return false;
+    if (c->nz == 1) return !c->haar3;
+    return c->haar3 && phiA3_spl(c) <= (1 << c->L);   // separable 3D Haar (pin P3)
 }
 // CSR by ray (count, scan, fill) and CSC by coefficient (stable key sort)
 static void build_phiA(Ctx* c) {
@@ -1850,7 +1857,9 @@ static void build_phiA(Ctx* c) {
     k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(kout.p, nnz, c->N, c->phiA_cp.p);
     check_launch(c, "k_bounds");
     const uint64_t nA = (uint64_t)(c->nx >> c->L) * (c->ny >> c->L);
-    c->phiA_part.alloc(nA * kPhiSeg);
+    const uint64_t NK = c->haar3 ? (uint64_t)(c->nzl >> c->L) : 1;
+    c->phiA_part.alloc(nA * kPhiSeg * NK);
+    if (c->haar3) c->phiA_mblk.alloc(nA * NK);
     CK(cudaStreamSynchronize(c->st));
     c->phiA_nnz = nnz;
     c->phiA_L = c->L;
@@ -1886,6 +1895,52 @@ static void phiA_step(Ctx* c) {
     check_launch(c, "k_record");
     c->mu_stale = true;
 }
+// separable 3D Haar with only the roots active (kernels_phi.cuh, 3D part)
+static void phiA3_step(Ctx* c) {
+    const int wA = c->nx >> c->L, nA = wA * (c->ny >> c->L), NK = c->nzl >> c->L, P = slab_stride(c);
+    const double cL = cpow3_host(c->L) / (double)(1 << c->L);   // (c/2)^L: the 2D phi_A carries 2^-L
+    const int spl = phiA3_spl(c);
+    c->timer_begin(T_PHI);
+    const unsigned nbb = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(blocks_for((uint64_t)nA * kPhiSeg * 32, 256),
+                                                                              (uint64_t)c->sms * 16));
+#define PB(S) k_phiA3_back<kPhiSeg, S><<<nbb, 256, 0, c->st>>>(nA, wA, c->nx, c->nzl, P, c->L, c->phiA_cp.p,       \
+                                                               c->phiA_row.p, c->phiA_valC.p, c->q.p, c->phiA_part.p)
+    switch (spl) { case 1: PB(1); break; case 2: PB(2); break; default: PB(4); break; }
+#undef PB
+    check_launch(c, "k_phiA3_back");
+    if (view_sharded(c)) allreduce_sum(c, c->phiA_part.p, (size_t)nA * kPhiSeg * NK, S_VIEWS);
+    k_phiA3_update<kPhiSeg><<<blocks_for((uint64_t)nA * NK, 256), 256, 0, c->st>>>(
+        nA, wA, c->nx, NK, P, c->L, cL, c->phiA_part.p, c->bdata.p, c->beta.p, c->phiA_mblk.p, c->Z0, c->bp_dbg.p,
+        c->bm_dbg.p, c->counters.p, c->flag.p);
+    check_launch(c, "k_phiA3_update");
+    const int nparts = (int)std::min<uint64_t>(nblk_warp(c, c->Ml), c->partial.n);
+#define PF(S) k_phiA3_fwd<S><<<nparts, 256, 0, c->st>>>(c->Ml, c->nzl, P, c->L, c->nx, wA, c->phiA_rp.p,          \
+                                                        c->phiA_col.p, c->phiA_val.p, c->phiA_mblk.p, c->I0.p, c->d.p, \
+                                                        c->q.p, c->partial.p, c->flag.p)
+    switch (spl) { case 1: PF(1); break; case 2: PF(2); break; default: PF(4); break; }
+#undef PF
+    check_launch(c, "k_phiA3_fwd");
+    c->timer_end(T_PHI);
+    c->tm.phi_launches++;
+    k_sum_partials<<<1, 1024, 0, c->st>>>(c->partial.p, nparts, c->scal.p);
+    check_launch(c, "k_sum_partials");
+    allreduce_sum(c, c->scal.p, 1);
+    k_record<<<1, 32, 0, c->st>>>(c->scal.p, c->counters.p, c->objs.p, c->cums.p, c->it.p);
+    check_launch(c, "k_record");
+    c->mu_stale = true;
+    c->bown_stale = true;   // the split update's beta plane is behind the Mallat beta
+}
+// the split update's own beta plane from the Mallat beta (after root-only iterations)
+static void refresh_bown(Ctx* c) {
+    if (!c->bown_stale) return;
+    c->bown_stale = false;
+    if (!wam_split_update(c)) return;
+    const TileMap tm = make_tilemap(c);
+    k_beta_planes<<<(unsigned)std::min<uint64_t>(blocks_for(tm.CT, 256), (uint64_t)c->sms * 16), 256, 0, c->st>>>(
+        tm, slab_stride(c), c->vg, 1, c->bown.p, c->beta.p, c->act.p, c->off, 1);
+    check_launch(c, "k_beta_planes");
+}
+
 static void sync_mu(Ctx* c) {
     if (!c->mu_stale) return;
     tile_launch(c, 0, nullptr, nullptr);   // mu = Omega beta
@@ -1956,10 +2011,12 @@ static void split_init(Ctx* c) {
 }
 
 static void wam_step(Ctx* c) {
-    if (c->nlist == 0 && c->phiA_ok && c->phiA_L == c->L && phiA_applicable(c)) {
-        phiA_step(c);
+    if (c->phiA_ok && c->phiA_L == c->L && phiA_applicable(c) && (c->haar3 ? c->nlist3 == 0 : c->nlist == 0)) {
+        if (c->haar3) phiA3_step(c);
+        else phiA_step(c);
         return;
     }
+    refresh_bown(c);
     c->mu_stale = false;   // the update below synthesises mu
     // view-sharded 2D with peer memory: split first (its partial b- rides along
     // as the second half of the fused back projection + all-reduce)
@@ -2119,6 +2176,7 @@ static int64_t wam_expand(Ctx* c, double factor) {
     const bool split = wam_split_update(c);
     TileMap tm;
     if (split) {   // criterion of the member's own tiles from its beta plane
+        refresh_bown(c);
         tm = make_tilemap(c);
         const int TS = 1 << c->L;
         const uint64_t ntl = (uint64_t)tm.TX * tm.rows * tm.TZ;

@@ -129,3 +129,29 @@ def test_wam3d_separable_haar_parity(wam, orc, name):
     _, bp, bm = c.stats()
     _, bp32, bm32 = p32.wam_stats()
     assert rel_l2(bm, bm32) < TOL_MIRROR and rel_l2(bp, bp32) < TOL_MIRROR
+
+
+@pytest.mark.parametrize("name", ["tiny3d16", "small3d"])
+def test_root_only_iterations_use_phi_a_3d(wam, orc, name):
+    """Separable 3D Haar with only the roots active: the iterations run over the
+    in-plane approximation columns (kernels_phi.cuh, 3D part), within the mirror
+    bars, and the first expansion still matches the oracle bit-exactly."""
+    cfg, p64, _, I0, d = problem_inputs(name, orc, wam)
+    p32 = orc.Problem(p64.geom, mirror=True)
+    c = _ctx(wam, cfg)
+    c.set_haar_dim(3)
+    c.set_data(d, I0)
+    c.wam_init(cfg["L"])
+    p32.set_haar_dim(3)
+    p32.wam_init(d, I0, cfg["L"])
+    n = cfg["schedule"][0]
+    og = [r["objective"] for r in c.wam_iterate(n)]
+    t = c.timing()
+    assert t["phi_launches"] == n and t["fwd_launches"] == 0 and t["back_launches"] == 0
+    assert rel_l2(og, [r[1] for r in p32.wam_iterate(n)]) < TOL_MIRROR
+    assert rel_l2(c.image(), p32.wam_get()["mu"]) < TOL_MIRROR
+    assert c.wam_expand(0.1) == p32.wam_expand(0.1)
+    assert np.array_equal(c.tree(), p32.wam_tree())
+    og2 = [r["objective"] for r in c.wam_iterate(2)]
+    assert c.timing()["phi_launches"] == 0
+    assert rel_l2(og2, [r[1] for r in p32.wam_iterate(2)]) < TOL_MIRROR
