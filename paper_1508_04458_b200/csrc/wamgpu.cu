@@ -1898,7 +1898,7 @@ static void phiA_step(Ctx* c) {
 // separable 3D Haar with only the roots active (kernels_phi.cuh, 3D part)
 static void phiA3_step(Ctx* c) {
     const int wA = c->nx >> c->L, nA = wA * (c->ny >> c->L), NK = c->nzl >> c->L, P = slab_stride(c);
-    const double cL = cpow3_host(c->L) / (double)(1 << c->L);   // (c/2)^L: the 2D phi_A carries 2^-L
+    const double cL = cpow3_host(c->L);   // phi(y_s|b,k) = phi_A(y|b) c^L (phi_A carries the in-plane 2^-L)
     const int spl = phiA3_spl(c);
     c->timer_begin(T_PHI);
     const unsigned nbb = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(blocks_for((uint64_t)nA * kPhiSeg * 32, 256),
