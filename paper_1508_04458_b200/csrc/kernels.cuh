@@ -1080,6 +1080,35 @@ __global__ void k_cols_set(uint64_t n, const unsigned long long* __restrict__ pt
     if (hi > lo) col[z] = make_ulonglong2(off + lo, off + hi);
 }
 
+// Counting placement of an unsorted (z, (y, phi)) batch into per-column runs,
+// replacing a radix sort of the batch (three 8-bit passes over 12 B pairs):
+// the split sums each column in exact fixed point, so the order of rays inside
+// a column is free and only the run bounds matter.  Warp-aggregated atomics:
+// lanes holding the same key (neighbouring rays cross the same blocks) take one
+// atomic per key.  k_key_hist counts keys in [0, n] (the sentinel n included,
+// so after an exclusive scan cnt[n] = number of real entries, as k_bounds);
+// k_key_place moves each real entry to cur[z]++ of a copy of the bounds.
+__global__ void k_key_hist(uint64_t n, const unsigned* __restrict__ keys, unsigned nkey,
+                           unsigned long long* __restrict__ cnt) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned k = i < n ? keys[i] : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    const int lane = threadIdx.x & 31;
+    if (k <= nkey && lane == __ffs(peers) - 1) atomicAdd(&cnt[k], (unsigned long long)__popc(peers));
+}
+__global__ void k_key_place(uint64_t n, const unsigned* __restrict__ keys, const uint2* __restrict__ vals,
+                            unsigned nkey, unsigned long long* __restrict__ cur, uint2* __restrict__ out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned k = i < n ? keys[i] : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    const int lane = threadIdx.x & 31, lead = __ffs(peers) - 1;
+    if (k >= nkey) return;   // warp-uniform per key group: whole groups leave together
+    unsigned long long b = 0;
+    if (lane == lead) b = atomicAdd(&cur[k], (unsigned long long)__popc(peers));
+    b = __shfl_sync(peers, b, lead);
+    out[b + __popc(peers & ((1u << lane) - 1u))] = vals[i];
+}
+
 // Incremental expansion walk, one WARP PER LEVEL: the warps of a block share
 // the same 32 rays (thread = ray), whose rows are staged once per 32-entry
 // round in shared memory (cp.async).  Only NEWLY active blocks are walked

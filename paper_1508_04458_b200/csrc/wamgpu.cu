@@ -157,7 +157,8 @@ struct wamgpu_ctx {
     DBuf<unsigned long long> cursor;    // Phi^- emission cursor of the expansion walk
     DBuf<long long> zfix, zfix2;        // 2D tree: per-ray Z(y) in 2^-32 fixed point (pin P8)
     DBuf<ulonglong2> cols;              // 2D tree: Phi^- range [lo, hi) of column z inside E
-    DBuf<unsigned long long> ptmp;      // column bounds of one sorted batch
+    DBuf<unsigned long long> ptmp;      // column bounds of one placed batch
+    DBuf<unsigned long long> pcur;      // placement cursors (copy of ptmp)
     std::vector<uint8_t> act_phi;       // tree that Phi^- / zfix currently cover
     DBuf<double> zA;                    // per-ray approximation part of Z (tree-independent)
     DBuf<uint8_t> cub_tmp;
@@ -1686,9 +1687,32 @@ static void phi_append(Ctx* c) {
         if (off) CK(cudaMemcpyAsync(t.p, c->E.p, off * sizeof(uint2), cudaMemcpyDeviceToDevice, c->st));
         c->E.swap(t);
     }
-    c->kout_s.ensure(std::max<uint64_t>(tot, 1));
     c->ptmp.ensure(c->N + 1);
     HTRACE("expand: E grow");
+    // Counting placement (default): histogram of the batch's keys, exclusive
+    // scan into the column bounds, warp-aggregated placement.  WAMGPU_PHI_SORT=1
+    // keeps the earlier radix sort + k_bounds (same runs, other ray order).
+    static const bool use_sort = [] {
+        const char* e = std::getenv("WAMGPU_PHI_SORT");
+        return e && e[0] == '1';
+    }();
+    if (!use_sort) {
+        CK(cudaMemsetAsync(c->ptmp.p, 0, (c->N + 1) * 8, c->st));
+        if (tot) {
+            k_key_hist<<<blocks_for(tot, 256), 256, 0, c->st>>>(tot, c->kin_s.p, (unsigned)c->N, c->ptmp.p);
+            check_launch(c, "k_key_hist");
+        }
+        exclusive_scan_u64(c, c->ptmp.p, c->N + 1);
+        if (tot) {
+            c->pcur.ensure(c->N + 1);
+            CK(cudaMemcpyAsync(c->pcur.p, c->ptmp.p, (c->N + 1) * 8, cudaMemcpyDeviceToDevice, c->st));
+            k_key_place<<<blocks_for(tot, 256), 256, 0, c->st>>>(tot, c->kin_s.p, c->vin_s.p, (unsigned)c->N,
+                                                                   c->pcur.p, c->E.p + off);
+            check_launch(c, "k_key_place");
+        }
+        HTRACE("expand: place");
+    } else {
+    c->kout_s.ensure(std::max<uint64_t>(tot, 1));
     if (tot) {
         const int bits = bits_for(c->N);
         auto vi = reinterpret_cast<unsigned long long*>(c->vin_s.p);
@@ -1704,6 +1728,7 @@ static void phi_append(Ctx* c) {
     HTRACE("expand: sort");
     k_bounds<<<blocks_for(c->N + 1, 256), 256, 0, c->st>>>(c->kout_s.p, tot, c->N, c->ptmp.p);
     check_launch(c, "k_bounds");
+    }
     k_cols_set<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->ptmp.p, off, c->cols.p);
     check_launch(c, "k_cols_set");
     // batch tails carry the sentinel key N (sorted last): ptmp[N] counts the rest
