@@ -54,3 +54,26 @@ def test_counting_placement_matches_radix_sort(name):
     a, b, a2 = _run(name, False), _run(name, True), _run(name, False)
     assert a == b
     assert a == a2
+
+
+def test_reinit_reuses_cached_z_approx(wam, orc):
+    """zA (the per-ray approximation part of Z) is computed once per (matrix,
+    L, Haar model) and reused by later wam_init calls (wamgpu.cu compute_z0):
+    a second run, and one after an AM init in between (L = 0 row sums), must
+    repeat the first bit for bit."""
+    from paper_1508_04458_b200 import configs
+    from wam_testutil import problem_inputs
+    cfg, _, _, I0, d = problem_inputs("small_lug", orc, wam)
+    c = wam.Context(0)
+    c.set_geometry(configs.geometry(cfg, wam.Geometry))
+    c.set_data(d, I0)
+    runs = []
+    for am_between in (False, False, True):
+        if am_between:
+            c.am_init()
+            c.am_iterate(2)
+        c.wam_init(cfg["L"])
+        rec = c.wam_run(cfg["J"], cfg["schedule"], 0.1)
+        runs.append(([r["objective"] for r in rec], c.tree().tobytes(), c.z_rows().tobytes(), c.scalars()["Z0"]))
+    assert runs[0] == runs[1] == runs[2]
+    c.close()
