@@ -1184,8 +1184,15 @@ __global__ void __launch_bounds__(32 * 8) k_walk_lv(uint64_t M, const unsigned l
     }
     __syncthreads();
     const int len = s_len[g * 32 + lane];
-    int maxlen = 0;   // CTA-uniform round count (barriers inside the loop)
-    for (int r = lane; r < nrays; r += 32) maxlen = max(maxlen, s_len[r]);
+    // nlev == 1 (every cfg2 expansion activates one level): each warp stages
+    // and walks only its own 32 rays, synchronised by __syncwarp, so warps
+    // do not wait for each other at a CTA barrier every round (ncu: 14% of the
+    // stall samples were that barrier) and run only their own rays' rounds.
+    const bool priv = nlev == 1;
+    int maxlen = 0;   // round count: CTA-uniform (barriers inside the loop), or the warp's own
+    if (priv) maxlen = len;
+    else
+        for (int r = lane; r < nrays; r += 32) maxlen = max(maxlen, s_len[r]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
     const bool pow2 = (nx & (nx - 1)) == 0;
@@ -1265,12 +1272,18 @@ __global__ void __launch_bounds__(32 * 8) k_walk_lv(uint64_t M, const unsigned l
     // buffered: round r+1 is in flight while round r is processed.
     auto stage = [&](int base, int st) {
         uint2 (*bs)[D + 1] = buf + st * nrays;
-        for (int j = RPI * w + half; j < nrays; j += RPI * nw) {
+        const int j0 = priv ? g * 32 + half : RPI * w + half, j1 = priv ? g * 32 + 32 : nrays;
+        const int js = priv ? RPI : RPI * nw;
+        for (int j = j0; j < j1; j += js) {
             const int nj = s_len[j];
             const bool ok = base + sub < nj;
             cp_async8(&bs[j][sub], A + (ok ? s_lo[j] + (unsigned)(base + sub) : 0ull), ok);
         }
         cp_async_commit();
+    };
+    auto rsync = [&]() {
+        if (priv) __syncwarp();
+        else __syncthreads();
     };
     if (NS == 2 && maxlen > 0) stage(0, 0);
     for (int base = 0, rnd = 0; base < maxlen; base += D, ++rnd) {
@@ -1283,7 +1296,7 @@ __global__ void __launch_bounds__(32 * 8) k_walk_lv(uint64_t M, const unsigned l
         } else {
             cp_async_wait<0>();
         }
-        __syncthreads();
+        rsync();
         uint2 (*bcur)[D + 1] = buf + (NS == 2 ? (rnd & 1) * nrays : 0);
         const int n = min(D, len - base);       // may be <= 0
         int nit = min(D, max(0, len - base));   // warp-uniform trip count (drains need convergence)
@@ -1315,7 +1328,7 @@ __global__ void __launch_bounds__(32 * 8) k_walk_lv(uint64_t M, const unsigned l
             }
             if (__any_sync(0xffffffffu, rc > kR - 3)) wdrain();
         }
-        __syncthreads();
+        rsync();
     }
     flush();
     wdrain();
