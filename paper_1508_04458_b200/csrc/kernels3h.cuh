@@ -462,12 +462,32 @@ __global__ void __launch_bounds__(32 * 5) k_walk3h(uint64_t M, const unsigned lo
                 const double hh = fabs(pH * cl), vv = fabs(pV * cl), dd = fabs(pD * cl), aa = fabs(pA * cl);
                 const double t = (((((hh + vv) + dd) + aa) + hh) + vv) + dd;
                 const unsigned* zb = zbits + zoff.off[l] + (uint64_t)cur * W;
+                // four set z-blocks per step: their tot slots are distinct, so
+                // the four load-add-store chains overlap (the level-1 warp's
+                // per-flush loop is what the other level warps wait for at the
+                // round barrier, profiles/r04_ncu_walk_src.txt); each slot still
+                // receives t in ray order, so the sums are unchanged
+                double* sb = stot + toff + lane;
                 for (int wi = 0; wi < W; ++wi) {
                     unsigned m = zb[wi];
                     while (m) {
-                        const int k = wi * 32 + __ffs(m) - 1;
+                        const int k0 = __ffs(m) - 1;
                         m &= m - 1;
-                        stot[toff + k * 32 + lane] += t;
+                        const int k1 = m ? __ffs(m) - 1 : -1;
+                        m &= m - 1;
+                        const int k2 = m ? __ffs(m) - 1 : -1;
+                        m &= m - 1;
+                        const int k3 = m ? __ffs(m) - 1 : -1;
+                        m &= m - 1;
+                        double* p0 = sb + (wi * 32 + k0) * 32;
+                        double* p1 = sb + (wi * 32 + (k1 < 0 ? k0 : k1)) * 32;
+                        double* p2 = sb + (wi * 32 + (k2 < 0 ? k0 : k2)) * 32;
+                        double* p3 = sb + (wi * 32 + (k3 < 0 ? k0 : k3)) * 32;
+                        const double v0 = *p0, v1 = *p1, v2 = *p2, v3 = *p3;
+                        *p0 = v0 + t;
+                        if (k1 >= 0) *p1 = v1 + t;
+                        if (k2 >= 0) *p2 = v2 + t;
+                        if (k3 >= 0) *p3 = v3 + t;
                     }
                 }
                 ++count;
