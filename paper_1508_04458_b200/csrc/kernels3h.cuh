@@ -400,7 +400,7 @@ __global__ void k_mark3h(int nx, int ny, int nzl, int P, int L, const double* __
 //   cnt[y*L + l-1] = number of level-l blocks b crossed with any active k.
 // MODE 2: emit one Psi entry per such (y, b): key = koff[l] + b, payload at pos.
 template <int MODE, int L>
-__global__ void __launch_bounds__(32 * 5) k_walk3h(uint64_t M, const unsigned long long* __restrict__ rp,
+__global__ void __launch_bounds__(32 * 6) k_walk3h(uint64_t M, const unsigned long long* __restrict__ rp,
                                                    const uint2* __restrict__ A, int nx, int ny, int nzl,
                                                    const unsigned* __restrict__ tbits, ActOff boff, int tree_words,
                                                    const unsigned* __restrict__ zbits, ActOff zoff, ActOff koff,
@@ -408,13 +408,20 @@ __global__ void __launch_bounds__(32 * 5) k_walk3h(uint64_t M, const unsigned lo
                                                    unsigned long long* __restrict__ cnt,
                                                    const unsigned long long* __restrict__ pos,
                                                    unsigned* __restrict__ keys, uint2* __restrict__ vidx,
-                                                   unsigned* __restrict__ pray, float4* __restrict__ ppsi) {
+                                                   unsigned* __restrict__ pray, float4* __restrict__ ppsi,
+                                                   int split1) {
     extern __shared__ unsigned char dsm[];
     unsigned* tsm = reinterpret_cast<unsigned*>(dsm);                                // tree_words
     double* stot = reinterpret_cast<double*>(dsm + ((tree_words * 4 + 15) / 16) * 16);  // sum_l (nzl>>l)*32
     __shared__ uint2 buf[32][33];
     __shared__ unsigned long long s_lo[32], s_len[32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, l = L - w, nlev = blockDim.x >> 5;
+    // split1 (MODE 1, level 1 walked): one extra warp also walks level 1 and
+    // owns the high 16 bits of every z-bit word, the level-1 warp the low 16,
+    // so the heaviest flush loop is shared (each tot slot keeps one owner and
+    // its ray-order sum)
+    const int nwarp = blockDim.x >> 5, nlev = nwarp - split1;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, l = w < nlev ? L - w : 1;
+    const unsigned hmask = !split1 || l != 1 ? 0xffffffffu : (w < nlev ? 0x0000ffffu : 0xffff0000u);
     for (int i = threadIdx.x; i < tree_words; i += blockDim.x) tsm[i] = tbits[i];
     int toff = 0;  // offset of this level's tot block in stot
     for (int k = L; k > l; --k) toff += (nzl >> k) * 32;
@@ -469,7 +476,7 @@ __global__ void __launch_bounds__(32 * 5) k_walk3h(uint64_t M, const unsigned lo
                 // receives t in ray order, so the sums are unchanged
                 double* sb = stot + toff + lane;
                 for (int wi = 0; wi < W; ++wi) {
-                    unsigned m = zb[wi];
+                    unsigned m = zb[wi] & hmask;
                     while (m) {
                         const int k0 = __ffs(m) - 1;
                         m &= m - 1;
@@ -505,7 +512,7 @@ __global__ void __launch_bounds__(32 * 5) k_walk3h(uint64_t M, const unsigned lo
     };
 
     for (unsigned long long base = 0; base < maxlen; base += 32) {
-        for (int j = w; j < 32; j += nlev) {
+        for (int j = w; j < 32; j += nwarp) {
             const unsigned long long nj = s_len[j];
             const bool ok = base + lane < nj;
             cp_async8(&buf[j][lane], A + (ok ? s_lo[j] + base + lane : 0), ok);
@@ -539,7 +546,7 @@ __global__ void __launch_bounds__(32 * 5) k_walk3h(uint64_t M, const unsigned lo
     }
     flush();
     if (MODE == 1) {
-        if (y < M) cnt[y * L + (l - 1)] = count;
+        if (y < M && w < nlev) cnt[y * L + (l - 1)] = count;
         __syncthreads();
         if (w == 0 && y < M) {
             for (int k = 1; k <= L - nlev; ++k) cnt[y * L + (k - 1)] = 0;

@@ -1174,13 +1174,20 @@ static void launch_walk3h(Ctx* c, int nlev, unsigned long long* cnt, const unsig
     for (int l = 1; l <= c->L; ++l) stot += (size_t)(c->nzl >> l) * 32 * 8;
     const size_t smem = ((size_t)c->tree_words * 4 + 15) / 16 * 16 + stot;
     if (smem > 200 * 1024) throw ConfigError("tree too large for the shared-memory 3D walk");
+    // Z walk with level 1 walked and >= 32 level-1 z-blocks: a second warp
+    // takes half of the level-1 flush loop (WAMGPU_WALK3_SPLIT=0 turns it off)
+    static const bool split_on = [] {
+        const char* e = std::getenv("WAMGPU_WALK3_SPLIT");
+        return !(e && e[0] == '0');
+    }();
+    const int split1 = (MODE == 1 && split_on && nlev == c->L && (c->nzl >> 1) >= 32) ? 1 : 0;
 #define W3(LV)                                                                                                   \
     case LV: {                                                                                                   \
         auto kf = k_walk3h<MODE, LV>;                                                                            \
         if (smem > 32 * 1024) CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        kf<<<nb, 32 * nlev, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->nzl, c->tbits.p, c->boff,     \
-                                           c->tree_words, c->zbits.p, c->zoff, c->koff, c->zA.p, c->zrow.p, cnt,  \
-                                           pos, c->kin_s.p, c->vin_s.p, c->pray_s.p, c->ppsi_s.p);                \
+        kf<<<nb, 32 * (nlev + split1), smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, c->nzl, c->tbits.p,  \
+                                           c->boff, c->tree_words, c->zbits.p, c->zoff, c->koff, c->zA.p, c->zrow.p, \
+                                           cnt, pos, c->kin_s.p, c->vin_s.p, c->pray_s.p, c->ppsi_s.p, split1);    \
     } break;
     switch (c->L) {
         W3(1) W3(2) W3(3) W3(4) W3(5)
