@@ -114,6 +114,9 @@ CONFIGS = {
                      phantom="luggage"),
     "tiny3d24": dict(nx=32, ny=32, nz=24, voxel=4.0, views=60, detectors=64, I0=1e5, L=3, J=10, seed=24,
                      phantom="luggage"),
+    # 64 slices: 32 level-1 z-blocks, so the 3D Z walk splits level 1 across two warps
+    "tiny3d64": dict(nx=32, ny=32, nz=64, voxel=4.0, views=60, detectors=64, I0=1e5, L=3, J=10, seed=25,
+                     phantom="luggage"),
     "small_lug": dict(nx=128, ny=128, nz=1, voxel=2.0, views=120, detectors=192, I0=2e5, L=4, J=20, seed=13,
                       phantom="luggage"),
 }

@@ -91,7 +91,7 @@ def test_wam3d_parity_tree_bit_exact(wam, orc, name):
     assert rel_l2(bm, bm32) < TOL_MIRROR and rel_l2(bp, bp32) < TOL_MIRROR
 
 
-@pytest.mark.parametrize("name", ["tiny3d", "tiny3d16", "tiny3d24", "small3d"])
+@pytest.mark.parametrize("name", ["tiny3d", "tiny3d16", "tiny3d24", "tiny3d64", "small3d"])
 def test_wam3d_separable_haar_parity(wam, orc, name):
     """Separable 3D Haar model (pin P3): octree tree bit-exact vs both oracles
     after every expansion, Z0 bit-exact vs the mirror, mu / I-div within bars."""
