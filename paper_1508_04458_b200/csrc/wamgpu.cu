@@ -224,7 +224,7 @@ struct wamgpu_ctx {
     size_t tev_used[T_NCAT] = {};
     int64_t launches = 0;
 
-    void timer_begin(Cat c) {
+    void timer_begin(Cat c, cudaStream_t s = nullptr) {
         if (!ktime) return;
         auto& v = tev[c];
         if (tev_used[c] == v.size()) {
@@ -233,11 +233,11 @@ struct wamgpu_ctx {
             CK(cudaEventCreate(&b));
             v.push_back({a, b});
         }
-        CK(cudaEventRecord(v[tev_used[c]].first, st));
+        CK(cudaEventRecord(v[tev_used[c]].first, s ? s : st));
     }
-    void timer_end(Cat c) {
+    void timer_end(Cat c, cudaStream_t s = nullptr) {
         if (!ktime) return;
-        CK(cudaEventRecord(tev[c][tev_used[c]].second, st));
+        CK(cudaEventRecord(tev[c][tev_used[c]].second, s ? s : st));
         tev_used[c]++;
     }
 };
@@ -2068,6 +2068,27 @@ static void wam_step(Ctx* c) {
     const bool split = wam_split_update(c);   // 3D view group: reduce-scatter / own tiles / all-gather
     const TileMap tm = split ? make_tilemap(c) : TileMap{};
     double* bm2 = fused ? c->ar.extra.p : c->g.p + c->N;
+    // one GPU, 2D: the signed split (b- over Phi^-) and the back projection
+    // (g = H^T q) both read only q and write disjoint halves of [g || b-], so
+    // the split runs on the side stream concurrently with the back projection
+    // (WAMGPU_SPLIT_OVERLAP=0: sequential)
+    static const bool ovl_on = [] {
+        const char* e = std::getenv("WAMGPU_SPLIT_OVERLAP");
+        return !(e && e[0] == '0');
+    }();
+    const bool ovl = ovl_on && !c->haar3 && c->nlist && c->nzl == 1 && !fused && !split && !view_sharded(c) &&
+                     c->split_variant == 0;
+    if (ovl) {
+        CK(cudaEventRecord(c->ev_x, c->st));
+        CK(cudaStreamWaitEvent(c->st2, c->ev_x, 0));
+        c->timer_begin(T_SPLIT, c->st2);
+        const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist + 7) / 8, (uint64_t)c->sms * 16);
+        k_split<12><<<nb, 256, 0, c->st2>>>(c->nlist, c->list.p, c->cols.p, c->E.p, c->q.p, bm2);
+        check_launch(c, "k_split");
+        c->timer_end(T_SPLIT, c->st2);
+        c->tm.split_launches++;
+        CK(cudaEventRecord(c->ev_y, c->st2));
+    }
     if (split) {
         back_launch(c, c->q.p, c->rs_send.p, nullptr, true, tm);   // g straight into the tile-major T
         CK(cudaEventRecord(c->ev_x, c->st));
@@ -2112,7 +2133,7 @@ static void wam_step(Ctx* c) {
         check_launch(c, "k_split3h");
         c->timer_end(T_SPLIT);
         c->tm.split_launches++;
-    } else if (!c->haar3 && c->nlist) {
+    } else if (!c->haar3 && c->nlist && !ovl) {
         c->timer_begin(T_SPLIT);
         const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist + 7) / 8, (uint64_t)c->sms * 16);
         if (c->nzl == 1) {
@@ -2156,6 +2177,7 @@ static void wam_step(Ctx* c) {
     } else if (view_sharded(c)) {
         allreduce_sum(c, c->g.p, 2 * NV(c), S_VIEWS);   // view shards: partial sums of [g || b-]
     }
+    if (ovl) CK(cudaStreamWaitEvent(c->st, c->ev_y, 0));
     c->timer_begin(T_UPDATE);
     tile_launch(c, 1, nullptr, nullptr);
     c->timer_end(T_UPDATE);
