@@ -1083,19 +1083,13 @@ __global__ void k_cols_set(uint64_t n, const unsigned long long* __restrict__ pt
 // Counting placement of an unsorted (z, (y, phi)) batch into per-column runs,
 // replacing a radix sort of the batch (three 8-bit passes over 12 B pairs):
 // the split sums each column in exact fixed point, so the order of rays inside
-// a column is free and only the run bounds matter.  Warp-aggregated atomics:
-// lanes holding the same key (neighbouring rays cross the same blocks) take one
-// atomic per key.  k_key_hist counts keys in [0, n] (the sentinel n included,
-// so after an exclusive scan cnt[n] = number of real entries, as k_bounds);
-// k_key_place moves each real entry to cur[z]++ of a copy of the bounds.
-__global__ void k_key_hist(uint64_t n, const unsigned* __restrict__ keys, unsigned nkey,
-                           unsigned long long* __restrict__ cnt) {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const unsigned k = i < n ? keys[i] : 0xffffffffu;
-    const unsigned peers = __match_any_sync(0xffffffffu, k);
-    const int lane = threadIdx.x & 31;
-    if (k <= nkey && lane == __ffs(peers) - 1) atomicAdd(&cnt[k], (unsigned long long)__popc(peers));
-}
+// a column is free and only the run bounds matter.  The key histogram is taken
+// by the expansion walk as it drains (k_walk_lv, kcnt: one atomic per distinct
+// key among the lanes' k-th entries); after an exclusive scan it holds the
+// column bounds and cnt[n] = number of real entries (sentinels not counted).
+// k_key_place moves each real entry to cur[z]++ of a copy of the bounds, with
+// warp-aggregated atomics (lanes holding the same key take one atomic; plain
+// per-entry atomics measured slower, profiles/r04_placement_ab.txt).
 __global__ void k_key_place(uint64_t n, const unsigned* __restrict__ keys, const uint2* __restrict__ vals,
                             unsigned nkey, unsigned long long* __restrict__ cur, uint2* __restrict__ out) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1158,7 +1152,8 @@ __global__ void __launch_bounds__(32 * 8) k_walk_lv(uint64_t M, const unsigned l
                                                     int tree_words, const long long* __restrict__ zin,
                                                     long long* __restrict__ zout,
                                                     unsigned long long* __restrict__ cursor, unsigned long long cap,
-                                                    unsigned* __restrict__ keys, uint2* __restrict__ vals) {
+                                                    unsigned* __restrict__ keys, uint2* __restrict__ vals,
+                                                    unsigned long long* __restrict__ kcnt) {
     constexpr int kR = WLV_R;
     extern __shared__ __align__(16) unsigned char wsm[];
     const WalkSmem L_ = walk_smem(G, nlev, tree_words, D, NS);
@@ -1254,11 +1249,29 @@ __global__ void __launch_bounds__(32 * 8) k_walk_lv(uint64_t M, const unsigned l
             if (lane == 0) nb = atomicAdd(cursor, need);
             nb = __shfl_sync(0xffffffffu, nb, 0);
         }
-        for (int k = 0; k < rc; ++k) {
-            const unsigned long long j = pre + (unsigned)k;
-            const unsigned long long p = j < rem ? cb + j : nb + (j - rem);
-            const uint2 r = ring[k * TB + threadIdx.x];
-            if (p < cap) { keys[p] = r.x; vals[p] = make_uint2((unsigned)y, r.y); }
+        if (kcnt == nullptr) {
+            for (int k = 0; k < rc; ++k) {
+                const unsigned long long j = pre + (unsigned)k;
+                const unsigned long long p = j < rem ? cb + j : nb + (j - rem);
+                const uint2 r = ring[k * TB + threadIdx.x];
+                if (p < cap) { keys[p] = r.x; vals[p] = make_uint2((unsigned)y, r.y); }
+            }
+        } else {
+            // the counting placement's key histogram, taken here (no separate
+            // histogram pass): the lanes' k-th entries (neighbouring rays,
+            // often the same block) share one atomic per distinct key
+            const int mrc = (int)__reduce_max_sync(0xffffffffu, (unsigned)rc);
+            for (int k = 0; k < mrc; ++k) {
+                const bool v = k < rc;
+                const uint2 r = v ? ring[k * TB + threadIdx.x] : make_uint2(0xffffffffu, 0u);
+                if (v) {
+                    const unsigned long long j = pre + (unsigned)k;
+                    const unsigned long long p = j < rem ? cb + j : nb + (j - rem);
+                    if (p < cap) { keys[p] = r.x; vals[p] = make_uint2((unsigned)y, r.y); }
+                }
+                const unsigned peers = __match_any_sync(0xffffffffu, r.x);
+                if (v && lane == __ffs(peers) - 1) atomicAdd(&kcnt[r.x], (unsigned long long)__popc(peers));
+            }
         }
         if (T > rem) { cb = nb + (T - rem); ce = nb + need; }
         else cb += T;

@@ -1072,7 +1072,8 @@ static void upload_tree_bits(Ctx* c, const std::vector<uint8_t>& src) {
 
 // incremental expansion walk over the new-block bits in tbits: levels in
 // lvpack (4 bits each, nlev warps), zfix -> zfix2, triples -> kin_s / vin_s
-static void launch_walk_lv(Ctx* c, int nlev, unsigned lvpack, unsigned long long cap) {
+static void launch_walk_lv(Ctx* c, int nlev, unsigned lvpack, unsigned long long cap,
+                           unsigned long long* kcnt = nullptr) {
     // G ray groups of 32 per CTA so that a CTA has ~4 warps whatever nlev is
     const int G = std::max(1, 4 / nlev);
     const unsigned nb = blocks_for(c->Ml, 32 * G);
@@ -1083,7 +1084,8 @@ static void launch_walk_lv(Ctx* c, int nlev, unsigned lvpack, unsigned long long
         CK(cudaFuncSetAttribute(k_walk_lv<D, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
         k_walk_lv<D, NS><<<nb, 32 * nlev * G, smem, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, c->ny, nlev, G, lvpack, \
                                                             c->tbits.p, c->boff, c->tree_words, c->zfix.p,        \
-                                                            c->zfix2.p, c->cursor.p, cap, c->kin_s.p, c->vin_s.p); \
+                                                            c->zfix2.p, c->cursor.p, cap, c->kin_s.p, c->vin_s.p,  \
+                                                            kcnt);                                                \
     }
     switch (c->walk_variant) {
         case 1: WL(8, 2) break;
@@ -1685,11 +1687,17 @@ static void phi_append(Ctx* c) {
     // capacity guess for the batch (a short guess costs a second walk)
     unsigned long long tot = 0;
     uint64_t cap = std::max<uint64_t>({c->kin_s.n, 2 * c->phi_batch, c->nnz / 4, (uint64_t)1 << 20});
+    static const bool use_sort = [] {
+        const char* e = std::getenv("WAMGPU_PHI_SORT");
+        return e && e[0] == '1';
+    }();
+    c->ptmp.ensure(c->N + 1);
     for (int attempt = 0;; ++attempt) {
         c->kin_s.ensure(cap);
         c->vin_s.ensure(cap);
         CK(cudaMemsetAsync(c->cursor.p, 0, 8, c->st));
-        launch_walk_lv(c, nlev, lvpack, c->kin_s.n);
+        if (!use_sort) CK(cudaMemsetAsync(c->ptmp.p, 0, (c->N + 1) * 8, c->st));
+        launch_walk_lv(c, nlev, lvpack, c->kin_s.n, use_sort ? nullptr : c->ptmp.p);
         CK(cudaMemcpyAsync(&tot, c->cursor.p, 8, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
         if (tot <= c->kin_s.n) break;
@@ -1708,19 +1716,11 @@ static void phi_append(Ctx* c) {
     }
     c->ptmp.ensure(c->N + 1);
     HTRACE("expand: E grow");
-    // Counting placement (default): histogram of the batch's keys, exclusive
-    // scan into the column bounds, warp-aggregated placement.  WAMGPU_PHI_SORT=1
-    // keeps the earlier radix sort + k_bounds (same runs, other ray order).
-    static const bool use_sort = [] {
-        const char* e = std::getenv("WAMGPU_PHI_SORT");
-        return e && e[0] == '1';
-    }();
+    // Counting placement (default): the walk histogrammed the batch's keys
+    // into ptmp (sentinels not counted), exclusive scan into the column
+    // bounds, warp-aggregated placement.  WAMGPU_PHI_SORT=1 keeps the earlier
+    // radix sort + k_bounds (same runs, other ray order).
     if (!use_sort) {
-        CK(cudaMemsetAsync(c->ptmp.p, 0, (c->N + 1) * 8, c->st));
-        if (tot) {
-            k_key_hist<<<blocks_for(tot, 256), 256, 0, c->st>>>(tot, c->kin_s.p, (unsigned)c->N, c->ptmp.p);
-            check_launch(c, "k_key_hist");
-        }
         exclusive_scan_u64(c, c->ptmp.p, c->N + 1);
         if (tot) {
             c->pcur.ensure(c->N + 1);
