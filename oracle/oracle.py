@@ -68,6 +68,7 @@ def lib():
         _lib.orc_poisson.argtypes = [C.c_uint64, C.c_uint64, C.c_double]
         _lib.orc_solve_update.argtypes = [C.c_double] * 5 + [_d]
         _lib.orc_create.argtypes = [C.POINTER(Geometry), C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        _lib.orc_create_ex.argtypes = [C.POINTER(Geometry), C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         _lib.orc_destroy.argtypes = [C.c_void_p]
         _lib.orc_destroy.restype = None
     return _lib
@@ -112,10 +113,12 @@ def make_geometry(nx, ny, nz, voxel, views, detectors, spacing=1.0, beam=2, sod=
 class Problem:
     """Oracle problem: geometry + system matrix + AM/WAM state (f64 or fp32-mirror)."""
 
-    def __init__(self, geom: Geometry, mirror=False, threads=0):
+    def __init__(self, geom: Geometry, mirror=False, threads=0, slim=False):
+        """slim: CSR only (no exact-h copy, no CSC mirror; fp32 h in mirror mode),
+        bit-identical results; the memory mode for cfg4."""
         L = lib()
         h = C.c_void_p()
-        _chk(L.orc_create(C.byref(geom), int(mirror), int(threads), C.byref(h)))
+        _chk(L.orc_create_ex(C.byref(geom), int(mirror), int(threads), 1 if slim else 0, C.byref(h)))
         self.h = h
         self.geom = geom
         M, N, nnz, nz = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_int()

@@ -258,9 +258,23 @@ static double poisson(uint64_t seed, uint64_t stream, double m) {
 
 using namespace orc;
 
+// Psi lists of one level (3D model): per in-plane block b, the rays crossing b
+// (ascending) with psi_A, psi_H, psi_V, psi_D (2^-l scaled quadrant
+// combinations of phi_walk; fp32-rounded in mirror mode, exact f64 otherwise).
+struct PsiLevel {
+    std::vector<uint64_t> ptr;                 // [b + 1]
+    std::vector<uint32_t> ray;                 // [entry]
+    std::vector<std::array<double, 4>> val;    // [entry]
+};
+
 struct orc_problem {
     Geom g;
     bool mirror = false;
+    // slim (ORC_SLIM): CSR only, no exact-h copy and no CSC mirror; h stored as
+    // fp32 in mirror mode.  Back projection is then a ray-ordered CSR scatter
+    // per slice group, which adds the terms of every voxel in the same
+    // (ascending-ray) order as the CSC gather, so results are bit-identical.
+    bool slim = false;
     int threads = 0;
     uint64_t Ms = 0, Ns = 0;
     int nz = 1;
@@ -268,9 +282,11 @@ struct orc_problem {
     std::vector<uint64_t> rp;
     std::vector<uint32_t> ci;
     std::vector<double> hexact, hv;  // hv = stored h (fp32-rounded in mirror mode)
+    std::vector<float> hv32;         // slim + mirror: stored h as fp32
     std::vector<uint64_t> cp;
     std::vector<uint32_t> ri;
     std::vector<double> cv;
+    inline double hvk(uint64_t k) const { return hv32.empty() ? hv[k] : (double)hv32[k]; }
     std::vector<double> d, I0;  // stored data
     // AM state
     bool am_ready = false;
@@ -288,10 +304,9 @@ struct orc_problem {
     int wam_iter = 0;
     // separable 3D Haar (pin P3): act[l] is over (nz>>l, ny>>l, nx>>l) blocks
     bool haar3 = false;
-    // mirror mode, 3D: Psi lists per (level, in-plane block) with any active z-block
-    std::vector<std::vector<uint64_t>> psi_ptr;            // [l][b + 1]
-    std::vector<std::vector<uint32_t>> psi_ray;            // [l][entry]
-    std::vector<std::vector<std::array<float, 4>>> psi_val; // [l][entry] A, H, V, D (2^-l scaled)
+    // 3D: Psi lists per (level, in-plane block) with any active z-block (and,
+    // at reference precision, every level-L block for the approximation split)
+    std::vector<PsiLevel> psi;                              // [l]
     // mirror mode: explicit negative-phi columns for active details, per slice-0 Mallat z
     std::vector<uint64_t> nphi_ptr;
     std::vector<uint32_t> nphi_row;
@@ -312,35 +327,37 @@ static void build_matrix(orc_problem* p) {
     p->rays.resize(p->Ms);
     for (int v = 0; v < V; ++v)
         for (int k = 0; k < D; ++k) p->rays[(uint64_t)v * D + k] = make_ray(g, v, k);
-    // threaded trace, per-chunk buffers concatenated in row order (== serial build)
+    // threaded two-pass trace (count, then fill in place): each row holds the
+    // entries of trace_ray in Siddon order, exactly as the serial build emits them
     int nt = resolve_threads(p->threads);
-    std::vector<std::vector<uint32_t>> cols(nt);
-    std::vector<std::vector<double>> vals(nt);
     std::vector<uint64_t> cnt(p->Ms);
-    std::vector<std::size_t> chunk_lo(nt, 0), chunk_hi(nt, 0);
-    parallel_for(p->Ms, nt, [&](std::size_t lo, std::size_t hi, int b) {
-        chunk_lo[b] = lo; chunk_hi[b] = hi;
+    parallel_for(p->Ms, nt, [&](std::size_t lo, std::size_t hi, int) {
         for (std::size_t y = lo; y < hi; ++y) {
-            uint64_t before = vals[b].size();
-            trace(g, p->rays[y], [&](int ix, int iy, double len) {
-                cols[b].push_back((uint32_t)iy * (uint32_t)g.nx + (uint32_t)ix);  // projector.hpp:141
-                vals[b].push_back(len);
-            });
-            cnt[y] = vals[b].size() - before;
+            uint64_t c = 0;
+            trace(g, p->rays[y], [&](int, int, double) { ++c; });
+            cnt[y] = c;
         }
     });
     p->rp.assign(p->Ms + 1, 0);
     for (uint64_t y = 0; y < p->Ms; ++y) p->rp[y + 1] = p->rp[y] + cnt[y];
-    uint64_t nnz = p->rp[p->Ms];
-    p->ci.resize(nnz); p->hexact.resize(nnz);
-    uint64_t off = 0;
-    for (int b = 0; b < nt; ++b) {
-        std::copy(cols[b].begin(), cols[b].end(), p->ci.begin() + off);
-        std::copy(vals[b].begin(), vals[b].end(), p->hexact.begin() + off);
-        off += cols[b].size();
-    }
-    p->hv.resize(nnz);
-    for (uint64_t k = 0; k < nnz; ++k) p->hv[k] = p->st(p->hexact[k]);
+    std::vector<uint64_t>().swap(cnt);
+    const uint64_t nnz = p->rp[p->Ms];
+    p->ci.resize(nnz);
+    const bool f32 = p->slim && p->mirror;
+    if (!p->slim) p->hexact.resize(nnz);
+    if (f32) p->hv32.resize(nnz); else p->hv.resize(nnz);
+    parallel_for(p->Ms, nt, [&](std::size_t lo, std::size_t hi, int) {
+        for (std::size_t y = lo; y < hi; ++y) {
+            uint64_t k = p->rp[y];
+            trace(g, p->rays[y], [&](int ix, int iy, double len) {
+                p->ci[k] = (uint32_t)iy * (uint32_t)g.nx + (uint32_t)ix;  // projector.hpp:141
+                if (!p->slim) p->hexact[k] = len;
+                if (f32) p->hv32[k] = (float)len; else p->hv[k] = p->st(len);
+                ++k;
+            });
+        }
+    });
+    if (p->slim) return;
     // system_matrix.hpp:61-75 counting-sort transpose (rows ascending per column)
     p->cp.assign(p->Ns + 1, 0);
     for (uint32_t c : p->ci) p->cp[c + 1]++;
@@ -355,14 +372,51 @@ static void build_matrix(orc_problem* p) {
         }
 }
 
+// Slab transposes: a[s*n + i] <-> t[i*nz + s] (the 3D loops below keep one
+// voxel's or one ray's nz values contiguous; the summation orders are those of
+// the per-slice loops, so the results are bit-identical).
+static void to_slab(const double* a, uint64_t n, int nz, std::vector<double>& t, int threads) {
+    t.resize(n * (uint64_t)nz);
+    parallel_for(n, threads, [&](std::size_t lo, std::size_t hi, int) {
+        for (std::size_t i = lo; i < hi; ++i)
+            for (int s = 0; s < nz; ++s) t[i * nz + s] = a[(uint64_t)s * n + i];
+    });
+}
+static void from_slab(const std::vector<double>& t, uint64_t n, int nz, double* a, int threads) {
+    parallel_for(n, threads, [&](std::size_t lo, std::size_t hi, int) {
+        for (int s = 0; s < nz; ++s)
+            for (std::size_t i = lo; i < hi; ++i) a[(uint64_t)s * n + i] = t[i * nz + s];
+    });
+}
+
 // forward_project: l(s*M+y) = sum_k h_k mu(s*N+col_k), CSR order.
 static void forward(const orc_problem* p, const double* mu, double* out) {
+    if (p->nz > 1) {  // slab form: one ray's entries applied to all slices at once
+        const int nz = p->nz;
+        std::vector<double> muT, lT(p->Ms * (uint64_t)nz);
+        to_slab(mu, p->Ns, nz, muT, p->threads);
+        parallel_for(p->Ms, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+            std::vector<double> acc((std::size_t)nz);
+            for (std::size_t y = lo; y < hi; ++y) {
+                std::fill(acc.begin(), acc.end(), 0.0);
+                double* a = acc.data();
+                for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) {
+                    const double h = p->hvk(k);
+                    const double* m = muT.data() + (uint64_t)p->ci[k] * nz;
+                    for (int s = 0; s < nz; ++s) a[s] += h * m[s];
+                }
+                std::copy(acc.begin(), acc.end(), lT.begin() + y * nz);
+            }
+        });
+        from_slab(lT, p->Ms, nz, out, p->threads);
+        return;
+    }
     parallel_for(p->Ms, p->threads, [&](std::size_t lo, std::size_t hi, int) {
         for (int s = 0; s < p->nz; ++s) {
             const double* m = mu + (uint64_t)s * p->Ns;
             for (std::size_t y = lo; y < hi; ++y) {
                 double acc = 0.0;
-                for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) acc += p->hv[k] * m[p->ci[k]];
+                for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) acc += p->hvk(k) * m[p->ci[k]];
                 out[(uint64_t)s * p->Ms + y] = acc;
             }
         }
@@ -371,6 +425,40 @@ static void forward(const orc_problem* p, const double* mu, double* out) {
 
 // back_project: voxel-driven gather over the CSC mirror.
 static void back(const orc_problem* p, const double* w, double* out) {
+    if (p->nz > 1 || p->slim) {
+        const int nz = p->nz;
+        std::vector<double> wT, gT(p->Ns * (uint64_t)nz, 0.0);
+        to_slab(w, p->Ms, nz, wT, p->threads);
+        if (!p->slim) {  // CSC gather, rows ascending per column
+            parallel_for(p->Ns, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+                for (std::size_t x = lo; x < hi; ++x) {
+                    double* a = gT.data() + x * nz;
+                    for (uint64_t k = p->cp[x]; k < p->cp[x + 1]; ++k) {
+                        const double h = p->cv[k];
+                        const double* ws = wT.data() + (uint64_t)p->ri[k] * nz;
+                        for (int s = 0; s < nz; ++s) a[s] += h * ws[s];
+                    }
+                }
+            });
+        } else {  // CSR scatter in ascending ray order (== the CSC order), slice groups per thread
+            const int G = std::min(resolve_threads(p->threads), nz);
+            parallel_for((std::size_t)G, G, [&](std::size_t lo, std::size_t hi, int) {
+                for (std::size_t gi = lo; gi < hi; ++gi) {
+                    const int s0 = (int)((uint64_t)nz * gi / G), s1 = (int)((uint64_t)nz * (gi + 1) / G);
+                    for (uint64_t y = 0; y < p->Ms; ++y) {
+                        const double* ws = wT.data() + y * nz;
+                        for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) {
+                            const double h = p->hvk(k);
+                            double* a = gT.data() + (uint64_t)p->ci[k] * nz;
+                            for (int s = s0; s < s1; ++s) a[s] += h * ws[s];
+                        }
+                    }
+                }
+            });
+        }
+        from_slab(gT, p->Ns, nz, out, p->threads);
+        return;
+    }
     parallel_for(p->Ns, p->threads, [&](std::size_t lo, std::size_t hi, int) {
         for (int s = 0; s < p->nz; ++s) {
             const double* ws = w + (uint64_t)s * p->Ms;
@@ -479,7 +567,7 @@ static void phi_walk(const orc_problem* p, int L, uint64_t y, CB&& cb) {
     if (L == 0) {  // Omega = I: every voxel is its own approximation block
         for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) {
             const int ix = (int)(p->ci[k] % (uint32_t)nx), iy = (int)(p->ci[k] / (uint32_t)nx);
-            cb(0, iy, ix, p->hv[k], 0.0, 0.0, 0.0);
+            cb(0, iy, ix, p->hvk(k), 0.0, 0.0, 0.0);
         }
         return;
     }
@@ -496,7 +584,7 @@ static void phi_walk(const orc_problem* p, int L, uint64_t y, CB&& cb) {
     };
     for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) {
         const int ix = (int)(p->ci[k] % (uint32_t)nx), iy = (int)(p->ci[k] / (uint32_t)nx);
-        const double h = p->hv[k];
+        const double h = p->hvk(k);
         for (int l = 1; l <= L; ++l) {
             const int bi = iy >> l, bj = ix >> l;
             const int key = bi * (nx >> l) + bj;
@@ -563,43 +651,84 @@ static void compute_z0(orc_problem* p) {
 
 // Explicit negative-phi columns (mirror mode, == the GPU's Phi^- CSC): for every
 // active detail coefficient of slice 0, rays ascending, value (float)phi < 0.
+// Ray chunks with a FIXED count (independent of the thread count), so that
+// chunk-ordered combinations are deterministic on any host.
+static constexpr std::size_t kRayChunks = 64;
+static inline std::size_t chunk_lo(std::size_t n, std::size_t C, std::size_t c) { return n * c / C; }
+
+// Two-pass bucket fill over rays: count(y, add) calls add(bucket) per entry;
+// fill(y, put) calls put(bucket, entry) in the same order.  Entries of a
+// bucket end up in ascending ray order (chunks are contiguous ray ranges and
+// are laid out in chunk order) whatever the thread count.
+template <typename Entry, typename Walk, typename Store>
+static void bucket_rays(const orc_problem* p, std::size_t nbuckets, std::vector<uint64_t>& ptr, Walk&& walk,
+                        Store&& store) {
+    const std::size_t M = p->Ms, C = std::min<std::size_t>(kRayChunks, std::max<std::size_t>(M, 1));
+    std::vector<std::vector<uint64_t>> start(C);   // counts, then each chunk's write cursors
+    parallel_for(C, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+        for (std::size_t c = lo; c < hi; ++c) {
+            start[c].assign(nbuckets, 0);
+            for (std::size_t y = chunk_lo(M, C, c); y < chunk_lo(M, C, c + 1); ++y)
+                walk(y, [&](std::size_t b, const Entry&) { start[c][b]++; });
+        }
+    });
+    ptr.assign(nbuckets + 1, 0);
+    for (std::size_t b = 0; b < nbuckets; ++b) {
+        uint64_t s = ptr[b];
+        for (std::size_t c = 0; c < C; ++c) { const uint64_t n = start[c][b]; start[c][b] = s; s += n; }
+        ptr[b + 1] = s;
+    }
+    store((uint64_t)ptr[nbuckets], Entry{});   // sizing call: index == total
+    parallel_for(C, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+        for (std::size_t c = lo; c < hi; ++c) {
+            auto& st = start[c];
+            for (std::size_t y = chunk_lo(M, C, c); y < chunk_lo(M, C, c + 1); ++y)
+                walk(y, [&](std::size_t b, const Entry& e) { store(st[b]++, e); });
+        }
+    });
+}
+
 static void build_nphi(orc_problem* p) {
     const int L = p->L, nx = p->g.nx;
     const uint64_t N = p->Ns;
-    std::vector<std::vector<std::pair<uint32_t, double>>> cols(N);
-    for (uint64_t y = 0; y < p->Ms; ++y) {
+    using E = std::pair<uint32_t, double>;
+    bool sized = false;
+    auto store = [&](uint64_t i, const E& e) {
+        if (!sized) { p->nphi_row.resize(i); p->nphi_val.resize(i); sized = true; return; }
+        p->nphi_row[i] = e.first; p->nphi_val[i] = e.second;
+    };
+    bucket_rays<E>(p, N, p->nphi_ptr, [&](std::size_t y, auto&& put) {
         phi_walk(p, L, y, [&](int l, int bi, int bj, double, double pH, double pV, double pD) {
             if (l < 1 || !is_active(p, l, bi, bj)) return;
             BlockIdx z = mallat(nx, p->g.ny, l, bi, bj);
             double v[3] = {(double)(float)pH, (double)(float)pV, (double)(float)pD};
             uint32_t zz[3] = {z.H, z.V, z.D};
             for (int t = 0; t < 3; ++t)
-                if (v[t] < 0.0) cols[zz[t]].push_back({(uint32_t)y, v[t]});
+                if (v[t] < 0.0) put(zz[t], E{(uint32_t)y, v[t]});
         });
-    }
-    p->nphi_ptr.assign(N + 1, 0);
-    for (uint64_t z = 0; z < N; ++z) p->nphi_ptr[z + 1] = p->nphi_ptr[z] + cols[z].size();
-    p->nphi_row.resize(p->nphi_ptr[N]);
-    p->nphi_val.resize(p->nphi_ptr[N]);
-    for (uint64_t z = 0; z < N; ++z)
-        for (std::size_t i = 0; i < cols[z].size(); ++i) {
-            p->nphi_row[p->nphi_ptr[z] + i] = cols[z][i].first;
-            p->nphi_val[p->nphi_ptr[z] + i] = cols[z][i].second;
-        }
+    }, store);
 }
 
 // Direct signed split (reference mode): b+(z), b-(z) for every active z of all
-// slices from the same q; per-thread
-// accumulators combined in chunk order.
+// slices from the same q.  Rays are cut
+// into kRayChunks fixed chunks; chunk partials are combined in chunk order (a
+// wave of one chunk per thread at a time bounds the memory), so the result
+// does not depend on the thread count.
 static void direct_split(const orc_problem* p, const std::vector<double>& w, std::vector<double>& bp,
                          std::vector<double>& bm, bool all_coeffs) {
     const int L = p->L, nx = p->g.nx, ny = p->g.ny, nz = p->nz;
     const uint64_t N = p->Ns, M = p->Ms, NT = N * nz;
-    int nt = resolve_threads(p->threads);
+    const std::size_t C = std::min<std::size_t>(kRayChunks, std::max<uint64_t>(M, 1));
+    const int nt = (int)std::min<std::size_t>((std::size_t)resolve_threads(p->threads), C);
+    bp.assign(NT, 0.0); bm.assign(NT, 0.0);
     std::vector<std::vector<double>> tp(nt), tm(nt);
-    parallel_for(M, nt, [&](std::size_t lo, std::size_t hi, int b) {
-        tp[b].assign(NT, 0.0); tm[b].assign(NT, 0.0);
-        auto& P = tp[b]; auto& Mn = tm[b];
+    for (std::size_t c0 = 0; c0 < C; c0 += nt) {
+        const std::size_t nw = std::min<std::size_t>(nt, C - c0);
+        parallel_for(nw, nt, [&](std::size_t wlo, std::size_t whi, int) {
+          for (std::size_t wi = wlo; wi < whi; ++wi) {
+            tp[wi].assign(NT, 0.0); tm[wi].assign(NT, 0.0);
+            auto& P = tp[wi]; auto& Mn = tm[wi];
+            const std::size_t lo = chunk_lo(M, C, c0 + wi), hi = chunk_lo(M, C, c0 + wi + 1);
         for (std::size_t y = lo; y < hi; ++y) {
             phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {
                 for (int s = 0; s < nz; ++s) {
@@ -626,11 +755,10 @@ static void direct_split(const orc_problem* p, const std::vector<double>& w, std
                 }
             });
         }
-    });
-    bp.assign(NT, 0.0); bm.assign(NT, 0.0);
-    for (int b = 0; b < nt; ++b) {
-        if (tp[b].empty()) continue;
-        for (uint64_t z = 0; z < NT; ++z) { bp[z] += tp[b][z]; bm[z] += tm[b][z]; }
+          }
+        });
+        for (std::size_t wi = 0; wi < nw; ++wi)   // chunk order
+            for (uint64_t z = 0; z < NT; ++z) { bp[z] += tp[wi][z]; bm[z] += tm[wi][z]; }
     }
 }
 
@@ -829,7 +957,8 @@ static inline bool active3(const orc_problem* p, int l, int bk, int bi, int bj) 
 static double z_row3(const orc_problem* p, uint64_t y) {
     const int L = p->L, nz = p->g.nz;
     double zA = 0.0;
-    std::vector<std::vector<double>> tot(L + 1);
+    static thread_local std::vector<std::vector<double>> tot;
+    tot.resize(L + 1);
     for (int l = 1; l <= L; ++l) tot[l].assign(nz >> l, 0.0);
     const double cL = cpow3(L);
     phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {
@@ -849,37 +978,46 @@ static double z_row3(const orc_problem* p, uint64_t y) {
     return best;
 }
 
-// Psi lists (mirror mode): per (level l, in-plane block b) with ANY active z-block,
-// the rays crossing b (ascending) with fp32 psi_A, psi_H, psi_V, psi_D.
-static void build_psi3(orc_problem* p) {
-    const int L = p->L, nx = p->g.nx, ny = p->g.ny, nz = p->g.nz;
-    p->psi_ptr.assign(L + 1, {});
-    p->psi_ray.assign(L + 1, {});
-    p->psi_val.assign(L + 1, {});
-    std::vector<std::vector<uint8_t>> anyk(L + 1);
-    for (int l = 1; l <= L; ++l) {
-        const int hl = ny >> l, wl = nx >> l;
-        anyk[l].assign((std::size_t)hl * wl, 0);
-        for (int k = 0; k < (nz >> l); ++k)
-            for (int bi = 0; bi < hl; ++bi)
-                for (int bj = 0; bj < wl; ++bj)
-                    if (active3(p, l, k, bi, bj)) anyk[l][(std::size_t)bi * wl + bj] = 1;
-    }
-    std::vector<std::vector<std::vector<std::pair<uint32_t, std::array<float, 4>>>>> cols(L + 1);
-    for (int l = 1; l <= L; ++l) cols[l].resize((std::size_t)(ny >> l) * (nx >> l));
-    for (uint64_t y = 0; y < p->Ms; ++y)
-        phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {
-            const std::size_t b = (std::size_t)bi * (nx >> l) + bj;
-            if (!anyk[l][b]) return;
-            cols[l][b].push_back({(uint32_t)y, {(float)pA, (float)pH, (float)pV, (float)pD}});
+// Psi lists of level l over the in-plane blocks with want[b] != 0: rays
+// ascending, (psi_A, psi_H, psi_V, psi_D) fp32-rounded in mirror mode.
+static void build_psi_level(const orc_problem* p, int l, const std::vector<uint8_t>& want, PsiLevel& out) {
+    const int L = p->L, nx = p->g.nx;
+    const int wl = nx >> l;
+    const bool r32 = p->mirror;
+    struct E { uint32_t y; std::array<double, 4> v; };
+    bool sized = false;
+    auto store = [&](uint64_t i, const E& e) {
+        if (!sized) { out.ray.resize(i); out.val.resize(i); sized = true; return; }
+        out.ray[i] = e.y; out.val[i] = e.v;
+    };
+    bucket_rays<E>(p, want.size(), out.ptr, [&](std::size_t y, auto&& put) {
+        phi_walk(p, L, y, [&](int ll, int bi, int bj, double pA, double pH, double pV, double pD) {
+            if (ll != l) return;
+            const std::size_t b = (std::size_t)bi * wl + bj;
+            if (!want[b]) return;
+            if (r32) put(b, E{(uint32_t)y, {(double)(float)pA, (double)(float)pH, (double)(float)pV, (double)(float)pD}});
+            else put(b, E{(uint32_t)y, {pA, pH, pV, pD}});
         });
-    for (int l = 1; l <= L; ++l) {
-        const std::size_t nb = cols[l].size();
-        p->psi_ptr[l].assign(nb + 1, 0);
-        for (std::size_t b = 0; b < nb; ++b) p->psi_ptr[l][b + 1] = p->psi_ptr[l][b] + cols[l][b].size();
-        for (std::size_t b = 0; b < nb; ++b)
-            for (auto& e : cols[l][b]) { p->psi_ray[l].push_back(e.first); p->psi_val[l].push_back(e.second); }
-    }
+    }, store);
+}
+
+// in-plane blocks of level l with any active z-block (all of them at level L
+// when the approximations are split directly, i.e. at reference precision)
+static std::vector<uint8_t> psi_want(const orc_problem* p, int l, bool all) {
+    const int nx = p->g.nx, ny = p->g.ny, nz = p->g.nz;
+    const int hl = ny >> l, wl = nx >> l;
+    std::vector<uint8_t> w((std::size_t)hl * wl, all ? 1 : 0);
+    if (!all)
+        for (int k = 0; k < (nz >> l); ++k)
+            for (std::size_t b = 0; b < w.size(); ++b)
+                if (p->act[l][(std::size_t)k * w.size() + b]) w[b] = 1;
+    return w;
+}
+
+static void build_psi3(orc_problem* p) {
+    const int L = p->L;
+    p->psi.assign(L + 1, {});
+    for (int l = 1; l <= L; ++l) build_psi_level(p, l, psi_want(p, l, !p->mirror && l == L), p->psi[l]);
 }
 
 // b-(z) of every active 3D detail (mirror mode, from the Psi lists):
@@ -887,28 +1025,28 @@ static void build_psi3(orc_problem* p) {
 //   z-high subband p: sum_y psi_p < 0 ? psi_p c^l Qlo : (psi_p > 0 ? -psi_p c^l Qhi : 0)
 // with Qlo / Qhi the ray-wise sums of q over the lower / upper half of the
 // z-block's slices (ascending slice order).  Rays ascending within a list.
-static void split3_mirror(const orc_problem* p, const std::vector<double>& q, std::vector<double>& bm) {
+// qT: q in slab layout [y][s].  Blocks are independent (parallel over them).
+static void split3_mirror(const orc_problem* p, const std::vector<double>& qT, std::vector<double>& bm) {
     const int L = p->L, nx = p->g.nx, ny = p->g.ny, nz = p->g.nz;
-    const uint64_t M = p->Ms;
     bm.assign(p->Ns * nz, 0.0);
     for (int l = 1; l <= L; ++l) {
         const double cl = cpow3(l);
-        const int hw = 1 << (l - 1);
-        for (int bi = 0; bi < (ny >> l); ++bi)
-            for (int bj = 0; bj < (nx >> l); ++bj) {
-                const std::size_t b = (std::size_t)bi * (nx >> l) + bj;
+        const int hw = 1 << (l - 1), wl = nx >> l;
+        const PsiLevel& ps = p->psi[l];
+        parallel_for((std::size_t)(ny >> l) * wl, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+            for (std::size_t b = lo; b < hi; ++b) {
+                const int bi = (int)(b / wl), bj = (int)(b % wl);
                 for (int k = 0; k < (nz >> l); ++k) {
                     if (!active3(p, l, k, bi, bj)) continue;
                     double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-                    for (uint64_t e = p->psi_ptr[l][b]; e < p->psi_ptr[l][b + 1]; ++e) {
-                        const uint64_t y = p->psi_ray[l][e];
-                        const auto& ps = p->psi_val[l][e];
+                    for (uint64_t e = ps.ptr[b]; e < ps.ptr[b + 1]; ++e) {
+                        const double* qy = qT.data() + (uint64_t)ps.ray[e] * nz + (uint64_t)k * 2 * hw;
+                        const auto& v = ps.val[e];
                         double qlo = 0.0, qhi = 0.0;
-                        for (int s = 0; s < hw; ++s) qlo += q[(uint64_t)(k * 2 * hw + s) * M + y];
-                        for (int s = 0; s < hw; ++s) qhi += q[(uint64_t)(k * 2 * hw + hw + s) * M + y];
+                        for (int s = 0; s < hw; ++s) qlo += qy[s];
+                        for (int s = 0; s < hw; ++s) qhi += qy[hw + s];
                         const double qall = qlo + qhi;
-                        const double A = (double)ps[0] * cl, H = (double)ps[1] * cl, V = (double)ps[2] * cl,
-                                     D = (double)ps[3] * cl;
+                        const double A = v[0] * cl, H = v[1] * cl, V = v[2] * cl, D = v[3] * cl;
                         const double lowp[3] = {H, V, D}, highp[4] = {A, H, V, D};
                         for (int t = 0; t < 3; ++t)
                             if (lowp[t] < 0.0) acc[t] += lowp[t] * qall;
@@ -922,46 +1060,58 @@ static void split3_mirror(const orc_problem* p, const std::vector<double>& q, st
                     for (int t = 0; t < 7; ++t) bm[z[1 + t]] = acc[t];
                 }
             }
+        });
     }
 }
 
 // Direct signed split (reference precision, 3D): b+ / b- for every active z
 // (or every z with all_coeffs) from the exact phi(y_s|z) = psi c^l sigma_z(s).
-static void direct_split3(const orc_problem* p, const std::vector<double>& w, std::vector<double>& bp,
+// Block-driven over the f64 Psi lists: every z accumulates its (ray, slice)
+// terms in ascending (ray, slice) order, the order of a serial ray walk.
+// all_coeffs (init): the lists of every block are built one level at a time.
+static void direct_split3(const orc_problem* p, const std::vector<double>& qT, std::vector<double>& bp,
                           std::vector<double>& bm, bool all_coeffs) {
     const int L = p->L, nx = p->g.nx, ny = p->g.ny, nz = p->g.nz;
-    const uint64_t M = p->Ms, NT = p->Ns * nz;
-    int nt = resolve_threads(p->threads);
-    std::vector<std::vector<double>> tp(nt), tm(nt);
-    parallel_for(M, nt, [&](std::size_t lo, std::size_t hi, int bt) {
-        tp[bt].assign(NT, 0.0); tm[bt].assign(NT, 0.0);
-        auto& P = tp[bt]; auto& Mn = tm[bt];
-        auto add = [&](uint64_t z, double t, double phi) {
-            if (phi > 0.0) P[z] += t; else if (phi < 0.0) Mn[z] += t;
-        };
-        for (std::size_t y = lo; y < hi; ++y)
-            phi_walk(p, L, y, [&](int l, int bi, int bj, double pA, double pH, double pV, double pD) {
-                const double cl = cpow3(l), cL = cpow3(L);
-                const int hw = 1 << (l - 1);
-                for (int s = 0; s < nz; ++s) {
-                    const double qy = w[(uint64_t)s * M + y];
-                    const int k = s >> l;
-                    const double sg = ((s >> (l - 1)) & 1) ? -1.0 : 1.0;
-                    (void)hw;
+    const uint64_t NT = p->Ns * nz;
+    bp.assign(NT, 0.0); bm.assign(NT, 0.0);
+    const double cL = cpow3(L);
+    for (int l = 1; l <= L; ++l) {
+        PsiLevel tmp;
+        const PsiLevel* ps = &p->psi[l];
+        if (all_coeffs) { build_psi_level(p, l, psi_want(p, l, true), tmp); ps = &tmp; }
+        const double cl = cpow3(l);
+        const int wl = nx >> l, bz = 1 << l;
+        parallel_for((std::size_t)(ny >> l) * wl, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+            for (std::size_t b = lo; b < hi; ++b) {
+                const int bi = (int)(b / wl), bj = (int)(b % wl);
+                for (int k = 0; k < (nz >> l); ++k) {
+                    const bool act = all_coeffs || active3(p, l, k, bi, bj), doA = l == L;
+                    if (!act && !doA) continue;
+                    double P[8] = {0, 0, 0, 0, 0, 0, 0, 0}, Mn[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    auto add = [&](int t, double v, double phi) {
+                        if (phi > 0.0) P[t] += v; else if (phi < 0.0) Mn[t] += v;
+                    };
+                    for (uint64_t e = ps->ptr[b]; e < ps->ptr[b + 1]; ++e) {
+                        const double* qy = qT.data() + (uint64_t)ps->ray[e] * nz;
+                        const double pA = ps->val[e][0], pH = ps->val[e][1], pV = ps->val[e][2], pD = ps->val[e][3];
+                        for (int s = k * bz; s < (k + 1) * bz; ++s) {
+                            const double q = qy[s];
+                            const double sg = ((s >> (l - 1)) & 1) ? -1.0 : 1.0;
+                            if (doA) { const double ph = pA * cL; add(0, q * ph, ph); }
+                            if (!act) continue;
+                            const double ph[7] = {pH * cl, pV * cl, pD * cl, pA * cl * sg, pH * cl * sg,
+                                                  pV * cl * sg, pD * cl * sg};
+                            for (int t = 0; t < 7; ++t) add(1 + t, q * ph[t], ph[t]);
+                        }
+                    }
                     uint64_t z[8];
                     mallat3(nx, ny, nz, l, k, bi, bj, z);
-                    if (l == L) { const double ph = pA * cL; add(z[0], qy * ph, ph); }
-                    if (!all_coeffs && !active3(p, l, k, bi, bj)) continue;
-                    const double ph[7] = {pH * cl, pV * cl, pD * cl, pA * cl * sg, pH * cl * sg, pV * cl * sg,
-                                          pD * cl * sg};
-                    for (int t = 0; t < 7; ++t) add(z[1 + t], qy * ph[t], ph[t]);
+                    if (doA) { bp[z[0]] = P[0]; bm[z[0]] = Mn[0]; }
+                    if (act)
+                        for (int t = 1; t < 8; ++t) { bp[z[t]] = P[t]; bm[z[t]] = Mn[t]; }
                 }
-            });
-    });
-    bp.assign(NT, 0.0); bm.assign(NT, 0.0);
-    for (int b = 0; b < nt; ++b) {
-        if (tp[b].empty()) continue;
-        for (uint64_t z = 0; z < NT; ++z) { bp[z] += tp[b][z]; bm[z] += tm[b][z]; }
+            }
+        });
     }
 }
 
@@ -984,18 +1134,23 @@ extern "C" {
 
 const char* orc_last_error(void) { return g_err.c_str(); }
 
-int orc_create(const orc_geometry* gc, int mirror, int threads, orc_problem** out) {
+int orc_create_ex(const orc_geometry* gc, int mirror, int threads, int flags, orc_problem** out) {
     ORC_TRY({
         if (!out) throw contract_error("null out");
         auto* p = new orc_problem();
         try {
             p->g = make_geom(gc);
             p->mirror = mirror != 0;
+            p->slim = (flags & ORC_SLIM) != 0;
             p->threads = threads;
             build_matrix(p);
         } catch (...) { delete p; throw; }
         *out = p;
     })
+}
+
+int orc_create(const orc_geometry* gc, int mirror, int threads, orc_problem** out) {
+    return orc_create_ex(gc, mirror, threads, 0, out);
 }
 
 int orc_create_csr(uint64_t M, int nx, int ny, const uint64_t* rp, const uint32_t* ci, const double* val,
@@ -1047,12 +1202,14 @@ int orc_get_csr(const orc_problem* p, uint64_t* rp, uint32_t* ci, double* val) {
     ORC_TRY({
         if (rp) std::copy(p->rp.begin(), p->rp.end(), rp);
         if (ci) std::copy(p->ci.begin(), p->ci.end(), ci);
+        if (p->slim && (ci || val)) throw contract_error("slim problem: the exact CSR is not kept");
         if (val) std::copy(p->hexact.begin(), p->hexact.end(), val);
     })
 }
 
 int orc_get_csc(const orc_problem* p, uint64_t* cp, uint32_t* ri, double* val) {
     ORC_TRY({
+        if (p->slim) throw contract_error("slim problem: no CSC mirror");
         if (cp) std::copy(p->cp.begin(), p->cp.end(), cp);
         if (ri) std::copy(p->ri.begin(), p->ri.end(), ri);
         if (val) std::copy(p->cv.begin(), p->cv.end(), val);
@@ -1132,17 +1289,36 @@ int orc_simulate(const orc_problem* p, const double* mu, const double* I0, uint6
                  double* dout) {
     ORC_TRY({
         const uint64_t M = p->Ms, N = p->Ns;
-        parallel_for(M, p->threads, [&](std::size_t lo, std::size_t hi, int) {
-            for (int s = 0; s < p->nz; ++s)
+        if (!p->hexact.empty()) {
+            parallel_for(M, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+                for (int s = 0; s < p->nz; ++s)
+                    for (std::size_t y = lo; y < hi; ++y) {
+                        double acc = 0.0;  // exact f64 h, CSR order
+                        for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k)
+                            acc += p->hexact[k] * mu[(uint64_t)s * N + p->ci[k]];
+                        const uint64_t id = (uint64_t)s * M + y;
+                        double m = I0[id] * std::exp(-acc);
+                        dout[id] = noisy ? poisson(seed, id, m) : m;
+                    }
+            });
+        } else {  // slim: exact h re-traced (the same trace_ray entries, same CSR order)
+            parallel_for(M, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+                std::vector<std::pair<uint32_t, double>> row;
                 for (std::size_t y = lo; y < hi; ++y) {
-                    double acc = 0.0;  // exact f64 h, CSR order
-                    for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k)
-                        acc += p->hexact[k] * mu[(uint64_t)s * N + p->ci[k]];
-                    const uint64_t id = (uint64_t)s * M + y;
-                    double m = I0[id] * std::exp(-acc);
-                    dout[id] = noisy ? poisson(seed, id, m) : m;
+                    row.clear();
+                    trace(p->g, p->rays[y], [&](int ix, int iy, double len) {
+                        row.push_back({(uint32_t)iy * (uint32_t)p->g.nx + (uint32_t)ix, len});
+                    });
+                    for (int s = 0; s < p->nz; ++s) {
+                        double acc = 0.0;
+                        for (const auto& e : row) acc += e.second * mu[(uint64_t)s * N + e.first];
+                        const uint64_t id = (uint64_t)s * M + y;
+                        double m = I0[id] * std::exp(-acc);
+                        dout[id] = noisy ? poisson(seed, id, m) : m;
+                    }
                 }
-        });
+            });
+        }
     })
 }
 
@@ -1183,7 +1359,7 @@ int orc_am_init(orc_problem* p, const double* d, const double* I0, const double*
         double z0 = 0.0;                                  // Z0 = max_y sum_x h
         for (uint64_t y = 0; y < p->Ms; ++y) {
             double s = 0.0;
-            for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) s += p->hv[k];
+            for (uint64_t k = p->rp[y]; k < p->rp[y + 1]; ++k) s += p->hvk(k);
             z0 = std::max(z0, s);
         }
         if (!(z0 > 0.0)) throw numeric_error("am: Z0 must be positive");
@@ -1262,8 +1438,14 @@ int orc_wam_init(orc_problem* p, const double* d, const double* I0, int L, const
             else { dwt2(p->g.nx, p->g.ny, p->nz, L, g.data(), p->bdata.data()); build_nphi(p); }
         } else {
             std::vector<double> bp, bm;
-            if (p->haar3) direct_split3(p, p->d, bp, bm, true);
-            else direct_split(p, p->d, bp, bm, true);
+            if (p->haar3) {
+                std::vector<double> dT;
+                to_slab(p->d.data(), p->Ms, p->nz, dT, p->threads);
+                direct_split3(p, dT, bp, bm, true);
+                build_psi3(p);
+            } else {
+                direct_split(p, p->d, bp, bm, true);
+            }
             p->bdata.resize(NT);
             for (uint64_t z = 0; z < NT; ++z) p->bdata[z] = bp[z] + bm[z];
         }
@@ -1289,26 +1471,32 @@ int orc_wam_iterate(orc_problem* p, int n, orc_record* recs) {
                 back(p, p->q.data(), g.data());
                 if (p->haar3) {
                     dwt3(nx, ny, nz, L, g.data(), S.data());
-                    split3_mirror(p, p->q, bm);
+                    std::vector<double> qT;
+                    to_slab(p->q.data(), p->Ms, nz, qT, p->threads);
+                    split3_mirror(p, qT, bm);
                 } else {
                     dwt2(nx, ny, p->nz, L, g.data(), S.data());
                     bm.assign(NT, 0.0);
                     // b-(z): exact fixed-point sum (2^-20 units) of q*phi over the
                     // Phi^- column -- order-independent, mirrored bit-for-bit by
                     // the GPU split whatever order its columns hold
-                    for (int s = 0; s < p->nz; ++s)
-                        for (uint64_t z = 0; z < N; ++z) {
-                            long long acc = 0;
-                            for (uint64_t k = p->nphi_ptr[z]; k < p->nphi_ptr[z + 1]; ++k)
-                                acc += std::llrint(p->q[(uint64_t)s * p->Ms + p->nphi_row[k]] * p->nphi_val[k] *
-                                                   1048576.0);
-                            bm[(uint64_t)s * N + z] = (double)acc * (1.0 / 1048576.0);
-                        }
+                    parallel_for(N, p->threads, [&](std::size_t lo, std::size_t hi, int) {
+                        for (int s = 0; s < p->nz; ++s)
+                            for (uint64_t z = lo; z < hi; ++z) {
+                                long long acc = 0;
+                                for (uint64_t k = p->nphi_ptr[z]; k < p->nphi_ptr[z + 1]; ++k)
+                                    acc += std::llrint(p->q[(uint64_t)s * p->Ms + p->nphi_row[k]] * p->nphi_val[k] *
+                                                       1048576.0);
+                                bm[(uint64_t)s * N + z] = (double)acc * (1.0 / 1048576.0);
+                            }
+                    });
                 }
                 bp.resize(NT);
                 for (uint64_t z = 0; z < NT; ++z) bp[z] = S[z] - bm[z];
             } else if (p->haar3) {
-                direct_split3(p, p->q, bp, bm, false);
+                std::vector<double> qT;
+                to_slab(p->q.data(), p->Ms, nz, qT, p->threads);
+                direct_split3(p, qT, bp, bm, false);
             } else {
                 direct_split(p, p->q, bp, bm, false);
             }
@@ -1403,7 +1591,8 @@ int orc_wam_expand(orc_problem* p, double factor, int64_t* newly) {
             p->act = na;
             if (cnt > 0) {
                 compute_z0(p);
-                if (p->mirror) { if (p->haar3) build_psi3(p); else build_nphi(p); }
+                if (p->haar3) build_psi3(p);
+                else if (p->mirror) build_nphi(p);
             }
         }
         if (newly) *newly = cnt;

@@ -57,6 +57,12 @@ const char* orc_last_error(void);
 /* mirror = 0: reference-faithful f64 storage (image.hpp:54, system_matrix.hpp:80)
  * mirror = 1: fp32 storage + fp64 accumulation, mirroring the GPU (pin P7) */
 int orc_create(const orc_geometry* g, int mirror, int threads, orc_problem** out);
+/* flags: ORC_SLIM = CSR only (no exact-h copy, no CSC; fp32 h in mirror mode):
+ * the memory mode for cfg4 (1.87e9 entries per slice).  Results are
+ * bit-identical to the full problem's (back projection by an ascending-ray
+ * CSR scatter, the CSC's order); get_csr values / get_csc are unavailable. */
+#define ORC_SLIM 1
+int orc_create_ex(const orc_geometry* g, int mirror, int threads, int flags, orc_problem** out);
 /* explicit-H problem (SPEC.md:70, 79, 307 examples): CSR over an nx*ny grid */
 int orc_create_csr(uint64_t M, int nx, int ny, const uint64_t* row_ptr, const uint32_t* col,
                    const double* val, int mirror, int threads, orc_problem** out);
