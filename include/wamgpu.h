@@ -145,7 +145,23 @@ int wamgpu_selftest_fused_back(wamgpu_ctx* const* ctxs, int R, const double* con
 int wamgpu_set_geometry(wamgpu_ctx* ctx, const wamgpu_geometry* g);
 int wamgpu_set_matrix_csr(wamgpu_ctx* ctx, uint64_t rows, uint64_t cols, uint64_t nnz,
                           const uint64_t* row_ptr, const uint32_t* col_idx, const double* values);
-/* geometry of the image grid for set_matrix_csr users (nx*ny == cols) */
+/* WAMH system-matrix cache: replaces wamrec::load_system_matrix /
+ * save_system_matrix (system_matrix.hpp:87-158).  load reads version 1 (the
+ * reference's layout: "WAMH", u32 1, u64 M, N, nnz, row_ptr u64[M+1], col_idx
+ * u32[nnz], values f64[nnz]; values converted to fp32 on the way in) or
+ * version 2 (this library's device layout: v1 header with version 2, u64 flags
+ * (bit 0: CSC present), u32 nx, u32 ny (0 = unknown), row_ptr u64[M+1],
+ * {col u32, h f32}[nnz], then with bit 0 col_ptr u64[N+1], {row u32, h f32}[nnz]),
+ * streaming only this rank's rows; like set_matrix_csr it must follow
+ * set_comm / set_partition / set_grid.  save writes the whole matrix (not from
+ * a view shard) as version 1 (f64 values of the fp32 device values) or 2
+ * (with_csc: also the CSC mirror).  IoError (4) on open/short read/write
+ * failures, bad magic or version, or a size inconsistent with the header. */
+int wamgpu_load_matrix_wamh(wamgpu_ctx* ctx, const char* path);
+int wamgpu_save_matrix_wamh(wamgpu_ctx* ctx, const char* path, int version, int with_csc);
+/* geometry of the image grid for set_matrix_csr users (nx*ny == cols); must
+ * precede the matrix (ContractError afterwards: the partition, slab layouts and
+ * matrix-derived caches follow the grid) */
 int wamgpu_set_grid(wamgpu_ctx* ctx, int nx, int ny, int nz);
 int wamgpu_matrix_info(const wamgpu_ctx* ctx, uint64_t* rows, uint64_t* cols, uint64_t* nnz_local,
                        uint64_t* row_begin, uint64_t* row_end);

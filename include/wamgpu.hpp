@@ -17,14 +17,33 @@
 
 #include "wamgpu.h"
 
+// With the reference headers on the include path the ABI status codes are
+// re-thrown AS the reference's own classes (wamgpu::ConfigError IS
+// wamrec::ConfigError), so a caller's `catch (const wamrec::ConfigError&)`
+// keeps working after the switch; without them, look-alike classes stand in.
+#if defined(__has_include) && !defined(WAMGPU_NO_WAMREC)
+#if __has_include(<wamrec/errors.hpp>)
+#include <wamrec/errors.hpp>
+#define WAMGPU_HAVE_WAMREC 1
+#endif
+#endif
+
 namespace wamgpu {
 
+#ifdef WAMGPU_HAVE_WAMREC
+using Error = wamrec::Error;                  // errors.hpp:9-13
+using ConfigError = wamrec::ConfigError;      // errors.hpp:15-19
+using ContractError = wamrec::ContractError;  // errors.hpp:21-25
+using NumericError = wamrec::NumericError;    // errors.hpp:27-31
+using IoError = wamrec::IoError;              // errors.hpp:33-37
+#else
 struct Error : std::runtime_error { using std::runtime_error::runtime_error; };
 struct ConfigError : Error { using Error::Error; };
 struct ContractError : Error { using Error::Error; };
 struct NumericError : Error { using Error::Error; };
 struct IoError : Error { using Error::Error; };
-struct CudaError : Error { using Error::Error; };
+#endif
+struct CudaError : Error { using Error::Error; };   // no reference equivalent
 
 inline void check(int rc, const wamgpu_ctx* c) {
     if (rc == WAMGPU_OK) return;
@@ -89,6 +108,15 @@ class Context {
         if (nx > 0) check(wamgpu_set_grid(c_, nx, ny, 1), c_);
         check(wamgpu_set_matrix_csr(c_, H.rows(), H.cols(), H.nnz(), H.row_ptr().data(), H.col_idx().data(),
                                     H.values().data()), c_);
+    }
+
+    /// load_system_matrix(path) (system_matrix.hpp:136-158) straight onto the
+    /// device: WAMH v1 (the reference's cache) or v2 (fp32 device layout).
+    void load_system_matrix(const std::string& path) { check(wamgpu_load_matrix_wamh(c_, path.c_str()), c_); }
+    /// save_system_matrix(m, path) (system_matrix.hpp:117-134); version 2 = fp32
+    /// device layout (with_csc: plus the CSC mirror).
+    void save_system_matrix(const std::string& path, int version = 1, bool with_csc = false) {
+        check(wamgpu_save_matrix_wamh(c_, path.c_str(), version, with_csc ? 1 : 0), c_);
     }
 
     uint64_t rows() const { uint64_t r = 0; check(wamgpu_matrix_info(c_, &r, nullptr, nullptr, nullptr, nullptr), c_); return r; }

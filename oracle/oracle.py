@@ -384,6 +384,18 @@ class RefMatrix:
         _chk(R.ref_build_from_rays(nx, ny, C.c_double(voxel), C.c_uint64(rays.shape[0]), P(rays), C.byref(h)), R)
         return cls(h)
 
+    def save(self, path):
+        """wamrec::save_system_matrix (system_matrix.hpp:117-134)."""
+        _chk(reflib().ref_save(self.h, os.fsencode(path)), reflib())
+
+    @classmethod
+    def load(cls, path):
+        """wamrec::load_system_matrix (system_matrix.hpp:136-158)."""
+        R = reflib()
+        h = C.c_void_p()
+        _chk(R.ref_load(os.fsencode(path), C.byref(h)), R)
+        return cls(h)
+
     def csr(self):
         rp = np.empty(self.M + 1, np.uint64)
         ci = np.empty(self.nnz, np.uint32)

@@ -61,6 +61,7 @@ EXPORTED = [
     "wamgpu_set_kernel_timing", "wamgpu_rasterize", "wamgpu_simulate", "wamgpu_host_rays", "wamgpu_set_haar_dim",
     "wamgpu_p2p_export", "wamgpu_p2p_import", "wamgpu_selftest_fused_allreduce", "wamgpu_selftest_fused_back",
     "wamgpu_set_comm_local", "wamgpu_set_partition", "wamgpu_get_partition", "wamgpu_wam_expand_with", "wamgpu_simulate_device",
+    "wamgpu_load_matrix_wamh", "wamgpu_save_matrix_wamh",
 ]
 P2P_BLOB = 256   # WAMGPU_P2P_BLOB
 
@@ -280,6 +281,16 @@ class Context:
         _chk(load().wamgpu_set_matrix_csr(self.h, C.c_uint64(rp.size - 1), C.c_uint64(cols), C.c_uint64(v.size),
                                           _p(rp, C.c_uint64), _p(ci, C.c_uint32), _p(v)), self.h)
         self._info()
+
+    def load_matrix_wamh(self, path):
+        """load_system_matrix (system_matrix.hpp:136-158): WAMH v1 (reference) or v2."""
+        _chk(load().wamgpu_load_matrix_wamh(self.h, os.fsencode(path)), self.h)
+        self._info()
+
+    def save_matrix_wamh(self, path, version=2, with_csc=False):
+        """save_system_matrix (system_matrix.hpp:117-134): v1 = reference layout,
+        v2 = fp32 device layout (optionally with the CSC mirror)."""
+        _chk(load().wamgpu_save_matrix_wamh(self.h, os.fsencode(path), int(version), int(bool(with_csc))), self.h)
 
     def matrix_csr(self):
         rp = np.empty(self.row1 - self.row0 + 1, np.uint64)

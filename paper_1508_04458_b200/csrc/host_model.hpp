@@ -17,6 +17,7 @@ struct Error : std::runtime_error {
 struct ConfigError : Error { explicit ConfigError(const std::string& w) : Error(WAMGPU_ERR_CONFIG, w) {} };
 struct ContractError : Error { explicit ContractError(const std::string& w) : Error(WAMGPU_ERR_CONTRACT, w) {} };
 struct NumericError : Error { explicit NumericError(const std::string& w) : Error(WAMGPU_ERR_NUMERIC, w) {} };
+struct IoError : Error { explicit IoError(const std::string& w) : Error(WAMGPU_ERR_IO, w) {} };
 struct CudaError : Error { explicit CudaError(const std::string& w) : Error(WAMGPU_ERR_CUDA, w) {} };
 
 struct RayD { double ox, oy, dx, dy, tmin, tmax; };  // detail::Ray, projector.hpp:16-20

@@ -18,6 +18,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <condition_variable>
@@ -524,14 +525,16 @@ static void check_flag(Ctx* c, const char* where) {
 }
 
 // ------------------------------------------------------------- system model
-static void finish_matrix(Ctx* c) {
+static void finish_matrix(Ctx* c, bool have_csc = false) {
     c->zA_L = -1;
     c->phiA_ok = false;
     c->phiA_L = -1;
     c->phiA_rp.release(); c->phiA_cp.release(); c->phiA_col.release(); c->phiA_row.release();
     c->phiA_val.release(); c->phiA_valC.release(); c->phiA_part.release();
     // CSC mirror (system_matrix.hpp:61-75): stable radix sort of CSR entries by
-    // column keeps rows ascending within every column.
+    // column keeps rows ascending within every column (unless a WAMH v2 cache
+    // supplied it: cp and C are then already on the device)
+    if (!have_csc) {
     DBuf<unsigned> kin, kout;
     DBuf<uint2> vin, vout;
     kin.alloc(std::max<uint64_t>(c->nnz, 1));
@@ -549,6 +552,7 @@ static void finish_matrix(Ctx* c) {
     check_launch(c, "k_bounds");
     c->C.swap(vout);
     kout.release();
+    }
     {   // tiled 2D image layout for the forward gathers: opt-in (WAMGPU_MU_TILED=1).
         // Measured at cfg2 (round 1): 0.773 ms tiled vs 0.7455 ms row-major per
         // forward -- the address arithmetic costs more than the L1 hits it buys.
@@ -716,6 +720,186 @@ static void set_matrix_csr(Ctx* c, uint64_t rows, uint64_t cols, uint64_t nnz, c
     if (c->nnz) CK(cudaMemcpyAsync(c->A.p, ent.data(), c->nnz * 8, cudaMemcpyHostToDevice, c->st));
     finish_matrix(c);
     build_tile_order(c);
+}
+
+// ------------------------------------------------------------- WAMH cache
+// wamrec::save/load_system_matrix (system_matrix.hpp:87-158).  v1 is the
+// reference's layout byte for byte: "WAMH", u32 version = 1, u64 M, N, nnz,
+// row_ptr u64[M+1], col_idx u32[nnz], values f64[nnz] (32-byte header, no
+// padding).  v2 (this library) stores the device layout so a cache uploads
+// without conversion: the v1 header with version = 2, then u64 flags (bit 0:
+// CSC mirror present), u32 nx, u32 ny (0 = unknown), row_ptr u64[M+1],
+// entries {col u32, h f32}[nnz], and with bit 0 col_ptr u64[N+1] and
+// {row u32, h f32}[nnz] (rows ascending per column).  Values on the device
+// are fp32 (pin P7), so a v1 file written here carries fp32-representable
+// f64 values.  Errors map to IoError like the reference (errors.hpp:32-35).
+static constexpr uint64_t WAMH_CHUNK = 1ull << 24;   // entries per streamed chunk
+
+struct File {
+    FILE* f = nullptr;
+    std::string path;
+    File(const char* p, const char* mode) : path(p ? p : "") {
+        if (!p) throw ContractError("WAMH: null path");
+        f = std::fopen(p, mode);
+    }
+    ~File() { if (f) std::fclose(f); }
+    void read(void* dst, size_t bytes) {
+        if (bytes && std::fread(dst, 1, bytes, f) != bytes) throw IoError("unexpected end of file: " + path);
+    }
+    void write(const void* src, size_t bytes) {
+        if (bytes && std::fwrite(src, 1, bytes, f) != bytes) throw IoError("write failed: " + path);
+    }
+    void seek(uint64_t off) {
+        if (fseeko(f, (off_t)off, SEEK_SET) != 0) throw IoError("seek failed: " + path);
+    }
+    uint64_t size() {
+        const off_t cur = ftello(f);
+        fseeko(f, 0, SEEK_END);
+        const off_t n = ftello(f);
+        fseeko(f, cur, SEEK_SET);
+        return (uint64_t)n;
+    }
+};
+
+static void load_matrix_wamh(Ctx* c, const char* path) {
+    File F(path, "rb");
+    if (!F.f) throw IoError("cannot open for reading: " + F.path);
+    char magic[4] = {};
+    uint32_t version = 0;
+    uint64_t rows = 0, cols = 0, nnz = 0, flags = 0;
+    uint32_t gx = 0, gy = 0;
+    F.read(magic, 4);
+    if (std::memcmp(magic, "WAMH", 4) != 0) throw IoError("not a system-matrix cache file: " + F.path);
+    F.read(&version, 4);
+    if (version != 1 && version != 2) throw IoError("unsupported cache version in " + F.path);
+    F.read(&rows, 8); F.read(&cols, 8); F.read(&nnz, 8);
+    uint64_t hdr = 32;
+    if (version == 2) { F.read(&flags, 8); F.read(&gx, 4); F.read(&gy, 4); hdr = 48; }
+    const bool csc = version == 2 && (flags & 1);
+    const uint64_t ebytes = version == 1 ? 12 : 8;
+    const uint64_t want = hdr + 8 * (rows + 1) + ebytes * nnz + (csc ? 8 * (cols + 1) + 8 * nnz : 0);
+    if (rows > (1ull << 32) || cols > (1ull << 32) || nnz > (1ull << 40) || F.size() != want)
+        throw IoError("truncated or inconsistent cache file: " + F.path);
+    if (gx && gy) {
+        if ((uint64_t)gx * gy != cols) throw IoError("cache grid nx*ny != cols: " + F.path);
+        if (c->have_grid && ((uint64_t)c->nx * c->ny != cols)) throw ContractError("WAMH: cols != nx*ny of the grid");
+        if (!c->have_grid) { c->nx = (int)gx; c->ny = (int)gy; c->nz = 1; c->have_grid = true; }
+    }
+    std::vector<uint64_t> rp(rows + 1);
+    F.read(rp.data(), 8 * (rows + 1));
+    if (rp[0] != 0 || rp[rows] != nnz) throw ContractError("SystemMatrix: inconsistent CSR arrays");
+    for (uint64_t y = 0; y < rows; ++y)
+        if (rp[y + 1] < rp[y]) throw ContractError("SystemMatrix: row_ptr not monotone");
+    if (c->have_grid && (uint64_t)c->nx * c->ny != cols) throw ContractError("SystemMatrix: cols != nx*ny of the grid");
+    c->M = rows;
+    c->N = cols;
+    if (!c->have_grid) { c->nx = (int)cols; c->ny = 1; c->nz = 1; }
+    partition(c, (int)rows, 1);
+    const uint64_t k0 = rp[c->row0], k1 = rp[c->row1];
+    c->nnz = k1 - k0;
+    std::vector<unsigned long long> lrp(c->Ml + 1);
+    for (uint64_t y = 0; y <= c->Ml; ++y) lrp[y] = rp[c->row0 + y] - k0;
+    c->rp.alloc(c->Ml + 1);
+    c->A.alloc_padded(std::max<uint64_t>(c->nnz, 1));
+    CK(cudaMemcpyAsync(c->rp.p, lrp.data(), (c->Ml + 1) * 8, cudaMemcpyHostToDevice, c->st));
+    std::vector<uint2> ent(std::min<uint64_t>(std::max<uint64_t>(c->nnz, 1), WAMH_CHUNK));
+    std::vector<uint32_t> ci;
+    std::vector<double> val;
+    const uint64_t col_off = hdr + 8 * (rows + 1);
+    for (uint64_t o = 0; o < c->nnz; o += WAMH_CHUNK) {
+        const uint64_t n = std::min(WAMH_CHUNK, c->nnz - o);
+        if (version == 1) {   // SoA f64 -> device {col, fp32 h}
+            ci.resize(n); val.resize(n);
+            F.seek(col_off + 4 * (k0 + o));
+            F.read(ci.data(), 4 * n);
+            F.seek(col_off + 4 * nnz + 8 * (k0 + o));
+            F.read(val.data(), 8 * n);
+            for (uint64_t k = 0; k < n; ++k) {
+                const float h = (float)val[k];
+                ent[k].x = ci[k];
+                std::memcpy(&ent[k].y, &h, 4);
+            }
+        } else {
+            F.seek(col_off + 8 * (k0 + o));
+            F.read(ent.data(), 8 * n);
+        }
+        for (uint64_t k = 0; k < n; ++k)
+            if (ent[k].x >= cols) throw ContractError("SystemMatrix: column index out of range");
+        CK(cudaMemcpy(c->A.p + o, ent.data(), 8 * n, cudaMemcpyHostToDevice));
+    }
+    // the stored CSC mirror serves only a context holding every row
+    const bool use_csc = csc && c->row0 == 0 && c->row1 == rows;
+    if (use_csc) {
+        const uint64_t csc_off = col_off + 8 * nnz;
+        std::vector<unsigned long long> cp(cols + 1);
+        F.seek(csc_off);
+        F.read(cp.data(), 8 * (cols + 1));
+        if (cp[0] != 0 || cp[cols] != nnz) throw IoError("inconsistent CSC mirror in " + F.path);
+        c->cp.alloc(cols + 1);
+        CK(cudaMemcpyAsync(c->cp.p, cp.data(), 8 * (cols + 1), cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        c->C.alloc_padded(std::max<uint64_t>(nnz, 1));
+        for (uint64_t o = 0; o < nnz; o += WAMH_CHUNK) {
+            const uint64_t n = std::min(WAMH_CHUNK, nnz - o);
+            F.read(ent.data(), 8 * n);
+            for (uint64_t k = 0; k < n; ++k)
+                if (ent[k].x >= rows) throw ContractError("SystemMatrix: CSC row index out of range");
+            CK(cudaMemcpy(c->C.p + o, ent.data(), 8 * n, cudaMemcpyHostToDevice));
+        }
+    }
+    finish_matrix(c, use_csc);
+    build_tile_order(c);
+}
+
+static void save_matrix_wamh(Ctx* c, const char* path, int version, int with_csc) {
+    if (!c->have_matrix) throw ContractError("wamgpu: no system matrix set");
+    if (version != 1 && version != 2) throw ConfigError("WAMH: version must be 1 or 2");
+    if (c->row0 != 0 || c->row1 != c->M)
+        throw ContractError("WAMH: this context holds a view shard of the matrix, not all of it");
+    File F(path, "wb");
+    if (!F.f) throw IoError("cannot open for writing: " + F.path);
+    const uint32_t ver = (uint32_t)version;
+    const uint64_t M = c->M, N = c->N, nnz = c->nnz;
+    F.write("WAMH", 4); F.write(&ver, 4); F.write(&M, 8); F.write(&N, 8); F.write(&nnz, 8);
+    const bool csc = version == 2 && with_csc;
+    if (version == 2) {
+        const uint64_t flags = csc ? 1 : 0;
+        const uint32_t gx = c->have_grid && c->nz == 1 ? (uint32_t)c->nx : 0, gy = gx ? (uint32_t)c->ny : 0;
+        F.write(&flags, 8); F.write(&gx, 4); F.write(&gy, 4);
+    }
+    CK(cudaStreamSynchronize(c->st));
+    std::vector<unsigned long long> rp(M + 1);
+    CK(cudaMemcpy(rp.data(), c->rp.p, 8 * (M + 1), cudaMemcpyDeviceToHost));
+    F.write(rp.data(), 8 * (M + 1));
+    std::vector<uint2> ent(std::min<uint64_t>(std::max<uint64_t>(nnz, 1), WAMH_CHUNK));
+    auto stream = [&](const uint2* dev, uint64_t n_all, auto&& emit) {
+        for (uint64_t o = 0; o < n_all; o += WAMH_CHUNK) {
+            const uint64_t n = std::min(WAMH_CHUNK, n_all - o);
+            CK(cudaMemcpy(ent.data(), dev + o, 8 * n, cudaMemcpyDeviceToHost));
+            emit(n);
+        }
+    };
+    if (version == 1) {
+        std::vector<uint32_t> ci(ent.size());
+        std::vector<double> val(ent.size());
+        stream(c->A.p, nnz, [&](uint64_t n) {
+            for (uint64_t k = 0; k < n; ++k) ci[k] = ent[k].x;
+            F.write(ci.data(), 4 * n);
+        });
+        stream(c->A.p, nnz, [&](uint64_t n) {
+            for (uint64_t k = 0; k < n; ++k) { float h; std::memcpy(&h, &ent[k].y, 4); val[k] = h; }
+            F.write(val.data(), 8 * n);
+        });
+    } else {
+        stream(c->A.p, nnz, [&](uint64_t n) { F.write(ent.data(), 8 * n); });
+        if (csc) {
+            std::vector<unsigned long long> cp(N + 1);
+            CK(cudaMemcpy(cp.data(), c->cp.p, 8 * (N + 1), cudaMemcpyDeviceToHost));
+            F.write(cp.data(), 8 * (N + 1));
+            stream(c->C.p, nnz, [&](uint64_t n) { F.write(ent.data(), 8 * n); });
+        }
+    }
+    if (std::fflush(F.f) != 0) throw IoError("write failed: " + F.path);
 }
 
 // ------------------------------------------------------------- pipeline steps
@@ -1641,9 +1825,13 @@ static void z0_from_zfix(Ctx* c) {
 // tree act_host from the tree act_phi they cover.  Columns of blocks that were
 // already active never change: one walk over the NEW blocks (k_walk_lv) emits
 // their negative phi as unsorted triples and adds their |phi| terms to the
-// fixed-point Z; the batch is radix-sorted by z straight into E after the
-// existing entries, and k_cols_set records each new column's [lo, hi).  Within
-// a column the ray order is arbitrary: the split sums in exact fixed point.
+// fixed-point Z.  The batch is placed by COUNTING straight into E after the
+// existing entries: the walk takes the key histogram as it drains its lane
+// rings (sentinel entries are not counted), an exclusive scan gives the column
+// bounds, and k_key_place moves each entry to its column's cursor
+// (warp-aggregated).  WAMGPU_PHI_SORT=1 keeps the older path, a CUB radix sort
+// by key.  k_cols_set records each new column's [lo, hi).  Within a column the
+// ray order is arbitrary: the split sums in exact fixed point.
 
 static void phi_append(Ctx* c) {
     // active detail list from the host tree (level by level, the H, V, D of a
@@ -1750,7 +1938,8 @@ static void phi_append(Ctx* c) {
     }
     k_cols_set<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->ptmp.p, off, c->cols.p);
     check_launch(c, "k_cols_set");
-    // batch tails carry the sentinel key N (sorted last): ptmp[N] counts the rest
+    // ptmp[N] = the batch's valid entries: the scan total on the counting path
+    // (sentinels never counted), the sentinel key N's bound on the sort path
     unsigned long long valid = 0;
     CK(cudaMemcpyAsync(&valid, c->ptmp.p + c->N, 8, cudaMemcpyDeviceToHost, c->st));
     c->zfix.swap(c->zfix2);
@@ -2412,7 +2601,10 @@ static Ctx* create(int device) {
 
 static void destroy(Ctx* c) {
     cudaSetDevice(c->device);
+    // both streams first: the side stream's split may still read A/C/E if an
+    // error escaped between its launch and the join in wam_step
     cudaStreamSynchronize(c->st);
+    cudaStreamSynchronize(c->st2);
     for (auto& v : c->tev)
         for (auto& p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto e : c->ev_iter) cudaEventDestroy(e);
@@ -2789,7 +2981,9 @@ int wamgpu_set_grid(wamgpu_ctx* ctx, int nx, int ny, int nz) {
     API_TRY(ctx, {
         NEED(ctx);
         if (nx < 1 || ny < 1 || nz < 1) throw ConfigError("set_grid: invalid grid");
-        if (ctx->have_matrix && (uint64_t)nx * ny != ctx->N) throw ContractError("set_grid: nx*ny != matrix cols");
+        // the grid shapes everything derived from the matrix (partition, slab
+        // stride, tile order, the zA / Phi_A caches): it must come first
+        if (ctx->have_matrix) throw ContractError("set_grid: must precede the system matrix");
         ctx->nx = nx; ctx->ny = ny; ctx->nz = nz; ctx->have_grid = true;
     })
 }
@@ -2797,6 +2991,14 @@ int wamgpu_set_grid(wamgpu_ctx* ctx, int nx, int ny, int nz) {
 int wamgpu_set_matrix_csr(wamgpu_ctx* ctx, uint64_t rows, uint64_t cols, uint64_t nnz, const uint64_t* rp,
                           const uint32_t* ci, const double* val) {
     API_TRY(ctx, { NEED(ctx); set_matrix_csr(ctx, rows, cols, nnz, rp, ci, val); })
+}
+
+int wamgpu_load_matrix_wamh(wamgpu_ctx* ctx, const char* path) {
+    API_TRY(ctx, { NEED(ctx); load_matrix_wamh(ctx, path); })
+}
+
+int wamgpu_save_matrix_wamh(wamgpu_ctx* ctx, const char* path, int version, int with_csc) {
+    API_TRY(ctx, { NEED(ctx); save_matrix_wamh(ctx, path, version, with_csc); })
 }
 
 int wamgpu_matrix_info(const wamgpu_ctx* ctx, uint64_t* rows, uint64_t* cols, uint64_t* nnz, uint64_t* r0,

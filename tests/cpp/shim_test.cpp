@@ -60,12 +60,32 @@ int main() {
     for (std::size_t i = 1; i < ra.size(); ++i) mono = mono && ra[i].objective <= ra[i - 1].objective * (1 + 1e-6);
     for (std::size_t i = 1; i < rw.size(); ++i) mono = mono && rw[i].objective <= rw[i - 1].objective * (1 + 1e-6);
     bool threw = false;
-    try { ctx.init_state(9); } catch (const wamgpu::ConfigError&) { threw = true; }
+    try { ctx.init_state(9); } catch (const wamrec::ConfigError&) { threw = true; }   // the reference's class
+    // WAMH: the reference's own cache file (save_system_matrix) loads onto the
+    // device bit-identical to set_matrix; the device's v1 file loads back
+    // through the reference's load_system_matrix as the fp32-rounded matrix
+    const std::string ref_file = "/tmp/wamgpu_shim_ref.wamh", dev_file = "/tmp/wamgpu_shim_dev.wamh";
+    wamrec::save_system_matrix(H, ref_file);
+    wamgpu::Context ctx3(0);
+    ctx3.load_system_matrix(ref_file);
+    std::vector<double> l3 = ctx3.forward_project(mu);
+    double diff3 = 0.0;
+    for (std::size_t y = 0; y < l.size(); ++y) diff3 = std::max(diff3, std::fabs(l[y] - l3[y]));
+    ctx3.save_system_matrix(dev_file, 1);
+    wamrec::SystemMatrix H2 = wamrec::load_system_matrix(dev_file);
+    bool wamh = diff3 == 0.0 && H2.rows() == H.rows() && H2.cols() == H.cols() && H2.row_ptr() == H.row_ptr() &&
+                H2.col_idx() == H.col_idx();
+    for (std::uint64_t k = 0; wamh && k < H.nnz(); ++k) wamh = H2.values()[k] == (double)(float)H.values()[k];
+    bool io_threw = false;
+    try { ctx3.load_system_matrix("/nonexistent/x.wamh"); } catch (const wamrec::IoError&) { io_threw = true; }
+    std::remove(ref_file.c_str());
+    std::remove(dev_file.c_str());
     std::printf("forward rel %.3e, set_geometry max diff %.3e, AM obj %.6e -> %.6e, WAM obj %.6e -> %.6e, "
-                "active %lld, monotone %d, config error mapped %d\n",
+                "active %lld, monotone %d, config error mapped %d, WAMH %d, io error mapped %d\n",
                 rel, diff2, ra.front().objective, ra.back().objective, rw.front().objective, rw.back().objective,
-                (long long)rw.back().active_set, (int)mono, (int)threw);
-    const bool ok = rel < 1e-12 && diff2 == 0.0 && mono && threw && rw.back().objective < rw.front().objective;
+                (long long)rw.back().active_set, (int)mono, (int)threw, (int)wamh, (int)io_threw);
+    const bool ok = rel < 1e-12 && diff2 == 0.0 && mono && threw && rw.back().objective < rw.front().objective &&
+                    wamh && io_threw;
     std::printf(ok ? "SHIM OK\n" : "SHIM FAIL\n");
     return ok ? 0 : 1;
 }
