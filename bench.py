@@ -46,11 +46,12 @@ def _args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="wamgpu", choices=["wamgpu", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg4")
     ap.add_argument("--algo", default=None, choices=[None, "wam", "am"])
     ap.add_argument("--iters", type=int, default=None, help="override J")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--cpu-iters", type=int, default=3, help="iterations in the GPU line's cpu_baseline sample")
+    ap.add_argument("--cpu-threads", type=int, default=0, help="host threads of the CPU legs (0 = all)")
     ap.add_argument("--nz", type=int, default=None,
                     help="override the slice count of a 3D config (one z-slab shard of an R-GPU run = nz/R)")
     ap.add_argument("--view-groups", type=int, default=None,
@@ -188,30 +189,118 @@ def _inputs(cfg, W, device=0):
     return g, I0, d
 
 
-def cpu_reference(cfg, algo, iters, threads=0, inputs=None):
-    """The oracle port (f64, reference precision) on the host cores: returns
-    (seconds per iteration, sample description, cores)."""
+def _baseline_metric():
+    """BASELINE.json's metric string, printed verbatim by both arms."""
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as f:
+            return json.load(f)["metric"]
+    except Exception:
+        return "AM iterations/sec and ray-voxel updates/sec at 1/2/4/8 B200 vs HBM roofline"
+
+
+def _oracle_module():
+    """The CPU oracle (test infrastructure: only the CPU legs of this file use
+    it), rebuilt with -march=native for the host it runs on when a compiler is
+    present (bit-identical results: -ffp-contract=off)."""
+    if "ORC_LIB" not in os.environ:
+        from oracle import oracle as O0
+        nat = O0.build_native(os.path.join("/tmp", f"wamgpu_orc_native_{os.getpid()}"))
+        if nat:
+            os.environ["ORC_LIB"] = nat
     from oracle import oracle as O
-    from paper_1508_04458_b200 import configs
-    og = O.make_geometry(**configs.geometry(cfg))
-    t0 = time.perf_counter()
-    p = O.Problem(og, mirror=False, threads=threads)
-    t_build = time.perf_counter() - t0
-    if inputs is None:
-        mu_true = O.rasterize(og, configs.phantom(cfg))
-        I0 = configs.incident(cfg, p.M)
-        d = p.simulate(mu_true, I0, cfg["seed"])
-    else:
-        I0, d = inputs
-    t0 = time.perf_counter()
-    if algo == "wam":
+    return O
+
+
+class CpuSample:
+    """A bounded sample of the workload on the host cores: the reference-
+    precision oracle port (f64 CSR+CSC, direct signed split), all threads.
+
+    2D: the full problem.  Axial 3D: slices are independent in-plane problems
+    (pin P2) and the separable Haar couples only the 2^L slices of a z-block,
+    so a sample is the CENTRAL z-block of the stack (2^L slices, 8 for AM) with
+    its own seeded Poisson draw; its time per iteration scales by
+    nz / nz_sample to the whole stack (every pass is linear in the slice
+    count).  Big configs use the slim CSR-only oracle.  step() runs the NEXT
+    iteration of the sampled run, with the scheduled expansion after it."""
+
+    def __init__(self, cfg, algo, threads, inputs=None):
+        O = _oracle_module()
+        from paper_1508_04458_b200 import configs
+        self.algo, self.cfg = algo, cfg
+        scfg = dict(cfg)
         if cfg["nz"] > 1:
-            p.set_haar_dim(cfg["haar"])
-        p.wam_init(d, I0, cfg["L"])
-    else:
-        p.am_init(d, I0)
-    t_init = time.perf_counter() - t0
-    return p, t_build, t_init
+            nzs = (1 << cfg["L"]) if algo == "wam" and cfg["haar"] == 3 else 8
+            nzs = min(nzs, cfg["nz"])
+            scfg["nz"] = nzs
+            inputs = None
+            self.scale = cfg["nz"] / nzs
+            s0 = (cfg["nz"] - nzs) // 2
+            self.what = (f"central z-block (slices {s0}-{s0 + nzs - 1} of {cfg['nz']}) of {cfg['name']}, "
+                         f"scaled x{self.scale:g}")
+        else:
+            self.scale = 1.0
+            self.what = f"{cfg['name']} (whole problem)"
+        og = O.make_geometry(**configs.geometry(scfg))
+        self.slim = cfg["nx"] * cfg["ny"] >= 1 << 20
+        t0 = time.perf_counter()
+        self.p = O.Problem(og, mirror=False, threads=threads, slim=self.slim)
+        self.t_build = time.perf_counter() - t0
+        self.nnz = self.p.nnz
+        if inputs is None:
+            # the phantom of the full stack restricted to the central slices:
+            # centred geometries put slice s of the sample at z of slice s0+s
+            mu = O.rasterize(og, configs.phantom(cfg))
+            I0 = configs.incident(scfg, self.p.M)
+            d = self.p.simulate(mu, I0, cfg["seed"])
+        else:
+            I0, d = inputs
+        t0 = time.perf_counter()
+        if algo == "wam":
+            if scfg["nz"] > 1:
+                self.p.set_haar_dim(cfg["haar"])
+            self.p.wam_init(d, I0, cfg["L"])
+        else:
+            self.p.am_init(d, I0)
+        self.t_init = time.perf_counter() - t0
+        self.done = 0
+        self.sched = set(cfg["schedule"]) if algo == "wam" else set()
+        self.t_expand = 0.0
+        self.label = "native" if os.environ.get("ORC_LIB") else "portable"
+
+    def step(self):
+        """One iteration (plus the scheduled expansion after it): seconds."""
+        t0 = time.perf_counter()
+        if self.algo == "wam":
+            self.p.wam_iterate(1)
+            self.done += 1
+            if self.done in self.sched:
+                self.p.wam_expand(0.1)
+        else:
+            self.p.am_iterate(1)
+            self.done += 1
+        return time.perf_counter() - t0
+
+    def rate(self, times):
+        """iterations/s of the WHOLE workload from per-iteration sample times."""
+        return 1.0 / (sum(times) / len(times) * self.scale)
+
+    def sample(self, first, n, threads):
+        return (f"{self.algo.upper()} iterations {first}-{first + n - 1} (with their scheduled expansions) of "
+                f"the {self.what}; f64 oracle port ({'slim CSR-only' if self.slim else 'CSR+CSC'}, "
+                f"direct signed split), {threads} threads, -O3 -ffp-contract=off "
+                f"{'-march=native' if self.label == 'native' else '(portable)'}; H build {self.t_build:.1f}s "
+                f"and init {self.t_init:.1f}s untimed")
+
+
+def _lscpu():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def run_reference(args):
@@ -222,27 +311,24 @@ def run_reference(args):
     cfg = configs.get(args.config)
     algo = args.algo or cfg["algo"]
     cores = os.cpu_count() or 1
-    p, t_build, t_init = cpu_reference(cfg, algo, args.cpu_iters, threads=cores)
-    step = (lambda: p.wam_iterate(args.cpu_iters)) if algo == "wam" else (lambda: p.am_iterate(args.cpu_iters))
+    threads = args.cpu_threads or cores
+    cs = CpuSample(cfg, algo, threads)
     for _ in range(args.warmup):
-        step()
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        step()
-        times.append(time.perf_counter() - t0)
-    sec_per_iter = sum(times) / (args.steps * args.cpu_iters)
-    val = 1.0 / sec_per_iter
-    sample = (f"{args.cpu_iters} {algo.upper()} iterations of {cfg['name']} per step (f64 CSR+CSC, direct signed "
-              f"split), oracle port, {cores} threads; H build {t_build:.1f}s and init {t_init:.1f}s untimed")
+        cs.step()
+    first = cs.done + 1
+    times = [cs.step() for _ in range(args.steps)]
+    val = cs.rate(times)
+    J = cfg["J"]
     line = {
-        "impl": "reference", "metric": f"{algo.upper()} iterations/sec ({cfg['name']})", "value": val,
+        "impl": "reference", "metric": _baseline_metric(), "value": val,
         "unit": "iterations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * sum(times) / args.steps * cs.scale, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded phantom, Poisson counts)",
-        "config": {"workload": _workload_desc(cfg, p.nnz, algo, cfg["J"]), "threads": cores},
-        "ray_voxel_updates_per_s": 2 * p.nnz * val,
-        "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": cores, "kind": "port", "sample": sample},
+        "config": {"workload": _workload_desc(cfg, cs.nnz, algo, J), "threads": threads, "cpu_model": _lscpu(),
+                   "step": "one iteration of the sampled run (scaled to the whole stack)"},
+        "ray_voxel_updates_per_s": 2 * cs.nnz * cfg["nz"] * val,
+        "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": threads, "kind": "port",
+                         "sample": cs.sample(first, args.steps, threads), "cpu_model": _lscpu()},
         "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -334,6 +420,39 @@ def _slab_tree(tree, cfg, s0, nzl):
     return np.concatenate(out)
 
 
+def _parity_pass(ctx, cfg):
+    """Stepwise run (iterate / expand) hashing the tree after each scheduled
+    expansion; compared with tests/golden/big_<cfg>.json when present."""
+    import hashlib
+    path = os.path.join(ROOT, "tests", "golden", f"big_{cfg['name']}.json")
+    fx = None
+    if os.path.exists(path):
+        with open(path) as f:
+            fx = json.load(f)
+    ctx.wam_init(cfg["L"])
+    out = {"fixture": os.path.relpath(path, ROOT) if fx else None, "expansions": []}
+    z0_init = ctx.scalars()["Z0"]
+    done = 0
+    for k, ev in enumerate(cfg["schedule"]):
+        ctx.wam_iterate(ev - done)
+        done = ev
+        n = ctx.wam_expand(0.1)
+        sha = hashlib.sha256(np.ascontiguousarray(ctx.tree()).tobytes()).hexdigest()
+        e = {"after_iter": ev, "newly": n, "tree_sha256": sha, "Z0": ctx.scalars()["Z0"]}
+        if fx and k < len(fx["oracles"]["mirror"]["expansions"]):
+            m = fx["oracles"]["mirror"]["expansions"][k]
+            e["mirror_oracle_match"] = (m["tree_sha256"] == sha and m["newly"] == n and
+                                        float.fromhex(m["Z0"]) == e["Z0"])
+            f64 = fx["oracles"].get("f64")
+            if f64:
+                e["f64_oracle_tree_match"] = f64["expansions"][k]["tree_sha256"] == sha
+        out["expansions"].append(e)
+    if fx:
+        out["Z0_init_mirror_match"] = float.fromhex(fx["oracles"]["mirror"]["Z0_init"]) == z0_init
+        out["fixture_iterations"] = fx["J"]
+    return out
+
+
 def _sum_timing(ts):
     out = dict(ts[0])
     for t in ts[1:]:
@@ -423,6 +542,13 @@ def main():
         t_run = ctx.timing()
         return t_init, t_run, recs
 
+    # ---- untimed parity pass: the tree after every scheduled expansion (and
+    # Z0) against the committed oracle fixture of this config, when there is one
+    # (tests/golden/big_<cfg>.json; bit-exact vs the fp32-mirror oracle)
+    parity = None
+    if algo == "wam" and world == 1 and not args.shard and not args.nz and J == cfg["J"]:
+        parity = _parity_pass(ctx, cfg)
+
     for _ in range(args.warmup):
         step_device()
 
@@ -461,11 +587,13 @@ def main():
     # ---- end-to-end through the C-ABI with host buffers (H2D d, I0; D2H mu)
     plumb.barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    # (at most 5 steps: a cfg4 step is ~8 s; the kernels are the device-timed ones above)
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(e2e_steps):
         ctx.set_data(d, I0)
         step_device()
         img = ctx.image()
-    e2e_s = plumb.max((time.perf_counter() - t0) / args.steps)
+    e2e_s = plumb.max((time.perf_counter() - t0) / e2e_steps)
     Ml = ctx.row1 - ctx.row0
     nz = cfg["nz"]
     h2d = 2 * 4 * Ml * nz
@@ -507,20 +635,17 @@ def main():
         cpu = None
         if world == 1 and not args.no_cpu_baseline and not args.shard:
             try:
-                cores = os.cpu_count() or 1
-                p, tb, tinit = cpu_reference(cfg, algo, args.cpu_iters, threads=cores, inputs=(I0, d))
-                t0 = time.perf_counter()
-                (p.wam_iterate if algo == "wam" else p.am_iterate)(args.cpu_iters)
-                cs = (time.perf_counter() - t0) / args.cpu_iters
-                cpu = {"value": 1.0 / cs, "unit": "iterations/s", "cores": cores, "kind": "port",
-                       "sample": f"{args.cpu_iters} {algo.upper()} iterations of {cfg['name']} after init "
-                                 f"(f64 oracle port, {cores} threads; H build {tb:.1f}s, init {tinit:.1f}s untimed)"}
-                del p
+                threads = args.cpu_threads or os.cpu_count() or 1
+                cs = CpuSample(cfg, algo, threads, inputs=(I0, d) if cfg["nz"] == 1 else None)
+                ts = [cs.step() for _ in range(args.cpu_iters)]
+                cpu = {"value": cs.rate(ts), "unit": "iterations/s", "cores": threads, "kind": "port",
+                       "sample": cs.sample(1, args.cpu_iters, threads), "cpu_model": _lscpu()}
+                del cs
             except Exception as e:  # the baseline is reported, never the target
                 cpu = {"value": None, "unit": "iterations/s", "cores": os.cpu_count(), "kind": "port",
                        "sample": f"failed: {e}"}
         line = {
-            "metric": f"{algo.upper()} iterations/sec ({cfg['name']}) and ray-voxel updates/sec vs HBM roofline",
+            "metric": _baseline_metric(),
             "value": iters_per_s, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 storage / f64 accumulation",
@@ -530,10 +655,15 @@ def main():
                        "parallelism": (f"views/{world}" if cfg["nz"] == 1 else
                                        f"views/{part['view_groups']} x z-slabs/{part['z_groups']}"),
                        "collective": collective},
-            "ray_voxel_updates_per_s": 2 * nnz * nz * J / (ms_step * 1e-3),
+            # H passes only (forward + back launches; a 3D launch covers every
+            # slice): the root-only iterations run over the approximation
+            # columns Phi_A instead of H and are counted apart
+            "ray_voxel_updates_per_s": (fwd_n + back_n) / args.steps * nnz * nz / (ms_step * 1e-3),
+            "h_passes_per_step": (fwd_n + back_n) / args.steps,
             "final_objective": final_obj,
             "tree": {"active_set_by_iteration": sorted({r["active_set"] for r in recs}),
-                     "coefficients": N, "phi_minus_nnz": split_nnz},
+                     "coefficients": N * nz, "phi_minus_nnz": split_nnz},
+            "parity": parity,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
                          "algorithmic_bytes": fwd_bytes if "forward" in dom else back_bytes},
@@ -546,7 +676,7 @@ def main():
                                         "phi_a": phi_ms / args.steps},
                         "phi_a_iterations_per_step": phi_n / args.steps},
             "e2e": {"value": J / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "wall_s_timed": wall,

@@ -14,7 +14,10 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = os.path.join(HERE, "liborc.so")
+# ORC_LIB: an alternative build of the same source (bench.py's CPU legs build
+# one with -march=native on the host they time; -ffp-contract=off keeps it
+# bit-identical)
+_LIB = os.environ.get("ORC_LIB") or os.path.join(HERE, "liborc.so")
 _REFLIB = os.path.join(HERE, "_ref", "libwamref.so")
 
 _d = C.POINTER(C.c_double)
@@ -49,6 +52,21 @@ class Record(C.Structure):
 def build():
     """Compile liborc.so (and oracle/_ref when /root/reference is present)."""
     subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def build_native(out_dir):
+    """liborc.so tuned for THIS host (-march=native; -ffp-contract=off keeps
+    every result bit-identical to the portable build).  Returns its path, or
+    None when no compiler is available."""
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, "liborc.so")
+    cmd = ["g++", "-std=c++20", "-O3", "-march=native", "-ffp-contract=off", "-fPIC", "-pthread", "-shared",
+           "-o", out, os.path.join(HERE, "wam_oracle.cpp")]
+    try:
+        subprocess.run(cmd, check=True, capture_output=True)
+    except Exception:
+        return None
+    return out
 
 
 _lib = None
