@@ -286,6 +286,124 @@ __global__ void __launch_bounds__(32 * WPB, MINB) k_fwd3s(uint64_t M, int sbeg, 
     }
 }
 
+// ---- banded forward (large slabs).  When the slab of mu exceeds L2 (cfg4:
+// 1M voxels x 128 slices x 4 B = 512 MB against 126 MB), every view's rays
+// sweep the whole image and the gathers go to DRAM (ncu, cfg4 k_fwd3s: 584 GB
+// read per launch, 18.7% L2 hits, DRAM 71% busy).  The image is cut into B
+// horizontal bands of hb rows (a band's mu is L2-resident); a ray's Siddon
+// entries are monotone in iy, so its entries inside band b form one
+// contiguous range [blo, bhi) (k_band_bounds).  Band b's launch adds each
+// ray's band-b segment to a running fp64 sum per (ray, slice) in lacc, bands
+// in fixed order 0..B-1 (deterministic, no atomics); the last band's launch
+// finishes as k_fwd3s does (l out, or q = fp32(I0 exp(-l)) + I-div partial).
+
+// per ray y: band b's entries are [rp[y] + blo[y*B + b], rp[y] + bhi[y*B + b])
+// (empty bands lo = hi = 0).  Warp per ray; a band boundary is where an
+// entry's band differs from its predecessor's.
+// bad: set when some row is not monotone in iy (an explicit matrix whose row
+// is not in Siddon order): a band would then need several ranges, and the
+// caller keeps the unbanded forward.
+__global__ void k_band_bounds(uint64_t M, const unsigned long long* __restrict__ rp, const uint2* __restrict__ A,
+                              int nx, int hb, int B, unsigned* __restrict__ blo, unsigned* __restrict__ bhi,
+                              int* __restrict__ bad) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t y = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; y < M; y += W) {
+        for (int b = lane; b < B; b += 32) { blo[y * B + b] = 0u; bhi[y * B + b] = 0u; }
+        __syncwarp();
+        const uint64_t lo = rp[y], n = rp[y + 1] - lo;
+        for (uint64_t k0 = 0; k0 < n; k0 += 32) {
+            const uint64_t k = k0 + lane;
+            const int band = k < n ? (int)(A[lo + k].x / (unsigned)nx) / hb : -1;
+            const int prev = __shfl_up_sync(0xffffffffu, band, 1);
+            int pb = lane ? prev : -1;
+            if (lane == 0 && k0) pb = (int)(A[lo + k - 1].x / (unsigned)nx) / hb;
+            if (k < n && band != pb) {
+                blo[y * B + band] = (unsigned)k;
+                if (pb >= 0) bhi[y * B + pb] = (unsigned)k;
+            }
+            if (k + 1 == n) bhi[y * B + band] = (unsigned)n;
+        }
+        __syncwarp();
+        // every entry in exactly one band range <=> the ranges cover n
+        unsigned long long cov = 0;
+        for (int b = lane; b < B; b += 32) {
+            const unsigned a = blo[y * B + b], e = bhi[y * B + b];
+            cov += e >= a ? e - a : (1ull << 40);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cov += __shfl_xor_sync(0xffffffffu, cov, o);
+        if (lane == 0 && cov != n) atomicOr(bad, 1);
+        __syncwarp();
+    }
+}
+
+template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P, int WPB = 8, int MINB = 1>
+__global__ void __launch_bounds__(32 * WPB, MINB) k_fwd3s_band(uint64_t M, int nz, int band, int B,
+                                               const unsigned long long* __restrict__ rp,
+                                               const unsigned* __restrict__ blo, const unsigned* __restrict__ bhi,
+                                               const uint2* __restrict__ A, const float* __restrict__ mu,
+                                               const float* __restrict__ I0, const float* __restrict__ d,
+                                               float* __restrict__ q, double* __restrict__ lacc,
+                                               double* __restrict__ lout, double* __restrict__ partial,
+                                               int* __restrict__ flag) {
+    constexpr int G = 32 / LPR, SB = LPR * SPL;
+    static_assert(P % SB == 0, "slab parts");
+    __shared__ __align__(16) SlabStage<G> s_st[WPB];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, g = lane / LPR, lig = lane % LPR;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const bool last = band == B - 1;
+    double tacc = 0.0;
+    for (uint64_t y0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + wib) * G; y0 < M; y0 += W * G)
+    for (int s0 = 0; s0 < nz; s0 += SB) {
+        const uint64_t y = y0 + g;
+        const bool ok = y < M;
+        const uint64_t base = ok ? rp[y] : 0;
+        const uint64_t lo = ok ? base + blo[y * B + band] : 0, hi = ok ? base + bhi[y * B + band] : 0;
+        const int maxlen = (int)__reduce_max_sync(0xffffffffu, (unsigned)(hi - lo));
+        if (maxlen == 0 && band > 0 && !last) continue;   // nothing to add anywhere in the warp
+        double acc[SPL];
+        slab_dot_g<LPR, SPL, U, NF, SIGNED, P>(A, mu + s0, lo, hi, maxlen, lig, g, s_st[wib], acc);
+        if (!ok) continue;
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+            const int s = s0 + slab_slice<LPR, SPL>(lig, j);
+            if (s >= nz) continue;
+            const uint64_t id = y * P + s;
+            double tot = acc[j];
+            if (band > 0) {
+                if (hi == lo && !last) continue;              // nothing to add for this ray
+                tot = lacc[id] + acc[j];
+            }
+            if (!last) {
+                lacc[id] = tot;
+                continue;
+            }
+            if (!isfinite(tot)) atomicOr(flag, 1);
+            if (MODE == 0) {
+                lout[id] = tot;
+            } else {
+                const double qq = (double)I0[id] * exp(-tot);
+                q[id] = (float)qq;
+                tacc += idiv_term((double)d[id], qq);
+            }
+        }
+    }
+    if (MODE == 1 && last) {
+        __shared__ double sm[32];
+        double v = tacc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) sm[wib] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sm[w];
+            partial[blockIdx.x] = t;
+        }
+    }
+}
+
 // Tile-major layout of the view-group split update (wamgpu.cu tile_update_split):
 // the Rv members of a slab own tile rows [r*rows, (r+1)*rows) of the 2^L-cube
 // tiles; chunk r of a tile-major buffer holds them, tile (kt, ti, tj) at local

@@ -199,6 +199,11 @@ struct wamgpu_ctx {
     int split_variant = 0;                  // WAMGPU_SPLIT_VARIANT
     int walk_variant = 0;                   // WAMGPU_WALK_VARIANT
     int slab_variant = 112;                 // WAMGPU_SLAB_VARIANT (3D slab SpMM)
+    // banded 3D forward (kernels3d.cuh k_fwd3s_band): image rows cut into
+    // band_B bands of band_hb rows; per (local ray, band) entry range
+    int band_B = 0, band_hb = 0, band_P = 0;
+    DBuf<unsigned> blo, bhi;
+    DBuf<double> lacc;                      // running per-(ray, slice) sums between band launches
     bool mu_nonneg = false;                 // AM: mu has no sign bit set (see am_init)
     double t_trace = 0.0;                   // WAMGPU_TRACE_HOST phase clock
     // fused back projection + all-reduce over NVLink peer memory (kernels_ar.cuh)
@@ -527,6 +532,8 @@ static void check_flag(Ctx* c, const char* where) {
 // ------------------------------------------------------------- system model
 static void finish_matrix(Ctx* c, bool have_csc = false) {
     c->zA_L = -1;
+    c->band_B = 0; c->band_hb = 0; c->band_P = 0;
+    c->blo.release(); c->bhi.release(); c->lacc.release();
     c->phiA_ok = false;
     c->phiA_L = -1;
     c->phiA_rp.release(); c->phiA_cp.release(); c->phiA_col.release(); c->phiA_row.release();
@@ -950,6 +957,44 @@ template <int P> struct SlabShape {
         case 16: X(3, 2, 4, 6) break;                                                                              \
         default: X(3, 4, 8, 2) break;                                                                              \
     }
+// Bands of the 3D forward (k_fwd3s_band): only when the mu slab outgrows L2.
+// WAMGPU_FWD_BAND_MB (default 48; 0 = never): target mu bytes per band.
+static int forward_bands(Ctx* c) {
+    const int P = slab_stride(c);
+    if (c->nzl == 1 || !c->Ml) return 1;
+    if (c->band_P == P && c->band_B > 0) return c->band_B;
+    double mb = 48.0;
+    if (const char* e = std::getenv("WAMGPU_FWD_BAND_MB")) mb = std::atof(e);
+    const double row = (double)c->nx * P * 4.0, slab = row * c->ny;
+    int B = 1, hb = c->ny;
+    if (mb > 0.0 && slab > 2.0 * mb * 1048576.0) {
+        hb = std::max(1, (int)(mb * 1048576.0 / row));
+        B = (c->ny + hb - 1) / hb;
+        if (B > 64) { B = 64; hb = (c->ny + B - 1) / B; B = (c->ny + hb - 1) / hb; }
+    }
+    c->band_P = P;
+    c->band_B = B;
+    c->band_hb = hb;
+    if (B == 1) return 1;
+    c->blo.alloc(c->Ml * (uint64_t)B);
+    c->bhi.alloc(c->Ml * (uint64_t)B);
+    CK(cudaMemsetAsync(c->flag.p, 0, 4, c->st));
+    k_band_bounds<<<nblk_warp(c, c->Ml), 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, hb, B, c->blo.p, c->bhi.p,
+                                                          c->flag.p);
+    check_launch(c, "k_band_bounds");
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, c->flag.p, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemsetAsync(c->flag.p, 0, 4, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (bad) {   // rows not monotone in iy (explicit matrix): keep the unbanded forward
+        c->blo.release(); c->bhi.release();
+        c->band_B = 1;
+        return 1;
+    }
+    c->lacc.alloc(c->Ml * (uint64_t)P);
+    return B;
+}
+
 template <int MODE, int P>
 static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxblk, bool nonneg) {
     using S = SlabShape<P>;
@@ -963,6 +1008,24 @@ static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxbl
                                                             c->q.p, l, c->partial.p, c->flag.p);
             return nb;
         }
+    }
+    const int B = forward_bands(c);
+    if (B > 1) {
+        // bands in fixed order; MODE 0 accumulates straight in l
+        double* acc = MODE == 0 ? l : c->lacc.p;
+        nb = std::min<unsigned>(nblk_warp(c, (c->Ml + S::G - 1) / S::G), maxblk);
+        for (int b = 0; b < B; ++b) {
+            if (uns)
+                k_fwd3s_band<MODE, S::LPR, S::SPL, 4, 3, false, P, 8, 2><<<nb, 256, 0, c->st>>>(
+                    c->Ml, c->nzl, b, B, c->rp.p, c->blo.p, c->bhi.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, acc, l,
+                    c->partial.p, c->flag.p);
+            else
+                k_fwd3s_band<MODE, S::LPR, S::SPL, 4, 3, true, P, 8, 2><<<nb, 256, 0, c->st>>>(
+                    c->Ml, c->nzl, b, B, c->rp.p, c->blo.p, c->bhi.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, acc, l,
+                    c->partial.p, c->flag.p);
+        }
+        launched(c, B - 1);
+        return nb;
     }
 #define FX(NF, U, WPB, MINB)                                                                                       \
     {                                                                                                              \

@@ -155,3 +155,32 @@ def test_root_only_iterations_use_phi_a_3d(wam, orc, name):
     og2 = [r["objective"] for r in c.wam_iterate(2)]
     assert c.timing()["phi_launches"] == 0
     assert rel_l2(og2, [r[1] for r in p32.wam_iterate(2)]) < TOL_MIRROR
+
+
+@pytest.mark.parametrize("name", ["tiny3d16", "small3d"])
+def test_banded_forward(wam, orc, name, monkeypatch):
+    """The banded 3D forward (k_fwd3s_band: image rows in bands whose mu stays
+    L2-resident, per-ray band segments summed in band order; the cfg4 path) is
+    forced on small stacks with a tiny band size: forward projection and the
+    separable-Haar WAM run agree with the unbanded forward and the oracles."""
+    cfg, p32, mu_true, I0, d = problem_inputs(name, orc, wam, mirror=True)
+    out = {}
+    for mb in ("0", "0.004"):
+        monkeypatch.setenv("WAMGPU_FWD_BAND_MB", mb)
+        c = _ctx(wam, cfg)
+        l = c.forward_project(mu_true)
+        c.set_haar_dim(3)
+        c.set_data(d, I0)
+        c.wam_init(cfg["L"])
+        r = c.wam_run(cfg["J"], cfg["schedule"], 0.1)
+        out[mb] = (l, [x["objective"] for x in r], c.tree(), c.image())
+        c.close()
+    (l0, o0, t0, m0), (l1, o1, t1, m1) = out["0"], out["0.004"]
+    assert rel_l2(l1, l0) < 1e-14
+    assert rel_l2(l1, p32.forward_project(mu_true.astype(np.float32).astype(np.float64))) < 1e-14
+    assert rel_l2(o1, o0) < 1e-12 and np.array_equal(t1, t0) and rel_l2(m1, m0) < 1e-9
+    p32.set_haar_dim(3)
+    p32.wam_init(d, I0, cfg["L"])
+    ro = p32.wam_run(cfg["J"], cfg["schedule"], 0.1)
+    assert np.array_equal(t1, p32.wam_tree())
+    assert rel_l2(o1, [x[1] for x in ro]) < TOL_MIRROR
