@@ -116,6 +116,22 @@ int wamgpu_set_partition(wamgpu_ctx* ctx, int view_groups);
 int wamgpu_get_partition(const wamgpu_ctx* ctx, int* view_groups, int* z_groups, int* slab_begin,
                          int* slab_slices);
 
+/* The rank grid above, computed on the host without a GPU (the same
+ * arithmetic set_geometry applies): rank's view group / z group, its CSR rows
+ * [row_begin, row_end) (row = view*detectors + det), its slices
+ * [slab_begin, slab_begin + slab_slices) and their slab stride, and, when the
+ * view group splits the coefficient update (algo 1 = AM, 2 = WAM; haar_dim,
+ * levels of the WAM model), the rows it owns: image rows (AM) or rows of
+ * 2^levels-cube tiles (separable-Haar WAM). */
+typedef struct {
+    int view_groups, z_groups, view_group, z_group;
+    uint64_t row_begin, row_end;
+    int slab_begin, slab_slices, slab_stride;
+    int split_update, own_row_begin, own_rows;
+} wamgpu_plan;
+int wamgpu_plan_partition(const wamgpu_geometry* g, int rank, int nranks, int view_groups, int algo, int haar_dim,
+                          int levels, wamgpu_plan* out);
+
 /* Fused back projection + all-reduce over NVLink peer memory (view-sharded 2D,
  * DESIGN.md §7): replaces the back-projection kernel + ncclAllReduce of
  * [g || b-] by one kernel per rank.  After set_comm and the matrix: every rank

@@ -61,7 +61,7 @@ EXPORTED = [
     "wamgpu_set_kernel_timing", "wamgpu_rasterize", "wamgpu_simulate", "wamgpu_host_rays", "wamgpu_set_haar_dim",
     "wamgpu_p2p_export", "wamgpu_p2p_import", "wamgpu_selftest_fused_allreduce", "wamgpu_selftest_fused_back",
     "wamgpu_set_comm_local", "wamgpu_set_partition", "wamgpu_get_partition", "wamgpu_wam_expand_with", "wamgpu_simulate_device",
-    "wamgpu_load_matrix_wamh", "wamgpu_save_matrix_wamh",
+    "wamgpu_load_matrix_wamh", "wamgpu_save_matrix_wamh", "wamgpu_plan_partition",
 ]
 P2P_BLOB = 256   # WAMGPU_P2P_BLOB
 
@@ -82,6 +82,26 @@ class Geometry(C.Structure):
                     detector_spacing=self.detector_spacing, views=self.views, beam=self.beam,
                     source_to_center=self.source_to_center, source_to_detector=self.source_to_detector,
                     fan_angle_step=self.fan_angle_step)
+
+
+class Plan(C.Structure):
+    """wamgpu_plan: one rank's share of the rank grid (host-only arithmetic)."""
+    _fields_ = [("view_groups", C.c_int), ("z_groups", C.c_int), ("view_group", C.c_int), ("z_group", C.c_int),
+                ("row_begin", C.c_uint64), ("row_end", C.c_uint64), ("slab_begin", C.c_int),
+                ("slab_slices", C.c_int), ("slab_stride", C.c_int), ("split_update", C.c_int),
+                ("own_row_begin", C.c_int), ("own_rows", C.c_int)]
+
+    def asdict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+def plan_partition(g, rank, nranks, view_groups=0, algo="wam", haar_dim=3, levels=0):
+    """The rank grid of wamgpu_set_partition / set_geometry for `rank` of
+    `nranks`, computed on the host (no GPU needed)."""
+    out = Plan()
+    _chk(load().wamgpu_plan_partition(C.byref(g), int(rank), int(nranks), int(view_groups),
+                                      1 if algo == "am" else 2, int(haar_dim), int(levels), C.byref(out)))
+    return out.asdict()
 
 
 class Primitive(C.Structure):

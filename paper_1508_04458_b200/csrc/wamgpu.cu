@@ -621,16 +621,45 @@ static void finish_matrix(Ctx* c, bool have_csc = false) {
 // A 2D problem shards views only (Rv = R).  An axial 3D stack defaults to
 // z-slabs only (Rv = 1, scalars cross GPUs); wamgpu_set_partition picks Rv > 1
 // (view shards of a slab sum their partial back projections over comm_v).
-static void resolve_grid(Ctx* c) {
-    const int R = c->nranks;
-    int Rv = c->nz == 1 ? R : (c->vgroups_req > 0 ? c->vgroups_req : 1);
-    if (c->nz == 1 && c->vgroups_req > 0 && c->vgroups_req != R)
-        throw ConfigError("partition: a 2D problem shards views across all ranks");
+// The partition arithmetic itself is host-only (GridPlan), shared with the
+// GPU-free wamgpu_plan_partition that the multi-rank CPU tests call.
+struct GridPlan {
+    int Rv = 1, Rz = 1, vg = 0, zg = 0;
+    uint64_t row0 = 0, row1 = 0;
+    int s0 = 0, nzl = 1;
+};
+static GridPlan make_plan(int nz, int views, int detectors, int rank, int R, int vreq) {
+    GridPlan p;
+    if (R < 1 || rank < 0 || rank >= R) throw ContractError("partition: invalid rank / rank count");
+    int Rv = nz == 1 ? R : (vreq > 0 ? vreq : 1);
+    if (nz == 1 && vreq > 0 && vreq != R) throw ConfigError("partition: a 2D problem shards views across all ranks");
     if (Rv < 1 || R % Rv) throw ConfigError("partition: view groups must divide the rank count");
-    c->Rv = Rv;
-    c->Rz = R / Rv;
-    c->vg = c->rank % Rv;
-    c->zg = c->rank / Rv;
+    p.Rv = Rv;
+    p.Rz = R / Rv;
+    p.vg = rank % Rv;
+    p.zg = rank / Rv;
+    if (nz > 128 * p.Rz) throw ConfigError("wamgpu: at most 128 slices per GPU slab");
+    const int v0 = (int)((int64_t)views * p.vg / p.Rv), v1 = (int)((int64_t)views * (p.vg + 1) / p.Rv);
+    p.row0 = (uint64_t)v0 * detectors;
+    p.row1 = (uint64_t)v1 * detectors;
+    if (nz == 1) {
+        p.s0 = 0;
+        p.nzl = 1;
+    } else {
+        p.s0 = (int)((int64_t)nz * p.zg / p.Rz);
+        p.nzl = (int)((int64_t)nz * (p.zg + 1) / p.Rz) - p.s0;
+        if (p.nzl < 1) throw ConfigError("wamgpu: more z groups than slices");
+        if (p.nzl > 128) throw ConfigError("wamgpu: at most 128 slices per GPU slab");
+    }
+    return p;
+}
+
+static void resolve_grid(Ctx* c) {
+    const GridPlan p = make_plan(c->nz, 1, 1, c->rank, c->nranks, c->vgroups_req);
+    c->Rv = p.Rv;
+    c->Rz = p.Rz;
+    c->vg = p.vg;
+    c->zg = p.zg;
     if (c->comm_kind == 1 && c->Rv > 1 && c->Rz > 1 && !c->comm_v) {   // collective over the whole comm
         NK(ncclCommSplit(c->comm, c->zg, c->vg, &c->comm_v, nullptr));
         NK(ncclCommSplit(c->comm, c->vg, c->zg, &c->comm_z, nullptr));
@@ -638,20 +667,12 @@ static void resolve_grid(Ctx* c) {
 }
 
 static void partition(Ctx* c, int views, int detectors) {
-    if (c->nz > 128 * c->Rz) throw ConfigError("wamgpu: at most 128 slices per GPU slab");
     resolve_grid(c);
-    const int v0 = (int)((int64_t)views * c->vg / c->Rv), v1 = (int)((int64_t)views * (c->vg + 1) / c->Rv);
-    c->row0 = (uint64_t)v0 * detectors;
-    c->row1 = (uint64_t)v1 * detectors;
-    if (c->nz == 1) {
-        c->s0 = 0;
-        c->nzl = 1;
-    } else {
-        c->s0 = (int)((int64_t)c->nz * c->zg / c->Rz);
-        c->nzl = (int)((int64_t)c->nz * (c->zg + 1) / c->Rz) - c->s0;
-        if (c->nzl < 1) throw ConfigError("wamgpu: more z groups than slices");
-        if (c->nzl > 128) throw ConfigError("wamgpu: at most 128 slices per GPU slab");
-    }
+    const GridPlan p = make_plan(c->nz, views, detectors, c->rank, c->nranks, c->vgroups_req);
+    c->row0 = p.row0;
+    c->row1 = p.row1;
+    c->s0 = p.s0;
+    c->nzl = p.nzl;
     c->Ml = c->row1 - c->row0;
 }
 
@@ -3054,6 +3075,36 @@ int wamgpu_set_grid(wamgpu_ctx* ctx, int nx, int ny, int nz) {
 int wamgpu_set_matrix_csr(wamgpu_ctx* ctx, uint64_t rows, uint64_t cols, uint64_t nnz, const uint64_t* rp,
                           const uint32_t* ci, const double* val) {
     API_TRY(ctx, { NEED(ctx); set_matrix_csr(ctx, rows, cols, nnz, rp, ci, val); })
+}
+
+int wamgpu_plan_partition(const wamgpu_geometry* g, int rank, int nranks, int view_groups, int algo, int haar_dim,
+                          int levels, wamgpu_plan* out) {
+    const wamgpu_ctx* none = nullptr;
+    API_TRY(none, {
+        NEED(g); NEED(out);
+        validate(*g);
+        const GridPlan p = make_plan(g->nz, g->views, g->detectors, rank, nranks, view_groups);
+        *out = wamgpu_plan{};
+        out->view_groups = p.Rv; out->z_groups = p.Rz; out->view_group = p.vg; out->z_group = p.zg;
+        out->row_begin = p.row0; out->row_end = p.row1;
+        out->slab_begin = p.s0; out->slab_slices = p.nzl;
+        int P = 1;
+        if (p.nzl > 1) { P = 8; while (P < p.nzl) P *= 2; }
+        out->slab_stride = P;
+        // the view group's split update (wamgpu.cu am/wam_split_update): its
+        // members own disjoint image rows (AM) or rows of 2^L-cube tiles (WAM)
+        const bool on = split_update_enabled() && g->nz > 1 && p.Rv > 1;
+        if (on && algo == 1 && g->ny % p.Rv == 0) {
+            out->split_update = 1;
+            out->own_rows = g->ny / p.Rv;
+            out->own_row_begin = p.vg * out->own_rows;
+        } else if (on && algo == 2 && haar_dim == 3 && levels >= 0 && levels < 20 &&
+                   ((g->ny >> levels) % p.Rv) == 0) {
+            out->split_update = 1;
+            out->own_rows = (g->ny >> levels) / p.Rv;
+            out->own_row_begin = p.vg * out->own_rows;
+        }
+    })
 }
 
 int wamgpu_load_matrix_wamh(wamgpu_ctx* ctx, const char* path) {

@@ -12,8 +12,21 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 
+def _geom(name):
+    import paper_1508_04458_b200 as W
+    from paper_1508_04458_b200 import configs
+    return W, configs.get(name), configs.geometry(configs.get(name), W.Geometry)
+
+
+def lib_plan(name, rank, nranks, view_groups=0, algo="wam", levels=0, haar=3):
+    """The rank's share as libwamgpu.so computes it (wamgpu_plan_partition:
+    the arithmetic set_geometry applies; host-only, no GPU)."""
+    W, cfg, g = _geom(name)
+    return W.plan_partition(g, rank, nranks, view_groups, algo, haar, levels)
+
+
 def view_range(V, rank, nranks):
-    """libwamgpu.so: v0 = V*rank/P, v1 = V*(rank+1)/P (integer division)."""
+    """The documented rule: v0 = V*rank/P, v1 = V*(rank+1)/P."""
     return V * rank // nranks, V * (rank + 1) // nranks
 
 
@@ -34,9 +47,8 @@ def _worker(rank, world, port, out):
     from wam_testutil import problem_inputs
     cfg, p, mu_true, I0, d = problem_inputs("tiny", O, None)
     rp, ci, v = p.csr()
-    D = cfg["detectors"]
-    v0, v1 = view_range(cfg["views"], rank, world)
-    r0, r1 = v0 * D, v1 * D
+    pl = lib_plan("tiny", rank, world)                    # the library's own row shard
+    r0, r1 = pl["row_begin"], pl["row_end"]
     # one AM iteration, sharded: partial H^T q and H^T d over own rows, all-reduce
     q = I0 * np.exp(-p.forward_project(np.zeros(p.N)))
     def partial_back(w):
@@ -67,6 +79,56 @@ def test_view_partition_covers_rows_once():
             rng = [view_range(V, r, P) for r in range(P)]
             assert rng[0][0] == 0 and rng[-1][1] == V
             assert all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
+
+
+@pytest.mark.parametrize("name", ["tiny", "cfg1", "cfg2"])
+@pytest.mark.parametrize("R", [1, 2, 3, 8])
+def test_library_plan_2d_is_view_sharding(name, R):
+    W, cfg, g = _geom(name)
+    D = cfg["detectors"]
+    rows = []
+    for r in range(R):
+        pl = lib_plan(name, r, R)
+        assert (pl["view_groups"], pl["z_groups"], pl["view_group"]) == (R, 1, r)
+        v0, v1 = view_range(cfg["views"], r, R)
+        assert (pl["row_begin"], pl["row_end"]) == (v0 * D, v1 * D)
+        assert pl["slab_slices"] == 1 and pl["split_update"] == 0
+        rows.append((pl["row_begin"], pl["row_end"]))
+    assert rows[0][0] == 0 and rows[-1][1] == cfg["views"] * D
+    assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+    with pytest.raises(W.ConfigError):          # 2D shards views over ALL ranks
+        W.plan_partition(g, 0, R + 1, view_groups=1)
+
+
+@pytest.mark.parametrize("name,R,Rv", [("cfg3", 8, 8), ("cfg3", 8, 1), ("cfg3", 8, 2), ("cfg4", 8, 8),
+                                       ("cfg4", 4, 2), ("tiny3d16", 4, 2), ("cfg5", 8, 8)])
+def test_library_plan_3d_grid(name, R, Rv):
+    """Every (ray, slice) once; slab strides; the split update's owned tile rows
+    tile the image (view groups x z-slabs, rank = zg*Rv + vg)."""
+    W, cfg, g = _geom(name)
+    algo = "am" if cfg["algo"] == "am" else "wam"
+    L = cfg["L"]
+    seen = np.zeros((cfg["views"], cfg["nz"]), np.int32)
+    own = {}
+    for r in range(R):
+        pl = lib_plan(name, r, R, Rv, algo, L)
+        vg, zg, (v0, v1), (s0, s1) = grid_of(r, R, Rv, cfg["views"], cfg["nz"])
+        assert (pl["view_group"], pl["z_group"]) == (vg, zg)
+        D = cfg["detectors"]
+        assert (pl["row_begin"], pl["row_end"]) == (v0 * D, v1 * D)
+        assert (pl["slab_begin"], pl["slab_begin"] + pl["slab_slices"]) == (s0, s1)
+        P = pl["slab_stride"]
+        assert P >= pl["slab_slices"] and P in (8, 16, 32, 64, 128)
+        seen[v0:v1, s0:s1] += 1
+        if Rv > 1:
+            assert pl["split_update"] == 1
+            own.setdefault(zg, []).append((pl["own_row_begin"], pl["own_rows"]))
+    assert (seen == 1).all()
+    unit = cfg["ny"] if algo == "am" else cfg["ny"] >> L
+    for zg, lst in own.items():
+        lst.sort()
+        assert lst[0][0] == 0 and sum(n for _, n in lst) == unit
+        assert all(a[0] + a[1] == b[0] for a, b in zip(lst, lst[1:]))
 
 
 def test_two_rank_sharded_am_step_matches_single_rank():
@@ -193,10 +255,12 @@ def _grid_worker(rank, world, port, Rv, out):
     Rz = world // Rv
     # sub-groups as ncclCommSplit builds them (every rank creates every group)
     vgroups = [dist.new_group([z * Rv + v for v in range(Rv)]) for z in range(Rz)]
-    vg, zg, (v0, v1), (s0, s1) = grid_of(rank, world, Rv, cfg["views"], cfg["nz"])
-    D, M, N = cfg["detectors"], p.M, p.N
+    pl = lib_plan("tiny3d16", rank, world, Rv, "wam", cfg["L"])   # the library's grid
+    zg = pl["z_group"]
+    s0, s1 = pl["slab_begin"], pl["slab_begin"] + pl["slab_slices"]
+    M, N = p.M, p.N
     rp, ci, v = p.csr()          # in-plane matrix, shared by every slice (pin P2)
-    r0, r1 = v0 * D, v1 * D
+    r0, r1 = pl["row_begin"], pl["row_end"]
     q = (I0 * np.exp(-p.forward_project(np.zeros(N * cfg["nz"])))).reshape(cfg["nz"], M)
     g = np.zeros((s1 - s0, N))
     for y in range(r0, r1):
