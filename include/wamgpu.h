@@ -116,6 +116,17 @@ int wamgpu_set_partition(wamgpu_ctx* ctx, int view_groups);
 int wamgpu_get_partition(const wamgpu_ctx* ctx, int* view_groups, int* z_groups, int* slab_begin,
                          int* slab_slices);
 
+/* 3D forward projector of an axial stack: kind 0 = slab SpMM over
+ * the stored in-plane matrix (projector.hpp:123-148 built once, read per pass);
+ * kind 1 = on the fly: every pass re-traces the rays (projector.hpp:52-119 on
+ * the device, bit-identical h) and stages the image tiles in shared memory by
+ * TMA.  Kind 1 needs a geometry (not an explicit matrix) and >= 17 local
+ * slices; the first launch checks that every ray bundle fits its tiles and
+ * falls back to kind 0 otherwise.  get: state 0 = stored matrix, 1 = on the fly
+ * requested (not launched yet), 2 = on the fly active, -1 = rejected. */
+int wamgpu_set_projector(wamgpu_ctx* ctx, int kind);
+int wamgpu_get_projector(const wamgpu_ctx* ctx, int* state);
+
 /* The rank grid above, computed on the host without a GPU (the same
  * arithmetic set_geometry applies): rank's view group / z group, its CSR rows
  * [row_begin, row_end) (row = view*detectors + det), its slices

@@ -62,6 +62,7 @@ EXPORTED = [
     "wamgpu_p2p_export", "wamgpu_p2p_import", "wamgpu_selftest_fused_allreduce", "wamgpu_selftest_fused_back",
     "wamgpu_set_comm_local", "wamgpu_set_partition", "wamgpu_get_partition", "wamgpu_wam_expand_with", "wamgpu_simulate_device",
     "wamgpu_load_matrix_wamh", "wamgpu_save_matrix_wamh", "wamgpu_plan_partition",
+    "wamgpu_set_projector", "wamgpu_get_projector",
 ]
 P2P_BLOB = 256   # WAMGPU_P2P_BLOB
 
@@ -256,6 +257,17 @@ class Context:
     def set_partition(self, view_groups: int):
         """Rank grid: view_groups x (nranks / view_groups) z groups (3D); 0 = default."""
         _chk(load().wamgpu_set_partition(self.h, int(view_groups)), self.h)
+
+    def set_projector(self, kind: int):
+        """3D forward projector: 0 = slab SpMM over the stored in-plane matrix,
+        1 = on the fly (rays re-traced every pass, image tiles staged by TMA)."""
+        _chk(load().wamgpu_set_projector(self.h, int(kind)), self.h)
+
+    def projector(self) -> int:
+        """0 stored matrix, 1 on the fly requested, 2 on the fly active, -1 rejected."""
+        v = C.c_int()
+        _chk(load().wamgpu_get_projector(self.h, C.byref(v)), self.h)
+        return v.value
 
     def partition(self):
         v = [C.c_int() for _ in range(4)]

@@ -34,6 +34,7 @@
 #include "kernels.cuh"
 #include "kernels3d.cuh"
 #include "kernels3h.cuh"
+#include "kernels3t.cuh"
 #include "kernels_ar.cuh"
 #include "kernels_phi.cuh"
 
@@ -205,6 +206,17 @@ struct wamgpu_ctx {
     DBuf<unsigned> blo, bhi;
     DBuf<double> lacc;                      // running per-(ray, slice) sums between band launches
     bool mu_nonneg = false;                 // AM: mu has no sign bit set (see am_init)
+    // on-the-fly 3D forward with TMA-staged image tiles (kernels3t.cuh): the
+    // local ray table stays on the device; fwd3t: 0 off, 1 on (first launch
+    // checks the bundle geometry), 2 verified, -1 rejected (slab SpMM kept)
+    DBuf<wamgpu::RayDev> rays_dev;
+    int geo_V = 0, geo_D = 0;
+    double geo_h = 0.0;
+    int fwd3t = 0, fwd3t_req = 0;
+    DBuf<int> t3flag;
+    const void* t3_ptr = nullptr;           // tensor maps are encoded per (pointer, stride)
+    int t3_P = 0;
+    CUtensorMap t3_mx{}, t3_my{};
     double t_trace = 0.0;                   // WAMGPU_TRACE_HOST phase clock
     // fused back projection + all-reduce over NVLink peer memory (kernels_ar.cuh)
     struct {
@@ -518,6 +530,17 @@ static void check_flag(Ctx* c, const char* where) {
     int f = 0;
     CK(cudaMemcpyAsync(&f, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
+    if (c->fwd3t == 2) {
+        int t = 0;
+        CK(cudaMemcpyAsync(&t, c->t3flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        if (t) {
+            CK(cudaMemsetAsync(c->t3flag.p, 0, sizeof(int), c->st));
+            if (t & ~1) throw NumericError(std::string(where) + ": on-the-fly TMA forward: tile/ring error " +
+                                           std::to_string(t));
+            f |= 1;
+        }
+    }
     if (f) {
         CK(cudaMemsetAsync(c->flag.p, 0, sizeof(int), c->st));
         std::string what = std::string(where) + ": ";
@@ -697,10 +720,15 @@ static void set_geometry(Ctx* c, const wamgpu_geometry& g) {
     c->M = (uint64_t)g.views * g.detectors;
     c->N = (uint64_t)g.nx * g.ny;
     partition(c, g.views, g.detectors);
-    DBuf<RayDev> dr;
+    DBuf<RayDev>& dr = c->rays_dev;   // kept: the on-the-fly forward traces from it
     dr.alloc(std::max<uint64_t>(c->Ml, 1));
     if (c->Ml)
         CK(cudaMemcpyAsync(dr.p, rays.data() + c->row0, c->Ml * sizeof(RayDev), cudaMemcpyHostToDevice, c->st));
+    c->geo_D = g.detectors;
+    c->geo_V = (int)(c->Ml / (uint64_t)g.detectors);
+    c->geo_h = g.voxel_size;
+    c->fwd3t = (c->fwd3t_req && c->Ml == (uint64_t)c->geo_V * g.detectors) ? 1 : 0;
+    c->t3_ptr = nullptr;
     c->rp.alloc(c->Ml + 1);
     k_trace_count<<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(dr.p, c->Ml, g.nx, g.ny, g.voxel_size, c->rp.p);
     check_launch(c, "k_trace_count");
@@ -746,6 +774,7 @@ static void set_matrix_csr(Ctx* c, uint64_t rows, uint64_t cols, uint64_t nnz, c
     c->A.alloc_padded(std::max<uint64_t>(c->nnz, 1));
     CK(cudaMemcpyAsync(c->rp.p, lrp.data(), (c->Ml + 1) * 8, cudaMemcpyHostToDevice, c->st));
     if (c->nnz) CK(cudaMemcpyAsync(c->A.p, ent.data(), c->nnz * 8, cudaMemcpyHostToDevice, c->st));
+    c->rays_dev.release(); c->fwd3t = 0;   // explicit matrix: no ray table to trace from
     finish_matrix(c);
     build_tile_order(c);
 }
@@ -875,6 +904,7 @@ static void load_matrix_wamh(Ctx* c, const char* path) {
             CK(cudaMemcpy(c->C.p + o, ent.data(), 8 * n, cudaMemcpyHostToDevice));
         }
     }
+    c->rays_dev.release(); c->fwd3t = 0;   // explicit matrix: no ray table to trace from
     finish_matrix(c, use_csc);
     build_tile_order(c);
 }
@@ -1016,6 +1046,85 @@ static int forward_bands(Ctx* c) {
     return B;
 }
 
+
+// ---- on-the-fly 3D forward with TMA-staged tiles (kernels3t.cuh) ----------
+// The tensor maps describe the slab vector x[iy][ix][s] (fp32, slab stride P)
+// as a 3D tensor (s, ix, iy); boxes of 32 slices x T3_TW x T3_RB pixels for
+// x-major bundles and 32 x T3_RB x T3_TW for y-major ones.  The driver entry
+// point comes through the runtime (no libcuda link dependency).
+typedef CUresult (*PFN_tmEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_tmEncodeTiled tm_encode_fn() {
+    static PFN_tmEncodeTiled fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (PFN_tmEncodeTiled)p;
+    }();
+    return fn;
+}
+static bool t3_maps(Ctx* c, const float* x, int P) {
+    if (c->t3_ptr == x && c->t3_P == P) return true;
+    PFN_tmEncodeTiled enc = tm_encode_fn();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)P, (cuuint64_t)c->nx, (cuuint64_t)c->ny};
+    const cuuint64_t strides[2] = {(cuuint64_t)P * 4, (cuuint64_t)c->nx * P * 4};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const cuuint32_t bx[3] = {T3_ZB, T3_TW, T3_RB}, by[3] = {T3_ZB, T3_RB, T3_TW};
+    if (enc(&c->t3_mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), dims, strides, bx, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (enc(&c->t3_my, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), dims, strides, by, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    c->t3_ptr = x;
+    c->t3_P = P;
+    return true;
+}
+// returns the number of I-divergence partials (CTAs), 0 when the path is not taken
+template <int MODE>
+static unsigned fwd3t_launch(Ctx* c, const float* mu, double* l, bool nonneg) {
+    const int P = slab_stride(c);
+    if (c->fwd3t <= 0 || P < T3_ZB || !c->rays_dev.p || !c->Ml) return 0;
+    if (!t3_maps(c, mu, P)) { c->fwd3t = -1; return 0; }
+    const unsigned ncb = (c->geo_D + T3_CB - 1) / T3_CB, nvg = (c->geo_V + T3_VG - 1) / T3_VG;
+    const unsigned nzc = (c->nzl + T3_ZB - 1) / T3_ZB, nb = ncb * nvg * nzc;
+    if (MODE == 1) c->partial.ensure(nb);
+    T3Args a{c->rays_dev.p, c->geo_V, c->geo_D, c->nx, c->ny, c->nzl, P, c->geo_h,
+             c->I0.p, c->d.p, c->q.p, l, c->partial.p, c->t3flag.p};
+    const size_t smem = sizeof(T3Smem);
+    const bool uns = nonneg && c->slab_variant >= 100;
+    auto go = [&](auto kern) {
+        static bool attr = false;   // per instantiation
+        if (!attr) {
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        kern<<<nb, T3_RAYS, smem, c->st>>>(c->t3_mx, c->t3_my, a);
+    };
+    if (uns) go(k_fwd3t<MODE, 2, false>);
+    else go(k_fwd3t<MODE, 2, true>);
+    if (c->fwd3t == 1) {   // first launch for this geometry: did every bundle fit its boxes and rings?
+        int f = 0;
+        CK(cudaMemcpyAsync(&f, c->t3flag.p, 4, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        if (f & ~1) {
+            CK(cudaMemsetAsync(c->t3flag.p, 0, 4, c->st));
+            std::fprintf(stderr, "[wamgpu] on-the-fly TMA forward rejected for this geometry (flag 0x%x): "
+                                 "stored-H slab SpMM kept\n", f);
+            c->fwd3t = -1;
+            return 0;
+        }
+        c->fwd3t = 2;
+    }
+    return nb;
+}
+
 template <int MODE, int P>
 static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxblk, bool nonneg) {
     using S = SlabShape<P>;
@@ -1066,7 +1175,11 @@ static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxbl
 // update clamps at 0)
 template <int MODE>
 static unsigned fwd3_launch(Ctx* c, const float* mu, double* l, unsigned maxblk, bool nonneg) {
-    unsigned nb = 0;
+    unsigned nb = fwd3t_launch<MODE>(c, mu, l, nonneg);
+    if (nb) {
+        check_launch(c, "k_fwd3t");
+        return nb;
+    }
     switch (slab_stride(c)) {
         case 8: nb = fwd3_launch_p<MODE, 8>(c, mu, l, maxblk, nonneg); break;
         case 16: nb = fwd3_launch_p<MODE, 16>(c, mu, l, maxblk, nonneg); break;
@@ -2669,6 +2782,7 @@ static Ctx* create(int device) {
     if (const char* e = std::getenv("WAMGPU_WALK_VARIANT")) c->walk_variant = std::atoi(e);
     if (const char* e = std::getenv("WAMGPU_SLAB_VARIANT")) c->slab_variant = std::atoi(e);
     if (const char* e = std::getenv("WAMGPU_BACK_VARIANT")) c->back_variant = std::atoi(e);
+    if (const char* e = std::getenv("WAMGPU_FWD3T")) c->fwd3t_req = std::atoi(e);
     CK(cudaEventCreate(&c->ev_t0));
     CK(cudaEventCreate(&c->ev_a));
     CK(cudaEventCreate(&c->ev_b));
@@ -2677,6 +2791,8 @@ static Ctx* create(int device) {
     c->counters.alloc(2);
     c->scal.alloc(8);
     c->partial.alloc(1024);
+    c->t3flag.alloc(1);
+    CK(cudaMemsetAsync(c->t3flag.p, 0, 4, c->st));
     CK(cudaMemsetAsync(c->flag.p, 0, 4, c->st));
     CK(cudaMemsetAsync(c->counters.p, 0, 16, c->st));
     CK(cudaStreamSynchronize(c->st));
@@ -2836,6 +2952,21 @@ int wamgpu_set_partition(wamgpu_ctx* ctx, int view_groups) {
         if (view_groups < 0 || (view_groups > 0 && ctx->nranks % view_groups))
             throw ConfigError("set_partition: view groups must divide the rank count");
         ctx->vgroups_req = view_groups;
+    })
+}
+
+int wamgpu_set_projector(wamgpu_ctx* ctx, int kind) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (kind != 0 && kind != 1) throw ConfigError("set_projector: kind must be 0 (stored matrix) or 1 (on the fly)");
+        ctx->fwd3t_req = kind;
+        ctx->fwd3t = (kind && ctx->rays_dev.p && ctx->geo_D > 0 && ctx->Ml == (uint64_t)ctx->geo_V * ctx->geo_D) ? 1 : 0;
+    })
+}
+int wamgpu_get_projector(const wamgpu_ctx* ctx, int* state) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (state) *state = ctx->fwd3t;
     })
 }
 

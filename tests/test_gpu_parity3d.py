@@ -184,3 +184,35 @@ def test_banded_forward(wam, orc, name, monkeypatch):
     ro = p32.wam_run(cfg["J"], cfg["schedule"], 0.1)
     assert np.array_equal(t1, p32.wam_tree())
     assert rel_l2(o1, [x[1] for x in ro]) < TOL_MIRROR
+
+
+@pytest.mark.parametrize("name", ["tiny3d24", "small3d", "tiny3d64"])
+def test_on_the_fly_tma_forward(wam, orc, name):
+    """The on-the-fly 3D forward (kernels3t.cuh k_fwd3t: rays re-traced every
+    pass with the device Siddon tracer, image tiles staged by TMA, north_star
+    item (2)) against the stored-matrix slab SpMM and the oracle: the same fp32
+    h and the same ray-order fp64 sums, so line integrals are BIT-identical,
+    and so are q, mu and the tree of a separable-Haar WAM run (only the order
+    of the objective's partial sums differs).  Ragged bundles: 60 / 72 views
+    (groups of 8), 96 channels (groups of 64), 24 / 40 slices (chunks of 32)."""
+    cfg, p32, mu_true, I0, d = problem_inputs(name, orc, wam, mirror=True)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(mu_true.size).astype(np.float32).astype(np.float64)   # signed values
+    out = {}
+    for kind in (0, 1):
+        c = _ctx(wam, cfg)
+        c.set_projector(kind)
+        l, lx = c.forward_project(mu_true), c.forward_project(x)
+        assert c.projector() == (2 if kind else 0), "on-the-fly projector rejected its bundle geometry"
+        c.set_haar_dim(3)
+        c.set_data(d, I0)
+        c.wam_init(cfg["L"])
+        r = c.wam_run(cfg["J"], cfg["schedule"], 0.1)
+        out[kind] = (l, lx, [v["objective"] for v in r], c.tree(), c.image(), c.q())
+        assert c.projector() == (2 if kind else 0)
+        c.close()
+    (l0, x0, o0, t0, m0, q0), (l1, x1, o1, t1, m1, q1) = out[0], out[1]
+    assert np.array_equal(l1, l0) and np.array_equal(x1, x0)
+    assert rel_l2(l1, p32.forward_project(mu_true.astype(np.float32).astype(np.float64))) < 1e-14
+    assert np.array_equal(t1, t0) and np.array_equal(m1, m0) and np.array_equal(q1, q0)
+    assert rel_l2(o1, o0) < 1e-13
