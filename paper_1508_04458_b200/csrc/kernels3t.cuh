@@ -8,7 +8,7 @@
 // Why tiles: the slab SpMM gathers every (entry, slice) value from L1/L2 and
 // moves 2.4 B per ray-voxel update from L2 (ncu, cfg4: 579 GB per launch =
 // 9.4 TB/s, ~80% of the ~6300 B/clk L2 cap): it is L2-bandwidth-bound.  Here a
-// CTA owns a BUNDLE of T3_VG adjacent views x T3_CB adjacent channels (512
+// CTA owns a BUNDLE of 512/CB adjacent views x CB adjacent channels (512
 // rays that cross the same image strip) for one chunk of 32 slices and marches
 // along the bundle's major axis in steps of T3_TW pixels.  For every step one
 // elected thread issues the TMA loads of the [minor rows x T3_TW columns x 32
@@ -28,9 +28,7 @@
 
 namespace wamgpu {
 
-constexpr int T3_VG = 8;      // views per bundle
-constexpr int T3_CB = 64;     // channels per bundle
-constexpr int T3_RAYS = T3_VG * T3_CB;
+constexpr int T3_RAYS = 512;  // rays (threads) per bundle: CB adjacent channels x 512/CB adjacent views
 constexpr int T3_TW = 4;      // major-axis pixels per step
 constexpr int T3_ZB = 32;     // slices per CTA
 constexpr int T3_RB = 32;     // minor-axis pixels per TMA box
@@ -42,9 +40,10 @@ constexpr int T3_WARPS = T3_RAYS / 32;
 
 struct T3Smem {
     float buf[2][T3_BUFPIX][T3_ZB];          // 2 x 80 KB, TMA destinations
-    uint2 ring[T3_CAP][T3_RAYS];             // (tile pixel, h bits) per ray per step
+    uint2 ring[T3_CAP][T3_RAYS];             // per ray per step: x = byte offset of the tile pixel | low 3 h bits << 29,
+                                             //                   y = high word of double(h * 2^896)
     int cnt[T3_RAYS];
-    double oray[2 * T3_VG][4];               // outer rays (ox, oy, dx, dy) of every view
+    double oray[32][4];                      // outer rays (ox, oy, dx, dy) of every view (<= 16 views)
     unsigned long long full[2], empty[2];    // mbarriers
     int hdr[2][4];                           // per buffer: minor origin, major origin, boxes
     int kmin, kmax, nalive;
@@ -52,7 +51,7 @@ struct T3Smem {
 };
 
 // error bits raised in flag (the host then keeps the stored-H slab SpMM):
-//   0x100 box taller than T3_NBOX*T3_RB   0x200 ring overflow / direction mismatch
+//   0x100 box taller than T3_NBOX*T3_RB   0x200 ray against the bundle's march direction
 //   0x400 entry outside the staged box    0x800 ray alive after the march / barrier timeout
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned n) {
@@ -147,22 +146,28 @@ struct T3Args {
 };
 
 // MODE 0: l (fp64) out; MODE 1: q = fp32(I0 exp(-l)) + I-divergence partial per CTA.
-// NF of every 4 conversions by F2F, the rest by the exact bit move (kernels3d.cuh).
-template <int MODE, int NF, bool SIGNED>
+// NF of every 4 slab values are converted by F2F, the rest by the exact bit
+// move (kernels3d.cuh f2d_scaled); h never takes a conversion: the tracer
+// stores the words of double(h * 2^896) (h = fp32(len) is a positive normal
+// float: high word (bits >> 3) + (1792 << 20), low word bits << 29).
+// CB channels x VG = 512/CB views per bundle.
+template <int MODE, int NF, bool SIGNED, int CB>
 __global__ void __launch_bounds__(T3_RAYS, 1) k_fwd3t(const __grid_constant__ CUtensorMap tmx,
                                                       const __grid_constant__ CUtensorMap tmy, T3Args a) {
+    constexpr int VG = T3_RAYS / CB;
+    static_assert(VG >= 1 && 2 * VG <= 32, "bundle shape");
     extern __shared__ __align__(128) unsigned char t3_raw[];
     T3Smem& S = *reinterpret_cast<T3Smem*>(t3_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int ncb = (a.D + T3_CB - 1) / T3_CB, nvg = (a.V + T3_VG - 1) / T3_VG;
+    const int ncb = (a.D + CB - 1) / CB, nvg = (a.V + VG - 1) / VG;
     const int cbn = blockIdx.x % ncb, vg = (blockIdx.x / ncb) % nvg, zc = blockIdx.x / (ncb * nvg);
-    const int s0 = zc * T3_ZB, v0 = vg * T3_VG, c0 = cbn * T3_CB;
-    const int vi = tid / T3_CB, ci = tid % T3_CB;
+    const int s0 = zc * T3_ZB, v0 = vg * VG, c0 = cbn * CB;
+    const int vi = tid / CB, ci = tid % CB;
     const bool valid = v0 + vi < a.V && c0 + ci < a.D;
     const uint64_t y = (uint64_t)(v0 + vi) * a.D + (c0 + ci);
 
     // bundle major axis and direction from its central ray
-    const RayDev rc = a.rays[(uint64_t)min(v0 + T3_VG / 2, a.V - 1) * a.D + min(c0 + T3_CB / 2, a.D - 1)];
+    const RayDev rc = a.rays[(uint64_t)min(v0 + VG / 2, a.V - 1) * a.D + min(c0 + CB / 2, a.D - 1)];
     const bool xmaj = fabs(rc.dx) >= fabs(rc.dy);
     const int smaj = (xmaj ? rc.dx : rc.dy) > 0.0 ? 1 : -1;
     const int nmaj = xmaj ? a.nx : a.ny, nmin = xmaj ? a.ny : a.nx;
@@ -175,8 +180,8 @@ __global__ void __launch_bounds__(T3_RAYS, 1) k_fwd3t(const __grid_constant__ CU
         mbar_init(&S.empty[0], T3_WARPS); mbar_init(&S.empty[1], T3_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < 2 * T3_VG) {   // outer rays of every view of the bundle
-        const int vv = min(v0 + (tid >> 1), a.V - 1), cc = (tid & 1) ? min(c0 + T3_CB - 1, a.D - 1) : c0;
+    if (tid < 2 * VG) {   // outer rays of every view of the bundle
+        const int vv = min(v0 + (tid >> 1), a.V - 1), cc = (tid & 1) ? min(c0 + CB - 1, a.D - 1) : c0;
         const RayDev r = a.rays[(uint64_t)vv * a.D + cc];
         S.oray[tid][0] = r.ox; S.oray[tid][1] = r.oy; S.oray[tid][2] = r.dx; S.oray[tid][3] = r.dy;
     }
@@ -208,12 +213,13 @@ __global__ void __launch_bounds__(T3_RAYS, 1) k_fwd3t(const __grid_constant__ CU
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[g][j] = 0.0;
 
-    // producer (warp 0): box of step k into buffer b; lane l evaluates outer ray
-    // l>>1 at the step's entry (l&1 = 0) ... both planes by every lane pair
+    // producer (warp 0): box of step k into buffer b.  Lane l < 2 VG holds an
+    // outer ray (first / last channel of view l >> 1) and evaluates it at the
+    // two planes bounding the step; the box is the min/max over them +- 1.
     auto produce = [&](int k, int b) {
         const int ma = smaj > 0 ? k * T3_TW : nmaj - (k + 1) * T3_TW;   // lowest real major index of the step
         int lo = 1 << 30, hi = -(1 << 30);
-        if (lane < 2 * T3_VG) {
+        if (lane < 2 * VG) {
             const double ox = S.oray[lane][0], oy = S.oray[lane][1], dx = S.oray[lane][2], dy = S.oray[lane][3];
 #pragma unroll
             for (int pl = 0; pl < 2; ++pl) {
@@ -256,15 +262,20 @@ __global__ void __launch_bounds__(T3_RAYS, 1) k_fwd3t(const __grid_constant__ CU
             const unsigned ph = (unsigned)((k - kmin) >> 1) & 1u;
             if (!mbar_wait(&S.full[b], ph)) atomicOr(a.flag, 0x800);
             const int lo = S.hdr[b][0], ma = S.hdr[b][1], nb = S.hdr[b][2];
-            // ---- trace this ray through the step's columns
-            int n = 0;
-            {
-                const int mend = (k + 1) * T3_TW;
+            // ---- trace this ray through the step's columns, at most T3_CAP
+            // cells per round (steep rays of wide bundles take several rounds),
+            // then consume the warp's 32 rings
+            const unsigned char* bb = reinterpret_cast<const unsigned char*>(&S.buf[b][0][0]) + lig * 16;
+            const int mend = (k + 1) * T3_TW;
+            bool more;
+            do {
+                int n = 0;
+                bool pend = false;
                 while (tr.alive) {
                     const int cm = xmaj ? tr.ix : tr.iy;
                     const int m = smaj > 0 ? cm : nmaj - 1 - cm;
                     if (m >= mend) break;
-                    if (n >= T3_CAP) { atomicOr(a.flag, 0x200); break; }
+                    if (n >= T3_CAP) { pend = true; break; }
                     int cx, cy;
                     const double len = tr.next(a.nx, a.ny, cx, cy);
                     if (len > 0.0) {
@@ -272,34 +283,43 @@ __global__ void __launch_bounds__(T3_RAYS, 1) k_fwd3t(const __grid_constant__ CU
                         unsigned pix;
                         if (xmaj) pix = (unsigned)(mi * T3_TW + mj);
                         else pix = (unsigned)((mi >> 5) * T3_BOXPIX + mj * T3_RB + (mi & 31));
-                        if (mi < 0 || mi >= nb * T3_RB || mj < 0 || mj >= T3_TW) { atomicOr(a.flag, 0x400); pix = 0; }
-                        S.ring[n][tid] = make_uint2(pix, __float_as_uint((float)len));
+                        const unsigned hb = __float_as_uint((float)len);
+                        if (mi < 0 || mi >= nb * T3_RB || mj < 0 || mj >= T3_TW || (hb >> 23) == 0u) {
+                            if (hb) atomicOr(a.flag, 0x400);   // outside the box, or a denormal h (h = 0 adds nothing)
+                            continue;
+                        }
+                        S.ring[n][tid] = make_uint2((pix * (unsigned)(T3_ZB * 4)) | (hb << 29), (hb >> 3) + 0x70000000u);
                         ++n;
                     }
                 }
                 S.cnt[tid] = n;
-            }
-            __syncwarp();
-            // ---- consume: 8 groups of 4 rays, 8 lanes x 4 slices per ray
-            const float* bb = &S.buf[b][0][0] + lig * 4;
+                more = __any_sync(0xffffffffu, pend);
+                __syncwarp();
+                // 8 groups of 4 rays, 8 lanes x 4 slices per ray; the ring entry two
+                // turns ahead and the slab values one turn ahead are in flight
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                const int rl = w * 32 + g * 4 + sub;
-                const int ne = S.cnt[rl];
-                for (int e = 0; e < ne; ++e) {
-                    const uint2 en = S.ring[e][rl];
-                    const float4 m4 = *reinterpret_cast<const float4*>(bb + (size_t)en.x * T3_ZB);
-                    const double hh = (double)__uint_as_float(en.y);
-                    const double hs = hh * kTwo896;
-                    const float f[4] = {m4.x, m4.y, m4.z, m4.w};
+                for (int g = 0; g < 8; ++g) {
+                    const int rl = w * 32 + g * 4 + sub;
+                    const int ne = S.cnt[rl];
+                    uint2 e0 = S.ring[0][rl], e1 = S.ring[1][rl];
+                    float4 mc = *reinterpret_cast<const float4*>(bb + (e0.x & 0x1ff80u));
+                    for (int e = 0; e < ne; ++e) {
+                        const float4 mn = *reinterpret_cast<const float4*>(bb + (e1.x & 0x1ff80u));
+                        const uint2 e2 = S.ring[min(e + 2, T3_CAP - 1)][rl];
+                        const int lw = (int)(e0.x & 0xe0000000u);
+                        const double hs = __hiloint2double((int)e0.y, lw);
+                        const double hh = __hiloint2double((int)(e0.y - 0x38000000u), lw);
+                        const float f[4] = {mc.x, mc.y, mc.z, mc.w};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        if (j < NF) acc[g][j] = fma(hh, (double)f[j], acc[g][j]);
-                        else acc[g][j] = fma(hs, f2d_scaled<SIGNED>(f[j]), acc[g][j]);
+                        for (int j = 0; j < 4; ++j) {
+                            if (j < NF) acc[g][j] = fma(hh, (double)f[j], acc[g][j]);
+                            else acc[g][j] = fma(hs, f2d_scaled<SIGNED>(f[j]), acc[g][j]);
+                        }
+                        e0 = e1; e1 = e2; mc = mn;
                     }
                 }
-            }
-            __syncwarp();
+                __syncwarp();
+            } while (more);
             if (lane == 0) mbar_arrive(&S.empty[b]);
             if (w == 0 && k + 2 <= kmax) {
                 if (!mbar_wait(&S.empty[b], ph)) atomicOr(a.flag, 0x800);
@@ -316,7 +336,7 @@ __global__ void __launch_bounds__(T3_RAYS, 1) k_fwd3t(const __grid_constant__ CU
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
             const int rl = w * 32 + g * 4 + sub;
-            const int rv = v0 + rl / T3_CB, rch = c0 + rl % T3_CB;
+            const int rv = v0 + rl / CB, rch = c0 + rl % CB;
             if (rv >= a.V || rch >= a.D) continue;
             const uint64_t yy = (uint64_t)rv * a.D + rch;
 #pragma unroll

@@ -212,7 +212,7 @@ struct wamgpu_ctx {
     DBuf<wamgpu::RayDev> rays_dev;
     int geo_V = 0, geo_D = 0;
     double geo_h = 0.0;
-    int fwd3t = 0, fwd3t_req = 0;
+    int fwd3t = 0, fwd3t_req = 0, t3_cb = 64;
     DBuf<int> t3flag;
     const void* t3_ptr = nullptr;           // tensor maps are encoded per (pointer, stride)
     int t3_P = 0;
@@ -728,6 +728,7 @@ static void set_geometry(Ctx* c, const wamgpu_geometry& g) {
     c->geo_V = (int)(c->Ml / (uint64_t)g.detectors);
     c->geo_h = g.voxel_size;
     c->fwd3t = (c->fwd3t_req && c->Ml == (uint64_t)c->geo_V * g.detectors) ? 1 : 0;
+    c->t3_cb = 64;
     c->t3_ptr = nullptr;
     c->rp.alloc(c->Ml + 1);
     k_trace_count<<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(dr.p, c->Ml, g.nx, g.ny, g.voxel_size, c->rp.p);
@@ -1086,43 +1087,61 @@ static bool t3_maps(Ctx* c, const float* x, int P) {
     c->t3_P = P;
     return true;
 }
-// returns the number of I-divergence partials (CTAs), 0 when the path is not taken
+// returns the number of I-divergence partials (CTAs), 0 when the path is not taken.
+// Bundle shape: 64 channels x 8 views, or 32 x 16 when the first launch finds a
+// 64-channel bundle taller than its tile buffer (wide fans); WAMGPU_FWD3T_NF:
+// F2F share of the slab-value conversions (of 4; default 1).
+template <int MODE, int NF, int CB>
+static void fwd3t_go(Ctx* c, unsigned nb, const T3Args& a, bool uns) {
+    static bool attr = false;   // per (MODE, NF, CB)
+    if (!attr) {
+        CK(cudaFuncSetAttribute(k_fwd3t<MODE, NF, false, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(T3Smem)));
+        CK(cudaFuncSetAttribute(k_fwd3t<MODE, NF, true, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(T3Smem)));
+        attr = true;
+    }
+    if (uns) k_fwd3t<MODE, NF, false, CB><<<nb, T3_RAYS, sizeof(T3Smem), c->st>>>(c->t3_mx, c->t3_my, a);
+    else k_fwd3t<MODE, NF, true, CB><<<nb, T3_RAYS, sizeof(T3Smem), c->st>>>(c->t3_mx, c->t3_my, a);
+}
 template <int MODE>
 static unsigned fwd3t_launch(Ctx* c, const float* mu, double* l, bool nonneg) {
     const int P = slab_stride(c);
     if (c->fwd3t <= 0 || P < T3_ZB || !c->rays_dev.p || !c->Ml) return 0;
     if (!t3_maps(c, mu, P)) { c->fwd3t = -1; return 0; }
-    const unsigned ncb = (c->geo_D + T3_CB - 1) / T3_CB, nvg = (c->geo_V + T3_VG - 1) / T3_VG;
-    const unsigned nzc = (c->nzl + T3_ZB - 1) / T3_ZB, nb = ncb * nvg * nzc;
-    if (MODE == 1) c->partial.ensure(nb);
-    T3Args a{c->rays_dev.p, c->geo_V, c->geo_D, c->nx, c->ny, c->nzl, P, c->geo_h,
-             c->I0.p, c->d.p, c->q.p, l, c->partial.p, c->t3flag.p};
-    const size_t smem = sizeof(T3Smem);
     const bool uns = nonneg && c->slab_variant >= 100;
-    auto go = [&](auto kern) {
-        static bool attr = false;   // per instantiation
-        if (!attr) {
-            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
+    static const int nf = [] { const char* e = std::getenv("WAMGPU_FWD3T_NF"); return e ? std::atoi(e) : 1; }();
+    for (;;) {
+        const int CB = c->t3_cb, VG = T3_RAYS / CB;
+        const unsigned ncb = (c->geo_D + CB - 1) / CB, nvg = (c->geo_V + VG - 1) / VG;
+        const unsigned nzc = (c->nzl + T3_ZB - 1) / T3_ZB, nb = ncb * nvg * nzc;
+        if (MODE == 1) c->partial.ensure(nb);
+        T3Args a{c->rays_dev.p, c->geo_V, c->geo_D, c->nx, c->ny, c->nzl, P, c->geo_h,
+                 c->I0.p, c->d.p, c->q.p, l, c->partial.p, c->t3flag.p};
+#define T3GO(NFv)                                                          \
+    {                                                                      \
+        if (CB == 64) fwd3t_go<MODE, NFv, 64>(c, nb, a, uns);              \
+        else fwd3t_go<MODE, NFv, 32>(c, nb, a, uns);                       \
+    }
+        switch (nf) {
+            case 0: T3GO(0) break;
+            case 2: T3GO(2) break;
+            default: T3GO(1) break;
         }
-        kern<<<nb, T3_RAYS, smem, c->st>>>(c->t3_mx, c->t3_my, a);
-    };
-    if (uns) go(k_fwd3t<MODE, 2, false>);
-    else go(k_fwd3t<MODE, 2, true>);
-    if (c->fwd3t == 1) {   // first launch for this geometry: did every bundle fit its boxes and rings?
+#undef T3GO
+        if (c->fwd3t == 2) return nb;
+        // first launch for this geometry: did every bundle fit its boxes?
         int f = 0;
         CK(cudaMemcpyAsync(&f, c->t3flag.p, 4, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
-        if (f & ~1) {
-            CK(cudaMemsetAsync(c->t3flag.p, 0, 4, c->st));
-            std::fprintf(stderr, "[wamgpu] on-the-fly TMA forward rejected for this geometry (flag 0x%x): "
-                                 "stored-H slab SpMM kept\n", f);
-            c->fwd3t = -1;
-            return 0;
-        }
-        c->fwd3t = 2;
+        if (!(f & ~1)) { c->fwd3t = 2; return nb; }
+        CK(cudaMemsetAsync(c->t3flag.p, 0, 4, c->st));
+        if (CB == 64 && (f & 0x100)) { c->t3_cb = 32; continue; }   // box too tall (entries then fall outside it): narrower bundles
+        std::fprintf(stderr, "[wamgpu] on-the-fly TMA forward rejected for this geometry (flag 0x%x, %d-channel "
+                             "bundles): stored-H slab SpMM kept\n", f, CB);
+        c->fwd3t = -1;
+        return 0;
     }
-    return nb;
 }
 
 template <int MODE, int P>

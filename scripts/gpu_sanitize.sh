@@ -6,7 +6,7 @@ sel="tests/test_gpu_parity.py::test_wam_parity_tree_bit_exact[tiny] tests/test_g
 tests/test_gpu_parity.py::test_root_only_iterations_use_phi_a tests/test_gpu_parity3d.py::test_wam3d_parity_tree_bit_exact[tiny3d] \
 tests/test_gpu_parity3d.py::test_am3d_parity[tiny3d] tests/test_gpu_parity3d.py::test_wam3d_separable_haar_parity[tiny3d16] \
 tests/test_gpu_fused_ar.py::test_fused_allreduce_protocol[257-2] tests/test_gpu_fused_ar.py::test_fused_allreduce_protocol[4103-4] \
-tests/test_gpu_fused_ar.py::test_fused_back_producer_shards"
+tests/test_gpu_fused_ar.py::test_fused_back_producer_shards tests/test_gpu_parity3d.py::test_on_the_fly_tma_forward[tiny3d24]"
 extra=""
 [ "$tool" = "memcheck" ] && extra="--leak-check no"
 [ "$tool" = "initcheck" ] && extra="--track-unused-memory no"
