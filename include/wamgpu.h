@@ -116,6 +116,14 @@ int wamgpu_set_partition(wamgpu_ctx* ctx, int view_groups);
 int wamgpu_get_partition(const wamgpu_ctx* ctx, int* view_groups, int* z_groups, int* slab_begin,
                          int* slab_slices);
 
+/* Debug (WAMGPU_GUARD=1 in the environment before the first allocation): every
+ * device allocation carries 256-byte guard bands and a NaN-filled body; this
+ * call checks the bands of all live allocations of the process (checked = how
+ * many, bad = how many were overwritten; wamgpu_last_error(NULL) names the
+ * first).  Without WAMGPU_GUARD both are 0.  The library's own stand-in for
+ * compute-sanitizer memcheck / initcheck where that tool is unavailable. */
+int wamgpu_debug_guards(uint64_t* checked, uint64_t* bad);
+
 /* 3D forward projector of an axial stack: kind 0 = slab SpMM over
  * the stored in-plane matrix (projector.hpp:123-148 built once, read per pass);
  * kind 1 = on the fly: every pass re-traces the rays (projector.hpp:52-119 on

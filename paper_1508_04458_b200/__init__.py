@@ -62,7 +62,7 @@ EXPORTED = [
     "wamgpu_p2p_export", "wamgpu_p2p_import", "wamgpu_selftest_fused_allreduce", "wamgpu_selftest_fused_back",
     "wamgpu_set_comm_local", "wamgpu_set_partition", "wamgpu_get_partition", "wamgpu_wam_expand_with", "wamgpu_simulate_device",
     "wamgpu_load_matrix_wamh", "wamgpu_save_matrix_wamh", "wamgpu_plan_partition",
-    "wamgpu_set_projector", "wamgpu_get_projector",
+    "wamgpu_set_projector", "wamgpu_get_projector", "wamgpu_debug_guards",
 ]
 P2P_BLOB = 256   # WAMGPU_P2P_BLOB
 
@@ -94,6 +94,14 @@ class Plan(C.Structure):
 
     def asdict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+def debug_guards():
+    """(checked, bad, message): guard bands of every live device allocation
+    (WAMGPU_GUARD=1 must be in the environment before the library allocates)."""
+    n, b = C.c_uint64(), C.c_uint64()
+    _chk(load().wamgpu_debug_guards(C.byref(n), C.byref(b)), None)
+    return n.value, b.value, (load().wamgpu_last_error(None).decode() if b.value else "")
 
 
 def plan_partition(g, rank, nranks, view_groups=0, algo="wam", haar_dim=3, levels=0):

@@ -51,6 +51,73 @@ namespace wamgpu {
         if (r_ != ncclSuccess) throw CudaError(std::string(#x) + ": " + ncclGetErrorString(r_)); \
     } while (0)
 
+// ---- guard bands (WAMGPU_GUARD=1, debug).  compute-sanitizer is closed on the
+// GPU pool this was developed on (profiles/r06/sanitizer_memcheck_closed.log),
+// so the library carries its own write-overrun and uninitialised-read check:
+// every device allocation gets a 256-byte band of 0xA5 on both sides and its
+// body is filled with 0xFF (NaN as fp32/fp64: a value read before it is written
+// poisons the results and trips the NumericError flags / parity tests);
+// wamgpu_debug_guards() verifies every live allocation's bands.
+constexpr size_t kGuard = 256;
+struct GuardReg {
+    std::mutex m;
+    std::map<void*, size_t> live;   // user pointer -> user bytes
+};
+static GuardReg& guard_reg() { static GuardReg g; return g; }
+static bool guard_on() {
+    static const bool on = [] { const char* e = std::getenv("WAMGPU_GUARD"); return e && std::atoi(e) != 0; }();
+    return on;
+}
+static void* dev_malloc(size_t bytes) {
+    void* p = nullptr;
+    if (!guard_on()) { CK(cudaMalloc(&p, bytes)); return p; }
+    char* raw = nullptr;
+    CK(cudaMalloc(&raw, bytes + 2 * kGuard));
+    CK(cudaMemset(raw, 0xA5, kGuard));
+    CK(cudaMemset(raw + kGuard, 0xFF, bytes));
+    CK(cudaMemset(raw + kGuard + bytes, 0xA5, kGuard));
+    // the fills run on the default stream, asynchronously to the host and
+    // unordered against the contexts' non-blocking streams: finish them before
+    // anyone writes real data into the body
+    CK(cudaStreamSynchronize(nullptr));
+    p = raw + kGuard;
+    std::lock_guard<std::mutex> l(guard_reg().m);
+    guard_reg().live[p] = bytes;
+    return p;
+}
+static void dev_free(void* p) {
+    if (!guard_on()) { cudaFree(p); return; }
+    {
+        std::lock_guard<std::mutex> l(guard_reg().m);
+        guard_reg().live.erase(p);
+    }
+    cudaFree(static_cast<char*>(p) - kGuard);
+}
+// (checked, bad): every live allocation's two bands compared with 0xA5
+static std::pair<uint64_t, uint64_t> check_guards(std::string* first_bad) {
+    uint64_t n = 0, bad = 0;
+    if (!guard_on()) return {0, 0};
+    CK(cudaDeviceSynchronize());
+    std::lock_guard<std::mutex> l(guard_reg().m);
+    std::vector<unsigned char> h(2 * kGuard);
+    for (auto& kv : guard_reg().live) {
+        char* u = static_cast<char*>(kv.first);
+        CK(cudaMemcpy(h.data(), u - kGuard, kGuard, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(h.data() + kGuard, u + kv.second, kGuard, cudaMemcpyDeviceToHost));
+        ++n;
+        for (size_t i = 0; i < 2 * kGuard; ++i)
+            if (h[i] != 0xA5) {
+                ++bad;
+                if (first_bad && first_bad->empty())
+                    *first_bad = "allocation of " + std::to_string(kv.second) + " bytes: " +
+                                 (i < kGuard ? "byte " + std::to_string((long)i - (long)kGuard) + " before its start"
+                                             : "byte " + std::to_string(i - kGuard) + " past its end") + " overwritten";
+                break;
+            }
+    }
+    return {n, bad};
+}
+
 template <class T>
 struct DBuf {
     T* p = nullptr;
@@ -61,7 +128,7 @@ struct DBuf {
     ~DBuf() { release(); }
     void alloc(size_t n_) {
         release();
-        if (n_) CK(cudaMalloc(&p, n_ * sizeof(T)));
+        if (n_) p = static_cast<T*>(dev_malloc(n_ * sizeof(T)));
         n = n_;
     }
     void ensure(size_t n_) { if (n < n_) alloc(n_); }
@@ -69,7 +136,7 @@ struct DBuf {
     // loads just past the logical end stay inside the allocation
     void alloc_padded(size_t n_) { alloc(n_ + 64); n = n_ + 64; }
     void ensure_padded(size_t n_) { if (n < n_ + 64) alloc_padded(n_); }
-    void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+    void release() { if (p) dev_free(p); p = nullptr; n = 0; }
     void swap(DBuf& o) { std::swap(p, o.p); std::swap(n, o.n); }
 };
 
@@ -2971,6 +3038,17 @@ int wamgpu_set_partition(wamgpu_ctx* ctx, int view_groups) {
         if (view_groups < 0 || (view_groups > 0 && ctx->nranks % view_groups))
             throw ConfigError("set_partition: view groups must divide the rank count");
         ctx->vgroups_req = view_groups;
+    })
+}
+
+int wamgpu_debug_guards(uint64_t* checked, uint64_t* bad) {
+    const wamgpu_ctx* none = nullptr;
+    API_TRY(none, {
+        std::string what;
+        const auto r = wamgpu::check_guards(&what);
+        if (checked) *checked = r.first;
+        if (bad) *bad = r.second;
+        if (r.second) g_err = what;
     })
 }
 
