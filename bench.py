@@ -600,6 +600,11 @@ def main():
     d2h = 4 * img.size
 
     iters_per_s = J / (ms_step * 1e-3)
+    try:
+        import torch
+        ctx_sms = torch.cuda.get_device_properties(local).multi_processor_count
+    except Exception:
+        ctx_sms = 148
     line = None
     if rank == 0:
         hbm, peak_kind = _peaks()
@@ -621,8 +626,11 @@ def main():
         fwd_gbs = fwd_bytes / (fwd_avg * 1e-3) / 1e9
         back_gbs = back_bytes / (back_avg * 1e-3) / 1e9
         fwd_name = ("k_fwd_patch<1,4,8,5> (K2 CSR forward + Beer + I-div, 4 rays/warp)" if nz == 1 else
-                    "k_forward3<1> (K2' slab forward + Beer + I-div)")
-        back_name = "k_back<1,12,1> (K3 CSC back projection)" if nz == 1 else "k_back3 (K3' slab back projection)"
+                    "k_fwd3s / k_fwd3s_band<1,...> (K2' slab forward over the in-plane matrix + Beer + I-div; "
+                    "banded when the mu slab exceeds L2)")
+        back_name = ("k_back<0,12,1> (K3 CSC back projection)" if nz == 1 and algo == "wam" else
+                     "k_back<1,12,1> (K3 CSC back projection + AM update)" if nz == 1 else
+                     "k_back3s<...> (K3' slab back projection over the in-plane CSC)")
         dom = fwd_name if sum(fwd_ms) >= sum(back_ms) else back_name
         ach = fwd_gbs if sum(fwd_ms) >= sum(back_ms) else back_gbs
         traffic = None
@@ -632,6 +640,23 @@ def main():
             traffic = tr.get(cfg["name"], {}).get("k_forward" if "forward" in dom else "k_back")
         except Exception:
             pass
+        # 3D: the slab passes are not HBM-bound (one DFMA + one fp32->fp64
+        # conversion per ray-voxel update from L1/L2-resident slabs, DESIGN.md
+        # §4.2): also report the dominant pass against the fp64-FMA issue peak
+        # (64 DFMA lanes per clock per SM at the SM clock sampled under load)
+        binding = None
+        clocks = clk.summary()
+        if nz > 1:
+            mhz = clocks.get("sm_mhz") or 1965.0
+            dom_ms = fwd_avg if sum(fwd_ms) >= sum(back_ms) else back_avg
+            upd = nnz_local * nz / (dom_ms * 1e-3)
+            peak_upd = ctx_sms * 64 * mhz * 1e6
+            binding = {"resource": "fp64 FMA issue (one DFMA + one fp32->fp64 conversion per ray-voxel update; "
+                                   "slab gathers served by L1/L2)",
+                       "achieved": upd, "peak": peak_upd, "unit": "ray-voxel updates/s", "frac": upd / peak_upd,
+                       "updates_per_clk_per_sm": upd / (ctx_sms * mhz * 1e6),
+                       "evidence": "profiles/r06/ncu_cfg4_pass.txt (issue, XU, fp64, L1/L2 shares of the banded "
+                                   "forward, the back projection and the split)"}
         cpu = None
         if world == 1 and not args.no_cpu_baseline and not args.shard:
             try:
@@ -666,7 +691,8 @@ def main():
             "parity": parity,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
-                         "algorithmic_bytes": fwd_bytes if "forward" in dom else back_bytes},
+                         "algorithmic_bytes": fwd_bytes if "forward" in dom else back_bytes,
+                         "binding": binding},
             "kernels": {"fwd_avg_ms": fwd_avg, "fwd_gbs": fwd_gbs, "fwd_frac": fwd_gbs / hbm,
                         "gather_gbs": (4 * nnz_local * nz / (fwd_avg * 1e-3) / 1e9) if nz > 1 else None,
                         "back_avg_ms": back_avg, "back_gbs": back_gbs, "back_frac": back_gbs / hbm,
@@ -678,7 +704,7 @@ def main():
             "e2e": {"value": J / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps},
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "wall_s_timed": wall,
             "cpu_baseline": cpu,
         }

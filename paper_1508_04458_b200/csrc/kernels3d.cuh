@@ -136,10 +136,18 @@ template <int G> struct SlabStage {
 // consumed (a loop-carried register set, so ptxas cannot sink them), and the
 // chunk after the current one is staged into the other smem buffer from
 // registers prefetched a whole chunk ahead.
-template <int LPR, int SPL, int U, int NF, bool SIGNED, int P>
+// UX >= 100 selects the ping-pong pipeline (U = UX % 100): two register sets of
+// gathered slab values alternate between "in flight" and "being consumed"
+// (the round loop is unrolled by two), and h is read from the staged chunk when
+// a round is consumed instead of travelling with the gathers.  The copy
+// pipeline below moves 40 registers per round (IMAD.MOV: 50 of the 185 SASS
+// instructions of a 32-DFMA round at P = 128).
+template <int LPR, int SPL, int UX, int NF, bool SIGNED, int P>
 __device__ __forceinline__ void slab_dot_g(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
                                            uint64_t hi, int maxlen, int lig, int g,
                                            SlabStage<32 / LPR>& st, double (&acc)[SPL]) {
+    constexpr bool PP = UX >= 100;
+    constexpr int U = UX % 100;
     constexpr int kSlabK = SlabStage<32 / LPR>::K, NL = kSlabK / LPR, RPC = kSlabK / U;
     static_assert(kSlabK % U == 0 && (U % 4 == 0 || U == 2) && NL >= 1, "unroll");
     using L = SlabLd<SPL>;
@@ -192,8 +200,59 @@ __device__ __forceinline__ void slab_dot_g(const uint2* __restrict__ A, const fl
     stage(0);
     if (kSlabK < maxlen) fetch(kSlabK);
     __syncwarp();
-    issue(0, 0);
     const int nr = (maxlen + U - 1) / U;
+    if constexpr (PP) {
+        static_assert(U % 4 == 0, "ping-pong rounds gather four entries per index load");
+        typename L::T va[U][L::NV], vb[U][L::NV];
+        auto gather = [&](typename L::T (&vv)[U][L::NV], int r) {   // round r's slab values
+            const int chunk = r / RPC, j0 = (r % RPC) * U;
+            if (j0 == 0 && r > 0) {   // first round of a new chunk: stage it, prefetch the one after
+                stage(chunk & 1);
+                if ((chunk + 1) * kSlabK < maxlen) fetch((chunk + 1) * kSlabK);
+                __syncwarp();
+            }
+            const unsigned* sc = st.c[chunk & 1][g];
+#pragma unroll
+            for (int u = 0; u < U; u += 4) {
+                const uint4 c4 = *reinterpret_cast<const uint4*>(sc + j0 + u);
+                slab_load<LPR, SPL>(xl + (uint64_t)c4.x * P, vv[u]);
+                slab_load<LPR, SPL>(xl + (uint64_t)c4.y * P, vv[u + 1]);
+                slab_load<LPR, SPL>(xl + (uint64_t)c4.z * P, vv[u + 2]);
+                slab_load<LPR, SPL>(xl + (uint64_t)c4.w * P, vv[u + 3]);
+            }
+        };
+        auto consume = [&](const typename L::T (&vv)[U][L::NV], int r) {
+            const int chunk = r / RPC, j0 = (r % RPC) * U;
+            const double* sh = st.h[chunk & 1][g] + j0;
+#pragma unroll
+            for (int u = 0; u < U; u += 2) {
+                const double2 h01 = *reinterpret_cast<const double2*>(sh + u);
+                const double hp[2] = {h01.x, h01.y};
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    float f[SPL];
+                    slab_unpack<SPL>(vv[u + k], f);
+                    const double hs = hp[k] * kTwo896;
+#pragma unroll
+                    for (int j = 0; j < SPL; ++j) {
+                        if ((((u + k) * SPL + j) & 3) < NF) acc[j] = fma(hp[k], (double)f[j], acc[j]);
+                        else acc[j] = fma(hs, f2d_scaled<SIGNED>(f[j]), acc[j]);
+                    }
+                }
+            }
+        };
+        gather(va, 0);
+        for (int r = 0; r < nr; r += 2) {
+            if (r + 1 < nr) gather(vb, r + 1);
+            consume(va, r);
+            if (r + 1 < nr) {
+                if (r + 2 < nr) gather(va, r + 2);
+                consume(vb, r + 1);
+            }
+        }
+        return;
+    }
+    issue(0, 0);
     // (an explicit two-set ping-pong without these copies was measured slower:
     // 156 registers uncapped, 8.77 vs 8.04 ms at cfg5 with a 128 cap)
     for (int r = 0; r < nr; ++r) {

@@ -709,7 +709,8 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
                                                    const unsigned* __restrict__ eray, const float4* __restrict__ epsi,
                                                    const float* __restrict__ q, const uint8_t* __restrict__ act,
                                                    ActOff off, ActOff koff, double* __restrict__ bm,
-                                                   TileMap tmap) {
+                                                   TileMap tmap, const unsigned long long* __restrict__ bptr,
+                                                   int B, int band) {
     constexpr int LPE = 32 / E, S = P * E / 32, NG = S / 2;
     static_assert(S >= 2 && S % 4 == 0, "slices per lane: a multiple of 4");
     __shared__ double red[4][7][P / 2];
@@ -725,7 +726,12 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
         for (int g = 0; g < NG; ++g)
 #pragma unroll
             for (int t = 0; t < 7; ++t) acc[g][t] = 0.0;
-        const uint64_t e0 = ptr[key], e1 = ptr[key + 1];
+        // banded (bptr != nullptr): this launch takes the key's entries whose
+        // rays lie in ray band `band` and ADDS their sums to what the earlier
+        // bands left in bm (fixed band order: deterministic)
+        const uint64_t e0 = bptr ? bptr[key * (uint64_t)(B + 1) + band] : ptr[key];
+        const uint64_t e1 = bptr ? bptr[key * (uint64_t)(B + 1) + band + 1] : ptr[key + 1];
+        if (band > 0 && e0 == e1) continue;   // nothing to add (uniform over the warp)
         unsigned yv[U];
         float4 ps[U];
         float4 qv[U][S / 4];
@@ -818,12 +824,38 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
             for (int t = 0; t < 7; ++t) {
                 double sum = 0.0;
                 for (int gg = g0; gg < g1; ++gg) sum += red[wib][t][gg];
-                bm[tmap.L ? coef_tile_pos(tmap, l, yy[t], xx[t], zz[t]) : ((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]] =
-                    sum;
+                double* o = bm + (tmap.L ? coef_tile_pos(tmap, l, yy[t], xx[t], zz[t])
+                                         : ((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]);
+                *o = band > 0 ? *o + sum : sum;
             }
         }
         __syncwarp();
     }
+}
+
+// Ray bands of the 3D split.  The split gathers one P*4-byte row of q per Psi
+// entry; a block's list holds every view, and the q slab outgrows L2 at the
+// BASELINE sizes (cfg4: 755 MB, so the final tree's 8.7e8 entries re-read
+// 444 GB from DRAM per split).  Cutting the rays into B bands whose q rows stay
+// L2-resident and running the split band by band turns that into L2 hits.
+// Lists are sorted by (key, ray), so a band is one contiguous range per key:
+// bptr[key*(B+1) + b] = first entry of `key` with ray >= b*rpb (b = B: its end).
+__global__ void k_split_band_ptr(uint64_t nkeys, const unsigned long long* __restrict__ ptr,
+                                 const unsigned* __restrict__ eray, int B, unsigned rpb,
+                                 unsigned long long* __restrict__ bptr) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nkeys * (uint64_t)(B + 1)) return;
+    const uint64_t key = i / (B + 1);
+    const int b = (int)(i % (B + 1));
+    uint64_t lo = ptr[key], hi = ptr[key + 1];
+    if (b == B) { bptr[i] = hi; return; }
+    const unsigned r0 = (unsigned)b * rpb;
+    while (lo < hi) {   // lower bound of r0
+        const uint64_t mid = (lo + hi) >> 1;
+        if (eray[mid] < r0) lo = mid + 1;
+        else hi = mid;
+    }
+    bptr[i] = lo;
 }
 
 }  // namespace wamgpu

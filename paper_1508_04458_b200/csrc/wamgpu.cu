@@ -272,6 +272,9 @@ struct wamgpu_ctx {
     int band_B = 0, band_hb = 0, band_P = 0;
     DBuf<unsigned> blo, bhi;
     DBuf<double> lacc;                      // running per-(ray, slice) sums between band launches
+    // ray bands of the separable-3D split (kernels3h.cuh k_split_band_ptr)
+    DBuf<unsigned long long> bptr3;
+    int sband_B = 1;
     bool mu_nonneg = false;                 // AM: mu has no sign bit set (see am_init)
     // on-the-fly 3D forward with TMA-staged image tiles (kernels3t.cuh): the
     // local ray table stays on the device; fwd3t: 0 off, 1 on (first launch
@@ -1050,7 +1053,14 @@ static unsigned nblk_warp(const Ctx* c, uint64_t n) {
 // conversion share NF (of 4 values, F2F; the rest by bit moves) of the v2
 // kernel:
 //   12 = NF 3 (default), 3 = NF 2, 8 = NF 0, 9 = NF 4, 11 = NF 1;
-//   1 = round-1 k_forward3/k_back3 (warp per ray, shuffles, F2F only; P >= 32).
+//   1 = round-1 k_forward3/k_back3 (warp per ray, shuffles, F2F only; P >= 32);
+//   17 / 18 = NF 3 / 2 with the ping-pong pipeline everywhere, 19 = NF 3 with
+//   the copy pipeline everywhere (the round-1 default).  The default runs the
+//   ping-pong pipeline (slab_dot_g UX = 104: two register sets, no per-round
+//   register copies) in the forward and the plain back projection and the copy
+//   pipeline in the fused AM update: cfg4 forward 71.1 -> 64.4, back 61.9 ->
+//   56.4 ms per pass; cfg3 8.33 -> 7.62 / 7.73 -> 7.31; cfg5 forward 8.07 ->
+//   7.35 but fused-update back 8.01 -> 8.52 (profiles/r06/pp_split_ab.txt).
 // Variant + 100 (default 112): the unsigned bit move for vectors known to be
 // non-negative.  cfg5 sweep (profiles/r02_slab_sweep.txt): 1 -> 11.3 ms per
 // pass, 9 -> 8.45, 12 -> 8.25, 112 -> 8.04 (forward) / 7.89 (back).  One launch
@@ -1074,7 +1084,10 @@ template <int P> struct SlabShape {
         case 14: X(3, 2, 4, 5) break;                                                                              \
         case 15: X(3, 4, 4, 1) break;                                                                              \
         case 16: X(3, 2, 4, 6) break;                                                                              \
-        default: X(3, 4, 8, 2) break;                                                                              \
+        case 17: X(3, 104, 8, 2) break;                                                                            \
+        case 18: X(2, 104, 8, 2) break;                                                                            \
+        case 19: X(3, 4, 8, 2) break;                                                                              \
+        default: X(3, DEFU, 8, 2) break;                                                                           \
     }
 // Bands of the 3D forward (k_fwd3s_band): only when the mu slab outgrows L2.
 // WAMGPU_FWD_BAND_MB (default 48; 0 = never): target mu bytes per band.
@@ -1230,16 +1243,15 @@ static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxbl
         // bands in fixed order; MODE 0 accumulates straight in l
         double* acc = MODE == 0 ? l : c->lacc.p;
         nb = std::min<unsigned>(nblk_warp(c, (c->Ml + S::G - 1) / S::G), maxblk);
+#define BAND(UXv, SG)                                                                                              \
+    k_fwd3s_band<MODE, S::LPR, S::SPL, UXv, 3, SG, P, 8, 2><<<nb, 256, 0, c->st>>>(                                \
+        c->Ml, c->nzl, b, B, c->rp.p, c->blo.p, c->bhi.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, acc, l,             \
+        c->partial.p, c->flag.p)
         for (int b = 0; b < B; ++b) {
-            if (uns)
-                k_fwd3s_band<MODE, S::LPR, S::SPL, 4, 3, false, P, 8, 2><<<nb, 256, 0, c->st>>>(
-                    c->Ml, c->nzl, b, B, c->rp.p, c->blo.p, c->bhi.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, acc, l,
-                    c->partial.p, c->flag.p);
-            else
-                k_fwd3s_band<MODE, S::LPR, S::SPL, 4, 3, true, P, 8, 2><<<nb, 256, 0, c->st>>>(
-                    c->Ml, c->nzl, b, B, c->rp.p, c->blo.p, c->bhi.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, acc, l,
-                    c->partial.p, c->flag.p);
+            if (v != 19) { if (uns) BAND(104, false); else BAND(104, true); }
+            else { if (uns) BAND(4, false); else BAND(4, true); }
         }
+#undef BAND
         launched(c, B - 1);
         return nb;
     }
@@ -1253,7 +1265,9 @@ static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxbl
             k_fwd3s<MODE, S::LPR, S::SPL, U, NF, true, P, WPB, MINB><<<nb, 32 * WPB, 0, c->st>>>(                  \
                 c->Ml, 0, c->nzl, c->rp.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, l, c->partial.p, c->flag.p);       \
     }
+#define DEFU 104
     SLAB_SWITCH(FX, v)
+#undef DEFU
 #undef FX
     return nb;
 }
@@ -1300,7 +1314,14 @@ static void back3_launch_p(Ctx* c, const float* w, double* out, const double* ba
             c->N, 0, c->nzl, c->order.p, c->cp.p, c->C.p, w, out, nullptr, nullptr, 0.0, c->flag.p, tm);           \
     }
 #define BX(NF, U, WPB, MINB) if (uns) { BX1(NF, U, WPB, MINB, false) } else { BX1(NF, U, WPB, MINB, true) }
-    SLAB_SWITCH(BX, v)
+    // default: ping-pong pipeline for the plain back projection; the fused AM update keeps the copy
+    // pipeline (cfg5: 8.52 vs 8.01 ms per pass with ping-pong)
+#define DEFU 104
+    if (!bam) { SLAB_SWITCH(BX, v) }
+#undef DEFU
+#define DEFU 4
+    if (bam) { SLAB_SWITCH(BX, v) }
+#undef DEFU
 #undef BX
 #undef BX1
 }
@@ -1695,6 +1716,27 @@ static void rebuild_psi3(Ctx* c, int nlev) {
     k_bounds<<<blocks_for(c->nkeys3 + 1, 256), 256, 0, c->st>>>(c->kout_s.p, tot, c->nkeys3, c->np.p);
     check_launch(c, "k_bounds");
     c->nnz_phi = tot;
+    // ray bands of the split (WAMGPU_SPLIT_BAND_MB; default 0 = off: measured no
+    // gain, cfg4 52.4-55.5 vs 53.0 ms per launch, profiles/r06/pp_split_ab.txt): only
+    // when the q slab outgrows L2
+    {
+        static const double mb = [] { const char* e = std::getenv("WAMGPU_SPLIT_BAND_MB"); return e ? std::atof(e) : 0.0; }();
+        const double row = (double)slab_stride(c) * 4.0, slab = row * (double)c->Ml;
+        int B = 1;
+        unsigned rpb = (unsigned)c->Ml;
+        if (mb > 0.0 && tot && slab > 2.0 * mb * 1048576.0) {
+            rpb = (unsigned)std::max(1.0, mb * 1048576.0 / row);
+            B = (int)((c->Ml + rpb - 1) / rpb);
+            if (B > 32) { B = 32; rpb = (unsigned)((c->Ml + B - 1) / B); B = (int)((c->Ml + rpb - 1) / rpb); }
+        }
+        c->sband_B = B;
+        if (B > 1) {
+            const uint64_t n = c->nkeys3 * (uint64_t)(B + 1);
+            c->bptr3.ensure(n);
+            k_split_band_ptr<<<blocks_for(n, 256), 256, 0, c->st>>>(c->nkeys3, c->np.p, c->E3ray.p, B, rpb, c->bptr3.p);
+            check_launch(c, "k_split_band_ptr");
+        }
+    }
     CK(cudaStreamSynchronize(c->st));
 }
 
@@ -2574,9 +2616,13 @@ static void wam_step(Ctx* c) {
 #define S3H(S) k_split3h<S><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p, c->E3ray.p, \
                                                    c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3, tm);
 #define S3E(S, EE) S3EU(S, EE, 2)
-#define S3EU(S, EE, UU) k_split3h_e<S, EE, UU><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl,  \
-                                                                     c->np.p, c->E3ray.p, c->E3psi.p, c->q.p,     \
-                                                                     c->act.p, c->off, c->koff, bm3, tm);
+#define S3EU(S, EE, UU)                                                                                            \
+    for (int sb_ = 0; sb_ < c->sband_B; ++sb_)                                                                     \
+        k_split3h_e<S, EE, UU><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p,        \
+                                                      c->E3ray.p, c->E3psi.p, c->q.p, c->act.p, c->off, c->koff,   \
+                                                      bm3, tm, c->sband_B > 1 ? c->bptr3.p : nullptr, c->sband_B,  \
+                                                      sb_);                                                        \
+    launched(c, c->sband_B - 1);
         const int P = slab_stride(c);
         if (c->split_variant == 1 && P >= 32) {
             switch (spl_of(c)) { case 1: S3H(1) break; case 2: S3H(2) break; default: S3H(4) break; }
