@@ -833,6 +833,143 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
     }
 }
 
+// ---- split, lane per ACTIVE z-block (default).  k_split3h_e spends the same
+// work on every z-block of a listed in-plane block, but at the BASELINE trees
+// only ~1/3 of them are active (cfg4 final tree: 6.3e6 of 1.7e7 level-1 blocks),
+// and it issues both products of every z-high coefficient although one of its
+// two multipliers is always zero.  Here the warp compacts the block's active
+// z-blocks from its z-bit words; lane j of an entry group owns the j-th active
+// z-block (and the (j+32)-th when more than 32 are active) and follows the
+// oracle's formulation (oracle/wam_oracle.cpp split3_mirror): per entry
+//   qlo / qhi = slice-order sums of q over the z-block's halves, qall = qlo + qhi,
+//   z-low  p in H,V,D:   acc += (p < 0 ? p : 0) * qall
+//   z-high p in A,H,V,D: acc += p < 0 ? p * qlo : -p * qhi        (p = psi c^l)
+// i.e. 7 FMAs per (entry, active z-block).  32/lpe entry groups run side by
+// side (lpe = lanes per entry = the active count rounded up to a power of two)
+// and are combined by a fixed xor butterfly.  psi is moved into fp64 by the
+// exact bit move (f2d_scaled, times cl * 2^896: bit-identical to (double)psi * cl).
+template <int LL>
+__device__ __forceinline__ void split3z_q(const float* __restrict__ qrow, int k, double& qlo, double& qhi) {
+    constexpr int HW = 1 << (LL - 1);
+    const float* p = qrow + ((size_t)k << LL);
+    float f[2 * HW];
+    if constexpr (LL == 1) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+        f[0] = v.x; f[1] = v.y;
+    } else {
+#pragma unroll
+        for (int i = 0; i < HW / 2; ++i) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(p) + i);
+            f[4 * i] = v.x; f[4 * i + 1] = v.y; f[4 * i + 2] = v.z; f[4 * i + 3] = v.w;
+        }
+    }
+    qlo = 0.0; qhi = 0.0;
+#pragma unroll
+    for (int i = 0; i < HW; ++i) qlo += (double)f[i];
+#pragma unroll
+    for (int i = 0; i < HW; ++i) qhi += (double)f[HW + i];
+}
+__device__ __forceinline__ int nth_set64(unsigned w0, unsigned w1, int n) {   // n-th (0-based) set bit of w1:w0
+    const int c0 = __popc(w0);
+    return n < c0 ? (int)__fns(w0, 0, n + 1) : 32 + (int)__fns(w1, 0, n - c0 + 1);
+}
+template <int P, int LL>
+__device__ __forceinline__ void split3z_block(unsigned b, int lane, unsigned w0, unsigned w1, int na, int nx, int ny,
+                                              int nzl, uint64_t e0, uint64_t e1, const unsigned* __restrict__ eray,
+                                              const float4* __restrict__ epsi, const float* __restrict__ q,
+                                              double* __restrict__ bm, const TileMap& tmap) {
+    const int lpe = na > 16 ? 32 : (na > 8 ? 16 : (na > 4 ? 8 : (na > 2 ? 4 : (na > 1 ? 2 : 1))));
+    const int E = 32 / lpe, grp = lane / lpe, j = lane % lpe;
+    const int k0 = j < na ? nth_set64(w0, w1, j) : -1;
+    const int k1 = j + 32 < na ? nth_set64(w0, w1, j + 32) : -1;
+    const bool two = na > 32;   // warp-uniform
+    const double cls = cpow3(LL) * kTwo896;
+    double acc[2][7];
+#pragma unroll
+    for (int z = 0; z < 2; ++z)
+#pragma unroll
+        for (int t = 0; t < 7; ++t) acc[z][t] = 0.0;
+    auto step = [&](const float4& ps, double qlo, double qhi, double (&a)[7]) {
+        const double qall = qlo + qhi;
+        const float pf[4] = {ps.x, ps.y, ps.z, ps.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const double pc = f2d_scaled<true>(pf[t]) * cls;   // == (double)psi * c^l
+            const bool neg = pf[t] < 0.0f;
+            if (t > 0) a[t - 1] = fma(neg ? pc : 0.0, qall, a[t - 1]);
+            a[3 + t] = fma(neg ? pc : -pc, neg ? qlo : qhi, a[3 + t]);
+        }
+    };
+    // software pipeline: entry e + E's ray, psi and q values are in flight while e is consumed
+    uint64_t e = e0 + grp;
+    unsigned yn = 0;
+    float4 pn = make_float4(0.f, 0.f, 0.f, 0.f);
+    double l0 = 0.0, h0 = 0.0, l1 = 0.0, h1 = 0.0;
+    auto fetch = [&](uint64_t ee) {
+        if (ee < e1) {
+            yn = __ldg(eray + ee);
+            pn = __ldg(epsi + ee);
+            const float* qrow = q + (uint64_t)yn * P;
+            if (k0 >= 0) split3z_q<LL>(qrow, k0, l0, h0);
+            if (two && k1 >= 0) split3z_q<LL>(qrow, k1, l1, h1);
+        }
+    };
+    fetch(e);
+    while (e < e1) {
+        const float4 pc4 = pn;
+        const double cl0 = l0, ch0 = h0, cl1 = l1, ch1 = h1;
+        fetch(e + E);
+        if (k0 >= 0) step(pc4, cl0, ch0, acc[0]);
+        if (two && k1 >= 0) step(pc4, cl1, ch1, acc[1]);
+        e += E;
+    }
+    // combine the entry groups (lanes j, j + lpe, ...): fixed order
+    for (int o = lpe; o < 32; o <<= 1)
+#pragma unroll
+        for (int z = 0; z < 2; ++z)
+#pragma unroll
+            for (int t = 0; t < 7; ++t) acc[z][t] += __shfl_xor_sync(0xffffffffu, acc[z][t], o);
+    if (grp == 0) {
+        const int hl = ny >> LL, wl = nx >> LL, dl = nzl >> LL;
+        const int bi = (int)(b / wl), bj = (int)(b % wl);
+#pragma unroll
+        for (int z = 0; z < 2; ++z) {
+            const int k = z ? k1 : k0;
+            if (k < 0) continue;
+            const int zz[7] = {k, k, k, dl + k, dl + k, dl + k, dl + k};
+            const int yy[7] = {hl + bi, bi, hl + bi, bi, hl + bi, bi, hl + bi};
+            const int xx[7] = {bj, wl + bj, wl + bj, bj, bj, wl + bj, wl + bj};
+#pragma unroll
+            for (int t = 0; t < 7; ++t)
+                bm[tmap.L ? coef_tile_pos(tmap, LL, yy[t], xx[t], zz[t]) : ((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]] =
+                    acc[z][t];
+        }
+    }
+}
+template <int P>
+__global__ void __launch_bounds__(128) k_split3z(uint64_t nlist, const uint2* __restrict__ list, int nx, int ny,
+                                                 int nzl, const unsigned long long* __restrict__ ptr,
+                                                 const unsigned* __restrict__ eray, const float4* __restrict__ epsi,
+                                                 const float* __restrict__ q, const unsigned* __restrict__ zbits,
+                                                 ActOff zoff, ActOff koff, double* __restrict__ bm, TileMap tmap) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nlist; it += W) {
+        const unsigned b = list[it].x;
+        const int l = (int)list[it].y;
+        const int nk = nzl >> l, nw = (nk + 31) >> 5;
+        const unsigned* zb = zbits + zoff.off[l] + (uint64_t)b * nw;
+        const unsigned w0 = zb[0], w1 = nw > 1 ? zb[1] : 0u;
+        const int na = __popc(w0) + __popc(w1);
+        if (na == 0) continue;
+        const uint64_t key = koff.off[l] + b;
+        const uint64_t e0 = ptr[key], e1 = ptr[key + 1];
+#define SZ(LLv) case LLv: if constexpr ((P >> LLv) >= 1) split3z_block<P, LLv>(b, lane, w0, w1, na, nx, ny, nzl, e0, e1, eray, epsi, q, bm, tmap); break;
+        switch (l) { SZ(1) SZ(2) SZ(3) SZ(4) SZ(5) default: break; }
+#undef SZ
+    }
+}
+
 // Ray bands of the 3D split.  The split gathers one P*4-byte row of q per Psi
 // entry; a block's list holds every view, and the q slab outgrows L2 at the
 // BASELINE sizes (cfg4: 755 MB, so the final tree's 8.7e8 entries re-read

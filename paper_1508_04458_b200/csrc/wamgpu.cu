@@ -2634,7 +2634,19 @@ static void wam_step(Ctx* c) {
             switch (P) { case 32: S3EU(32, 4, 1) break; case 64: S3EU(64, 2, 1) break; default: S3EU(128, 1, 1) break; }
         } else if (c->split_variant == 4 && P >= 32) {
             switch (P) { case 32: S3EU(32, 4, 4) break; case 64: S3EU(64, 4, 4) break; default: S3EU(128, 2, 4) break; }
-        } else {   // measured: cfg3 (64 slices) E=4 188 ms/run vs 364; cfg4 (128) E=2 1888 vs 2157 (E=4) / 2500;
+        } else if (c->split_variant != 6) {   // default: lane per ACTIVE z-block (kernels3h.cuh k_split3z)
+#define S3Z(S) k_split3z<S><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p, c->E3ray.p, \
+                                                   c->E3psi.p, c->q.p, c->zbits.p, c->zoff, c->koff, bm3, tm);
+            switch (P) {
+                case 8: S3Z(8) break;
+                case 16: S3Z(16) break;
+                case 32: S3Z(32) break;
+                case 64: S3Z(64) break;
+                default: S3Z(128) break;
+            }
+#undef S3Z
+        } else {   // variant 6, the round-1 default: every z-block of a listed block, E entries in flight.
+                   // measured: cfg3 (64 slices) E=4 188 ms/run vs 364; cfg4 (128) E=2 1888 vs 2157 (E=4) / 2500;
                    // one pipelined round (U = 1) 182 ms/run at cfg3 vs 188 (U = 2) / 189 (U = 4).
                    // Sharded small slabs: S = P*E/32 = 4 slices per lane.
             switch (P) {

@@ -1,0 +1,17 @@
+# lane-per-active-z-block split (k_split3z, default) vs the round-1 kernel (WAMGPU_SPLIT_VARIANT=6)
+mkdir -p gpurun_out/sz
+timeout 900 python -m pytest tests/test_gpu_parity3d.py tests/test_gpu_sharded3d.py -x -q > gpurun_out/sz/pytest.log 2>&1; echo "pytest rc=$?"; tail -n 6 gpurun_out/sz/pytest.log
+run() { echo "== $1 $2 SPLIT=$3"; WAMGPU_SPLIT_VARIANT=$3 timeout 900 python scripts/cfg4_iters.py $1 $2 2>&1 | grep -v "^$" | tail -n 2; }
+{ run cfg3 30 6; run cfg3 30 0; run cfg4 40 6; run cfg4 40 0; } > gpurun_out/sz/ab.log 2>&1
+python - <<'PY'
+import re
+for l in open("gpurun_out/sz/ab.log"):
+    l = l.strip()
+    if l.startswith("=="): print(l); continue
+    m = re.search(r"'total_ms': ([0-9.]+), 'fwd_ms': ([0-9.]+), 'back_ms': ([0-9.]+), 'split_ms': ([0-9.]+).*'expand_ms': ([0-9.]+).*'fwd_launches': (\d+), 'back_launches': (\d+), 'split_launches': (\d+)", l)
+    if m:
+        t, f, b, s, e, nf, nb, ns = m.groups()
+        print(f"   total {float(t):.0f} ms  fwd {float(f)/max(int(nf),1):.2f}  back {float(b)/max(int(nb),1):.2f}  split {float(s)/max(int(ns),1):.2f} ms/launch ({float(s):.0f} per run)  expand {float(e):.0f}")
+    elif "objective" in l: print("   " + l[:110])
+    else: print("   ?", l[:300])
+PY
