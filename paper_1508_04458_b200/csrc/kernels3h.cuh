@@ -702,6 +702,9 @@ __global__ void __launch_bounds__(128) k_split3h(uint64_t nlist, const uint2* __
 // U rounds of E entries: the q rows of round r+1 are loaded before round r is
 // consumed (software pipeline; ncu at cfg4 showed 44% of the stall samples on
 // the first use of the q gathers with only the current round in flight).
+// (A two-stage pipeline -- entries of round r+2 and q rows of round r+1 in flight,
+// evict-first Psi loads -- was measured slower: cfg3 9.06 vs 7.82, cfg4 60.3 vs
+// 53.9 ms per launch at a 128-register cap, profiles/r06/split_prefetch_ab.txt.)
 // Templated on the slab stride P (8 .. 128): S = P*E/32 slices per lane.
 template <int P, int E, int U = 2>
 __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* __restrict__ list, int nx, int ny,
@@ -833,7 +836,10 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
     }
 }
 
-// ---- split, lane per ACTIVE z-block (default).  k_split3h_e spends the same
+// ---- split, lane per ACTIVE z-block (opt-in WAMGPU_SPLIT_VARIANT=7; measured 2x
+// slower than k_split3h_e: its 8-byte per-lane q loads are scattered over the row,
+// the multipliers are prepared per z-block instead of per 4 z-blocks, and most
+// z-blocks of a listed block turn out to be active).  k_split3h_e spends the same
 // work on every z-block of a listed in-plane block, but at the BASELINE trees
 // only ~1/3 of them are active (cfg4 final tree: 6.3e6 of 1.7e7 level-1 blocks),
 // and it issues both products of every z-high coefficient although one of its

@@ -1086,6 +1086,8 @@ template <int P> struct SlabShape {
         case 16: X(3, 2, 4, 6) break;                                                                              \
         case 17: X(3, 104, 8, 2) break;                                                                            \
         case 18: X(2, 104, 8, 2) break;                                                                            \
+        case 20: X(1, 104, 8, 2) break;                                                                            \
+        case 21: X(0, 104, 8, 2) break;                                                                            \
         case 19: X(3, 4, 8, 2) break;                                                                              \
         default: X(3, DEFU, 8, 2) break;                                                                           \
     }
@@ -1247,11 +1249,17 @@ static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxbl
     k_fwd3s_band<MODE, S::LPR, S::SPL, UXv, 3, SG, P, 8, 2><<<nb, 256, 0, c->st>>>(                                \
         c->Ml, c->nzl, b, B, c->rp.p, c->blo.p, c->bhi.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, acc, l,             \
         c->partial.p, c->flag.p)
+#define BAND2(SG)                                                                                                  \
+    k_fwd3s_band<MODE, S::LPR, S::SPL, 104, 2, SG, P, 8, 2><<<nb, 256, 0, c->st>>>(                                \
+        c->Ml, c->nzl, b, B, c->rp.p, c->blo.p, c->bhi.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, acc, l,             \
+        c->partial.p, c->flag.p)
         for (int b = 0; b < B; ++b) {
-            if (v != 19) { if (uns) BAND(104, false); else BAND(104, true); }
+            if (v == 18 || v == 12) { if (uns) BAND2(false); else BAND2(true); }   // NF 2: cfg4 63.0-63.7 vs 64.1-64.6 ms
+            else if (v != 19) { if (uns) BAND(104, false); else BAND(104, true); }
             else { if (uns) BAND(4, false); else BAND(4, true); }
         }
 #undef BAND
+#undef BAND2
         launched(c, B - 1);
         return nb;
     }
@@ -1317,7 +1325,9 @@ static void back3_launch_p(Ctx* c, const float* w, double* out, const double* ba
     // default: ping-pong pipeline for the plain back projection; the fused AM update keeps the copy
     // pipeline (cfg5: 8.52 vs 8.01 ms per pass with ping-pong)
 #define DEFU 104
-    if (!bam) { SLAB_SWITCH(BX, v) }
+    if (!bam) {   // default: NF 1 (cfg4 56.3 / 51.3 / 50.1 / 50.4 ms per pass for NF 3 / 2 / 1 / 0, profiles/r06/nf_sweep.txt)
+        if (v == 12) { BX(1, 104, 8, 2) } else { SLAB_SWITCH(BX, v) }
+    }
 #undef DEFU
 #define DEFU 4
     if (bam) { SLAB_SWITCH(BX, v) }
@@ -2634,7 +2644,8 @@ static void wam_step(Ctx* c) {
             switch (P) { case 32: S3EU(32, 4, 1) break; case 64: S3EU(64, 2, 1) break; default: S3EU(128, 1, 1) break; }
         } else if (c->split_variant == 4 && P >= 32) {
             switch (P) { case 32: S3EU(32, 4, 4) break; case 64: S3EU(64, 4, 4) break; default: S3EU(128, 2, 4) break; }
-        } else if (c->split_variant != 6) {   // default: lane per ACTIVE z-block (kernels3h.cuh k_split3z)
+        } else if (c->split_variant == 7) {   // lane per ACTIVE z-block (kernels3h.cuh k_split3z): measured 2x slower
+                                              // (cfg3 16.5 vs 7.8, cfg4 92 vs 54 ms per launch, profiles/r06/split3z_ab.txt)
 #define S3Z(S) k_split3z<S><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p, c->E3ray.p, \
                                                    c->E3psi.p, c->q.p, c->zbits.p, c->zoff, c->koff, bm3, tm);
             switch (P) {
@@ -2645,7 +2656,7 @@ static void wam_step(Ctx* c) {
                 default: S3Z(128) break;
             }
 #undef S3Z
-        } else {   // variant 6, the round-1 default: every z-block of a listed block, E entries in flight.
+        } else {   // default: every z-block of a listed block, E entries in flight.
                    // measured: cfg3 (64 slices) E=4 188 ms/run vs 364; cfg4 (128) E=2 1888 vs 2157 (E=4) / 2500;
                    // one pipelined round (U = 1) 182 ms/run at cfg3 vs 188 (U = 2) / 189 (U = 4).
                    // Sharded small slabs: S = P*E/32 = 4 slices per lane.

@@ -220,14 +220,14 @@ def test_on_the_fly_tma_forward(wam, orc, name):
 
 @pytest.mark.parametrize("name", ["tiny3d16", "small3d", "tiny3d64"])
 def test_split_variants_agree(wam, orc, name, monkeypatch):
-    """The default 3D split (k_split3z: a lane per ACTIVE z-block, the oracle's
-    qlo/qhi/qall formulation, one product per z-high coefficient) against the
-    round-1 kernel (WAMGPU_SPLIT_VARIANT=6: every z-block of a listed block, both
-    products): same tree, b- equal to rounding (the two sum in different but
-    fixed orders), and b- within 1e-12 of the mirror oracle's."""
+    """The opt-in 3D split k_split3z (WAMGPU_SPLIT_VARIANT=7: a lane per ACTIVE
+    z-block, the oracle's qlo/qhi/qall formulation, one product per z-high
+    coefficient) against the default k_split3h_e (every z-block of a listed
+    block, both products): same tree, b- equal to rounding (the two sum in
+    different but fixed orders), and b- within the mirror bar."""
     cfg, p32, _, I0, d = problem_inputs(name, orc, wam, mirror=True)
     out = {}
-    for v in ("0", "6"):
+    for v in ("7", "0"):
         monkeypatch.setenv("WAMGPU_SPLIT_VARIANT", v)
         c = _ctx(wam, cfg)
         c.set_haar_dim(3)
@@ -236,7 +236,7 @@ def test_split_variants_agree(wam, orc, name, monkeypatch):
         r = c.wam_run(cfg["J"], cfg["schedule"], 0.1)
         out[v] = ([x["objective"] for x in r], c.tree(), c.image(), c.stats()[2])
         c.close()
-    (o0, t0, m0, b0), (o6, t6, m6, b6) = out["0"], out["6"]
+    (o0, t0, m0, b0), (o6, t6, m6, b6) = out["7"], out["0"]
     assert np.array_equal(t0, t6)
     assert rel_l2(b0, b6) < 1e-13 and rel_l2(o0, o6) < 1e-12 and rel_l2(m0, m6) < 1e-6
     p32.set_haar_dim(3)
