@@ -410,9 +410,13 @@ __global__ void __launch_bounds__(32 * 6) k_walk3h(uint64_t M, const unsigned lo
                                                    unsigned* __restrict__ keys, uint2* __restrict__ vidx,
                                                    unsigned* __restrict__ pray, float4* __restrict__ ppsi,
                                                    int split1) {
+    // The tree bits stay in global memory (read-only, L1-resident: 43 KB at cfg4).
+    // Holding them in shared memory, as the first version did, left 2 CTAs --
+    // 2 to 12 warps -- per SM (82 KB per CTA at cfg4), and the walk ran at 2% of
+    // the HBM roofline on latency alone.
     extern __shared__ unsigned char dsm[];
-    unsigned* tsm = reinterpret_cast<unsigned*>(dsm);                                // tree_words
-    double* stot = reinterpret_cast<double*>(dsm + ((tree_words * 4 + 15) / 16) * 16);  // sum_l (nzl>>l)*32
+    double* stot = reinterpret_cast<double*>(dsm);   // MODE 1: sum over the walked levels of (nzl>>l)*32
+    (void)tree_words;
     __shared__ uint2 buf[32][33];
     __shared__ unsigned long long s_lo[32], s_len[32];
     // split1 (MODE 1, level 1 walked): one extra warp also walks level 1 and
@@ -422,7 +426,6 @@ __global__ void __launch_bounds__(32 * 6) k_walk3h(uint64_t M, const unsigned lo
     const int nwarp = blockDim.x >> 5, nlev = nwarp - split1;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, l = w < nlev ? L - w : 1;
     const unsigned hmask = !split1 || l != 1 ? 0xffffffffu : (w < nlev ? 0x0000ffffu : 0xffff0000u);
-    for (int i = threadIdx.x; i < tree_words; i += blockDim.x) tsm[i] = tbits[i];
     int toff = 0;  // offset of this level's tot block in stot
     for (int k = L; k > l; --k) toff += (nzl >> k) * 32;
     const int nk = nzl >> l;
@@ -530,7 +533,7 @@ __global__ void __launch_bounds__(32 * 6) k_walk3h(uint64_t M, const unsigned lo
                 flush();
                 cur = key;
                 const unsigned bit = bo + (unsigned)key;
-                av = (tsm[bit >> 5] >> (bit & 31)) & 1u;
+                av = (__ldg(tbits + (bit >> 5)) >> (bit & 31)) & 1u;
             }
             if (av) {
                 const int quad = (((iy >> (l - 1)) & 1) << 1) | ((ix >> (l - 1)) & 1);

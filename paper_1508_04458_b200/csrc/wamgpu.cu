@@ -1670,10 +1670,12 @@ static void upload_tree3(Ctx* c, int* nlev_out) {
 template <int MODE>
 static void launch_walk3h(Ctx* c, int nlev, unsigned long long* cnt, const unsigned long long* pos) {
     const unsigned nb = blocks_for(c->Ml, 32);
+    // shared memory: the per-(ray, z-block) totals of the WALKED levels (Z walk only)
     size_t stot = 0;
-    for (int l = 1; l <= c->L; ++l) stot += (size_t)(c->nzl >> l) * 32 * 8;
-    const size_t smem = ((size_t)c->tree_words * 4 + 15) / 16 * 16 + stot;
-    if (smem > 200 * 1024) throw ConfigError("tree too large for the shared-memory 3D walk");
+    if (MODE == 1)
+        for (int l = c->L; l > c->L - nlev && l >= 1; --l) stot += (size_t)(c->nzl >> l) * 32 * 8;
+    const size_t smem = stot;
+    if (smem > 200 * 1024) throw ConfigError("slab too deep for the shared-memory 3D walk");
     // Z walk with level 1 walked and >= 32 level-1 z-blocks: a second warp
     // takes half of the level-1 flush loop (WAMGPU_WALK3_SPLIT=0 turns it off)
     static const bool split_on = [] {
