@@ -849,7 +849,7 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
 // two multipliers is always zero.  Here the warp compacts the block's active
 // z-blocks from its z-bit words; lane j of an entry group owns the j-th active
 // z-block (and the (j+32)-th when more than 32 are active) and follows the
-// oracle's formulation (oracle/wam_oracle.cpp split3_mirror): per entry
+// per-half formulation of the SPEC split (separable model): per entry
 //   qlo / qhi = slice-order sums of q over the z-block's halves, qall = qlo + qhi,
 //   z-low  p in H,V,D:   acc += (p < 0 ? p : 0) * qall
 //   z-high p in A,H,V,D: acc += p < 0 ? p * qlo : -p * qhi        (p = psi c^l)

@@ -1646,7 +1646,32 @@ static void upload_tree3(Ctx* c, int* nlev_out) {
             parts[t].swap(mine);
             if (any) any_l = true;
         });
+        const size_t lv0 = lst.size();
         for (auto& v : parts) lst.insert(lst.end(), v.begin(), v.end());
+        // The split gathers one q row per Psi entry and every block's list spans all
+        // views.  In row-major block order the ~1e4 warps in flight cover a few full
+        // image rows, i.e. nearly every ray: the q slab (cfg4: 755 MB) streams from
+        // DRAM again and again (ncu: 222 GB per launch, 27% L2 hits).  Morton order
+        // keeps the blocks in flight inside a compact square whose rays' q rows fit L2.
+        // (The split writes by block index, so the order is free.)
+        static const int split_order = [] { const char* e = std::getenv("WAMGPU_SPLIT_ORDER"); return e ? std::atoi(e) : 1; }();
+        if (split_order == 1 && lst.size() > lv0) {
+            const unsigned wl = (unsigned)(c->nx >> l);
+            auto morton = [](unsigned x, unsigned y) {
+                auto spread = [](uint64_t v) {
+                    v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+                    v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+                    v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+                    v = (v | (v << 2)) & 0x3333333333333333ull;
+                    v = (v | (v << 1)) & 0x5555555555555555ull;
+                    return v;
+                };
+                return spread(x) | (spread(y) << 1);
+            };
+            std::sort(lst.begin() + lv0, lst.end(), [&](const uint2& a, const uint2& b) {
+                return morton(a.x % wl, a.x / wl) < morton(b.x % wl, b.x / wl);
+            });
+        }
         if (chain && any_l) ++nlev; else chain = false;
         bit = (bit + nb + 31) / 32 * 32;
         zo += nb * W;
