@@ -556,8 +556,8 @@ def main():
     ctx.set_kernel_timing(True)
     dev_ms, fwd_ms, back_ms, launches = [], [], [], 0
     fwd_n = back_n = 0
-    split_ms = upd_ms = exp_ms = comm_ms = phi_ms = 0.0
-    phi_n = 0
+    split_ms = upd_ms = exp_ms = comm_ms = phi_ms = cfwd_ms = cback_ms = 0.0
+    phi_n = cfwd_n = cback_n = proj_entries = 0
     split_nnz = 0
     plumb.barrier()
     with ClockSampler(local) as clk:
@@ -577,6 +577,11 @@ def main():
                 comm_ms += t["comm_ms"]
                 phi_ms += t["phi_ms"]
                 phi_n += t["phi_launches"]
+                cfwd_ms += t["coarse_fwd_ms"]
+                cback_ms += t["coarse_back_ms"]
+                cfwd_n += t["coarse_fwd_launches"]
+                cback_n += t["coarse_back_launches"]
+                proj_entries += t["proj_entries"]
                 split_nnz = t["split_nnz"]
         wall = time.perf_counter() - t_wall
     plumb.barrier()
@@ -683,8 +688,13 @@ def main():
             # H passes only (forward + back launches; a 3D launch covers every
             # slice): the root-only iterations run over the approximation
             # columns Phi_A instead of H and are counted apart
-            "ray_voxel_updates_per_s": (fwd_n + back_n) / args.steps * nnz * nz / (ms_step * 1e-3),
+            # (updates actually executed: proj_entries counts the in-plane entries
+            # every forward / back launch streamed, H or a block-coarsened Hc)
+            "ray_voxel_updates_per_s": proj_entries * world / args.steps * nz / (ms_step * 1e-3),
             "h_passes_per_step": (fwd_n + back_n) / args.steps,
+            "coarse_passes_per_step": (cfwd_n + cback_n) / args.steps,
+            "pixel_equivalent_updates_per_s": (fwd_n + back_n + cfwd_n + cback_n) / args.steps * nnz * nz
+                                              / (ms_step * 1e-3),
             "final_objective": final_obj,
             "tree": {"active_set_by_iteration": sorted({r["active_set"] for r in recs}),
                      "coefficients": N * nz, "phi_minus_nnz": split_nnz},
@@ -697,6 +707,7 @@ def main():
                         "gather_gbs": (4 * nnz_local * nz / (fwd_avg * 1e-3) / 1e9) if nz > 1 else None,
                         "back_avg_ms": back_avg, "back_gbs": back_gbs, "back_frac": back_gbs / hbm,
                         "per_step_ms": {"forward": sum(fwd_ms) / args.steps, "back": sum(back_ms) / args.steps,
+                                        "forward_coarse": cfwd_ms / args.steps, "back_coarse": cback_ms / args.steps,
                                         "split": split_ms / args.steps, "update": upd_ms / args.steps,
                                         "expand": exp_ms / args.steps, "comm": comm_ms / args.steps,
                                         "phi_a": phi_ms / args.steps},

@@ -85,6 +85,11 @@ typedef struct {
     int64_t split_nnz;       /* Phi^- entries gathered per split launch (last) */
     double phi_ms;           /* iterations over the approximation columns (root-only tree) */
     int64_t phi_launches;    /* such iterations (their back / update / forward are not in the above) */
+    double coarse_fwd_ms;    /* forward / back launches over a block-coarsened matrix (wavelet AM while the */
+    double coarse_back_ms;   /* finest active tree level is > 1); NOT included in fwd_ms / back_ms */
+    int64_t coarse_fwd_launches, coarse_back_launches;
+    int64_t proj_entries;    /* in-plane matrix entries streamed by the forward and back launches above
+                                (H and the block-coarsened Hc alike: x slices = ray-voxel updates actually done) */
 } wamgpu_timing;
 
 int wamgpu_version(void);

@@ -18,7 +18,7 @@ import numpy as np
 from . import configs  # noqa: F401  (re-export)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIBPATH = os.path.join(HERE, "libwamgpu.so")
+LIBPATH = os.environ.get("WAMGPU_LIB") or os.path.join(HERE, "libwamgpu.so")   # WAMGPU_LIB: A/B against another build
 
 BEAM_PARALLEL, BEAM_FAN_FLAT, BEAM_FAN_ARC = 0, 1, 2
 
@@ -129,7 +129,9 @@ class Timing(C.Structure):
                                           "expand_ms", "comm_ms")] + \
                [(n, C.c_int64) for n in ("fwd_launches", "back_launches", "split_launches", "update_launches",
                                          "expand_events", "kernel_launches", "split_nnz")] + \
-               [("phi_ms", C.c_double), ("phi_launches", C.c_int64)]
+               [("phi_ms", C.c_double), ("phi_launches", C.c_int64), ("coarse_fwd_ms", C.c_double),
+                ("coarse_back_ms", C.c_double), ("coarse_fwd_launches", C.c_int64),
+                ("coarse_back_launches", C.c_int64), ("proj_entries", C.c_int64)]
 
     def asdict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

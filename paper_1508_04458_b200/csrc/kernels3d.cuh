@@ -83,6 +83,9 @@ __device__ __forceinline__ void slab_dot(const uint2* __restrict__ A, const floa
 // Summation stays sequential per (ray, slice) in Siddon / CSC order.
 template <bool SIGNED>
 __device__ __forceinline__ double f2d_scaled(float f) {
+    // (One 32x32->64 multiply by 2^29 -- IMAD.WIDE gives both words at once, 1 / 2
+    // instructions instead of 2 / 3 -- was measured SLOWER: cfg4 back 1734 vs 1668 ms,
+    // forward 2108 vs 2094 ms per run, profiles/r07/ab1.txt; the shifts stay.)
     const unsigned u = __float_as_uint(f);
     const unsigned hi = SIGNED ? (((u & 0x7fffffffu) >> 3) | (u & 0x80000000u)) : (u >> 3);
     return __hiloint2double((int)hi, (int)(u << 29));
@@ -120,6 +123,26 @@ __device__ __forceinline__ void slab_unpack(const typename SlabLd<SPL>::T (&v)[S
     }
 }
 
+// Entry sources of the slab SpMM.  The system matrix: uint2 {column, fp32 h}.
+// The block-coarsened matrices of the wavelet-AM iteration (kernels3c.cuh):
+// separate column and fp64 value arrays.
+struct Ent64 {
+    const unsigned* c;
+    const double* v;
+};
+struct Ent64Val {
+    unsigned c;
+    double h;
+};
+__device__ __forceinline__ uint2 ent_ld(const uint2* A, uint64_t k) { return ld_stream(A + k); }
+__device__ __forceinline__ uint2 ent_zero(const uint2*) { return make_uint2(0u, 0u); }
+__device__ __forceinline__ unsigned ent_col(const uint2& e) { return e.x; }
+__device__ __forceinline__ double ent_h(const uint2& e) { return (double)__uint_as_float(e.y); }
+__device__ __forceinline__ Ent64Val ent_ld(const Ent64& A, uint64_t k) { return Ent64Val{__ldcs(A.c + k), __ldcs(A.v + k)}; }
+__device__ __forceinline__ Ent64Val ent_zero(const Ent64&) { return Ent64Val{0u, 0.0}; }
+__device__ __forceinline__ unsigned ent_col(const Ent64Val& e) { return e.c; }
+__device__ __forceinline__ double ent_h(const Ent64Val& e) { return e.h; }
+
 // per-warp staging: 2 chunk buffers x G groups x K entries (K = 32, 16 for
 // G = 8 to stay in 48 KB of static smem per CTA); strides K+4 / K+2 keep the
 // G 16-byte broadcasts of a load in distinct bank quads
@@ -142,8 +165,8 @@ template <int G> struct SlabStage {
 // a round is consumed instead of travelling with the gathers.  The copy
 // pipeline below moves 40 registers per round (IMAD.MOV: 50 of the 185 SASS
 // instructions of a 32-DFMA round at P = 128).
-template <int LPR, int SPL, int UX, int NF, bool SIGNED, int P>
-__device__ __forceinline__ void slab_dot_g(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
+template <int LPR, int SPL, int UX, int NF, bool SIGNED, int P, class AP>
+__device__ __forceinline__ void slab_dot_g(const AP& A, const float* __restrict__ x, uint64_t lo,
                                            uint64_t hi, int maxlen, int lig, int g,
                                            SlabStage<32 / LPR>& st, double (&acc)[SPL]) {
     constexpr bool PP = UX >= 100;
@@ -155,19 +178,19 @@ __device__ __forceinline__ void slab_dot_g(const uint2* __restrict__ A, const fl
     for (int j = 0; j < SPL; ++j) acc[j] = 0.0;
     if (maxlen <= 0) return;
     const float* xl = x + slab_slice<LPR, SPL>(lig, 0);
-    uint2 nx[NL];
+    decltype(ent_zero(A)) nx[NL];
     auto fetch = [&](int base) {
 #pragma unroll
         for (int t = 0; t < NL; ++t) {
             const uint64_t k = lo + base + lig + LPR * t;
-            nx[t] = k < hi ? ld_stream(A + k) : make_uint2(0u, 0u);
+            nx[t] = k < hi ? ent_ld(A, k) : ent_zero(A);
         }
     };
     auto stage = [&](int buf) {
 #pragma unroll
         for (int t = 0; t < NL; ++t) {
-            st.c[buf][g][lig + LPR * t] = nx[t].x;
-            st.h[buf][g][lig + LPR * t] = (double)__uint_as_float(nx[t].y);
+            st.c[buf][g][lig + LPR * t] = ent_col(nx[t]);
+            st.h[buf][g][lig + LPR * t] = ent_h(nx[t]);
         }
     };
     typename L::T v[U][L::NV];
@@ -294,9 +317,9 @@ __device__ __forceinline__ void slab_dot_g(const uint2* __restrict__ A, const fl
 // the host may instead launch once per part (sbeg = part start, nz = its end)
 // so that one part's slab columns stay L2-resident (cfg4: 1M voxels x 32 slices
 // = 128 MB per part against the 512 MB whole slab).
-template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P, int WPB = 8, int MINB = 1>
+template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P, int WPB = 8, int MINB = 1, class AP = const uint2*>
 __global__ void __launch_bounds__(32 * WPB, MINB) k_fwd3s(uint64_t M, int sbeg, int nz, const unsigned long long* __restrict__ rp,
-                                               const uint2* __restrict__ A, const float* __restrict__ mu,
+                                               AP A, const float* __restrict__ mu,
                                                const float* __restrict__ I0, const float* __restrict__ d,
                                                float* __restrict__ q, double* __restrict__ lout,
                                                double* __restrict__ partial, int* __restrict__ flag) {
@@ -495,10 +518,10 @@ __device__ __forceinline__ uint64_t coef_tile_pos(const TileMap& m, int l, int y
 }
 
 // K3 3D v2: one warp = G voxels of the tile order; MODE as k_back3.
-template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P, int WPB = 8, int MINB = 1>
+template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P, int WPB = 8, int MINB = 1, class AP = const uint2*>
 __global__ void __launch_bounds__(32 * WPB, MINB) k_back3s(uint64_t N, int sbeg, int nz, const unsigned* __restrict__ order,
                                                 const unsigned long long* __restrict__ cp,
-                                                const uint2* __restrict__ C, const float* __restrict__ w,
+                                                AP C, const float* __restrict__ w,
                                                 double* __restrict__ g, const double* __restrict__ bam,
                                                 float* __restrict__ mu, double Z0, int* __restrict__ flag,
                                                 TileMap tmap) {

@@ -839,6 +839,458 @@ __global__ void __launch_bounds__(128) k_split3h_e(uint64_t nlist, const uint2* 
     }
 }
 
+// ---- split, pipelined (default): k_split3p ---------------------------------
+// Same lane map as k_split3h_e (E entry groups of LPE = 32/E lanes, S = P*E/32
+// consecutive slices per lane) with the per-entry work cut down.  ncu of
+// k_split3h_e at cfg4 (profiles/r06/ncu_split_cfg4_src.txt): DFMA was 12.5% of
+// the issue samples; register copies of the software pipeline 20%, fp64
+// min/max/select chains for the multipliers 10%, address arithmetic 15%.
+//  * sums of q first: qlo / qhi = slice-order sums of the z-block's halves (the
+//    SPEC's per-half formulation), then 3 + 4 (+4) FMAs per z-block instead of
+//    7 per slice pair; the loop is specialised per level, so which half a slice
+//    belongs to is static (no per-pair selects);
+//  * c^l is factored out of the sums (one multiplication per output), so the
+//    multipliers are plain conversions of min(psi, 0) / min(-psi, 0) taken in
+//    fp32 (FMNMX) instead of fp64 compare/select chains after psi * c^l;
+//  * q >= 0 moves into fp64 by ONE multiply (f2d_scaled<false>, exact);
+//  * level whose half fits a lane (TRICK): z-high = L - Pq with
+//    L = sum min(p,0) (qlo+qhi)  (the z-low sum, needed anyway) and
+//    Pq = sum p qhi, since min(p,0) qlo - max(p,0) qhi = min(p,0)(qlo+qhi) - p qhi:
+//    3 + 3 + 2 FMAs per z-block instead of 3 + 8;
+//  * three-stage pipeline on two register sets without copies: (ray, psi) of
+//    round r+2 and the q row of round r+1 are in flight while round r is consumed.
+// Sums are fp64 FMAs of exact fp32 x fp32 products in entry order per group,
+// groups combined by a fixed xor butterfly: deterministic, and within 1e-15
+// relative of k_split3h_e (different association; tests compare both to the oracle).
+template <int S>
+struct SplitSet {
+    unsigned y;
+    float4 ps;
+    float4 q[S / 4];
+};
+template <int P, int E, int LV, bool TRICK>
+__device__ __forceinline__ void split3p_block(unsigned b, int l, int lane, int wib, int nx, int ny, int nzl,
+                                              uint64_t e0, uint64_t e1, const unsigned* __restrict__ eray,
+                                              const float4* __restrict__ epsi, const float* __restrict__ q,
+                                              const uint8_t* __restrict__ act, const ActOff& off,
+                                              double* __restrict__ bm, const TileMap& tmap,
+                                              double (&red)[4][7][P / 2]) {
+    constexpr int LPE = 32 / E, S = P * E / 32;
+    static_assert(S == 4 || S == 8, "slices per lane");
+    // LV > 0: half size HS = 2^(LV-1) < S, NZ complete z-blocks per lane.
+    // LV == 0: runtime level with HS >= S (the lane lies inside one half).
+    constexpr int HS = LV > 0 ? (1 << (LV - 1)) : S;
+    constexpr int NZ = LV > 0 ? S / (2 * HS) : 1;
+    static_assert(LV == 0 || 2 * HS <= S, "level does not fit a lane");
+    constexpr int NA = LV > 0 ? 7 * NZ : 7;
+    const int grp = lane / LPE, j = lane % LPE;
+    const bool hh = LV == 0 ? (((j * S) >> (l - 1)) & 1) != 0 : false;
+    double acc[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) acc[i] = 0.0;
+    SplitSet<S> A, B;
+    const uint64_t n = e1 - e0;
+    const uint64_t nr = (n + E - 1) / E;
+    auto load_idx = [&](SplitSet<S>& x, uint64_t r) {
+        const uint64_t ee = e0 + r * E + grp;
+        const bool ok = ee < e1;
+        const uint64_t ei = ok ? ee : e0;   // always a valid index
+        x.y = __ldg(eray + ei);
+        x.ps = ok ? __ldg(epsi + ei) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    auto load_q = [&](SplitSet<S>& x) {
+        const float4* row = reinterpret_cast<const float4*>(q + (uint64_t)x.y * P + j * S);
+#pragma unroll
+        for (int v = 0; v < S / 4; ++v) x.q[v] = __ldg(row + v);
+    };
+    auto step = [&](SplitSet<S>& X, SplitSet<S>& Y, uint64_t r) {
+        const float pf[4] = {X.ps.x, X.ps.y, X.ps.z, X.ps.w};
+        double m[8];
+        if constexpr (LV > 0) {
+            // m[0..3] = min(psi_t, 0) (t = A,H,V,D); m[4] = min(-psi_A, 0);
+            // m[5..7] = TRICK ? psi_t : min(-psi_t, 0) (t = H,V,D)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) m[t] = (double)fminf(pf[t], 0.f);
+            m[4] = (double)fminf(-pf[0], 0.f);
+#pragma unroll
+            for (int t = 1; t < 4; ++t) m[4 + t] = TRICK ? (double)pf[t] : (double)fminf(-pf[t], 0.f);
+        } else {
+            // m[0..2] = min(psi_t, 0) (t = H,V,D: z-low); m[3..6] = this lane's half of z-high
+            // (low half min(psi,0), high half min(-psi,0)), scaled by 2^-896 (bit move)
+#pragma unroll
+            for (int t = 1; t < 4; ++t) m[t - 1] = f2d_scaled<true>(fminf(pf[t], 0.f));
+#pragma unroll
+            for (int t = 0; t < 4; ++t) m[3 + t] = f2d_scaled<true>(fminf(hh ? -pf[t] : pf[t], 0.f));
+        }
+        if (r + 2 < nr) load_idx(X, r + 2);
+        if (r + 1 < nr) load_q(Y);
+        float f[S];
+#pragma unroll
+        for (int v = 0; v < S / 4; ++v) {
+            f[4 * v] = X.q[v].x; f[4 * v + 1] = X.q[v].y; f[4 * v + 2] = X.q[v].z; f[4 * v + 3] = X.q[v].w;
+        }
+        if constexpr (LV > 0) {
+#pragma unroll
+            for (int z = 0; z < NZ; ++z) {
+                double qlo = f2d_scaled<false>(f[z * 2 * HS]), qhi = f2d_scaled<false>(f[z * 2 * HS + HS]);
+#pragma unroll
+                for (int i = 1; i < HS; ++i) {
+                    qlo += f2d_scaled<false>(f[z * 2 * HS + i]);
+                    qhi += f2d_scaled<false>(f[z * 2 * HS + HS + i]);
+                }
+                const double qall = qlo + qhi;
+                double* a = acc + 7 * z;
+#pragma unroll
+                for (int t = 0; t < 3; ++t) a[t] = fma(m[1 + t], qall, a[t]);
+                a[3] = fma(m[4], qhi, fma(m[0], qlo, a[3]));
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    if constexpr (TRICK) a[4 + t] = fma(m[5 + t], qhi, a[4 + t]);
+                    else a[4 + t] = fma(m[5 + t], qhi, fma(m[1 + t], qlo, a[4 + t]));
+                }
+            }
+        } else {
+            double qs = f2d_scaled<false>(f[0]);
+#pragma unroll
+            for (int i = 1; i < S; ++i) qs += f2d_scaled<false>(f[i]);
+            qs *= kTwo896;   // exact: the multipliers carry the 2^-896 here
+#pragma unroll
+            for (int t = 0; t < 7; ++t) acc[t] = fma(m[t], qs, acc[t]);
+        }
+    };
+    if (nr > 0) {
+        load_idx(A, 0);
+        if (nr > 1) load_idx(B, 1);
+        load_q(A);
+        for (uint64_t r = 0; r < nr; r += 2) {
+            step(A, B, r);
+            if (r + 1 < nr) step(B, A, r + 1);
+        }
+    }
+    if constexpr (LV > 0 && TRICK) {
+#pragma unroll
+        for (int z = 0; z < NZ; ++z)
+#pragma unroll
+            for (int t = 0; t < 3; ++t) acc[7 * z + 4 + t] = acc[7 * z + t] - acc[7 * z + 4 + t];
+    }
+    // combine the E entry groups (same slices: lanes j, j+LPE, ...), fixed order
+#pragma unroll
+    for (int o = LPE; o < 32; o <<= 1)
+#pragma unroll
+        for (int i = 0; i < NA; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    // red[t][slot]: t = 0..2 z-low H,V,D; 3..6 z-high A,H,V,D
+    if (grp == 0) {
+        if constexpr (LV > 0) {
+#pragma unroll
+            for (int z = 0; z < NZ; ++z)
+#pragma unroll
+                for (int t = 0; t < 7; ++t) red[wib][t][j * NZ + z] = acc[7 * z + t];
+        } else {
+#pragma unroll
+            for (int t = 0; t < 7; ++t) red[wib][t][j] = acc[t];
+        }
+    }
+    __syncwarp();
+    const double cls = cpow3(l) * kTwo896;
+    const int nk = nzl >> l, hl = ny >> l, wl = nx >> l, dl = nk;
+    const int bi = (int)(b / wl), bj = (int)(b % wl);
+    const int per = LV > 0 ? 1 : ((1 << l) / S);   // red slots per z-block
+    for (int k = lane; k < nk; k += 32) {
+        if (!act[off.off[l] + ((uint64_t)k * hl + bi) * wl + bj]) continue;
+        const int zz[7] = {k, k, k, dl + k, dl + k, dl + k, dl + k};
+        const int yy[7] = {hl + bi, bi, hl + bi, bi, hl + bi, bi, hl + bi};
+        const int xx[7] = {bj, wl + bj, wl + bj, bj, bj, wl + bj, wl + bj};
+#pragma unroll
+        for (int t = 0; t < 7; ++t) {
+            double sum = red[wib][t][k * per];
+            for (int gg = 1; gg < per; ++gg) sum += red[wib][t][k * per + gg];
+            bm[tmap.L ? coef_tile_pos(tmap, l, yy[t], xx[t], zz[t]) : ((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]] =
+                sum * cls;
+        }
+    }
+    __syncwarp();
+}
+template <int P, int E, bool TRICK, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) k_split3p(uint64_t nlist, const uint2* __restrict__ list, int nx, int ny,
+                                                 int nzl, const unsigned long long* __restrict__ ptr,
+                                                 const unsigned* __restrict__ eray, const float4* __restrict__ epsi,
+                                                 const float* __restrict__ q, const uint8_t* __restrict__ act,
+                                                 ActOff off, ActOff koff, double* __restrict__ bm, TileMap tmap) {
+    constexpr int S = P * E / 32;
+    __shared__ double red[4][7][P / 2];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nlist; it += W) {
+        const unsigned b = list[it].x;
+        const int l = (int)list[it].y;
+        const uint64_t key = koff.off[l] + b;
+        const uint64_t e0 = ptr[key], e1 = ptr[key + 1];
+#define SP(LVv) split3p_block<P, E, LVv, TRICK>(b, l, lane, wib, nx, ny, nzl, e0, e1, eray, epsi, q, act, off, bm, tmap, red)
+        if (l == 1) SP(1);
+        else if (l == 2) SP(2);
+        else if (S == 8 && l == 3) { if constexpr (S == 8) SP(3); }
+        else SP(0);
+#undef SP
+    }
+}
+
+// ---- split, CTA per block with a cp.async ring (k_split3c) -------------------
+// k_split3p is bound by memory latency, not by instructions: with 12-16 warps
+// per SM and one q row (P*4 bytes) per entry in flight per entry group, about
+// 12-16 KB per SM are in flight, which by Little's law caps the gathers near
+// 2-4 TB/s whatever the instruction count (cfg4: 7.6e9 entries/s x 512 B).  Here
+//  * the q rows travel by cp.async into a per-warp ring of D rounds in shared
+//    memory (no registers held by loads in flight); each lane copies and later
+//    reads back only its own S slices, so no barrier is needed between the two;
+//  * (ray, psi) are read 32 entries at a time, coalesced, one entry per lane,
+//    into a double-buffered per-warp index buffer (instead of every lane of a
+//    group loading its group's entry each round);
+//  * WPI warps share one block: each takes a contiguous range of the block's
+//    entries, so only 1/WPI as many blocks are in flight and, with the list in
+//    Morton order, their rays' q rows stay L2-resident.  The warps' partial
+//    sums meet in shared memory in warp order (deterministic).
+// Per-entry arithmetic = split3p (per-half sums, c^l factored out, L - Pq).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+// f2d_scaled by ONE 32x32->64 multiply by 2^29 (IMAD.WIDE: lo = u << 29, hi = u >> 3;
+// signed: the sign-extending multiply leaves ssss in hi[31:28], one AND keeps s at
+// bit 31).  Slower than the shifts in the slab SpMM (kernels3d.cuh) but faster here,
+// where the ALU pipe carries the min/select work: cfg4 split 1595 vs 2095 ms per run
+// with k_split3p (profiles/r07/ab1.txt, ab2.txt).
+template <bool SIGNED>
+__device__ __forceinline__ double f2d_wide(float f) {
+    if constexpr (SIGNED) {
+        long long w;   // inline PTX: nvcc strength-reduces the C++ multiply into shifts again
+        asm("mul.wide.s32 %0, %1, 536870912;" : "=l"(w) : "r"(__float_as_int(f)));
+        return __hiloint2double((int)(w >> 32) & (int)0x8fffffff, (int)(unsigned)w);
+    } else {
+        unsigned long long w;
+        asm("mul.wide.u32 %0, %1, 536870912;" : "=l"(w) : "r"(__float_as_uint(f)));
+        return __longlong_as_double((long long)w);
+    }
+}
+template <int S, int LV, bool TRICK>
+__device__ __forceinline__ void split3_consume(const float4& ps, const float (&f)[S], bool hh,
+                                               double (&acc)[LV > 0 ? 7 * (S >> LV) : 7]) {
+    constexpr int HS = LV > 0 ? (1 << (LV - 1)) : S;
+    constexpr int NZ = LV > 0 ? S / (2 * HS) : 1;
+    const float pf[4] = {ps.x, ps.y, ps.z, ps.w};
+    double m[8];
+    if constexpr (LV > 0) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) m[t] = (double)fminf(pf[t], 0.f);
+        m[4] = (double)fminf(-pf[0], 0.f);
+#pragma unroll
+        for (int t = 1; t < 4; ++t) m[4 + t] = TRICK ? (double)pf[t] : (double)fminf(-pf[t], 0.f);
+#pragma unroll
+        for (int z = 0; z < NZ; ++z) {
+            double qlo = f2d_wide<false>(f[z * 2 * HS]), qhi = f2d_wide<false>(f[z * 2 * HS + HS]);
+#pragma unroll
+            for (int i = 1; i < HS; ++i) {
+                qlo += f2d_wide<false>(f[z * 2 * HS + i]);
+                qhi += f2d_wide<false>(f[z * 2 * HS + HS + i]);
+            }
+            const double qall = qlo + qhi;
+            double* a = acc + 7 * z;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) a[t] = fma(m[1 + t], qall, a[t]);
+            a[3] = fma(m[4], qhi, fma(m[0], qlo, a[3]));
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                if constexpr (TRICK) a[4 + t] = fma(m[5 + t], qhi, a[4 + t]);
+                else a[4 + t] = fma(m[5 + t], qhi, fma(m[1 + t], qlo, a[4 + t]));
+            }
+        }
+    } else {
+#pragma unroll
+        for (int t = 1; t < 4; ++t) m[t - 1] = f2d_wide<true>(fminf(pf[t], 0.f));
+#pragma unroll
+        for (int t = 0; t < 4; ++t) m[3 + t] = f2d_wide<true>(fminf(hh ? -pf[t] : pf[t], 0.f));
+        double qs = f2d_wide<false>(f[0]);
+#pragma unroll
+        for (int i = 1; i < S; ++i) qs += f2d_wide<false>(f[i]);
+        qs *= kTwo896;   // exact: the multipliers carry the 2^-896 here
+#pragma unroll
+        for (int t = 0; t < 7; ++t) acc[t] = fma(m[t], qs, acc[t]);
+    }
+}
+template <int P, int E, int D, int WPI>
+struct Split3cSmem {
+    static constexpr int S = P * E / 32;
+    float4 ring[4][D][S / 4][32];   // [warp][round % D][16-byte part][lane]
+    unsigned iray[4][2][32];        // [warp][batch % 2][entry]
+    float4 ipsi[4][2][32];
+    double red[4][7][P / 2];
+};
+template <int P, int E, int LV, bool TRICK, int D, int WPI>
+__device__ __forceinline__ void split3c_block(unsigned b, int l, int lane, int wib, int nx, int ny, int nzl,
+                                              uint64_t e0, uint64_t e1, const unsigned* __restrict__ eray,
+                                              const float4* __restrict__ epsi, const float* __restrict__ q,
+                                              const uint8_t* __restrict__ act, const ActOff& off,
+                                              double* __restrict__ bm, const TileMap& tmap,
+                                              Split3cSmem<P, E, D, WPI>& sm) {
+    constexpr int LPE = 32 / E, S = P * E / 32;
+    static_assert(S == 4 || S == 8, "slices per lane");
+    static_assert(32 % E == 0 && (32 / E) >= 1, "entry groups");
+    constexpr int HS = LV > 0 ? (1 << (LV - 1)) : S;
+    constexpr int NZ = LV > 0 ? S / (2 * HS) : 1;
+    static_assert(LV == 0 || 2 * HS <= S, "level does not fit a lane");
+    constexpr int NA = LV > 0 ? 7 * NZ : 7;
+    constexpr int RPB = 32 / E;   // rounds per index batch (32 entries)
+    static_assert(D >= 2 && D - 1 <= RPB, "the ring may reach at most one index batch ahead");
+    const int grp = lane / LPE, j = lane % LPE;
+    const bool hh = LV == 0 ? (((j * S) >> (l - 1)) & 1) != 0 : false;
+    double acc[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) acc[i] = 0.0;
+    // this warp's entries [ws, we): contiguous chunks, multiples of 32 entries
+    const int wi = WPI == 1 ? 0 : wib;
+    const uint64_t n = e1 - e0;
+    const uint64_t chunk = ((n + WPI - 1) / WPI + 31) / 32 * 32;
+    const uint64_t ws0 = e0 + (uint64_t)wi * chunk, ws = ws0 < e1 ? ws0 : e1, we = ws + chunk < e1 ? ws + chunk : e1;
+    const uint64_t nr = (we - ws + E - 1) / E;
+    const uint64_t nbat = (we - ws + 31) / 32;
+    unsigned ry = 0;
+    float4 rp = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto ldg_batch = [&](uint64_t k) {   // lane i: entry ws + 32k + i
+        const uint64_t ee = ws + 32 * k + lane;
+        const bool ok = ee < we;
+        ry = __ldg(eray + (ok ? ee : ws));
+        rp = ok ? __ldg(epsi + ee) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    auto sts_batch = [&](uint64_t k) {
+        sm.iray[wib][k & 1][lane] = ry;
+        sm.ipsi[wib][k & 1][lane] = rp;
+    };
+    auto issue_q = [&](uint64_t r) {   // q row parts of round r into ring slot r % D
+        if (r < nr) {
+            const unsigned y = sm.iray[wib][(r / RPB) & 1][(r % RPB) * E + grp];
+            const float4* row = reinterpret_cast<const float4*>(q + (uint64_t)y * P + j * S);
+#pragma unroll
+            for (int v = 0; v < S / 4; ++v) cp_async16(&sm.ring[wib][r % D][v][lane], row + v);
+        }
+        cp_async_commit();
+    };
+    if (nr > 0) {
+        ldg_batch(0);
+        sts_batch(0);
+        if (nbat > 1) ldg_batch(1);
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < D - 1; ++r) issue_q(r);   // all in batch 0 (D - 1 <= RPB)
+        for (uint64_t r = 0; r < nr; ++r) {
+            const uint64_t ra = r + D - 1;   // round whose q goes out now
+            if (ra % RPB == 0 && ra / RPB < nbat) {
+                const uint64_t k = ra / RPB;   // batch k's registers -> shared, fetch batch k + 1
+                __syncwarp();                  // every lane is done reading buffer k & 1 (batch k - 2)
+                sts_batch(k);
+                if (k + 1 < nbat) ldg_batch(k + 1);
+                __syncwarp();
+            }
+            issue_q(ra);
+            const float4 ps = sm.ipsi[wib][(r / RPB) & 1][(r % RPB) * E + grp];
+            cp_async_wait<D - 1>();
+            float f[S];
+#pragma unroll
+            for (int v = 0; v < S / 4; ++v) {
+                const float4 t4 = sm.ring[wib][r % D][v][lane];
+                f[4 * v] = t4.x; f[4 * v + 1] = t4.y; f[4 * v + 2] = t4.z; f[4 * v + 3] = t4.w;
+            }
+            split3_consume<S, LV, TRICK>(ps, f, hh, acc);
+        }
+        cp_async_wait<0>();
+    }
+    if constexpr (LV > 0 && TRICK) {
+#pragma unroll
+        for (int z = 0; z < NZ; ++z)
+#pragma unroll
+            for (int t = 0; t < 3; ++t) acc[7 * z + 4 + t] = acc[7 * z + t] - acc[7 * z + 4 + t];
+    }
+#pragma unroll
+    for (int o = LPE; o < 32; o <<= 1)
+#pragma unroll
+        for (int i = 0; i < NA; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    if (grp == 0) {
+        if constexpr (LV > 0) {
+#pragma unroll
+            for (int z = 0; z < NZ; ++z)
+#pragma unroll
+                for (int t = 0; t < 7; ++t) sm.red[wib][t][j * NZ + z] = acc[7 * z + t];
+        } else {
+#pragma unroll
+            for (int t = 0; t < 7; ++t) sm.red[wib][t][j] = acc[t];
+        }
+    }
+    if constexpr (WPI == 1) __syncwarp(); else __syncthreads();
+    const double cls = cpow3(l) * kTwo896;
+    const int nk = nzl >> l, hl = ny >> l, wl = nx >> l, dl = nk;
+    const int bi = (int)(b / wl), bj = (int)(b % wl);
+    const int per = LV > 0 ? 1 : ((1 << l) / S);   // red slots per z-block
+    const int t0 = WPI == 1 ? lane : (int)threadIdx.x, tstep = WPI == 1 ? 32 : 32 * WPI;
+    for (int k = t0; k < nk; k += tstep) {
+        if (!act[off.off[l] + ((uint64_t)k * hl + bi) * wl + bj]) continue;
+        const int zz[7] = {k, k, k, dl + k, dl + k, dl + k, dl + k};
+        const int yy[7] = {hl + bi, bi, hl + bi, bi, hl + bi, bi, hl + bi};
+        const int xx[7] = {bj, wl + bj, wl + bj, bj, bj, wl + bj, wl + bj};
+#pragma unroll
+        for (int t = 0; t < 7; ++t) {
+            double tot = 0.0;
+            for (int w = (WPI == 1 ? wib : 0); w < (WPI == 1 ? wib + 1 : WPI); ++w) {   // warp order
+                double sum = sm.red[w][t][k * per];
+                for (int gg = 1; gg < per; ++gg) sum += sm.red[w][t][k * per + gg];
+                tot = (WPI == 1) ? sum : tot + sum;
+            }
+            bm[tmap.L ? coef_tile_pos(tmap, l, yy[t], xx[t], zz[t]) : ((uint64_t)yy[t] * nx + xx[t]) * P + zz[t]] =
+                tot * cls;
+        }
+    }
+    if constexpr (WPI == 1) __syncwarp(); else __syncthreads();
+}
+template <int P, int E, bool TRICK, int D, int WPI, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_split3c(uint64_t nlist, const uint2* __restrict__ list, int nx, int ny,
+                                                       int nzl, const unsigned long long* __restrict__ ptr,
+                                                       const unsigned* __restrict__ eray,
+                                                       const float4* __restrict__ epsi, const float* __restrict__ q,
+                                                       const uint8_t* __restrict__ act, ActOff off, ActOff koff,
+                                                       double* __restrict__ bm, TileMap tmap,
+                                                       unsigned long long* __restrict__ ctr) {
+    static_assert(WPI == 1 || WPI == 4, "warps per item");
+    constexpr int S = P * E / 32;
+    __shared__ Split3cSmem<P, E, D, WPI> sm;
+    __shared__ unsigned long long s_it;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    // Items are handed out in list (Morton) order from one counter, so the blocks
+    // in flight are always consecutive list items: a static grid stride lets the
+    // workers drift apart (items differ 2x in length) and with them the window of
+    // q rows that should stay in L2.
+    for (;;) {
+        uint64_t it;
+        if constexpr (WPI == 1) {
+            unsigned long long v = 0;
+            if (lane == 0) v = atomicAdd(ctr, 1ull);
+            it = __shfl_sync(0xffffffffu, v, 0);
+        } else {
+            if (threadIdx.x == 0) s_it = atomicAdd(ctr, 1ull);
+            __syncthreads();
+            it = s_it;
+            __syncthreads();
+        }
+        if (it >= nlist) break;
+        const unsigned b = list[it].x;
+        const int l = (int)list[it].y;
+        const uint64_t key = koff.off[l] + b;
+        const uint64_t e0 = ptr[key], e1 = ptr[key + 1];
+#define SP(LVv) split3c_block<P, E, LVv, TRICK, D, WPI>(b, l, lane, wib, nx, ny, nzl, e0, e1, eray, epsi, q, act, off, bm, tmap, sm)
+        if (l == 1) SP(1);
+        else if (l == 2) SP(2);
+        else if (S == 8 && l == 3) { if constexpr (S == 8) SP(3); }
+        else SP(0);
+#undef SP
+    }
+}
+
 // ---- split, lane per ACTIVE z-block (opt-in WAMGPU_SPLIT_VARIANT=7; measured 2x
 // slower than k_split3h_e: its 8-byte per-lane q loads are scattered over the row,
 // the multipliers are prepared per z-block instead of per 4 z-blocks, and most

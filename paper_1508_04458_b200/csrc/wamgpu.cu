@@ -37,6 +37,7 @@
 #include "kernels3t.cuh"
 #include "kernels_ar.cuh"
 #include "kernels_phi.cuh"
+#include "kernels3c.cuh"
 
 namespace wamgpu {
 
@@ -140,7 +141,7 @@ struct DBuf {
     void swap(DBuf& o) { std::swap(p, o.p); std::swap(n, o.n); }
 };
 
-enum Cat { T_FWD = 0, T_BACK, T_SPLIT, T_UPDATE, T_EXPAND, T_COMM, T_PHI, T_NCAT };
+enum Cat { T_FWD = 0, T_BACK, T_SPLIT, T_UPDATE, T_EXPAND, T_COMM, T_PHI, T_FWDC, T_BACKC, T_NCAT };
 
 // In-process rank group (wamgpu_set_comm_local): R contexts driven by R host
 // threads of one process.  Collectives are a device-side rank-order reduction
@@ -250,6 +251,19 @@ struct wamgpu_ctx {
     DBuf<uint2> sidx3;                  // Psi sort output (persistent)
     DBuf<float4> E3psi, ppsi_s;
     DBuf<uint2> list3;                  // (in-plane block, level) with any active z-block
+    // block-coarsened matrices Hc, c = 2^k (kernels3c.cuh): built once per matrix and level
+    struct Coarse {
+        bool ok = false;
+        uint64_t nnz = 0, Nc = 0;
+        DBuf<unsigned long long> rp, cp;
+        DBuf<unsigned> col, row, order;
+        DBuf<double> val, valC;
+    } coarse[6];   // index k = 1 .. LMAX
+    DBuf<float> mu_c;                   // mu on the coarse grid (forward operand)
+    DBuf<double> g_c;                   // block sums of g (coarse back projection)
+    int fine_level = 0;                 // finest level with an active block (0: none)
+    std::vector<std::vector<unsigned>> morton;   // per level: in-plane blocks in Morton order (host, cached)
+    int morton_nx = 0, morton_ny = 0;
     uint64_t nlist3 = 0;
     int walk_nlev = 1;
     ActOff off{};
@@ -298,7 +312,8 @@ struct wamgpu_ctx {
         uint64_t n = 0;
     } ar;
     DBuf<unsigned long long> counters;
-    DBuf<int> flag, it;
+    DBuf<int> flag, flag2, it;
+    DBuf<unsigned long long> split_ctr;   // work counter of k_split3c
     DBuf<double> objs;
     DBuf<unsigned long long> cums;
     int iter = 0;
@@ -629,6 +644,11 @@ static void finish_matrix(Ctx* c, bool have_csc = false) {
     c->blo.release(); c->bhi.release(); c->lacc.release();
     c->phiA_ok = false;
     c->phiA_L = -1;
+    for (auto& cm : c->coarse) {
+        cm.ok = false;
+        cm.rp.release(); cm.cp.release(); cm.col.release(); cm.row.release(); cm.order.release();
+        cm.val.release(); cm.valC.release();
+    }
     c->phiA_rp.release(); c->phiA_cp.release(); c->phiA_col.release(); c->phiA_row.release();
     c->phiA_val.release(); c->phiA_valC.release(); c->phiA_part.release();
     // CSC mirror (system_matrix.hpp:61-75): stable radix sort of CSR entries by
@@ -1249,17 +1269,21 @@ static unsigned fwd3_launch_p(Ctx* c, const float* mu, double* l, unsigned maxbl
     k_fwd3s_band<MODE, S::LPR, S::SPL, UXv, 3, SG, P, 8, 2><<<nb, 256, 0, c->st>>>(                                \
         c->Ml, c->nzl, b, B, c->rp.p, c->blo.p, c->bhi.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, acc, l,             \
         c->partial.p, c->flag.p)
-#define BAND2(SG)                                                                                                  \
-    k_fwd3s_band<MODE, S::LPR, S::SPL, 104, 2, SG, P, 8, 2><<<nb, 256, 0, c->st>>>(                                \
+#define BANDN(NFv, SG)                                                                                             \
+    k_fwd3s_band<MODE, S::LPR, S::SPL, 104, NFv, SG, P, 8, 2><<<nb, 256, 0, c->st>>>(                              \
         c->Ml, c->nzl, b, B, c->rp.p, c->blo.p, c->bhi.p, c->A.p, mu, c->I0.p, c->d.p, c->q.p, acc, l,             \
         c->partial.p, c->flag.p)
+#define BAND2(SG) BANDN(2, SG)
         for (int b = 0; b < B; ++b) {
             if (v == 18 || v == 12) { if (uns) BAND2(false); else BAND2(true); }   // NF 2: cfg4 63.0-63.7 vs 64.1-64.6 ms
+            else if (v == 20) { if (uns) BANDN(1, false); else BANDN(1, true); }
+            else if (v == 21) { if (uns) BANDN(0, false); else BANDN(0, true); }
             else if (v != 19) { if (uns) BAND(104, false); else BAND(104, true); }
             else { if (uns) BAND(4, false); else BAND(4, true); }
         }
 #undef BAND
 #undef BAND2
+#undef BANDN
         launched(c, B - 1);
         return nb;
     }
@@ -1385,6 +1409,7 @@ static void back_launch(Ctx* c, const float* w, double* out, const double* bam, 
     check_launch(c, "k_back3");
     c->timer_end(T_BACK);
     c->tm.back_launches++;
+    c->tm.proj_entries += (int64_t)c->nnz;
 }
 // nonneg: w >= 0 with no -0.0 (q, d); false for caller-supplied vectors
 static void back_into(Ctx* c, const float* w, double* out, bool nonneg = true) {
@@ -1424,6 +1449,7 @@ static void back_allreduce(Ctx* c, const float* w, const double* extra) {
     check_launch(c, "k_fused_allreduce");
     c->timer_end(T_BACK);
     c->tm.back_launches++;
+    c->tm.proj_entries += (int64_t)c->nnz;
 }
 
 // plain l = H mu (fp64 out), for forward_project
@@ -1445,10 +1471,14 @@ static void forward_plain(Ctx* c, const float* mu, double* l) {
     check_launch(c, "k_forward3");
 }
 
+static int coarse_k(const Ctx* c);
+static unsigned fwd3c_launch(Ctx* c, int k, unsigned maxblk);
 // q = I0 exp(-H mu), objective -> scal[0] (all-reduced), record
 static void forward_fused(Ctx* c, bool record) {
-    c->timer_begin(T_FWD);
+    const int ck = (c->nzl > 1 && c->algo == 2) ? coarse_k(c) : 0;
+    c->timer_begin(ck > 0 ? T_FWDC : T_FWD);
     int nparts = c->nblk_row;
+    uint64_t entries = c->nnz;
     if (c->nzl == 1) {
 #define FV(FGv, U, MB)                                                                                              \
     if (c->lgx >= 0)                                                                                               \
@@ -1502,11 +1532,13 @@ static void forward_fused(Ctx* c, bool record) {
 #undef FP
 #undef FV
     } else {
-        nparts = (int)fwd3_launch<1>(c, c->mu.p, nullptr, (unsigned)c->partial.n, c->algo == 1 && c->mu_nonneg);
+        if (ck > 0) { nparts = (int)fwd3c_launch(c, ck, (unsigned)c->partial.n); entries = c->coarse[ck].nnz; }
+        else nparts = (int)fwd3_launch<1>(c, c->mu.p, nullptr, (unsigned)c->partial.n, c->algo == 1 && c->mu_nonneg);
     }
     check_launch(c, "k_forward3");
-    c->timer_end(T_FWD);
-    c->tm.fwd_launches++;
+    c->timer_end(ck > 0 ? T_FWDC : T_FWD);
+    if (ck > 0) c->tm.coarse_fwd_launches++; else c->tm.fwd_launches++;
+    c->tm.proj_entries += (int64_t)entries;
     k_sum_partials<<<1, 1024, 0, c->st>>>(c->partial.p, nparts, c->scal.p);
     check_launch(c, "k_sum_partials");
     allreduce_sum(c, c->scal.p, 1);
@@ -1610,7 +1642,7 @@ static void upload_tree3(Ctx* c, int* nlev_out) {
     std::vector<unsigned> w, zw;
     uint64_t bit = 0, zo = 0, ko = 0;
     for (int l = 0; l <= LMAX + 1; ++l) c->boff.off[l] = c->zoff.off[l] = c->koff.off[l] = 0;
-    int nlev = 0;
+    int nlev = 0, fine = 0;
     bool chain = true;
     std::vector<uint2> lst;
     for (int l = c->L; l >= 1; --l) {
@@ -1646,18 +1678,22 @@ static void upload_tree3(Ctx* c, int* nlev_out) {
             parts[t].swap(mine);
             if (any) any_l = true;
         });
-        const size_t lv0 = lst.size();
-        for (auto& v : parts) lst.insert(lst.end(), v.begin(), v.end());
         // The split gathers one q row per Psi entry and every block's list spans all
-        // views.  In row-major block order the ~1e4 warps in flight cover a few full
-        // image rows, i.e. nearly every ray: the q slab (cfg4: 755 MB) streams from
-        // DRAM again and again (ncu: 222 GB per launch, 27% L2 hits).  Morton order
-        // keeps the blocks in flight inside a compact square whose rays' q rows fit L2.
-        // (The split writes by block index, so the order is free.)
+        // views.  In row-major block order the blocks in flight cover a few full image
+        // rows, i.e. nearly every ray: the q slab (cfg4: 755 MB) streams from DRAM again
+        // and again (ncu: 222 GB per launch, 27% L2 hits).  Morton order keeps the blocks
+        // in flight inside a compact square.  (The split writes by block index, so the
+        // order is free.)  WAMGPU_SPLIT_ORDER=0: row-major.
         static const int split_order = [] { const char* e = std::getenv("WAMGPU_SPLIT_ORDER"); return e ? std::atoi(e) : 1; }();
-        if (split_order == 1 && lst.size() > lv0) {
-            const unsigned wl = (unsigned)(c->nx >> l);
-            auto morton = [](unsigned x, unsigned y) {
+        if (split_order == 1) {
+            if (c->morton_nx != c->nx || c->morton_ny != c->ny) {
+                c->morton.clear();
+                c->morton_nx = c->nx; c->morton_ny = c->ny;
+            }
+            if ((int)c->morton.size() <= l) c->morton.resize(l + 1);
+            std::vector<unsigned>& perm = c->morton[l];
+            if (perm.size() != nb) {   // once per grid and level
+                const unsigned wl = (unsigned)(c->nx >> l);
                 auto spread = [](uint64_t v) {
                     v = (v | (v << 16)) & 0x0000ffff0000ffffull;
                     v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
@@ -1666,12 +1702,20 @@ static void upload_tree3(Ctx* c, int* nlev_out) {
                     v = (v | (v << 1)) & 0x5555555555555555ull;
                     return v;
                 };
-                return spread(x) | (spread(y) << 1);
-            };
-            std::sort(lst.begin() + lv0, lst.end(), [&](const uint2& a, const uint2& b) {
-                return morton(a.x % wl, a.x / wl) < morton(b.x % wl, b.x / wl);
-            });
+                std::vector<std::pair<uint64_t, unsigned>> kv(nb);
+                for (uint64_t b = 0; b < nb; ++b) kv[b] = {spread(b % wl) | (spread(b / wl) << 1), (unsigned)b};
+                std::sort(kv.begin(), kv.end());
+                perm.resize(nb);
+                for (uint64_t b = 0; b < nb; ++b) perm[b] = kv[b].second;
+            }
+            for (uint64_t i = 0; i < nb; ++i) {
+                const uint64_t b = perm[i];
+                if ((w[(bit + b) >> 5] >> ((bit + b) & 31)) & 1u) lst.push_back(make_uint2((unsigned)b, (unsigned)l));
+            }
+        } else {
+            for (auto& v : parts) lst.insert(lst.end(), v.begin(), v.end());
         }
+        if (any_l) fine = l;   // levels run L..1: the last hit is the finest
         if (chain && any_l) ++nlev; else chain = false;
         bit = (bit + nb + 31) / 32 * 32;
         zo += nb * W;
@@ -1685,6 +1729,7 @@ static void upload_tree3(Ctx* c, int* nlev_out) {
     c->zbits.ensure(zw.size());
     CK(cudaMemcpyAsync(c->tbits.p, w.data(), w.size() * 4, cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(c->zbits.p, zw.data(), zw.size() * 4, cudaMemcpyHostToDevice, c->st));
+    c->fine_level = fine;
     c->nlist3 = lst.size();
     c->list3.ensure(std::max<size_t>(lst.size(), 1));
     if (!lst.empty()) CK(cudaMemcpyAsync(c->list3.p, lst.data(), lst.size() * 8, cudaMemcpyHostToDevice, c->st));
@@ -1834,7 +1879,7 @@ static void end_call(Ctx* c) {
     CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
     c->tm.total_ms = ms;
     double* dst[T_NCAT] = {&c->tm.fwd_ms, &c->tm.back_ms, &c->tm.split_ms, &c->tm.update_ms, &c->tm.expand_ms,
-                           &c->tm.comm_ms, &c->tm.phi_ms};
+                           &c->tm.comm_ms, &c->tm.phi_ms, &c->tm.coarse_fwd_ms, &c->tm.coarse_back_ms};
     for (int k = 0; k < T_NCAT; ++k) {
         double s = 0.0;
         for (size_t i = 0; i < c->tev_used[k]; ++i) {
@@ -2372,6 +2417,7 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     c->Z0 = compute_z0(c, L, true);
     c->nlist = 0;
     c->nlist3 = 0;
+    c->fine_level = 0;
     c->nnz_phi = 0;
     c->phi_batch = 0;
     if (!c->haar3) {                     // 3D: the tree is empty, no Psi lists yet
@@ -2460,6 +2506,141 @@ static void build_phiA(Ctx* c) {
     c->phiA_L = c->L;
     c->phiA_ok = true;
 }
+// ---- block-coarsened projections (kernels3c.cuh) ---------------------------
+// WAMGPU_COARSE=0: always project over H.  WAMGPU_COARSE_CHECK=1: verify on
+// the device, before every coarse forward, that mu is constant on the blocks.
+static bool coarse_enabled() {   // read per call: tests switch it between contexts
+    const char* e = std::getenv("WAMGPU_COARSE");
+    return !(e && e[0] == '0');
+}
+// coarsening exponent k (block edge 2^k) the current tree allows; 0 = project over H
+static int coarse_k(const Ctx* c) {
+    if (!coarse_enabled() || !c->haar3 || c->nzl <= 1 || !c->phiA_beta_ok || view_sharded(c)) return 0;
+    if (c->fine_level <= 1) return 0;
+    const int k = std::min(c->fine_level - 1, LMAX);
+    if ((c->nx >> k) << k != c->nx || (c->ny >> k) << k != c->ny || slab_stride(c) < 8) return 0;
+    return k;
+}
+static void build_coarse(Ctx* c, int k) {
+    Ctx::Coarse& m = c->coarse[k];
+    if (m.ok) return;
+    m.Nc = (uint64_t)(c->nx >> k) * (c->ny >> k);
+    m.rp.alloc(c->Ml + 1);
+    k_coarse_count<<<blocks_for(c->Ml + 1, 128), 128, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, k, m.rp.p);
+    check_launch(c, "k_coarse_count");
+    exclusive_scan_u64(c, m.rp.p, c->Ml + 1);
+    unsigned long long nnz = 0;
+    CK(cudaMemcpyAsync(&nnz, m.rp.p + c->Ml, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    const uint64_t n1 = std::max<unsigned long long>(nnz, 1);
+    if (nnz >= (1ull << 32)) throw ConfigError("coarse matrix: more than 2^32 entries");
+    m.col.alloc(n1);
+    m.val.alloc(n1);
+    DBuf<unsigned> kin, kout;
+    DBuf<uint2> vin, vout;
+    kin.alloc(n1);
+    vin.alloc(n1);
+    k_coarse_fill<<<blocks_for(c->Ml, 128), 128, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->nx, k, m.rp.p, m.col.p,
+                                                              m.val.p, kin.p, vin.p);
+    check_launch(c, "k_coarse_fill");
+    sort_pairs(c, kin, vin, kout, vout, nnz, m.Nc);
+    kin.release();
+    vin.release();
+    m.row.alloc(n1);
+    m.valC.alloc(n1);
+    if (nnz) {
+        k_phiA_gather<<<blocks_for(nnz, 256), 256, 0, c->st>>>(nnz, vout.p, m.val.p, m.row.p, m.valC.p);
+        check_launch(c, "k_phiA_gather");
+    }
+    m.cp.alloc(m.Nc + 1);
+    k_bounds<<<blocks_for(m.Nc + 1, 256), 256, 0, c->st>>>(kout.p, nnz, m.Nc, m.cp.p);
+    check_launch(c, "k_bounds");
+    {   // coarse blocks in 16 x 16 tile order (as build_tile_order)
+        std::vector<unsigned> o;
+        o.reserve(m.Nc);
+        const int T = 16, wx = c->nx >> k, wy = c->ny >> k;
+        for (int ty = 0; ty < wy; ty += T)
+            for (int tx = 0; tx < wx; tx += T)
+                for (int iy = ty; iy < std::min(ty + T, wy); ++iy)
+                    for (int ix = tx; ix < std::min(tx + T, wx); ++ix) o.push_back((unsigned)(iy * wx + ix));
+        m.order.alloc(m.Nc);
+        CK(cudaMemcpyAsync(m.order.p, o.data(), m.Nc * 4, cudaMemcpyHostToDevice, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
+    c->cub_tmp.release();
+    m.nnz = nnz;
+    m.ok = true;
+}
+// l = Hc mu_c fused with q = I0 exp(-l) and the I-divergence partials; returns the partial count
+template <int P>
+static unsigned fwd3c_launch_p(Ctx* c, int k, unsigned maxblk) {
+    using S = SlabShape<P>;
+    Ctx::Coarse& m = c->coarse[k];
+    const unsigned nb = std::min<unsigned>(nblk_warp(c, (c->Ml + S::G - 1) / S::G), maxblk);
+    k_fwd3s<1, S::LPR, S::SPL, 104, 2, true, P, 8, 2, Ent64><<<nb, 256, 0, c->st>>>(
+        c->Ml, 0, c->nzl, m.rp.p, Ent64{m.col.p, m.val.p}, c->mu_c.p, c->I0.p, c->d.p, c->q.p, nullptr,
+        c->partial.p, c->flag.p);
+    return nb;
+}
+static unsigned fwd3c_launch(Ctx* c, int k, unsigned maxblk) {
+    build_coarse(c, k);
+    Ctx::Coarse& m = c->coarse[k];
+    const int P = slab_stride(c);
+    c->mu_c.ensure(m.Nc * P);
+    if (std::getenv("WAMGPU_COARSE_CHECK") != nullptr) {
+        CK(cudaMemsetAsync(c->flag2.p, 0, 4, c->st));
+        k_mu_coarse_check<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->N, c->nx, k, P, c->nzl, c->mu.p, c->flag2.p);
+        int bad = 0;
+        CK(cudaMemcpyAsync(&bad, c->flag2.p, 4, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        if (bad) throw NumericError("coarse projection: mu is not constant on the 2^k blocks");
+    }
+    k_mu_coarse<<<blocks_for(m.Nc * (P / 4), 256), 256, 0, c->st>>>(m.Nc, c->nx >> k, c->nx, k, P, c->mu.p, c->mu_c.p);
+    check_launch(c, "k_mu_coarse");
+    unsigned nb = 0;
+    switch (P) {
+        case 8: nb = fwd3c_launch_p<8>(c, k, maxblk); break;
+        case 16: nb = fwd3c_launch_p<16>(c, k, maxblk); break;
+        case 32: nb = fwd3c_launch_p<32>(c, k, maxblk); break;
+        case 64: nb = fwd3c_launch_p<64>(c, k, maxblk); break;
+        default: nb = fwd3c_launch_p<128>(c, k, maxblk); break;
+    }
+    check_launch(c, "k_fwd3s (coarse)");
+    launched(c, 1);
+    return nb;
+}
+// g = expand(Hc^T w): block sums over the coarse CSC, then the block mean on every pixel
+template <int P>
+static void back3c_launch_p(Ctx* c, int k, const float* w) {
+    using S = SlabShape<P>;
+    Ctx::Coarse& m = c->coarse[k];
+    const unsigned nb = nblk_warp(c, (m.Nc + S::G - 1) / S::G);
+    k_back3s<0, S::LPR, S::SPL, 104, 1, false, P, 8, 2, Ent64><<<nb, 256, 0, c->st>>>(
+        m.Nc, 0, c->nzl, m.order.p, m.cp.p, Ent64{m.row.p, m.valC.p}, w, c->g_c.p, nullptr, nullptr, 0.0,
+        c->flag.p, TileMap{});
+}
+static void back3c_into(Ctx* c, int k, const float* w, double* out) {
+    build_coarse(c, k);
+    Ctx::Coarse& m = c->coarse[k];
+    const int P = slab_stride(c);
+    c->g_c.ensure(m.Nc * P);
+    c->timer_begin(T_BACKC);
+    switch (P) {
+        case 8: back3c_launch_p<8>(c, k, w); break;
+        case 16: back3c_launch_p<16>(c, k, w); break;
+        case 32: back3c_launch_p<32>(c, k, w); break;
+        case 64: back3c_launch_p<64>(c, k, w); break;
+        default: back3c_launch_p<128>(c, k, w); break;
+    }
+    check_launch(c, "k_back3s (coarse)");
+    k_g_expand<<<blocks_for(c->N * (P / 2), 256), 256, 0, c->st>>>(c->N, c->nx >> k, c->nx, k, P, c->g_c.p, out);
+    check_launch(c, "k_g_expand");
+    launched(c, 1);
+    c->timer_end(T_BACKC);
+    c->tm.coarse_back_launches++;
+    c->tm.proj_entries += (int64_t)m.nnz;
+}
+
 // one wavelet-AM iteration with only the roots active: S = Φ_Aᵀ q̂, root
 // solves, ℓ = Φ_A β fused with q̂ and the I-divergence (mu is left stale)
 static void phiA_step(Ctx* c) {
@@ -2644,7 +2825,9 @@ static void wam_step(Ctx* c) {
         back_launch(c, c->q.p, c->rs_send.p, nullptr, true, tm);   // g straight into the tile-major T
         CK(cudaEventRecord(c->ev_x, c->st));
     } else if (!fused) {
-        back_into(c, c->q.p, c->g.p);
+        const int ck = coarse_k(c);
+        if (ck > 0) back3c_into(c, ck, c->q.p, c->g.p);
+        else back_into(c, c->q.p, c->g.p);
     }
     if (c->haar3 && c->nlist3) {
         c->timer_begin(T_SPLIT);
@@ -2683,7 +2866,52 @@ static void wam_step(Ctx* c) {
                 default: S3Z(128) break;
             }
 #undef S3Z
-        } else {   // default: every z-block of a listed block, E entries in flight.
+        } else if (c->split_variant >= 10 && c->split_variant <= 14 && c->sband_B == 1 && P >= 64) {
+            // k_split3c: cp.async ring; 10: 4 warps per block, D 4; 11: warp per block; 12: 3 CTAs per SM; 13: D 6; 14: D 2
+#define S3C(Pv, Ev, Dv, Wv, Mv)                                                                                    \
+    {                                                                                                              \
+        const unsigned nbc = Wv == 1 ? nb : (unsigned)std::min<uint64_t>(c->nlist3, (uint64_t)c->sms * Mv);        \
+        CK(cudaMemsetAsync(c->split_ctr.p, 0, 8, c->st));                                                          \
+        k_split3c<Pv, Ev, true, Dv, Wv, Mv><<<nbc, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl,   \
+            c->np.p, c->E3ray.p, c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3, tm, c->split_ctr.p);          \
+    }
+#define S3CV(Pv, Ev)                                                                                               \
+    switch (c->split_variant) {                                                                                    \
+        case 10: S3C(Pv, Ev, 4, 4, 4) break;                                                                       \
+        case 11: S3C(Pv, Ev, 4, 1, 4) break;                                                                       \
+        case 12: S3C(Pv, Ev, 4, 4, 3) break;                                                                       \
+        case 13: S3C(Pv, Ev, 6, 4, 4) break;                                                                       \
+        default: S3C(Pv, Ev, 2, 4, 4) break;                                                                       \
+    }
+            if (P == 64) { S3CV(64, 4) } else { S3CV(128, 2) }
+#undef S3CV
+#undef S3C
+        } else if (c->split_variant == 9 && c->sband_B == 1 && P >= 64) {   // 128-register cap (4 CTAs per SM)
+            if (P == 64) k_split3p<64, 4, true, 4><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p,
+                                                      c->E3ray.p, c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3, tm);
+            else k_split3p<128, 2, true, 4><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p,
+                                                      c->E3ray.p, c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3, tm);
+        } else if ((c->split_variant == 0 || c->split_variant == 8) && c->sband_B == 1) {
+            // default: k_split3p (per-half q sums, c^l factored out, three-stage ping-pong pipeline);
+            // 8 = the same without the L - Pq form of z-high
+#define S3P(S, EE)                                                                                                 \
+    if (c->split_variant == 0)                                                                                     \
+        k_split3p<S, EE, true><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p,        \
+                                                      c->E3ray.p, c->E3psi.p, c->q.p, c->act.p, c->off, c->koff,   \
+                                                      bm3, tm);                                                    \
+    else                                                                                                           \
+        k_split3p<S, EE, false><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p,       \
+                                                       c->E3ray.p, c->E3psi.p, c->q.p, c->act.p, c->off, c->koff,  \
+                                                       bm3, tm);
+            switch (P) {
+                case 8: S3P(8, 16) break;
+                case 16: S3P(16, 8) break;
+                case 32: S3P(32, 4) break;
+                case 64: S3P(64, 4) break;
+                default: S3P(128, 2) break;
+            }
+#undef S3P
+        } else {   // k_split3h_e (WAMGPU_SPLIT_VARIANT=6, and the ray-banded split): every z-block of a listed block, E entries in flight.
                    // measured: cfg3 (64 slices) E=4 188 ms/run vs 364; cfg4 (128) E=2 1888 vs 2157 (E=4) / 2500;
                    // one pipelined round (U = 1) 182 ms/run at cfg3 vs 188 (U = 2) / 189 (U = 4).
                    // Sharded small slabs: S = P*E/32 = 4 slices per lane.
@@ -2969,6 +3197,8 @@ static Ctx* create(int device) {
     CK(cudaEventCreate(&c->ev_a));
     CK(cudaEventCreate(&c->ev_b));
     c->flag.alloc(1);
+    c->flag2.alloc(1);
+    c->split_ctr.alloc(1);
     c->it.alloc(1);
     c->counters.alloc(2);
     c->scal.alloc(8);
