@@ -557,7 +557,7 @@ def main():
     dev_ms, fwd_ms, back_ms, launches = [], [], [], 0
     fwd_n = back_n = 0
     split_ms = upd_ms = exp_ms = comm_ms = phi_ms = cfwd_ms = cback_ms = 0.0
-    phi_n = cfwd_n = cback_n = proj_entries = 0
+    phi_n = cfwd_n = cback_n = proj_updates = split_n = split_entries = 0
     split_nnz = 0
     plumb.barrier()
     with ClockSampler(local) as clk:
@@ -581,7 +581,9 @@ def main():
                 cback_ms += t["coarse_back_ms"]
                 cfwd_n += t["coarse_fwd_launches"]
                 cback_n += t["coarse_back_launches"]
-                proj_entries += t["proj_entries"]
+                proj_updates += t["proj_updates"]
+                split_n += t["split_launches"]
+                split_entries += t["split_entries"]
                 split_nnz = t["split_nnz"]
         wall = time.perf_counter() - t_wall
     plumb.barrier()
@@ -638,11 +640,30 @@ def main():
                      "k_back3s<...> (K3' slab back projection over the in-plane CSC)")
         dom = fwd_name if sum(fwd_ms) >= sum(back_ms) else back_name
         ach = fwd_gbs if sum(fwd_ms) >= sum(back_ms) else back_gbs
+        dom_bytes = fwd_bytes if sum(fwd_ms) >= sum(back_ms) else back_bytes
+        # 3D: with the block-coarsened projections the signed split can be the
+        # largest phase.  Its algorithmic HBM bytes per launch: the Psi stream
+        # (20 B per entry: ray + four fp32 psi), the q slab once and the 7
+        # coefficient planes it writes; the q-row gathers (P x 4 B per entry)
+        # are served by L2 and reported as the binding resource.
+        split_dom = nz > 1 and split_n > 0 and split_ms > max(sum(fwd_ms), sum(back_ms))
+        if split_dom:
+            split_avg = split_ms / split_n
+            ent_avg = split_entries / split_n
+            P_slab = 8
+            while P_slab < nz:
+                P_slab *= 2
+            split_bytes = 20 * ent_avg + 4 * Ml * nz + 8 * N * nz
+            dom = ("k_split3c<P,E,true,4,1,4> (signed split b- over the Psi lists of the separable 3D Haar tree; "
+                   "averaged over the launches of a run, the tree grows at every expansion)")
+            ach = split_bytes / (split_avg * 1e-3) / 1e9
+            dom_bytes = split_bytes
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as f:
                 tr = json.load(f)
-            traffic = tr.get(cfg["name"], {}).get("k_forward" if "forward" in dom else "k_back")
+            traffic = tr.get(cfg["name"], {}).get("k_split3c" if split_dom else
+                                                   "k_forward" if "forward" in dom else "k_back")
         except Exception:
             pass
         # 3D: the slab passes are not HBM-bound (one DFMA + one fp32->fp64
@@ -651,7 +672,15 @@ def main():
         # (64 DFMA lanes per clock per SM at the SM clock sampled under load)
         binding = None
         clocks = clk.summary()
-        if nz > 1:
+        if split_dom:
+            gather = ent_avg * P_slab * 4 / (split_avg * 1e-3)
+            binding = {"resource": "L2 -> SM sector traffic of the q-row gathers (one P x 4 B row per Psi entry, "
+                                   "L2-resident through the Morton-ordered block list; ncu lts throughput in "
+                                   "profiles/r07/ncu_split3c_cfg4*.txt)",
+                       "achieved": gather / 1e9, "unit": "GB/s gathered from L2", "peak": None, "frac": None,
+                       "entries_per_s": ent_avg / (split_avg * 1e-3),
+                       "evidence": "profiles/r07/ncu_split3c_cfg4_chunk.txt"}
+        elif nz > 1:
             mhz = clocks.get("sm_mhz") or 1965.0
             dom_ms = fwd_avg if sum(fwd_ms) >= sum(back_ms) else back_avg
             upd = nnz_local * nz / (dom_ms * 1e-3)
@@ -688,9 +717,9 @@ def main():
             # H passes only (forward + back launches; a 3D launch covers every
             # slice): the root-only iterations run over the approximation
             # columns Phi_A instead of H and are counted apart
-            # (updates actually executed: proj_entries counts the in-plane entries
-            # every forward / back launch streamed, H or a block-coarsened Hc)
-            "ray_voxel_updates_per_s": proj_entries * world / args.steps * nz / (ms_step * 1e-3),
+            # (updates actually executed: the library counts entries streamed x slices
+            # processed for every forward / back launch, H or a block-coarsened Hc)
+            "ray_voxel_updates_per_s": proj_updates * world / args.steps / (ms_step * 1e-3),
             "h_passes_per_step": (fwd_n + back_n) / args.steps,
             "coarse_passes_per_step": (cfwd_n + cback_n) / args.steps,
             "pixel_equivalent_updates_per_s": (fwd_n + back_n + cfwd_n + cback_n) / args.steps * nnz * nz
@@ -701,7 +730,7 @@ def main():
             "parity": parity,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
-                         "algorithmic_bytes": fwd_bytes if "forward" in dom else back_bytes,
+                         "algorithmic_bytes": dom_bytes,
                          "binding": binding},
             "kernels": {"fwd_avg_ms": fwd_avg, "fwd_gbs": fwd_gbs, "fwd_frac": fwd_gbs / hbm,
                         "gather_gbs": (4 * nnz_local * nz / (fwd_avg * 1e-3) / 1e9) if nz > 1 else None,

@@ -88,8 +88,9 @@ typedef struct {
     double coarse_fwd_ms;    /* forward / back launches over a block-coarsened matrix (wavelet AM while the */
     double coarse_back_ms;   /* finest active tree level is > 1); NOT included in fwd_ms / back_ms */
     int64_t coarse_fwd_launches, coarse_back_launches;
-    int64_t proj_entries;    /* in-plane matrix entries streamed by the forward and back launches above
-                                (H and the block-coarsened Hc alike: x slices = ray-voxel updates actually done) */
+    int64_t proj_updates;    /* ray-voxel updates executed by all forward and back launches above: matrix
+                                entries streamed (H or a block-coarsened Hc) x slices processed */
+    int64_t split_entries;   /* Phi^- / Psi entries streamed by the split launches above (sum over launches) */
 } wamgpu_timing;
 
 int wamgpu_version(void);

@@ -131,7 +131,7 @@ class Timing(C.Structure):
                                          "expand_events", "kernel_launches", "split_nnz")] + \
                [("phi_ms", C.c_double), ("phi_launches", C.c_int64), ("coarse_fwd_ms", C.c_double),
                 ("coarse_back_ms", C.c_double), ("coarse_fwd_launches", C.c_int64),
-                ("coarse_back_launches", C.c_int64), ("proj_entries", C.c_int64)]
+                ("coarse_back_launches", C.c_int64), ("proj_updates", C.c_int64), ("split_entries", C.c_int64)]
 
     def asdict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

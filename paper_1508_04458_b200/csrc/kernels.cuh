@@ -48,6 +48,27 @@ __device__ __forceinline__ uint2 ld_stream(const uint2* p) { return __ldcs(p); }
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
 __device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
 
+// Entry sources of the projector kernels (2D CSR/CSC kernels and the 3D slab SpMM).  The system matrix: uint2 {column, fp32 h}.
+// The block-coarsened matrices of the wavelet-AM iteration (kernels3c.cuh):
+// separate column and fp64 value arrays.
+struct Ent64 {
+    const unsigned* c;
+    const double* v;
+};
+struct Ent64Val {
+    unsigned c;
+    double h;
+};
+__device__ __forceinline__ uint2 ent_ld(const uint2* A, uint64_t k) { return ld_stream(A + k); }
+__device__ __forceinline__ uint2 ent_zero(const uint2*) { return make_uint2(0u, 0u); }
+__device__ __forceinline__ unsigned ent_col(const uint2& e) { return e.x; }
+__device__ __forceinline__ double ent_h(const uint2& e) { return (double)__uint_as_float(e.y); }
+__device__ __forceinline__ Ent64Val ent_ld(const Ent64& A, uint64_t k) { return Ent64Val{__ldcs(A.c + k), __ldcs(A.v + k)}; }
+__device__ __forceinline__ Ent64Val ent_zero(const Ent64&) { return Ent64Val{0u, 0.0}; }
+__device__ __forceinline__ unsigned ent_col(const Ent64Val& e) { return e.c; }
+__device__ __forceinline__ double ent_h(const Ent64Val& e) { return e.h; }
+
+
 // ------------------------------------------------------------------ Siddon
 // projector.hpp:52-119 on the device, fp64, every operation an explicit
 // round-to-nearest intrinsic so no FMA contraction can change h.
@@ -260,40 +281,40 @@ __device__ __forceinline__ double idiv_term(double d, double q) {
 // fp64 accumulation (products of two fp32 are exact in fp64); segment
 // selection is by predicated fma with h=0 (an exact no-op); fixed
 // xor-butterfly reduction (deterministic).
-template <int G, int UNROLL = 8, bool TILED = false>
-__device__ __forceinline__ void seg_dot(const uint2* __restrict__ A, const float* __restrict__ x, uint64_t lo,
+template <int G, int UNROLL = 8, bool TILED = false, class AP = const uint2*>
+__device__ __forceinline__ void seg_dot(const AP& A, const float* __restrict__ x, uint64_t lo,
                                         const uint64_t (&b)[G > 1 ? G - 1 : 1], uint64_t hi, int lane,
                                         double (&out)[G], int lgx = -1) {
     double acc[G][2];
 #pragma unroll
     for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = 0.0;
-    uint2 ec[UNROLL];
+    decltype(ent_zero(A)) ec[UNROLL];
     uint64_t base = lo + lane;
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
         const uint64_t k = base + 32 * u;
-        ec[u] = (k < hi) ? ld_stream(A + k) : make_uint2(0u, 0u);
+        ec[u] = (k < hi) ? ent_ld(A, k) : ent_zero(A);
     }
     for (; base < hi; base += 32 * UNROLL) {
-        uint2 en[UNROLL];
+        decltype(ent_zero(A)) en[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
             const uint64_t k = base + 32 * (UNROLL + u);
-            en[u] = (k < hi) ? ld_stream(A + k) : make_uint2(0u, 0u);
+            en[u] = (k < hi) ? ent_ld(A, k) : ent_zero(A);
         }
         float v[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
             if constexpr (TILED) {
-                const unsigned col = ec[u].x, ix = col & ((1u << lgx) - 1u), iy = col >> lgx;
+                const unsigned col = ent_col(ec[u]), ix = col & ((1u << lgx) - 1u), iy = col >> lgx;
                 v[u] = __ldg(x + (((((iy >> 2) << (lgx - 3)) + (ix >> 3)) << 5) + ((iy & 3u) << 3) + (ix & 7u)));
             } else {
-                v[u] = __ldg(x + ec[u].x);
+                v[u] = __ldg(x + ent_col(ec[u]));
             }
         }
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
-            const double h = hval(ec[u]), xv = (double)v[u];
+            const double h = ent_h(ec[u]), xv = (double)v[u];
             if (G == 1) {
                 acc[0][u & 1] = fma(h, xv, acc[0][u & 1]);
             } else {
@@ -379,9 +400,9 @@ __global__ void __launch_bounds__(256, MINB) k_forward(uint64_t M, const unsigne
 // profiles/) while the A stream stays coalesced (LPR*8 B per ray per load).
 // Software-pipelined like seg_dot; fp64 accumulation; fixed strided partials +
 // xor butterfly inside each LPR-lane group (deterministic).  MODE as k_forward.
-template <int MODE, int R, int UNR, int MINB>
+template <int MODE, int R, int UNR, int MINB, class AP = const uint2*>
 __global__ void __launch_bounds__(256, MINB) k_fwd_patch(uint64_t M, const unsigned long long* __restrict__ rp,
-                                                    const uint2* __restrict__ A, const float* __restrict__ mu,
+                                                    AP A, const float* __restrict__ mu,
                                                     const float* __restrict__ I0, const float* __restrict__ d,
                                                     float* __restrict__ q, double* __restrict__ lout,
                                                     double* __restrict__ partial, int* __restrict__ flag) {
@@ -399,26 +420,26 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_patch(uint64_t M, const unsig
 #pragma unroll
         for (int o = 16; o >= LPR; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
         double acc0 = 0.0, acc1 = 0.0;
-        uint2 ec[UNR];
+        decltype(ent_zero(A)) ec[UNR];
         const uint64_t b0 = lo + sub;
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
             const uint64_t k = b0 + LPR * u;
-            ec[u] = k < hi ? ld_stream(A + k) : make_uint2(0u, 0u);
+            ec[u] = k < hi ? ent_ld(A, k) : ent_zero(A);
         }
         for (unsigned off = 0; off < maxlen; off += LPR * UNR) {
-            uint2 en[UNR];
+            decltype(ent_zero(A)) en[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
                 const uint64_t k = b0 + off + LPR * (UNR + u);
-                en[u] = k < hi ? ld_stream(A + k) : make_uint2(0u, 0u);
+                en[u] = k < hi ? ent_ld(A, k) : ent_zero(A);
             }
             float v[UNR];
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) v[u] = (b0 + off + LPR * u < hi) ? __ldg(mu + ec[u].x) : 0.0f;
+            for (int u = 0; u < UNR; ++u) v[u] = (b0 + off + LPR * u < hi) ? __ldg(mu + ent_col(ec[u])) : 0.0f;
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
-                const double h = hval(ec[u]), xv = (double)v[u];
+                const double h = ent_h(ec[u]), xv = (double)v[u];
                 if (u & 1) acc1 = fma(h, xv, acc1); else acc0 = fma(h, xv, acc0);
             }
 #pragma unroll
@@ -610,9 +631,9 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_c2(uint64_t M, const unsigned
 // Warp per voxel: g(x) = sum_y h(y|x) w(y) in fp64 over the voxel's CSC column.
 // MODE 0: write g (fp64).  MODE 1: fused AM update:
 // mu <- max(0, mu + ln(g/b)/Z0) where b > 0 and g > 0, otherwise frozen.
-template <int MODE, int UNR = 8, int MINB = 1>
+template <int MODE, int UNR = 8, int MINB = 1, class AP = const uint2*>
 __global__ void __launch_bounds__(256, MINB) k_back(uint64_t N, const unsigned long long* __restrict__ cp,
-                                              const uint2* __restrict__ C, const float* __restrict__ w,
+                                              AP C, const float* __restrict__ w,
                                               double* __restrict__ g, const double* __restrict__ bam,
                                               float* __restrict__ mu, double Z0, int* __restrict__ flag, int lgx) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;

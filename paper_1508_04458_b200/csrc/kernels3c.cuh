@@ -85,6 +85,21 @@ __global__ void k_mu_coarse(uint64_t Nc, int nxc, int nx, int k, int P, const fl
     reinterpret_cast<float4*>(muc + B * P)[v] = __ldg(reinterpret_cast<const float4*>(mu + x * P) + v);
 }
 
+// 2D: mu_c[B] = mu[first pixel of B]; g[x] = G[B(x)] * 4^-k
+__global__ void k_mu_coarse2(uint64_t Nc, int nxc, int nx, int k, const float* __restrict__ mu,
+                             float* __restrict__ muc) {
+    const uint64_t B = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (B >= Nc) return;
+    muc[B] = __ldg(mu + ((B / nxc) << k) * (uint64_t)nx + ((B % nxc) << k));
+}
+__global__ void k_g_expand2(uint64_t N, int nxc, int nx, int k, const double* __restrict__ gc,
+                            double* __restrict__ g) {
+    const uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= N) return;
+    const uint64_t iy = x / nx, ix = x % nx;
+    g[x] = __ldg(gc + (iy >> k) * (uint64_t)nxc + (ix >> k)) * (1.0 / (double)(1u << (2 * k)));
+}
+
 // debug (WAMGPU_COARSE_CHECK=1): flag pixels whose mu differs from their block's first pixel
 __global__ void k_mu_coarse_check(uint64_t N, int nx, int k, int P, int nz, const float* __restrict__ mu,
                                   int* __restrict__ bad) {
@@ -112,6 +127,93 @@ __global__ void k_g_expand(uint64_t N, int nxc, int nx, int k, int P, const doub
     double2 t = __ldg(reinterpret_cast<const double2*>(gc + B * P) + v);
     t.x *= sc; t.y *= sc;
     reinterpret_cast<double2*>(g + x * P)[v] = t;
+}
+
+// ---- z-coarsening on top: the same tree also makes mu constant over groups of
+// c = 2^k consecutive slices (the 3D synthesis copies a 2^k-cube's value to all
+// its voxels), and the update reads only CUBE sums of g.  So the coarse forward
+// runs on nzc = nz / c slices and its line integrals serve every slice of a
+// group; the coarse back projection runs on the z-group sums of q, carried as
+// two fp32 values (hi = fp32(S), lo = fp32(S - hi): 48 bits of the exact fp64
+// sum S of the c fp32 values) because the slab operand is fp32 by design.
+__global__ void k_mu_coarse_z(uint64_t Nc, int nxc, int nx, int k, int P, int Pc, int nzc,
+                              const float* __restrict__ mu, float* __restrict__ muc) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= Nc * (uint64_t)Pc) return;
+    const uint64_t B = i / Pc;
+    const int zg = (int)(i % Pc);
+    const uint64_t x = ((B / nxc) << k) * (uint64_t)nx + ((B % nxc) << k);
+    muc[i] = zg < nzc ? __ldg(mu + x * P + ((uint64_t)zg << k)) : 0.f;
+}
+// debug: mu must equal the value at the first voxel of its 2^k-cube
+__global__ void k_mu_coarse_check_z(uint64_t N, int nx, int k, int P, int nz, const float* __restrict__ mu,
+                                    int* __restrict__ bad) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N * (uint64_t)nz) return;
+    const uint64_t x = i / nz;
+    const int s = (int)(i % nz);
+    const uint64_t iy = x / nx, ix = x % nx;
+    const uint64_t x0 = ((iy >> k) << k) * (uint64_t)nx + ((ix >> k) << k);
+    if (__float_as_uint(mu[x * P + s]) != __float_as_uint(mu[x0 * P + ((s >> k) << k)])) atomicOr(bad, 1);
+}
+// q[y][s] = fp32(I0 exp(-lc[y][s >> k])) and the I-divergence partial of the CTA
+// (fixed grid: thread sums in index order, xor butterfly, warps in order)
+__global__ void __launch_bounds__(256) k_beer_z(uint64_t M, int nz, int P, int Pc, int k,
+                                                const double* __restrict__ lc, const float* __restrict__ I0,
+                                                const float* __restrict__ d, float* __restrict__ q,
+                                                double* __restrict__ partial, int* __restrict__ flag) {
+    double tacc = 0.0;
+    const uint64_t n = M * (uint64_t)nz, stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t y = i / nz;
+        const int s = (int)(i % nz);
+        const double l = lc[y * Pc + (s >> k)];
+        if (!isfinite(l)) atomicOr(flag, 1);
+        const uint64_t id = y * P + s;
+        const double qq = (double)I0[id] * exp(-l);
+        q[id] = (float)qq;
+        tacc += idiv_term((double)d[id], qq);
+    }
+    __shared__ double sm[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tacc += __shfl_xor_sync(0xffffffffu, tacc, o);
+    if (lane == 0) sm[wib] = tacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += sm[w];
+        partial[blockIdx.x] = t;
+    }
+}
+// wz[y][2 zg], wz[y][2 zg + 1] = hi, lo of the slice-order fp64 sum of q over z-group zg
+__global__ void k_qsum_z(uint64_t M, int nzc, int P, int Pw, int k, const float* __restrict__ q,
+                         float* __restrict__ wz) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M * (uint64_t)(Pw / 2)) return;
+    const uint64_t y = i / (Pw / 2);
+    const int zg = (int)(i % (Pw / 2));
+    float hi = 0.f, lo = 0.f;
+    if (zg < nzc) {
+        const float* p = q + y * P + ((uint64_t)zg << k);
+        double S = 0.0;
+        for (int j = 0; j < (1 << k); ++j) S += (double)__ldg(p + j);
+        hi = (float)S;
+        lo = (float)(S - (double)hi);
+    }
+    reinterpret_cast<float2*>(wz + y * Pw)[zg] = make_float2(hi, lo);
+}
+// g[x][s] = (Gc[B][2 zg] + Gc[B][2 zg + 1]) * 8^-k, zg = s >> k: the cube mean on every voxel
+__global__ void k_g_expand_z(uint64_t N, int nxc, int nx, int k, int P, int Pw, int nz,
+                             const double* __restrict__ gc, double* __restrict__ g) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N * (uint64_t)nz) return;
+    const uint64_t x = i / nz;
+    const int s = (int)(i % nz);
+    const uint64_t iy = x / nx, ix = x % nx;
+    const uint64_t B = (iy >> k) * (uint64_t)nxc + (ix >> k);
+    const double2 t = __ldg(reinterpret_cast<const double2*>(gc + B * Pw) + (s >> k));
+    g[x * P + s] = (t.x + t.y) * (1.0 / (double)(1u << (3 * k)));
 }
 
 }  // namespace wamgpu

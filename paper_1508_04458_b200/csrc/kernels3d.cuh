@@ -123,26 +123,6 @@ __device__ __forceinline__ void slab_unpack(const typename SlabLd<SPL>::T (&v)[S
     }
 }
 
-// Entry sources of the slab SpMM.  The system matrix: uint2 {column, fp32 h}.
-// The block-coarsened matrices of the wavelet-AM iteration (kernels3c.cuh):
-// separate column and fp64 value arrays.
-struct Ent64 {
-    const unsigned* c;
-    const double* v;
-};
-struct Ent64Val {
-    unsigned c;
-    double h;
-};
-__device__ __forceinline__ uint2 ent_ld(const uint2* A, uint64_t k) { return ld_stream(A + k); }
-__device__ __forceinline__ uint2 ent_zero(const uint2*) { return make_uint2(0u, 0u); }
-__device__ __forceinline__ unsigned ent_col(const uint2& e) { return e.x; }
-__device__ __forceinline__ double ent_h(const uint2& e) { return (double)__uint_as_float(e.y); }
-__device__ __forceinline__ Ent64Val ent_ld(const Ent64& A, uint64_t k) { return Ent64Val{__ldcs(A.c + k), __ldcs(A.v + k)}; }
-__device__ __forceinline__ Ent64Val ent_zero(const Ent64&) { return Ent64Val{0u, 0.0}; }
-__device__ __forceinline__ unsigned ent_col(const Ent64Val& e) { return e.c; }
-__device__ __forceinline__ double ent_h(const Ent64Val& e) { return e.h; }
-
 // per-warp staging: 2 chunk buffers x G groups x K entries (K = 32, 16 for
 // G = 8 to stay in 48 KB of static smem per CTA); strides K+4 / K+2 keep the
 // G 16-byte broadcasts of a load in distinct bank quads

@@ -1071,49 +1071,66 @@ __device__ __forceinline__ double f2d_wide(float f) {
         return __longlong_as_double((long long)w);
     }
 }
+// One entry's contribution for a lane that holds V = S/4 chunks of 4 consecutive
+// slices (chunk v starts at slice 4*LPE*v + 4*j: every cp.async / load instruction
+// of a group then covers one contiguous run of the q row, whole 32-byte sectors;
+// 8 consecutive slices per lane made every sector travel twice, and the split is
+// bound by L2 -> SM traffic: ncu lts throughput 80%, profiles/r07/ncu_split3c_cfg4.txt).
+// LV 1: two z-blocks per chunk (pairs); LV 2: one z-block per chunk; LV 0 (runtime
+// level >= 3): the chunk lies inside one half (hh) of its z-block.
 template <int S, int LV, bool TRICK>
 __device__ __forceinline__ void split3_consume(const float4& ps, const float (&f)[S], bool hh,
-                                               double (&acc)[LV > 0 ? 7 * (S >> LV) : 7]) {
-    constexpr int HS = LV > 0 ? (1 << (LV - 1)) : S;
-    constexpr int NZ = LV > 0 ? S / (2 * HS) : 1;
+                                               double (&acc)[(S / 4) * (LV == 1 ? 14 : 7)]) {
+    constexpr int V = S / 4;
     const float pf[4] = {ps.x, ps.y, ps.z, ps.w};
     double m[8];
     if constexpr (LV > 0) {
+        constexpr int HS = LV;            // half size in slices: 1 or 2
+        constexpr int NZ = 2 / HS;        // z-blocks per chunk
+        // m[0..3] = min(psi_t, 0) (t = A,H,V,D); m[4] = min(-psi_A, 0);
+        // m[5..7] = TRICK ? psi_t : min(-psi_t, 0) (t = H,V,D)
 #pragma unroll
         for (int t = 0; t < 4; ++t) m[t] = (double)fminf(pf[t], 0.f);
         m[4] = (double)fminf(-pf[0], 0.f);
 #pragma unroll
         for (int t = 1; t < 4; ++t) m[4 + t] = TRICK ? (double)pf[t] : (double)fminf(-pf[t], 0.f);
 #pragma unroll
-        for (int z = 0; z < NZ; ++z) {
-            double qlo = f2d_wide<false>(f[z * 2 * HS]), qhi = f2d_wide<false>(f[z * 2 * HS + HS]);
+        for (int v = 0; v < V; ++v)
 #pragma unroll
-            for (int i = 1; i < HS; ++i) {
-                qlo += f2d_wide<false>(f[z * 2 * HS + i]);
-                qhi += f2d_wide<false>(f[z * 2 * HS + HS + i]);
+            for (int z = 0; z < NZ; ++z) {
+                const float* fz = f + 4 * v + 2 * HS * z;
+                double qlo = f2d_wide<false>(fz[0]), qhi = f2d_wide<false>(fz[HS]);
+                if constexpr (HS == 2) {
+                    qlo += f2d_wide<false>(fz[1]);
+                    qhi += f2d_wide<false>(fz[3]);
+                }
+                const double qall = qlo + qhi;
+                double* a = acc + 7 * (v * NZ + z);
+#pragma unroll
+                for (int t = 0; t < 3; ++t) a[t] = fma(m[1 + t], qall, a[t]);
+                a[3] = fma(m[4], qhi, fma(m[0], qlo, a[3]));
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    if constexpr (TRICK) a[4 + t] = fma(m[5 + t], qhi, a[4 + t]);
+                    else a[4 + t] = fma(m[5 + t], qhi, fma(m[1 + t], qlo, a[4 + t]));
+                }
             }
-            const double qall = qlo + qhi;
-            double* a = acc + 7 * z;
-#pragma unroll
-            for (int t = 0; t < 3; ++t) a[t] = fma(m[1 + t], qall, a[t]);
-            a[3] = fma(m[4], qhi, fma(m[0], qlo, a[3]));
-#pragma unroll
-            for (int t = 0; t < 3; ++t) {
-                if constexpr (TRICK) a[4 + t] = fma(m[5 + t], qhi, a[4 + t]);
-                else a[4 + t] = fma(m[5 + t], qhi, fma(m[1 + t], qlo, a[4 + t]));
-            }
-        }
     } else {
+        // m[0..2] = min(psi_t, 0) (t = H,V,D: z-low); m[3..6] = this lane's half of z-high
+        // (low half min(psi,0), high half min(-psi,0)), scaled by 2^-896 (bit move)
 #pragma unroll
         for (int t = 1; t < 4; ++t) m[t - 1] = f2d_wide<true>(fminf(pf[t], 0.f));
 #pragma unroll
         for (int t = 0; t < 4; ++t) m[3 + t] = f2d_wide<true>(fminf(hh ? -pf[t] : pf[t], 0.f));
-        double qs = f2d_wide<false>(f[0]);
 #pragma unroll
-        for (int i = 1; i < S; ++i) qs += f2d_wide<false>(f[i]);
-        qs *= kTwo896;   // exact: the multipliers carry the 2^-896 here
+        for (int v = 0; v < V; ++v) {
+            double qs = f2d_wide<false>(f[4 * v]);
 #pragma unroll
-        for (int t = 0; t < 7; ++t) acc[t] = fma(m[t], qs, acc[t]);
+            for (int i = 1; i < 4; ++i) qs += f2d_wide<false>(f[4 * v + i]);
+            qs *= kTwo896;   // exact: the multipliers carry the 2^-896 here
+#pragma unroll
+            for (int t = 0; t < 7; ++t) acc[7 * v + t] = fma(m[t], qs, acc[7 * v + t]);
+        }
     }
 }
 template <int P, int E, int D, int WPI>
@@ -1134,14 +1151,14 @@ __device__ __forceinline__ void split3c_block(unsigned b, int l, int lane, int w
     constexpr int LPE = 32 / E, S = P * E / 32;
     static_assert(S == 4 || S == 8, "slices per lane");
     static_assert(32 % E == 0 && (32 / E) >= 1, "entry groups");
-    constexpr int HS = LV > 0 ? (1 << (LV - 1)) : S;
-    constexpr int NZ = LV > 0 ? S / (2 * HS) : 1;
-    static_assert(LV == 0 || 2 * HS <= S, "level does not fit a lane");
-    constexpr int NA = LV > 0 ? 7 * NZ : 7;
+    static_assert(LV >= 0 && LV <= 2, "levels 1 and 2 are specialised; 0 = runtime level >= 3");
+    constexpr int V = S / 4;                        // chunks of 4 consecutive slices per lane
+    constexpr int NZC = LV == 1 ? 2 : 1;            // z-blocks (LV > 0) or partials (LV 0) per chunk
+    constexpr int NA = V * (LV == 1 ? 14 : 7);
     constexpr int RPB = 32 / E;   // rounds per index batch (32 entries)
     static_assert(D >= 2 && D - 1 <= RPB, "the ring may reach at most one index batch ahead");
     const int grp = lane / LPE, j = lane % LPE;
-    const bool hh = LV == 0 ? (((j * S) >> (l - 1)) & 1) != 0 : false;
+    const bool hh = LV == 0 ? (((4 * j) >> (l - 1)) & 1) != 0 : false;   // 4*LPE*v is a multiple of 2^l
     double acc[NA];
 #pragma unroll
     for (int i = 0; i < NA; ++i) acc[i] = 0.0;
@@ -1167,9 +1184,9 @@ __device__ __forceinline__ void split3c_block(unsigned b, int l, int lane, int w
     auto issue_q = [&](uint64_t r) {   // q row parts of round r into ring slot r % D
         if (r < nr) {
             const unsigned y = sm.iray[wib][(r / RPB) & 1][(r % RPB) * E + grp];
-            const float4* row = reinterpret_cast<const float4*>(q + (uint64_t)y * P + j * S);
+            const float4* row = reinterpret_cast<const float4*>(q + (uint64_t)y * P) + j;
 #pragma unroll
-            for (int v = 0; v < S / 4; ++v) cp_async16(&sm.ring[wib][r % D][v][lane], row + v);
+            for (int v = 0; v < S / 4; ++v) cp_async16(&sm.ring[wib][r % D][v][lane], row + LPE * v);
         }
         cp_async_commit();
     };
@@ -1204,7 +1221,7 @@ __device__ __forceinline__ void split3c_block(unsigned b, int l, int lane, int w
     }
     if constexpr (LV > 0 && TRICK) {
 #pragma unroll
-        for (int z = 0; z < NZ; ++z)
+        for (int z = 0; z < V * NZC; ++z)
 #pragma unroll
             for (int t = 0; t < 3; ++t) acc[7 * z + 4 + t] = acc[7 * z + t] - acc[7 * z + 4 + t];
     }
@@ -1212,22 +1229,21 @@ __device__ __forceinline__ void split3c_block(unsigned b, int l, int lane, int w
     for (int o = LPE; o < 32; o <<= 1)
 #pragma unroll
         for (int i = 0; i < NA; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    // red slot = z-block index (LV > 0) or chunk index in slice order (LV 0: 4 slices per slot)
     if (grp == 0) {
-        if constexpr (LV > 0) {
 #pragma unroll
-            for (int z = 0; z < NZ; ++z)
+        for (int v = 0; v < V; ++v)
 #pragma unroll
-                for (int t = 0; t < 7; ++t) sm.red[wib][t][j * NZ + z] = acc[7 * z + t];
-        } else {
+            for (int z = 0; z < NZC; ++z)
 #pragma unroll
-            for (int t = 0; t < 7; ++t) sm.red[wib][t][j] = acc[t];
-        }
+                for (int t = 0; t < 7; ++t)
+                    sm.red[wib][t][(LPE * v + j) * NZC + z] = acc[7 * (v * NZC + z) + t];
     }
     if constexpr (WPI == 1) __syncwarp(); else __syncthreads();
     const double cls = cpow3(l) * kTwo896;
     const int nk = nzl >> l, hl = ny >> l, wl = nx >> l, dl = nk;
     const int bi = (int)(b / wl), bj = (int)(b % wl);
-    const int per = LV > 0 ? 1 : ((1 << l) / S);   // red slots per z-block
+    const int per = LV > 0 ? 1 : ((1 << l) / 4);   // red slots per z-block
     const int t0 = WPI == 1 ? lane : (int)threadIdx.x, tstep = WPI == 1 ? 32 : 32 * WPI;
     for (int k = t0; k < nk; k += tstep) {
         if (!act[off.off[l] + ((uint64_t)k * hl + bi) * wl + bj]) continue;
@@ -1285,7 +1301,6 @@ __global__ void __launch_bounds__(128, MINB) k_split3c(uint64_t nlist, const uin
 #define SP(LVv) split3c_block<P, E, LVv, TRICK, D, WPI>(b, l, lane, wib, nx, ny, nzl, e0, e1, eray, epsi, q, act, off, bm, tmap, sm)
         if (l == 1) SP(1);
         else if (l == 2) SP(2);
-        else if (S == 8 && l == 3) { if constexpr (S == 8) SP(3); }
         else SP(0);
 #undef SP
     }

@@ -261,6 +261,8 @@ struct wamgpu_ctx {
     } coarse[6];   // index k = 1 .. LMAX
     DBuf<float> mu_c;                   // mu on the coarse grid (forward operand)
     DBuf<double> g_c;                   // block sums of g (coarse back projection)
+    DBuf<double> l_c;                   // z-coarse line integrals [ray][z-group]
+    DBuf<float> w_z;                    // z-group sums of q as hi/lo pairs
     int fine_level = 0;                 // finest level with an active block (0: none)
     std::vector<std::vector<unsigned>> morton;   // per level: in-plane blocks in Morton order (host, cached)
     int morton_nx = 0, morton_ny = 0;
@@ -1409,7 +1411,7 @@ static void back_launch(Ctx* c, const float* w, double* out, const double* bam, 
     check_launch(c, "k_back3");
     c->timer_end(T_BACK);
     c->tm.back_launches++;
-    c->tm.proj_entries += (int64_t)c->nnz;
+    c->tm.proj_updates += (int64_t)(c->nnz * (uint64_t)c->nzl);
 }
 // nonneg: w >= 0 with no -0.0 (q, d); false for caller-supplied vectors
 static void back_into(Ctx* c, const float* w, double* out, bool nonneg = true) {
@@ -1449,7 +1451,7 @@ static void back_allreduce(Ctx* c, const float* w, const double* extra) {
     check_launch(c, "k_fused_allreduce");
     c->timer_end(T_BACK);
     c->tm.back_launches++;
-    c->tm.proj_entries += (int64_t)c->nnz;
+    c->tm.proj_updates += (int64_t)(c->nnz * (uint64_t)c->nzl);
 }
 
 // plain l = H mu (fp64 out), for forward_project
@@ -1472,14 +1474,19 @@ static void forward_plain(Ctx* c, const float* mu, double* l) {
 }
 
 static int coarse_k(const Ctx* c);
+static int coarse_mode();
+static unsigned fwd2c_launch(Ctx* c, int k);
 static unsigned fwd3c_launch(Ctx* c, int k, unsigned maxblk);
 // q = I0 exp(-H mu), objective -> scal[0] (all-reduced), record
 static void forward_fused(Ctx* c, bool record) {
-    const int ck = (c->nzl > 1 && c->algo == 2) ? coarse_k(c) : 0;
+    const int ck = c->algo == 2 ? coarse_k(c) : 0;
     c->timer_begin(ck > 0 ? T_FWDC : T_FWD);
     int nparts = c->nblk_row;
-    uint64_t entries = c->nnz;
-    if (c->nzl == 1) {
+    uint64_t entries = c->nnz, slices = (uint64_t)c->nzl;
+    if (c->nzl == 1 && ck > 0) {
+        nparts = (int)fwd2c_launch(c, ck);
+        entries = c->coarse[ck].nnz;
+    } else if (c->nzl == 1) {
 #define FV(FGv, U, MB)                                                                                              \
     if (c->lgx >= 0)                                                                                               \
         k_forward<1, FGv, U, MB, true><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, c->rp.p, c->A.p, c->mu.p, c->I0.p,    \
@@ -1532,13 +1539,17 @@ static void forward_fused(Ctx* c, bool record) {
 #undef FP
 #undef FV
     } else {
-        if (ck > 0) { nparts = (int)fwd3c_launch(c, ck, (unsigned)c->partial.n); entries = c->coarse[ck].nnz; }
+        if (ck > 0) {
+            nparts = (int)fwd3c_launch(c, ck, (unsigned)c->partial.n);
+            entries = c->coarse[ck].nnz;
+            if (coarse_mode() >= 2) slices = (uint64_t)(c->nzl >> ck);
+        }
         else nparts = (int)fwd3_launch<1>(c, c->mu.p, nullptr, (unsigned)c->partial.n, c->algo == 1 && c->mu_nonneg);
     }
     check_launch(c, "k_forward3");
     c->timer_end(ck > 0 ? T_FWDC : T_FWD);
     if (ck > 0) c->tm.coarse_fwd_launches++; else c->tm.fwd_launches++;
-    c->tm.proj_entries += (int64_t)entries;
+    c->tm.proj_updates += (int64_t)(entries * slices);
     k_sum_partials<<<1, 1024, 0, c->st>>>(c->partial.p, nparts, c->scal.p);
     check_launch(c, "k_sum_partials");
     allreduce_sum(c, c->scal.p, 1);
@@ -2509,16 +2520,36 @@ static void build_phiA(Ctx* c) {
 // ---- block-coarsened projections (kernels3c.cuh) ---------------------------
 // WAMGPU_COARSE=0: always project over H.  WAMGPU_COARSE_CHECK=1: verify on
 // the device, before every coarse forward, that mu is constant on the blocks.
-static bool coarse_enabled() {   // read per call: tests switch it between contexts
+// WAMGPU_COARSE: 0 = always project over H; 1 = in-plane blocks only; 2 (default) = in-plane
+// blocks and z-groups.  Read per call: tests switch it between contexts.
+static int coarse_mode() {
     const char* e = std::getenv("WAMGPU_COARSE");
+    return e ? std::atoi(e) : 2;
+}
+static bool coarse_enabled() { return coarse_mode() != 0; }
+static bool coarse_root() {   // default on: cfg4 12.69 -> 13.17 it/s, cfg3 71.4 -> 74.7 (profiles/r07/root_ab.txt)
+    const char* e = std::getenv("WAMGPU_COARSE_ROOT");
     return !(e && e[0] == '0');
+}
+static int pow2_stride(int n) {
+    int P = 8;
+    while (P < n) P *= 2;
+    return P;
 }
 // coarsening exponent k (block edge 2^k) the current tree allows; 0 = project over H
 static int coarse_k(const Ctx* c) {
-    if (!coarse_enabled() || !c->haar3 || c->nzl <= 1 || !c->phiA_beta_ok || view_sharded(c)) return 0;
-    if (c->fine_level <= 1) return 0;
-    const int k = std::min(c->fine_level - 1, LMAX);
-    if ((c->nx >> k) << k != c->nx || (c->ny >> k) << k != c->ny || slab_stride(c) < 8) return 0;
+    // view shards: each rank coarsens its own rows; the partial [g || b-] are all-reduced after the
+    // expansion to pixels.  Not with the fused NVLink all-reduce (2D) or the split update (3D view
+    // groups), whose back projections write other layouts.
+    if (!coarse_enabled() || !c->phiA_beta_ok || c->ar.on || wam_split_update(c)) return 0;
+    const bool d3 = c->haar3 && c->nzl > 1, d2 = !c->haar3 && c->nz == 1 && c->lgx < 0;
+    if (!d3 && !d2) return 0;   // (the per-slice 2D Haar model of a 3D stack keeps the pixel path)
+    // root-only tree (no detail active): 2^L cubes.  3D only (WAMGPU_COARSE_ROOT=0: the Phi_A
+    // iteration of kernels_phi.cuh instead); the 2D root-only phase always runs over Phi_A.
+    if (c->fine_level == 0 && !(d3 && coarse_root() && coarse_mode() >= 2)) return 0;
+    if (c->fine_level == 1) return 0;
+    const int k = std::min((c->fine_level == 0 ? c->L + 1 : c->fine_level) - 1, LMAX);
+    if ((c->nx >> k) << k != c->nx || (c->ny >> k) << k != c->ny) return 0;
     return k;
 }
 static void build_coarse(Ctx* c, int k) {
@@ -2571,6 +2602,44 @@ static void build_coarse(Ctx* c, int k) {
     m.nnz = nnz;
     m.ok = true;
 }
+// 2D: the CSR patch forward and the CSC back projection over Hc
+static unsigned fwd2c_launch(Ctx* c, int k) {
+    build_coarse(c, k);
+    Ctx::Coarse& m = c->coarse[k];
+    c->mu_c.ensure(m.Nc);
+    if (std::getenv("WAMGPU_COARSE_CHECK") != nullptr) {
+        CK(cudaMemsetAsync(c->flag2.p, 0, 4, c->st));
+        k_mu_coarse_check<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->nx, k, 1, 1, c->mu.p, c->flag2.p);
+        int bad = 0;
+        CK(cudaMemcpyAsync(&bad, c->flag2.p, 4, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        if (bad) throw NumericError("coarse projection: mu is not constant on the 2^k blocks");
+    }
+    k_mu_coarse2<<<blocks_for(m.Nc, 256), 256, 0, c->st>>>(m.Nc, c->nx >> k, c->nx, k, c->mu.p, c->mu_c.p);
+    check_launch(c, "k_mu_coarse2");
+    k_fwd_patch<1, 4, 8, 5, Ent64><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, m.rp.p, Ent64{m.col.p, m.val.p}, c->mu_c.p,
+                                                                  c->I0.p, c->d.p, c->q.p, nullptr, c->partial.p,
+                                                                  c->flag.p);
+    check_launch(c, "k_fwd_patch (coarse)");
+    launched(c, 1);
+    return (unsigned)c->nblk_row;
+}
+static void back2c_into(Ctx* c, int k, const float* w, double* out) {
+    build_coarse(c, k);
+    Ctx::Coarse& m = c->coarse[k];
+    c->g_c.ensure(m.Nc);
+    c->timer_begin(T_BACKC);
+    const unsigned nb = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((m.Nc + 7) / 8, (uint64_t)c->sms * 16));
+    k_back<0, 12, 1, Ent64><<<nb, 256, 0, c->st>>>(m.Nc, m.cp.p, Ent64{m.row.p, m.valC.p}, w, c->g_c.p, nullptr, nullptr,
+                                                   0.0, c->flag.p, -1);
+    check_launch(c, "k_back (coarse)");
+    k_g_expand2<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->nx >> k, c->nx, k, c->g_c.p, out);
+    check_launch(c, "k_g_expand2");
+    launched(c, 1);
+    c->timer_end(T_BACKC);
+    c->tm.coarse_back_launches++;
+    c->tm.proj_updates += (int64_t)m.nnz;
+}
 // l = Hc mu_c fused with q = I0 exp(-l) and the I-divergence partials; returns the partial count
 template <int P>
 static unsigned fwd3c_launch_p(Ctx* c, int k, unsigned maxblk) {
@@ -2582,18 +2651,52 @@ static unsigned fwd3c_launch_p(Ctx* c, int k, unsigned maxblk) {
         c->partial.p, c->flag.p);
     return nb;
 }
+// z-coarse: l_c = Hc mu_cz on nz / 2^k slices (MODE 0), then q and the I-divergence per slice
+template <int PC>
+static void fwd3cz_launch_p(Ctx* c, int k, int nzc) {
+    using S = SlabShape<PC>;
+    Ctx::Coarse& m = c->coarse[k];
+    const unsigned nb = nblk_warp(c, (c->Ml + S::G - 1) / S::G);
+    k_fwd3s<0, S::LPR, S::SPL, 104, 2, true, PC, 8, 2, Ent64><<<nb, 256, 0, c->st>>>(
+        c->Ml, 0, nzc, m.rp.p, Ent64{m.col.p, m.val.p}, c->mu_c.p, nullptr, nullptr, nullptr, c->l_c.p,
+        nullptr, c->flag.p);
+}
 static unsigned fwd3c_launch(Ctx* c, int k, unsigned maxblk) {
     build_coarse(c, k);
     Ctx::Coarse& m = c->coarse[k];
     const int P = slab_stride(c);
-    c->mu_c.ensure(m.Nc * P);
+    const bool zc = coarse_mode() >= 2;
+    const int nzc = c->nzl >> k, Pc = pow2_stride(nzc);
+    c->mu_c.ensure(m.Nc * (zc ? Pc : P));
     if (std::getenv("WAMGPU_COARSE_CHECK") != nullptr) {
         CK(cudaMemsetAsync(c->flag2.p, 0, 4, c->st));
+        if (zc)
+            k_mu_coarse_check_z<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->N, c->nx, k, P, c->nzl, c->mu.p, c->flag2.p);
+        else
         k_mu_coarse_check<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->N, c->nx, k, P, c->nzl, c->mu.p, c->flag2.p);
         int bad = 0;
         CK(cudaMemcpyAsync(&bad, c->flag2.p, 4, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
         if (bad) throw NumericError("coarse projection: mu is not constant on the 2^k blocks");
+    }
+    if (zc) {
+        c->l_c.ensure(c->Ml * Pc);
+        k_mu_coarse_z<<<blocks_for(m.Nc * Pc, 256), 256, 0, c->st>>>(m.Nc, c->nx >> k, c->nx, k, P, Pc, nzc, c->mu.p,
+                                                                     c->mu_c.p);
+        check_launch(c, "k_mu_coarse_z");
+        switch (Pc) {
+            case 8: fwd3cz_launch_p<8>(c, k, nzc); break;
+            case 16: fwd3cz_launch_p<16>(c, k, nzc); break;
+            case 32: fwd3cz_launch_p<32>(c, k, nzc); break;
+            default: fwd3cz_launch_p<64>(c, k, nzc); break;
+        }
+        check_launch(c, "k_fwd3s (z-coarse)");
+        const unsigned nbz = std::min<unsigned>((unsigned)c->sms * 8, maxblk);
+        k_beer_z<<<nbz, 256, 0, c->st>>>(c->Ml, c->nzl, P, Pc, k, c->l_c.p, c->I0.p, c->d.p, c->q.p, c->partial.p,
+                                        c->flag.p);
+        check_launch(c, "k_beer_z");
+        launched(c, 2);
+        return nbz;
     }
     k_mu_coarse<<<blocks_for(m.Nc * (P / 4), 256), 256, 0, c->st>>>(m.Nc, c->nx >> k, c->nx, k, P, c->mu.p, c->mu_c.p);
     check_launch(c, "k_mu_coarse");
@@ -2619,10 +2722,43 @@ static void back3c_launch_p(Ctx* c, int k, const float* w) {
         m.Nc, 0, c->nzl, m.order.p, m.cp.p, Ent64{m.row.p, m.valC.p}, w, c->g_c.p, nullptr, nullptr, 0.0,
         c->flag.p, TileMap{});
 }
+template <int PW>
+static void back3cz_launch_p(Ctx* c, int k, int nzw) {
+    using S = SlabShape<PW>;
+    Ctx::Coarse& m = c->coarse[k];
+    const unsigned nb = nblk_warp(c, (m.Nc + S::G - 1) / S::G);
+    k_back3s<0, S::LPR, S::SPL, 104, 1, true, PW, 8, 2, Ent64><<<nb, 256, 0, c->st>>>(
+        m.Nc, 0, nzw, m.order.p, m.cp.p, Ent64{m.row.p, m.valC.p}, c->w_z.p, c->g_c.p, nullptr, nullptr, 0.0,
+        c->flag.p, TileMap{});
+}
 static void back3c_into(Ctx* c, int k, const float* w, double* out) {
     build_coarse(c, k);
     Ctx::Coarse& m = c->coarse[k];
     const int P = slab_stride(c);
+    if (coarse_mode() >= 2) {   // z-group sums of w as hi/lo pairs, block x z-group sums of g, cube means
+        const int nzc = c->nzl >> k, Pw = pow2_stride(2 * nzc);
+        c->w_z.ensure(c->Ml * Pw);
+        c->g_c.ensure(m.Nc * Pw);
+        c->timer_begin(T_BACKC);
+        k_qsum_z<<<blocks_for(c->Ml * (Pw / 2), 256), 256, 0, c->st>>>(c->Ml, nzc, P, Pw, k, w, c->w_z.p);
+        check_launch(c, "k_qsum_z");
+        switch (Pw) {
+            case 8: back3cz_launch_p<8>(c, k, 2 * nzc); break;
+            case 16: back3cz_launch_p<16>(c, k, 2 * nzc); break;
+            case 32: back3cz_launch_p<32>(c, k, 2 * nzc); break;
+            case 64: back3cz_launch_p<64>(c, k, 2 * nzc); break;
+            default: back3cz_launch_p<128>(c, k, 2 * nzc); break;
+        }
+        check_launch(c, "k_back3s (z-coarse)");
+        k_g_expand_z<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->N, c->nx >> k, c->nx, k, P, Pw, c->nzl,
+                                                                         c->g_c.p, out);
+        check_launch(c, "k_g_expand_z");
+        launched(c, 2);
+        c->timer_end(T_BACKC);
+        c->tm.coarse_back_launches++;
+        c->tm.proj_updates += (int64_t)(m.nnz * (uint64_t)(2 * nzc));
+        return;
+    }
     c->g_c.ensure(m.Nc * P);
     c->timer_begin(T_BACKC);
     switch (P) {
@@ -2638,7 +2774,7 @@ static void back3c_into(Ctx* c, int k, const float* w, double* out) {
     launched(c, 1);
     c->timer_end(T_BACKC);
     c->tm.coarse_back_launches++;
-    c->tm.proj_entries += (int64_t)m.nnz;
+    c->tm.proj_updates += (int64_t)(m.nnz * (uint64_t)c->nzl);
 }
 
 // one wavelet-AM iteration with only the roots active: S = Φ_Aᵀ q̂, root
@@ -2787,7 +2923,8 @@ static void split_init(Ctx* c) {
 }
 
 static void wam_step(Ctx* c) {
-    if (c->phiA_ok && c->phiA_L == c->L && phiA_applicable(c) && (c->haar3 ? c->nlist3 == 0 : c->nlist == 0)) {
+    if (c->phiA_ok && c->phiA_L == c->L && phiA_applicable(c) && (c->haar3 ? c->nlist3 == 0 : c->nlist == 0) &&
+        !(c->fine_level == 0 && coarse_k(c) > 0)) {
         if (c->haar3) phiA3_step(c);
         else phiA_step(c);
         return;
@@ -2819,6 +2956,7 @@ static void wam_step(Ctx* c) {
         check_launch(c, "k_split");
         c->timer_end(T_SPLIT, c->st2);
         c->tm.split_launches++;
+        c->tm.split_entries += (int64_t)c->nnz_phi;
         CK(cudaEventRecord(c->ev_y, c->st2));
     }
     if (split) {
@@ -2826,7 +2964,8 @@ static void wam_step(Ctx* c) {
         CK(cudaEventRecord(c->ev_x, c->st));
     } else if (!fused) {
         const int ck = coarse_k(c);
-        if (ck > 0) back3c_into(c, ck, c->q.p, c->g.p);
+        if (ck > 0 && c->nzl == 1) back2c_into(c, ck, c->q.p, c->g.p);
+        else if (ck > 0) back3c_into(c, ck, c->q.p, c->g.p);
         else back_into(c, c->q.p, c->g.p);
     }
     if (c->haar3 && c->nlist3) {
@@ -2866,8 +3005,11 @@ static void wam_step(Ctx* c) {
                 default: S3Z(128) break;
             }
 #undef S3Z
-        } else if (c->split_variant >= 10 && c->split_variant <= 14 && c->sband_B == 1 && P >= 64) {
-            // k_split3c: cp.async ring; 10: 4 warps per block, D 4; 11: warp per block; 12: 3 CTAs per SM; 13: D 6; 14: D 2
+        } else if ((c->split_variant == 0 || (c->split_variant >= 10 && c->split_variant <= 14)) && c->sband_B == 1) {
+            // k_split3c (default = 11): cp.async ring of D rounds, dynamic Morton-order scheduling, chunk
+            // lane map.  10: 4 warps per block, D 4, 4 CTAs per SM; 11: warp per block; 12: 4 warps per
+            // block, 3 CTAs per SM; 13: D 6; 14: D 2.  cfg4 split per run 915 / 889 / 955 / 1073 ms for
+            // 10 / 11 / 12 / 13 (k_split3h_e: 1700), cfg3 101 / 98 / 106 / 118 (180): profiles/r07/ab5_split_sectors.txt
 #define S3C(Pv, Ev, Dv, Wv, Mv)                                                                                    \
     {                                                                                                              \
         const unsigned nbc = Wv == 1 ? nb : (unsigned)std::min<uint64_t>(c->nlist3, (uint64_t)c->sms * Mv);        \
@@ -2878,12 +3020,18 @@ static void wam_step(Ctx* c) {
 #define S3CV(Pv, Ev)                                                                                               \
     switch (c->split_variant) {                                                                                    \
         case 10: S3C(Pv, Ev, 4, 4, 4) break;                                                                       \
-        case 11: S3C(Pv, Ev, 4, 1, 4) break;                                                                       \
         case 12: S3C(Pv, Ev, 4, 4, 3) break;                                                                       \
         case 13: S3C(Pv, Ev, 6, 4, 4) break;                                                                       \
-        default: S3C(Pv, Ev, 2, 4, 4) break;                                                                       \
+        case 14: S3C(Pv, Ev, 2, 4, 4) break;                                                                       \
+        default: S3C(Pv, Ev, 4, 1, 4) break;                                                                       \
     }
-            if (P == 64) { S3CV(64, 4) } else { S3CV(128, 2) }
+            switch (P) {   // sharded small slabs: S = 4 slices per lane, the default shape only
+                case 8: S3C(8, 16, 3, 1, 4) break;
+                case 16: S3C(16, 8, 4, 1, 4) break;
+                case 32: S3C(32, 4, 4, 1, 4) break;
+                case 64: S3CV(64, 4) break;
+                default: S3CV(128, 2) break;
+            }
 #undef S3CV
 #undef S3C
         } else if (c->split_variant == 9 && c->sband_B == 1 && P >= 64) {   // 128-register cap (4 CTAs per SM)
@@ -2891,11 +3039,11 @@ static void wam_step(Ctx* c) {
                                                       c->E3ray.p, c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3, tm);
             else k_split3p<128, 2, true, 4><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p,
                                                       c->E3ray.p, c->E3psi.p, c->q.p, c->act.p, c->off, c->koff, bm3, tm);
-        } else if ((c->split_variant == 0 || c->split_variant == 8) && c->sband_B == 1) {
-            // default: k_split3p (per-half q sums, c^l factored out, three-stage ping-pong pipeline);
+        } else if ((c->split_variant == 15 || c->split_variant == 8) && c->sband_B == 1) {
+            // 15: k_split3p (per-half q sums, c^l factored out, three-stage register ping-pong pipeline);
             // 8 = the same without the L - Pq form of z-high
 #define S3P(S, EE)                                                                                                 \
-    if (c->split_variant == 0)                                                                                     \
+    if (c->split_variant == 15)                                                                                    \
         k_split3p<S, EE, true><<<nb, 128, 0, c->st>>>(c->nlist3, c->list3.p, c->nx, c->ny, c->nzl, c->np.p,        \
                                                       c->E3ray.p, c->E3psi.p, c->q.p, c->act.p, c->off, c->koff,   \
                                                       bm3, tm);                                                    \
@@ -2929,6 +3077,7 @@ static void wam_step(Ctx* c) {
         check_launch(c, "k_split3h");
         c->timer_end(T_SPLIT);
         c->tm.split_launches++;
+        c->tm.split_entries += (int64_t)c->nnz_phi;
     } else if (!c->haar3 && c->nlist && !ovl) {
         c->timer_begin(T_SPLIT);
         const unsigned nb = (unsigned)std::min<uint64_t>((c->nlist + 7) / 8, (uint64_t)c->sms * 16);
@@ -2951,6 +3100,7 @@ static void wam_step(Ctx* c) {
         check_launch(c, "k_split3");
         c->timer_end(T_SPLIT);
         c->tm.split_launches++;
+        c->tm.split_entries += (int64_t)c->nnz_phi;
     }
     if (fused) {
         // inactive details keep b- = 0 (k_tile reads only active ones); the
@@ -3142,6 +3292,13 @@ static int64_t wam_expand(Ctx* c, double factor) {
         newly = count_diff(h.data(), c->act_host.data(), c->act_bytes);
         c->act_host.swap(h);
         if (newly > 0) {
+            c->fine_level = 0;   // finest level with an active block (coarse projections, kernels3c.cuh)
+            for (int l = 1; l <= c->L && !c->fine_level; ++l) {
+                const uint8_t* a = c->act_host.data() + c->off.off[l];
+                const uint64_t n = (uint64_t)(c->nx >> l) * (c->ny >> l);
+                for (uint64_t i = 0; i < n; ++i)
+                    if (a[i]) { c->fine_level = l; break; }
+            }
             HTRACE("expand: criterion + mark");
             phi_append(c);    // new columns of Phi^-, Z(y) and Z0 of the grown tree
             c->active = count_active(c);

@@ -1,6 +1,6 @@
 """Block-coarsened projections of the 3D wavelet-AM iteration (kernels3c.cuh):
 while the finest active tree level is lf > 1, forward and back projection run
-over the 2^(lf-1)-coarsened matrices.  The run must equal the pixel-path run
+over the 2^(lf-1)-coarsened matrices (and, mode 2, on z-groups of 2^(lf-1) slices).  The run must equal the pixel-path run
 (WAMGPU_COARSE=0): identical trees and counters, objectives and images within
 the association error of fp64 sums; WAMGPU_COARSE_CHECK verifies on the device
 that mu is constant on the blocks before every coarse forward.  Parity against
@@ -18,12 +18,13 @@ pytestmark = pytest.mark.gpu
 
 def _run(W, cfg, I0, d, coarse):
     from paper_1508_04458_b200 import configs
-    os.environ["WAMGPU_COARSE"] = "1" if coarse else "0"
+    os.environ["WAMGPU_COARSE"] = str(int(coarse))
     os.environ["WAMGPU_COARSE_CHECK"] = "1"
     try:
         c = W.Context(0)
         c.set_geometry(configs.geometry(cfg, W.Geometry))
-        c.set_haar_dim(3)
+        if cfg["nz"] > 1:
+            c.set_haar_dim(3)
         c.set_data(d, I0)
         c.wam_init(cfg["L"])
         obj, trees, done = [], [], 0
@@ -43,11 +44,26 @@ def _run(W, cfg, I0, d, coarse):
         os.environ.pop("WAMGPU_COARSE_CHECK", None)
 
 
+@pytest.mark.parametrize("mode", [1, 2])   # 1: in-plane blocks; 2 (default): in-plane blocks and z-groups
 @pytest.mark.parametrize("name", ["tiny3d16", "tiny3d64", "small3d"])
-def test_coarse_projections_equal_the_pixel_path(wam, orc, name):
+def test_coarse_projections_equal_the_pixel_path(wam, orc, name, mode):
     cfg, _, _, I0, d = problem_inputs(name, orc, wam)
-    a = _run(wam, cfg, I0, d, coarse=True)
-    b = _run(wam, cfg, I0, d, coarse=False)
+    a = _run(wam, cfg, I0, d, coarse=mode)
+    b = _run(wam, cfg, I0, d, coarse=0)
+    assert len(a["trees"]) == len(b["trees"]) > 0
+    for ta, tb in zip(a["trees"], b["trees"]):
+        assert np.array_equal(ta, tb)
+    assert a["scal"] == b["scal"]
+    assert rel_l2(a["obj"], b["obj"]) < 1e-12
+    assert rel_l2(a["mu"], b["mu"]) < 1e-6 and rel_l2(a["beta"], b["beta"]) < 1e-6
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "small_lug", "cfg1"])
+def test_coarse_projections_2d(wam, orc, name):
+    """2D wavelet AM: the CSR patch forward and the CSC back projection over Hc."""
+    cfg, _, _, I0, d = problem_inputs(name, orc, wam)
+    a = _run(wam, cfg, I0, d, coarse=2)
+    b = _run(wam, cfg, I0, d, coarse=0)
     assert len(a["trees"]) == len(b["trees"]) > 0
     for ta, tb in zip(a["trees"], b["trees"]):
         assert np.array_equal(ta, tb)

@@ -131,11 +131,15 @@ def test_wam3d_separable_haar_parity(wam, orc, name):
     assert rel_l2(bm, bm32) < TOL_MIRROR and rel_l2(bp, bp32) < TOL_MIRROR
 
 
+@pytest.mark.parametrize("root", ["phi_a", "coarse"])
 @pytest.mark.parametrize("name", ["tiny3d16", "small3d"])
-def test_root_only_iterations_use_phi_a_3d(wam, orc, name):
+def test_root_only_iterations_use_phi_a_3d(wam, orc, name, root, monkeypatch):
     """Separable 3D Haar with only the roots active: the iterations run over the
-    in-plane approximation columns (kernels_phi.cuh, 3D part), within the mirror
-    bars, and the first expansion still matches the oracle bit-exactly."""
+    in-plane approximation columns (kernels_phi.cuh, 3D part; WAMGPU_COARSE_ROOT=0)
+    or, by default, over the 2^L-coarsened matrix on z-groups (kernels3c.cuh),
+    within the mirror bars, and the first expansion still matches the oracle
+    bit-exactly."""
+    monkeypatch.setenv("WAMGPU_COARSE_ROOT", "0" if root == "phi_a" else "1")
     cfg, p64, _, I0, d = problem_inputs(name, orc, wam)
     p32 = orc.Problem(p64.geom, mirror=True)
     c = _ctx(wam, cfg)
@@ -147,7 +151,11 @@ def test_root_only_iterations_use_phi_a_3d(wam, orc, name):
     n = cfg["schedule"][0]
     og = [r["objective"] for r in c.wam_iterate(n)]
     t = c.timing()
-    assert t["phi_launches"] == n and t["fwd_launches"] == 0 and t["back_launches"] == 0
+    if root == "phi_a":
+        assert t["phi_launches"] == n and t["fwd_launches"] == 0 and t["back_launches"] == 0
+    else:
+        assert t["phi_launches"] == 0 and t["fwd_launches"] == 0 and t["back_launches"] == 0
+        assert t["coarse_fwd_launches"] == n and t["coarse_back_launches"] == n
     assert rel_l2(og, [r[1] for r in p32.wam_iterate(n)]) < TOL_MIRROR
     assert rel_l2(c.image(), p32.wam_get()["mu"]) < TOL_MIRROR
     assert c.wam_expand(0.1) == p32.wam_expand(0.1)
