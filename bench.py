@@ -607,9 +607,12 @@ def main():
     d2h = 4 * img.size
 
     iters_per_s = J / (ms_step * 1e-3)
+    dev_mem = None
     try:
         import torch
         ctx_sms = torch.cuda.get_device_properties(local).multi_processor_count
+        free_b, total_b = torch.cuda.mem_get_info(local)
+        dev_mem = {"used": round((total_b - free_b) / 2**30, 1), "total": round(total_b / 2**30, 1)}
     except Exception:
         ctx_sms = 148
     line = None
@@ -674,11 +677,15 @@ def main():
         clocks = clk.summary()
         if split_dom:
             gather = ent_avg * P_slab * 4 / (split_avg * 1e-3)
-            binding = {"resource": "L2 -> SM sector traffic of the q-row gathers (one P x 4 B row per Psi entry, "
-                                   "L2-resident through the Morton-ordered block list; ncu lts throughput in "
-                                   "profiles/r07/ncu_split3c_cfg4*.txt)",
-                       "achieved": gather / 1e9, "unit": "GB/s gathered from L2", "peak": None, "frac": None,
-                       "entries_per_s": ent_avg / (split_avg * 1e-3),
+            # not measured live: the issue-slot utilisation of the committed ncu capture of the
+            # final-tree launch (profiles/r07/ncu_split3c_cfg4_chunk.txt: issue 61.7%, fp64 pipe
+            # 34.9%, L2 31.6%, DRAM 10.4%); achieved = Psi entries per second of this run
+            binding = {"resource": "instruction issue (per Psi entry and 128 slices: 2 cp.async + 2 LDS.128 per lane, "
+                                   "8 conversions, 4 adds, 32 DFMAs per lane at level 1; q-row gathers served by L2)",
+                       "achieved": ent_avg / (split_avg * 1e-3), "unit": "Psi entries/s", "peak": None,
+                       "frac": 0.617, "frac_source": "ncu smsp__issue_active of the final-tree launch (committed "
+                                                     "capture, not this run)",
+                       "q_gather_gbs_from_l2": gather / 1e9,
                        "evidence": "profiles/r07/ncu_split3c_cfg4_chunk.txt"}
         elif nz > 1:
             mhz = clocks.get("sm_mhz") or 1965.0
@@ -725,6 +732,7 @@ def main():
             "pixel_equivalent_updates_per_s": (fwd_n + back_n + cfwd_n + cback_n) / args.steps * nnz * nz
                                               / (ms_step * 1e-3),
             "final_objective": final_obj,
+            "device_memory_gib": dev_mem,   # after the timed steps: matrices (H, coarsened Hc), Psi lists, slabs
             "tree": {"active_set_by_iteration": sorted({r["active_set"] for r in recs}),
                      "coefficients": N * nz, "phi_minus_nnz": split_nnz},
             "parity": parity,
