@@ -611,10 +611,14 @@ def main():
     try:
         import torch
         ctx_sms = torch.cuda.get_device_properties(local).multi_processor_count
-        free_b, total_b = torch.cuda.mem_get_info(local)
-        dev_mem = {"used": round((total_b - free_b) / 2**30, 1), "total": round(total_b / 2**30, 1)}
     except Exception:
         ctx_sms = 148
+    try:
+        import torch
+        free_b, total_b = torch.cuda.mem_get_info(local)
+        dev_mem = {"used": round((total_b - free_b) / 2**30, 1), "total": round(total_b / 2**30, 1)}
+    except Exception as e:
+        dev_mem = {"error": str(e)[:120]}
     line = None
     if rank == 0:
         hbm, peak_kind = _peaks()

@@ -1078,22 +1078,27 @@ __device__ __forceinline__ double f2d_wide(float f) {
 // bound by L2 -> SM traffic: ncu lts throughput 80%, profiles/r07/ncu_split3c_cfg4.txt).
 // LV 1: two z-blocks per chunk (pairs); LV 2: one z-block per chunk; LV 0 (runtime
 // level >= 3): the chunk lies inside one half (hh) of its z-block.
+// The 8 fp64 multipliers of one Psi entry, computed ONCE per entry when its index
+// batch is staged (k_split3c), not by every lane of the entry's group in every round:
+//   LV > 0: {min(psi_t,0) t = A,H,V,D;  min(-psi_A,0);  TRICK ? psi_t : min(-psi_t,0) t = H,V,D}
+//   LV 0  : {min(psi_t,0) t = A,H,V,D;  min(-psi_t,0) t = A,H,V,D}   (low-half / high-half sets)
+// min/max in fp32 (FMNMX), then exact conversions; c^l is applied once per output.
+template <int LV, bool TRICK>
+__device__ __forceinline__ void split3_multipliers(const float4& ps, double (&m)[8]) {
+    const float pf[4] = {ps.x, ps.y, ps.z, ps.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) m[t] = (double)fminf(pf[t], 0.f);
+    m[4] = (double)fminf(-pf[0], 0.f);
+#pragma unroll
+    for (int t = 1; t < 4; ++t) m[4 + t] = (LV > 0 && TRICK) ? (double)pf[t] : (double)fminf(-pf[t], 0.f);
+}
 template <int S, int LV, bool TRICK>
-__device__ __forceinline__ void split3_consume(const float4& ps, const float (&f)[S], bool hh,
+__device__ __forceinline__ void split3_consume(const double (&m)[8], const float (&f)[S], bool hh,
                                                double (&acc)[(S / 4) * (LV == 1 ? 14 : 7)]) {
     constexpr int V = S / 4;
-    const float pf[4] = {ps.x, ps.y, ps.z, ps.w};
-    double m[8];
     if constexpr (LV > 0) {
         constexpr int HS = LV;            // half size in slices: 1 or 2
         constexpr int NZ = 2 / HS;        // z-blocks per chunk
-        // m[0..3] = min(psi_t, 0) (t = A,H,V,D); m[4] = min(-psi_A, 0);
-        // m[5..7] = TRICK ? psi_t : min(-psi_t, 0) (t = H,V,D)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) m[t] = (double)fminf(pf[t], 0.f);
-        m[4] = (double)fminf(-pf[0], 0.f);
-#pragma unroll
-        for (int t = 1; t < 4; ++t) m[4 + t] = TRICK ? (double)pf[t] : (double)fminf(-pf[t], 0.f);
 #pragma unroll
         for (int v = 0; v < V; ++v)
 #pragma unroll
@@ -1116,20 +1121,19 @@ __device__ __forceinline__ void split3_consume(const float4& ps, const float (&f
                 }
             }
     } else {
-        // m[0..2] = min(psi_t, 0) (t = H,V,D: z-low); m[3..6] = this lane's half of z-high
-        // (low half min(psi,0), high half min(-psi,0)), scaled by 2^-896 (bit move)
+        // z-low: min(psi_t,0), t = H,V,D; z-high: this lane's half (low: min(psi,0), high: min(-psi,0))
+        double mh[4];
 #pragma unroll
-        for (int t = 1; t < 4; ++t) m[t - 1] = f2d_wide<true>(fminf(pf[t], 0.f));
-#pragma unroll
-        for (int t = 0; t < 4; ++t) m[3 + t] = f2d_wide<true>(fminf(hh ? -pf[t] : pf[t], 0.f));
+        for (int t = 0; t < 4; ++t) mh[t] = hh ? m[4 + t] : m[t];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             double qs = f2d_wide<false>(f[4 * v]);
 #pragma unroll
             for (int i = 1; i < 4; ++i) qs += f2d_wide<false>(f[4 * v + i]);
-            qs *= kTwo896;   // exact: the multipliers carry the 2^-896 here
 #pragma unroll
-            for (int t = 0; t < 7; ++t) acc[7 * v + t] = fma(m[t], qs, acc[7 * v + t]);
+            for (int t = 0; t < 3; ++t) acc[7 * v + t] = fma(m[1 + t], qs, acc[7 * v + t]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) acc[7 * v + 3 + t] = fma(mh[t], qs, acc[7 * v + 3 + t]);
         }
     }
 }
@@ -1138,7 +1142,7 @@ struct Split3cSmem {
     static constexpr int S = P * E / 32;
     float4 ring[4][D][S / 4][32];   // [warp][round % D][16-byte part][lane]
     unsigned iray[4][2][32];        // [warp][batch % 2][entry]
-    float4 ipsi[4][2][32];
+    double2 imul[4][2][4][32];      // [warp][batch % 2][multiplier pair][entry]: 8 fp64 multipliers per entry
     double red[4][7][P / 2];
 };
 template <int P, int E, int LV, bool TRICK, int D, int WPI>
@@ -1179,7 +1183,10 @@ __device__ __forceinline__ void split3c_block(unsigned b, int l, int lane, int w
     };
     auto sts_batch = [&](uint64_t k) {
         sm.iray[wib][k & 1][lane] = ry;
-        sm.ipsi[wib][k & 1][lane] = rp;
+        double m[8];
+        split3_multipliers<LV, TRICK>(rp, m);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) sm.imul[wib][k & 1][t][lane] = make_double2(m[2 * t], m[2 * t + 1]);
     };
     auto issue_q = [&](uint64_t r) {   // q row parts of round r into ring slot r % D
         if (r < nr) {
@@ -1207,7 +1214,12 @@ __device__ __forceinline__ void split3c_block(unsigned b, int l, int lane, int w
                 __syncwarp();
             }
             issue_q(ra);
-            const float4 ps = sm.ipsi[wib][(r / RPB) & 1][(r % RPB) * E + grp];
+            double m[8];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const double2 mm = sm.imul[wib][(r / RPB) & 1][t][(r % RPB) * E + grp];
+                m[2 * t] = mm.x; m[2 * t + 1] = mm.y;
+            }
             cp_async_wait<D - 1>();
             float f[S];
 #pragma unroll
@@ -1215,7 +1227,7 @@ __device__ __forceinline__ void split3c_block(unsigned b, int l, int lane, int w
                 const float4 t4 = sm.ring[wib][r % D][v][lane];
                 f[4 * v] = t4.x; f[4 * v + 1] = t4.y; f[4 * v + 2] = t4.z; f[4 * v + 3] = t4.w;
             }
-            split3_consume<S, LV, TRICK>(ps, f, hh, acc);
+            split3_consume<S, LV, TRICK>(m, f, hh, acc);
         }
         cp_async_wait<0>();
     }

@@ -3005,10 +3005,10 @@ static void wam_step(Ctx* c) {
                 default: S3Z(128) break;
             }
 #undef S3Z
-        } else if ((c->split_variant == 0 || (c->split_variant >= 10 && c->split_variant <= 14)) && c->sband_B == 1) {
+        } else if ((c->split_variant == 0 || (c->split_variant >= 10 && c->split_variant <= 14 && c->split_variant != 13)) && c->sband_B == 1) {
             // k_split3c (default = 11): cp.async ring of D rounds, dynamic Morton-order scheduling, chunk
             // lane map.  10: 4 warps per block, D 4, 4 CTAs per SM; 11: warp per block; 12: 4 warps per
-            // block, 3 CTAs per SM; 13: D 6; 14: D 2.  cfg4 split per run 915 / 889 / 955 / 1073 ms for
+            // block, 3 CTAs per SM; 14: D 2 (13, D 6, went when the per-entry multipliers took its shared memory).  cfg4 split per run 915 / 889 / 955 / 1073 ms for
             // 10 / 11 / 12 / 13 (k_split3h_e: 1700), cfg3 101 / 98 / 106 / 118 (180): profiles/r07/ab5_split_sectors.txt
 #define S3C(Pv, Ev, Dv, Wv, Mv)                                                                                    \
     {                                                                                                              \
@@ -3021,7 +3021,6 @@ static void wam_step(Ctx* c) {
     switch (c->split_variant) {                                                                                    \
         case 10: S3C(Pv, Ev, 4, 4, 4) break;                                                                       \
         case 12: S3C(Pv, Ev, 4, 4, 3) break;                                                                       \
-        case 13: S3C(Pv, Ev, 6, 4, 4) break;                                                                       \
         case 14: S3C(Pv, Ev, 2, 4, 4) break;                                                                       \
         default: S3C(Pv, Ev, 4, 1, 4) break;                                                                       \
     }
