@@ -613,10 +613,11 @@ def main():
         ctx_sms = torch.cuda.get_device_properties(local).multi_processor_count
     except Exception:
         ctx_sms = 148
-    try:
-        import torch
-        free_b, total_b = torch.cuda.mem_get_info(local)
-        dev_mem = {"used": round((total_b - free_b) / 2**30, 1), "total": round(total_b / 2**30, 1)}
+    try:   # NVML, not torch: libwamgpu has the system NCCL loaded, torch's CUDA library wants its own
+        import pynvml
+        pynvml.nvmlInit()
+        mi = pynvml.nvmlDeviceGetMemoryInfo(pynvml.nvmlDeviceGetHandleByIndex(local))
+        dev_mem = {"used": round(mi.used / 2**30, 1), "total": round(mi.total / 2**30, 1)}
     except Exception as e:
         dev_mem = {"error": str(e)[:120]}
     line = None

@@ -204,7 +204,9 @@ __global__ void k_qsum_z(uint64_t M, int nzc, int P, int Pw, int k, const float*
     reinterpret_cast<float2*>(wz + y * Pw)[zg] = make_float2(hi, lo);
 }
 // g[x][s] = (Gc[B][2 zg] + Gc[B][2 zg + 1]) * 8^-k, zg = s >> k: the cube mean on every voxel
-__global__ void k_g_expand_z(uint64_t N, int nxc, int nx, int k, int P, int Pw, int nz,
+// seg > 1: column B was back-projected in seg segments (rows B*seg .. B*seg+seg-1 of gc),
+// added here in segment order
+__global__ void k_g_expand_z(uint64_t N, int nxc, int nx, int k, int P, int Pw, int nz, int seg,
                              const double* __restrict__ gc, double* __restrict__ g) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N * (uint64_t)nz) return;
@@ -212,8 +214,21 @@ __global__ void k_g_expand_z(uint64_t N, int nxc, int nx, int k, int P, int Pw, 
     const int s = (int)(i % nz);
     const uint64_t iy = x / nx, ix = x % nx;
     const uint64_t B = (iy >> k) * (uint64_t)nxc + (ix >> k);
-    const double2 t = __ldg(reinterpret_cast<const double2*>(gc + B * Pw) + (s >> k));
-    g[x * P + s] = (t.x + t.y) * (1.0 / (double)(1u << (3 * k)));
+    double hi = 0.0, lo = 0.0;
+    for (int j = 0; j < seg; ++j) {
+        const double2 t = __ldg(reinterpret_cast<const double2*>(gc + (B * seg + j) * Pw) + (s >> k));
+        hi += t.x; lo += t.y;
+    }
+    g[x * P + s] = (hi + lo) * (1.0 / (double)(1u << (3 * k)));
+}
+// bounds of the column segments: cpseg[B*seg + j] = cp[B] + len_B * j / seg, cpseg[Nc*seg] = cp[Nc]
+__global__ void k_seg_bounds(uint64_t Nc, int seg, const unsigned long long* __restrict__ cp,
+                             unsigned long long* __restrict__ cpseg) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > Nc * (uint64_t)seg) return;
+    if (i == Nc * (uint64_t)seg) { cpseg[i] = cp[Nc]; return; }
+    const uint64_t B = i / seg, j = i % seg, lo = cp[B], len = cp[B + 1] - lo;
+    cpseg[i] = lo + len * j / seg;
 }
 
 }  // namespace wamgpu

@@ -144,6 +144,16 @@ __global__ void k_tile3h(int mode, int nx, int ny, int nzl, int P, int L, const 
         }
         return;
     }
+    if (mode == 3) {   // b+ / b- of every coefficient only (wamgpu_get_stats after a coarse-domain update)
+        for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+            const int z = e % TS, r = e / TS, i = r / TS, j = r % TS;
+            const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, L, nx, ny, nzl, P, act, off);
+            const double bmv = ci.approx ? 0.0 : bm[ci.idx];
+            bp_out[ci.idx] = x[(z * TS + i) * TS + j] - bmv;
+            bm_out[ci.idx] = bmv;
+        }
+        return;
+    }
     unsigned long long upd = 0, deg = 0;
     for (int e = threadIdx.x; e < T3; e += blockDim.x) {
         const int z = e % TS, r = e / TS, i = r / TS, j = r % TS;
@@ -185,6 +195,90 @@ __global__ void k_tile3h(int mode, int nx, int ny, int nzl, int P, int L, const 
         const uint64_t p = vox(z, i, j);
         mu[p] = (float)x[(z * TS + i) * TS + j];
         if (mu64) mu64[p] = x[(z * TS + i) * TS + j];
+    }
+}
+
+// k_tile3h mode 1 in the COARSE domain (kernels3c.cuh): while the finest active
+// level is k + 1, the update needs only the levels above k, i.e. the leading
+// (TS >> k)^3 corner of every tile's transform, and that corner is the transform
+// of the 2^k-cube sums G of g.  One CTA per tile works on the (TS >> k)^3 cube:
+//   a_k   = G kC3^k 2^-k   (k roundings, exactly what k levels of cube_fwd make of the
+//           cube mean G 8^-k spread over the cube: sums of equal values and the
+//           factors 1/2, 4 are exact, only the products by kC3 round)
+//   cube_fwd over the remaining L - k levels, the same root solves, cube_inv,
+//   mu_c = k times (v kC3) / 2   (cube_inv with zero details below level k + 1)
+// so beta and the coarse mu are BIT-IDENTICAL to the full-tile update followed by
+// k_mu_coarse_z.  The coefficient positions of the corner are the tile's own
+// (coef_info3 unchanged).  mu_c goes straight into the z-coarse forward operand;
+// the pixel mu is left stale (synthesised from beta when read).  b+ / b- of the
+// levels below k + 1 are not produced here (k_tile3h mode 3 on demand).
+// gc: Nc*seg rows of Pw doubles, (hi, lo) pairs per z-group (k_back3s over Hc).
+__global__ void k_tile3hc(int k, int nx, int ny, int nzl, int P, int L, int Pw, int seg, int Pc,
+                          const double* __restrict__ gc, const double* __restrict__ bm,
+                          const double* __restrict__ bdata, const uint8_t* __restrict__ act, ActOff off,
+                          float* __restrict__ beta, float* __restrict__ muc, double* __restrict__ bp_out,
+                          double* __restrict__ bm_out, double Z0, unsigned long long* __restrict__ counters,
+                          int* __restrict__ flag) {
+    extern __shared__ double smh[];
+    const int Lc = L - k, TS = 1 << Lc, T3 = TS * TS * TS, nxc = nx >> k;
+    double* x = smh;
+    double* t = smh + T3;
+    const int tj = blockIdx.x, ti = blockIdx.y, kt = blockIdx.z;
+    const double half_k = 1.0 / (double)(1 << k);
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, r = e / TS, i = r / TS, j = r % TS;
+        const uint64_t B = (uint64_t)(ti * TS + i) * nxc + (tj * TS + j);
+        const int zg = kt * TS + z;
+        double hi = 0.0, lo = 0.0;
+        for (int sg = 0; sg < seg; ++sg) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(gc + (B * seg + sg) * Pw) + zg);
+            hi += v.x; lo += v.y;
+        }
+        double v = hi + lo;
+        for (int q = 0; q < k; ++q) v = v * kC3;
+        x[(z * TS + i) * TS + j] = v * half_k;
+    }
+    __syncthreads();
+    cube_fwd(x, t, TS, Lc);
+    unsigned long long upd = 0, deg = 0;
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, r = e / TS, i = r / TS, j = r % TS;
+        const CoefInfo3 ci = coef_info3(z, i, j, kt, ti, tj, L, nx, ny, nzl, P, act, off);
+        float bo = beta[ci.idx];
+        const double bmv = ci.approx ? 0.0 : bm[ci.idx];
+        const double bpv = x[(z * TS + i) * TS + j] - bmv;
+        if (bp_out) { bp_out[ci.idx] = bpv; bm_out[ci.idx] = bmv; }
+        if (ci.active) {
+            double nb;
+            const int rr = solve_update(bdata[ci.idx], bpv, bmv, Z0, (double)bo, &nb);
+            if (rr == 0) {
+                if (!isfinite(nb)) atomicOr(flag, 4);
+                bo = (float)nb;
+                beta[ci.idx] = bo;
+                ++upd;
+            } else if (rr == 2) {
+                ++deg;
+            }
+        }
+        x[(z * TS + i) * TS + j] = (double)bo;
+    }
+    // (blockDim.x is a multiple of 32: full warps)
+    for (int o = 16; o > 0; o >>= 1) {
+        upd += __shfl_xor_sync(0xffffffffu, upd, o);
+        deg += __shfl_xor_sync(0xffffffffu, deg, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (upd) atomicAdd(counters + 0, upd);
+        if (deg) atomicAdd(counters + 1, deg);
+    }
+    __syncthreads();
+    cube_inv(x, t, TS, Lc);
+    for (int e = threadIdx.x; e < T3; e += blockDim.x) {
+        const int z = e % TS, r = e / TS, i = r / TS, j = r % TS;
+        double v = x[(z * TS + i) * TS + j];
+        for (int q = 0; q < k; ++q) v = (v * kC3) * 0.5;
+        const uint64_t B = (uint64_t)(ti * TS + i) * nxc + (tj * TS + j);
+        muc[B * Pc + (kt * TS + z)] = (float)v;
     }
 }
 

@@ -258,12 +258,16 @@ struct wamgpu_ctx {
         DBuf<unsigned long long> rp, cp;
         DBuf<unsigned> col, row, order;
         DBuf<double> val, valC;
+        int seg = 1;                          // column segments of the z-coarse back projection
+        DBuf<unsigned long long> cpseg;       // seg > 1: Nc*seg + 1 segment bounds (k_seg_bounds)
     } coarse[6];   // index k = 1 .. LMAX
     DBuf<float> mu_c;                   // mu on the coarse grid (forward operand)
     DBuf<double> g_c;                   // block sums of g (coarse back projection)
     DBuf<double> l_c;                   // z-coarse line integrals [ray][z-group]
     DBuf<float> w_z;                    // z-group sums of q as hi/lo pairs
     int fine_level = 0;                 // finest level with an active block (0: none)
+    int mu_c_k = -1;                    // mu_c holds the z-coarse mu of this k (written by the coarse-domain update)
+    int stats_k = -1;                   // >= 0: bp_dbg / bm_dbg lack the levels <= k (coarse-domain update): refresh on read
     std::vector<std::vector<unsigned>> morton;   // per level: in-plane blocks in Morton order (host, cached)
     int morton_nx = 0, morton_ny = 0;
     uint64_t nlist3 = 0;
@@ -649,7 +653,7 @@ static void finish_matrix(Ctx* c, bool have_csc = false) {
     for (auto& cm : c->coarse) {
         cm.ok = false;
         cm.rp.release(); cm.cp.release(); cm.col.release(); cm.row.release(); cm.order.release();
-        cm.val.release(); cm.valC.release();
+        cm.val.release(); cm.valC.release(); cm.cpseg.release(); cm.seg = 1;
     }
     c->phiA_rp.release(); c->phiA_cp.release(); c->phiA_col.release(); c->phiA_row.release();
     c->phiA_val.release(); c->phiA_valC.release(); c->phiA_part.release();
@@ -1477,6 +1481,7 @@ static int coarse_k(const Ctx* c);
 static int coarse_mode();
 static unsigned fwd2c_launch(Ctx* c, int k);
 static unsigned fwd3c_launch(Ctx* c, int k, unsigned maxblk);
+static void sync_mu(Ctx* c);
 // q = I0 exp(-H mu), objective -> scal[0] (all-reduced), record
 static void forward_fused(Ctx* c, bool record) {
     const int ck = c->algo == 2 ? coarse_k(c) : 0;
@@ -2429,6 +2434,8 @@ static void wam_init(Ctx* c, int L, const double* init_beta) {
     c->nlist = 0;
     c->nlist3 = 0;
     c->fine_level = 0;
+    c->mu_c_k = -1;
+    c->stats_k = -1;
     c->nnz_phi = 0;
     c->phi_batch = 0;
     if (!c->haar3) {                     // 3D: the tree is empty, no Psi lists yet
@@ -2597,6 +2604,15 @@ static void build_coarse(Ctx* c, int k) {
         m.order.alloc(m.Nc);
         CK(cudaMemcpyAsync(m.order.p, o.data(), m.Nc * 4, cudaMemcpyHostToDevice, c->st));
     }
+    // few, long columns (root phase at cfg4: 4,096 columns of ~3e4 entries, 64 CTAs on 148 SMs:
+    // 2.9 ms per launch, profiles/r07/ncu_coarse_root_cfg4.txt): the z-coarse back projection runs
+    // over column SEGMENTS and k_g_expand_z adds a column's partials in segment order
+    m.seg = c->nzl > 1 ? (m.Nc <= 4096 ? 8 : (m.Nc <= 16384 ? 4 : (m.Nc <= 65536 ? 2 : 1))) : 1;
+    if (m.seg > 1) {
+        m.cpseg.alloc(m.Nc * m.seg + 1);
+        k_seg_bounds<<<blocks_for(m.Nc * m.seg + 1, 256), 256, 0, c->st>>>(m.Nc, m.seg, m.cp.p, m.cpseg.p);
+        check_launch(c, "k_seg_bounds");
+    }
     CK(cudaStreamSynchronize(c->st));
     c->cub_tmp.release();
     m.nnz = nnz;
@@ -2620,8 +2636,7 @@ static unsigned fwd2c_launch(Ctx* c, int k) {
     k_fwd_patch<1, 4, 8, 5, Ent64><<<c->nblk_row, 256, 0, c->st>>>(c->Ml, m.rp.p, Ent64{m.col.p, m.val.p}, c->mu_c.p,
                                                                   c->I0.p, c->d.p, c->q.p, nullptr, c->partial.p,
                                                                   c->flag.p);
-    check_launch(c, "k_fwd_patch (coarse)");
-    launched(c, 1);
+    // (counted by forward_fused's check_launch)
     return (unsigned)c->nblk_row;
 }
 static void back2c_into(Ctx* c, int k, const float* w, double* out) {
@@ -2635,7 +2650,6 @@ static void back2c_into(Ctx* c, int k, const float* w, double* out) {
     check_launch(c, "k_back (coarse)");
     k_g_expand2<<<blocks_for(c->N, 256), 256, 0, c->st>>>(c->N, c->nx >> k, c->nx, k, c->g_c.p, out);
     check_launch(c, "k_g_expand2");
-    launched(c, 1);
     c->timer_end(T_BACKC);
     c->tm.coarse_back_launches++;
     c->tm.proj_updates += (int64_t)m.nnz;
@@ -2669,6 +2683,7 @@ static unsigned fwd3c_launch(Ctx* c, int k, unsigned maxblk) {
     const int nzc = c->nzl >> k, Pc = pow2_stride(nzc);
     c->mu_c.ensure(m.Nc * (zc ? Pc : P));
     if (std::getenv("WAMGPU_COARSE_CHECK") != nullptr) {
+        sync_mu(c);
         CK(cudaMemsetAsync(c->flag2.p, 0, 4, c->st));
         if (zc)
             k_mu_coarse_check_z<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->N, c->nx, k, P, c->nzl, c->mu.p, c->flag2.p);
@@ -2681,9 +2696,12 @@ static unsigned fwd3c_launch(Ctx* c, int k, unsigned maxblk) {
     }
     if (zc) {
         c->l_c.ensure(c->Ml * Pc);
-        k_mu_coarse_z<<<blocks_for(m.Nc * Pc, 256), 256, 0, c->st>>>(m.Nc, c->nx >> k, c->nx, k, P, Pc, nzc, c->mu.p,
-                                                                     c->mu_c.p);
-        check_launch(c, "k_mu_coarse_z");
+        if (c->mu_c_k != k) {   // (the coarse-domain update leaves mu_c ready)
+            sync_mu(c);
+            k_mu_coarse_z<<<blocks_for(m.Nc * Pc, 256), 256, 0, c->st>>>(m.Nc, c->nx >> k, c->nx, k, P, Pc, nzc,
+                                                                         c->mu.p, c->mu_c.p);
+            check_launch(c, "k_mu_coarse_z");
+        }
         switch (Pc) {
             case 8: fwd3cz_launch_p<8>(c, k, nzc); break;
             case 16: fwd3cz_launch_p<16>(c, k, nzc); break;
@@ -2694,10 +2712,10 @@ static unsigned fwd3c_launch(Ctx* c, int k, unsigned maxblk) {
         const unsigned nbz = std::min<unsigned>((unsigned)c->sms * 8, maxblk);
         k_beer_z<<<nbz, 256, 0, c->st>>>(c->Ml, c->nzl, P, Pc, k, c->l_c.p, c->I0.p, c->d.p, c->q.p, c->partial.p,
                                         c->flag.p);
-        check_launch(c, "k_beer_z");
-        launched(c, 2);
+        // (k_beer_z is counted by forward_fused's check_launch)
         return nbz;
     }
+    c->mu_c_k = -1;
     k_mu_coarse<<<blocks_for(m.Nc * (P / 4), 256), 256, 0, c->st>>>(m.Nc, c->nx >> k, c->nx, k, P, c->mu.p, c->mu_c.p);
     check_launch(c, "k_mu_coarse");
     unsigned nb = 0;
@@ -2708,8 +2726,7 @@ static unsigned fwd3c_launch(Ctx* c, int k, unsigned maxblk) {
         case 64: nb = fwd3c_launch_p<64>(c, k, maxblk); break;
         default: nb = fwd3c_launch_p<128>(c, k, maxblk); break;
     }
-    check_launch(c, "k_fwd3s (coarse)");
-    launched(c, 1);
+    // (counted by forward_fused's check_launch)
     return nb;
 }
 // g = expand(Hc^T w): block sums over the coarse CSC, then the block mean on every pixel
@@ -2726,19 +2743,25 @@ template <int PW>
 static void back3cz_launch_p(Ctx* c, int k, int nzw) {
     using S = SlabShape<PW>;
     Ctx::Coarse& m = c->coarse[k];
-    const unsigned nb = nblk_warp(c, (m.Nc + S::G - 1) / S::G);
+    const uint64_t ncol = m.Nc * (uint64_t)m.seg;   // seg > 1: column segments in column order (no tile order)
+    const unsigned nb = nblk_warp(c, (ncol + S::G - 1) / S::G);
     k_back3s<0, S::LPR, S::SPL, 104, 1, true, PW, 8, 2, Ent64><<<nb, 256, 0, c->st>>>(
-        m.Nc, 0, nzw, m.order.p, m.cp.p, Ent64{m.row.p, m.valC.p}, c->w_z.p, c->g_c.p, nullptr, nullptr, 0.0,
-        c->flag.p, TileMap{});
+        ncol, 0, nzw, m.seg > 1 ? nullptr : m.order.p, m.seg > 1 ? m.cpseg.p : m.cp.p, Ent64{m.row.p, m.valC.p},
+        c->w_z.p, c->g_c.p, nullptr, nullptr, 0.0, c->flag.p, TileMap{});
 }
-static void back3c_into(Ctx* c, int k, const float* w, double* out) {
+static bool coarse_update_on(const Ctx* c) {   // WAMGPU_COARSE_UPDATE=0: full-tile update after expanding g
+    const char* e = std::getenv("WAMGPU_COARSE_UPDATE");
+    return coarse_mode() >= 2 && c->haar3 && c->nzl > 1 && !(e && e[0] == '0');
+}
+// expand = false: leave the cube sums in g_c for the coarse-domain update (tile_update_coarse)
+static void back3c_into(Ctx* c, int k, const float* w, double* out, bool expand = true) {
     build_coarse(c, k);
     Ctx::Coarse& m = c->coarse[k];
     const int P = slab_stride(c);
     if (coarse_mode() >= 2) {   // z-group sums of w as hi/lo pairs, block x z-group sums of g, cube means
         const int nzc = c->nzl >> k, Pw = pow2_stride(2 * nzc);
         c->w_z.ensure(c->Ml * Pw);
-        c->g_c.ensure(m.Nc * Pw);
+        c->g_c.ensure(m.Nc * m.seg * Pw);
         c->timer_begin(T_BACKC);
         k_qsum_z<<<blocks_for(c->Ml * (Pw / 2), 256), 256, 0, c->st>>>(c->Ml, nzc, P, Pw, k, w, c->w_z.p);
         check_launch(c, "k_qsum_z");
@@ -2750,10 +2773,11 @@ static void back3c_into(Ctx* c, int k, const float* w, double* out) {
             default: back3cz_launch_p<128>(c, k, 2 * nzc); break;
         }
         check_launch(c, "k_back3s (z-coarse)");
-        k_g_expand_z<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->N, c->nx >> k, c->nx, k, P, Pw, c->nzl,
-                                                                         c->g_c.p, out);
-        check_launch(c, "k_g_expand_z");
-        launched(c, 2);
+        if (expand) {
+            k_g_expand_z<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->N, c->nx >> k, c->nx, k, P, Pw,
+                                                                             c->nzl, m.seg, c->g_c.p, out);
+            check_launch(c, "k_g_expand_z");
+        }
         c->timer_end(T_BACKC);
         c->tm.coarse_back_launches++;
         c->tm.proj_updates += (int64_t)(m.nnz * (uint64_t)(2 * nzc));
@@ -2771,10 +2795,30 @@ static void back3c_into(Ctx* c, int k, const float* w, double* out) {
     check_launch(c, "k_back3s (coarse)");
     k_g_expand<<<blocks_for(c->N * (P / 2), 256), 256, 0, c->st>>>(c->N, c->nx >> k, c->nx, k, P, c->g_c.p, out);
     check_launch(c, "k_g_expand");
-    launched(c, 1);
     c->timer_end(T_BACKC);
     c->tm.coarse_back_launches++;
     c->tm.proj_updates += (int64_t)(m.nnz * (uint64_t)c->nzl);
+}
+
+// analysis, root solves and synthesis on the (TS >> k)^3 corner of every tile (k_tile3hc):
+// beta and the z-coarse mu_c bit-identical to the full-tile update; the pixel mu goes stale
+static void tile_update_coarse(Ctx* c, int k) {
+    Ctx::Coarse& m = c->coarse[k];
+    const int P = slab_stride(c), nzc = c->nzl >> k, Pw = pow2_stride(2 * nzc), Pc = pow2_stride(nzc);
+    const int TS = 1 << (c->L - k), T3 = TS * TS * TS;
+    c->mu_c.ensure(m.Nc * Pc);
+    dim3 grid(c->nx >> c->L, c->ny >> c->L, c->nzl >> c->L);
+    const int bs = T3 >= 256 ? 256 : (T3 >= 64 ? 64 : 32);
+    const size_t smem = 2ull * T3 * sizeof(double);
+    if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(k_tile3hc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_tile3hc<<<grid, bs, smem, c->st>>>(k, c->nx, c->ny, c->nzl, P, c->L, Pw, m.seg, Pc, c->g_c.p, c->g.p + NV(c),
+                                         c->bdata.p, c->act.p, c->off, c->beta.p, c->mu_c.p, c->bp_dbg.p,
+                                         c->bm_dbg.p, c->Z0, c->counters.p, c->flag.p);
+    check_launch(c, "k_tile3hc");
+    c->mu_stale = true;
+    c->mu_c_k = k;
+    c->stats_k = k;
 }
 
 // one wavelet-AM iteration with only the roots active: S = Φ_Aᵀ q̂, root
@@ -2959,13 +3003,15 @@ static void wam_step(Ctx* c) {
         c->tm.split_entries += (int64_t)c->nnz_phi;
         CK(cudaEventRecord(c->ev_y, c->st2));
     }
+    // block-coarsened projections (kernels3c.cuh) and, in 3D, the update in the coarse domain
+    const int ck = (!split && !fused) ? coarse_k(c) : 0;
+    const bool cupd = ck > 0 && coarse_update_on(c) && !view_sharded(c);   // (view shards all-reduce the pixel g)
     if (split) {
         back_launch(c, c->q.p, c->rs_send.p, nullptr, true, tm);   // g straight into the tile-major T
         CK(cudaEventRecord(c->ev_x, c->st));
     } else if (!fused) {
-        const int ck = coarse_k(c);
         if (ck > 0 && c->nzl == 1) back2c_into(c, ck, c->q.p, c->g.p);
-        else if (ck > 0) back3c_into(c, ck, c->q.p, c->g.p);
+        else if (ck > 0) back3c_into(c, ck, c->q.p, c->g.p, !cupd);
         else back_into(c, c->q.p, c->g.p);
     }
     if (c->haar3 && c->nlist3) {
@@ -3124,7 +3170,13 @@ static void wam_step(Ctx* c) {
     }
     if (ovl) CK(cudaStreamWaitEvent(c->st, c->ev_y, 0));
     c->timer_begin(T_UPDATE);
-    tile_launch(c, 1, nullptr, nullptr);
+    if (cupd) {
+        tile_update_coarse(c, ck);
+    } else {
+        tile_launch(c, 1, nullptr, nullptr);
+        c->mu_c_k = -1;
+        c->stats_k = -1;
+    }
     c->timer_end(T_UPDATE);
     c->tm.update_launches++;
     forward_fused(c, true);
@@ -4039,6 +4091,16 @@ int wamgpu_get_stats(const wamgpu_ctx* ctx, double* b, double* bp, double* bm) {
         NEED(ctx);
         Ctx* c = const_cast<wamgpu_ctx*>(ctx);
         if (c->algo != 2) throw ContractError("get_stats: no wavelet-AM state");
+        if (c->stats_k > 0 && c->coarse[c->stats_k].ok) {
+            // the last update ran in the coarse domain: b+ / b- of the levels below were not
+            // produced.  Expand the cube sums still held in g_c and analyse the full tiles.
+            const int k = c->stats_k, P = slab_stride(c), nzc = c->nzl >> k, Pw = pow2_stride(2 * nzc);
+            k_g_expand_z<<<blocks_for(c->N * c->nzl, 256), 256, 0, c->st>>>(c->N, c->nx >> k, c->nx, k, P, Pw, c->nzl,
+                                                                             c->coarse[k].seg, c->g_c.p, c->g.p);
+            check_launch(c, "k_g_expand_z");
+            tile_launch(c, 3, nullptr, nullptr);
+            c->stats_k = -1;
+        }
         if (b) download_slab<double>(c, c->bdata.p, b, c->N, c->N, 0);
         if (bp) download_slab<double>(c, c->bp_dbg.p, bp, c->N, c->N, 0);
         if (bm) download_slab<double>(c, c->bm_dbg.p, bm, c->N, c->N, 0);
