@@ -187,21 +187,23 @@ __global__ void __launch_bounds__(256) k_beer_z(uint64_t M, int nz, int P, int P
     }
 }
 // wz[y][2 zg], wz[y][2 zg + 1] = hi, lo of the slice-order fp64 sum of q over z-group zg
-__global__ void k_qsum_z(uint64_t M, int nzc, int P, int Pw, int k, const float* __restrict__ q,
+// dbl: the 8 bytes hold the fp64 sum itself (double-operand back projection, k_back3s XD)
+__global__ void k_qsum_z(uint64_t M, int nzc, int P, int Pw, int k, int dbl, const float* __restrict__ q,
                          float* __restrict__ wz) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= M * (uint64_t)(Pw / 2)) return;
     const uint64_t y = i / (Pw / 2);
     const int zg = (int)(i % (Pw / 2));
     float hi = 0.f, lo = 0.f;
+    double S = 0.0;
     if (zg < nzc) {
         const float* p = q + y * P + ((uint64_t)zg << k);
-        double S = 0.0;
         for (int j = 0; j < (1 << k); ++j) S += (double)__ldg(p + j);
         hi = (float)S;
         lo = (float)(S - (double)hi);
     }
-    reinterpret_cast<float2*>(wz + y * Pw)[zg] = make_float2(hi, lo);
+    if (dbl) reinterpret_cast<double*>(wz + y * Pw)[zg] = S;
+    else reinterpret_cast<float2*>(wz + y * Pw)[zg] = make_float2(hi, lo);
 }
 // g[x][s] = (Gc[B][2 zg] + Gc[B][2 zg + 1]) * 8^-k, zg = s >> k: the cube mean on every voxel
 // seg > 1: column B was back-projected in seg segments (rows B*seg .. B*seg+seg-1 of gc),

@@ -145,7 +145,11 @@ template <int G> struct SlabStage {
 // a round is consumed instead of travelling with the gathers.  The copy
 // pipeline below moves 40 registers per round (IMAD.MOV: 50 of the 185 SASS
 // instructions of a 32-DFMA round at P = 128).
-template <int LPR, int SPL, int UX, int NF, bool SIGNED, int P, class AP>
+// XD: x is a slab of DOUBLES seen as float pairs (stride P floats = P/2 doubles): the loads
+// and the lane-to-slice map are those of the float slab, a lane's SPL floats are SPL/2
+// doubles (a float4 chunk = 2 doubles), and acc[0 .. SPL/2) take plain DFMAs with no
+// conversion at all (the z-coarse back projection over fp64 z-group sums, kernels3c.cuh).
+template <int LPR, int SPL, int UX, int NF, bool SIGNED, int P, bool XD = false, class AP>
 __device__ __forceinline__ void slab_dot_g(const AP& A, const float* __restrict__ x, uint64_t lo,
                                            uint64_t hi, int maxlen, int lig, int g,
                                            SlabStage<32 / LPR>& st, double (&acc)[SPL]) {
@@ -235,11 +239,19 @@ __device__ __forceinline__ void slab_dot_g(const AP& A, const float* __restrict_
                 for (int k = 0; k < 2; ++k) {
                     float f[SPL];
                     slab_unpack<SPL>(vv[u + k], f);
+                    if constexpr (XD) {
+                        static_assert(SPL >= 4 && SPL % 2 == 0, "double operand: float4 chunks");
+#pragma unroll
+                        for (int j = 0; j < SPL / 2; ++j)
+                            acc[j] = fma(hp[k], __hiloint2double(__float_as_int(f[2 * j + 1]), __float_as_int(f[2 * j])),
+                                         acc[j]);
+                    } else {
                     const double hs = hp[k] * kTwo896;
 #pragma unroll
                     for (int j = 0; j < SPL; ++j) {
                         if ((((u + k) * SPL + j) & 3) < NF) acc[j] = fma(hp[k], (double)f[j], acc[j]);
                         else acc[j] = fma(hs, f2d_scaled<SIGNED>(f[j]), acc[j]);
+                    }
                     }
                 }
             }
@@ -255,6 +267,7 @@ __device__ __forceinline__ void slab_dot_g(const AP& A, const float* __restrict_
         }
         return;
     }
+    static_assert(PP || !XD, "double operand: ping-pong pipeline only");
     issue(0, 0);
     // (an explicit two-set ping-pong without these copies was measured slower:
     // 156 registers uncapped, 8.77 vs 8.04 ms at cfg5 with a 128 cap)
@@ -498,7 +511,8 @@ __device__ __forceinline__ uint64_t coef_tile_pos(const TileMap& m, int l, int y
 }
 
 // K3 3D v2: one warp = G voxels of the tile order; MODE as k_back3.
-template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P, int WPB = 8, int MINB = 1, class AP = const uint2*>
+template <int MODE, int LPR, int SPL, int U, int NF, bool SIGNED, int P, int WPB = 8, int MINB = 1, class AP = const uint2*,
+          bool XD = false>
 __global__ void __launch_bounds__(32 * WPB, MINB) k_back3s(uint64_t N, int sbeg, int nz, const unsigned* __restrict__ order,
                                                 const unsigned long long* __restrict__ cp,
                                                 AP C, const float* __restrict__ w,
@@ -518,8 +532,18 @@ __global__ void __launch_bounds__(32 * WPB, MINB) k_back3s(uint64_t N, int sbeg,
         const uint64_t lo = ok ? cp[x] : 0, hi = ok ? cp[x + 1] : 0;
         const int maxlen = (int)__reduce_max_sync(0xffffffffu, (unsigned)(hi - lo));
         double acc[SPL];
-        slab_dot_g<LPR, SPL, U, NF, SIGNED, P>(C, w + s0, lo, hi, maxlen, lig, gr, s_st[wib], acc);
+        slab_dot_g<LPR, SPL, U, NF, SIGNED, P, XD>(C, w + s0, lo, hi, maxlen, lig, gr, s_st[wib], acc);
         if (!ok) continue;
+        if constexpr (XD) {   // MODE 0 only: (sum, 0) in the (hi, lo) slots of the z-group
+            static_assert(MODE == 0, "double operand: plain back projection");
+#pragma unroll
+            for (int j = 0; j < SPL / 2; ++j) {
+                const int s = s0 + slab_slice<LPR, SPL>(lig, 2 * j);
+                if (s >= nz) continue;
+                *reinterpret_cast<double2*>(g + x * P + s) = make_double2(acc[j], 0.0);
+            }
+            continue;
+        }
 #pragma unroll
         for (int j = 0; j < SPL; ++j) {
             const int s = s0 + slab_slice<LPR, SPL>(lig, j);

@@ -1097,6 +1097,7 @@ static unsigned nblk_warp(const Ctx* c, uint64_t n) {
 template <int P> struct SlabShape {
     static constexpr int LPR = P <= 16 ? 4 : (P <= 64 ? 8 : 16), SPL = P / LPR, G = 32 / LPR;
 };
+static int SlabShapeSPL(int P) { return P / (P <= 16 ? 4 : (P <= 64 ? 8 : 16)); }
 // X(NF, U, WPB, MINB): F2F share, gathers per round, warps per CTA, min CTAs per SM.
 // The default needs MINB = 2: (256, 1) lets ptxas take 170 registers (1 CTA, 8 warps
 // per SM) and the slab passes ran 1.65x slower (cfg5 13.5 vs 8.1 ms per forward).
@@ -2739,12 +2740,25 @@ static void back3c_launch_p(Ctx* c, int k, const float* w) {
         m.Nc, 0, c->nzl, m.order.p, m.cp.p, Ent64{m.row.p, m.valC.p}, w, c->g_c.p, nullptr, nullptr, 0.0,
         c->flag.p, TileMap{});
 }
+// WAMGPU_COARSE_DBL=0: z-group sums of q as fp32 (hi, lo) pairs instead of doubles
+static bool coarse_dbl() {
+    const char* e = std::getenv("WAMGPU_COARSE_DBL");
+    return !(e && e[0] == '0');
+}
 template <int PW>
 static void back3cz_launch_p(Ctx* c, int k, int nzw) {
     using S = SlabShape<PW>;
     Ctx::Coarse& m = c->coarse[k];
     const uint64_t ncol = m.Nc * (uint64_t)m.seg;   // seg > 1: column segments in column order (no tile order)
     const unsigned nb = nblk_warp(c, (ncol + S::G - 1) / S::G);
+    if constexpr (S::SPL >= 4) {
+        if (coarse_dbl()) {   // fp64 z-group sums as the operand: no conversions (default)
+            k_back3s<0, S::LPR, S::SPL, 104, 1, true, PW, 8, 2, Ent64, true><<<nb, 256, 0, c->st>>>(
+                ncol, 0, nzw, m.seg > 1 ? nullptr : m.order.p, m.seg > 1 ? m.cpseg.p : m.cp.p,
+                Ent64{m.row.p, m.valC.p}, c->w_z.p, c->g_c.p, nullptr, nullptr, 0.0, c->flag.p, TileMap{});
+            return;
+        }
+    }
     k_back3s<0, S::LPR, S::SPL, 104, 1, true, PW, 8, 2, Ent64><<<nb, 256, 0, c->st>>>(
         ncol, 0, nzw, m.seg > 1 ? nullptr : m.order.p, m.seg > 1 ? m.cpseg.p : m.cp.p, Ent64{m.row.p, m.valC.p},
         c->w_z.p, c->g_c.p, nullptr, nullptr, 0.0, c->flag.p, TileMap{});
@@ -2763,7 +2777,8 @@ static void back3c_into(Ctx* c, int k, const float* w, double* out, bool expand 
         c->w_z.ensure(c->Ml * Pw);
         c->g_c.ensure(m.Nc * m.seg * Pw);
         c->timer_begin(T_BACKC);
-        k_qsum_z<<<blocks_for(c->Ml * (Pw / 2), 256), 256, 0, c->st>>>(c->Ml, nzc, P, Pw, k, w, c->w_z.p);
+        const int dbl = coarse_dbl() && SlabShapeSPL(Pw) >= 4;
+        k_qsum_z<<<blocks_for(c->Ml * (Pw / 2), 256), 256, 0, c->st>>>(c->Ml, nzc, P, Pw, k, dbl, w, c->w_z.p);
         check_launch(c, "k_qsum_z");
         switch (Pw) {
             case 8: back3cz_launch_p<8>(c, k, 2 * nzc); break;
