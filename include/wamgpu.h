@@ -216,6 +216,14 @@ int wamgpu_get_matrix_csc(const wamgpu_ctx* ctx, uint64_t* col_ptr, uint32_t* ro
 int wamgpu_forward_project(wamgpu_ctx* ctx, const double* mu, double* l);
 int wamgpu_back_project(wamgpu_ctx* ctx, const double* w, double* out);
 
+/* core-model on caller vectors of length n (no matrix needed):
+ * predicted_means q(y) = I0(y) exp(-l(y)); a non-finite l(y) -> WAMGPU_ERR_NUMERIC
+ * naming the ray.  i_divergence I(d||q) = sum d log(d/q) - d + q with 0 log 0 = 0;
+ * any q(y) <= 0 -> WAMGPU_ERR_NUMERIC.  The iteration itself never calls these:
+ * its forward kernels fuse both. */
+int wamgpu_predicted_means(wamgpu_ctx* ctx, uint64_t n, const double* I0, const double* l, double* q);
+int wamgpu_i_divergence(wamgpu_ctx* ctx, uint64_t n, const double* d, const double* q, double* out);
+
 /* TransmissionData: d and I0 over ALL rays (z*M + y); each rank
  * keeps its own view rows. */
 int wamgpu_set_data(wamgpu_ctx* ctx, const double* d, const double* I0);

@@ -133,6 +133,19 @@ class Context {
         check(wamgpu_back_project(c_, w.data(), out.data()), c_);
         return out;
     }
+    // SPEC.md:81-98
+    std::vector<double> predicted_means(const std::vector<double>& I0, const std::vector<double>& l) const {
+        if (I0.size() != l.size()) throw ContractError("predicted_means: length mismatch");
+        std::vector<double> q(l.size());
+        check(wamgpu_predicted_means(c_, l.size(), I0.data(), l.data(), q.data()), c_);
+        return q;
+    }
+    double i_divergence(const std::vector<double>& d, const std::vector<double>& q) const {
+        if (d.size() != q.size()) throw ContractError("i_divergence: length mismatch");
+        double v = 0.0;
+        check(wamgpu_i_divergence(c_, d.size(), d.data(), q.data(), &v), c_);
+        return v;
+    }
 
     // ---- data + solvers
     void set_data(const std::vector<double>& d, const std::vector<double>& I0) {

@@ -63,6 +63,7 @@ EXPORTED = [
     "wamgpu_set_comm_local", "wamgpu_set_partition", "wamgpu_get_partition", "wamgpu_wam_expand_with", "wamgpu_simulate_device",
     "wamgpu_load_matrix_wamh", "wamgpu_save_matrix_wamh", "wamgpu_plan_partition",
     "wamgpu_set_projector", "wamgpu_get_projector", "wamgpu_debug_guards",
+    "wamgpu_predicted_means", "wamgpu_i_divergence",
 ]
 P2P_BLOB = 256   # WAMGPU_P2P_BLOB
 
@@ -362,6 +363,25 @@ class Context:
         out = np.empty(self.N * self.nz)
         _chk(load().wamgpu_back_project(self.h, _p(w), _p(out)), self.h)
         return out
+
+    # ---- core-model, standalone on caller vectors
+    def predicted_means(self, I0, l):
+        I0 = np.ascontiguousarray(I0, np.float64).ravel()
+        l = np.ascontiguousarray(l, np.float64).ravel()
+        if I0.size != l.size:
+            raise ContractError("predicted_means: length mismatch")
+        q = np.empty(l.size)
+        _chk(load().wamgpu_predicted_means(self.h, C.c_uint64(l.size), _p(I0), _p(l), _p(q)), self.h)
+        return q
+
+    def i_divergence(self, d, q):
+        d = np.ascontiguousarray(d, np.float64).ravel()
+        q = np.ascontiguousarray(q, np.float64).ravel()
+        if d.size != q.size:
+            raise ContractError("i_divergence: length mismatch")
+        out = C.c_double(0.0)
+        _chk(load().wamgpu_i_divergence(self.h, C.c_uint64(d.size), _p(d), _p(q), C.byref(out)), self.h)
+        return out.value
 
     def set_data(self, d, I0):
         self._d = np.ascontiguousarray(d, np.float64)

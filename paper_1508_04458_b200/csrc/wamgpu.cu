@@ -9,7 +9,8 @@
 //   k_forward<1> l = H mu, q = I0 e^-l, I-div partials                  K2
 //   k_sum_partials + [allreduce] + k_record
 // At scheduled expansions: k_tile<0> (fp64 image) -> max -> k_mark ->
-// k_walk<0> (Z0) -> k_walk<1,2> + radix sort (Phi^- CSC rebuild)      K7, K8.
+// k_walk<0> (Z0) -> k_walk<1,2> + counting placement (Phi^- CSC rebuild; radix
+// sort under WAMGPU_PHI_SORT=1)                                         K7, K8.
 // The AM baseline is k_back<1> (fused update) + k_forward<1>.
 #include <cub/cub.cuh>
 #include <nccl.h>
@@ -38,6 +39,7 @@
 #include "kernels_ar.cuh"
 #include "kernels_phi.cuh"
 #include "kernels3c.cuh"
+#include "kernels_ops.cuh"
 
 namespace wamgpu {
 
@@ -3962,6 +3964,64 @@ int wamgpu_back_project(wamgpu_ctx* ctx, const double* w, double* out) {
         back_into(c, c->fscratch.p, c->dscratch.p, false);
         if (view_sharded(c)) allreduce_sum(c, c->dscratch.p, NV(c), S_VIEWS);
         download_slab<double>(c, c->dscratch.p, out, c->N, c->N, 0);
+    })
+}
+
+// predicted_means on caller vectors: q = I0 exp(-l), fp64.
+int wamgpu_predicted_means(wamgpu_ctx* ctx, uint64_t n, const double* I0, const double* l, double* q) {
+    API_TRY(ctx, {
+        NEED(ctx);
+        if (n) { NEED(I0); NEED(l); NEED(q); }
+        Ctx* c = ctx;
+        if (n) {
+            DBuf<double> dI, dl, dq;
+            DBuf<unsigned long long> bad;
+            dI.alloc(n); dl.alloc(n); dq.alloc(n); bad.alloc(1);
+            CK(cudaMemcpyAsync(dI.p, I0, n * 8, cudaMemcpyHostToDevice, c->st));
+            CK(cudaMemcpyAsync(dl.p, l, n * 8, cudaMemcpyHostToDevice, c->st));
+            CK(cudaMemsetAsync(bad.p, 0xff, 8, c->st));
+            const int nb = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)c->sms * 8);
+            k_pred_means<<<nb, 256, 0, c->st>>>(dI.p, dl.p, dq.p, n, bad.p);
+            check_launch(c, "k_pred_means");
+            unsigned long long first = 0;
+            CK(cudaMemcpyAsync(&first, bad.p, 8, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            if (first != ~0ull)
+                throw NumericError("predicted_means: non-finite line integral at ray " + std::to_string(first));
+            CK(cudaMemcpyAsync(q, dq.p, n * 8, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+        }
+    })
+}
+
+// i_divergence on caller vectors: fixed-order fp64 sum.
+int wamgpu_i_divergence(wamgpu_ctx* ctx, uint64_t n, const double* d, const double* q, double* out) {
+    API_TRY(ctx, {
+        NEED(ctx); NEED(out);
+        if (n) { NEED(d); NEED(q); }
+        Ctx* c = ctx;
+        *out = 0.0;
+        if (n) {
+            const int nb = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)c->sms * 8);
+            DBuf<double> dd, dq, part;
+            DBuf<unsigned long long> bad;
+            dd.alloc(n); dq.alloc(n); part.alloc(nb + 1); bad.alloc(1);
+            CK(cudaMemcpyAsync(dd.p, d, n * 8, cudaMemcpyHostToDevice, c->st));
+            CK(cudaMemcpyAsync(dq.p, q, n * 8, cudaMemcpyHostToDevice, c->st));
+            CK(cudaMemsetAsync(bad.p, 0xff, 8, c->st));
+            k_idiv_partials<<<nb, 256, 0, c->st>>>(dd.p, dq.p, n, part.p, bad.p);
+            check_launch(c, "k_idiv_partials");
+            k_sum_partials<<<1, 1024, 0, c->st>>>(part.p, nb, part.p + nb);
+            check_launch(c, "k_sum_partials");
+            unsigned long long first = 0;
+            CK(cudaMemcpyAsync(&first, bad.p, 8, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaMemcpyAsync(out, part.p + nb, 8, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            if (first != ~0ull) {
+                *out = 0.0;
+                throw NumericError("i_divergence: q <= 0 at ray " + std::to_string(first));
+            }
+        }
     })
 }
 
