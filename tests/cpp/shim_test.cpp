@@ -78,14 +78,27 @@ int main() {
     for (std::uint64_t k = 0; wamh && k < H.nnz(); ++k) wamh = H2.values()[k] == (double)(float)H.values()[k];
     bool io_threw = false;
     try { ctx3.load_system_matrix("/nonexistent/x.wamh"); } catch (const wamrec::IoError&) { io_threw = true; }
+    // standalone core ops: Beer's law on the device line integrals
+    // against std::exp, the zero of the I-divergence, and the reference's NumericError
+    std::vector<double> qd = ctx.predicted_means(std::vector<double>(l.size(), 1e5), l);
+    double qrel = 0.0;
+    for (std::size_t y = 0; y < l.size(); ++y) {
+        const double e = 1e5 * std::exp(-l[y]);
+        qrel = std::max(qrel, std::fabs(qd[y] - e) / e);
+    }
+    bool core = qrel < 1e-14 && ctx.i_divergence(qd, qd) == 0.0 &&
+                std::fabs(ctx.i_divergence({2.0}, {1.0}) - (2.0 * std::log(2.0) - 1.0)) < 1e-15;
+    bool num_threw = false;
+    try { ctx.i_divergence({1.0, 1.0}, {1.0, 0.0}); } catch (const wamrec::NumericError&) { num_threw = true; }
+    core = core && num_threw;
     std::remove(ref_file.c_str());
     std::remove(dev_file.c_str());
     std::printf("forward rel %.3e, set_geometry max diff %.3e, AM obj %.6e -> %.6e, WAM obj %.6e -> %.6e, "
-                "active %lld, monotone %d, config error mapped %d, WAMH %d, io error mapped %d\n",
+                "active %lld, monotone %d, config error mapped %d, WAMH %d, io error mapped %d, core ops %d (q rel %.1e)\n",
                 rel, diff2, ra.front().objective, ra.back().objective, rw.front().objective, rw.back().objective,
-                (long long)rw.back().active_set, (int)mono, (int)threw, (int)wamh, (int)io_threw);
+                (long long)rw.back().active_set, (int)mono, (int)threw, (int)wamh, (int)io_threw, (int)core, qrel);
     const bool ok = rel < 1e-12 && diff2 == 0.0 && mono && threw && rw.back().objective < rw.front().objective &&
-                    wamh && io_threw;
+                    wamh && io_threw && core;
     std::printf(ok ? "SHIM OK\n" : "SHIM FAIL\n");
     return ok ? 0 : 1;
 }
