@@ -667,11 +667,18 @@ def main():
             ach = split_bytes / (split_avg * 1e-3) / 1e9
             dom_bytes = split_bytes
         traffic = None
+        traffic_note = "GB per launch, ncu dram read+write (profiles/dram_traffic.json)"
         try:
             with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as f:
                 tr = json.load(f)
-            traffic = tr.get(cfg["name"], {}).get("k_split3c" if split_dom else
+            traffic = tr.get(cfg["name"], {}).get("k_split3c_final_tree" if split_dom else
                                                    "k_forward" if "forward" in dom else "k_back")
+            if split_dom and traffic is not None:
+                # one capture exists, of the LARGEST launch of a run (final tree); `achieved` above
+                # averages over a run's launches, so compare this with the final tree's own bytes
+                traffic_note = ("GB, ncu dram read+write of the final-tree launch (8.67e8 Psi entries, 19.2 GB "
+                                "algorithmic for THAT launch: 2.8x, q rows re-fetched from DRAM when the "
+                                "slab falls out of L2); profiles/r07/ncu_split3c_cfg4_chunk.txt")
         except Exception:
             pass
         # 3D: the slab passes are not HBM-bound (one DFMA + one fp32->fp64
@@ -743,6 +750,7 @@ def main():
             "parity": parity,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+                         "traffic_note": traffic_note if traffic is not None else None,
                          "algorithmic_bytes": dom_bytes,
                          "binding": binding},
             "kernels": {"fwd_avg_ms": fwd_avg, "fwd_gbs": fwd_gbs, "fwd_frac": fwd_gbs / hbm,
